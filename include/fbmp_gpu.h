@@ -1,0 +1,184 @@
+/*
+ * fbmp_gpu.h -- C ABI of the B200 (sm_100a) blind-pansharpening hot path.
+ *
+ * This is the drop-in boundary for the reference's C++ entry points (reference paths are
+ * relative to /root/reference/proj). Every function takes plain pointers and sizes; there
+ * are no torch, CUDA or C++ types in the signatures. The C++ shim in
+ * paper_2103_09943_b200/host/ implements the reference's `fbmp::` API on top of these
+ * calls (see INTEGRATION.md for the bindings a maintainer would add).
+ *
+ * Conventions
+ *   - Planes are row-major float64; stacks are band-major ([band][row][col]).
+ *   - `factor` is the decimation ratio c (= r); HR dims are factor x LR dims.
+ *   - Host-pointer calls are synchronous: they upload, compute, download and return.
+ *   - `_dev` calls take device pointers (allocated on the context's device) and enqueue on
+ *     the context's stream; they return once the result is on the device.
+ *   - Return codes mirror the reference error taxonomy (include/fbmp/errors.hpp:8-33):
+ *       0 ok, 1 ParamError, 2 DimensionError, 3 NumericalError, 4 CUDA/runtime error.
+ *     The message (same text as the reference's exception, including the "channel i: "
+ *     prefix of pansharpen.cpp:80-92) is available from fbmp_gpu_last_error() on the
+ *     calling thread.
+ */
+#ifndef FBMP_GPU_H
+#define FBMP_GPU_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum fbmp_status {
+    FBMP_OK = 0,
+    FBMP_PARAM_ERROR = 1,
+    FBMP_DIMENSION_ERROR = 2,
+    FBMP_NUMERICAL_ERROR = 3,
+    FBMP_RUNTIME_ERROR = 4
+};
+
+/* PansharpenParams (pansharpen.hpp:15-26), Laplacian prior. `threads` is accepted for API
+ * parity and ignored: all channels of a call are solved concurrently on the device. */
+typedef struct fbmp_ps_params {
+    double lambda;   /* 2e-4 */
+    int radius;      /* 1 */
+    double eps;      /* 1e-4 */
+    double cg_tol;   /* 5e-5 */
+    int cg_max_iter; /* 2000 */
+    int threads;     /* 0 */
+} fbmp_ps_params;
+
+/* KernelEstParams (kernel_estimator.hpp:16-31). init: 0 = dirac, 1 = uniform. */
+typedef struct fbmp_ke_params {
+    int n;          /* 29 */
+    double alpha1;  /* 1.0 */
+    double alpha2;  /* 0.006 */
+    double mu1, mu2, mu3; /* 100 */
+    double rho;     /* 0.5 */
+    int t_max;      /* 10000 */
+    double th;      /* 1e-5 */
+    int init;       /* 0 */
+} fbmp_ke_params;
+
+/* SpectralWeightConfig (spectral_weights.hpp:9-14); band_indices are applied by the caller. */
+typedef struct fbmp_sw_params {
+    int l;               /* 4 */
+    double lambda_omega; /* 10 */
+    int factor;          /* 2 */
+} fbmp_sw_params;
+
+typedef struct fbmp_gpu_ctx fbmp_gpu_ctx;
+
+/* Per-solve statistics of the last pansharpen / blind call on a context. */
+typedef struct fbmp_gpu_stats {
+    int admm_iters;      /* ADMM iterations of the kernel fit (0 if not run) */
+    int cg_iters[64];    /* CG iterations per channel (first 64 channels) */
+    double ms_weights, ms_kernel_fit, ms_pansharpen; /* device time of the stages */
+} fbmp_gpu_stats;
+
+void fbmp_gpu_default_ps_params(fbmp_ps_params* p);
+void fbmp_gpu_default_ke_params(fbmp_ke_params* p);
+void fbmp_gpu_default_sw_params(fbmp_sw_params* p);
+
+/* Context: owns the device workspace, cuFFT plans and the stream. One per host thread. */
+int fbmp_gpu_ctx_create(int device, fbmp_gpu_ctx** out);
+void fbmp_gpu_ctx_destroy(fbmp_gpu_ctx* ctx);
+const char* fbmp_gpu_last_error(void);
+int fbmp_gpu_ctx_stats(fbmp_gpu_ctx* ctx, fbmp_gpu_stats* out);
+/* The context's cudaStream_t, as an opaque pointer (for device-resident callers). */
+void* fbmp_gpu_ctx_stream(fbmp_gpu_ctx* ctx);
+/* Number of kernels this library launched on the context so far (instrumentation). */
+long long fbmp_gpu_ctx_launches(fbmp_gpu_ctx* ctx);
+
+/* ---- full pipeline ----------------------------------------------------------------------- */
+
+/* pansharpen (pansharpen.hpp:95-96 / pansharpen.cpp:367-424). lrms: N*h*w, pan: H*W,
+ * k: n*n taps, out: N*H*W. cg_iters (optional, N ints) receives per-channel CG counts. */
+int fbmp_gpu_pansharpen(fbmp_gpu_ctx* ctx, const double* lrms, int N, int h, int w, const double* pan,
+                        const double* k, int n, int factor, const fbmp_ps_params* params, double* out,
+                        int* cg_iters);
+
+/* estimate_kernel_tgv (kernel_estimator.hpp:114-118): combine_bands(lrms, omega) then the
+ * TGV^2 fit. k_out: n*n. iters (optional) receives the ADMM iteration count. */
+int fbmp_gpu_estimate_kernel_tgv(fbmp_gpu_ctx* ctx, const double* lrms_subset, int nb, int h, int w,
+                                 const double* pan, const double* omega, int factor,
+                                 const fbmp_ke_params* params, double* k_out, int* iters);
+
+/* estimate_kernel_plane with KernelPrior::tgv2 (kernel_estimator.hpp:109-112). obs: h*w.
+ * state_out (optional, 17*n*n: u,p1,p2,x0,x1,y0..y3,z,L1_0,L1_1,L2_0..L2_3,L3) receives the
+ * final TgvAdmmState; hook_t >= 0 stops right before the {u,p} solve of iteration hook_t
+ * and returns that state (the reference's before_up_solve hook point). */
+int fbmp_gpu_estimate_kernel_plane(fbmp_gpu_ctx* ctx, const double* pan, int H, int W, const double* obs,
+                                   int factor, const fbmp_ke_params* params, double* k_out, int* iters,
+                                   double* state_out, int hook_t);
+
+/* solve_weights (spectral_weights.hpp:24-25). omega_out: nb doubles. */
+int fbmp_gpu_solve_weights(fbmp_gpu_ctx* ctx, const double* lrms_subset, int nb, int h, int w,
+                           const double* pan, const fbmp_sw_params* cfg, double* omega_out);
+
+/* combine_bands (spectral_weights.hpp:28-29). out: h*w. */
+int fbmp_gpu_combine_bands(fbmp_gpu_ctx* ctx, const double* lrms_subset, int nb, int h, int w,
+                           const double* omega, double* out);
+
+/* SPEC.md:584-591 blind composition (solve_weights on all bands -> estimate_kernel_tgv ->
+ * pansharpen). k_out: n*n (n = ke->n), omega_out: N (both optional). */
+int fbmp_gpu_blind(fbmp_gpu_ctx* ctx, const double* lrms, int N, int h, int w, const double* pan,
+                   const fbmp_sw_params* sw, const fbmp_ke_params* ke, const fbmp_ps_params* ps, double* out,
+                   double* k_out, double* omega_out);
+
+/* Device-resident blind solve (same semantics; all pointers are device pointers). */
+int fbmp_gpu_blind_dev(fbmp_gpu_ctx* ctx, const double* d_lrms, int N, int h, int w, const double* d_pan,
+                       const fbmp_sw_params* sw, const fbmp_ke_params* ke, const fbmp_ps_params* ps,
+                       double* d_out, double* d_k_out);
+
+/* Batch of independent scenes (no reference equivalent; BASELINE config C4): S scenes of
+ * identical shape, each with its own weights, kernel fit and HRMS solve. */
+int fbmp_gpu_blind_batch(fbmp_gpu_ctx* ctx, const double* lrms, int S, int N, int h, int w, const double* pan,
+                         const fbmp_sw_params* sw, const fbmp_ke_params* ke, const fbmp_ps_params* ps,
+                         double* out, double* k_out);
+
+/* ---- unit-level entry points (parity tests) -------------------------------------------- */
+
+/* apply_prior / apply_prior_adjoint (pansharpen.hpp:28-29): circular 5-point Laplacian. */
+int fbmp_gpu_apply_prior(fbmp_gpu_ctx* ctx, const double* img, int H, int W, double* out);
+/* MattingMatrix::apply(Plane) (pansharpen.hpp:47, :197-202), matrix-free: y = M(guide) x. */
+int fbmp_gpu_llp_apply(fbmp_gpu_ctx* ctx, const double* guide, const double* x, int H, int W, int radius,
+                       double eps, double* y);
+/* B^T U D B p (the data term of pansharpen.cpp:218-223). */
+int fbmp_gpu_data_apply(fbmp_gpu_ctx* ctx, const double* p, int H, int W, const double* k, int n, int factor,
+                        double* out);
+/* The full CG operator A(p) of pansharpen.cpp:218-223 with M built on `guide`. */
+int fbmp_gpu_cg_operator(fbmp_gpu_ctx* ctx, const double* guide, const double* p, int H, int W, const double* k,
+                         int n, int factor, const fbmp_ps_params* params, double* out);
+/* warmstart_cg (pansharpen.hpp:73-75) with M built on `guide` (= L(pan_n) in the pipeline). */
+int fbmp_gpu_warmstart_cg(fbmp_gpu_ctx* ctx, const double* x, int h, int w, const double* guide, const double* k,
+                          int n, int factor, const fbmp_ps_params* params, int max_iters, int error_on_cap,
+                          double* z_out, int* iters, double* final_residual);
+/* guided_coeffs + guided_output (pansharpen.hpp:83-84). a_out / c_out optional. */
+int fbmp_gpu_guided_filter(fbmp_gpu_ctx* ctx, const double* input, const double* guide, int H, int W, int radius,
+                           double eps, double* a_out, double* c_out, double* v_out);
+/* guided_output alone (pansharpen.hpp:84). */
+int fbmp_gpu_guided_output(fbmp_gpu_ctx* ctx, const double* a, const double* c, const double* guide, int H, int W,
+                           int radius, double* out);
+/* solve_channel_fft (pansharpen.hpp:90-91). */
+int fbmp_gpu_solve_channel_fft(fbmp_gpu_ctx* ctx, const double* x, int h, int w, const double* k, int n,
+                               int factor, const double* v, const fbmp_ps_params* params, double* out);
+/* box_mean (ops.hpp:32), circular convolution and its adjoint (ops.hpp:10-15). */
+int fbmp_gpu_box_mean(fbmp_gpu_ctx* ctx, const double* img, int H, int W, int radius, double* out);
+int fbmp_gpu_convolve(fbmp_gpu_ctx* ctx, const double* img, int H, int W, const double* k, int n, int adjoint,
+                      double* out);
+/* shrink2 (kernel_estimator.hpp:65): cols is ncols consecutive planes of m samples, in place. */
+int fbmp_gpu_shrink2(fbmp_gpu_ctx* ctx, double* cols, int ncols, long long m, double t);
+/* project_simplex (kernel_estimator.hpp:68). */
+int fbmp_gpu_project_simplex(fbmp_gpu_ctx* ctx, const double* v, int m, double* out);
+/* solve_up (kernel_estimator.hpp:78-80) with optional mu3 coupling to anchor (= z - L3).
+ * fields: 12 n*n planes x0,x1,y0..y3,L1_0,L1_1,L2_0..L2_3. */
+int fbmp_gpu_solve_up(fbmp_gpu_ctx* ctx, const double* fields, int n, const fbmp_ke_params* params,
+                      double coupling, const double* anchor, double* u, double* p1, double* p2);
+/* E^T E (n^2 x n^2) and E^T f of ObservationSystem (kernel_estimator.cpp:57-71), unscaled. */
+int fbmp_gpu_gram(fbmp_gpu_ctx* ctx, const double* pan, int H, int W, const double* obs, int factor, int n,
+                  double* EtE, double* Etf);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FBMP_GPU_H */

@@ -916,7 +916,7 @@ Up solve_up_core(const vec x[2], const vec y[4], const vec L1[2], const vec L2[4
         x2[i] = x[1][i] - L1[1][i];
         y1[i] = y[0][i] - L2[0][i];
         y2[i] = y[3][i] - L2[3][i];
-        yc[i] = (y[1][i] - L2[1][i] + (y[2][i] - L2[2][i])) * 0.5;
+        yc[i] = (((y[1][i] - L2[1][i]) + y[2][i]) - L2[2][i]) * 0.5;  // Plane ops evaluate left to right
     }
     vec g1 = diff(x1.data(), n, n, GH, true), g2 = diff(x2.data(), n, n, GV, true);
     vec h1 = diff(y1.data(), n, n, GH, true), h2 = diff(yc.data(), n, n, GV, true);

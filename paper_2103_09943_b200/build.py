@@ -1,0 +1,82 @@
+"""Build the sm_100a CUDA library (libfbmp_gpu.so) and the C++ reference-API shim in-tree.
+
+nvcc cross-compiles for sm_100a without a GPU; the .so files are written next to the
+sources (paper_2103_09943_b200/lib/) so they travel with the repo snapshot to the GPU box.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+HOST = os.path.join(HERE, "host")
+LIBDIR = os.path.join(HERE, "lib")
+BUILD = os.path.join(HERE, "build")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+CUDA_LIB = "/usr/local/cuda/lib64"
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
+                  "-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "--expt-relaxed-constexpr"]
+CU_SOURCES = ["pansharpen.cu", "kernel_fit.cu", "capi.cu"]
+GPU_LIB = os.path.join(LIBDIR, "libfbmp_gpu.so")
+SHIM_LIB = os.path.join(LIBDIR, "libfbmp.so")
+
+
+def _stale(target: str, deps: list[str]) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _run(cmd: list[str]) -> None:
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+        raise RuntimeError(f"build step failed: {cmd[0]} ... {cmd[-1]}")
+
+
+def build_gpu(force: bool = False, verbose: bool = False) -> str:
+    os.makedirs(LIBDIR, exist_ok=True)
+    os.makedirs(BUILD, exist_ok=True)
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
+    headers.append(os.path.join(ROOT, "include", "fbmp_gpu.h"))
+    objs, jobs = [], []
+    for src in CU_SOURCES:
+        sp = os.path.join(CSRC, src)
+        obj = os.path.join(BUILD, src.replace(".cu", ".o"))
+        objs.append(obj)
+        if force or _stale(obj, [sp] + headers):
+            extra = ["-Xptxas", "-v"] if verbose else []
+            jobs.append([NVCC] + NVFLAGS + extra + ["-c", sp, "-o", obj])
+    with ThreadPoolExecutor(max_workers=len(jobs) or 1) as ex:
+        list(ex.map(_run, jobs))
+    if force or jobs or _stale(GPU_LIB, objs):
+        _run([NVCC] + ARCH + ["-shared", "-o", GPU_LIB] + objs +
+             ["-L" + CUDA_LIB, "-lcufft", "-lcudart", "-Xlinker", "-rpath," + CUDA_LIB])
+    return GPU_LIB
+
+
+def build_shim(force: bool = False) -> str:
+    srcs = [os.path.join(HOST, f) for f in sorted(os.listdir(HOST)) if f.endswith(".cpp")]
+    hdrs = [os.path.join(ROOT, "include", "fbmp", f) for f in os.listdir(os.path.join(ROOT, "include", "fbmp"))]
+    if force or _stale(SHIM_LIB, srcs + hdrs + [GPU_LIB]):
+        _run(["g++", "-O2", "-std=c++20", "-fPIC", "-shared", "-Wall", "-Wextra",
+              "-I" + os.path.join(ROOT, "include"), "-o", SHIM_LIB] + srcs +
+             ["-L" + LIBDIR, "-lfbmp_gpu", "-Wl,-rpath,$ORIGIN"])
+    return SHIM_LIB
+
+
+def build(force: bool = False, verbose: bool = False) -> None:
+    build_gpu(force, verbose)
+    if os.path.isdir(HOST) and any(f.endswith(".cpp") for f in os.listdir(HOST)):
+        build_shim(force)
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(GPU_LIB)

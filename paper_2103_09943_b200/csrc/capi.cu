@@ -1,0 +1,724 @@
+// capi.cu -- the C ABI (include/fbmp_gpu.h): context management and the reference-facing
+// entry points. Host-pointer calls upload, run the device path and download; there is no
+// CPU fallback anywhere in this library.
+#include <cstring>
+#include <string>
+
+#include "kernel_fit.cuh"
+#include "pansharpen.cuh"
+
+namespace fbmp_gpu {
+
+thread_local std::string g_last_error;
+
+Context::Context(int dev) : device(dev) {
+    FBMP_CUDA(cudaSetDevice(dev));
+    FBMP_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    cudaDeviceProp prop{};
+    FBMP_CUDA(cudaGetDeviceProperties(&prop, dev));
+    sm_count = prop.multiProcessorCount;
+    if (prop.major < 10)
+        throw Failure(FBMP_RUNTIME_ERROR, "fbmp_gpu requires an sm_100 (Blackwell) device; found " +
+                                              std::string(prop.name));
+}
+
+Context::~Context() {
+    cudaSetDevice(device);
+    for (auto& kv : plans) cufftDestroy(kv.second);
+    ws.clear();
+    if (stream) cudaStreamDestroy(stream);
+}
+
+cufftHandle Context::plan(int kind, int rows, int cols, int batch) {
+    const auto key = std::make_tuple(kind, rows, cols, batch, 0);
+    auto it = plans.find(key);
+    if (it != plans.end()) return it->second;
+    cufftHandle h;
+    int dims[2] = {rows, cols};
+    FBMP_CUFFT(cufftPlanMany(&h, 2, dims, nullptr, 1, 0, nullptr, 1, 0, kind == 0 ? CUFFT_D2Z : CUFFT_Z2D, batch));
+    FBMP_CUFFT(cufftSetStream(h, stream));
+    plans[key] = h;
+    return h;
+}
+
+void validate_ps(const fbmp_ps_params& p) {  // pansharpen.cpp:96-105 (Laplacian prior)
+    if (!(p.lambda > 0)) param_error("pansharpen: lambda must be positive");
+    if (p.radius < 1) param_error("pansharpen: radius must be >= 1");
+    if (!(p.eps > 0)) param_error("pansharpen: eps must be positive");
+    if (!(p.cg_tol > 0)) param_error("pansharpen: cg_tol must be positive");
+    if (p.cg_max_iter < 1) param_error("pansharpen: cg_max_iter must be >= 1");
+    if (p.threads < 0) param_error("pansharpen: threads must be >= 0");
+}
+
+static void check_kernel(int n, int H, int W) {
+    if (n < 1 || n % 2 == 0) param_error("kernel size must be odd and positive");
+    if (n > H || n > W) dim_error("kernel larger than image");
+}
+
+// Batched HRMS solve on device-resident data (pansharpen.cpp:367-424) for S scenes of N
+// channels each: lrms S*N*h*w, pan S*H*W, taps S*n*n, out S*N*H*W.
+void pansharpen_device(Context& ctx, const double* d_lrms, int S, int N, int h, int w, const double* d_pan,
+                       const double* d_taps, int n, int c, const fbmp_ps_params& prm, double* d_out,
+                       std::vector<int>& cg_iters) {
+    validate_ps(prm);
+    const int H = h * c, W = w * c;
+    if (2 * prm.radius + 1 > std::min(H, W)) dim_error("matting matrix: window larger than image");
+    check_kernel(n, H, W);
+    const int NC = S * N;
+    const size_t P = static_cast<size_t>(H) * W, p = static_cast<size_t>(h) * w;
+    const PsGeo G = make_geo(NC, h, w, c, n, prm.radius, prm.lambda, prm.eps, N);
+    double* scale = ctx.scratch<double>("ps_scale", S);
+    double* lpan = ctx.scratch<double>("ps_lpan", P * S);
+    double* xn = ctx.scratch<double>("ps_xn", p * NC);
+    peak_scale(ctx, d_pan, static_cast<long long>(P), d_lrms, static_cast<long long>(p) * N, S, scale);
+    laplacian_scaled(ctx, d_pan, H, W, S, scale, lpan);
+    scale_copy(ctx, d_lrms, static_cast<long long>(p) * NC, scale, static_cast<long long>(p) * N, xn);
+
+    CgBuffers B;
+    B.z = ctx.scratch<double>("cg_z", P * NC);
+    B.r = ctx.scratch<double>("cg_r", P * NC);
+    B.p = ctx.scratch<double>("cg_p", 2 * P * NC);
+    B.Ap = ctx.scratch<double>("cg_ap", P * NC);
+    B.q = ctx.scratch<double>("cg_q", p * NC);
+    const size_t nbmax = (P / 256 + 64) * 2 + 4096;
+    B.part = ctx.scratch<double>("cg_part", 4 * nbmax * NC);
+    B.st = ctx.scratch<CgState>("cg_state", NC);
+    std::vector<CgState> hs;
+    cg_solve(ctx, G, d_taps, lpan, xn, B, prm.cg_max_iter, prm.cg_tol, hs);
+    cg_iters.assign(NC, 0);
+    for (int i = 0; i < NC; ++i) cg_iters[i] = hs[i].iters;
+    for (int i = 0; i < NC; ++i) {  // first failing channel in index order (pansharpen.cpp:421-422)
+        const std::string tag = "channel " + std::to_string(i % N) + ": ";
+        if (hs[i].done == 2)
+            num_error(tag + "warmstart: conjugate gradients hit a non-positive curvature direction");
+        if (hs[i].done == 3) {
+            // residual of the normal equations, only for the message (pansharpen.cpp:257-262)
+            const int sc = i / N;
+            double* az = ctx.scratch<double>("cg_res_az", P);
+            double* rhs = ctx.scratch<double>("cg_res_rhs", P);
+            const PsGeo G1 = make_geo(1, h, w, c, n, prm.radius, prm.lambda, prm.eps);
+            cg_operator_apply(ctx, G1, d_taps + static_cast<size_t>(sc) * n * n, lpan + sc * P, B.z + i * P, az, 0);
+            data_rhs(ctx, G1, d_taps + static_cast<size_t>(sc) * n * n, xn + i * p, rhs);
+            std::vector<double> a(P), b(P);
+            d2h(a.data(), az, P * sizeof(double), ctx.stream);
+            d2h(b.data(), rhs, P * sizeof(double), ctx.stream);
+            FBMP_CUDA(cudaStreamSynchronize(ctx.stream));
+            double s2 = 0.0;
+            for (size_t k = 0; k < P; ++k) s2 += (a[k] - b[k]) * (a[k] - b[k]);
+            num_error(tag + "warmstart: conjugate gradients did not converge in " + std::to_string(prm.cg_max_iter) +
+                      " iterations (residual " + std::to_string(std::sqrt(s2) / hs[i].rhs_norm) + " relative)");
+        }
+    }
+    double* v = ctx.scratch<double>("ps_v", P * NC);
+    guided_filter(ctx, NC, H, W, prm.radius, prm.eps, B.z, 1, lpan, nullptr, nullptr, v, N);
+    int* flag = ctx.scratch<int>("ps_flag", NC);
+    FBMP_CUDA(cudaMemsetAsync(flag, 0, sizeof(int) * NC, ctx.stream));
+    solve_channel_fft(ctx, G, d_taps, xn, v, scale, d_out, flag);
+    std::vector<int> hf(NC);
+    d2h(hf.data(), flag, sizeof(int) * NC, ctx.stream);
+    FBMP_CUDA(cudaStreamSynchronize(ctx.stream));
+    for (int i = 0; i < NC; ++i)
+        if (hf[i])
+            num_error("channel " + std::to_string(i % N) +
+                      ": solve_channel_fft: alias-group system condition number exceeds 1e14 (prior transfer "
+                      "function too small)");
+}
+
+// SPEC.md:584-591 blind composition for S scenes on device-resident data:
+// solve_weights (all bands) -> combine_bands -> estimate_kernel_tgv -> pansharpen.
+void blind_device(Context& ctx, const double* d_lrms, int S, int N, int h, int w, const double* d_pan,
+                  const fbmp_sw_params& sw, const fbmp_ke_params& ke, const fbmp_ps_params& ps, double* d_out,
+                  double* d_k, double* d_omega_out, std::vector<int>& admm_iters, std::vector<int>& cg_iters) {
+    const int c = sw.factor;
+    if (c < 1) param_error("solve_weights: factor must be >= 1");
+    if (sw.l < 1) param_error("solve_weights: l must be >= 1");
+    if (sw.lambda_omega < 0.0) param_error("solve_weights: lambda_omega must be >= 0");
+    validate_ke(ke);
+    validate_ps(ps);
+    const int H = h * c, W = w * c;
+    const long long p = static_cast<long long>(h) * w;
+    cudaEvent_t e0, e1, e2, e3;
+    cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2); cudaEventCreate(&e3);
+    cudaEventRecord(e0, ctx.stream);
+    double* omega = d_omega_out ? d_omega_out : ctx.scratch<double>("bl_omega", static_cast<size_t>(S) * N);
+    int* st = ctx.scratch<int>("bl_sw_status", S);
+    solve_weights_device(ctx, d_lrms, S, N, h, w, d_pan, sw.l, sw.lambda_omega, c, omega, st);
+    double* obs = ctx.scratch<double>("bl_obs", static_cast<size_t>(S) * p);
+    combine_bands_device(ctx, d_lrms, S, N, p, omega, obs);
+    std::vector<int> hst(S);
+    d2h(hst.data(), st, S * sizeof(int), ctx.stream);
+    FBMP_CUDA(cudaStreamSynchronize(ctx.stream));
+    for (int s = 0; s < S; ++s) {
+        if (hst[s] == 1)
+            num_error("solve_weights: normal matrix is singular (bands linearly dependent and lambda_omega too small)");
+        if (hst[s] == 2) num_error("solve_weights: stationarity residual too large (ill-conditioned system)");
+    }
+    cudaEventRecord(e1, ctx.stream);
+    estimate_kernel_device(ctx, d_pan, obs, S, H, W, c, ke, d_k, admm_iters, nullptr, -1);
+    cudaEventRecord(e2, ctx.stream);
+    pansharpen_device(ctx, d_lrms, S, N, h, w, d_pan, d_k, ke.n, c, ps, d_out, cg_iters);
+    cudaEventRecord(e3, ctx.stream);
+    cudaEventSynchronize(e3);
+    float a = 0, b = 0, d = 0;
+    cudaEventElapsedTime(&a, e0, e1);
+    cudaEventElapsedTime(&b, e1, e2);
+    cudaEventElapsedTime(&d, e2, e3);
+    ctx.stats.ms_weights = a;
+    ctx.stats.ms_kernel_fit = b;
+    ctx.stats.ms_pansharpen = d;
+    ctx.stats.admm_iters = admm_iters.empty() ? 0 : admm_iters[0];
+    for (int i = 0; i < 64; ++i) ctx.stats.cg_iters[i] = i < static_cast<int>(cg_iters.size()) ? cg_iters[i] : 0;
+    cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2); cudaEventDestroy(e3);
+}
+
+}  // namespace fbmp_gpu
+
+using namespace fbmp_gpu;
+
+struct fbmp_gpu_ctx {
+    Context impl;
+    explicit fbmp_gpu_ctx(int dev) : impl(dev) {}
+};
+
+template <class F>
+static int guarded(F&& f) {
+    try {
+        f();
+        return FBMP_OK;
+    } catch (const Failure& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "out of host memory";
+        return FBMP_RUNTIME_ERROR;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return FBMP_RUNTIME_ERROR;
+    }
+}
+
+// Device copy of a host array in a context scratch slot.
+static double* upload(Context& ctx, const std::string& slot, const double* src, size_t count) {
+    double* d = ctx.scratch<double>(slot, count ? count : 1);
+    if (count) h2d(d, src, count * sizeof(double), ctx.stream);
+    return d;
+}
+static void download(Context& ctx, double* dst, const double* d, size_t count) {
+    d2h(dst, d, count * sizeof(double), ctx.stream);
+    FBMP_CUDA(cudaStreamSynchronize(ctx.stream));
+}
+static fbmp_ps_params ps_or_default(const fbmp_ps_params* p) {
+    fbmp_ps_params d;
+    fbmp_gpu_default_ps_params(&d);
+    return p ? *p : d;
+}
+static fbmp_ke_params ke_or_default(const fbmp_ke_params* p) {
+    fbmp_ke_params d;
+    fbmp_gpu_default_ke_params(&d);
+    return p ? *p : d;
+}
+static fbmp_sw_params sw_or_default(const fbmp_sw_params* p) {
+    fbmp_sw_params d;
+    fbmp_gpu_default_sw_params(&d);
+    return p ? *p : d;
+}
+
+extern "C" {
+
+void fbmp_gpu_default_ps_params(fbmp_ps_params* p) {
+    p->lambda = 2e-4;
+    p->radius = 1;
+    p->eps = 1e-4;
+    p->cg_tol = 5e-5;
+    p->cg_max_iter = 2000;
+    p->threads = 0;
+}
+void fbmp_gpu_default_ke_params(fbmp_ke_params* p) {
+    p->n = 29;
+    p->alpha1 = 1.0;
+    p->alpha2 = 0.006;
+    p->mu1 = p->mu2 = p->mu3 = 100.0;
+    p->rho = 0.5;
+    p->t_max = 10000;
+    p->th = 1e-5;
+    p->init = 0;
+}
+void fbmp_gpu_default_sw_params(fbmp_sw_params* p) {
+    p->l = 4;
+    p->lambda_omega = 10.0;
+    p->factor = 2;
+}
+
+int fbmp_gpu_ctx_create(int device, fbmp_gpu_ctx** out) {
+    return guarded([&] { *out = new fbmp_gpu_ctx(device); });
+}
+void fbmp_gpu_ctx_destroy(fbmp_gpu_ctx* ctx) { delete ctx; }
+const char* fbmp_gpu_last_error(void) { return g_last_error.c_str(); }
+int fbmp_gpu_ctx_stats(fbmp_gpu_ctx* ctx, fbmp_gpu_stats* out) {
+    *out = ctx->impl.stats;
+    return FBMP_OK;
+}
+void* fbmp_gpu_ctx_stream(fbmp_gpu_ctx* ctx) { return ctx->impl.stream; }
+long long fbmp_gpu_ctx_launches(fbmp_gpu_ctx* ctx) { return ctx->impl.launches; }
+
+int fbmp_gpu_pansharpen(fbmp_gpu_ctx* ctx, const double* lrms, int N, int h, int w, const double* pan,
+                        const double* k, int n, int factor, const fbmp_ps_params* params, double* out,
+                        int* cg_iters) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        const fbmp_ps_params prm = ps_or_default(params);
+        validate_ps(prm);
+        if (N < 1) dim_error("multi-band image needs at least one band");
+        if (factor < 1) param_error("downsample: factor must be >= 1");
+        const size_t p = static_cast<size_t>(h) * w, P = p * factor * factor;
+        double* d_l = upload(C, "api_lrms", lrms, p * N);
+        double* d_p = upload(C, "api_pan", pan, P);
+        double* d_k = upload(C, "api_taps", k, static_cast<size_t>(n) * n);
+        double* d_o = C.scratch<double>("api_out", P * N);
+        std::vector<int> it;
+        pansharpen_device(C, d_l, 1, N, h, w, d_p, d_k, n, factor, prm, d_o, it);
+        download(C, out, d_o, P * N);
+        for (int i = 0; i < N && i < 64; ++i) C.stats.cg_iters[i] = it[i];
+        if (cg_iters)
+            for (int i = 0; i < N; ++i) cg_iters[i] = it[i];
+    });
+}
+
+int fbmp_gpu_apply_prior(fbmp_gpu_ctx* ctx, const double* img, int H, int W, double* out) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        const size_t P = static_cast<size_t>(H) * W;
+        double* d_i = upload(C, "u_in", img, P);
+        double* d_o = C.scratch<double>("u_out", P);
+        laplacian_scaled(C, d_i, H, W, 1, nullptr, d_o);
+        download(C, out, d_o, P);
+    });
+}
+
+int fbmp_gpu_llp_apply(fbmp_gpu_ctx* ctx, const double* guide, const double* x, int H, int W, int radius, double eps,
+                       double* y) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        if (radius < 1) param_error("matting matrix: radius must be >= 1");
+        if (2 * radius + 1 > std::min(H, W)) dim_error("matting matrix: window larger than image");
+        const size_t P = static_cast<size_t>(H) * W;
+        double* d_g = upload(C, "u_guide", guide, P);
+        double* d_x = upload(C, "u_in", x, P);
+        double* d_o = C.scratch<double>("u_out", P);
+        double one = 1.0;
+        double* d_k = upload(C, "u_taps", &one, 1);
+        const PsGeo G = make_geo(1, H, W, 1, 1, radius, 1.0, eps);
+        cg_operator_apply(C, G, d_k, d_g, d_x, d_o, 1);
+        download(C, y, d_o, P);
+    });
+}
+
+int fbmp_gpu_data_apply(fbmp_gpu_ctx* ctx, const double* p, int H, int W, const double* k, int n, int factor,
+                        double* out) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        if (factor < 1) param_error("downsample: factor must be >= 1");
+        if (H % factor || W % factor) dim_error("downsample: dimensions not divisible by factor");
+        check_kernel(n, H, W);
+        const size_t P = static_cast<size_t>(H) * W;
+        double* d_x = upload(C, "u_in", p, P);
+        double* d_k = upload(C, "u_taps", k, static_cast<size_t>(n) * n);
+        double* d_o = C.scratch<double>("u_out", P);
+        const PsGeo G = make_geo(1, H / factor, W / factor, factor, n, 1, 1.0, 1.0);
+        cg_operator_apply(C, G, d_k, nullptr, d_x, d_o, 2);
+        download(C, out, d_o, P);
+    });
+}
+
+int fbmp_gpu_cg_operator(fbmp_gpu_ctx* ctx, const double* guide, const double* p, int H, int W, const double* k,
+                         int n, int factor, const fbmp_ps_params* params, double* out) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        const fbmp_ps_params prm = ps_or_default(params);
+        if (H % factor || W % factor) dim_error("downsample: dimensions not divisible by factor");
+        check_kernel(n, H, W);
+        const size_t P = static_cast<size_t>(H) * W;
+        double* d_g = upload(C, "u_guide", guide, P);
+        double* d_x = upload(C, "u_in", p, P);
+        double* d_k = upload(C, "u_taps", k, static_cast<size_t>(n) * n);
+        double* d_o = C.scratch<double>("u_out", P);
+        const PsGeo G = make_geo(1, H / factor, W / factor, factor, n, prm.radius, prm.lambda, prm.eps);
+        cg_operator_apply(C, G, d_k, d_g, d_x, d_o, 0);
+        download(C, out, d_o, P);
+    });
+}
+
+int fbmp_gpu_warmstart_cg(fbmp_gpu_ctx* ctx, const double* x, int h, int w, const double* guide, const double* k,
+                          int n, int factor, const fbmp_ps_params* params, int max_iters, int error_on_cap,
+                          double* z_out, int* iters, double* final_residual) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        const fbmp_ps_params prm = ps_or_default(params);
+        const int H = h * factor, W = w * factor;
+        check_kernel(n, H, W);
+        if (2 * prm.radius + 1 > std::min(H, W)) dim_error("matting matrix: window larger than image");
+        const size_t P = static_cast<size_t>(H) * W, p = static_cast<size_t>(h) * w;
+        double* d_g = upload(C, "w_guide", guide, P);
+        double* d_x = upload(C, "w_x", x, p);
+        double* d_k = upload(C, "w_taps", k, static_cast<size_t>(n) * n);
+        const PsGeo G = make_geo(1, h, w, factor, n, prm.radius, prm.lambda, prm.eps);
+        CgBuffers B;
+        B.z = C.scratch<double>("cg_z", P);
+        B.r = C.scratch<double>("cg_r", P);
+        B.p = C.scratch<double>("cg_p", 2 * P);
+        B.Ap = C.scratch<double>("cg_ap", P);
+        B.q = C.scratch<double>("cg_q", p);
+        B.part = C.scratch<double>("cg_part", 4 * ((P / 256 + 64) * 2 + 4096));
+        B.st = C.scratch<CgState>("cg_state", 1);
+        std::vector<CgState> hs;
+        cg_solve(C, G, d_k, d_g, d_x, B, max_iters, prm.cg_tol, hs);
+        download(C, z_out, B.z, P);
+        if (iters) *iters = hs[0].iters;
+        const bool converged = hs[0].done == 1;
+        double resid = 0.0;
+        if (final_residual || (!converged && error_on_cap)) {
+            double* az = C.scratch<double>("cg_res_az", P);
+            double* rhs = C.scratch<double>("cg_res_rhs", P);
+            cg_operator_apply(C, G, d_k, d_g, B.z, az, 0);
+            data_rhs(C, G, d_k, d_x, rhs);
+            std::vector<double> a(P), b(P);
+            d2h(a.data(), az, P * sizeof(double), C.stream);
+            d2h(b.data(), rhs, P * sizeof(double), C.stream);
+            FBMP_CUDA(cudaStreamSynchronize(C.stream));
+            double s = 0.0;
+            for (size_t i = 0; i < P; ++i) s += (a[i] - b[i]) * (a[i] - b[i]);
+            resid = std::sqrt(s);
+            if (hs[0].rhs_norm == 0.0) resid = 0.0;
+        }
+        if (final_residual) *final_residual = resid;
+        if (hs[0].done == 2) num_error("warmstart: conjugate gradients hit a non-positive curvature direction");
+        if (!converged && error_on_cap)
+            num_error("warmstart: conjugate gradients did not converge in " + std::to_string(max_iters) +
+                      " iterations (residual " + std::to_string(resid / hs[0].rhs_norm) + " relative)");
+    });
+}
+
+int fbmp_gpu_guided_filter(fbmp_gpu_ctx* ctx, const double* input, const double* guide, int H, int W, int radius,
+                           double eps, double* a_out, double* c_out, double* v_out) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        if (!(eps > 0)) param_error("guided_coeffs: eps must be positive");
+        if (radius < 0) param_error("box_mean: negative radius");
+        if (2 * radius + 1 > std::min(H, W)) dim_error("box_mean: window larger than image");
+        const size_t P = static_cast<size_t>(H) * W;
+        double* d_i = upload(C, "g_in", input, P);
+        double* d_g = upload(C, "g_guide", guide, P);
+        double* d_a = C.scratch<double>("g_a", P);
+        double* d_c = C.scratch<double>("g_c", P);
+        double* d_v = C.scratch<double>("g_v", P);
+        guided_filter(C, 1, H, W, radius, eps, d_i, 0, d_g, d_a, d_c, d_v, 1);
+        if (a_out) download(C, a_out, d_a, P);
+        if (c_out) download(C, c_out, d_c, P);
+        if (v_out) download(C, v_out, d_v, P);
+    });
+}
+
+int fbmp_gpu_guided_output(fbmp_gpu_ctx* ctx, const double* a, const double* c, const double* guide, int H, int W,
+                           int radius, double* out) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        if (radius < 0) param_error("box_mean: negative radius");
+        if (2 * radius + 1 > std::min(H, W)) dim_error("box_mean: window larger than image");
+        const size_t P = static_cast<size_t>(H) * W;
+        double* d_a = upload(C, "g_a", a, P);
+        double* d_c = upload(C, "g_c", c, P);
+        double* d_g = upload(C, "g_guide", guide, P);
+        double* d_ab = C.scratch<double>("g_ab", P);
+        double* d_cb = C.scratch<double>("g_cb", P);
+        double* d_o = C.scratch<double>("g_v", P);
+        box_mean(C, d_a, H, W, 1, radius, d_ab);
+        box_mean(C, d_c, H, W, 1, radius, d_cb);
+        guided_combine(C, d_ab, d_cb, d_g, static_cast<long long>(P), d_o);  // pansharpen.cpp:306-311
+        download(C, out, d_o, P);
+    });
+}
+
+int fbmp_gpu_solve_channel_fft(fbmp_gpu_ctx* ctx, const double* x, int h, int w, const double* k, int n, int factor,
+                               const double* v, const fbmp_ps_params* params, double* out) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        const fbmp_ps_params prm = ps_or_default(params);
+        validate_ps(prm);
+        const int H = h * factor, W = w * factor;
+        check_kernel(n, H, W);
+        const size_t P = static_cast<size_t>(H) * W, p = static_cast<size_t>(h) * w;
+        double* d_x = upload(C, "f_x", x, p);
+        double* d_v = upload(C, "f_v", v, P);
+        double* d_k = upload(C, "f_taps", k, static_cast<size_t>(n) * n);
+        double* d_o = C.scratch<double>("f_out", P);
+        int* flag = C.scratch<int>("f_flag", 1);
+        FBMP_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), C.stream));
+        const PsGeo G = make_geo(1, h, w, factor, n, prm.radius, prm.lambda, prm.eps);
+        solve_channel_fft(C, G, d_k, d_x, d_v, nullptr, d_o, flag);
+        int hf = 0;
+        d2h(&hf, flag, sizeof(int), C.stream);
+        download(C, out, d_o, P);
+        if (hf)
+            num_error("solve_channel_fft: alias-group system condition number exceeds 1e14 (prior transfer function "
+                      "too small)");
+    });
+}
+
+int fbmp_gpu_box_mean(fbmp_gpu_ctx* ctx, const double* img, int H, int W, int radius, double* out) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        if (radius < 0) param_error("box_mean: negative radius");
+        if (2 * radius + 1 > std::min(H, W)) dim_error("box_mean: window larger than image");
+        const size_t P = static_cast<size_t>(H) * W;
+        double* d_i = upload(C, "u_in", img, P);
+        double* d_o = C.scratch<double>("u_out", P);
+        box_mean(C, d_i, H, W, 1, radius, d_o);
+        download(C, out, d_o, P);
+    });
+}
+
+int fbmp_gpu_convolve(fbmp_gpu_ctx* ctx, const double* img, int H, int W, const double* k, int n, int adjoint,
+                      double* out) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        if (H < 1 || W < 1) dim_error("circular_convolve: empty image");
+        check_kernel(n, H, W);
+        const size_t P = static_cast<size_t>(H) * W;
+        double* d_i = upload(C, "u_in", img, P);
+        double* d_k = upload(C, "u_taps", k, static_cast<size_t>(n) * n);
+        double* d_o = C.scratch<double>("u_out", P);
+        convolve(C, d_i, H, W, d_k, n, adjoint, d_o);
+        download(C, out, d_o, P);
+    });
+}
+
+
+int fbmp_gpu_solve_weights(fbmp_gpu_ctx* ctx, const double* lrms_subset, int nb, int h, int w, const double* pan,
+                           const fbmp_sw_params* cfg, double* omega_out) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        const fbmp_sw_params sw = sw_or_default(cfg);
+        const int c = sw.factor;
+        if (c < 1) param_error("solve_weights: factor must be >= 1");
+        if (sw.l < 1) param_error("solve_weights: l must be >= 1");
+        if (sw.lambda_omega < 0.0) param_error("solve_weights: lambda_omega must be >= 0");
+        if (nb < 1) dim_error("multi-band image needs at least one band");
+        const size_t p = static_cast<size_t>(h) * w, P = p * c * c;
+        const int H = h * c, W = w * c;
+        if (sw.l + 1 > std::min(h, w) || c * sw.l + 1 > std::min(H, W))  // ops.cpp:132-133
+            dim_error("circular_box_blur: window larger than image");
+        double* d_l = upload(C, "api_lrms", lrms_subset, p * nb);
+        double* d_p = upload(C, "api_pan", pan, P);
+        double* d_o = C.scratch<double>("api_omega", nb);
+        int* st = C.scratch<int>("api_status", 1);
+        solve_weights_device(C, d_l, 1, nb, h, w, d_p, sw.l, sw.lambda_omega, c, d_o, st);
+        int hs = 0;
+        d2h(&hs, st, sizeof(int), C.stream);
+        download(C, omega_out, d_o, nb);
+        if (hs == 1)
+            num_error("solve_weights: normal matrix is singular (bands linearly dependent and lambda_omega too small)");
+        if (hs == 2) num_error("solve_weights: stationarity residual too large (ill-conditioned system)");
+    });
+}
+
+int fbmp_gpu_combine_bands(fbmp_gpu_ctx* ctx, const double* lrms_subset, int nb, int h, int w, const double* omega,
+                           double* out) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        const size_t p = static_cast<size_t>(h) * w;
+        double* d_l = upload(C, "api_lrms", lrms_subset, p * nb);
+        double* d_w = upload(C, "api_omega", omega, nb);
+        double* d_o = C.scratch<double>("api_obs", p);
+        combine_bands_device(C, d_l, 1, nb, static_cast<long long>(p), d_w, d_o);
+        download(C, out, d_o, p);
+    });
+}
+
+static void estimate_plane_host(Context& C, const double* pan, int H, int W, const double* obs, int factor,
+                                const fbmp_ke_params& prm, double* k_out, int* iters, double* state_out, int hook_t) {
+    validate_ke(prm);
+    if (factor < 1) param_error("build_observation: factor must be >= 1");
+    if (H % factor || W % factor) dim_error("build_observation: PAN dimensions must be factor times the observation");
+    const size_t P = static_cast<size_t>(H) * W, p = P / (static_cast<size_t>(factor) * factor);
+    const int n = prm.n, m = n * n;
+    double* d_p = upload(C, "api_pan", pan, P);
+    double* d_f = upload(C, "api_obs", obs, p);
+    double* d_k = C.scratch<double>("api_k", m);
+    double* d_s = state_out ? C.scratch<double>("api_state", static_cast<size_t>(17) * m) : nullptr;
+    std::vector<int> it;
+    estimate_kernel_device(C, d_p, d_f, 1, H, W, factor, prm, d_k, it, d_s, hook_t);
+    download(C, k_out, d_k, m);
+    if (d_s) download(C, state_out, d_s, static_cast<size_t>(17) * m);
+    if (iters) *iters = it[0];
+    C.stats.admm_iters = it[0];
+}
+
+int fbmp_gpu_estimate_kernel_plane(fbmp_gpu_ctx* ctx, const double* pan, int H, int W, const double* obs, int factor,
+                                   const fbmp_ke_params* params, double* k_out, int* iters, double* state_out,
+                                   int hook_t) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        estimate_plane_host(C, pan, H, W, obs, factor, ke_or_default(params), k_out, iters, state_out, hook_t);
+    });
+}
+
+int fbmp_gpu_estimate_kernel_tgv(fbmp_gpu_ctx* ctx, const double* lrms_subset, int nb, int h, int w, const double* pan,
+                                 const double* omega, int factor, const fbmp_ke_params* params, double* k_out,
+                                 int* iters) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        const size_t p = static_cast<size_t>(h) * w;
+        std::vector<double> obs(p);
+        {
+            double* d_l = upload(C, "api_lrms", lrms_subset, p * nb);
+            double* d_w = upload(C, "api_omega", omega, nb);
+            double* d_o = C.scratch<double>("api_obs2", p);
+            combine_bands_device(C, d_l, 1, nb, static_cast<long long>(p), d_w, d_o);
+            download(C, obs.data(), d_o, p);
+        }
+        estimate_plane_host(C, pan, h * factor, w * factor, obs.data(), factor, ke_or_default(params), k_out, iters,
+                            nullptr, -1);
+    });
+}
+
+int fbmp_gpu_blind_dev(fbmp_gpu_ctx* ctx, const double* d_lrms, int N, int h, int w, const double* d_pan,
+                       const fbmp_sw_params* sw, const fbmp_ke_params* ke, const fbmp_ps_params* ps, double* d_out,
+                       double* d_k_out) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        std::vector<int> ai, ci;
+        blind_device(C, d_lrms, 1, N, h, w, d_pan, sw_or_default(sw), ke_or_default(ke), ps_or_default(ps), d_out,
+                     d_k_out, nullptr, ai, ci);
+    });
+}
+
+int fbmp_gpu_blind(fbmp_gpu_ctx* ctx, const double* lrms, int N, int h, int w, const double* pan,
+                   const fbmp_sw_params* sw, const fbmp_ke_params* ke, const fbmp_ps_params* ps, double* out,
+                   double* k_out, double* omega_out) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        const fbmp_sw_params swp = sw_or_default(sw);
+        const fbmp_ke_params kep = ke_or_default(ke);
+        const int c = swp.factor;
+        if (c < 1) param_error("solve_weights: factor must be >= 1");
+        const size_t p = static_cast<size_t>(h) * w, P = p * c * c;
+        double* d_l = upload(C, "api_lrms", lrms, p * N);
+        double* d_p = upload(C, "api_pan", pan, P);
+        double* d_o = C.scratch<double>("api_out", P * N);
+        double* d_k = C.scratch<double>("api_k", static_cast<size_t>(kep.n) * kep.n);
+        double* d_w = C.scratch<double>("api_omega", N);
+        std::vector<int> ai, ci;
+        blind_device(C, d_l, 1, N, h, w, d_p, swp, kep, ps_or_default(ps), d_o, d_k, d_w, ai, ci);
+        download(C, out, d_o, P * N);
+        if (k_out) download(C, k_out, d_k, static_cast<size_t>(kep.n) * kep.n);
+        if (omega_out) download(C, omega_out, d_w, N);
+    });
+}
+
+int fbmp_gpu_blind_batch(fbmp_gpu_ctx* ctx, const double* lrms, int S, int N, int h, int w, const double* pan,
+                         const fbmp_sw_params* sw, const fbmp_ke_params* ke, const fbmp_ps_params* ps, double* out,
+                         double* k_out) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        const fbmp_sw_params swp = sw_or_default(sw);
+        const fbmp_ke_params kep = ke_or_default(ke);
+        const int c = swp.factor;
+        if (c < 1) param_error("solve_weights: factor must be >= 1");
+        const size_t p = static_cast<size_t>(h) * w, P = p * c * c;
+        double* d_l = upload(C, "api_lrms", lrms, p * N * S);
+        double* d_p = upload(C, "api_pan", pan, P * S);
+        double* d_o = C.scratch<double>("api_out", P * N * S);
+        double* d_k = C.scratch<double>("api_k", static_cast<size_t>(kep.n) * kep.n * S);
+        std::vector<int> ai, ci;
+        blind_device(C, d_l, S, N, h, w, d_p, swp, kep, ps_or_default(ps), d_o, d_k, nullptr, ai, ci);
+        download(C, out, d_o, P * N * S);
+        if (k_out) download(C, k_out, d_k, static_cast<size_t>(kep.n) * kep.n * S);
+    });
+}
+
+int fbmp_gpu_shrink2(fbmp_gpu_ctx* ctx, double* cols, int ncols, long long m, double t) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        if (t < 0) param_error("shrink2: threshold must be non-negative");
+        if (ncols < 1 || m < 1) return;
+        double* d = upload(C, "u_cols", cols, static_cast<size_t>(ncols) * m);
+        shrink2_device(C, d, ncols, m, t);
+        download(C, cols, d, static_cast<size_t>(ncols) * m);
+    });
+}
+
+int fbmp_gpu_project_simplex(fbmp_gpu_ctx* ctx, const double* v, int m, double* out) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        double* d_v = upload(C, "u_in", v, m);
+        double* d_o = C.scratch<double>("u_out", m);
+        int* st = C.scratch<int>("u_status", 1);
+        project_simplex_device(C, d_v, m, d_o, st);
+        int hs = 0;
+        d2h(&hs, st, sizeof(int), C.stream);
+        download(C, out, d_o, m);
+        if (hs) num_error("project_simplex: empty support (non-finite input?)");
+    });
+}
+
+int fbmp_gpu_solve_up(fbmp_gpu_ctx* ctx, const double* fields, int n, const fbmp_ke_params* params, double coupling,
+                      const double* anchor, double* u, double* p1, double* p2) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        const fbmp_ke_params prm = ke_or_default(params);
+        const size_t m = static_cast<size_t>(n) * n;
+        double* d_f = upload(C, "u_fields", fields, 12 * m);
+        double* d_a = anchor ? upload(C, "u_anchor", anchor, m) : nullptr;
+        double* d_u = C.scratch<double>("u_u", m);
+        double* d_p1 = C.scratch<double>("u_p1", m);
+        double* d_p2 = C.scratch<double>("u_p2", m);
+        solve_up_device(C, d_f, n, prm, coupling, d_a, d_u, d_p1, d_p2);
+        download(C, u, d_u, m);
+        download(C, p1, d_p1, m);
+        download(C, p2, d_p2, m);
+    });
+}
+
+int fbmp_gpu_gram(fbmp_gpu_ctx* ctx, const double* pan, int H, int W, const double* obs, int factor, int n,
+                  double* EtE, double* Etf) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        if (n < 1 || n % 2 == 0) param_error("build_observation: kernel side must be odd");
+        if (factor < 1) param_error("build_observation: factor must be >= 1");
+        if (H % factor || W % factor) dim_error("build_observation: PAN dimensions must be factor times the observation");
+        if (n > std::min(H, W)) dim_error("build_observation: kernel larger than PAN image");
+        const size_t P = static_cast<size_t>(H) * W, p = P / (static_cast<size_t>(factor) * factor);
+        const size_t n2 = static_cast<size_t>(n) * n;
+        double* d_p = upload(C, "api_pan", pan, P);
+        double* d_f = upload(C, "api_obs", obs, p);
+        double* d_G = C.scratch<double>("api_EtE", n2 * n2);
+        double* d_e = C.scratch<double>("api_Etf", n2);
+        gram_device(C, d_p, d_f, H, W, factor, n, d_G, d_e);
+        download(C, EtE, d_G, n2 * n2);
+        download(C, Etf, d_e, n2);
+    });
+}
+
+}  // extern "C"

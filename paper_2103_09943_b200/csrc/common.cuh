@@ -1,0 +1,186 @@
+// common.cuh -- shared device/host infrastructure for the sm_100a blind-pansharpening path.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "fbmp_gpu.h"
+
+namespace fbmp_gpu {
+
+// ---------------------------------------------------------------------------------------
+// Errors: the reference taxonomy (errors.hpp:8-33) as status codes at the C ABI.
+// ---------------------------------------------------------------------------------------
+struct Failure : std::runtime_error {
+    int code;
+    Failure(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void param_error(const std::string& m) { throw Failure(FBMP_PARAM_ERROR, m); }
+[[noreturn]] inline void dim_error(const std::string& m) { throw Failure(FBMP_DIMENSION_ERROR, m); }
+[[noreturn]] inline void num_error(const std::string& m) { throw Failure(FBMP_NUMERICAL_ERROR, m); }
+
+#define FBMP_CUDA(call)                                                                          \
+    do {                                                                                         \
+        cudaError_t e_ = (call);                                                                 \
+        if (e_ != cudaSuccess)                                                                   \
+            throw ::fbmp_gpu::Failure(FBMP_RUNTIME_ERROR, std::string("CUDA error: ") +          \
+                                                              cudaGetErrorString(e_) + " at " +  \
+                                                              __FILE__ + ":" + std::to_string(__LINE__)); \
+    } while (0)
+
+#define FBMP_CUFFT(call)                                                                         \
+    do {                                                                                         \
+        cufftResult r_ = (call);                                                                 \
+        if (r_ != CUFFT_SUCCESS)                                                                 \
+            throw ::fbmp_gpu::Failure(FBMP_RUNTIME_ERROR, "cuFFT error " + std::to_string(r_) +  \
+                                                              " at " + __FILE__ + ":" +          \
+                                                              std::to_string(__LINE__));         \
+    } while (0)
+
+// ---------------------------------------------------------------------------------------
+// Device buffers
+// ---------------------------------------------------------------------------------------
+template <class T>
+struct DevBuf {
+    T* ptr = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t count) { resize(count); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : ptr(o.ptr), n(o.n) { o.ptr = nullptr; o.n = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) { release(); ptr = o.ptr; n = o.n; o.ptr = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void release() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        n = 0;
+    }
+    void resize(size_t count) {
+        if (count <= n && ptr) return;
+        release();
+        if (count) FBMP_CUDA(cudaMalloc(&ptr, count * sizeof(T)));
+        n = count;
+    }
+    T* get() const { return ptr; }
+};
+
+// ---------------------------------------------------------------------------------------
+// Context: device, stream, cached workspaces and cuFFT plans.
+// ---------------------------------------------------------------------------------------
+struct Context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    long long launches = 0;
+    fbmp_gpu_stats stats{};
+    std::map<std::string, std::unique_ptr<DevBuf<unsigned char>>> ws;
+    std::map<std::tuple<int, int, int, int, int>, cufftHandle> plans;  // (kind, rows, cols, batch, 0)
+    int sm_count = 148;
+
+    explicit Context(int dev);
+    ~Context();
+    // named scratch buffer of at least `bytes` (contents undefined, reused across calls)
+    template <class T>
+    T* scratch(const std::string& name, size_t count) {
+        auto& b = ws[name];
+        if (!b) b = std::make_unique<DevBuf<unsigned char>>();
+        b->resize(count * sizeof(T));
+        return reinterpret_cast<T*>(b->get());
+    }
+    cufftHandle plan(int kind, int rows, int cols, int batch);
+    void count(int k = 1) { launches += k; }
+};
+
+// RAII device selection for calls made from arbitrary host threads.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+inline void h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    FBMP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+}
+inline void d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    FBMP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+}
+inline void check_launch() { FBMP_CUDA(cudaGetLastError()); }
+
+inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
+
+// ---------------------------------------------------------------------------------------
+// Device helpers
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ int floordiv(int a, int b) {  // b > 0
+    return (a >= 0) ? a / b : -((-a + b - 1) / b);
+}
+__device__ __forceinline__ int wrapi(int a, int m) {
+    int r = a % m;
+    return r < 0 ? r + m : r;
+}
+
+// Deterministic block reduction of one double (fixed shuffle tree + fixed warp order).
+// Every thread must call it; the result is valid in all threads.
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    return v;
+}
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* red /* >= NT/32 + 1 */) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        double s = lane < NT / 32 ? red[lane] : 0.0;
+        s = warp_sum(s);
+        if (lane == 0) red[NT / 32] = s;
+    }
+    __syncthreads();
+    return red[NT / 32];
+}
+
+// Sum of a partial array in a fixed order (identical bits in every block that calls it).
+template <int NT>
+__device__ __forceinline__ double sum_partials(const double* part, int n, int stride, double* red) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += NT) s += __ldcg(part + static_cast<size_t>(i) * stride);
+    return block_sum<NT>(s, red);
+}
+
+// Last-block election (threadFenceReduction pattern). Call after the block's partial
+// has been written by thread 0; returns true in every thread of the last block.
+__device__ __forceinline__ bool elect_last_block(unsigned int* counter, unsigned int nblocks) {
+    __shared__ bool am_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int prev = atomicAdd(counter, 1u);
+        am_last = (prev == nblocks - 1);
+    }
+    __syncthreads();
+    if (am_last) __threadfence();
+    return am_last;
+}
+
+}  // namespace fbmp_gpu

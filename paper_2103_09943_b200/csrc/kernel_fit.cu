@@ -1,0 +1,1223 @@
+// kernel_fit.cu -- sm_100a kernels of Algorithm 1 (TGV^2 + simplex blur-kernel fit,
+// reference /root/reference/proj/src/kernel_estimator.cpp) and of the spectral-weight stage
+// that feeds it (spectral_weights.cpp).
+//
+//   K_SW    box blurs + normal equations + full-pivot solve of Eq. (8), one block per scene
+//   K_GRAM  E^T E through its c-periodic block-Toeplitz structure: only the c^2 (2n-1)^2
+//           distinct sums T[rho][d] = sum_x P(x - rho) P(x - rho - d) are formed (E is never
+//           materialised); E^T f likewise from PAN patches staged in shared memory
+//   K_CHOL  blocked Cholesky of E^T E + mu3 I, explicit symmetric inverse (L^-T L^-1)
+//   K_ADMM  the whole ADMM loop in one persistent CTA per scene: all 17 n x n fields live in
+//           shared memory, DFTs as small matrix products, simplex projection by ranks;
+//           the only global traffic per iteration is the (E^T E + mu3 I)^-1 mat-vec (L2).
+#include <cmath>
+
+#include "kernel_fit.cuh"
+
+namespace fbmp_gpu {
+
+namespace {
+
+constexpr int NT = 256;
+
+inline int grid1d(Context& ctx, long long n, int threads = 256) {
+    long long b = (n + threads - 1) / threads;
+    const long long cap = static_cast<long long>(ctx.sm_count) * 16;
+    return static_cast<int>(std::max(1LL, std::min(b, cap)));
+}
+template <class K>
+void set_smem(K kernel, size_t bytes) {
+    FBMP_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+}
+
+// =============================================================================================
+// Spectral weights (spectral_weights.cpp:9-53)
+// =============================================================================================
+// Circular box blur along columns (ops.cpp:139-145) with output decimation dc:
+// out[b][r][j] = gain * sum_{t=-lead}^{win-lead-1} in[b][r][(dc*j - t) mod Win]
+__global__ void k_blur_h(const double* __restrict__ in, int B, int Hin, int Win, int Wout, int dc, int win,
+                         double* __restrict__ out) {
+    const int lead = (win - 1) / 2;
+    const double gain = 1.0 / win;
+    const long long tot = static_cast<long long>(B) * Hin * Wout;
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < tot;
+         e += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int j = static_cast<int>(e % Wout);
+        const long long br = e / Wout;
+        const double* row = in + br * Win;
+        double s = 0.0;
+        for (int t = -lead; t < win - lead; ++t) s += row[wrapi(dc * j - t, Win)];
+        out[e] = s * gain;
+    }
+}
+// ... and along rows (ops.cpp:146-152) with output decimation dr.
+__global__ void k_blur_v(const double* __restrict__ in, int B, int Hin, int W, int Hout, int dr, int win,
+                         double* __restrict__ out) {
+    const int lead = (win - 1) / 2;
+    const double gain = 1.0 / win;
+    const long long tot = static_cast<long long>(B) * Hout * W;
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < tot;
+         e += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int j = static_cast<int>(e % W);
+        const long long bi = e / W;
+        const int i = static_cast<int>(bi % Hout);
+        const long long b = bi / Hout;
+        const double* col = in + b * static_cast<long long>(Hin) * W + j;
+        double s = 0.0;
+        for (int t = -lead; t < win - lead; ++t) s += col[static_cast<size_t>(wrapi(dr * i - t, Hin)) * W];
+        out[e] = s * gain;
+    }
+}
+
+// per-block partial dot products: pairs (i<=j) of A columns, then A_i . b
+__global__ void __launch_bounds__(NT) k_sw_dots(const double* __restrict__ A, const double* __restrict__ bvec, int nb,
+                                                long long p, int nblk, double* __restrict__ part) {
+    __shared__ double red[NT / 32 + 1];
+    const int s = blockIdx.y;
+    const double* As = A + static_cast<size_t>(s) * nb * p;
+    const double* bs = bvec + static_cast<size_t>(s) * p;
+    const long long chunk = (p + nblk - 1) / nblk;
+    const long long lo = blockIdx.x * chunk, hi = std::min(p, lo + chunk);
+    const int nv = nb * (nb + 1) / 2 + nb;
+    int v = 0;
+    for (int i = 0; i < nb; ++i)
+        for (int j = i; j <= nb; ++j, ++v) {
+            const double* x = As + static_cast<size_t>(i) * p;
+            const double* y = j < nb ? As + static_cast<size_t>(j) * p : bs;
+            double acc = 0.0;
+            for (long long k = lo + threadIdx.x; k < hi; k += NT) acc += x[k] * y[k];
+            const double bsum = block_sum<NT>(acc, red);
+            if (threadIdx.x == 0) part[(static_cast<size_t>(s) * nblk + blockIdx.x) * nv + v] = bsum;
+        }
+}
+
+// one block per scene: sum partials, add lambda G^T G, full-pivot solve, stationarity check
+__global__ void k_sw_solve(const double* __restrict__ part, int nb, int nblk, double lambda_omega,
+                           double* __restrict__ omega, int* __restrict__ status) {
+    extern __shared__ double sh[];
+    const int s = blockIdx.x;
+    const int nv = nb * (nb + 1) / 2 + nb;
+    for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+        double acc = 0.0;
+        for (int b = 0; b < nblk; ++b) acc += part[(static_cast<size_t>(s) * nblk + b) * nv + v];
+        sh[v] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    double* N = sh + nv;          // nb*nb
+    double* rhs = N + nb * nb;    // nb
+    double* A = rhs + nb;         // nb*nb work
+    double* bw = A + nb * nb;     // nb
+    double* y = bw + nb;          // nb
+    int* perm = reinterpret_cast<int*>(y + nb);
+    int v = 0;
+    for (int i = 0; i < nb; ++i)
+        for (int j = i; j <= nb; ++j, ++v) {
+            if (j < nb) N[i * nb + j] = N[j * nb + i] = sh[v];
+            else rhs[i] = sh[v];
+        }
+    if (nb > 1)
+        for (int i = 0; i < nb; ++i)
+            for (int j = 0; j < nb; ++j) {
+                double g = 0.0;
+                for (int r = 0; r < nb - 1; ++r) {
+                    const double gi = (i == r) ? -1.0 : (i == r + 1 ? 1.0 : 0.0);
+                    const double gj = (j == r) ? -1.0 : (j == r + 1 ? 1.0 : 0.0);
+                    g += gi * gj;
+                }
+                N[i * nb + j] += lambda_omega * g;
+            }
+    for (int i = 0; i < nb * nb; ++i) A[i] = N[i];
+    for (int i = 0; i < nb; ++i) { bw[i] = rhs[i]; perm[i] = i; }
+    double maxpiv = 0.0;
+    int rank = 0;
+    for (int k = 0; k < nb; ++k) {  // Gauss with full pivoting (stands in for Eigen::FullPivLU)
+        int pr = k, pc = k;
+        double best = -1.0;
+        for (int i = k; i < nb; ++i)
+            for (int j = k; j < nb; ++j)
+                if (fabs(A[i * nb + j]) > best) { best = fabs(A[i * nb + j]); pr = i; pc = j; }
+        if (k == 0) maxpiv = best;
+        if (best <= maxpiv * 2.220446049250313e-16 * nb || best == 0.0) break;
+        ++rank;
+        if (pr != k) {
+            for (int j = 0; j < nb; ++j) { const double t = A[k * nb + j]; A[k * nb + j] = A[pr * nb + j]; A[pr * nb + j] = t; }
+            const double t = bw[k]; bw[k] = bw[pr]; bw[pr] = t;
+        }
+        if (pc != k) {
+            for (int i = 0; i < nb; ++i) { const double t = A[i * nb + k]; A[i * nb + k] = A[i * nb + pc]; A[i * nb + pc] = t; }
+            const int t = perm[k]; perm[k] = perm[pc]; perm[pc] = t;
+        }
+        for (int i = k + 1; i < nb; ++i) {
+            const double f = A[i * nb + k] / A[k * nb + k];
+            for (int j = k; j < nb; ++j) A[i * nb + j] -= f * A[k * nb + j];
+            bw[i] -= f * bw[k];
+        }
+    }
+    if (rank < nb) { status[s] = 1; return; }
+    for (int i = nb - 1; i >= 0; --i) {
+        double t = bw[i];
+        for (int j = i + 1; j < nb; ++j) t -= A[i * nb + j] * y[j];
+        y[i] = t / A[i * nb + i];
+    }
+    double* om = omega + static_cast<size_t>(s) * nb;
+    for (int i = 0; i < nb; ++i) om[perm[i]] = y[i];
+    double r2 = 0.0, b2 = 0.0;
+    for (int i = 0; i < nb; ++i) {
+        double t = 0.0;
+        for (int j = 0; j < nb; ++j) t += N[i * nb + j] * om[j];
+        r2 += (t - rhs[i]) * (t - rhs[i]);
+        b2 += rhs[i] * rhs[i];
+    }
+    status[s] = (sqrt(r2) <= 1e-8 * sqrt(b2) + 1e-12) ? 0 : 2;
+}
+
+__global__ void k_combine(const double* __restrict__ lrms, int S, int nb, long long p, const double* __restrict__ omega,
+                          double* __restrict__ out) {
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < S * p;
+         e += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long s = e / p, j = e - s * p;
+        double acc = 0.0;
+        for (int i = 0; i < nb; ++i) acc += omega[s * nb + i] * lrms[(s * nb + i) * p + j];
+        out[e] = acc;
+    }
+}
+
+// PAN statistics: {sum, min, max, max|v|} per scene
+__global__ void __launch_bounds__(NT) k_stats_partial(const double* __restrict__ pan, long long P, int nblk,
+                                                      double* __restrict__ part) {
+    __shared__ double red[NT / 32 + 1];
+    __shared__ double mn[NT], mx[NT], ma[NT];
+    const int s = blockIdx.y;
+    const double* ps = pan + static_cast<size_t>(s) * P;
+    double sum = 0.0, lo = INFINITY, hi = -INFINITY, am = 0.0;
+    for (long long i = blockIdx.x * static_cast<long long>(NT) + threadIdx.x; i < P; i += static_cast<long long>(nblk) * NT) {
+        const double v = ps[i];
+        sum += v;
+        lo = fmin(lo, v);
+        hi = fmax(hi, v);
+        am = fmax(am, fabs(v));
+    }
+    const double bs = block_sum<NT>(sum, red);
+    mn[threadIdx.x] = lo; mx[threadIdx.x] = hi; ma[threadIdx.x] = am;
+    __syncthreads();
+    for (int o = NT / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            mn[threadIdx.x] = fmin(mn[threadIdx.x], mn[threadIdx.x + o]);
+            mx[threadIdx.x] = fmax(mx[threadIdx.x], mx[threadIdx.x + o]);
+            ma[threadIdx.x] = fmax(ma[threadIdx.x], ma[threadIdx.x + o]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        double* o = part + (static_cast<size_t>(s) * nblk + blockIdx.x) * 4;
+        o[0] = bs; o[1] = mn[0]; o[2] = mx[0]; o[3] = ma[0];
+    }
+}
+__global__ void k_stats_final(const double* __restrict__ part, int nblk, double* __restrict__ stats) {
+    const int s = blockIdx.x;
+    if (threadIdx.x != 0) return;
+    double sum = 0.0, lo = INFINITY, hi = -INFINITY, am = 0.0;
+    for (int b = 0; b < nblk; ++b) {
+        const double* o = part + (static_cast<size_t>(s) * nblk + b) * 4;
+        sum += o[0]; lo = fmin(lo, o[1]); hi = fmax(hi, o[2]); am = fmax(am, o[3]);
+    }
+    stats[s * 4 + 0] = sum; stats[s * 4 + 1] = lo; stats[s * 4 + 2] = hi; stats[s * 4 + 3] = am;
+}
+
+// =============================================================================================
+// K_GRAM
+// =============================================================================================
+constexpr int TG = 16;  // LR tile side of the Gram kernels
+
+// T[s][rho][d] partials for one LR tile and one sampling phase rho = (rho_r, rho_c):
+//   sum_{(i,j) in tile} P(c i - rho_r + C, c j - rho_c + C) * P(c i - rho_r - dr + C, c j - rho_c - dc + C)
+// with P = pan * scale (the reference's pan_n, kernel_estimator.cpp:443-444).
+__global__ void __launch_bounds__(NT) k_gram_T(const double* __restrict__ pan, const double* __restrict__ scale, int H,
+                                               int W, int h, int w, int c, int n, double* __restrict__ part,
+                                               int ntiles) {
+    extern __shared__ double reg[];
+    const int s = blockIdx.z, phase = blockIdx.y, tile = blockIdx.x;
+    const int rho_r = phase / c, rho_c = phase - rho_r * c;
+    const int ntx = (w + TG - 1) / TG;
+    const int i0 = (tile / ntx) * TG, j0 = (tile % ntx) * TG;
+    const int C = (n - 1) / 2, D = 2 * n - 1, nd = D * D;
+    const int SR = c * (TG - 1) + 2 * (n - 1) + 1;
+    const int R0 = c * i0 - rho_r + C - (n - 1), C0 = c * j0 - rho_c + C - (n - 1);
+    const double sc = scale ? scale[s] : 1.0;
+    const double* ps = pan + static_cast<size_t>(s) * H * W;
+    for (int e = threadIdx.x; e < SR * SR; e += NT) {
+        const int y = e / SR, x = e - y * SR;
+        reg[e] = ps[static_cast<size_t>(wrapi(R0 + y, H)) * W + wrapi(C0 + x, W)] * sc;
+    }
+    __syncthreads();
+    const int ni = min(TG, h - i0), nj = min(TG, w - j0);
+    double* out = part + ((static_cast<size_t>(s) * ntiles + tile) * c * c + phase) * nd;
+    constexpr int K = 8;
+    for (int o0 = 0; o0 < nd; o0 += NT * K) {
+        double acc[K];
+        int off[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            acc[k] = 0.0;
+            const int o = o0 + k * NT + threadIdx.x;
+            const int dr = o / D - (n - 1), dc = o % D - (n - 1);
+            off[k] = (o < nd) ? dr * SR + dc : 0;
+        }
+        for (int ii = 0; ii < ni; ++ii)
+            for (int jj = 0; jj < nj; ++jj) {
+                const int cp = (c * ii + n - 1) * SR + c * jj + n - 1;
+                const double cv = reg[cp];
+#pragma unroll
+                for (int k = 0; k < K; ++k) acc[k] = fma(cv, reg[cp - off[k]], acc[k]);
+            }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int o = o0 + k * NT + threadIdx.x;
+            if (o < nd) out[o] = acc[k];
+        }
+    }
+}
+
+// E^T f partials: sum_{(i,j) in tile} P(c i - tr + C, c j - tc + C) * f(i, j), f = obs * scale
+__global__ void __launch_bounds__(NT) k_gram_etf(const double* __restrict__ pan, const double* __restrict__ obs,
+                                                 const double* __restrict__ scale, int H, int W, int h, int w, int c,
+                                                 int n, double* __restrict__ part, int ntiles) {
+    extern __shared__ double reg[];
+    const int s = blockIdx.z, tile = blockIdx.x;
+    const int ntx = (w + TG - 1) / TG;
+    const int i0 = (tile / ntx) * TG, j0 = (tile % ntx) * TG;
+    const int C = (n - 1) / 2, n2 = n * n;
+    const int SR = c * (TG - 1) + n;
+    const int R0 = c * i0 + C - (n - 1), C0 = c * j0 + C - (n - 1);
+    const double sc = scale ? scale[s] : 1.0;
+    const double* ps = pan + static_cast<size_t>(s) * H * W;
+    const double* fs = obs + static_cast<size_t>(s) * h * w;
+    double* sf = reg + ((SR * SR + 1) & ~1);
+    for (int e = threadIdx.x; e < SR * SR; e += NT) {
+        const int y = e / SR, x = e - y * SR;
+        reg[e] = ps[static_cast<size_t>(wrapi(R0 + y, H)) * W + wrapi(C0 + x, W)] * sc;
+    }
+    const int ni = min(TG, h - i0), nj = min(TG, w - j0);
+    for (int e = threadIdx.x; e < TG * TG; e += NT) {
+        const int a = e / TG, b = e - a * TG;
+        sf[e] = (a < ni && b < nj) ? fs[static_cast<size_t>(i0 + a) * w + j0 + b] * sc : 0.0;
+    }
+    __syncthreads();
+    for (int tap = threadIdx.x; tap < n2; tap += NT) {
+        const int tr = tap / n, tc = tap - tr * n;
+        double acc = 0.0;
+        for (int ii = 0; ii < ni; ++ii)
+            for (int jj = 0; jj < nj; ++jj)
+                acc = fma(reg[(c * ii + n - 1 - tr) * SR + c * jj + n - 1 - tc], sf[ii * TG + jj], acc);
+        part[(static_cast<size_t>(s) * ntiles + tile) * n2 + tap] = acc;
+    }
+}
+
+// fixed-order reduction over tiles: out[s][v] = sum_t part[s][t][v]
+__global__ void k_reduce_tiles(const double* __restrict__ part, int S, int ntiles, int nv, double* __restrict__ out) {
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < static_cast<long long>(S) * nv;
+         e += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long s = e / nv, v = e - s * nv;
+        double acc = 0.0;
+        for (int t = 0; t < ntiles; ++t) acc += part[(s * ntiles + t) * nv + v];
+        out[e] = acc;
+    }
+}
+
+// G[(tr,tc),(tr',tc')] = T[tr mod c][tc mod c][tr'-tr][tc'-tc] (+ mu3 on the diagonal)
+__global__ void k_gram_expand(const double* __restrict__ T, int S, int c, int n, double mu3, double* __restrict__ M) {
+    const int n2 = n * n, D = 2 * n - 1, nd = D * D;
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+         e < static_cast<long long>(S) * n2 * n2; e += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long s = e / (static_cast<long long>(n2) * n2);
+        const int ab = static_cast<int>(e - s * n2 * static_cast<long long>(n2));
+        const int a = ab / n2, b = ab - a * n2;
+        const int tr = a / n, tc = a - tr * n, tr2 = b / n, tc2 = b - tr2 * n;
+        const int phase = (tr % c) * c + (tc % c);
+        const int d = (tr2 - tr + n - 1) * D + (tc2 - tc + n - 1);
+        double v = T[(s * c * c + phase) * nd + d];
+        if (a == b) v += mu3;
+        M[e] = v;
+    }
+}
+
+// =============================================================================================
+// K_CHOL: blocked right-looking Cholesky (lower), explicit inverse
+// =============================================================================================
+constexpr int NBK = 32;
+
+// factor the panel A[K:N, K:K+nb] in shared memory (diagonal block + sub-panel solve)
+__global__ void __launch_bounds__(NT) k_potrf_panel(double* __restrict__ M, int N, int K, int* __restrict__ status) {
+    extern __shared__ double pnl[];
+    const int s = blockIdx.x;
+    if (status[s]) return;
+    double* A = M + static_cast<size_t>(s) * N * N;
+    const int nb = min(NBK, N - K), rows = N - K;
+    for (int e = threadIdx.x; e < rows * nb; e += NT) {
+        const int i = e / nb, j = e - i * nb;
+        pnl[e] = A[static_cast<size_t>(K + i) * N + K + j];
+    }
+    __shared__ int fail;
+    if (threadIdx.x == 0) fail = 0;
+    __syncthreads();
+    for (int k = 0; k < nb; ++k) {
+        if (threadIdx.x == 0) {
+            const double d = pnl[k * nb + k];
+            if (!(d > 0)) fail = 1;
+            pnl[k * nb + k] = sqrt(d);
+        }
+        __syncthreads();
+        if (fail) break;
+        const double l = pnl[k * nb + k];
+        for (int i = k + 1 + threadIdx.x; i < rows; i += NT) pnl[i * nb + k] /= l;
+        __syncthreads();
+        for (int e = threadIdx.x; e < (rows - k - 1) * (nb - k - 1); e += NT) {
+            const int i = k + 1 + e / (nb - k - 1), j = k + 1 + e % (nb - k - 1);
+            if (j <= i) pnl[i * nb + j] -= pnl[i * nb + k] * pnl[j * nb + k];
+        }
+        __syncthreads();
+    }
+    if (fail) {
+        if (threadIdx.x == 0) status[s] = 1;
+        return;
+    }
+    for (int e = threadIdx.x; e < rows * nb; e += NT) {
+        const int i = e / nb, j = e - i * nb;
+        A[static_cast<size_t>(K + i) * N + K + j] = (i >= j) ? pnl[e] : 0.0;
+    }
+}
+
+// trailing update A[I][J] -= L[I][K:K+nb] L[J][K:K+nb]^T for 32x32 lower tiles beyond K+nb
+__global__ void __launch_bounds__(NT) k_syrk(double* __restrict__ M, int N, int K, const int* __restrict__ status) {
+    __shared__ double LI[NBK][NBK + 1], LJ[NBK][NBK + 1];
+    const int s = blockIdx.y;
+    if (status[s]) return;
+    double* A = M + static_cast<size_t>(s) * N * N;
+    const int base = K + NBK;
+    const int nt = (N - base + NBK - 1) / NBK;
+    // blockIdx.x enumerates lower tiles (ti >= tj)
+    int t = blockIdx.x, ti = 0;
+    while (t >= ti + 1) { t -= ti + 1; ++ti; }
+    const int tj = t;
+    if (ti >= nt) return;
+    const int r0 = base + ti * NBK, c0 = base + tj * NBK;
+    for (int e = threadIdx.x; e < NBK * NBK; e += NT) {
+        const int a = e / NBK, b = e - a * NBK;
+        LI[a][b] = (r0 + a < N) ? A[static_cast<size_t>(r0 + a) * N + K + b] : 0.0;
+        LJ[a][b] = (c0 + a < N) ? A[static_cast<size_t>(c0 + a) * N + K + b] : 0.0;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < NBK * NBK; e += NT) {
+        const int a = e / NBK, b = e - a * NBK;
+        const int i = r0 + a, j = c0 + b;
+        if (i < N && j < N && j <= i) {
+            double acc = 0.0;
+#pragma unroll 8
+            for (int k = 0; k < NBK; ++k) acc = fma(LI[a][k], LJ[b][k], acc);
+            A[static_cast<size_t>(i) * N + j] -= acc;
+        }
+    }
+}
+
+// L^-1 column by column (one warp per column, forward substitution)
+__global__ void __launch_bounds__(NT) k_trtri(const double* __restrict__ M, int N, double* __restrict__ Linv,
+                                              const int* __restrict__ status) {
+    extern __shared__ double ys[];
+    const int s = blockIdx.y;
+    if (status[s]) return;
+    const double* L = M + static_cast<size_t>(s) * N * N;
+    double* Li = Linv + static_cast<size_t>(s) * N * N;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int j = blockIdx.x * (NT / 32) + warp;
+    if (j >= N) return;
+    double* y = ys + warp * N;
+    for (int i = lane; i < N; i += 32) y[i] = 0.0;
+    __syncwarp();
+    if (lane == 0) y[j] = 1.0 / L[static_cast<size_t>(j) * N + j];
+    __syncwarp();
+    for (int i = j + 1; i < N; ++i) {
+        const double* row = L + static_cast<size_t>(i) * N;
+        double acc = 0.0;
+        for (int k = j + lane; k < i; k += 32) acc = fma(row[k], y[k], acc);
+        acc = warp_sum(acc);
+        if (lane == 0) y[i] = -acc / row[i];
+        __syncwarp();
+    }
+    for (int i = lane; i < N; i += 32) Li[static_cast<size_t>(i) * N + j] = y[i];
+}
+
+// Ginv[a][b] = sum_k Linv[k][a] Linv[k][b] (a >= b), mirrored -> exactly symmetric
+__global__ void __launch_bounds__(NT) k_inv_gram(const double* __restrict__ Linv, int N, double* __restrict__ Ginv,
+                                                 const int* __restrict__ status) {
+    __shared__ double A_[NBK][NBK + 1], B_[NBK][NBK + 1];
+    const int s = blockIdx.y;
+    if (status[s]) return;
+    const double* Li = Linv + static_cast<size_t>(s) * N * N;
+    double* G = Ginv + static_cast<size_t>(s) * N * N;
+    int t = blockIdx.x, ti = 0;
+    while (t >= ti + 1) { t -= ti + 1; ++ti; }
+    const int tj = t;
+    const int nt = (N + NBK - 1) / NBK;
+    if (ti >= nt) return;
+    const int a0 = ti * NBK, b0 = tj * NBK;
+    double acc[NBK * NBK / NT];
+#pragma unroll
+    for (int q = 0; q < NBK * NBK / NT; ++q) acc[q] = 0.0;
+    for (int k0 = a0; k0 < N; k0 += NBK) {  // Linv[k][a] = 0 for k < a
+        __syncthreads();
+        for (int e = threadIdx.x; e < NBK * NBK; e += NT) {
+            const int kk = e / NBK, x = e - kk * NBK;
+            const int k = k0 + kk;
+            A_[kk][x] = (k < N && a0 + x < N) ? Li[static_cast<size_t>(k) * N + a0 + x] : 0.0;
+            B_[kk][x] = (k < N && b0 + x < N) ? Li[static_cast<size_t>(k) * N + b0 + x] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < NBK * NBK / NT; ++q) {
+            const int e = threadIdx.x + q * NT;
+            const int a = e / NBK, b = e - a * NBK;
+            double v = acc[q];
+            for (int kk = 0; kk < NBK; ++kk) v = fma(A_[kk][a], B_[kk][b], v);
+            acc[q] = v;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < NBK * NBK / NT; ++q) {
+        const int e = threadIdx.x + q * NT;
+        const int a = a0 + e / NBK, b = b0 + e % NBK;
+        if (a < N && b < N && b <= a) {
+            G[static_cast<size_t>(a) * N + b] = acc[q];
+            G[static_cast<size_t>(b) * N + a] = acc[q];
+        }
+    }
+}
+
+// =============================================================================================
+// K_ADMM
+// =============================================================================================
+struct AdmmArgs {
+    int n, m;
+    double alpha1, alpha2, mu1, mu2, mu3, rho, th, coupling;
+    int t_max, t_begin, phase_begin, hook_t, init_kind, init_state;
+};
+
+constexpr int NTADMM = 512;
+enum { F_U = 0, F_P1, F_P2, F_X0, F_X1, F_Y0, F_Y1, F_Y2, F_Y3, F_Z, F_L10, F_L11, F_L20, F_L21, F_L22, F_L23, F_L3 };
+
+struct AdmmSmem {
+    double* f[17];
+    double *bz, *zz, *unew, *tmp6;  // tmp6: 6*m
+    double *spec, *rowt;            // 3 complex planes each (6*m doubles)
+    double *twc, *tws;              // n
+    double* red;
+};
+
+__device__ inline double dft_tw(const double* twc, const double* tws, int k, bool im) { return im ? tws[k] : twc[k]; }
+
+// forward 2-D DFT of 3 real n x n planes (src[f]) -> spec (3 interleaved complex planes)
+__device__ void dft3_forward(const AdmmSmem& S, int n, const double* const src[3]) {
+    const int m = n * n;
+    for (int e = threadIdx.x; e < 3 * m; e += blockDim.x) {  // rows: T[r][kc] = sum_c x[r][c] w^(kc c)
+        const int f = e / m, rc = e - f * m, r = rc / n, kc = rc - r * n;
+        const double* x = src[f] + r * n;
+        double re = 0.0, im = 0.0;
+        int idx = 0;
+        for (int c = 0; c < n; ++c) {
+            re = fma(x[c], S.twc[idx], re);
+            im = fma(-x[c], S.tws[idx], im);
+            idx += kc;
+            if (idx >= n) idx -= n;
+        }
+        S.rowt[2 * e] = re;
+        S.rowt[2 * e + 1] = im;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < 3 * m; e += blockDim.x) {  // cols: F[kr][kc] = sum_r T[r][kc] w^(kr r)
+        const int f = e / m, rc = e - f * m, kr = rc / n, kc = rc - kr * n;
+        const double* T = S.rowt + 2 * (f * m + kc);
+        double re = 0.0, im = 0.0;
+        int idx = 0;
+        for (int r = 0; r < n; ++r) {
+            const double tr = T[2 * r * n], ti = T[2 * r * n + 1];
+            const double wc = S.twc[idx], wsn = -S.tws[idx];
+            re = fma(tr, wc, fma(-ti, wsn, re));
+            im = fma(tr, wsn, fma(ti, wc, im));
+            idx += kr;
+            if (idx >= n) idx -= n;
+        }
+        S.spec[2 * e] = re;
+        S.spec[2 * e + 1] = im;
+    }
+    __syncthreads();
+}
+
+// inverse 2-D DFT of spec -> dst[f] = Re(.) / m  (fft_util.cpp:47-56)
+__device__ void dft3_inverse(const AdmmSmem& S, int n, double* const dst[3]) {
+    const int m = n * n;
+    for (int e = threadIdx.x; e < 3 * m; e += blockDim.x) {  // rows over kc
+        const int f = e / m, rc = e - f * m, kr = rc / n, c = rc - kr * n;
+        const double* F = S.spec + 2 * (f * m + kr * n);
+        double re = 0.0, im = 0.0;
+        int idx = 0;
+        for (int kc = 0; kc < n; ++kc) {
+            const double fr = F[2 * kc], fi = F[2 * kc + 1];
+            const double wc = S.twc[idx], wsn = S.tws[idx];
+            re = fma(fr, wc, fma(-fi, wsn, re));
+            im = fma(fr, wsn, fma(fi, wc, im));
+            idx += c;
+            if (idx >= n) idx -= n;
+        }
+        S.rowt[2 * e] = re;
+        S.rowt[2 * e + 1] = im;
+    }
+    __syncthreads();
+    const double inv = 1.0 / static_cast<double>(m);
+    for (int e = threadIdx.x; e < 3 * m; e += blockDim.x) {
+        const int f = e / m, rc = e - f * m, r = rc / n, c = rc - r * n;
+        const double* T = S.rowt + 2 * (f * m + c);
+        double re = 0.0;
+        int idx = 0;
+        for (int kr = 0; kr < n; ++kr) {
+            re = fma(T[2 * kr * n], S.twc[idx], fma(-T[2 * kr * n + 1], S.tws[idx], re));
+            idx += r;
+            if (idx >= n) idx -= n;
+        }
+        dst[f][rc] = re * inv;
+    }
+    __syncthreads();
+}
+
+// {u,p} solve (kernel_estimator.cpp:137-233) on fields in shared memory; writes u -> uout,
+// p1 -> p1out, p2 -> p2out. anchor (nullable) already holds z - L3.
+__device__ void up_solve(const AdmmSmem& S, int n, double a1m1, double a2m2, double coupling, const double* x0,
+                         const double* x1, const double* y0, const double* y1, const double* y2, const double* y3,
+                         const double* L10, const double* L11, const double* L20, const double* L21, const double* L22,
+                         const double* L23, const double* anchor, double* uout, double* p1out, double* p2out) {
+    const int m = n * n;
+    double* x1m = S.tmp6;
+    double* x2m = S.tmp6 + m;
+    double* y1m = S.tmp6 + 2 * m;
+    double* y2m = S.tmp6 + 3 * m;
+    double* ycm = S.tmp6 + 4 * m;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        x1m[i] = x0[i] - L10[i];
+        x2m[i] = x1[i] - L11[i];
+        y1m[i] = y0[i] - L20[i];
+        y2m[i] = y3[i] - L23[i];
+        ycm[i] = (((y1[i] - L21[i]) + y2[i]) - L22[i]) * 0.5;
+    }
+    __syncthreads();
+    double* B1 = uout;  // reuse the output planes as right-hand sides
+    double* B2 = p1out;
+    double* B3 = p2out;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        const int r = i / n, c = i - r * n;
+        const int cl = r * n + (c + n - 1) % n, ru = ((r + n - 1) % n) * n + c;  // left / upper neighbours
+        const double g1 = x1m[cl] - x1m[i], g2 = x2m[ru] - x2m[i];               // ops.cpp:87-97
+        const double h1 = y1m[cl] - y1m[i], h2 = ycm[ru] - ycm[i];
+        const double k1 = y2m[ru] - y2m[i], k2 = ycm[cl] - ycm[i];
+        double b1 = (g1 + g2) * a1m1;
+        if (coupling > 0.0 && anchor) b1 = b1 + anchor[i] * coupling;
+        B1[i] = b1;
+        B2[i] = (x1m[i] * -a1m1) + (h1 + h2) * a2m2;
+        B3[i] = (x2m[i] * -a1m1) + (k1 + k2) * a2m2;
+    }
+    __syncthreads();
+    const double* src[3] = {B1, B2, B3};
+    dft3_forward(S, n, src);
+    // max |den| for the singular tolerance (kernel_estimator.cpp:174-197)
+    double dmax = 0.0;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        const int r = i / n, c = i - r * n;
+        const double dvr = S.twc[r] - 1.0, dvi = S.tws[r];
+        const double dhr = S.twc[c] - 1.0, dhi = S.tws[c];
+        const double av2 = dvr * dvr + dvi * dvi, ah2 = dhr * dhr + dhi * dhi;
+        const double d1 = a1m1 * (ah2 + av2) + coupling;
+        const double d2 = a1m1 + 0.5 * a2m2 * av2 + a2m2 * ah2;
+        const double d3 = a1m1 + 0.5 * a2m2 * ah2 + a2m2 * av2;
+        const double d4r = -a1m1 * dhr, d4i = -a1m1 * dhi, d5r = -a1m1 * dvr, d5i = -a1m1 * dvi;
+        const double d6r = 0.5 * a2m2 * (dhr * dvr + dhi * dvi), d6i = 0.5 * a2m2 * (dhr * dvi - dhi * dvr);
+        // den = d1 (d2 d3 - |d6|^2) - conj(d4)(d4 d3 - conj(d6) d5) + conj(d5)(d4 d6 - d2 d5)
+        const double t1 = d1 * (d2 * d3 - (d6r * d6r + d6i * d6i));
+        const double ar = d4r * d3 - (d6r * d5r + d6i * d5i), ai = d4i * d3 - (d6r * d5i - d6i * d5r);
+        const double br = (d4r * d6r - d4i * d6i) - d2 * d5r, bi = (d4r * d6i + d4i * d6r) - d2 * d5i;
+        const double dr_ = t1 - (d4r * ar + d4i * ai) + (d5r * br + d5i * bi);
+        const double di_ = -(d4r * ai - d4i * ar) + (d5r * bi - d5i * br);
+        dmax = fmax(dmax, sqrt(dr_ * dr_ + di_ * di_));
+    }
+    // block max (exact)
+    S.red[threadIdx.x] = dmax;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) S.red[threadIdx.x] = fmax(S.red[threadIdx.x], S.red[threadIdx.x + o]);
+        __syncthreads();
+    }
+    const double tol = 1e-12 * S.red[0];
+    __syncthreads();
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        const int r = i / n, c = i - r * n;
+        const double dvr = S.twc[r] - 1.0, dvi = S.tws[r];
+        const double dhr = S.twc[c] - 1.0, dhi = S.tws[c];
+        const double av2 = dvr * dvr + dvi * dvi, ah2 = dhr * dhr + dhi * dhi;
+        const double d1 = a1m1 * (ah2 + av2) + coupling;
+        const double d2 = a1m1 + 0.5 * a2m2 * av2 + a2m2 * ah2;
+        const double d3 = a1m1 + 0.5 * a2m2 * ah2 + a2m2 * av2;
+        // complex helpers
+        struct Z { double x, y; };
+        auto mul = [](Z a, Z b) { return Z{a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x}; };
+        auto cj = [](Z a) { return Z{a.x, -a.y}; };
+        auto sub = [](Z a, Z b) { return Z{a.x - b.x, a.y - b.y}; };
+        auto add = [](Z a, Z b) { return Z{a.x + b.x, a.y + b.y}; };
+        auto rs = [](double s, Z a) { return Z{s * a.x, s * a.y}; };
+        const Z dh{dhr, dhi}, dv{dvr, dvi};
+        const Z d4 = rs(-a1m1, dh), d5 = rs(-a1m1, dv);
+        const Z d6 = rs(0.5 * a2m2, mul(cj(dh), dv));
+        const double n6 = d6.x * d6.x + d6.y * d6.y;
+        const Z den = add(sub(Z{d1 * (d2 * d3 - n6), 0.0}, mul(cj(d4), sub(rs(d3, d4), mul(cj(d6), d5)))),
+                          mul(cj(d5), sub(mul(d4, d6), rs(d2, d5))));
+        Z b1{S.spec[2 * i], S.spec[2 * i + 1]};
+        Z b2{S.spec[2 * (m + i)], S.spec[2 * (m + i) + 1]};
+        Z b3{S.spec[2 * (2 * m + i)], S.spec[2 * (2 * m + i) + 1]};
+        Z fu, fp1, fp2;
+        const double aden = sqrt(den.x * den.x + den.y * den.y);
+        if (aden > tol) {
+            const Z nu = add(sub(rs(d2 * d3 - n6, b1), mul(cj(d4), sub(rs(d3, b2), mul(cj(d6), b3)))),
+                             mul(cj(d5), sub(mul(b2, d6), rs(d2, b3))));
+            const Z np1 = add(sub(rs(d1, sub(rs(d3, b2), mul(cj(d6), b3))), mul(b1, sub(rs(d3, d4), mul(cj(d6), d5)))),
+                              mul(cj(d5), sub(mul(d4, b3), mul(b2, d5))));
+            const Z np2 = add(sub(rs(d1, sub(rs(d2, b3), mul(d6, b2))), mul(cj(d4), sub(mul(d4, b3), mul(b2, d5)))),
+                              mul(b1, sub(mul(d4, d6), rs(d2, d5))));
+            const double dd = den.x * den.x + den.y * den.y;
+            auto divz = [&](Z a) { return Z{(a.x * den.x + a.y * den.y) / dd, (a.y * den.x - a.x * den.y) / dd}; };
+            fu = divz(nu);
+            fp1 = divz(np1);
+            fp2 = divz(np2);
+        } else {
+            // rank-deficient bin (DC with coupling 0): the system is diag(d1, d2, d3) there,
+            // whose minimum-norm solution is the pseudo-inverse (kernel_estimator.cpp:213-225)
+            const double dtol = 1e-12 * fmax(fabs(d1), fmax(fabs(d2), fabs(d3)));
+            fu = fabs(d1) > dtol ? rs(1.0 / d1, b1) : Z{0.0, 0.0};
+            fp1 = fabs(d2) > dtol ? rs(1.0 / d2, b2) : Z{0.0, 0.0};
+            fp2 = fabs(d3) > dtol ? rs(1.0 / d3, b3) : Z{0.0, 0.0};
+        }
+        S.spec[2 * i] = fu.x; S.spec[2 * i + 1] = fu.y;
+        S.spec[2 * (m + i)] = fp1.x; S.spec[2 * (m + i) + 1] = fp1.y;
+        S.spec[2 * (2 * m + i)] = fp2.x; S.spec[2 * (2 * m + i) + 1] = fp2.y;
+    }
+    __syncthreads();
+    double* dst[3] = {uout, p1out, p2out};
+    dft3_inverse(S, n, dst);
+}
+
+// deterministic block sum for NTADMM threads
+__device__ __forceinline__ double admm_sum(double v, double* red) { return block_sum<NTADMM>(v, red); }
+
+// Euclidean projection onto the simplex (kernel_estimator.cpp:112-128) by ranks: element i
+// takes the position it would have in a descending sort (ties by index); its cumulative sum
+// and candidate threshold follow; tau comes from the largest-rank qualifying element.
+__device__ int project_simplex_block(const double* v, double* out, int m, double* red, int* ired) {
+    int best_rank = 0;
+    double best_tau = 0.0;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        const double vi = v[i];
+        double css = 0.0;
+        int cnt = 0;
+        for (int k = 0; k < m; ++k) {
+            const double vk = v[k];
+            if (vk > vi || (vk == vi && k <= i)) {
+                css += vk;
+                ++cnt;
+            }
+        }
+        const double cand = (1.0 - css) / static_cast<double>(cnt);
+        if (vi + cand > 0.0 && cnt > best_rank) {
+            best_rank = cnt;
+            best_tau = cand;
+        }
+    }
+    ired[threadIdx.x] = best_rank;
+    red[threadIdx.x] = best_tau;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o && ired[threadIdx.x + o] > ired[threadIdx.x]) {
+            ired[threadIdx.x] = ired[threadIdx.x + o];
+            red[threadIdx.x] = red[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    const int support = ired[0];
+    const double tau = red[0];
+    __syncthreads();
+    if (support > 0)
+        for (int i = threadIdx.x; i < m; i += blockDim.x) out[i] = fmax(v[i] + tau, 0.0);
+    __syncthreads();
+    return support;
+}
+
+size_t admm_smem_doubles(int n) {
+    const int m = n * n;
+    return static_cast<size_t>(17 + 3 + 6 + 6 + 6) * m + 2 * n + 2 * NTADMM + 8;
+}
+
+__global__ void __launch_bounds__(NTADMM) k_admm(AdmmArgs A, const double* __restrict__ Ginv_all,
+                                                 const double* __restrict__ Etf_all, double* __restrict__ state_all,
+                                                 int* __restrict__ info_all, double* __restrict__ k_out) {
+    extern __shared__ double smem[];
+    const int s = blockIdx.x;
+    const int n = A.n, m = A.m;
+    const double* Ginv = Ginv_all + static_cast<size_t>(s) * m * m;
+    const double* Etf = Etf_all + static_cast<size_t>(s) * m;
+    double* gstate = state_all + static_cast<size_t>(s) * 17 * m;
+    int* info = info_all + s * 4;
+    AdmmSmem S;
+    double* p = smem;
+    for (int f = 0; f < 17; ++f) { S.f[f] = p; p += m; }
+    S.bz = p; p += m;
+    S.zz = p; p += m;
+    S.unew = p; p += m;
+    S.tmp6 = p; p += 6 * m;
+    S.spec = p; p += 6 * m;
+    S.rowt = p; p += 6 * m;
+    S.twc = p; p += n;
+    S.tws = p; p += n;
+    S.red = p; p += NTADMM;
+    int* ired = reinterpret_cast<int*>(p);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        const double wv = 2.0 * M_PI * k / n;
+        S.twc[k] = cos(wv);
+        S.tws[k] = sin(wv);
+    }
+    double** F = S.f;
+    if (A.init_state) {  // kernel_estimator.cpp:297-307
+        const int cc = (n - 1) / 2;
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+            const double u0 = A.init_kind == 0 ? (i == cc * n + cc ? 1.0 : 0.0) : 1.0 / (static_cast<double>(n) * n);
+            F[F_U][i] = u0;
+            F[F_Z][i] = u0;
+            for (int f = F_P1; f <= F_L3; ++f)
+                if (f != F_Z) F[f][i] = 0.0;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+            const int r = i / n, c = i - r * n;
+            F[F_X0][i] = F[F_U][r * n + (c + 1) % n] - F[F_U][i];
+            F[F_X1][i] = F[F_U][((r + 1) % n) * n + c] - F[F_U][i];
+        }
+    } else {
+        for (int e = threadIdx.x; e < 17 * m; e += blockDim.x) F[e / m][e % m] = gstate[e];
+    }
+    __syncthreads();
+    const double a1m1 = A.alpha1 * A.mu1, a2m2 = A.alpha2 * A.mu2;
+    const double t1 = 1.0 / A.mu1, t2 = 1.0 / A.mu2;
+    int status = 0, iters = A.t_begin, t = A.t_begin;
+    int phase = A.phase_begin;
+    for (; t < A.t_max; ++t) {
+        if (phase == 0) {
+            // x-step and y-step (kernel_estimator.cpp:325-337), z-step right-hand side (:340)
+            for (int i = threadIdx.x; i < m; i += blockDim.x) {
+                const int r = i / n, c = i - r * n;
+                const int ir = r * n + (c + 1) % n, id = ((r + 1) % n) * n + c;
+                const double* u = F[F_U];
+                const double* p1 = F[F_P1];
+                const double* p2 = F[F_P2];
+                double a0 = ((u[ir] - u[i]) - p1[i]) + F[F_L10][i];
+                double a1 = ((u[id] - u[i]) - p2[i]) + F[F_L11][i];
+                const double nrm = sqrt(a0 * a0 + a1 * a1);
+                const double sc = nrm > t1 ? (nrm - t1) / nrm : 0.0;
+                F[F_X0][i] = a0 * sc;
+                F[F_X1][i] = a1 * sc;
+                const double e0 = p1[ir] - p1[i];
+                const double cr = ((p1[id] - p1[i]) + (p2[ir] - p2[i])) * 0.5;
+                const double e3 = p2[id] - p2[i];
+                const double b0 = e0 + F[F_L20][i], b1 = cr + F[F_L21][i], b2 = cr + F[F_L22][i],
+                             b3 = e3 + F[F_L23][i];
+                const double nrm2 = sqrt(b0 * b0 + b1 * b1 + b2 * b2 + b3 * b3);
+                const double sc2 = nrm2 > t2 ? (nrm2 - t2) / nrm2 : 0.0;
+                F[F_Y0][i] = b0 * sc2;
+                F[F_Y1][i] = b1 * sc2;
+                F[F_Y2][i] = b2 * sc2;
+                F[F_Y3][i] = b3 * sc2;
+                S.bz[i] = Etf[i] + A.mu3 * (u[i] + F[F_L3][i]);
+            }
+            __syncthreads();
+            // z = project_simplex((E^T E + mu3 I)^-1 (E^T f + mu3 (u + L3)))   (:341, :79-83)
+            for (int i = threadIdx.x; i < m; i += blockDim.x) {
+                double a0 = 0.0, a1 = 0.0;
+                int j = 0;
+                for (; j + 1 < m; j += 2) {
+                    a0 = fma(__ldg(Ginv + static_cast<size_t>(j) * m + i), S.bz[j], a0);
+                    a1 = fma(__ldg(Ginv + static_cast<size_t>(j + 1) * m + i), S.bz[j + 1], a1);
+                }
+                if (j < m) a0 = fma(__ldg(Ginv + static_cast<size_t>(j) * m + i), S.bz[j], a0);
+                S.zz[i] = a0 + a1;
+            }
+            __syncthreads();
+            bool finite = true;
+            for (int i = threadIdx.x; i < m; i += blockDim.x) finite = finite && isfinite(S.zz[i]);
+            if (!__syncthreads_and(finite)) { status = 3; iters = t; break; }
+            const int support = project_simplex_block(S.zz, F[F_Z], m, S.red, ired);
+            if (support == 0) { status = 3; iters = t; break; }
+            if (t == A.hook_t) { status = 4; break; }
+        }
+        phase = 0;
+        // {u,p}-step with the mu3 tie to z - L3 (:349-355)
+        for (int i = threadIdx.x; i < m; i += blockDim.x) S.bz[i] = F[F_Z][i] - F[F_L3][i];
+        __syncthreads();
+        double* p1n = S.tmp6 + 5 * m;  // u_new -> S.unew, p1 -> spare, p2 -> zz
+        up_solve(S, n, a1m1, a2m2, A.coupling, F[F_X0], F[F_X1], F[F_Y0], F[F_Y1], F[F_Y2], F[F_Y3], F[F_L10],
+                 F[F_L11], F[F_L20], F[F_L21], F[F_L22], F[F_L23], S.bz, S.unew, p1n, S.zz);
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+            F[F_P1][i] = p1n[i];
+            F[F_P2][i] = S.zz[i];
+        }
+        __syncthreads();
+        // multipliers (:367-373), change of u (:375-376)
+        double dd = 0.0, un = 0.0;
+        bool fin_u = true, fin_z = true;
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+            const int r = i / n, c = i - r * n;
+            const int ir = r * n + (c + 1) % n, id = ((r + 1) % n) * n + c;
+            const double* u1 = S.unew;
+            const double* p1 = F[F_P1];
+            const double* p2 = F[F_P2];
+            F[F_L10][i] += (((u1[ir] - u1[i]) - p1[i]) - F[F_X0][i]) * A.rho;
+            F[F_L11][i] += (((u1[id] - u1[i]) - p2[i]) - F[F_X1][i]) * A.rho;
+            const double e0 = p1[ir] - p1[i];
+            const double cr = ((p1[id] - p1[i]) + (p2[ir] - p2[i])) * 0.5;
+            const double e3 = p2[id] - p2[i];
+            F[F_L20][i] += (e0 - F[F_Y0][i]) * A.rho;
+            F[F_L21][i] += (cr - F[F_Y1][i]) * A.rho;
+            F[F_L22][i] += (cr - F[F_Y2][i]) * A.rho;
+            F[F_L23][i] += (e3 - F[F_Y3][i]) * A.rho;
+            F[F_L3][i] += (u1[i] - F[F_Z][i]) * A.rho;
+            const double du = F[F_U][i] - u1[i];
+            dd += du * du;
+            un += u1[i] * u1[i];
+            fin_u = fin_u && isfinite(u1[i]);
+            fin_z = fin_z && isfinite(F[F_Z][i]);
+        }
+        const double delta = sqrt(admm_sum(dd, S.red));
+        const double scale = fmax(sqrt(admm_sum(un, S.red)), 1e-300);
+        const bool all_u = __syncthreads_and(fin_u);
+        const bool all_z = __syncthreads_and(fin_z);
+        for (int i = threadIdx.x; i < m; i += blockDim.x) F[F_U][i] = S.unew[i];
+        __syncthreads();
+        iters = t + 1;
+        if (!all_u) { status = 1; break; }  // check_finite (:379-380)
+        if (!all_z) { status = 2; break; }
+        if (delta / scale < A.th) { ++t; break; }
+    }
+    for (int e = threadIdx.x; e < 17 * m; e += blockDim.x) gstate[e] = F[e / m][e % m];
+    if (k_out)
+        for (int i = threadIdx.x; i < m; i += blockDim.x) k_out[static_cast<size_t>(s) * m + i] = F[F_Z][i];
+    if (threadIdx.x == 0) {
+        info[0] = iters;
+        info[1] = status;
+        info[2] = t;
+        info[3] = 0;
+    }
+}
+
+// standalone {u,p} solve for the public solve_up (kernel_estimator.cpp:237-241)
+__global__ void __launch_bounds__(NTADMM) k_solve_up(int n, double a1m1, double a2m2, double coupling,
+                                                     const double* __restrict__ fields, const double* __restrict__ anchor,
+                                                     double* __restrict__ u, double* __restrict__ p1,
+                                                     double* __restrict__ p2) {
+    extern __shared__ double smem[];
+    const int m = n * n;
+    AdmmSmem S;
+    double* p = smem;
+    double* fl[12];
+    for (int f = 0; f < 12; ++f) { fl[f] = p; p += m; }
+    double* anc = p; p += m;
+    double* uo = p; p += m;
+    double* p1o = p; p += m;
+    double* p2o = p; p += m;
+    S.tmp6 = p; p += 6 * m;
+    S.spec = p; p += 6 * m;
+    S.rowt = p; p += 6 * m;
+    S.twc = p; p += n;
+    S.tws = p; p += n;
+    S.red = p; p += NTADMM;
+    for (int e = threadIdx.x; e < 12 * m; e += blockDim.x) fl[e / m][e % m] = fields[e];
+    for (int i = threadIdx.x; i < m; i += blockDim.x) anc[i] = anchor ? anchor[i] : 0.0;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        const double wv = 2.0 * M_PI * k / n;
+        S.twc[k] = cos(wv);
+        S.tws[k] = sin(wv);
+    }
+    __syncthreads();
+    up_solve(S, n, a1m1, a2m2, coupling, fl[0], fl[1], fl[2], fl[3], fl[4], fl[5], fl[6], fl[7], fl[8], fl[9], fl[10],
+             fl[11], anchor ? anc : nullptr, uo, p1o, p2o);
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        u[i] = uo[i];
+        p1[i] = p1o[i];
+        p2[i] = p2o[i];
+    }
+}
+
+__global__ void k_shrink2(double* __restrict__ cols, int ncols, long long m, double t) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < m;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        double n2 = 0.0;
+        for (int j = 0; j < ncols; ++j) n2 += cols[j * m + i] * cols[j * m + i];
+        const double nrm = sqrt(n2);
+        const double sc = nrm > t ? (nrm - t) / nrm : 0.0;
+        for (int j = 0; j < ncols; ++j) cols[j * m + i] *= sc;
+    }
+}
+
+__global__ void __launch_bounds__(NTADMM) k_project(const double* __restrict__ v, int m, double* __restrict__ out,
+                                                    int* __restrict__ status) {
+    extern __shared__ double sh[];
+    double* vs = sh;
+    double* os = sh + m;
+    double* red = os + m;
+    int* ired = reinterpret_cast<int*>(red + NTADMM);
+    for (int i = threadIdx.x; i < m; i += blockDim.x) vs[i] = v[i];
+    __syncthreads();
+    const int support = project_simplex_block(vs, os, m, red, ired);
+    if (threadIdx.x == 0) *status = support == 0;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) out[i] = os[i];
+}
+
+}  // namespace
+
+// =============================================================================================
+// host wrappers
+// =============================================================================================
+void validate_ke(const fbmp_ke_params& p) {  // kernel_estimator.cpp:36-45
+    if (p.n < 1 || p.n % 2 == 0) param_error("kernel estimation: n must be odd and positive");
+    if (p.alpha1 <= 0 || p.alpha2 <= 0) param_error("kernel estimation: alpha weights must be positive");
+    if (p.mu1 <= 0 || p.mu2 <= 0 || p.mu3 <= 0) param_error("kernel estimation: mu penalties must be positive");
+    const double rho_max = (1.0 + std::sqrt(5.0)) / 2.0;
+    if (!(p.rho > 0 && p.rho < rho_max)) param_error("kernel estimation: rho must lie in (0, (1+sqrt(5))/2)");
+    if (!(p.th > 0)) param_error("kernel estimation: th must be positive");
+    if (p.t_max < 1) param_error("kernel estimation: t_max must be >= 1");
+}
+
+void solve_weights_device(Context& ctx, const double* d_lrms, int S, int nb, int h, int w, const double* d_pan, int l,
+                          double lambda_omega, int c, double* d_omega, int* d_status) {
+    const int H = h * c, W = w * c;
+    const long long p = static_cast<long long>(h) * w;
+    double* t1 = ctx.scratch<double>("sw_t1", static_cast<size_t>(S) * H * w);
+    double* bvec = ctx.scratch<double>("sw_b", static_cast<size_t>(S) * p);
+    double* t2 = ctx.scratch<double>("sw_t2", static_cast<size_t>(S) * nb * p);
+    double* A = ctx.scratch<double>("sw_A", static_cast<size_t>(S) * nb * p);
+    const int hwin = c * l + 1, lwin = l + 1;
+    k_blur_h<<<grid1d(ctx, static_cast<long long>(S) * H * w), 256, 0, ctx.stream>>>(d_pan, S, H, W, w, c, hwin, t1);
+    k_blur_v<<<grid1d(ctx, static_cast<long long>(S) * p), 256, 0, ctx.stream>>>(t1, S, H, w, h, c, hwin, bvec);
+    k_blur_h<<<grid1d(ctx, static_cast<long long>(S) * nb * p), 256, 0, ctx.stream>>>(d_lrms, S * nb, h, w, w, 1, lwin, t2);
+    k_blur_v<<<grid1d(ctx, static_cast<long long>(S) * nb * p), 256, 0, ctx.stream>>>(t2, S * nb, h, w, h, 1, lwin, A);
+    const int nblk = static_cast<int>(std::max(1LL, std::min<long long>(64, (p + 4095) / 4096)));
+    const int nv = nb * (nb + 1) / 2 + nb;
+    double* part = ctx.scratch<double>("sw_part", static_cast<size_t>(S) * nblk * nv);
+    k_sw_dots<<<dim3(nblk, S), NT, 0, ctx.stream>>>(A, bvec, nb, p, nblk, part);
+    const size_t sm = (nv + 3 * nb * nb + 4 * nb + nb) * sizeof(double) + 64;
+    k_sw_solve<<<S, 64, sm, ctx.stream>>>(part, nb, nblk, lambda_omega, d_omega, d_status);
+    ctx.count(6);
+    check_launch();
+}
+
+void combine_bands_device(Context& ctx, const double* d_lrms, int S, int nb, long long p, const double* d_omega,
+                          double* d_out) {
+    k_combine<<<grid1d(ctx, S * p), 256, 0, ctx.stream>>>(d_lrms, S, nb, p, d_omega, d_out);
+    ctx.count();
+    check_launch();
+}
+
+void pan_stats(Context& ctx, const double* d_pan, int S, long long P, double* d_stats) {
+    const int nblk = static_cast<int>(std::max(1LL, std::min<long long>(256, (P + 8191) / 8192)));
+    double* part = ctx.scratch<double>("stats_part", static_cast<size_t>(S) * nblk * 4);
+    k_stats_partial<<<dim3(nblk, S), NT, 0, ctx.stream>>>(d_pan, P, nblk, part);
+    k_stats_final<<<S, 32, 0, ctx.stream>>>(part, nblk, d_stats);
+    ctx.count(2);
+    check_launch();
+}
+
+static void gram_T_and_etf(Context& ctx, const double* d_pan, const double* d_obs, int S, int H, int W, int c, int n,
+                           const double* d_scale, double* T, double* Etf) {
+    const int h = H / c, w = W / c;
+    const int ntiles = ceil_div(h, TG) * ceil_div(w, TG);
+    const int D = 2 * n - 1, nd = D * D, n2 = n * n;
+    const int SR = c * (TG - 1) + 2 * (n - 1) + 1;
+    const size_t smT = static_cast<size_t>(SR) * SR * sizeof(double);
+    if (smT > 227 * 1024) param_error("build_observation: kernel side too large for the device Gram kernel");
+    set_smem(k_gram_T, smT);
+    double* partT = ctx.scratch<double>("gram_partT", static_cast<size_t>(S) * ntiles * c * c * nd);
+    k_gram_T<<<dim3(ntiles, c * c, S), NT, smT, ctx.stream>>>(d_pan, d_scale, H, W, h, w, c, n, partT, ntiles);
+    k_reduce_tiles<<<grid1d(ctx, static_cast<long long>(S) * c * c * nd), 256, 0, ctx.stream>>>(partT, S, ntiles,
+                                                                                                c * c * nd, T);
+    const int SRf = c * (TG - 1) + n;
+    const size_t smF = (static_cast<size_t>((SRf * SRf + 1) & ~1) + TG * TG) * sizeof(double);
+    set_smem(k_gram_etf, smF);
+    double* partF = ctx.scratch<double>("gram_partF", static_cast<size_t>(S) * ntiles * n2);
+    k_gram_etf<<<dim3(ntiles, 1, S), NT, smF, ctx.stream>>>(d_pan, d_obs, d_scale, H, W, h, w, c, n, partF, ntiles);
+    k_reduce_tiles<<<grid1d(ctx, static_cast<long long>(S) * n2), 256, 0, ctx.stream>>>(partF, S, ntiles, n2, Etf);
+    ctx.count(4);
+    check_launch();
+}
+
+void gram_device(Context& ctx, const double* d_pan, const double* d_obs, int H, int W, int c, int n, double* d_EtE,
+                 double* d_Etf) {
+    const int D = 2 * n - 1;
+    double* T = ctx.scratch<double>("gram_T", static_cast<size_t>(c) * c * D * D);
+    gram_T_and_etf(ctx, d_pan, d_obs, 1, H, W, c, n, nullptr, T, d_Etf);
+    const long long n2 = static_cast<long long>(n) * n;
+    k_gram_expand<<<grid1d(ctx, n2 * n2), 256, 0, ctx.stream>>>(T, 1, c, n, 0.0, d_EtE);
+    ctx.count();
+    check_launch();
+}
+
+void build_observation(Context& ctx, const double* d_pan, const double* d_obs, int S, int H, int W, int c, int n,
+                       double mu3, const double* d_scale, ObsSystem& sys, bool want_inverse) {
+    const int n2 = n * n, D = 2 * n - 1;
+    sys.S = S;
+    sys.n = n;
+    sys.n2 = n2;
+    const size_t NN = static_cast<size_t>(n2) * n2;
+    sys.M = ctx.scratch<double>("obs_M", S * NN);
+    sys.Etf = ctx.scratch<double>("obs_Etf", static_cast<size_t>(S) * n2);
+    sys.Ginv = ctx.scratch<double>("obs_Ginv", S * NN);
+    sys.g = nullptr;
+    sys.status = ctx.scratch<int>("obs_status", S);
+    double* T = ctx.scratch<double>("gram_T", static_cast<size_t>(S) * c * c * D * D);
+    gram_T_and_etf(ctx, d_pan, d_obs, S, H, W, c, n, d_scale, T, sys.Etf);
+    k_gram_expand<<<grid1d(ctx, static_cast<long long>(S) * NN), 256, 0, ctx.stream>>>(T, S, c, n, mu3, sys.M);
+    ctx.count();
+    FBMP_CUDA(cudaMemsetAsync(sys.status, 0, sizeof(int) * S, ctx.stream));
+    const int N = n2;
+    const size_t smP = static_cast<size_t>(N) * NBK * sizeof(double);
+    if (smP > 227 * 1024) param_error("build_observation: kernel side too large for the device Cholesky");
+    set_smem(k_potrf_panel, smP);
+    for (int K = 0; K < N; K += NBK) {
+        k_potrf_panel<<<S, NT, smP, ctx.stream>>>(sys.M, N, K, sys.status);
+        ctx.count();
+        if (K + NBK < N) {
+            const int nt = ceil_div(N - K - NBK, NBK);
+            k_syrk<<<dim3(nt * (nt + 1) / 2, S), NT, 0, ctx.stream>>>(sys.M, N, K, sys.status);
+            ctx.count();
+        }
+    }
+    check_launch();
+    if (!want_inverse) return;
+    double* Linv = ctx.scratch<double>("obs_Linv", S * NN);
+    const size_t smT = static_cast<size_t>(NT / 32) * N * sizeof(double);
+    set_smem(k_trtri, smT);
+    k_trtri<<<dim3(ceil_div(N, NT / 32), S), NT, smT, ctx.stream>>>(sys.M, N, Linv, sys.status);
+    const int nt = ceil_div(N, NBK);
+    k_inv_gram<<<dim3(nt * (nt + 1) / 2, S), NT, 0, ctx.stream>>>(Linv, N, sys.Ginv, sys.status);
+    ctx.count(2);
+    check_launch();
+}
+
+void admm_device(Context& ctx, const ObsSystem& sys, const fbmp_ke_params& prm, double* d_state, bool init_state,
+                 int t_begin, int phase_begin, int hook_t, int* d_info, double* d_k) {
+    AdmmArgs A;
+    A.n = sys.n;
+    A.m = sys.n2;
+    A.alpha1 = prm.alpha1;
+    A.alpha2 = prm.alpha2;
+    A.mu1 = prm.mu1;
+    A.mu2 = prm.mu2;
+    A.mu3 = prm.mu3;
+    A.rho = prm.rho;
+    A.th = prm.th;
+    A.coupling = prm.mu3;
+    A.t_max = prm.t_max;
+    A.t_begin = t_begin;
+    A.phase_begin = phase_begin;
+    A.hook_t = hook_t;
+    A.init_kind = prm.init;
+    A.init_state = init_state ? 1 : 0;
+    const size_t sm = admm_smem_doubles(sys.n) * sizeof(double);
+    if (sm > 227 * 1024) param_error("kernel estimation: kernel side too large for the device ADMM (n <= 25)");
+    set_smem(k_admm, sm);
+    k_admm<<<sys.S, NTADMM, sm, ctx.stream>>>(A, sys.Ginv, sys.Etf, d_state, d_info, d_k);
+    ctx.count();
+    check_launch();
+}
+
+void admm_device(Context& ctx, const ObsSystem& sys, const fbmp_ke_params& prm, double* d_state, bool init_state,
+                 int t_begin, int phase_begin, int hook_t, int* d_info) {
+    admm_device(ctx, sys, prm, d_state, init_state, t_begin, phase_begin, hook_t, d_info, nullptr);
+}
+
+void solve_up_device(Context& ctx, const double* d_fields, int n, const fbmp_ke_params& prm, double coupling,
+                     const double* d_anchor, double* d_u, double* d_p1, double* d_p2) {
+    const int m = n * n;
+    const size_t sm = (static_cast<size_t>(12 + 4 + 18) * m + 2 * n + NTADMM + 8) * sizeof(double);
+    if (sm > 227 * 1024) param_error("solve_up: field size too large for the device solver");
+    set_smem(k_solve_up, sm);
+    k_solve_up<<<1, NTADMM, sm, ctx.stream>>>(n, prm.alpha1 * prm.mu1, prm.alpha2 * prm.mu2, coupling, d_fields,
+                                             d_anchor, d_u, d_p1, d_p2);
+    ctx.count();
+    check_launch();
+}
+
+void shrink2_device(Context& ctx, double* d_cols, int ncols, long long m, double t) {
+    k_shrink2<<<grid1d(ctx, m), 256, 0, ctx.stream>>>(d_cols, ncols, m, t);
+    ctx.count();
+    check_launch();
+}
+
+void project_simplex_device(Context& ctx, const double* d_v, int m, double* d_out, int* d_status) {
+    const size_t sm = (2 * static_cast<size_t>(m) + 2 * NTADMM) * sizeof(double);
+    if (sm > 227 * 1024) param_error("project_simplex: vector too long for the device projection");
+    set_smem(k_project, sm);
+    k_project<<<1, NTADMM, sm, ctx.stream>>>(d_v, m, d_out, d_status);
+    ctx.count();
+    check_launch();
+}
+
+void estimate_kernel_device(Context& ctx, const double* d_pan, const double* d_obs, int S, int H, int W, int c,
+                            const fbmp_ke_params& prm, double* d_k, std::vector<int>& iters, double* d_state_out,
+                            int hook_t) {
+    validate_ke(prm);
+    const int n = prm.n;
+    if (c < 1) param_error("build_observation: factor must be >= 1");
+    if (H % c || W % c) dim_error("build_observation: PAN dimensions must be factor times the observation");
+    if (n > std::min(H, W)) dim_error("build_observation: kernel larger than PAN image");
+    const long long P = static_cast<long long>(H) * W;
+    double* stats = ctx.scratch<double>("ke_stats", static_cast<size_t>(S) * 4);
+    pan_stats(ctx, d_pan, S, P, stats);
+    std::vector<double> hs(static_cast<size_t>(S) * 4);
+    d2h(hs.data(), stats, hs.size() * sizeof(double), ctx.stream);
+    FBMP_CUDA(cudaStreamSynchronize(ctx.stream));
+    std::vector<double> scale(S);
+    for (int s = 0; s < S; ++s) {  // kernel_estimator.cpp:269-289
+        const double mean = hs[s * 4] / static_cast<double>(P);
+        const double dev = std::max(hs[s * 4 + 2] - mean, mean - hs[s * 4 + 1]);
+        if (dev <= 1e-12 * std::max(1.0, std::abs(mean)))
+            num_error("kernel estimation: constant PAN image is unidentifiable (E^T E has rank 1)");
+        const double m = hs[s * 4 + 3];
+        if (m <= 0.0) num_error("kernel estimation: PAN image is identically zero");
+        const double hw = static_cast<double>(H / c) * (W / c);
+        scale[s] = std::sqrt(16384.0 / hw) / m;
+    }
+    double* d_scale = ctx.scratch<double>("ke_scale", S);
+    h2d(d_scale, scale.data(), S * sizeof(double), ctx.stream);
+    ObsSystem sys;
+    build_observation(ctx, d_pan, d_obs, S, H, W, c, n, prm.mu3, d_scale, sys, true);
+    const int m = n * n;
+    double* state = d_state_out ? d_state_out : ctx.scratch<double>("ke_state", static_cast<size_t>(S) * 17 * m);
+    int* info = ctx.scratch<int>("ke_info", static_cast<size_t>(S) * 4);
+    admm_device(ctx, sys, prm, state, true, 0, 0, hook_t, info, d_k);
+    std::vector<int> hinfo(static_cast<size_t>(S) * 4), hst(S);
+    d2h(hinfo.data(), info, hinfo.size() * sizeof(int), ctx.stream);
+    d2h(hst.data(), sys.status, S * sizeof(int), ctx.stream);
+    FBMP_CUDA(cudaStreamSynchronize(ctx.stream));
+    iters.assign(S, 0);
+    for (int s = 0; s < S; ++s) {
+        if (hst[s]) num_error("build_observation: factorization of E^T E + mu3 I failed");
+        iters[s] = hinfo[s * 4];
+        const int st = hinfo[s * 4 + 1];
+        const std::string it = std::to_string(hinfo[s * 4]);
+        if (st == 1) num_error("kernel estimation diverged: non-finite u at iteration " + it);
+        if (st == 2) num_error("kernel estimation diverged: non-finite z at iteration " + it);
+        if (st == 3) num_error("project_simplex: empty support (non-finite input?)");
+    }
+}
+
+}  // namespace fbmp_gpu

@@ -1,0 +1,1062 @@
+// pansharpen.cu -- sm_100a kernels of Algorithm 2 (per-channel HRMS estimation under the
+// local Laplacian prior), reference /root/reference/proj/src/pansharpen.cpp.
+//
+// Hot loop (pansharpen.cpp:237-256) per CG iteration, all channels of a scene batched in
+// grid.y, three kernels, scalars resident on the device:
+//   K_Q  p <- r + beta p (fused on load), q = D B p at the LR points          (north-star b)
+//   K_A  Ap = B^T U q + lambda L M L p, matrix-free matting operator          (north-star a)
+//   K_U  z += alpha p, r -= alpha Ap, ||r||^2, ||z||^2, stop test             (north-star c)
+// Reductions are deterministic: fixed per-block trees, per-block partials, and a fixed-order
+// final sum in the last block to finish (threadfence reduction); no floating-point atomics.
+#include <cmath>
+
+#include "pansharpen.cuh"
+
+namespace fbmp_gpu {
+
+PsGeo make_geo(int N, int h, int w, int c, int n, int rw, double lambda, double eps, int cps) {
+    PsGeo G;
+    G.N = N;
+    G.cps = cps > 0 ? cps : N;
+    G.h = h; G.w = w; G.c = c;
+    G.H = h * c; G.W = w * c;
+    G.n = n; G.C = (n - 1) / 2;
+    G.g = (G.C + c - 1) / c;
+    G.rw = rw;
+    G.lambda = lambda;
+    G.eps = eps;
+    return G;
+}
+
+namespace {
+
+constexpr int TQ = 16;            // K_Q LR tile side
+constexpr int NTQ = TQ * TQ;      // threads per K_Q block
+constexpr int TA = 32;            // K_A / K_GF HR tile side
+constexpr int NTA = 256;          // threads per K_A block
+constexpr int NTU = 256;          // threads per K_U block
+constexpr int UPT = 8;            // elements per thread in K_U
+
+__host__ __device__ inline int plane_stride(int pw) {  // >= pw*pw and == 4 (mod 16)
+    const int s = pw * pw;
+    return s + ((4 - s % 16) + 16) % 16;
+}
+
+// ------------------------------------------------------------------------------------------
+// K_Q: q = D B p at the LR points of a TQ x TQ LR tile (+ fused p update in CG mode).
+// The HR region (tile footprint + halo c*g >= C) is staged in shared memory split into
+// c x c sampling phases so that lanes reading consecutive LR columns hit consecutive words.
+// ------------------------------------------------------------------------------------------
+template <bool CG>
+__global__ void __launch_bounds__(NTQ) k_q(PsGeo G, const double* __restrict__ taps, const double* __restrict__ src,
+                                           double* __restrict__ pbuf, double* __restrict__ q, CgState* st,
+                                           double* __restrict__ part, int nblk) {
+    __shared__ double red[NTQ / 32 + 1];
+    extern __shared__ double sm[];
+    const int ch = blockIdx.y;
+    int t = 0;
+    double beta = 0.0;
+    if (CG) {
+        if (st[ch].done) return;
+        t = st[ch].t;
+        beta = t ? st[ch].beta : 0.0;
+    }
+    const int c = G.c, n = G.n, C = G.C, g = G.g;
+    const size_t P = static_cast<size_t>(G.H) * G.W;
+    const double* rc = src + ch * P;
+    const double* pold = CG ? pbuf + (static_cast<size_t>((t + 1) & 1) * G.N + ch) * P : nullptr;
+    double* pnew = CG ? pbuf + (static_cast<size_t>(t & 1) * G.N + ch) * P : nullptr;
+
+    const int ntx = (G.w + TQ - 1) / TQ;
+    const int tyb = blockIdx.x / ntx, txb = blockIdx.x - tyb * ntx;
+    const int i0 = tyb * TQ, j0 = txb * TQ;
+    const int PW = TQ + 2 * g, PS = plane_stride(PW), SR = c * PW;
+    double* sk = sm;
+    double* planes = sm + ((n * n + 1) & ~1);
+    const double* tp = taps + static_cast<size_t>(ch / G.cps) * n * n;
+    for (int e = threadIdx.x; e < n * n; e += NTQ) sk[e] = tp[e];
+
+    const int R0 = c * (i0 - g), C0 = c * (j0 - g);
+    double pp = 0.0;
+    for (int e = threadIdx.x; e < SR * SR; e += NTQ) {
+        const int rr = e / SR, cc = e - rr * SR;
+        const int R = wrapi(R0 + rr, G.H), Cc = wrapi(C0 + cc, G.W);
+        const size_t gi = static_cast<size_t>(R) * G.W + Cc;
+        double v = __ldg(rc + gi);
+        if (CG) {
+            v = v + __ldg(pold + gi) * beta;  // pansharpen.cpp:254  p = r + p * beta
+            const int orr = rr - c * g, occ = cc - c * g;
+            if (orr >= 0 && orr < c * TQ && occ >= 0 && occ < c * TQ && R0 + rr < G.H && C0 + cc < G.W) {
+                pnew[gi] = v;
+                pp += v * v;
+            }
+        }
+        planes[((rr % c) * c + (cc % c)) * PS + (rr / c) * PW + cc / c] = v;
+    }
+    __syncthreads();
+
+    const int ti = threadIdx.x / TQ, tj = threadIdx.x - ti * TQ;
+    const int i = i0 + ti, j = j0 + tj;
+    if (i < G.h && j < G.w) {
+        double acc = 0.0;
+        for (int a = -C; a <= C; ++a) {  // (B p)(ci,cj) = sum_ab k[a+C][b+C] p(ci-a, cj-b)
+            const int rr = c * (ti + g) - a;
+            const double* base = planes + (rr % c) * c * PS + (rr / c) * PW;
+            const double* krow = sk + (a + C) * n;
+            const int cc0 = c * (tj + g) - C;
+            int pc = cc0 % c, J = cc0 / c;
+            for (int b = C; b >= -C; --b) {
+                acc = fma(krow[b + C], base[pc * PS + J], acc);
+                if (++pc == c) { pc = 0; ++J; }
+            }
+        }
+        q[static_cast<size_t>(ch) * G.h * G.w + static_cast<size_t>(i) * G.w + j] = acc;
+    }
+    if (CG) {
+        const double bs = block_sum<NTQ>(pp, red);
+        if (threadIdx.x == 0) part[static_cast<size_t>(ch) * nblk + blockIdx.x] = bs;
+        if (elect_last_block(&st[ch].cnt_q, nblk)) {
+            const double tot = sum_partials<NTQ>(part + static_cast<size_t>(ch) * nblk, nblk, 1, red);
+            if (threadIdx.x == 0) {
+                st[ch].pp = tot;
+                st[ch].cnt_q = 0;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// K_A: out = B^T U q (+) lambda * L M L p on a TA x TA HR tile.
+// MODE 0: full CG operator (pansharpen.cpp:218-223); 1: M p only (:197-202); 2: data term only.
+// The matting operator is applied matrix-free (pansharpen.cpp:155-164 regrouped per window):
+//   (M s)_m = sum_{interior k with m in w_k} [ s_m - mean_k(s) - (I_m - mu_k) a_k ],
+//   a_k = mean_k((I - mu_k) s) / (eps/|w| + var_k),
+// with mu_k, var_k recomputed in-tile from the guide I (no per-scene maps are read).
+// ------------------------------------------------------------------------------------------
+struct ApplyLayout {
+    int hp, hI, hs, hwin, hM;  // halos of p, I, s, window stats, M s
+    int iq0, jq0, QH, QW;      // LR q window
+    int off_q, off_p, off_I, off_s, off_x, off_a, off_mu, off_w, off_M, total;
+};
+
+__host__ __device__ inline ApplyLayout apply_layout(const PsGeo& G, int mode, int r0, int c0) {
+    ApplyLayout L{};
+    const int rw = G.rw;
+    const int e = mode == 0 ? 1 : 0;
+    L.hM = e;
+    L.hwin = rw + e;
+    L.hs = 2 * rw + e;
+    L.hI = 2 * rw + e;
+    L.hp = mode == 2 ? 0 : L.hs + e;
+    const int c = G.c, C = G.C;
+    // LR rows whose c-multiple lies within C of the tile rows
+    auto fdiv = [](int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); };
+    L.iq0 = fdiv(r0 - C + c - 1, c);
+    L.jq0 = fdiv(c0 - C + c - 1, c);
+    L.QH = fdiv(r0 + TA - 1 + C, c) - L.iq0 + 1;
+    L.QW = fdiv(c0 + TA - 1 + C, c) - L.jq0 + 1;
+    int o = 0;
+    auto take = [&](int cnt) { const int at = o; o += (cnt + 1) & ~1; return at; };
+    const int n2 = G.n * G.n;
+    const int dq = (TA - 1 + 2 * C) / c + 2;  // upper bound of QH / QW for any tile origin
+    take(n2);  // taps at offset 0
+    L.off_q = take(dq * dq);
+    if (mode != 2) {
+        const int sp = TA + 2 * L.hp, sI = TA + 2 * L.hI, ss = TA + 2 * L.hs, sw = TA + 2 * L.hwin,
+                  sM = TA + 2 * L.hM;
+        L.off_p = take(sp * sp);
+        L.off_I = take(sI * sI);
+        L.off_s = mode == 0 ? take(ss * ss) : L.off_p;
+        L.off_x = take(sw * sw);
+        L.off_a = take(sw * sw);
+        L.off_mu = take(sw * sw);
+        L.off_w = take(sw * sw);
+        L.off_M = take(sM * sM);
+    }
+    L.total = o;
+    return L;
+}
+
+template <int MODE, bool CG>
+__global__ void __launch_bounds__(NTA) k_apply(PsGeo G, const double* __restrict__ taps,
+                                               const double* __restrict__ guide, const double* __restrict__ pin,
+                                               const double* __restrict__ q, double* __restrict__ out, CgState* st,
+                                               double* __restrict__ part, int nblk) {
+    __shared__ double red[NTA / 32 + 1];
+    extern __shared__ double sm[];
+    const int ch = blockIdx.y;
+    const size_t P = static_cast<size_t>(G.H) * G.W;
+    const double* p = pin + ch * P;
+    int t = 0;
+    if (CG) {
+        if (st[ch].done) return;
+        t = st[ch].t;
+        p = pin + (static_cast<size_t>(t & 1) * G.N + ch) * P;
+    }
+    const int ntx = (G.W + TA - 1) / TA;
+    const int by = blockIdx.x / ntx, bx = blockIdx.x - by * ntx;
+    const int r0 = by * TA, c0 = bx * TA;
+    const ApplyLayout L = apply_layout(G, MODE, r0, c0);
+    const int H = G.H, W = G.W, c = G.c, n = G.n, C = G.C, rw = G.rw;
+    double* sk = sm;
+    double* sq = sm + L.off_q;
+    const double* tp = taps + static_cast<size_t>(ch / G.cps) * n * n;
+    if (guide) guide += static_cast<size_t>(ch / G.cps) * P;
+    for (int e = threadIdx.x; e < n * n; e += NTA) sk[e] = tp[e];
+    if (MODE != 1) {
+        const double* qc = q + static_cast<size_t>(ch) * G.h * G.w;
+        for (int e = threadIdx.x; e < L.QH * L.QW; e += NTA) {
+            const int a = e / L.QW, b = e - a * L.QW;
+            sq[e] = __ldg(qc + static_cast<size_t>(wrapi(L.iq0 + a, G.h)) * G.w + wrapi(L.jq0 + b, G.w));
+        }
+    }
+    const int SPW = TA + 2 * L.hp, SIW = TA + 2 * L.hI, SSW = TA + 2 * L.hs, SWW = TA + 2 * L.hwin,
+              SMW = TA + 2 * L.hM;
+    double *sp = sm + L.off_p, *sI = sm + L.off_I, *ss = sm + L.off_s;
+    double *sx = sm + L.off_x, *sa = sm + L.off_a, *smu = sm + L.off_mu, *swt = sm + L.off_w, *sM = sm + L.off_M;
+    if (MODE != 2) {
+        for (int e = threadIdx.x; e < SPW * SPW; e += NTA) {
+            const int y = e / SPW, x = e - y * SPW;
+            sp[e] = __ldg(p + static_cast<size_t>(wrapi(r0 - L.hp + y, H)) * W + wrapi(c0 - L.hp + x, W));
+        }
+        for (int e = threadIdx.x; e < SIW * SIW; e += NTA) {
+            const int y = e / SIW, x = e - y * SIW;
+            sI[e] = __ldg(guide + static_cast<size_t>(wrapi(r0 - L.hI + y, H)) * W + wrapi(c0 - L.hI + x, W));
+        }
+        __syncthreads();
+        if (MODE == 0) {  // s = L p on R + hs (ops.cpp:70-78 stencil order)
+            for (int e = threadIdx.x; e < SSW * SSW; e += NTA) {
+                const int y = e / SSW + 1, x = e % SSW + 1;
+                ss[e] = 4.0 * sp[y * SPW + x] - sp[(y - 1) * SPW + x] - sp[(y + 1) * SPW + x] - sp[y * SPW + x - 1] -
+                        sp[y * SPW + x + 1];
+            }
+            __syncthreads();
+        }
+        // per-window statistics on R + hwin
+        const double ws = static_cast<double>((2 * rw + 1) * (2 * rw + 1));
+        const int oI = L.hI - L.hwin, oS = L.hs - L.hwin;
+        for (int e = threadIdx.x; e < SWW * SWW; e += NTA) {
+            const int y = e / SWW, x = e - y * SWW;
+            const int gr = wrapi(r0 - L.hwin + y, H), gc = wrapi(c0 - L.hwin + x, W);
+            double xb = 0.0, a = 0.0, mu = 0.0, wt = 0.0;
+            if (gr >= rw && gr < H - rw && gc >= rw && gc < W - rw) {  // interior centre (:152-153)
+                double s1 = 0.0, s2 = 0.0, sx_ = 0.0;
+                for (int dy = -rw; dy <= rw; ++dy)
+                    for (int dx = -rw; dx <= rw; ++dx) {
+                        const double iv = sI[(y + oI + dy) * SIW + x + oI + dx];
+                        s1 += iv;
+                        s2 += iv * iv;
+                        sx_ += ss[(y + oS + dy) * SSW + x + oS + dx];
+                    }
+                mu = s1 / ws;
+                const double var = s2 / ws - mu * mu;
+                const double den = G.eps / ws + var;  // pansharpen.cpp:155
+                double sc = 0.0;
+                for (int dy = -rw; dy <= rw; ++dy)
+                    for (int dx = -rw; dx <= rw; ++dx)
+                        sc += (sI[(y + oI + dy) * SIW + x + oI + dx] - mu) * ss[(y + oS + dy) * SSW + x + oS + dx];
+                xb = sx_ / ws;
+                a = (sc / ws) / den;
+                wt = 1.0;
+            }
+            sx[e] = xb;
+            sa[e] = a;
+            smu[e] = mu;
+            swt[e] = wt;
+        }
+        __syncthreads();
+        // M s on R + hM
+        const int oW = L.hwin - L.hM, oSM = L.hs - L.hM, oIM = L.hI - L.hM;
+        for (int e = threadIdx.x; e < SMW * SMW; e += NTA) {
+            const int y = e / SMW, x = e - y * SMW;
+            const double sv = ss[(y + oSM) * SSW + x + oSM];
+            const double iv = sI[(y + oIM) * SIW + x + oIM];
+            double acc = 0.0;
+            for (int dy = -rw; dy <= rw; ++dy)
+                for (int dx = -rw; dx <= rw; ++dx) {
+                    const int k = (y + oW + dy) * SWW + x + oW + dx;
+                    acc += swt[k] * sv - sx[k] - (iv - smu[k]) * sa[k];
+                }
+            sM[e] = acc;
+        }
+    }
+    __syncthreads();
+
+    double* oc = out + ch * P;
+    double dotp = 0.0;
+    const int tx = threadIdx.x & 31, ty0 = threadIdx.x >> 5;
+    for (int ty = ty0; ty < TA; ty += NTA / 32) {
+        const int R = r0 + ty, Cc = c0 + tx;
+        if (R >= H || Cc >= W) continue;
+        double val = 0.0;
+        if (MODE != 1) {  // data term: sum over LR points within C of (R, Cc)
+            const int ilo = floordiv(R - C + c - 1, c), ihi = floordiv(R + C, c);
+            const int jlo = floordiv(Cc - C + c - 1, c), jhi = floordiv(Cc + C, c);
+            double acc = 0.0;
+            for (int i = ilo; i <= ihi; ++i) {
+                const double* krow = sk + (c * i - R + C) * n + C - Cc;
+                const double* qrow = sq + (i - L.iq0) * L.QW - L.jq0;
+                for (int j = jlo; j <= jhi; ++j) acc = fma(krow[c * j], qrow[j], acc);
+            }
+            val = acc;
+        }
+        if (MODE == 0) {
+            const int y = ty + 1, x = tx + 1;
+            const double tl = 4.0 * sM[y * SMW + x] - sM[(y - 1) * SMW + x] - sM[(y + 1) * SMW + x] -
+                              sM[y * SMW + x - 1] - sM[y * SMW + x + 1];
+            val = val + tl * G.lambda;
+        } else if (MODE == 1) {
+            val = sM[ty * SMW + tx];
+        }
+        oc[static_cast<size_t>(R) * W + Cc] = val;
+        if (CG) dotp += sp[(ty + L.hp) * SPW + tx + L.hp] * val;
+    }
+    if (CG) {
+        const double bs = block_sum<NTA>(dotp, red);
+        if (threadIdx.x == 0) part[static_cast<size_t>(ch) * nblk + blockIdx.x] = bs;
+        if (elect_last_block(&st[ch].cnt_a, nblk)) {
+            const double pAp = sum_partials<NTA>(part + static_cast<size_t>(ch) * nblk, nblk, 1, red);
+            if (threadIdx.x == 0) {
+                CgState& S = st[ch];
+                S.pAp = pAp;
+                if (!(pAp > 0)) {  // pansharpen.cpp:240-244
+                    S.done = (sqrt(S.rs) <= 1e-12 * S.rhs_norm) ? 1 : 2;
+                    S.iters = S.t + 1;
+                } else {
+                    S.alpha = S.rs / pAp;
+                }
+                S.cnt_a = 0;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// K_U: z += alpha p, r -= alpha Ap, ||r||^2, ||z||^2 and the relative-step stop test
+// (pansharpen.cpp:245-255).
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(NTU) k_update(PsGeo G, double* __restrict__ z, double* __restrict__ r,
+                                                const double* __restrict__ pbuf, const double* __restrict__ Ap,
+                                                CgState* st, double* __restrict__ part, int nblk) {
+    __shared__ double red[NTU / 32 + 1];
+    const int ch = blockIdx.y;
+    if (st[ch].done) return;
+    const int t = st[ch].t;
+    const double alpha = st[ch].alpha;
+    const size_t P = static_cast<size_t>(G.H) * G.W;
+    const double* pc = pbuf + (static_cast<size_t>(t & 1) * G.N + ch) * P;
+    double* zc = z + ch * P;
+    double* rc = r + ch * P;
+    const double* ac = Ap + ch * P;
+    double rr = 0.0, zz = 0.0;
+    const size_t base = static_cast<size_t>(blockIdx.x) * NTU * UPT;
+    if ((P & 1) == 0) {
+        const size_t nv = P / 2;
+        for (int k = 0; k < UPT / 2; ++k) {
+            const size_t vi = base / 2 + static_cast<size_t>(k) * NTU + threadIdx.x;
+            if (vi >= nv) break;
+            const double2 pv = __ldcs(reinterpret_cast<const double2*>(pc) + vi);
+            const double2 av = __ldcs(reinterpret_cast<const double2*>(ac) + vi);
+            double2 zv = __ldcs(reinterpret_cast<const double2*>(zc) + vi);
+            double2 rv = __ldcs(reinterpret_cast<const double2*>(rc) + vi);
+            zv.x = zv.x + pv.x * alpha; zv.y = zv.y + pv.y * alpha;
+            rv.x = rv.x - av.x * alpha; rv.y = rv.y - av.y * alpha;
+            __stcs(reinterpret_cast<double2*>(zc) + vi, zv);
+            __stcs(reinterpret_cast<double2*>(rc) + vi, rv);
+            rr += rv.x * rv.x + rv.y * rv.y;
+            zz += zv.x * zv.x + zv.y * zv.y;
+        }
+    } else {
+        for (int k = 0; k < UPT; ++k) {
+            const size_t i = base + static_cast<size_t>(k) * NTU + threadIdx.x;
+            if (i >= P) break;
+            const double zv = zc[i] + pc[i] * alpha;
+            const double rv = rc[i] - ac[i] * alpha;
+            zc[i] = zv;
+            rc[i] = rv;
+            rr += rv * rv;
+            zz += zv * zv;
+        }
+    }
+    const double brr = block_sum<NTU>(rr, red);
+    const double bzz = block_sum<NTU>(zz, red);
+    if (threadIdx.x == 0) {
+        part[(static_cast<size_t>(ch) * nblk + blockIdx.x) * 2] = brr;
+        part[(static_cast<size_t>(ch) * nblk + blockIdx.x) * 2 + 1] = bzz;
+    }
+    if (elect_last_block(&st[ch].cnt_u, nblk)) {
+        const double rs_new = sum_partials<NTU>(part + static_cast<size_t>(ch) * nblk * 2, nblk, 2, red);
+        const double zsq = sum_partials<NTU>(part + static_cast<size_t>(ch) * nblk * 2 + 1, nblk, 2, red);
+        if (threadIdx.x == 0) {
+            CgState& S = st[ch];
+            const double step = fabs(alpha) * sqrt(S.pp);
+            S.zz = zsq;
+            if (step <= S.cg_tol * fmax(sqrt(zsq), 1e-300)) {
+                S.done = 1;
+                S.iters = t + 1;
+            } else {
+                S.beta = rs_new / S.rs;
+                S.rs = rs_new;
+                S.t = t + 1;
+                if (S.t >= S.max_iters) {
+                    S.done = 3;
+                    S.iters = S.max_iters;
+                }
+            }
+            S.cnt_u = 0;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// rhs = B^T U x and CG initialisation (pansharpen.cpp:225-235).
+// ------------------------------------------------------------------------------------------
+template <bool CG>
+__global__ void __launch_bounds__(NTA) k_rhs(PsGeo G, const double* __restrict__ taps, const double* __restrict__ x,
+                                             double* __restrict__ rhs, double* __restrict__ z, double* __restrict__ p1,
+                                             CgState* st, double* __restrict__ part, int nblk, int max_iters,
+                                             double cg_tol) {
+    __shared__ double red[NTA / 32 + 1];
+    extern __shared__ double sk[];
+    const int ch = blockIdx.y;
+    const int H = G.H, W = G.W, c = G.c, n = G.n, C = G.C;
+    const double* tp = taps + static_cast<size_t>(ch / G.cps) * n * n;
+    for (int e = threadIdx.x; e < n * n; e += NTA) sk[e] = tp[e];
+    __syncthreads();
+    const int ntx = (W + TA - 1) / TA;
+    const int by = blockIdx.x / ntx, bx = blockIdx.x - by * ntx;
+    const size_t P = static_cast<size_t>(H) * W;
+    const double* xc = x + static_cast<size_t>(ch) * G.h * G.w;
+    double ss = 0.0;
+    const int tx = threadIdx.x & 31;
+    for (int ty = threadIdx.x >> 5; ty < TA; ty += NTA / 32) {
+        const int R = by * TA + ty, Cc = bx * TA + tx;
+        if (R >= H || Cc >= W) continue;
+        const int ilo = floordiv(R - C + c - 1, c), ihi = floordiv(R + C, c);
+        const int jlo = floordiv(Cc - C + c - 1, c), jhi = floordiv(Cc + C, c);
+        double acc = 0.0;
+        for (int i = ilo; i <= ihi; ++i) {
+            const double* krow = sk + (c * i - R + C) * n + C - Cc;
+            const double* xrow = xc + static_cast<size_t>(wrapi(i, G.h)) * G.w;
+            for (int j = jlo; j <= jhi; ++j) acc = fma(krow[c * j], __ldg(xrow + wrapi(j, G.w)), acc);
+        }
+        const size_t gi = ch * P + static_cast<size_t>(R) * W + Cc;
+        rhs[gi] = acc;
+        if (CG) {
+            z[gi] = 0.0;
+            p1[gi] = 0.0;
+            ss += acc * acc;
+        }
+    }
+    if (CG) {
+        const double bs = block_sum<NTA>(ss, red);
+        if (threadIdx.x == 0) part[static_cast<size_t>(ch) * nblk + blockIdx.x] = bs;
+        if (elect_last_block(&st[ch].cnt_init, nblk)) {
+            const double tot = sum_partials<NTA>(part + static_cast<size_t>(ch) * nblk, nblk, 1, red);
+            if (threadIdx.x == 0) {
+                CgState& S = st[ch];
+                S.rs = tot;
+                S.rhs_norm = sqrt(tot);
+                S.pp = S.pAp = S.alpha = S.beta = S.zz = 0.0;
+                S.cg_tol = cg_tol;
+                S.t = 0;
+                S.iters = 0;
+                S.max_iters = max_iters;
+                S.done = (S.rhs_norm == 0.0) ? 1 : (max_iters <= 0 ? 3 : 0);
+                S.cnt_q = S.cnt_a = S.cnt_u = 0;
+                S.cnt_init = 0;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// Guided filter (pansharpen.cpp:274-312), clamped windows (ops.cpp:104-128).
+// input = L(z0) when in_is_z0 (pansharpen.cpp:396-398), else the input plane itself.
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(NTA) k_guided(int H, int W, int rw, double eps, int cps, const double* __restrict__ in,
+                                                int in_is_z0, const double* __restrict__ guide,
+                                                double* __restrict__ aout, double* __restrict__ cout,
+                                                double* __restrict__ vout) {
+    extern __shared__ double sm[];
+    const int ch = blockIdx.y;
+    const size_t P = static_cast<size_t>(H) * W;
+    const double* ic = in + ch * P;
+    guide += static_cast<size_t>(ch / cps) * P;
+    const int ntx = (W + TA - 1) / TA;
+    const int by = blockIdx.x / ntx, bx = blockIdx.x - by * ntx;
+    const int r0 = by * TA, c0 = bx * TA;
+    const int hz = 2 * rw + (in_is_z0 ? 1 : 0), hin = 2 * rw, hac = rw;
+    const int SZ = TA + 2 * hz, SN = TA + 2 * hin, SA = TA + 2 * hac;
+    double* sz = sm;
+    double* sin_ = in_is_z0 ? sz + ((SZ * SZ + 1) & ~1) : sz;
+    double* sI = sin_ + ((SN * SN + 1) & ~1);
+    double* sa = sI + ((SN * SN + 1) & ~1);
+    double* sc = sa + ((SA * SA + 1) & ~1);
+    for (int e = threadIdx.x; e < SZ * SZ; e += NTA) {
+        const int y = e / SZ, x = e - y * SZ;
+        sz[e] = __ldg(ic + static_cast<size_t>(wrapi(r0 - hz + y, H)) * W + wrapi(c0 - hz + x, W));
+    }
+    for (int e = threadIdx.x; e < SN * SN; e += NTA) {
+        const int y = e / SN, x = e - y * SN;
+        sI[e] = __ldg(guide + static_cast<size_t>(wrapi(r0 - hin + y, H)) * W + wrapi(c0 - hin + x, W));
+    }
+    __syncthreads();
+    if (in_is_z0) {
+        for (int e = threadIdx.x; e < SN * SN; e += NTA) {
+            const int y = e / SN + 1, x = e % SN + 1;
+            sin_[e] = 4.0 * sz[y * SZ + x] - sz[(y - 1) * SZ + x] - sz[(y + 1) * SZ + x] - sz[y * SZ + x - 1] -
+                      sz[y * SZ + x + 1];
+        }
+        __syncthreads();
+    }
+    // a, c on R + rw (only in-image positions are ever consumed)
+    for (int e = threadIdx.x; e < SA * SA; e += NTA) {
+        const int y = e / SA, x = e - y * SA;
+        const int gr = r0 - hac + y, gc = c0 - hac + x;
+        double a = 0.0, cc = 0.0;
+        if (gr >= 0 && gr < H && gc >= 0 && gc < W) {
+            const int ra = max(0, gr - rw), rb = min(H - 1, gr + rw);
+            const int ca = max(0, gc - rw), cb = min(W - 1, gc + rw);
+            double s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0;
+            for (int yy = ra; yy <= rb; ++yy)
+                for (int xx = ca; xx <= cb; ++xx) {
+                    const int li = (yy - r0 + hin) * SN + (xx - c0 + hin);
+                    const double gv = sI[li], iv = sin_[li];
+                    s1 += gv;
+                    s2 += iv;
+                    s3 += gv * iv;
+                    s4 += gv * gv;
+                }
+            const double cnt = static_cast<double>((rb - ra + 1) * (cb - ca + 1));
+            const double mu = s1 / cnt, im = s2 / cnt, cgi = s3 / cnt, cgg = s4 / cnt;
+            const double var = cgg - mu * mu;
+            const double cov = cgi - mu * im;
+            a = cov / (var + eps);
+            cc = im - a * mu;
+        }
+        sa[e] = a;
+        sc[e] = cc;
+    }
+    __syncthreads();
+    const int tx = threadIdx.x & 31;
+    for (int ty = threadIdx.x >> 5; ty < TA; ty += NTA / 32) {
+        const int R = r0 + ty, Cc = c0 + tx;
+        if (R >= H || Cc >= W) continue;
+        const int ra = max(0, R - rw), rb = min(H - 1, R + rw);
+        const int ca = max(0, Cc - rw), cb = min(W - 1, Cc + rw);
+        double s1 = 0.0, s2 = 0.0;
+        for (int yy = ra; yy <= rb; ++yy)
+            for (int xx = ca; xx <= cb; ++xx) {
+                const int li = (yy - r0 + hac) * SA + (xx - c0 + hac);
+                s1 += sa[li];
+                s2 += sc[li];
+            }
+        const double cnt = static_cast<double>((rb - ra + 1) * (cb - ca + 1));
+        const double gv = sI[(ty + hin) * SN + tx + hin];
+        const size_t gi = ch * P + static_cast<size_t>(R) * W + Cc;
+        vout[gi] = (s1 / cnt) * gv + s2 / cnt;
+        if (aout) aout[gi] = sa[(ty + hac) * SA + tx + hac];
+        if (cout) cout[gi] = sc[(ty + hac) * SA + tx + hac];
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// Alias-group direct solve (pansharpen.cpp:337-363): one thread per LR frequency (kl, ll).
+// The c^2 x c^2 system A = diag(D) + u u^H / c^2 (D = lambda |L^|^2, u = conj(b^)) is solved in
+// closed form, eliminating through the coordinate j with the smallest D (the one that can be
+// ~0 near DC), which keeps the solve stable where Sherman-Morrison would cancel. The
+// eigenvalue-ratio test of :353-357 uses the exact extremal eigenvalues of the rank-one
+// update (secular equation) whenever the cheap interlacing bound is inconclusive.
+// ------------------------------------------------------------------------------------------
+struct cplx {
+    double x, y;
+};
+__device__ __forceinline__ cplx cmul(cplx a, cplx b) { return {a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x}; }
+__device__ __forceinline__ cplx cconj(cplx a) { return {a.x, -a.y}; }
+__device__ __forceinline__ double cnorm(cplx a) { return a.x * a.x + a.y * a.y; }
+
+__device__ __forceinline__ cplx half_lookup(const double2* X, int R, int Cc, int H, int W) {
+    const int WH = W / 2 + 1;
+    if (Cc < WH) {
+        const double2 v = X[static_cast<size_t>(R) * WH + Cc];
+        return {v.x, v.y};
+    }
+    const double2 v = X[static_cast<size_t>((H - R) % H) * WH + (W - Cc)];
+    return {v.x, -v.y};
+}
+
+// smallest root of c2 + sum |u_g|^2/(D_g - x) in (lo, hi), by bisection
+__device__ __noinline__ double secular_root(int m, const double* D, const double* u2, double c2, double lo,
+                                            double hi) {
+    for (int it = 0; it < 200; ++it) {
+        const double mid = 0.5 * (lo + hi);
+        if (!(mid > lo && mid < hi)) break;
+        double f = c2;
+        for (int g = 0; g < m; ++g)
+            if (u2[g] > 0.0) f += u2[g] / (D[g] - mid);
+        if (f > 0.0) hi = mid;
+        else lo = mid;
+    }
+    return 0.5 * (lo + hi);
+}
+
+__device__ __noinline__ bool alias_condition_ok(int m, const double* D, const double* u2, double c2) {
+    double dmin_all = INFINITY, dmax_all = -INFINITY;
+    double dmin_u = INFINITY, d2_u = INFINITY, dmax_u = -INFINITY, unorm = 0.0;
+    int mult_min = 0;
+    double min_defl = INFINITY, max_defl = -INFINITY;
+    for (int g = 0; g < m; ++g) {
+        dmin_all = fmin(dmin_all, D[g]);
+        dmax_all = fmax(dmax_all, D[g]);
+        if (u2[g] > 0.0) {
+            unorm += u2[g];
+            dmax_u = fmax(dmax_u, D[g]);
+            if (D[g] < dmin_u) { d2_u = dmin_u; dmin_u = D[g]; mult_min = 1; }
+            else if (D[g] == dmin_u) { ++mult_min; }
+            else if (D[g] < d2_u) d2_u = D[g];
+        } else {
+            min_defl = fmin(min_defl, D[g]);
+            max_defl = fmax(max_defl, D[g]);
+        }
+    }
+    const double ub_max = dmax_all + unorm / c2;
+    if (dmin_all > 0.0 && ub_max <= 1e14 * dmin_all) return true;
+    double ev_min = min_defl, ev_max = max_defl;
+    if (unorm > 0.0) {
+        double r;
+        if (mult_min >= 2) r = dmin_u;
+        else if (!(d2_u < INFINITY)) r = dmin_u + unorm / c2;
+        else r = secular_root(m, D, u2, c2, dmin_u, d2_u);
+        ev_min = fmin(ev_min, r);
+        const double top = secular_root(m, D, u2, c2, dmax_u, dmax_u + unorm / c2 * (1.0 + 1e-12) + 1e-300);
+        ev_max = fmax(ev_max, top);
+    }
+    return (ev_min > 0.0) && !(ev_max > 1e14 * ev_min);
+}
+
+template <int CM>
+__global__ void __launch_bounds__(128) k_alias(int H, int W, int h, int w, int c, int cps, double lambda,
+                                               const double2* __restrict__ Bh, const double2* __restrict__ Xh,
+                                               const double2* __restrict__ Vh, double2* __restrict__ Zh,
+                                               int* __restrict__ flag) {
+    constexpr int M = CM * CM;
+    const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= h * w) return;
+    const int ch = blockIdx.y;
+    const int kl = gid / w, ll = gid - kl * w;
+    const int m = c * c;
+    const double c2 = static_cast<double>(m);
+    const size_t HS = static_cast<size_t>(H) * (W / 2 + 1), LS = static_cast<size_t>(h) * (w / 2 + 1);
+    const double2* V = Vh + ch * HS;
+    double2* Z = Zh + ch * HS;
+    Bh += static_cast<size_t>(ch / cps) * HS;
+    const cplx xg = half_lookup(Xh + ch * LS, kl, ll, h, w);
+    double D[M], u2[M];
+    cplx u[M], rhs[M];
+    int jmin = 0;
+    for (int a = 0; a < c; ++a)
+        for (int b = 0; b < c; ++b) {
+            const int g = a * c + b;
+            const int R = kl + a * h, Cc = ll + b * w;
+            const cplx bv = half_lookup(Bh, R, Cc, H, W);
+            const cplx vv = half_lookup(V, R, Cc, H, W);
+            const double lh = 4.0 - 2.0 * cos(2.0 * M_PI * R / H) - 2.0 * cos(2.0 * M_PI * Cc / W);  // :56-63
+            D[g] = lambda * (lh * lh);
+            u[g] = cconj(bv);
+            u2[g] = cnorm(u[g]);
+            const cplx ux = cmul(u[g], xg);
+            rhs[g] = {ux.x + lambda * lh * vv.x, ux.y + lambda * lh * vv.y};
+            if (D[g] < D[jmin]) jmin = g;
+        }
+    if (!alias_condition_ok(m, D, u2, c2)) atomicExch(flag + ch, 1);
+    // sigma = u^H z / c^2 from the D_j-scaled secular identity (exact for D_j = 0)
+    const double Dj = D[jmin];
+    cplx num = cmul(cconj(u[jmin]), rhs[jmin]);
+    double den = c2 * Dj + u2[jmin];
+    for (int g = 0; g < m; ++g) {
+        if (g == jmin) continue;
+        const double ratio = Dj / D[g];
+        const cplx t = cmul(cconj(u[g]), rhs[g]);
+        num.x += t.x * ratio;
+        num.y += t.y * ratio;
+        den += u2[g] * ratio;
+    }
+    const cplx sigma = {num.x / den, num.y / den};
+    cplx zsum = {0.0, 0.0};
+    cplx zg[M];
+    for (int g = 0; g < m; ++g) {
+        if (g == jmin) continue;
+        const cplx us = cmul(u[g], sigma);
+        zg[g] = {(rhs[g].x - us.x) / D[g], (rhs[g].y - us.y) / D[g]};
+        const cplx t = cmul(cconj(u[g]), zg[g]);
+        zsum.x += t.x;
+        zsum.y += t.y;
+    }
+    if (u2[jmin] < c2 * Dj) {
+        const cplx us = cmul(u[jmin], sigma);
+        zg[jmin] = {(rhs[jmin].x - us.x) / Dj, (rhs[jmin].y - us.y) / Dj};
+    } else {
+        const cplx s = {c2 * sigma.x - zsum.x, c2 * sigma.y - zsum.y};
+        const cplx uc = cconj(u[jmin]);
+        const double d = u2[jmin];
+        zg[jmin] = {(s.x * uc.x + s.y * uc.y) / d, (s.y * uc.x - s.x * uc.y) / d};
+    }
+    const int WH = W / 2 + 1;
+    for (int a = 0; a < c; ++a)
+        for (int b = 0; b < c; ++b) {
+            const int Cc = ll + b * w;
+            if (Cc < WH) {
+                const int R = kl + a * h;
+                const cplx v = zg[a * c + b];
+                Z[static_cast<size_t>(R) * WH + Cc] = make_double2(v.x, v.y);
+            }
+        }
+}
+
+// out = (z_raw * (1/(H W))) * (1/scale)   (fft_util.cpp:47-56 then pansharpen.cpp:401)
+__global__ void k_unscale(const double* __restrict__ zr, long long n, double inv_n, const double* __restrict__ dscale,
+                          long long per_scale, double* __restrict__ out) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const double inv = dscale ? 1.0 / dscale[i / per_scale] : 1.0;
+        out[i] = (zr[i] * inv_n) * inv;
+    }
+}
+
+// ops.cpp:9-22 embed_kernel
+__global__ void k_embed(const double* __restrict__ taps, int n, int H, int W, double* __restrict__ out) {
+    if (threadIdx.x != 0) return;
+    taps += static_cast<size_t>(blockIdx.x) * n * n;
+    out += static_cast<size_t>(blockIdx.x) * H * W;
+    const int C = (n - 1) / 2;
+    for (int r = 0; r < n; ++r)
+        for (int q = 0; q < n; ++q) {
+            const int rr = wrapi(r - C, H), cc = wrapi(q - C, W);
+            out[static_cast<size_t>(rr) * W + cc] += taps[r * n + q];
+        }
+}
+
+// ---- small helpers ---------------------------------------------------------------------------
+__global__ void k_max_partial(const double* __restrict__ a, long long n, const double* __restrict__ b, long long nb,
+                              double* __restrict__ part) {
+    __shared__ double sh[256];
+    a += blockIdx.y * n;
+    b += blockIdx.y * nb;
+    part += static_cast<size_t>(blockIdx.y) * gridDim.x;
+    double m = -INFINITY;
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n + nb; i += gridDim.x * 256LL)
+        m = fmax(m, i < n ? a[i] : b[i - n]);
+    sh[threadIdx.x] = m;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (threadIdx.x < s) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + s]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+__global__ void k_peak_final(const double* __restrict__ part, int nb, double* __restrict__ scale) {
+    if (threadIdx.x != 0) return;
+    double m = -INFINITY;
+    for (int i = 0; i < nb; ++i) m = fmax(m, part[static_cast<size_t>(blockIdx.x) * nb + i]);
+    scale[blockIdx.x] = m > 0.0 ? 1.0 / m : 1.0;  // pansharpen.cpp:374-376
+}
+__global__ void k_scale_copy(const double* __restrict__ in, long long n, const double* __restrict__ s,
+                             long long per, double* __restrict__ out) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        out[i] = in[i] * s[i / per];
+}
+__global__ void k_guided_combine(const double* __restrict__ ab, const double* __restrict__ cb,
+                                 const double* __restrict__ g, long long n, double* __restrict__ out) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        out[i] = ab[i] * g[i] + cb[i];  // pansharpen.cpp:309-310
+}
+// L(in * s) with the reference's rounding: pan_n = pan * scale first (pansharpen.cpp:378-380)
+__global__ void k_lap_scaled(const double* __restrict__ in, int H, int W, const double* __restrict__ s,
+                             double* __restrict__ out) {
+    const double sc = s ? s[blockIdx.y] : 1.0;
+    const size_t P = static_cast<size_t>(H) * W;
+    const double* ic = in + blockIdx.y * P;
+    double* oc = out + blockIdx.y * P;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < static_cast<long long>(P);
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int r = static_cast<int>(i / W), c = static_cast<int>(i - static_cast<long long>(r) * W);
+        const int rm = (r + H - 1) % H, rp = (r + 1) % H, cm = (c + W - 1) % W, cp = (c + 1) % W;
+        const double x0 = __dmul_rn(ic[i], sc);
+        const double xn = __dmul_rn(ic[static_cast<size_t>(rm) * W + c], sc);
+        const double xs = __dmul_rn(ic[static_cast<size_t>(rp) * W + c], sc);
+        const double xw = __dmul_rn(ic[static_cast<size_t>(r) * W + cm], sc);
+        const double xe = __dmul_rn(ic[static_cast<size_t>(r) * W + cp], sc);
+        double v = __dmul_rn(4.0, x0);
+        v = __dsub_rn(v, xn);
+        v = __dsub_rn(v, xs);
+        v = __dsub_rn(v, xw);
+        v = __dsub_rn(v, xe);
+        oc[i] = v;
+    }
+}
+__global__ void k_box_mean(const double* __restrict__ in, int H, int W, int rad, double* __restrict__ out) {
+    const size_t P = static_cast<size_t>(H) * W;
+    const double* ic = in + blockIdx.y * P;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < static_cast<long long>(P);
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int r = static_cast<int>(i / W), c = static_cast<int>(i - static_cast<long long>(r) * W);
+        const int ra = max(0, r - rad), rb = min(H - 1, r + rad), ca = max(0, c - rad), cb = min(W - 1, c + rad);
+        double s = 0.0;
+        for (int y = ra; y <= rb; ++y)
+            for (int x = ca; x <= cb; ++x) s += ic[static_cast<size_t>(y) * W + x];
+        out[blockIdx.y * P + i] = s / static_cast<double>((rb - ra + 1) * (cb - ca + 1));
+    }
+}
+__global__ void k_convolve(const double* __restrict__ in, int H, int W, const double* __restrict__ taps, int n,
+                           int adjoint, double* __restrict__ out) {
+    const int C = (n - 1) / 2;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+         i < static_cast<long long>(H) * W; i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int r = static_cast<int>(i / W), c = static_cast<int>(i - static_cast<long long>(r) * W);
+        double s = 0.0;
+        for (int a = -C; a <= C; ++a)
+            for (int b = -C; b <= C; ++b) {
+                const int rr = adjoint ? r + a : r - a, cc = adjoint ? c + b : c - b;
+                s += taps[(a + C) * n + b + C] * in[static_cast<size_t>(wrapi(rr, H)) * W + wrapi(cc, W)];
+            }
+        out[i] = s;
+    }
+}
+
+inline int grid1d(Context& ctx, long long n, int threads = 256) {
+    long long b = (n + threads - 1) / threads;
+    const long long cap = static_cast<long long>(ctx.sm_count) * 16;
+    return static_cast<int>(std::max(1LL, std::min(b, cap)));
+}
+
+size_t q_smem(const PsGeo& G) {
+    const int PW = TQ + 2 * G.g;
+    return (static_cast<size_t>((G.n * G.n + 1) & ~1) + static_cast<size_t>(G.c) * G.c * plane_stride(PW)) *
+           sizeof(double);
+}
+size_t a_smem(const PsGeo& G, int mode) { return static_cast<size_t>(apply_layout(G, mode, 0, 0).total) * sizeof(double); }
+
+template <class K>
+void set_smem(K kernel, size_t bytes) {
+    FBMP_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+}
+
+void check_smem(size_t bytes, const char* what) {
+    if (bytes > 227 * 1024)
+        param_error(std::string(what) + ": problem parameters need more shared memory than an SM provides");
+}
+
+}  // namespace
+
+// =============================================================================================
+// host wrappers
+// =============================================================================================
+void data_rhs(Context& ctx, const PsGeo& G, const double* d_taps, const double* d_x, double* d_out) {
+    const int nb = ceil_div(G.W, TA) * ceil_div(G.H, TA);
+    const size_t sm = static_cast<size_t>(G.n) * G.n * sizeof(double);
+    set_smem(k_rhs<false>, sm);
+    k_rhs<false><<<dim3(nb, G.N), NTA, sm, ctx.stream>>>(G, d_taps, d_x, d_out, nullptr, nullptr, nullptr, nullptr,
+                                                         nb, 0, 0.0);
+    ctx.count();
+    check_launch();
+}
+
+void cg_operator_apply(Context& ctx, const PsGeo& G, const double* d_taps, const double* d_guide, const double* d_p,
+                       double* d_out, int mode) {
+    const int nbq = ceil_div(G.w, TQ) * ceil_div(G.h, TQ);
+    const int nba = ceil_div(G.W, TA) * ceil_div(G.H, TA);
+    double* q = ctx.scratch<double>("op_q", static_cast<size_t>(G.N) * G.h * G.w);
+    if (mode != 1) {
+        const size_t sq = q_smem(G);
+        check_smem(sq, "cg operator");
+        set_smem(k_q<false>, sq);
+        k_q<false><<<dim3(nbq, G.N), NTQ, sq, ctx.stream>>>(G, d_taps, d_p, nullptr, q, nullptr, nullptr, nbq);
+        ctx.count();
+        check_launch();
+    }
+    const size_t sa = a_smem(G, mode);
+    check_smem(sa, "cg operator");
+    if (mode == 0) {
+        set_smem(k_apply<0, false>, sa);
+        k_apply<0, false><<<dim3(nba, G.N), NTA, sa, ctx.stream>>>(G, d_taps, d_guide, d_p, q, d_out, nullptr, nullptr, nba);
+    } else if (mode == 1) {
+        set_smem(k_apply<1, false>, sa);
+        k_apply<1, false><<<dim3(nba, G.N), NTA, sa, ctx.stream>>>(G, d_taps, d_guide, d_p, q, d_out, nullptr, nullptr, nba);
+    } else {
+        set_smem(k_apply<2, false>, sa);
+        k_apply<2, false><<<dim3(nba, G.N), NTA, sa, ctx.stream>>>(G, d_taps, d_guide, d_p, q, d_out, nullptr, nullptr, nba);
+    }
+    ctx.count();
+    check_launch();
+}
+
+void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* d_guide, const double* d_x,
+              CgBuffers& B, int max_iters, double cg_tol, std::vector<CgState>& host_state) {
+    const int N = G.N;
+    const int nbq = ceil_div(G.w, TQ) * ceil_div(G.h, TQ);
+    const int nba = ceil_div(G.W, TA) * ceil_div(G.H, TA);
+    const size_t P = static_cast<size_t>(G.H) * G.W;
+    const int nbu = static_cast<int>((P + static_cast<size_t>(NTU) * UPT - 1) / (static_cast<size_t>(NTU) * UPT));
+    const size_t sq = q_smem(G), sa = a_smem(G, 0), sr = static_cast<size_t>(G.n) * G.n * sizeof(double);
+    check_smem(sq, "warmstart");
+    check_smem(sa, "warmstart");
+    set_smem(k_q<true>, sq);
+    set_smem(k_apply<0, true>, sa);
+    set_smem(k_rhs<true>, sr);
+    double* part_init = B.part;
+    double* part_q = part_init + static_cast<size_t>(N) * nba;
+    double* part_a = part_q + static_cast<size_t>(N) * nbq;
+    double* part_u = part_a + static_cast<size_t>(N) * nba;
+    // counters must start at zero
+    FBMP_CUDA(cudaMemsetAsync(B.st, 0, sizeof(CgState) * N, ctx.stream));
+    k_rhs<true><<<dim3(nba, N), NTA, sr, ctx.stream>>>(G, d_taps, d_x, B.r, B.z, B.p + static_cast<size_t>(N) * P,
+                                                       B.st, part_init, nba, max_iters, cg_tol);
+    ctx.count();
+    check_launch();
+
+    // One CUDA graph holds `chunk` iterations (3 kernels each); kernels of finished channels
+    // exit at their first instruction, so the host only polls the flags between graphs.
+    const int chunk = 8;
+    cudaGraph_t graph;
+    cudaGraphExec_t exec;
+    FBMP_CUDA(cudaStreamBeginCapture(ctx.stream, cudaStreamCaptureModeThreadLocal));
+    for (int it = 0; it < chunk; ++it) {
+        k_q<true><<<dim3(nbq, N), NTQ, sq, ctx.stream>>>(G, d_taps, B.r, B.p, B.q, B.st, part_q, nbq);
+        k_apply<0, true><<<dim3(nba, N), NTA, sa, ctx.stream>>>(G, d_taps, d_guide, B.p, B.q, B.Ap, B.st, part_a, nba);
+        k_update<<<dim3(nbu, N), NTU, 0, ctx.stream>>>(G, B.z, B.r, B.p, B.Ap, B.st, part_u, nbu);
+    }
+    FBMP_CUDA(cudaStreamEndCapture(ctx.stream, &graph));
+    FBMP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+
+    CgState* pinned = nullptr;
+    FBMP_CUDA(cudaMallocHost(&pinned, sizeof(CgState) * N * 2));
+    cudaEvent_t ev[2];
+    FBMP_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+    FBMP_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+    auto all_done = [&](const CgState* s) {
+        for (int i = 0; i < N; ++i)
+            if (!s[i].done) return false;
+        return true;
+    };
+    auto launch = [&](int slot) {
+        FBMP_CUDA(cudaGraphLaunch(exec, ctx.stream));
+        ctx.count(3 * chunk);
+        FBMP_CUDA(cudaMemcpyAsync(pinned + slot * N, B.st, sizeof(CgState) * N, cudaMemcpyDeviceToHost, ctx.stream));
+        FBMP_CUDA(cudaEventRecord(ev[slot], ctx.stream));
+    };
+    launch(0);
+    launch(1);
+    int k = 0;
+    const long long max_graphs = static_cast<long long>(max_iters) / chunk + 4;
+    for (long long guard = 0;; ++guard) {
+        const int slot = k & 1;
+        FBMP_CUDA(cudaEventSynchronize(ev[slot]));
+        if (all_done(pinned + slot * N) || guard > max_graphs) break;
+        launch(slot);
+        ++k;
+    }
+    FBMP_CUDA(cudaStreamSynchronize(ctx.stream));
+    host_state.resize(N);
+    FBMP_CUDA(cudaMemcpy(host_state.data(), B.st, sizeof(CgState) * N, cudaMemcpyDeviceToHost));
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+    cudaFreeHost(pinned);
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+}
+
+void guided_filter(Context& ctx, int N, int H, int W, int rw, double eps, const double* d_in, int in_is_z0,
+                   const double* d_guide, double* d_a, double* d_c, double* d_v, int cps) {
+    const int nb = ceil_div(W, TA) * ceil_div(H, TA);
+    const int hz = 2 * rw + (in_is_z0 ? 1 : 0), SZ = TA + 2 * hz, SN = TA + 4 * rw, SA = TA + 2 * rw;
+    const size_t sm = (static_cast<size_t>((SZ * SZ + 1) & ~1) + (in_is_z0 ? ((SN * SN + 1) & ~1) : 0) +
+                       ((SN * SN + 1) & ~1) + 2 * ((SA * SA + 1) & ~1)) * sizeof(double);
+    check_smem(sm, "guided filter");
+    set_smem(k_guided, sm);
+    k_guided<<<dim3(nb, N), NTA, sm, ctx.stream>>>(H, W, rw, eps, cps > 0 ? cps : N, d_in, in_is_z0, d_guide, d_a,
+                                                   d_c, d_v);
+    ctx.count();
+    check_launch();
+}
+
+void solve_channel_fft(Context& ctx, const PsGeo& G, const double* d_taps, const double* d_x, const double* d_v,
+                       const double* d_scale, double* d_out, int* d_flag) {
+    const int N = G.N, H = G.H, W = G.W, h = G.h, w = G.w, S = (G.N + G.cps - 1) / G.cps;
+    if (G.c > 8) param_error("solve_channel_fft: factor > 8 is not supported by the device solver");
+    const size_t P = static_cast<size_t>(H) * W;
+    const size_t HS = static_cast<size_t>(H) * (W / 2 + 1), LS = static_cast<size_t>(h) * (w / 2 + 1);
+    double* emb = ctx.scratch<double>("fft_emb", P * S);
+    double2* bh = ctx.scratch<double2>("fft_bh", HS * S);
+    double2* vh = ctx.scratch<double2>("fft_vh", HS * N);
+    double2* zh = ctx.scratch<double2>("fft_zh", HS * N);
+    double2* xh = ctx.scratch<double2>("fft_xh", LS * N);
+    double* zr = ctx.scratch<double>("fft_zr", P * N);
+    FBMP_CUDA(cudaMemsetAsync(emb, 0, P * S * sizeof(double), ctx.stream));
+    k_embed<<<S, 32, 0, ctx.stream>>>(d_taps, G.n, H, W, emb);
+    ctx.count();
+    FBMP_CUFFT(cufftExecD2Z(ctx.plan(0, H, W, S), emb, reinterpret_cast<cufftDoubleComplex*>(bh)));
+    FBMP_CUFFT(cufftExecD2Z(ctx.plan(0, H, W, N), const_cast<double*>(d_v), reinterpret_cast<cufftDoubleComplex*>(vh)));
+    FBMP_CUFFT(cufftExecD2Z(ctx.plan(0, h, w, N), const_cast<double*>(d_x), reinterpret_cast<cufftDoubleComplex*>(xh)));
+    const int nthreads = 128;
+    const dim3 grid(ceil_div(static_cast<long long>(h) * w, nthreads), N);
+    if (G.c <= 4)
+        k_alias<4><<<grid, nthreads, 0, ctx.stream>>>(H, W, h, w, G.c, G.cps, G.lambda, bh, xh, vh, zh, d_flag);
+    else
+        k_alias<8><<<grid, nthreads, 0, ctx.stream>>>(H, W, h, w, G.c, G.cps, G.lambda, bh, xh, vh, zh, d_flag);
+    ctx.count();
+    check_launch();
+    FBMP_CUFFT(cufftExecZ2D(ctx.plan(1, H, W, N), reinterpret_cast<cufftDoubleComplex*>(zh), zr));
+    k_unscale<<<grid1d(ctx, static_cast<long long>(P) * N), 256, 0, ctx.stream>>>(
+        zr, static_cast<long long>(P) * N, 1.0 / static_cast<double>(P), d_scale, static_cast<long long>(P) * G.cps,
+        d_out);
+    ctx.count();
+    check_launch();
+}
+
+void peak_scale(Context& ctx, const double* d_pan, long long P, const double* d_lrms, long long Np, int S,
+                double* d_scale) {
+    const int nb = std::min(grid1d(ctx, P + Np), 512);
+    double* part = ctx.scratch<double>("peak_part", static_cast<size_t>(nb) * S);
+    k_max_partial<<<dim3(nb, S), 256, 0, ctx.stream>>>(d_pan, P, d_lrms, Np, part);
+    k_peak_final<<<S, 32, 0, ctx.stream>>>(part, nb, d_scale);
+    ctx.count(2);
+    check_launch();
+}
+
+void scale_copy(Context& ctx, const double* d_in, long long n, const double* d_scale, long long per, double* d_out) {
+    k_scale_copy<<<grid1d(ctx, n), 256, 0, ctx.stream>>>(d_in, n, d_scale, per, d_out);
+    ctx.count();
+    check_launch();
+}
+
+void guided_combine(Context& ctx, const double* d_ab, const double* d_cb, const double* d_g, long long n,
+                    double* d_out) {
+    k_guided_combine<<<grid1d(ctx, n), 256, 0, ctx.stream>>>(d_ab, d_cb, d_g, n, d_out);
+    ctx.count();
+    check_launch();
+}
+
+void laplacian_scaled(Context& ctx, const double* d_in, int H, int W, int N, const double* d_scale, double* d_out) {
+    k_lap_scaled<<<dim3(grid1d(ctx, static_cast<long long>(H) * W), N), 256, 0, ctx.stream>>>(d_in, H, W, d_scale,
+                                                                                              d_out);
+    ctx.count();
+    check_launch();
+}
+
+void box_mean(Context& ctx, const double* d_in, int H, int W, int N, int radius, double* d_out) {
+    k_box_mean<<<dim3(grid1d(ctx, static_cast<long long>(H) * W), N), 256, 0, ctx.stream>>>(d_in, H, W, radius, d_out);
+    ctx.count();
+    check_launch();
+}
+
+void convolve(Context& ctx, const double* d_in, int H, int W, const double* d_taps, int n, int adjoint, double* d_out) {
+    k_convolve<<<grid1d(ctx, static_cast<long long>(H) * W), 256, 0, ctx.stream>>>(d_in, H, W, d_taps, n, adjoint,
+                                                                                   d_out);
+    ctx.count();
+    check_launch();
+}
+
+}  // namespace fbmp_gpu

@@ -1,0 +1,84 @@
+// pansharpen.cuh -- device-side entry points of Algorithm 2 (HRMS reconstruction).
+#pragma once
+#include "common.cuh"
+
+namespace fbmp_gpu {
+
+// Per-channel CG scalars (pansharpen.cpp:225-256), resident on the device.
+struct CgState {
+    double rs;        // r.r at the start of the current iteration
+    double rhs_norm;  // ||rhs||
+    double pp;        // ||p||^2 of the current iteration (K_Q)
+    double pAp;       // p.Ap (K_A)
+    double alpha;     // rs / pAp (K_A)
+    double beta;      // rs_new / rs for the next p update (K_U)
+    double zz;        // ||z||^2 after the update (K_U)
+    double cg_tol;
+    int t;            // iteration index
+    int done;         // 0 running, 1 converged, 2 non-positive curvature, 3 iteration cap
+    int iters;        // operator applications performed (reference's `it + 1`)
+    int max_iters;
+    unsigned int cnt_init, cnt_q, cnt_a, cnt_u;  // last-block election counters
+};
+
+struct PsGeo {
+    int H, W, h, w, c, n, C, g;  // C = (n-1)/2, g = ceil(C/c)
+    int rw;                       // matting / guided-filter window radius
+    double lambda, eps;
+    int N;                        // channels in the launch (all scenes)
+    int cps;                      // channels per scene: channel ch uses scene ch / cps's
+                                  // taps, guide and intensity scale
+};
+
+PsGeo make_geo(int N, int h, int w, int c, int n, int rw, double lambda, double eps, int cps = 0);
+
+// Workspace of one batched CG solve (all device pointers, channel-major).
+struct CgBuffers {
+    double* z;      // N*P  (output: warm start)
+    double* r;      // N*P
+    double* p;      // 2*N*P (parity double buffer)
+    double* Ap;     // N*P
+    double* q;      // N*p  (D B p at the LR points)
+    double* part;   // partial sums, 4 * N * max_blocks
+    CgState* st;    // N
+    int max_blocks;
+};
+
+// Enqueue the whole CG warm start for N channels sharing `guide` (= L(pan_n)) and taps.
+// x: N*h*w (already scaled). Returns after the loop finished (host polls device flags).
+void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* d_guide, const double* d_x,
+              CgBuffers& B, int max_iters, double cg_tol, std::vector<CgState>& host_state);
+
+// A(p) (pansharpen.cpp:218-223) for N channels: mode 0 full operator, 1 matting only (M p),
+// 2 data term only (B^T U D B p).
+void cg_operator_apply(Context& ctx, const PsGeo& G, const double* d_taps, const double* d_guide,
+                       const double* d_p, double* d_out, int mode);
+
+// rhs = B^T U x (pansharpen.cpp:225).
+void data_rhs(Context& ctx, const PsGeo& G, const double* d_taps, const double* d_x, double* d_out);
+
+// Guided filter (pansharpen.cpp:274-312, called as in :396-399 with input = L(z0) unless
+// input_is_plain): v = box(a)*guide + box(c). a_out/c_out optional.
+void guided_filter(Context& ctx, int N, int H, int W, int rw, double eps, const double* d_in, int in_is_z0,
+                   const double* d_guide, double* d_a, double* d_c, double* d_v, int cps = 0);
+
+// solve_channel_fft (pansharpen.cpp:314-365) for N channels (taps per scene).
+// d_scale (device, one per scene, optional): out is multiplied by 1/scale (pansharpen.cpp:401).
+void solve_channel_fft(Context& ctx, const PsGeo& G, const double* d_taps, const double* d_x, const double* d_v,
+                       const double* d_scale, double* d_out, int* d_flag);
+
+// Elementwise / stencil helpers.
+// per-scene 1/max(PAN, LRMS) (pansharpen.cpp:374-376); d_scale: S doubles
+void peak_scale(Context& ctx, const double* d_pan, long long P, const double* d_lrms, long long Np, int S,
+                double* d_scale);
+// out = in * scale[i / per_scale]
+void scale_copy(Context& ctx, const double* d_in, long long n, const double* d_scale, long long per_scale,
+                double* d_out);
+void guided_combine(Context& ctx, const double* d_ab, const double* d_cb, const double* d_g, long long n,
+                    double* d_out);
+void laplacian_scaled(Context& ctx, const double* d_in, int H, int W, int N, const double* d_scale, double* d_out);
+void box_mean(Context& ctx, const double* d_in, int H, int W, int N, int radius, double* d_out);
+void convolve(Context& ctx, const double* d_in, int H, int W, const double* d_taps, int n, int adjoint,
+              double* d_out);
+
+}  // namespace fbmp_gpu

@@ -18,6 +18,7 @@
 // (oracle/fbmp_numpy.py), see DESIGN.md "Oracle".
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <complex>
 #include <cstdint>
@@ -1137,6 +1138,67 @@ double tgv_objective(const Observation& O, const double* u, const double* p1, co
     return data + prm.alpha1 * tgv1 + prm.alpha2 * tgv2;
 }
 
+
+// Bounded CPU baseline (bench.py): the blind pipeline with the CG loop of every channel
+// capped at `cg_cap` iterations (no cap error), timing each stage with steady_clock.
+// times: {weights, kernel_fit, matting_build, cg_phase (channels threaded), post_phase}.
+void blind_sampled(const double* lrms, int N, int h, int w, const double* pan, int factor, int n, int threads,
+                   int cg_cap, double* times, int* cg_iters_done, int* admm_iters) {
+    using clk = std::chrono::steady_clock;
+    auto sec = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); };
+    const int H = h * factor, W = w * factor;
+    const size_t P = static_cast<size_t>(H) * W, p = static_cast<size_t>(h) * w;
+    auto t0 = clk::now();
+    vec om = solve_weights(lrms, N, h, w, pan, H, W, 4, 10.0, factor);
+    vec obs = combine_bands(lrms, N, p, om.data());
+    auto t1 = clk::now();
+    KeParams kp;
+    kp.n = n;
+    vec k = estimate_kernel_plane_tgv(pan, H, W, obs.data(), h, w, factor, kp, admm_iters, nullptr);
+    auto t2 = clk::now();
+    PsParams prm;
+    double peak = seq_max(pan, P);
+    for (int b = 0; b < N; ++b) peak = std::max(peak, seq_max(lrms + b * p, p));
+    const double scale = peak > 0.0 ? 1.0 / peak : 1.0;
+    vec pan_n(P);
+    for (size_t i = 0; i < P; ++i) pan_n[i] = pan[i] * scale;
+    vec lpan = laplacian(pan_n.data(), H, W);
+    const Matting M = Matting::build(lpan.data(), H, W, prm.radius, prm.eps);
+    auto t3 = clk::now();
+    std::vector<vec> z0(N), xn(N, vec(p));
+    int nt = threads > 0 ? threads : static_cast<int>(std::thread::hardware_concurrency());
+    nt = std::clamp(nt, 1, N);
+    auto run_phase = [&](auto&& body) {
+        std::atomic<int> next{0};
+        auto worker = [&] {
+            for (int i; (i = next.fetch_add(1)) < N;) body(i);
+        };
+        std::vector<std::thread> pool;
+        for (int t = 0; t < nt; ++t) pool.emplace_back(worker);
+        for (auto& t : pool) t.join();
+    };
+    run_phase([&](int i) {
+        for (size_t j = 0; j < p; ++j) xn[i][j] = lrms[i * p + j] * scale;
+        int it = 0, cv = 0;
+        z0[i] = warmstart_cg(xn[i].data(), h, w, k.data(), n, factor, M, prm, cg_cap, false, nullptr, &it, &cv);
+        cg_iters_done[i] = it;
+    });
+    auto t4 = clk::now();
+    run_phase([&](int i) {
+        vec lz = laplacian(z0[i].data(), H, W);
+        vec a, c, gm, gv, im;
+        guided_coeffs(lz.data(), lpan.data(), H, W, prm.radius, prm.eps, a, c, gm, gv, im);
+        vec v = guided_output(a.data(), c.data(), lpan.data(), H, W, prm.radius);
+        vec z = solve_channel_fft(xn[i].data(), h, w, k.data(), n, factor, v.data(), H, W, prm);
+    });
+    auto t5 = clk::now();
+    times[0] = sec(t0, t1);
+    times[1] = sec(t1, t2);
+    times[2] = sec(t2, t3);
+    times[3] = sec(t3, t4);
+    times[4] = sec(t4, t5);
+}
+
 }  // namespace orc
 
 // =============================================================================================
@@ -1361,6 +1423,11 @@ int orc_blind(const double* lrms, int N, int h, int w, const double* pan, int fa
         put(k, k_out);
         put(om, omega_out);
     });
+}
+
+int orc_blind_sampled(const double* lrms, int N, int h, int w, const double* pan, int factor, int n, int threads,
+                      int cg_cap, double* times, int* cg_iters_done, int* admm_iters) {
+    return guard([&] { blind_sampled(lrms, N, h, w, pan, factor, n, threads, cg_cap, times, cg_iters_done, admm_iters); });
 }
 
 }  // extern "C"

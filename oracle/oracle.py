@@ -316,3 +316,19 @@ def blind(lrms, pan, factor, n, l=4, lambda_omega=10.0, threads=0):
     _check(lib().orc_blind(_p(lrms), N, h, w, _p(pan), factor, n, l, C.c_double(lambda_omega), threads, _p(out),
                            _p(k), _p(om), C.byref(ta), it.ctypes.data_as(I)))
     return out, dict(kernel=k, omega=om, admm_iters=ta.value, cg_iters=it)
+
+
+def blind_sampled(lrms, pan, factor, n, cg_cap, threads=0):
+    """Stage-timed blind pipeline with every channel's CG capped at ``cg_cap`` iterations.
+
+    Returns dict(times=[weights, kernel_fit, matting_build, cg_phase, post_phase] seconds,
+    cg_done=[...], admm_iters). Used only by bench.py's CPU baseline / reference arm.
+    """
+    lrms, pan = _f(lrms), _f(pan)
+    N, h, w = lrms.shape
+    t = np.zeros(5)
+    done = np.zeros(N, np.int32)
+    ta = C.c_int(0)
+    _check(lib().orc_blind_sampled(_p(lrms), N, h, w, _p(pan), factor, n, threads, cg_cap, _p(t),
+                                   done.ctypes.data_as(I), C.byref(ta)))
+    return dict(times=list(t), cg_done=list(done), admm_iters=ta.value)

@@ -89,6 +89,11 @@ struct Context {
     std::map<std::string, std::unique_ptr<DevBuf<unsigned char>>> ws;
     std::map<std::tuple<int, int, int, int, int>, cufftHandle> plans;  // (kind, rows, cols, batch, 0)
     int sm_count = 148;
+    // kernel profiling of the CG loop (bench.py roofline): total device ms and launches that
+    // did work, per kernel class {K_Q, K_A, K_U}
+    bool profile = false;
+    double prof_ms[3] = {0, 0, 0};
+    long long prof_n[3] = {0, 0, 0};
 
     explicit Context(int dev);
     ~Context();
@@ -172,14 +177,14 @@ __device__ __forceinline__ double sum_partials(const double* part, int n, int st
 // has been written by thread 0; returns true in every thread of the last block.
 __device__ __forceinline__ bool elect_last_block(unsigned int* counter, unsigned int nblocks) {
     __shared__ bool am_last;
-    __threadfence();
-    __syncthreads();
+    __syncthreads();  // thread 0 wrote the block partial; all threads are past their reads
     if (threadIdx.x == 0) {
+        __threadfence();  // publish the partial before the arrival is counted
         const unsigned int prev = atomicAdd(counter, 1u);
         am_last = (prev == nblocks - 1);
+        if (am_last) __threadfence();
     }
     __syncthreads();
-    if (am_last) __threadfence();
     return am_last;
 }
 

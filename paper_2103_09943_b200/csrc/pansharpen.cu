@@ -9,8 +9,10 @@
 // Reductions are deterministic: fixed per-block trees, per-block partials, and a fixed-order
 // final sum in the last block to finish (threadfence reduction); no floating-point atomics.
 #include <cmath>
+#include <cstdlib>
 
 #include "pansharpen.cuh"
+#include "cg_fast.cuh"
 
 namespace fbmp_gpu {
 
@@ -351,20 +353,30 @@ __global__ void __launch_bounds__(NTU) k_update(PsGeo G, double* __restrict__ z,
     double rr = 0.0, zz = 0.0;
     const size_t base = static_cast<size_t>(blockIdx.x) * NTU * UPT;
     if ((P & 1) == 0) {
+        // all loads of the thread in flight before any arithmetic (memory-level parallelism)
+        constexpr int KV = UPT / 2;
         const size_t nv = P / 2;
-        for (int k = 0; k < UPT / 2; ++k) {
+        double2 pv[KV], av[KV], zv[KV], rv[KV];
+#pragma unroll
+        for (int k = 0; k < KV; ++k) {
+            const size_t vi = base / 2 + static_cast<size_t>(k) * NTU + threadIdx.x;
+            if (vi < nv) {
+                pv[k] = __ldcs(reinterpret_cast<const double2*>(pc) + vi);
+                av[k] = __ldcs(reinterpret_cast<const double2*>(ac) + vi);
+                zv[k] = __ldcs(reinterpret_cast<const double2*>(zc) + vi);
+                rv[k] = __ldcs(reinterpret_cast<const double2*>(rc) + vi);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < KV; ++k) {
             const size_t vi = base / 2 + static_cast<size_t>(k) * NTU + threadIdx.x;
             if (vi >= nv) break;
-            const double2 pv = __ldcs(reinterpret_cast<const double2*>(pc) + vi);
-            const double2 av = __ldcs(reinterpret_cast<const double2*>(ac) + vi);
-            double2 zv = __ldcs(reinterpret_cast<const double2*>(zc) + vi);
-            double2 rv = __ldcs(reinterpret_cast<const double2*>(rc) + vi);
-            zv.x = zv.x + pv.x * alpha; zv.y = zv.y + pv.y * alpha;
-            rv.x = rv.x - av.x * alpha; rv.y = rv.y - av.y * alpha;
-            __stcs(reinterpret_cast<double2*>(zc) + vi, zv);
-            __stcs(reinterpret_cast<double2*>(rc) + vi, rv);
-            rr += rv.x * rv.x + rv.y * rv.y;
-            zz += zv.x * zv.x + zv.y * zv.y;
+            zv[k].x = zv[k].x + pv[k].x * alpha; zv[k].y = zv[k].y + pv[k].y * alpha;
+            rv[k].x = rv[k].x - av[k].x * alpha; rv[k].y = rv[k].y - av[k].y * alpha;
+            __stcs(reinterpret_cast<double2*>(zc) + vi, zv[k]);
+            __stcs(reinterpret_cast<double2*>(rc) + vi, rv[k]);
+            rr += rv[k].x * rv[k].x + rv[k].y * rv[k].y;
+            zz += zv[k].x * zv[k].x + zv[k].y * zv[k].y;
         }
     } else {
         for (int k = 0; k < UPT; ++k) {
@@ -851,6 +863,86 @@ void check_smem(size_t bytes, const char* what) {
 
 }  // namespace
 
+// ---------------------------------------------------------------------------------------------
+// fast-path dispatch (cg_fast.cuh): radius 1, c in {1,2,4}, n <= 21, images >= 64 x 64
+// ---------------------------------------------------------------------------------------------
+bool fast_ok(const PsGeo& G) {
+    return G.rw == 1 && (G.c == 1 || G.c == 2 || G.c == 4) && G.n <= fast::a2::MAXN && G.H >= 64 && G.W >= 64 &&
+           std::getenv("FBMP_DISABLE_FAST") == nullptr;
+}
+
+using QFn = void (*)(PsGeo, const double*, const double*, double*, double*, CgState*, double*, int);
+struct QLaunch {
+    QFn fn = nullptr;
+    size_t smem = 0;
+    int nblk = 0;
+};
+template <int N_, int CF, bool CG>
+QLaunch q2_make(const PsGeo& G) {
+    QLaunch L;
+    L.fn = fast::k_q2<N_, CF, CG>;
+    L.smem = fast::QGeo<N_, CF>::smem;
+    L.nblk = fast::q2_blocks<N_, CF>(G);
+    return L;
+}
+template <bool CG>
+QLaunch q2_select(const PsGeo& G) {
+    if (!fast_ok(G)) return {};
+    if (G.c == 4) {
+        switch (G.n) {
+        case 21: return q2_make<21, 4, CG>(G);
+        case 17: return q2_make<17, 4, CG>(G);
+        case 15: return q2_make<15, 4, CG>(G);
+        case 7: return q2_make<7, 4, CG>(G);
+        default: break;
+        }
+    } else if (G.c == 2) {
+        switch (G.n) {
+        case 5: return q2_make<5, 2, CG>(G);
+        case 3: return q2_make<3, 2, CG>(G);
+        default: break;
+        }
+    }
+    return {};
+}
+
+// per-scene (mu_k, g_k) maps for the fast K_A
+void guide_stats(Context& ctx, const PsGeo& G, const double* d_guide, double* mu, double* gk) {
+    const int S = (G.N + G.cps - 1) / G.cps;
+    fast::k_guide_stats<<<dim3(grid1d(ctx, static_cast<long long>(G.H) * G.W), S), 256, 0, ctx.stream>>>(
+        d_guide, G.H, G.W, G.rw, G.eps, mu, gk);
+    ctx.count();
+    check_launch();
+}
+
+template <bool CG>
+void launch_apply2(Context& ctx, const PsGeo& G, const double* taps, const double* guide, const double* mu,
+                   const double* gk, const double* p, const double* q, double* out, CgState* st, double* part) {
+    const int S = (G.N + G.cps - 1) / G.cps;
+    const int nba = ceil_div(G.W, fast::a2::TA) * ceil_div(G.H, fast::a2::TA);
+    switch (G.c) {
+    case 1:
+        fast::k_apply2<CG, 1><<<dim3(nba, S), fast::NT, fast::a2::L<1>::smem, ctx.stream>>>(G, taps, guide, mu, gk, p,
+                                                                                           q, out, st, part, nba);
+        break;
+    case 2:
+        fast::k_apply2<CG, 2><<<dim3(nba, S), fast::NT, fast::a2::L<2>::smem, ctx.stream>>>(G, taps, guide, mu, gk, p,
+                                                                                           q, out, st, part, nba);
+        break;
+    default:
+        fast::k_apply2<CG, 4><<<dim3(nba, S), fast::NT, fast::a2::L<4>::smem, ctx.stream>>>(G, taps, guide, mu, gk, p,
+                                                                                           q, out, st, part, nba);
+        break;
+    }
+}
+
+template <bool CG>
+void prepare_apply2() {
+    set_smem(fast::k_apply2<CG, 1>, fast::a2::L<1>::smem);
+    set_smem(fast::k_apply2<CG, 2>, fast::a2::L<2>::smem);
+    set_smem(fast::k_apply2<CG, 4>, fast::a2::L<4>::smem);
+}
+
 // =============================================================================================
 // host wrappers
 // =============================================================================================
@@ -870,12 +962,31 @@ void cg_operator_apply(Context& ctx, const PsGeo& G, const double* d_taps, const
     const int nba = ceil_div(G.W, TA) * ceil_div(G.H, TA);
     double* q = ctx.scratch<double>("op_q", static_cast<size_t>(G.N) * G.h * G.w);
     if (mode != 1) {
-        const size_t sq = q_smem(G);
-        check_smem(sq, "cg operator");
-        set_smem(k_q<false>, sq);
-        k_q<false><<<dim3(nbq, G.N), NTQ, sq, ctx.stream>>>(G, d_taps, d_p, nullptr, q, nullptr, nullptr, nbq);
+        const QLaunch ql = q2_select<false>(G);
+        if (ql.fn) {
+            set_smem(ql.fn, ql.smem);
+            ql.fn<<<dim3(ql.nblk, G.N), fast::NT, ql.smem, ctx.stream>>>(G, d_taps, d_p, nullptr, q, nullptr, nullptr,
+                                                                          ql.nblk);
+        } else {
+            const size_t sq = q_smem(G);
+            check_smem(sq, "cg operator");
+            set_smem(k_q<false>, sq);
+            k_q<false><<<dim3(nbq, G.N), NTQ, sq, ctx.stream>>>(G, d_taps, d_p, nullptr, q, nullptr, nullptr, nbq);
+        }
         ctx.count();
         check_launch();
+    }
+    if (mode == 0 && fast_ok(G)) {
+        const size_t P = static_cast<size_t>(G.H) * G.W;
+        const int S = (G.N + G.cps - 1) / G.cps;
+        double* mu = ctx.scratch<double>("op_wmu", P * S);
+        double* gk = ctx.scratch<double>("op_wg", P * S);
+        guide_stats(ctx, G, d_guide, mu, gk);
+        prepare_apply2<false>();
+        launch_apply2<false>(ctx, G, d_taps, d_guide, mu, gk, d_p, q, d_out, nullptr, nullptr);
+        ctx.count();
+        check_launch();
+        return;
     }
     const size_t sa = a_smem(G, mode);
     check_smem(sa, "cg operator");
@@ -896,16 +1007,28 @@ void cg_operator_apply(Context& ctx, const PsGeo& G, const double* d_taps, const
 void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* d_guide, const double* d_x,
               CgBuffers& B, int max_iters, double cg_tol, std::vector<CgState>& host_state) {
     const int N = G.N;
-    const int nbq = ceil_div(G.w, TQ) * ceil_div(G.h, TQ);
-    const int nba = ceil_div(G.W, TA) * ceil_div(G.H, TA);
+    const QLaunch q2 = q2_select<true>(G);
+    const bool fastA = fast_ok(G);
+    const int nbq = q2.fn ? q2.nblk : ceil_div(G.w, TQ) * ceil_div(G.h, TQ);
+    const int nba = fastA ? ceil_div(G.W, fast::a2::TA) * ceil_div(G.H, fast::a2::TA) : ceil_div(G.W, TA) * ceil_div(G.H, TA);
     const size_t P = static_cast<size_t>(G.H) * G.W;
     const int nbu = static_cast<int>((P + static_cast<size_t>(NTU) * UPT - 1) / (static_cast<size_t>(NTU) * UPT));
-    const size_t sq = q_smem(G), sa = a_smem(G, 0), sr = static_cast<size_t>(G.n) * G.n * sizeof(double);
+    const size_t sq = q2.fn ? q2.smem : q_smem(G), sa = a_smem(G, 0), sr = static_cast<size_t>(G.n) * G.n * sizeof(double);
     check_smem(sq, "warmstart");
-    check_smem(sa, "warmstart");
-    set_smem(k_q<true>, sq);
-    set_smem(k_apply<0, true>, sa);
+    if (!fastA) check_smem(sa, "warmstart");
+    if (q2.fn) set_smem(q2.fn, q2.smem);
+    else set_smem(k_q<true>, sq);
+    if (fastA) prepare_apply2<true>();
+    else set_smem(k_apply<0, true>, sa);
     set_smem(k_rhs<true>, sr);
+    double* wmu = nullptr;
+    double* wg = nullptr;
+    if (fastA) {
+        const int S = (G.N + G.cps - 1) / G.cps;
+        wmu = ctx.scratch<double>("cg_wmu", P * S);
+        wg = ctx.scratch<double>("cg_wg", P * S);
+        guide_stats(ctx, G, d_guide, wmu, wg);
+    }
     double* part_init = B.part;
     double* part_q = part_init + static_cast<size_t>(N) * nba;
     double* part_a = part_q + static_cast<size_t>(N) * nbq;
@@ -919,14 +1042,28 @@ void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* 
 
     // One CUDA graph holds `chunk` iterations (3 kernels each); kernels of finished channels
     // exit at their first instruction, so the host only polls the flags between graphs.
+    // In profile mode event records bracket every kernel and graphs are not pipelined.
     const int chunk = 8;
+    const bool prof = ctx.profile;
+    std::vector<cudaEvent_t> pev(prof ? chunk * 4 : 0);
+    for (auto& e : pev) FBMP_CUDA(cudaEventCreate(&e));
     cudaGraph_t graph;
     cudaGraphExec_t exec;
     FBMP_CUDA(cudaStreamBeginCapture(ctx.stream, cudaStreamCaptureModeThreadLocal));
     for (int it = 0; it < chunk; ++it) {
-        k_q<true><<<dim3(nbq, N), NTQ, sq, ctx.stream>>>(G, d_taps, B.r, B.p, B.q, B.st, part_q, nbq);
-        k_apply<0, true><<<dim3(nba, N), NTA, sa, ctx.stream>>>(G, d_taps, d_guide, B.p, B.q, B.Ap, B.st, part_a, nba);
+        if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * 4 + 0], ctx.stream, cudaEventRecordExternal));
+        if (q2.fn)
+            q2.fn<<<dim3(nbq, N), fast::NT, sq, ctx.stream>>>(G, d_taps, B.r, B.p, B.q, B.st, part_q, nbq);
+        else
+            k_q<true><<<dim3(nbq, N), NTQ, sq, ctx.stream>>>(G, d_taps, B.r, B.p, B.q, B.st, part_q, nbq);
+        if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * 4 + 1], ctx.stream, cudaEventRecordExternal));
+        if (fastA)
+            launch_apply2<true>(ctx, G, d_taps, d_guide, wmu, wg, B.p, B.q, B.Ap, B.st, part_a);
+        else
+            k_apply<0, true><<<dim3(nba, N), NTA, sa, ctx.stream>>>(G, d_taps, d_guide, B.p, B.q, B.Ap, B.st, part_a, nba);
+        if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * 4 + 2], ctx.stream, cudaEventRecordExternal));
         k_update<<<dim3(nbu, N), NTU, 0, ctx.stream>>>(G, B.z, B.r, B.p, B.Ap, B.st, part_u, nbu);
+        if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * 4 + 3], ctx.stream, cudaEventRecordExternal));
     }
     FBMP_CUDA(cudaStreamEndCapture(ctx.stream, &graph));
     FBMP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
@@ -947,17 +1084,38 @@ void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* 
         FBMP_CUDA(cudaMemcpyAsync(pinned + slot * N, B.st, sizeof(CgState) * N, cudaMemcpyDeviceToHost, ctx.stream));
         FBMP_CUDA(cudaEventRecord(ev[slot], ctx.stream));
     };
-    launch(0);
-    launch(1);
-    int k = 0;
     const long long max_graphs = static_cast<long long>(max_iters) / chunk + 4;
-    for (long long guard = 0;; ++guard) {
-        const int slot = k & 1;
-        FBMP_CUDA(cudaEventSynchronize(ev[slot]));
-        if (all_done(pinned + slot * N) || guard > max_graphs) break;
-        launch(slot);
-        ++k;
+    int k = 0;
+    if (prof) {
+        // iterations with at least one active channel = max over channels of iters
+        for (long long g = 0; g <= max_graphs; ++g) {
+            launch(0);
+            FBMP_CUDA(cudaEventSynchronize(ev[0]));
+            int active_iters = 0;
+            for (int i = 0; i < N; ++i) active_iters = std::max(active_iters, pinned[i].done ? pinned[i].iters : pinned[i].t);
+            for (int it = 0; it < chunk; ++it) {
+                if (g * chunk + it >= active_iters) break;
+                for (int kk = 0; kk < 3; ++kk) {
+                    float ms = 0.f;
+                    FBMP_CUDA(cudaEventElapsedTime(&ms, pev[it * 4 + kk], pev[it * 4 + kk + 1]));
+                    ctx.prof_ms[kk] += ms;
+                    ctx.prof_n[kk] += 1;
+                }
+            }
+            if (all_done(pinned)) break;
+        }
+    } else {
+        launch(0);
+        launch(1);
+        for (long long guard = 0;; ++guard) {
+            const int slot = k & 1;
+            FBMP_CUDA(cudaEventSynchronize(ev[slot]));
+            if (all_done(pinned + slot * N) || guard > max_graphs) break;
+            launch(slot);
+            ++k;
+        }
     }
+    for (auto& e : pev) cudaEventDestroy(e);
     FBMP_CUDA(cudaStreamSynchronize(ctx.stream));
     host_state.resize(N);
     FBMP_CUDA(cudaMemcpy(host_state.data(), B.st, sizeof(CgState) * N, cudaMemcpyDeviceToHost));

@@ -124,6 +124,7 @@ _lib.fbmp_gpu_ctx_stream.argtypes = [C.c_void_p]
 _lib.fbmp_gpu_ctx_launches.restype = C.c_longlong
 _lib.fbmp_gpu_ctx_launches.argtypes = [C.c_void_p]
 _lib.fbmp_gpu_ctx_stats.argtypes = [C.c_void_p, C.POINTER(_Stats)]
+_lib.fbmp_gpu_ctx_set_profile.argtypes = [C.c_void_p, C.c_int]
 
 
 def _check(status: int) -> None:
@@ -158,6 +159,15 @@ class Context:
     @property
     def launches(self) -> int:
         return _lib.fbmp_gpu_ctx_launches(self.h)
+
+    def set_profile(self, on: bool) -> None:
+        _lib.fbmp_gpu_ctx_set_profile(self.h, int(on))
+
+    def kernel_profile(self) -> dict:
+        ms = (C.c_double * 3)()
+        n = (C.c_longlong * 3)()
+        _check(_lib.fbmp_gpu_ctx_kernel_profile(self.h, ms, n))
+        return {name: dict(total_ms=ms[i], launches=n[i]) for i, name in enumerate(("K_Q", "K_A", "K_U"))}
 
     def stats(self) -> dict:
         s = _Stats()
@@ -542,7 +552,8 @@ def blind_dev(d_lrms: int, N: int, h: int, w: int, d_pan: int, d_out: int, d_k: 
 EXPORTED_SYMBOLS = (
     "fbmp_gpu_default_ps_params", "fbmp_gpu_default_ke_params", "fbmp_gpu_default_sw_params",
     "fbmp_gpu_ctx_create", "fbmp_gpu_ctx_destroy", "fbmp_gpu_last_error", "fbmp_gpu_ctx_stats",
-    "fbmp_gpu_ctx_stream", "fbmp_gpu_ctx_launches", "fbmp_gpu_pansharpen", "fbmp_gpu_estimate_kernel_tgv",
+    "fbmp_gpu_ctx_stream", "fbmp_gpu_ctx_launches", "fbmp_gpu_ctx_set_profile", "fbmp_gpu_ctx_kernel_profile",
+    "fbmp_gpu_pansharpen", "fbmp_gpu_estimate_kernel_tgv",
     "fbmp_gpu_estimate_kernel_plane", "fbmp_gpu_solve_weights", "fbmp_gpu_combine_bands", "fbmp_gpu_blind",
     "fbmp_gpu_blind_dev", "fbmp_gpu_blind_batch", "fbmp_gpu_apply_prior", "fbmp_gpu_llp_apply",
     "fbmp_gpu_data_apply", "fbmp_gpu_cg_operator", "fbmp_gpu_warmstart_cg", "fbmp_gpu_guided_filter",

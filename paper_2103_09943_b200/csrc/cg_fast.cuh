@@ -438,5 +438,664 @@ __global__ void __launch_bounds__(NT, 2) k_apply2(PsGeo G, const double* __restr
     }
 }
 
+
+// ------------------------------------------------------------------------------------------
+// K_A3: K_A2 restructured for shared-memory traffic. Every stage works on a 2 x 4 register
+// micro-tile (horizontal and vertical 3-sums fused), I*s is formed on the fly, and the data
+// term keeps the thread's zero-padded sampling-phase sub-kernel in registers (N_, CF known
+// at compile time; N_ = 0 keeps the generic broadcast-tap loop).
+// ------------------------------------------------------------------------------------------
+namespace a3 {
+constexpr int TA = 32;
+constexpr int WP = TA + 8, WI = TA + 6, WK = TA + 4, WM = TA + 2;
+template <int CF>
+struct L {
+    static constexpr int QMAX = a2::maxq(CF);
+    static constexpr int O_TAPS = 0;                       // generic path only
+    static constexpr int O_I = O_TAPS + a2::MAXTAP;        // guide on R+3
+    static constexpr int O_MU = O_I + WI * WI;             // mu_k on R+2
+    static constexpr int O_G = O_MU + WK * WK;             // g_k on R+2
+    static constexpr int O_S = O_G + WK * WK;              // s on R+3
+    static constexpr int O_M = O_S + WI * WI;              // M s on R+1
+    static constexpr int O_Q = O_M + WM * WM;              // q window
+    static constexpr int O_U = O_Q + ((QMAX + 1) / 2) * 2; // p on R+4 -> (a, c1) on R+2 -> data out
+    static constexpr int U_SIZE = 2 * WK * WK;
+    static constexpr int TOTAL = O_U + U_SIZE;
+    static_assert(U_SIZE >= WP * WP && U_SIZE >= TA * TA, "union too small");
+    static constexpr size_t smem = TOTAL * sizeof(double);
+};
+template <int N_, int CF>
+struct DT {  // zero-padded sub-kernel extent of the data term
+    static constexpr int C = (N_ - 1) / 2;
+    static constexpr int DLO = -(C / CF);
+    static constexpr int DHI = (CF - 1 + C) / CF;
+    static constexpr int DM = DHI - DLO + 1;
+};
+}  // namespace a3
+
+template <bool CG, int N_, int CF>
+__global__ void __launch_bounds__(NT, 2) k_apply3(PsGeo G, const double* __restrict__ taps,
+                                                  const double* __restrict__ guide, const double* __restrict__ wmu,
+                                                  const double* __restrict__ wg, const double* __restrict__ pin,
+                                                  const double* __restrict__ q, double* __restrict__ out, CgState* st,
+                                                  double* __restrict__ part, int nblk) {
+    using namespace a3;
+    using Lay = L<CF>;
+    __shared__ double red[NT / 32 + 1];
+    extern __shared__ double sm[];
+    const int scene = blockIdx.y;
+    const int H = G.H, W = G.W, n = G.n, C = G.C;
+    const size_t P = static_cast<size_t>(H) * W;
+    const int ntx = (W + TA - 1) / TA;
+    const int by = blockIdx.x / ntx, bx = blockIdx.x - by * ntx;
+    const int r0 = by * TA, c0 = bx * TA;
+    double* sk = sm + Lay::O_TAPS;
+    double* sI = sm + Lay::O_I;
+    double* sMu = sm + Lay::O_MU;
+    double* sG = sm + Lay::O_G;
+    double* sS = sm + Lay::O_S;
+    double* sM = sm + Lay::O_M;
+    double* sq = sm + Lay::O_Q;
+    double* sU = sm + Lay::O_U;
+    const double* tp = taps + static_cast<size_t>(scene) * n * n;
+    {
+        const double* I = guide + scene * P;
+        const double* MU = wmu + scene * P;
+        const double* GK = wg + scene * P;
+        if (N_ == 0)
+            for (int e = threadIdx.x; e < n * n; e += NT) sk[e] = tp[e];
+        constexpr int KI = (WI * WI + NT - 1) / NT, KK = (WK * WK + NT - 1) / NT;
+        double vi[KI], vm[KK], vg[KK];
+#pragma unroll
+        for (int k = 0; k < KI; ++k) {
+            const int e = threadIdx.x + k * NT;
+            const int y = e / WI, x = e - y * WI;
+            if (e < WI * WI) vi[k] = __ldg(I + static_cast<size_t>(wrap_once(r0 - 3 + y, H)) * W + wrap_once(c0 - 3 + x, W));
+        }
+#pragma unroll
+        for (int k = 0; k < KK; ++k) {
+            const int e = threadIdx.x + k * NT;
+            const int y = e / WK, x = e - y * WK;
+            const size_t gi = static_cast<size_t>(wrap_once(r0 - 2 + y, H)) * W + wrap_once(c0 - 2 + x, W);
+            if (e < WK * WK) {
+                vm[k] = __ldg(MU + gi);
+                vg[k] = __ldg(GK + gi);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < KI; ++k)
+            if (threadIdx.x + k * NT < WI * WI) sI[threadIdx.x + k * NT] = vi[k];
+#pragma unroll
+        for (int k = 0; k < KK; ++k)
+            if (threadIdx.x + k * NT < WK * WK) {
+                sMu[threadIdx.x + k * NT] = vm[k];
+                sG[threadIdx.x + k * NT] = vg[k];
+            }
+    }
+    // data-term work item: (cell column, 4-cell row block, sampling phase)
+    constexpr int CW = TA / CF, RB = CW / 4;
+    const int it_J = threadIdx.x % CW;
+    const int it_rest = threadIdx.x / CW;
+    const int it_B = it_rest % RB;
+    const int it_ph = it_rest / RB;
+    const int pr = it_ph / CF, pc = it_ph - pr * CF;
+    using D = a3::DT<(N_ > 0 ? N_ : 1), CF>;
+    constexpr int DM = N_ > 0 ? D::DM : 1;
+    double kreg[DM][DM];
+    if (N_ > 0) {
+#pragma unroll
+        for (int a = 0; a < DM; ++a)
+#pragma unroll
+            for (int b = 0; b < DM; ++b) {
+                const int tr = CF * (a + D::DLO) - pr + D::C, tc = CF * (b + D::DLO) - pc + D::C;
+                kreg[a][b] = (tr >= 0 && tr < N_ && tc >= 0 && tc < N_) ? __ldg(tp + tr * N_ + tc) : 0.0;
+            }
+    }
+    const int iq0 = floordiv(r0 - C + CF - 1, CF), jq0 = floordiv(c0 - C + CF - 1, CF);
+    const int QH = floordiv(r0 + TA - 1 + C, CF) - iq0 + 1, QW = floordiv(c0 + TA - 1 + C, CF) - jq0 + 1;
+    const int dilo = floordiv(pr - C + CF - 1, CF), dihi = floordiv(pr + C, CF);
+    const int djlo = floordiv(pc - C + CF - 1, CF), djhi = floordiv(pc + C, CF);
+    // micro-tile coordinates (2 rows x 4 cols per thread)
+    const int mt_y = 2 * (threadIdx.x / 10), mt_x = 4 * (threadIdx.x % 10);
+
+    for (int chl = 0; chl < G.cps; ++chl) {
+        const int ch = scene * G.cps + chl;
+        if (CG && st[ch].done) continue;
+        const double* p = pin + ch * P;
+        if (CG) p = pin + (static_cast<size_t>(st[ch].t & 1) * G.N + ch) * P;
+        const double* qc = q + static_cast<size_t>(ch) * G.h * G.w;
+        __syncthreads();  // previous channel finished with the shared buffers
+        double* sP = sU;
+        {
+            constexpr int KP = (WP * WP + NT - 1) / NT;
+            double v[KP];
+#pragma unroll
+            for (int k = 0; k < KP; ++k) {
+                const int e = threadIdx.x + k * NT;
+                const int y = e / WP, x = e - y * WP;
+                if (e < WP * WP)
+                    v[k] = __ldg(p + static_cast<size_t>(wrap_once(r0 - 4 + y, H)) * W + wrap_once(c0 - 4 + x, W));
+            }
+#pragma unroll
+            for (int k = 0; k < KP; ++k)
+                if (threadIdx.x + k * NT < WP * WP) sP[threadIdx.x + k * NT] = v[k];
+        }
+        for (int e = threadIdx.x; e < QH * QW; e += NT) {
+            const int a = e / QW, b = e - a * QW;
+            sq[e] = __ldg(qc + static_cast<size_t>(wrapi(iq0 + a, G.h)) * G.w + wrapi(jq0 + b, G.w));
+        }
+        __syncthreads();
+        // own pixels' p for p.Ap, in the S5 mapping (row tid/8, columns 4 (tid%8) + j)
+        double pown[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) pown[j] = sP[(threadIdx.x / 8 + 4) * WP + 4 * (threadIdx.x % 8) + j + 4];
+        // S1: s = L p on R+3 (micro-tile 2 x 4; 19 x 10 tiles)
+        if (threadIdx.x < 190) {
+            double pv[4][6];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 6; ++j) pv[i][j] = sP[(mt_y + i) * WP + mt_x + j];
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int y = mt_y + i, x = mt_x + j;
+                    if (y < WI && x < WI)  // ops.cpp:70-78 stencil order
+                        sS[y * WI + x] = 4.0 * pv[i + 1][j + 1] - pv[i][j + 1] - pv[i + 2][j + 1] - pv[i + 1][j] -
+                                         pv[i + 1][j + 2];
+                }
+        }
+        __syncthreads();
+        // S2: per-window a_k, c1_k on R+2 (micro-tile 2 x 4; 18 x 9 tiles)
+        double* sA = sU;
+        double* sC = sU + WK * WK;
+        if (threadIdx.x < 162) {
+            const int wy = 2 * (threadIdx.x / 9), wx = 4 * (threadIdx.x % 9);
+            double hs[4][4], hi[4][4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                double sv[6], iv[6];
+#pragma unroll
+                for (int j = 0; j < 6; ++j) {
+                    const int o = (wy + i) * WI + wx + j;
+                    sv[j] = (wy + i < WI && wx + j < WI) ? sS[o] : 0.0;
+                    iv[j] = (wy + i < WI && wx + j < WI) ? sI[o] * sv[j] : 0.0;
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    hs[i][j] = sv[j] + sv[j + 1] + sv[j + 2];
+                    hi[i][j] = iv[j] + iv[j + 1] + iv[j + 2];
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int y = wy + i, x = wx + j;
+                    if (y < WK && x < WK) {
+                        const double ss = hs[i][j] + hs[i + 1][j] + hs[i + 2][j];
+                        const double sis = hi[i][j] + hi[i + 1][j] + hi[i + 2][j];
+                        const double mu = sMu[y * WK + x], g = sG[y * WK + x];
+                        const double xb = ss / 9.0;
+                        const double a = g * (sis / 9.0 - mu * xb);
+                        sA[y * WK + x] = a;
+                        sC[y * WK + x] = g != 0.0 ? xb - mu * a : 0.0;
+                    }
+                }
+        }
+        __syncthreads();
+        // S3: M s on R+1 = n_m s_m - box(c1) - I_m box(a) (micro-tile 2 x 4; 17 x 9 tiles)
+        if (threadIdx.x < 153) {
+            const int my = 2 * (threadIdx.x / 9), mx = 4 * (threadIdx.x % 9);
+            double ha[4][4], hc[4][4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                double av[6], cv[6];
+#pragma unroll
+                for (int j = 0; j < 6; ++j) {
+                    const int o = (my + i) * WK + mx + j;
+                    const bool ok = my + i < WK && mx + j < WK;
+                    av[j] = ok ? sA[o] : 0.0;
+                    cv[j] = ok ? sC[o] : 0.0;
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    ha[i][j] = av[j] + av[j + 1] + av[j + 2];
+                    hc[i][j] = cv[j] + cv[j + 1] + cv[j + 2];
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int y = my + i;
+                const int gr = wrap_once(r0 - 1 + y, H);
+                const int nr = max(min(gr + 1, H - 2) - max(gr - 1, 1) + 1, 0);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int x = mx + j;
+                    if (y < WM && x < WM) {
+                        const double ba = ha[i][j] + ha[i + 1][j] + ha[i + 2][j];
+                        const double bc = hc[i][j] + hc[i + 1][j] + hc[i + 2][j];
+                        const int gc = wrap_once(c0 - 1 + x, W);
+                        const int nc = max(min(gc + 1, W - 2) - max(gc - 1, 1) + 1, 0);
+                        const int si = (y + 2) * WI + x + 2;
+                        sM[y * WM + x] = static_cast<double>(nr * nc) * sS[si] - bc - sI[si] * ba;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        // S4: data term per sampling phase -> sO (4 cells along rows per thread)
+        double* sO = sU;
+        {
+            const int Jc = it_J, Ic0 = it_B * 4;
+            const int qj0 = c0 / CF + Jc - jq0, qi0 = r0 / CF + Ic0 - iq0;
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            if (N_ > 0) {
+#pragma unroll
+                for (int m = 0; m < DM + 3; ++m) {
+                    double qv[DM];
+                    const double* qrow = sq + (qi0 + D::DLO + m) * QW + qj0 + D::DLO;
+#pragma unroll
+                    for (int b = 0; b < DM; ++b) qv[b] = qrow[b];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int a = m - k;
+                        if (a >= 0 && a < DM) {
+#pragma unroll
+                            for (int b = 0; b < DM; ++b) acc[k] = fma(kreg[a][b], qv[b], acc[k]);
+                        }
+                    }
+                }
+            } else {
+                for (int di = dilo; di <= dihi; ++di) {
+                    const double* krow = sk + (CF * di - pr + C) * n + C - pc;
+                    for (int dj = djlo; dj <= djhi; ++dj) {
+                        const double kv = krow[CF * dj];
+                        const double* qq = sq + (qi0 + di) * QW + qj0 + dj;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) acc[k] = fma(kv, qq[k * QW], acc[k]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) sO[((Ic0 + k) * CF + pr) * TA + Jc * CF + pc] = acc[k];
+        }
+        __syncthreads();
+        // S5: t = L(M s), Ap = data + lambda t, p.Ap (1 x 4 per thread)
+        double* oc = out + ch * P;
+        double dotp = 0.0;
+        {
+            const int y = threadIdx.x / 8, x0 = 4 * (threadIdx.x % 8);
+            double mv[3][6];
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+#pragma unroll
+                for (int j = 0; j < 6; ++j) mv[i][j] = sM[(y + i) * WM + x0 + j];
+            const int R = r0 + y;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const double tl = 4.0 * mv[1][j + 1] - mv[0][j + 1] - mv[2][j + 1] - mv[1][j] - mv[1][j + 2];
+                const double val = sO[y * TA + x0 + j] + tl * G.lambda;
+                const int Cc = c0 + x0 + j;
+                if (R < H && Cc < W) {
+                    oc[static_cast<size_t>(R) * W + Cc] = val;
+                    dotp += pown[j] * val;
+                }
+            }
+        }
+        if (CG) {
+            const double bs = block_sum<NT>(dotp, red);
+            if (threadIdx.x == 0) part[static_cast<size_t>(ch) * nblk + blockIdx.x] = bs;
+            if (elect_last_block(&st[ch].cnt_a, nblk)) {
+                const double pAp = sum_partials<NT>(part + static_cast<size_t>(ch) * nblk, nblk, 1, red);
+                if (threadIdx.x == 0) {
+                    CgState& S = st[ch];
+                    S.pAp = pAp;
+                    if (!(pAp > 0)) {  // pansharpen.cpp:240-244
+                        S.done = (sqrt(S.rs) <= 1e-12 * S.rhs_norm) ? 1 : 2;
+                        S.iters = S.t + 1;
+                    } else {
+                        S.alpha = S.rs / pAp;
+                    }
+                    S.cnt_a = 0;
+                }
+            }
+        }
+    }
+}
+
+
+// ------------------------------------------------------------------------------------------
+// K_A4: K_A3 with conflict-free column strips. Every stage maps lanes to consecutive columns
+// and walks a strip of rows with the vertical 3-sums in a register sliding window, so each
+// shared load is a stride-1 (conflict-free) warp access and reused vertically.
+// ------------------------------------------------------------------------------------------
+namespace a4 {
+constexpr int TA = 32;
+constexpr int WP = TA + 8, WI = TA + 6, WK = TA + 4, WM = TA + 2;
+// stage strips: (columns, strips, rows per strip)
+constexpr int S1_COLS = WI, S1_STRIPS = 6, S1_ROWS = (WI + S1_STRIPS - 1) / S1_STRIPS;   // 38 x 6 x 7
+constexpr int S2_COLS = WK, S2_STRIPS = 6, S2_ROWS = (WK + S2_STRIPS - 1) / S2_STRIPS;   // 36 x 6 x 6
+constexpr int S3_COLS = WM, S3_STRIPS = 7, S3_ROWS = (WM + S3_STRIPS - 1) / S3_STRIPS;   // 34 x 7 x 5
+constexpr int S5_COLS = TA, S5_STRIPS = 8, S5_ROWS = TA / S5_STRIPS;                     // 32 x 8 x 4
+static_assert(S1_COLS * S1_STRIPS <= NT && S2_COLS * S2_STRIPS <= NT && S3_COLS * S3_STRIPS <= NT, "strips");
+template <int CF>
+struct L {
+    static constexpr int QMAX = a2::maxq(CF);
+    static constexpr int O_TAPS = 0;
+    static constexpr int O_I = O_TAPS + a2::MAXTAP;        // guide on R+3
+    static constexpr int O_MU = O_I + WI * WI;             // mu_k on R+2
+    static constexpr int O_G = O_MU + WK * WK;             // g_k on R+2
+    static constexpr int O_S = O_G + WK * WK;              // s on R+3
+    static constexpr int O_M = O_S + WI * WI;              // I*s on R+3, then M s on R+1
+    static constexpr int O_Q = O_M + WI * WI;              // q window
+    static constexpr int QWMAX = (TA - 1 + 2 * (a2::MAXN / 2)) / CF + 2;
+    static constexpr int QWP = QWMAX + ((8 - QWMAX % 16) + 16) % 16;   // row stride == 8 (mod 16)
+    static constexpr int O_U = O_Q + QWP * QWMAX;          // p on R+4 -> (a, c1) on R+2
+    static constexpr int U_SIZE = 2 * WK * WK;
+    static constexpr int O_O = O_U + U_SIZE;               // data term out (TA x TA)
+    static constexpr int TOTAL = O_O + TA * TA;
+    static_assert(U_SIZE >= WP * WP, "union too small");
+    static constexpr size_t smem = TOTAL * sizeof(double);
+};
+}  // namespace a4
+
+template <bool CG, int N_, int CF>
+__global__ void __launch_bounds__(NT, 2) k_apply4(PsGeo G, const double* __restrict__ taps,
+                                                  const double* __restrict__ guide, const double* __restrict__ wmu,
+                                                  const double* __restrict__ wg, const double* __restrict__ pin,
+                                                  const double* __restrict__ q, double* __restrict__ out, CgState* st,
+                                                  double* __restrict__ part, int nblk) {
+    using namespace a4;
+    using Lay = a4::L<CF>;
+    __shared__ double red[NT / 32 + 1];
+    extern __shared__ double sm[];
+    // blockIdx.y = scene * cgroups + group: the CTA handles channels [group*cpc, group*cpc+cpc)
+    const int cgroups = (G.cps + G.cpc - 1) / G.cpc;
+    const int scene = blockIdx.y / cgroups, group = blockIdx.y - scene * cgroups;
+    const int H = G.H, W = G.W, n = G.n, C = G.C;
+    const size_t P = static_cast<size_t>(H) * W;
+    const int ntx = (W + TA - 1) / TA;
+    const int by = blockIdx.x / ntx, bx = blockIdx.x - by * ntx;
+    const int r0 = by * TA, c0 = bx * TA;
+    double* sk = sm + Lay::O_TAPS;
+    double* sI = sm + Lay::O_I;
+    double* sMu = sm + Lay::O_MU;
+    double* sG = sm + Lay::O_G;
+    double* sS = sm + Lay::O_S;
+    double* sIS = sm + Lay::O_M;
+    double* sM = sm + Lay::O_M;
+    double* sq = sm + Lay::O_Q;
+    double* sU = sm + Lay::O_U;
+    const double* tp = taps + static_cast<size_t>(scene) * n * n;
+    // data term: output u = 128 warp + 32 k + lane (k = 0..3) -> (sampling phase, cell); the
+    // phase is uniform across a warp, so taps are broadcast reads
+    constexpr int CPR = TA / CF, CPP = CPR * CPR;  // cells per row / per phase
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int iq0 = floordiv(r0 - C + CF - 1, CF), jq0 = floordiv(c0 - C + CF - 1, CF);
+    const int QH = floordiv(r0 + TA - 1 + C, CF) - iq0 + 1, QW = floordiv(c0 + TA - 1 + C, CF) - jq0 + 1;
+    constexpr int QS = Lay::QWP;  // padded row stride of the q window
+    using D = a3::DT<(N_ > 0 ? N_ : 1), CF>;
+    constexpr int DM = N_ > 0 ? D::DM : 1;
+    const int ch_lo = group * G.cpc, ch_hi = min(G.cps, group * G.cpc + G.cpc);
+    constexpr int KP = (WP * WP + NT - 1) / NT;
+    const int QN = QH * QW;
+    constexpr int KQ = (Lay::QWMAX * Lay::QWMAX + NT - 1) / NT;
+    double pf_p[KP], pf_q[KQ];
+    // issue the loads of channel `chl`'s p (R+4) and q windows into registers
+    auto prefetch = [&](int chl) {
+        const int ch = scene * G.cps + chl;
+        const double* pp = pin + ch * P;
+        if (CG) pp = pin + (static_cast<size_t>(st[ch].t & 1) * G.N + ch) * P;
+        const double* qc = q + static_cast<size_t>(ch) * G.h * G.w;
+#pragma unroll
+        for (int k = 0; k < KP; ++k) {
+            const int e = threadIdx.x + k * NT;
+            const int y = e / WP, x = e - y * WP;
+            pf_p[k] = 0.0;
+            if (e < WP * WP && !(G.dbg & 32))
+                pf_p[k] = __ldg(pp + static_cast<size_t>(wrap_once(r0 - 4 + y, H)) * W + wrap_once(c0 - 4 + x, W));
+        }
+#pragma unroll
+        for (int k = 0; k < KQ; ++k) {
+            const int e = threadIdx.x + k * NT;
+            if (e < QN) {
+                const int a = e / QW, b = e - a * QW;
+                pf_q[k] = __ldg(qc + static_cast<size_t>(wrapi(iq0 + a, G.h)) * G.w + wrapi(jq0 + b, G.w));
+            }
+        }
+    };
+    auto next_active = [&](int chl) {
+        while (chl < ch_hi && CG && st[scene * G.cps + chl].done) ++chl;
+        return chl;
+    };
+    const double* I = guide + scene * P;
+    const double* MU = wmu + scene * P;
+    const double* GK = wg + scene * P;
+    for (int e = threadIdx.x; e < n * n; e += NT) sk[e] = tp[e];
+    constexpr int KI = (WI * WI + NT - 1) / NT, KK = (WK * WK + NT - 1) / NT;
+    double vi[KI], vm[KK], vg[KK];
+#pragma unroll
+    for (int k = 0; k < KI; ++k) {
+        const int e = threadIdx.x + k * NT;
+        const int y = e / WI, x = e - y * WI;
+        if (e < WI * WI) vi[k] = __ldg(I + static_cast<size_t>(wrap_once(r0 - 3 + y, H)) * W + wrap_once(c0 - 3 + x, W));
+    }
+#pragma unroll
+    for (int k = 0; k < KK; ++k) {
+        const int e = threadIdx.x + k * NT;
+        const int y = e / WK, x = e - y * WK;
+        const size_t gi = static_cast<size_t>(wrap_once(r0 - 2 + y, H)) * W + wrap_once(c0 - 2 + x, W);
+        if (e < WK * WK) {
+            vm[k] = __ldg(MU + gi);
+            vg[k] = __ldg(GK + gi);
+        }
+    }
+    int cur = next_active(ch_lo);
+    if (cur < ch_hi) prefetch(cur);  // first channel's p / q in flight with the guide tile
+#pragma unroll
+    for (int k = 0; k < KI; ++k)
+        if (threadIdx.x + k * NT < WI * WI) sI[threadIdx.x + k * NT] = vi[k];
+#pragma unroll
+    for (int k = 0; k < KK; ++k)
+        if (threadIdx.x + k * NT < WK * WK) {
+            sMu[threadIdx.x + k * NT] = vm[k];
+            sG[threadIdx.x + k * NT] = vg[k];
+        }
+
+    for (int chl = cur; chl < ch_hi; chl = cur) {
+        const int ch = scene * G.cps + chl;
+        __syncthreads();  // previous channel finished with the shared buffers
+        double* sP = sU;
+#pragma unroll
+        for (int k = 0; k < KP; ++k)
+            if (threadIdx.x + k * NT < WP * WP) sP[threadIdx.x + k * NT] = pf_p[k];
+#pragma unroll
+        for (int k = 0; k < KQ; ++k) {
+            const int e = threadIdx.x + k * NT;
+            if (e < QN) {
+                const int a = e / QW, b = e - a * QW;
+                sq[a * QS + b] = pf_q[k];
+            }
+        }
+        cur = next_active(chl + 1);
+        if (cur < ch_hi) prefetch(cur);  // in flight during this channel's stages
+        __syncthreads();
+        // own pixels' p for p.Ap in the S5 mapping (column tid % 32, rows 4 (tid / 32) + i)
+        double pown[S5_ROWS];
+#pragma unroll
+        for (int i = 0; i < S5_ROWS; ++i)
+            pown[i] = sP[(S5_ROWS * (threadIdx.x / S5_COLS) + i + 4) * WP + (threadIdx.x % S5_COLS) + 4];
+        // S4: data term (needs only q; writes its own buffer, so it runs before S1 without a barrier)
+        double* sO = sm + Lay::O_O;
+        if (N_ > 0 && !(G.dbg & 1)) {
+            // thread = (phase, cell column, 4 cell rows); zero-padded phase sub-kernel in registers,
+            // q rows slide through registers (each q value loaded once per thread)
+            constexpr int CW4 = TA / CF, RB4 = CW4 / 4;
+            const int Jc = threadIdx.x % CW4;
+            const int rest = threadIdx.x / CW4;
+            const int Ic0 = (rest % RB4) * 4;
+            const int ph = rest / RB4;
+            const int pr = ph / CF, pc = ph - pr * CF;
+            double kreg[DM][DM];
+#pragma unroll
+            for (int a = 0; a < DM; ++a)
+#pragma unroll
+                for (int b = 0; b < DM; ++b) {
+                    const int tr = CF * (a + D::DLO) - pr + D::C, tc = CF * (b + D::DLO) - pc + D::C;
+                    kreg[a][b] = (tr >= 0 && tr < N_ && tc >= 0 && tc < N_) ? sk[tr * N_ + tc] : 0.0;
+                }
+            const double* qb = sq + (r0 / CF + Ic0 - iq0 + D::DLO) * QS + (c0 / CF + Jc - jq0 + D::DLO);
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int m = 0; m < DM + 3; ++m) {
+                double qv[DM];
+#pragma unroll
+                for (int b = 0; b < DM; ++b) qv[b] = qb[m * QS + b];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int a = m - k;
+                    if (a >= 0 && a < DM) {
+#pragma unroll
+                        for (int b = 0; b < DM; ++b) acc[k] = fma(kreg[a][b], qv[b], acc[k]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) sO[((Ic0 + k) * CF + pr) * TA + Jc * CF + pc] = acc[k];
+        } else if (!(G.dbg & 1)) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int u = 128 * warp + 32 * k + lane;
+                const int ph = u / CPP, cell = u - ph * CPP;
+                const int pr = ph / CF, pc = ph - pr * CF;
+                const int ci = cell / CPR, cj = cell - ci * CPR;
+                const int dilo = floordiv(pr - C + CF - 1, CF), dihi = floordiv(pr + C, CF);
+                const int djlo = floordiv(pc - C + CF - 1, CF), djhi = floordiv(pc + C, CF);
+                const double* qb = sq + (r0 / CF + ci - iq0) * QS + (c0 / CF + cj - jq0);
+                double acc = 0.0;
+                for (int di = dilo; di <= dihi; ++di) {
+                    const double* krow = sk + (CF * di - pr + C) * n + C - pc;
+                    const double* qrow = qb + di * QS;
+                    for (int dj = djlo; dj <= djhi; ++dj) acc = fma(krow[CF * dj], qrow[dj], acc);
+                }
+                sO[(ci * CF + pr) * TA + cj * CF + pc] = acc;
+            }
+        }
+        // S1: s = L p and I*s on R+3; column strips, vertical sliding window of p's centre column
+        if (threadIdx.x < S1_COLS * S1_STRIPS && !(G.dbg & 2)) {
+            const int x = threadIdx.x % S1_COLS, y0 = S1_ROWS * (threadIdx.x / S1_COLS);
+            double up = sP[y0 * WP + x + 1], mid = sP[(y0 + 1) * WP + x + 1];
+#pragma unroll
+            for (int i = 0; i < S1_ROWS; ++i) {
+                const int y = y0 + i;
+                if (y < WI) {
+                    const double dn = sP[(y + 2) * WP + x + 1];
+                    const double v = 4.0 * mid - up - dn - sP[(y + 1) * WP + x] - sP[(y + 1) * WP + x + 2];
+                    sS[y * WI + x] = v;
+                    sIS[y * WI + x] = sI[y * WI + x] * v;
+                    up = mid;
+                    mid = dn;
+                }
+            }
+        }
+        __syncthreads();
+        // S2: per-window a_k, c1_k on R+2 from 3x3 sums of s and I*s
+        double* sA = sU;
+        double* sC = sU + WK * WK;
+        if (threadIdx.x < S2_COLS * S2_STRIPS && !(G.dbg & 4)) {
+            const int x = threadIdx.x % S2_COLS, y0 = S2_ROWS * (threadIdx.x / S2_COLS);
+            auto hrow = [&](const double* a, int y) { return a[y * WI + x] + a[y * WI + x + 1] + a[y * WI + x + 2]; };
+            double s0 = hrow(sS, y0), s1 = hrow(sS, y0 + 1);
+            double i0 = hrow(sIS, y0), i1 = hrow(sIS, y0 + 1);
+#pragma unroll
+            for (int i = 0; i < S2_ROWS; ++i) {
+                const int y = y0 + i;
+                if (y < WK) {
+                    const double s2 = hrow(sS, y + 2), i2 = hrow(sIS, y + 2);
+                    const double ss = s0 + s1 + s2, sis = i0 + i1 + i2;
+                    const double mu = sMu[y * WK + x], g = sG[y * WK + x];
+                    const double xb = ss * (1.0 / 9.0);  // box mean (fp64 division avoided)
+                    const double a = g * (sis * (1.0 / 9.0) - mu * xb);
+                    sA[y * WK + x] = a;
+                    sC[y * WK + x] = g != 0.0 ? xb - mu * a : 0.0;
+                    s0 = s1; s1 = s2; i0 = i1; i1 = i2;
+                }
+            }
+        }
+        __syncthreads();
+        // S3: M s on R+1 = n_m s_m - box(c1) - I_m box(a)
+        if (threadIdx.x < S3_COLS * S3_STRIPS && !(G.dbg & 8)) {
+            const int x = threadIdx.x % S3_COLS, y0 = S3_ROWS * (threadIdx.x / S3_COLS);
+            auto hrow = [&](const double* a, int y) { return a[y * WK + x] + a[y * WK + x + 1] + a[y * WK + x + 2]; };
+            double a0 = hrow(sA, y0), a1 = hrow(sA, y0 + 1);
+            double k0 = hrow(sC, y0), k1 = hrow(sC, y0 + 1);
+            const int gc = wrap_once(c0 - 1 + x, W);
+            const int nc = max(min(gc + 1, W - 2) - max(gc - 1, 1) + 1, 0);
+            double mres[S3_ROWS];
+#pragma unroll
+            for (int i = 0; i < S3_ROWS; ++i) {
+                const int y = y0 + i;
+                mres[i] = 0.0;
+                if (y < WM) {
+                    const double a2v = hrow(sA, y + 2), k2 = hrow(sC, y + 2);
+                    const double ba = a0 + a1 + a2v, bc = k0 + k1 + k2;
+                    const int gr = wrap_once(r0 - 1 + y, H);
+                    const int nr = max(min(gr + 1, H - 2) - max(gr - 1, 1) + 1, 0);
+                    const int si = (y + 2) * WI + x + 2;
+                    mres[i] = static_cast<double>(nr * nc) * sS[si] - bc - sI[si] * ba;
+                    a0 = a1; a1 = a2v; k0 = k1; k1 = k2;
+                }
+            }
+            // sM aliases I*s (dead after S2, not read in this stage)
+#pragma unroll
+            for (int i = 0; i < S3_ROWS; ++i)
+                if (y0 + i < WM) sM[(y0 + i) * WM + x] = mres[i];
+        }
+        __syncthreads();
+        // S5: t = L(M s), Ap = data + lambda t, p.Ap (column strips of 4 rows)
+        double* oc = out + ch * P;
+        double dotp = 0.0;
+        if (!(G.dbg & 16)) {
+            const int x = threadIdx.x % S5_COLS, y0 = S5_ROWS * (threadIdx.x / S5_COLS);
+            double up = sM[y0 * WM + x + 1], mid = sM[(y0 + 1) * WM + x + 1];
+            const int Cc = c0 + x;
+#pragma unroll
+            for (int i = 0; i < S5_ROWS; ++i) {
+                const int y = y0 + i;
+                const double dn = sM[(y + 2) * WM + x + 1];
+                const double tl = 4.0 * mid - up - dn - sM[(y + 1) * WM + x] - sM[(y + 1) * WM + x + 2];
+                const double val = sO[y * TA + x] + tl * G.lambda;
+                up = mid;
+                mid = dn;
+                const int R = r0 + y;
+                if (R < H && Cc < W) {
+                    oc[static_cast<size_t>(R) * W + Cc] = val;
+                    dotp += pown[i] * val;
+                }
+            }
+        }
+        if (CG) {
+            const double bs = block_sum<NT>(dotp, red);
+            if (threadIdx.x == 0) part[static_cast<size_t>(ch) * nblk + blockIdx.x] = bs;
+            if (elect_last_block(&st[ch].cnt_a, nblk)) {
+                const double pAp = sum_partials<NT>(part + static_cast<size_t>(ch) * nblk, nblk, 1, red);
+                if (threadIdx.x == 0) {
+                    CgState& S = st[ch];
+                    S.pAp = pAp;
+                    if (!(pAp > 0)) {  // pansharpen.cpp:240-244
+                        S.done = (sqrt(S.rs) <= 1e-12 * S.rhs_norm) ? 1 : 2;
+                        S.iters = S.t + 1;
+                    } else {
+                        S.alpha = S.rs / pAp;
+                    }
+                    S.cnt_a = 0;
+                }
+            }
+        }
+    }
+}
+
 }  // namespace fast
 }  // namespace fbmp_gpu

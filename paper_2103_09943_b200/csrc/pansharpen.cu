@@ -20,6 +20,10 @@ PsGeo make_geo(int N, int h, int w, int c, int n, int rw, double lambda, double 
     PsGeo G;
     G.N = N;
     G.cps = cps > 0 ? cps : N;
+    const char* env = std::getenv("FBMP_KA_CPC");
+    G.cpc = env ? std::max(1, std::atoi(env)) : G.cps;
+    const char* dbg = std::getenv("FBMP_KA_DBG");
+    G.dbg = dbg ? std::atoi(dbg) : 0;
     G.h = h; G.w = w; G.c = c;
     G.H = h * c; G.W = w * c;
     G.n = n; G.C = (n - 1) / 2;
@@ -915,32 +919,39 @@ void guide_stats(Context& ctx, const PsGeo& G, const double* d_guide, double* mu
     check_launch();
 }
 
+using AFn = void (*)(PsGeo, const double*, const double*, const double*, const double*, const double*,
+                     const double*, double*, CgState*, double*, int);
+template <bool CG>
+std::pair<AFn, size_t> apply3_select(const PsGeo& G) {
+    if (G.c == 4) {
+        const size_t sm = fast::a4::L<4>::smem;
+        switch (G.n) {
+        case 21: return {fast::k_apply4<CG, 21, 4>, sm};
+        case 17: return {fast::k_apply4<CG, 17, 4>, sm};
+        case 15: return {fast::k_apply4<CG, 15, 4>, sm};
+        case 7: return {fast::k_apply4<CG, 7, 4>, sm};
+        default: return {fast::k_apply4<CG, 0, 4>, sm};
+        }
+    }
+    if (G.c == 2) return {fast::k_apply4<CG, 0, 2>, fast::a4::L<2>::smem};
+    return {fast::k_apply4<CG, 0, 1>, fast::a4::L<1>::smem};
+}
+
 template <bool CG>
 void launch_apply2(Context& ctx, const PsGeo& G, const double* taps, const double* guide, const double* mu,
                    const double* gk, const double* p, const double* q, double* out, CgState* st, double* part) {
     const int S = (G.N + G.cps - 1) / G.cps;
-    const int nba = ceil_div(G.W, fast::a2::TA) * ceil_div(G.H, fast::a2::TA);
-    switch (G.c) {
-    case 1:
-        fast::k_apply2<CG, 1><<<dim3(nba, S), fast::NT, fast::a2::L<1>::smem, ctx.stream>>>(G, taps, guide, mu, gk, p,
-                                                                                           q, out, st, part, nba);
-        break;
-    case 2:
-        fast::k_apply2<CG, 2><<<dim3(nba, S), fast::NT, fast::a2::L<2>::smem, ctx.stream>>>(G, taps, guide, mu, gk, p,
-                                                                                           q, out, st, part, nba);
-        break;
-    default:
-        fast::k_apply2<CG, 4><<<dim3(nba, S), fast::NT, fast::a2::L<4>::smem, ctx.stream>>>(G, taps, guide, mu, gk, p,
-                                                                                           q, out, st, part, nba);
-        break;
-    }
+    const int nba = ceil_div(G.W, fast::a4::TA) * ceil_div(G.H, fast::a4::TA);
+    const int groups = (G.cps + G.cpc - 1) / G.cpc;
+    const auto fs = apply3_select<CG>(G);
+    fs.first<<<dim3(nba, S * groups), fast::NT, fs.second, ctx.stream>>>(G, taps, guide, mu, gk, p, q, out, st, part,
+                                                                          nba);
 }
 
 template <bool CG>
-void prepare_apply2() {
-    set_smem(fast::k_apply2<CG, 1>, fast::a2::L<1>::smem);
-    set_smem(fast::k_apply2<CG, 2>, fast::a2::L<2>::smem);
-    set_smem(fast::k_apply2<CG, 4>, fast::a2::L<4>::smem);
+void prepare_apply2(const PsGeo& G) {
+    const auto fs = apply3_select<CG>(G);
+    set_smem(fs.first, fs.second);
 }
 
 // =============================================================================================
@@ -982,7 +993,7 @@ void cg_operator_apply(Context& ctx, const PsGeo& G, const double* d_taps, const
         double* mu = ctx.scratch<double>("op_wmu", P * S);
         double* gk = ctx.scratch<double>("op_wg", P * S);
         guide_stats(ctx, G, d_guide, mu, gk);
-        prepare_apply2<false>();
+        prepare_apply2<false>(G);
         launch_apply2<false>(ctx, G, d_taps, d_guide, mu, gk, d_p, q, d_out, nullptr, nullptr);
         ctx.count();
         check_launch();
@@ -1018,7 +1029,7 @@ void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* 
     if (!fastA) check_smem(sa, "warmstart");
     if (q2.fn) set_smem(q2.fn, q2.smem);
     else set_smem(k_q<true>, sq);
-    if (fastA) prepare_apply2<true>();
+    if (fastA) prepare_apply2<true>(G);
     else set_smem(k_apply<0, true>, sa);
     set_smem(k_rhs<true>, sr);
     double* wmu = nullptr;

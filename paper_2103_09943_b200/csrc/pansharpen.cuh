@@ -28,6 +28,8 @@ struct PsGeo {
     int N;                        // channels in the launch (all scenes)
     int cps;                      // channels per scene: channel ch uses scene ch / cps's
                                   // taps, guide and intensity scale
+    int cpc;                      // channels per CTA in the fast K_A (guide tile reuse)
+    int dbg;                      // development: bitmask of K_A stages to skip (timing only)
 };
 
 PsGeo make_geo(int N, int h, int w, int c, int n, int rw, double lambda, double eps, int cps = 0);

@@ -135,6 +135,13 @@ int fbmp_gpu_blind_dev(fbmp_gpu_ctx* ctx, const double* d_lrms, int N, int h, in
                        const fbmp_sw_params* sw, const fbmp_ke_params* ke, const fbmp_ps_params* ps,
                        double* d_out, double* d_k_out);
 
+/* Channel-sharded blind solve (BASELINE config C3, one rank per GPU): the spectral weights,
+ * the kernel fit and the intensity normalisation use all N bands (replicated on every rank,
+ * deterministic), only bands [ch0, ch0+nch) are reconstructed. out: nch*H*W. */
+int fbmp_gpu_blind_subset(fbmp_gpu_ctx* ctx, const double* lrms, int N, int h, int w, const double* pan,
+                          const fbmp_sw_params* sw, const fbmp_ke_params* ke, const fbmp_ps_params* ps, int ch0,
+                          int nch, double* out, double* k_out);
+
 /* Batch of independent scenes (no reference equivalent; BASELINE config C4): S scenes of
  * identical shape, each with its own weights, kernel fit and HRMS solve. */
 int fbmp_gpu_blind_batch(fbmp_gpu_ctx* ctx, const double* lrms, int S, int N, int h, int w, const double* pan,

@@ -1320,9 +1320,9 @@ int orc_pansharpen(const double* lrms, int N, int h, int w, const double* pan, c
         for (int b = 0; b < N; ++b) cg_iters[b] = it[b];
     });
 }
-int orc_solve_weights(const double* lrms, int nb, int h, int w, const double* pan, int l, double lambda_omega,
-                      int factor, double* omega) {
-    return guard([&] { put(solve_weights(lrms, nb, h, w, pan, h * factor, w * factor, l, lambda_omega, factor), omega); });
+int orc_solve_weights(const double* lrms, int nb, int h, int w, const double* pan, int H, int W, int l,
+                      double lambda_omega, int factor, double* omega) {
+    return guard([&] { put(solve_weights(lrms, nb, h, w, pan, H, W, l, lambda_omega, factor), omega); });
 }
 int orc_combine_bands(const double* lrms, int nb, int h, int w, const double* omega, double* out) {
     return guard([&] { put(combine_bands(lrms, nb, static_cast<size_t>(h) * w, omega), out); });
@@ -1428,6 +1428,15 @@ int orc_blind(const double* lrms, int N, int h, int w, const double* pan, int fa
 int orc_blind_sampled(const double* lrms, int N, int h, int w, const double* pan, int factor, int n, int threads,
                       int cg_cap, double* times, int* cg_iters_done, int* admm_iters) {
     return guard([&] { blind_sampled(lrms, N, h, w, pan, factor, n, threads, cg_cap, times, cg_iters_done, admm_iters); });
+}
+
+// E (p x n^2) of ObservationSystem (kernel_estimator.cpp:57-68), for the construction KATs
+int orc_observation_matrix(const double* pan, int H, int W, int factor, int n, double* E) {
+    return guard([&] {
+        std::vector<double> obs(static_cast<size_t>(H / factor) * (W / factor), 0.0);
+        Observation O(pan, H, W, obs.data(), H / factor, W / factor, factor, n, 1.0);
+        put(O.E, E);
+    });
 }
 
 }  // extern "C"

@@ -217,7 +217,8 @@ def solve_weights(lrms, pan, l=4, lambda_omega=10.0, factor=4):
     lrms, pan = _f(lrms), _f(pan)
     nb, h, w = lrms.shape
     om = np.empty(nb)
-    _check(lib().orc_solve_weights(_p(lrms), nb, h, w, _p(pan), l, C.c_double(lambda_omega), factor, _p(om)))
+    _check(lib().orc_solve_weights(_p(lrms), nb, h, w, _p(pan), pan.shape[0], pan.shape[1], l,
+                                   C.c_double(lambda_omega), factor, _p(om)))
     return om
 
 
@@ -332,3 +333,12 @@ def blind_sampled(lrms, pan, factor, n, cg_cap, threads=0):
     _check(lib().orc_blind_sampled(_p(lrms), N, h, w, _p(pan), factor, n, threads, cg_cap, _p(t),
                                    done.ctypes.data_as(I), C.byref(ta)))
     return dict(times=list(t), cg_done=list(done), admm_iters=ta.value)
+
+
+def observation_matrix(pan, factor, n):
+    """E of kernel_estimator.cpp:57-68 (rows = LR pixels, cols = kernel taps)."""
+    pan = _f(pan)
+    p = (pan.shape[0] // factor) * (pan.shape[1] // factor)
+    E = np.empty((p, n * n))
+    _check(lib().orc_observation_matrix(_p(pan), pan.shape[0], pan.shape[1], factor, n, _p(E)))
+    return E

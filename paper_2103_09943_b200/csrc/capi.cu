@@ -59,20 +59,24 @@ static void check_kernel(int n, int H, int W) {
 // channels each: lrms S*N*h*w, pan S*H*W, taps S*n*n, out S*N*H*W.
 void pansharpen_device(Context& ctx, const double* d_lrms, int S, int N, int h, int w, const double* d_pan,
                        const double* d_taps, int n, int c, const fbmp_ps_params& prm, double* d_out,
-                       std::vector<int>& cg_iters) {
+                       std::vector<int>& cg_iters, int ch0 = 0, int nch = -1) {
     validate_ps(prm);
     const int H = h * c, W = w * c;
     if (2 * prm.radius + 1 > std::min(H, W)) dim_error("matting matrix: window larger than image");
     check_kernel(n, H, W);
-    const int NC = S * N;
+    const int NS = nch < 0 ? N : nch;  // channels solved per scene (a subset [ch0, ch0+NS) when S == 1)
+    if (ch0 < 0 || ch0 + NS > N || (S > 1 && NS != N)) param_error("pansharpen: invalid channel subset");
+    const int NC = S * NS;
     const size_t P = static_cast<size_t>(H) * W, p = static_cast<size_t>(h) * w;
-    const PsGeo G = make_geo(NC, h, w, c, n, prm.radius, prm.lambda, prm.eps, N);
+    const PsGeo G = make_geo(NC, h, w, c, n, prm.radius, prm.lambda, prm.eps, NS);
     double* scale = ctx.scratch<double>("ps_scale", S);
     double* lpan = ctx.scratch<double>("ps_lpan", P * S);
     double* xn = ctx.scratch<double>("ps_xn", p * NC);
+    // normalisation over PAN and ALL bands (pansharpen.cpp:374-376), also for a subset solve
     peak_scale(ctx, d_pan, static_cast<long long>(P), d_lrms, static_cast<long long>(p) * N, S, scale);
     laplacian_scaled(ctx, d_pan, H, W, S, scale, lpan);
-    scale_copy(ctx, d_lrms, static_cast<long long>(p) * NC, scale, static_cast<long long>(p) * N, xn);
+    scale_copy(ctx, d_lrms + static_cast<size_t>(ch0) * p, static_cast<long long>(p) * NC, scale,
+               static_cast<long long>(p) * NS, xn);
 
     CgBuffers B;
     B.z = ctx.scratch<double>("cg_z", P * NC);
@@ -88,12 +92,12 @@ void pansharpen_device(Context& ctx, const double* d_lrms, int S, int N, int h, 
     cg_iters.assign(NC, 0);
     for (int i = 0; i < NC; ++i) cg_iters[i] = hs[i].iters;
     for (int i = 0; i < NC; ++i) {  // first failing channel in index order (pansharpen.cpp:421-422)
-        const std::string tag = "channel " + std::to_string(i % N) + ": ";
+        const std::string tag = "channel " + std::to_string(ch0 + i % NS) + ": ";
         if (hs[i].done == 2)
             num_error(tag + "warmstart: conjugate gradients hit a non-positive curvature direction");
         if (hs[i].done == 3) {
             // residual of the normal equations, only for the message (pansharpen.cpp:257-262)
-            const int sc = i / N;
+            const int sc = i / NS;
             double* az = ctx.scratch<double>("cg_res_az", P);
             double* rhs = ctx.scratch<double>("cg_res_rhs", P);
             const PsGeo G1 = make_geo(1, h, w, c, n, prm.radius, prm.lambda, prm.eps);
@@ -110,7 +114,7 @@ void pansharpen_device(Context& ctx, const double* d_lrms, int S, int N, int h, 
         }
     }
     double* v = ctx.scratch<double>("ps_v", P * NC);
-    guided_filter(ctx, NC, H, W, prm.radius, prm.eps, B.z, 1, lpan, nullptr, nullptr, v, N);
+    guided_filter(ctx, NC, H, W, prm.radius, prm.eps, B.z, 1, lpan, nullptr, nullptr, v, NS);
     int* flag = ctx.scratch<int>("ps_flag", NC);
     FBMP_CUDA(cudaMemsetAsync(flag, 0, sizeof(int) * NC, ctx.stream));
     solve_channel_fft(ctx, G, d_taps, xn, v, scale, d_out, flag);
@@ -119,7 +123,7 @@ void pansharpen_device(Context& ctx, const double* d_lrms, int S, int N, int h, 
     FBMP_CUDA(cudaStreamSynchronize(ctx.stream));
     for (int i = 0; i < NC; ++i)
         if (hf[i])
-            num_error("channel " + std::to_string(i % N) +
+            num_error("channel " + std::to_string(ch0 + i % NS) +
                       ": solve_channel_fft: alias-group system condition number exceeds 1e14 (prior transfer "
                       "function too small)");
 }
@@ -128,7 +132,8 @@ void pansharpen_device(Context& ctx, const double* d_lrms, int S, int N, int h, 
 // solve_weights (all bands) -> combine_bands -> estimate_kernel_tgv -> pansharpen.
 void blind_device(Context& ctx, const double* d_lrms, int S, int N, int h, int w, const double* d_pan,
                   const fbmp_sw_params& sw, const fbmp_ke_params& ke, const fbmp_ps_params& ps, double* d_out,
-                  double* d_k, double* d_omega_out, std::vector<int>& admm_iters, std::vector<int>& cg_iters) {
+                  double* d_k, double* d_omega_out, std::vector<int>& admm_iters, std::vector<int>& cg_iters,
+                  int ch0 = 0, int nch = -1) {
     const int c = sw.factor;
     if (c < 1) param_error("solve_weights: factor must be >= 1");
     if (sw.l < 1) param_error("solve_weights: l must be >= 1");
@@ -156,7 +161,7 @@ void blind_device(Context& ctx, const double* d_lrms, int S, int N, int h, int w
     cudaEventRecord(e1, ctx.stream);
     estimate_kernel_device(ctx, d_pan, obs, S, H, W, c, ke, d_k, admm_iters, nullptr, -1);
     cudaEventRecord(e2, ctx.stream);
-    pansharpen_device(ctx, d_lrms, S, N, h, w, d_pan, d_k, ke.n, c, ps, d_out, cg_iters);
+    pansharpen_device(ctx, d_lrms, S, N, h, w, d_pan, d_k, ke.n, c, ps, d_out, cg_iters, ch0, nch);
     cudaEventRecord(e3, ctx.stream);
     cudaEventSynchronize(e3);
     float a = 0, b = 0, d = 0;
@@ -735,6 +740,29 @@ int fbmp_gpu_ctx_kernel_profile(fbmp_gpu_ctx* ctx, double* total_ms, long long* 
         launches[i] = ctx->impl.prof_n[i];
     }
     return FBMP_OK;
+}
+
+int fbmp_gpu_blind_subset(fbmp_gpu_ctx* ctx, const double* lrms, int N, int h, int w, const double* pan,
+                          const fbmp_sw_params* sw, const fbmp_ke_params* ke, const fbmp_ps_params* ps, int ch0,
+                          int nch, double* out, double* k_out) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        const fbmp_sw_params swp = sw_or_default(sw);
+        const fbmp_ke_params kep = ke_or_default(ke);
+        const int c = swp.factor;
+        if (c < 1) param_error("solve_weights: factor must be >= 1");
+        if (ch0 < 0 || nch < 1 || ch0 + nch > N) param_error("blind: invalid channel subset");
+        const size_t p = static_cast<size_t>(h) * w, P = p * c * c;
+        double* d_l = upload(C, "api_lrms", lrms, p * N);
+        double* d_p = upload(C, "api_pan", pan, P);
+        double* d_o = C.scratch<double>("api_out", P * nch);
+        double* d_k = C.scratch<double>("api_k", static_cast<size_t>(kep.n) * kep.n);
+        std::vector<int> ai, ci;
+        blind_device(C, d_l, 1, N, h, w, d_p, swp, kep, ps_or_default(ps), d_o, d_k, nullptr, ai, ci, ch0, nch);
+        download(C, out, d_o, P * nch);
+        if (k_out) download(C, k_out, d_k, static_cast<size_t>(kep.n) * kep.n);
+    });
 }
 
 }  // extern "C"

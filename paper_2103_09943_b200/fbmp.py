@@ -518,6 +518,24 @@ def blind(lrms, pan, factor, n, sw: SpectralWeightConfig | None = None, ke: Kern
                      ms_pansharpen=st["ms_pansharpen"])
 
 
+def blind_subset(lrms, pan, factor, n, ch0, nch, sw=None, ke=None, ps=None, ctx=None):
+    """Blind solve of bands [ch0, ch0+nch) with weights / kernel / normalisation over all bands
+    (one rank's share of a channel-sharded solve). Returns (hrms (nch, H, W), kernel)."""
+    lrms, pan = _f(lrms), _f(pan)
+    N, h, w = lrms.shape
+    sw = sw or SpectralWeightConfig(l=4, lambda_omega=10.0, factor=factor)
+    sw.factor = factor
+    ke = ke or KernelEstParams(n=n)
+    ke.n = n
+    ps = ps or PansharpenParams()
+    out = np.empty((nch, h * factor, w * factor))
+    k = np.empty((n, n))
+    c1, c2, c3 = sw.c(), ke.c(), ps.c()
+    _check(_lib.fbmp_gpu_blind_subset(_ctx(ctx), _p(lrms), N, h, w, _p(pan), C.byref(c1), C.byref(c2), C.byref(c3),
+                                      int(ch0), int(nch), _p(out), _p(k)))
+    return out, k
+
+
 def blind_batch(lrms, pan, factor, n, sw=None, ke=None, ps=None, ctx=None):
     """S independent scenes: lrms (S, N, h, w), pan (S, H, W) -> (hrms (S, N, H, W), kernels (S, n, n))."""
     lrms, pan = _f(lrms), _f(pan)
@@ -555,7 +573,7 @@ EXPORTED_SYMBOLS = (
     "fbmp_gpu_ctx_stream", "fbmp_gpu_ctx_launches", "fbmp_gpu_ctx_set_profile", "fbmp_gpu_ctx_kernel_profile",
     "fbmp_gpu_pansharpen", "fbmp_gpu_estimate_kernel_tgv",
     "fbmp_gpu_estimate_kernel_plane", "fbmp_gpu_solve_weights", "fbmp_gpu_combine_bands", "fbmp_gpu_blind",
-    "fbmp_gpu_blind_dev", "fbmp_gpu_blind_batch", "fbmp_gpu_apply_prior", "fbmp_gpu_llp_apply",
+    "fbmp_gpu_blind_dev", "fbmp_gpu_blind_batch", "fbmp_gpu_blind_subset", "fbmp_gpu_apply_prior", "fbmp_gpu_llp_apply",
     "fbmp_gpu_data_apply", "fbmp_gpu_cg_operator", "fbmp_gpu_warmstart_cg", "fbmp_gpu_guided_filter",
     "fbmp_gpu_guided_output", "fbmp_gpu_solve_channel_fft", "fbmp_gpu_box_mean", "fbmp_gpu_convolve",
     "fbmp_gpu_shrink2", "fbmp_gpu_project_simplex", "fbmp_gpu_solve_up", "fbmp_gpu_gram",

@@ -164,3 +164,45 @@ def test_blind_c1_matches_oracle(gpu, orc):
     assert rel(ig["kernel"], io["kernel"]) < TOL
     assert list(ig["cg_iters"]) == list(io["cg_iters"])
     assert rel(out_g, out_o) < TOL
+
+
+def _check_golden(gpu, name, n):
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", f"{name}_blind.npz"))
+    sc = synth.make_scene(name.upper())
+    out, info = gpu.blind(sc.lrms, sc.pan, 4, n)
+    assert info["admm_iters"] == int(g["admm_iters"])
+    assert list(info["cg_iters"]) == list(g["cg_iters"])
+    assert rel(info["kernel"], g["kernel"]) < TOL
+    lo, c = int(g["crop_origin"]), g["crop"].shape[1]
+    assert rel(out[:, lo:lo + c, lo:lo + c], g["crop"]) < TOL
+    assert rel(out.sum(axis=2), g["row_sums"]) < TOL
+    assert rel(np.linalg.norm(out.reshape(out.shape[0], -1), axis=1), g["band_norms"]) < TOL
+
+
+def test_golden_c1(gpu):
+    _check_golden(gpu, "c1", 15)
+
+
+def test_golden_c2(gpu):
+    """BASELINE configs[1] (the bench workload), against the committed oracle fixture."""
+    _check_golden(gpu, "c2", 17)
+
+
+def test_blind_subset_equals_full(gpu):
+    """Channel sharding (C3 mode): bands solved in blocks are bit-identical to one solve."""
+    sc = synth.make_scene("C1")
+    full, _ = gpu.blind(sc.lrms, sc.pan, 4, 15)
+    parts = [gpu.blind_subset(sc.lrms, sc.pan, 4, 15, c0, nc)[0] for c0, nc in ((0, 1), (1, 2), (3, 1))]
+    assert np.array_equal(np.concatenate(parts), full)
+
+
+def test_blind_batch_matches_scenes(gpu, orc):
+    """Scene batching (C4 mode): every scene of a batch equals its own solve and the oracle."""
+    scenes = [synth.make_scene("C4", s) for s in range(2)]  # BASELINE C4 scenes (512^2, 4 bands, n = 15)
+    out, ks = gpu.blind_batch(np.stack([s.lrms for s in scenes]), np.stack([s.pan for s in scenes]), 4, 15)
+    for i, sc in enumerate(scenes):
+        single, info = gpu.blind(sc.lrms, sc.pan, 4, 15)
+        assert np.array_equal(out[i], single) and np.array_equal(ks[i], info["kernel"])
+    ref, rinfo = orc.blind(scenes[0].lrms, scenes[0].pan, 4, 15, threads=4)
+    assert rel(out[0], ref) < TOL and rel(ks[0], rinfo["kernel"]) < TOL

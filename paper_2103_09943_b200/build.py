@@ -61,13 +61,21 @@ def build_gpu(force: bool = False, verbose: bool = False) -> str:
     return GPU_LIB
 
 
+SHIM_TEST = os.path.join(LIBDIR, "fbmp_shim_selftest")
+
+
 def build_shim(force: bool = False) -> str:
-    srcs = [os.path.join(HOST, f) for f in sorted(os.listdir(HOST)) if f.endswith(".cpp")]
+    """libfbmp.so: the reference's fbmp:: C++ API on top of libfbmp_gpu.so (+ its self-test)."""
+    srcs = [os.path.join(HOST, "fbmp_api.cpp")]
     hdrs = [os.path.join(ROOT, "include", "fbmp", f) for f in os.listdir(os.path.join(ROOT, "include", "fbmp"))]
     if force or _stale(SHIM_LIB, srcs + hdrs + [GPU_LIB]):
         _run(["g++", "-O2", "-std=c++20", "-fPIC", "-shared", "-Wall", "-Wextra",
               "-I" + os.path.join(ROOT, "include"), "-o", SHIM_LIB] + srcs +
              ["-L" + LIBDIR, "-lfbmp_gpu", "-Wl,-rpath,$ORIGIN"])
+    test_src = os.path.join(HOST, "shim_selftest.cpp")
+    if force or _stale(SHIM_TEST, [test_src, SHIM_LIB] + hdrs):
+        _run(["g++", "-O2", "-std=c++20", "-Wall", "-I" + os.path.join(ROOT, "include"), "-o", SHIM_TEST, test_src,
+              "-L" + LIBDIR, "-lfbmp", "-lfbmp_gpu", "-Wl,-rpath,$ORIGIN"])
     return SHIM_LIB
 
 

@@ -12,7 +12,11 @@
 //           the only global traffic per iteration is the (E^T E + mu3 I)^-1 mat-vec (L2).
 #include <cmath>
 
+#include <cooperative_groups.h>
+
 #include "kernel_fit.cuh"
+
+#include <cstdlib>
 
 namespace fbmp_gpu {
 
@@ -500,6 +504,7 @@ struct AdmmArgs {
     int n, m;
     double alpha1, alpha2, mu1, mu2, mu3, rho, th, coupling;
     int t_max, t_begin, phase_begin, hook_t, init_kind, init_state;
+    int cache_symbols;  // 1: per-frequency {u,p} symbols cached in shared memory
 };
 
 constexpr int NTADMM = 512;
@@ -511,43 +516,75 @@ struct AdmmSmem {
     double *spec, *rowt;            // 3 complex planes each (6*m doubles)
     double *twc, *tws;              // n
     double* red;
+    double* sym = nullptr;          // optional cache of the per-frequency symbols (11*m) + tol
 };
 
-__device__ inline double dft_tw(const double* twc, const double* tws, int k, bool im) { return im ? tws[k] : twc[k]; }
+// per-frequency symbols of the {u,p} system (kernel_estimator.cpp:175-195):
+// {d1, d2, d3, Re d4, Im d4, Re d5, Im d5, Re d6, Im d6, Re den, Im den}
+__device__ __forceinline__ void up_symbol(const AdmmSmem& S, int n, int i, double a1m1, double a2m2, double coupling,
+                                          double out[11]) {
+    const int r = i / n, c = i - r * n;
+    const double dvr = S.twc[r] - 1.0, dvi = S.tws[r];
+    const double dhr = S.twc[c] - 1.0, dhi = S.tws[c];
+    const double av2 = dvr * dvr + dvi * dvi, ah2 = dhr * dhr + dhi * dhi;
+    const double d1 = a1m1 * (ah2 + av2) + coupling;
+    const double d2 = a1m1 + 0.5 * a2m2 * av2 + a2m2 * ah2;
+    const double d3 = a1m1 + 0.5 * a2m2 * ah2 + a2m2 * av2;
+    const double d4r = -a1m1 * dhr, d4i = -a1m1 * dhi, d5r = -a1m1 * dvr, d5i = -a1m1 * dvi;
+    const double d6r = 0.5 * a2m2 * (dhr * dvr + dhi * dvi), d6i = 0.5 * a2m2 * (dhr * dvi - dhi * dvr);
+    // den = d1 (d2 d3 - |d6|^2) - conj(d4)(d4 d3 - conj(d6) d5) + conj(d5)(d4 d6 - d2 d5)
+    const double t1 = d1 * (d2 * d3 - (d6r * d6r + d6i * d6i));
+    const double ar = d4r * d3 - (d6r * d5r + d6i * d5i), ai = d4i * d3 - (d6r * d5i - d6i * d5r);
+    const double br = (d4r * d6r - d4i * d6i) - d2 * d5r, bi = (d4r * d6i + d4i * d6r) - d2 * d5i;
+    out[0] = d1; out[1] = d2; out[2] = d3;
+    out[3] = d4r; out[4] = d4i; out[5] = d5r; out[6] = d5i; out[7] = d6r; out[8] = d6i;
+    out[9] = t1 - (d4r * ar + d4i * ai) + (d5r * br + d5i * bi);
+    out[10] = -(d4r * ai - d4i * ar) + (d5r * bi - d5i * br);
+}
 
-// forward 2-D DFT of 3 real n x n planes (src[f]) -> spec (3 interleaved complex planes)
+
+// forward 2-D DFT of 3 real n x n planes (src[f]) -> spec (3 interleaved complex planes).
+// One thread per output bin computes all three fields, sharing twiddles and index updates.
 __device__ void dft3_forward(const AdmmSmem& S, int n, const double* const src[3]) {
     const int m = n * n;
-    for (int e = threadIdx.x; e < 3 * m; e += blockDim.x) {  // rows: T[r][kc] = sum_c x[r][c] w^(kc c)
-        const int f = e / m, rc = e - f * m, r = rc / n, kc = rc - r * n;
-        const double* x = src[f] + r * n;
-        double re = 0.0, im = 0.0;
+    for (int e = threadIdx.x; e < m; e += blockDim.x) {  // rows: T[r][kc] = sum_c x[r][c] w^(kc c)
+        const int r = e / n, kc = e - r * n;
+        const double *x0 = src[0] + r * n, *x1 = src[1] + r * n, *x2 = src[2] + r * n;
+        double re0 = 0.0, im0 = 0.0, re1 = 0.0, im1 = 0.0, re2 = 0.0, im2 = 0.0;
         int idx = 0;
         for (int c = 0; c < n; ++c) {
-            re = fma(x[c], S.twc[idx], re);
-            im = fma(-x[c], S.tws[idx], im);
+            const double wc = S.twc[idx], ws = S.tws[idx];
+            re0 = fma(x0[c], wc, re0); im0 = fma(-x0[c], ws, im0);
+            re1 = fma(x1[c], wc, re1); im1 = fma(-x1[c], ws, im1);
+            re2 = fma(x2[c], wc, re2); im2 = fma(-x2[c], ws, im2);
             idx += kc;
             if (idx >= n) idx -= n;
         }
-        S.rowt[2 * e] = re;
-        S.rowt[2 * e + 1] = im;
+        S.rowt[2 * e] = re0; S.rowt[2 * e + 1] = im0;
+        S.rowt[2 * (m + e)] = re1; S.rowt[2 * (m + e) + 1] = im1;
+        S.rowt[2 * (2 * m + e)] = re2; S.rowt[2 * (2 * m + e) + 1] = im2;
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < 3 * m; e += blockDim.x) {  // cols: F[kr][kc] = sum_r T[r][kc] w^(kr r)
-        const int f = e / m, rc = e - f * m, kr = rc / n, kc = rc - kr * n;
-        const double* T = S.rowt + 2 * (f * m + kc);
-        double re = 0.0, im = 0.0;
+    for (int e = threadIdx.x; e < m; e += blockDim.x) {  // cols: F[kr][kc] = sum_r T[r][kc] w^(kr r)
+        const int kr = e / n, kc = e - kr * n;
+        double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
         int idx = 0;
         for (int r = 0; r < n; ++r) {
-            const double tr = T[2 * r * n], ti = T[2 * r * n + 1];
             const double wc = S.twc[idx], wsn = -S.tws[idx];
-            re = fma(tr, wc, fma(-ti, wsn, re));
-            im = fma(tr, wsn, fma(ti, wc, im));
+#pragma unroll
+            for (int f = 0; f < 3; ++f) {
+                const double tr = S.rowt[2 * (f * m + r * n + kc)], ti = S.rowt[2 * (f * m + r * n + kc) + 1];
+                acc[f][0] = fma(tr, wc, fma(-ti, wsn, acc[f][0]));
+                acc[f][1] = fma(tr, wsn, fma(ti, wc, acc[f][1]));
+            }
             idx += kr;
             if (idx >= n) idx -= n;
         }
-        S.spec[2 * e] = re;
-        S.spec[2 * e + 1] = im;
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+            S.spec[2 * (f * m + e)] = acc[f][0];
+            S.spec[2 * (f * m + e) + 1] = acc[f][1];
+        }
     }
     __syncthreads();
 }
@@ -555,37 +592,58 @@ __device__ void dft3_forward(const AdmmSmem& S, int n, const double* const src[3
 // inverse 2-D DFT of spec -> dst[f] = Re(.) / m  (fft_util.cpp:47-56)
 __device__ void dft3_inverse(const AdmmSmem& S, int n, double* const dst[3]) {
     const int m = n * n;
-    for (int e = threadIdx.x; e < 3 * m; e += blockDim.x) {  // rows over kc
-        const int f = e / m, rc = e - f * m, kr = rc / n, c = rc - kr * n;
-        const double* F = S.spec + 2 * (f * m + kr * n);
-        double re = 0.0, im = 0.0;
+    for (int e = threadIdx.x; e < m; e += blockDim.x) {  // rows over kc
+        const int kr = e / n, c = e - kr * n;
+        double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
         int idx = 0;
         for (int kc = 0; kc < n; ++kc) {
-            const double fr = F[2 * kc], fi = F[2 * kc + 1];
             const double wc = S.twc[idx], wsn = S.tws[idx];
-            re = fma(fr, wc, fma(-fi, wsn, re));
-            im = fma(fr, wsn, fma(fi, wc, im));
+#pragma unroll
+            for (int f = 0; f < 3; ++f) {
+                const double fr = S.spec[2 * (f * m + kr * n + kc)], fi = S.spec[2 * (f * m + kr * n + kc) + 1];
+                acc[f][0] = fma(fr, wc, fma(-fi, wsn, acc[f][0]));
+                acc[f][1] = fma(fr, wsn, fma(fi, wc, acc[f][1]));
+            }
             idx += c;
             if (idx >= n) idx -= n;
         }
-        S.rowt[2 * e] = re;
-        S.rowt[2 * e + 1] = im;
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+            S.rowt[2 * (f * m + e)] = acc[f][0];
+            S.rowt[2 * (f * m + e) + 1] = acc[f][1];
+        }
     }
     __syncthreads();
     const double inv = 1.0 / static_cast<double>(m);
-    for (int e = threadIdx.x; e < 3 * m; e += blockDim.x) {
-        const int f = e / m, rc = e - f * m, r = rc / n, c = rc - r * n;
-        const double* T = S.rowt + 2 * (f * m + c);
-        double re = 0.0;
+    for (int e = threadIdx.x; e < m; e += blockDim.x) {  // cols, real part only
+        const int r = e / n, c = e - r * n;
+        double re[3] = {0.0, 0.0, 0.0};
         int idx = 0;
         for (int kr = 0; kr < n; ++kr) {
-            re = fma(T[2 * kr * n], S.twc[idx], fma(-T[2 * kr * n + 1], S.tws[idx], re));
+            const double wc = S.twc[idx], ws = S.tws[idx];
+#pragma unroll
+            for (int f = 0; f < 3; ++f)
+                re[f] = fma(S.rowt[2 * (f * m + kr * n + c)], wc, fma(-S.rowt[2 * (f * m + kr * n + c) + 1], ws, re[f]));
             idx += r;
             if (idx >= n) idx -= n;
         }
-        dst[f][rc] = re * inv;
+#pragma unroll
+        for (int f = 0; f < 3; ++f) dst[f][e] = re[f] * inv;
     }
     __syncthreads();
+}
+
+// block-wide max of a double (exact), NTADMM threads, warp shuffles + one shared pass
+__device__ __forceinline__ double block_max(double v, double* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double r = red[0];
+    for (int w = 1; w < NTADMM / 32; ++w) r = fmax(r, red[w]);
+    __syncthreads();
+    return r;
 }
 
 // {u,p} solve (kernel_estimator.cpp:137-233) on fields in shared memory; writes u -> uout,
@@ -595,74 +653,52 @@ __device__ void up_solve(const AdmmSmem& S, int n, double a1m1, double a2m2, dou
                          const double* L10, const double* L11, const double* L20, const double* L21, const double* L22,
                          const double* L23, const double* anchor, double* uout, double* p1out, double* p2out) {
     const int m = n * n;
-    double* x1m = S.tmp6;
-    double* x2m = S.tmp6 + m;
-    double* y1m = S.tmp6 + 2 * m;
-    double* y2m = S.tmp6 + 3 * m;
-    double* ycm = S.tmp6 + 4 * m;
-    for (int i = threadIdx.x; i < m; i += blockDim.x) {
-        x1m[i] = x0[i] - L10[i];
-        x2m[i] = x1[i] - L11[i];
-        y1m[i] = y0[i] - L20[i];
-        y2m[i] = y3[i] - L23[i];
-        ycm[i] = (((y1[i] - L21[i]) + y2[i]) - L22[i]) * 0.5;
-    }
-    __syncthreads();
-    double* B1 = uout;  // reuse the output planes as right-hand sides
+    double* B1 = uout;  // the output planes hold the right-hand sides
     double* B2 = p1out;
     double* B3 = p2out;
+    // right-hand sides (kernel_estimator.cpp:151-162), differences of the fields formed inline
     for (int i = threadIdx.x; i < m; i += blockDim.x) {
         const int r = i / n, c = i - r * n;
         const int cl = r * n + (c + n - 1) % n, ru = ((r + n - 1) % n) * n + c;  // left / upper neighbours
-        const double g1 = x1m[cl] - x1m[i], g2 = x2m[ru] - x2m[i];               // ops.cpp:87-97
-        const double h1 = y1m[cl] - y1m[i], h2 = ycm[ru] - ycm[i];
-        const double k1 = y2m[ru] - y2m[i], k2 = ycm[cl] - ycm[i];
+        auto x1m = [&](int k) { return x0[k] - L10[k]; };
+        auto x2m = [&](int k) { return x1[k] - L11[k]; };
+        auto y1m = [&](int k) { return y0[k] - L20[k]; };
+        auto y2m = [&](int k) { return y3[k] - L23[k]; };
+        auto ycm = [&](int k) { return (((y1[k] - L21[k]) + y2[k]) - L22[k]) * 0.5; };
+        const double g1 = x1m(cl) - x1m(i), g2 = x2m(ru) - x2m(i);  // ops.cpp:87-97
+        const double h1 = y1m(cl) - y1m(i), h2 = ycm(ru) - ycm(i);
+        const double k1 = y2m(ru) - y2m(i), k2 = ycm(cl) - ycm(i);
         double b1 = (g1 + g2) * a1m1;
         if (coupling > 0.0 && anchor) b1 = b1 + anchor[i] * coupling;
+        const double b2 = (x1m(i) * -a1m1) + (h1 + h2) * a2m2;
+        const double b3 = (x2m(i) * -a1m1) + (k1 + k2) * a2m2;
         B1[i] = b1;
-        B2[i] = (x1m[i] * -a1m1) + (h1 + h2) * a2m2;
-        B3[i] = (x2m[i] * -a1m1) + (k1 + k2) * a2m2;
+        B2[i] = b2;
+        B3[i] = b3;
     }
     __syncthreads();
     const double* src[3] = {B1, B2, B3};
     dft3_forward(S, n, src);
-    // max |den| for the singular tolerance (kernel_estimator.cpp:174-197)
-    double dmax = 0.0;
-    for (int i = threadIdx.x; i < m; i += blockDim.x) {
-        const int r = i / n, c = i - r * n;
-        const double dvr = S.twc[r] - 1.0, dvi = S.tws[r];
-        const double dhr = S.twc[c] - 1.0, dhi = S.tws[c];
-        const double av2 = dvr * dvr + dvi * dvi, ah2 = dhr * dhr + dhi * dhi;
-        const double d1 = a1m1 * (ah2 + av2) + coupling;
-        const double d2 = a1m1 + 0.5 * a2m2 * av2 + a2m2 * ah2;
-        const double d3 = a1m1 + 0.5 * a2m2 * ah2 + a2m2 * av2;
-        const double d4r = -a1m1 * dhr, d4i = -a1m1 * dhi, d5r = -a1m1 * dvr, d5i = -a1m1 * dvi;
-        const double d6r = 0.5 * a2m2 * (dhr * dvr + dhi * dvi), d6i = 0.5 * a2m2 * (dhr * dvi - dhi * dvr);
-        // den = d1 (d2 d3 - |d6|^2) - conj(d4)(d4 d3 - conj(d6) d5) + conj(d5)(d4 d6 - d2 d5)
-        const double t1 = d1 * (d2 * d3 - (d6r * d6r + d6i * d6i));
-        const double ar = d4r * d3 - (d6r * d5r + d6i * d5i), ai = d4i * d3 - (d6r * d5i - d6i * d5r);
-        const double br = (d4r * d6r - d4i * d6i) - d2 * d5r, bi = (d4r * d6i + d4i * d6r) - d2 * d5i;
-        const double dr_ = t1 - (d4r * ar + d4i * ai) + (d5r * br + d5i * bi);
-        const double di_ = -(d4r * ai - d4i * ar) + (d5r * bi - d5i * br);
-        dmax = fmax(dmax, sqrt(dr_ * dr_ + di_ * di_));
+    double tol;
+    if (S.sym) {
+        tol = S.sym[11 * m];
+    } else {  // max |den| for the singular tolerance (kernel_estimator.cpp:174-197)
+        double dmax = 0.0, sy[11];
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+            up_symbol(S, n, i, a1m1, a2m2, coupling, sy);
+            dmax = fmax(dmax, sqrt(sy[9] * sy[9] + sy[10] * sy[10]));
+        }
+        tol = 1e-12 * block_max(dmax, S.red);
     }
-    // block max (exact)
-    S.red[threadIdx.x] = dmax;
-    __syncthreads();
-    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-        if (threadIdx.x < o) S.red[threadIdx.x] = fmax(S.red[threadIdx.x], S.red[threadIdx.x + o]);
-        __syncthreads();
-    }
-    const double tol = 1e-12 * S.red[0];
-    __syncthreads();
     for (int i = threadIdx.x; i < m; i += blockDim.x) {
-        const int r = i / n, c = i - r * n;
-        const double dvr = S.twc[r] - 1.0, dvi = S.tws[r];
-        const double dhr = S.twc[c] - 1.0, dhi = S.tws[c];
-        const double av2 = dvr * dvr + dvi * dvi, ah2 = dhr * dhr + dhi * dhi;
-        const double d1 = a1m1 * (ah2 + av2) + coupling;
-        const double d2 = a1m1 + 0.5 * a2m2 * av2 + a2m2 * ah2;
-        const double d3 = a1m1 + 0.5 * a2m2 * ah2 + a2m2 * av2;
+        double sy[11];
+        if (S.sym) {
+#pragma unroll
+            for (int q = 0; q < 11; ++q) sy[q] = S.sym[q * m + i];
+        } else {
+            up_symbol(S, n, i, a1m1, a2m2, coupling, sy);
+        }
+        const double d1 = sy[0], d2 = sy[1], d3 = sy[2];
         // complex helpers
         struct Z { double x, y; };
         auto mul = [](Z a, Z b) { return Z{a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x}; };
@@ -670,12 +706,9 @@ __device__ void up_solve(const AdmmSmem& S, int n, double a1m1, double a2m2, dou
         auto sub = [](Z a, Z b) { return Z{a.x - b.x, a.y - b.y}; };
         auto add = [](Z a, Z b) { return Z{a.x + b.x, a.y + b.y}; };
         auto rs = [](double s, Z a) { return Z{s * a.x, s * a.y}; };
-        const Z dh{dhr, dhi}, dv{dvr, dvi};
-        const Z d4 = rs(-a1m1, dh), d5 = rs(-a1m1, dv);
-        const Z d6 = rs(0.5 * a2m2, mul(cj(dh), dv));
+        const Z d4{sy[3], sy[4]}, d5{sy[5], sy[6]}, d6{sy[7], sy[8]};
         const double n6 = d6.x * d6.x + d6.y * d6.y;
-        const Z den = add(sub(Z{d1 * (d2 * d3 - n6), 0.0}, mul(cj(d4), sub(rs(d3, d4), mul(cj(d6), d5)))),
-                          mul(cj(d5), sub(mul(d4, d6), rs(d2, d5))));
+        const Z den{sy[9], sy[10]};
         Z b1{S.spec[2 * i], S.spec[2 * i + 1]};
         Z b2{S.spec[2 * (m + i)], S.spec[2 * (m + i) + 1]};
         Z b3{S.spec[2 * (2 * m + i)], S.spec[2 * (2 * m + i) + 1]};
@@ -725,10 +758,9 @@ __device__ int project_simplex_block(const double* v, double* out, int m, double
         int cnt = 0;
         for (int k = 0; k < m; ++k) {
             const double vk = v[k];
-            if (vk > vi || (vk == vi && k <= i)) {
-                css += vk;
-                ++cnt;
-            }
+            const bool in = vk > vi || (vk == vi && k <= i);
+            css += in ? vk : 0.0;
+            cnt += in;
         }
         const double cand = (1.0 - css) / static_cast<double>(cnt);
         if (vi + cand > 0.0 && cnt > best_rank) {
@@ -736,36 +768,53 @@ __device__ int project_simplex_block(const double* v, double* out, int m, double
             best_tau = cand;
         }
     }
-    ired[threadIdx.x] = best_rank;
-    red[threadIdx.x] = best_tau;
-    __syncthreads();
-    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-        if (threadIdx.x < o && ired[threadIdx.x + o] > ired[threadIdx.x]) {
-            ired[threadIdx.x] = ired[threadIdx.x + o];
-            red[threadIdx.x] = red[threadIdx.x + o];
+    // arg-max of the qualifying rank (ranks are distinct, so the winner is unique)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const int orank = __shfl_xor_sync(0xffffffffu, best_rank, o);
+        const double otau = __shfl_xor_sync(0xffffffffu, best_tau, o);
+        if (orank > best_rank) {
+            best_rank = orank;
+            best_tau = otau;
         }
-        __syncthreads();
     }
-    const int support = ired[0];
-    const double tau = red[0];
     __syncthreads();
+    if ((threadIdx.x & 31) == 0) {
+        ired[threadIdx.x >> 5] = best_rank;
+        red[threadIdx.x >> 5] = best_tau;
+    }
+    __syncthreads();
+    int support = ired[0];
+    double tau = red[0];
+    for (int w = 1; w < static_cast<int>(blockDim.x) / 32; ++w)
+        if (ired[w] > support) {
+            support = ired[w];
+            tau = red[w];
+        }
     if (support > 0)
         for (int i = threadIdx.x; i < m; i += blockDim.x) out[i] = fmax(v[i] + tau, 0.0);
     __syncthreads();
     return support;
 }
 
-size_t admm_smem_doubles(int n) {
-    const int m = n * n;
-    return static_cast<size_t>(17 + 3 + 6 + 6 + 6) * m + 2 * n + 2 * NTADMM + 8;
+size_t admm_smem_doubles(int n, int cs = 1) {
+    const size_t m = static_cast<size_t>(n) * n, rp = (m + cs - 1) / cs;
+    return static_cast<size_t>(17 + 3 + 6 + 6 + 6) * m + 2 * n + NTADMM + NTADMM / 2 + 4 + 8 +
+           (cs > 1 ? rp * m + 2 * rp : 0);
 }
 
+// CS > 1: the CTAs of a thread-block cluster run the same (deterministic, bit-identical) ADMM
+// on one scene; each holds rows [crank*RP, crank*RP+RP) of the symmetric inverse in shared
+// memory, computes that slice of the z-step mat-vec, and the slices are all-gathered through
+// distributed shared memory (one cluster barrier per iteration, slices double-buffered).
 __global__ void __launch_bounds__(NTADMM) k_admm(AdmmArgs A, const double* __restrict__ Ginv_all,
                                                  const double* __restrict__ Etf_all, double* __restrict__ state_all,
-                                                 int* __restrict__ info_all, double* __restrict__ k_out) {
+                                                 int* __restrict__ info_all, double* __restrict__ k_out, int CS) {
+    namespace cg = cooperative_groups;
     extern __shared__ double smem[];
-    const int s = blockIdx.x;
+    const int s = blockIdx.x / CS, crank = blockIdx.x - (blockIdx.x / CS) * CS;
     const int n = A.n, m = A.m;
+    const int RP = (m + CS - 1) / CS, r_lo = min(m, crank * RP), r_hi = min(m, r_lo + RP);
     const double* Ginv = Ginv_all + static_cast<size_t>(s) * m * m;
     const double* Etf = Etf_all + static_cast<size_t>(s) * m;
     double* gstate = state_all + static_cast<size_t>(s) * 17 * m;
@@ -783,11 +832,32 @@ __global__ void __launch_bounds__(NTADMM) k_admm(AdmmArgs A, const double* __res
     S.tws = p; p += n;
     S.red = p; p += NTADMM;
     int* ired = reinterpret_cast<int*>(p);
+    p += NTADMM / 2 + 4;
+    double* Gs = p;          // CS > 1: rows [r_lo, r_hi) of the inverse
+    p += (CS > 1) ? static_cast<size_t>(RP) * m : 0;
+    double* zsl = p;         // CS > 1: 2 x RP mat-vec slice (double-buffered by iteration parity)
+    p += (CS > 1) ? 2 * RP : 0;
     for (int k = threadIdx.x; k < n; k += blockDim.x) {
         const double wv = 2.0 * M_PI * k / n;
         S.twc[k] = cos(wv);
         S.tws[k] = sin(wv);
     }
+    if (A.cache_symbols) {  // symbols and singular tolerance are iteration-independent
+        S.sym = p;
+        __syncthreads();
+        double dmax = 0.0, sy[11];
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+            up_symbol(S, n, i, A.alpha1 * A.mu1, A.alpha2 * A.mu2, A.coupling, sy);
+#pragma unroll
+            for (int q = 0; q < 11; ++q) S.sym[q * m + i] = sy[q];
+            dmax = fmax(dmax, sqrt(sy[9] * sy[9] + sy[10] * sy[10]));
+        }
+        const double tol = 1e-12 * block_max(dmax, S.red);
+        if (threadIdx.x == 0) S.sym[11 * m] = tol;
+    }
+    if (CS > 1)
+        for (size_t e = threadIdx.x; e < static_cast<size_t>(r_hi - r_lo) * m; e += blockDim.x)
+            Gs[e] = __ldg(Ginv + static_cast<size_t>(r_lo) * m + e);
     double** F = S.f;
     if (A.init_state) {  // kernel_estimator.cpp:297-307
         const int cc = (n - 1) / 2;
@@ -842,15 +912,33 @@ __global__ void __launch_bounds__(NTADMM) k_admm(AdmmArgs A, const double* __res
             }
             __syncthreads();
             // z = project_simplex((E^T E + mu3 I)^-1 (E^T f + mu3 (u + L3)))   (:341, :79-83)
-            for (int i = threadIdx.x; i < m; i += blockDim.x) {
-                double a0 = 0.0, a1 = 0.0;
-                int j = 0;
-                for (; j + 1 < m; j += 2) {
-                    a0 = fma(__ldg(Ginv + static_cast<size_t>(j) * m + i), S.bz[j], a0);
-                    a1 = fma(__ldg(Ginv + static_cast<size_t>(j + 1) * m + i), S.bz[j + 1], a1);
+            if (CS > 1) {
+                double* mine = zsl + (t & 1) * RP;
+                const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+                for (int i = r_lo + warp; i < r_hi; i += NTADMM / 32) {
+                    const double* row = Gs + static_cast<size_t>(i - r_lo) * m;
+                    double acc = 0.0;
+                    for (int j = lane; j < m; j += 32) acc = fma(row[j], S.bz[j], acc);
+                    acc = warp_sum(acc);
+                    if (lane == 0) mine[i - r_lo] = acc;
                 }
-                if (j < m) a0 = fma(__ldg(Ginv + static_cast<size_t>(j) * m + i), S.bz[j], a0);
-                S.zz[i] = a0 + a1;
+                cg::this_cluster().sync();
+                for (int i = threadIdx.x; i < m; i += blockDim.x) {
+                    const int owner = i / RP;
+                    const double* rem = cg::this_cluster().map_shared_rank(zsl, owner);
+                    S.zz[i] = rem[(t & 1) * RP + (i - owner * RP)];
+                }
+            } else {
+                for (int i = threadIdx.x; i < m; i += blockDim.x) {
+                    double a0 = 0.0, a1 = 0.0;
+                    int j = 0;
+                    for (; j + 1 < m; j += 2) {
+                        a0 = fma(__ldg(Ginv + static_cast<size_t>(j) * m + i), S.bz[j], a0);
+                        a1 = fma(__ldg(Ginv + static_cast<size_t>(j + 1) * m + i), S.bz[j + 1], a1);
+                    }
+                    if (j < m) a0 = fma(__ldg(Ginv + static_cast<size_t>(j) * m + i), S.bz[j], a0);
+                    S.zz[i] = a0 + a1;
+                }
             }
             __syncthreads();
             bool finite = true;
@@ -864,14 +952,9 @@ __global__ void __launch_bounds__(NTADMM) k_admm(AdmmArgs A, const double* __res
         // {u,p}-step with the mu3 tie to z - L3 (:349-355)
         for (int i = threadIdx.x; i < m; i += blockDim.x) S.bz[i] = F[F_Z][i] - F[F_L3][i];
         __syncthreads();
-        double* p1n = S.tmp6 + 5 * m;  // u_new -> S.unew, p1 -> spare, p2 -> zz
+        // old p1, p2 are dead after the y-step: the solve writes them in place, u_new separately
         up_solve(S, n, a1m1, a2m2, A.coupling, F[F_X0], F[F_X1], F[F_Y0], F[F_Y1], F[F_Y2], F[F_Y3], F[F_L10],
-                 F[F_L11], F[F_L20], F[F_L21], F[F_L22], F[F_L23], S.bz, S.unew, p1n, S.zz);
-        for (int i = threadIdx.x; i < m; i += blockDim.x) {
-            F[F_P1][i] = p1n[i];
-            F[F_P2][i] = S.zz[i];
-        }
-        __syncthreads();
+                 F[F_L11], F[F_L20], F[F_L21], F[F_L22], F[F_L23], S.bz, S.unew, F[F_P1], F[F_P2]);
         // multipliers (:367-373), change of u (:375-376)
         double dd = 0.0, un = 0.0;
         bool fin_u = true, fin_z = true;
@@ -901,22 +984,28 @@ __global__ void __launch_bounds__(NTADMM) k_admm(AdmmArgs A, const double* __res
         const double scale = fmax(sqrt(admm_sum(un, S.red)), 1e-300);
         const bool all_u = __syncthreads_and(fin_u);
         const bool all_z = __syncthreads_and(fin_z);
-        for (int i = threadIdx.x; i < m; i += blockDim.x) F[F_U][i] = S.unew[i];
-        __syncthreads();
+        {  // u <- u_new by swapping the buffers (all threads hold the same pointers)
+            double* tmp = F[F_U];
+            F[F_U] = S.unew;
+            S.unew = tmp;
+        }
         iters = t + 1;
         if (!all_u) { status = 1; break; }  // check_finite (:379-380)
         if (!all_z) { status = 2; break; }
         if (delta / scale < A.th) { ++t; break; }
     }
-    for (int e = threadIdx.x; e < 17 * m; e += blockDim.x) gstate[e] = F[e / m][e % m];
-    if (k_out)
-        for (int i = threadIdx.x; i < m; i += blockDim.x) k_out[static_cast<size_t>(s) * m + i] = F[F_Z][i];
-    if (threadIdx.x == 0) {
-        info[0] = iters;
-        info[1] = status;
-        info[2] = t;
-        info[3] = 0;
+    if (crank == 0) {
+        for (int e = threadIdx.x; e < 17 * m; e += blockDim.x) gstate[e] = F[e / m][e % m];
+        if (k_out)
+            for (int i = threadIdx.x; i < m; i += blockDim.x) k_out[static_cast<size_t>(s) * m + i] = F[F_Z][i];
+        if (threadIdx.x == 0) {
+            info[0] = iters;
+            info[1] = status;
+            info[2] = t;
+            info[3] = 0;
+        }
     }
+    if (CS > 1) cg::this_cluster().sync();  // no CTA leaves while a peer may still read its slice
 }
 
 // standalone {u,p} solve for the public solve_up (kernel_estimator.cpp:237-241)
@@ -1131,10 +1220,34 @@ void admm_device(Context& ctx, const ObsSystem& sys, const fbmp_ke_params& prm, 
     A.hook_t = hook_t;
     A.init_kind = prm.init;
     A.init_state = init_state ? 1 : 0;
-    const size_t sm = admm_smem_doubles(sys.n) * sizeof(double);
+    // cluster size: the smallest power of two whose inverse slice fits next to the ADMM state
+    int cs = 1;
+    const char* env = std::getenv("FBMP_ADMM_CLUSTER");
+    const int cs_max = env ? std::max(1, std::atoi(env)) : 16;
+    if (sys.n2 >= 100)
+        for (int c = 2; c <= cs_max; c *= 2)
+            if (admm_smem_doubles(sys.n, c) * sizeof(double) <= 220 * 1024) { cs = c; break; }
+    size_t sm = admm_smem_doubles(sys.n, cs) * sizeof(double);
     if (sm > 227 * 1024) param_error("kernel estimation: kernel side too large for the device ADMM (n <= 25)");
+    const size_t sym_bytes = (11 * static_cast<size_t>(sys.n2) + 2) * sizeof(double);
+    A.cache_symbols = sm + sym_bytes <= 225 * 1024 ? 1 : 0;
+    if (A.cache_symbols) sm += sym_bytes;
     set_smem(k_admm, sm);
-    k_admm<<<sys.S, NTADMM, sm, ctx.stream>>>(A, sys.Ginv, sys.Etf, d_state, d_info, d_k);
+    if (cs > 8) FBMP_CUDA(cudaFuncSetAttribute(k_admm, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(sys.S * cs);
+    cfg.blockDim = dim3(NTADMM);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = ctx.stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    FBMP_CUDA(cudaLaunchKernelEx(&cfg, k_admm, A, static_cast<const double*>(sys.Ginv),
+                                 static_cast<const double*>(sys.Etf), d_state, d_info, d_k, cs));
     ctx.count();
     check_launch();
 }

@@ -23,4 +23,5 @@ for i in range(reps):
     t = time.perf_counter()
     fbmp.blind_dev(d_l.data_ptr(), N, h, w, d_p.data_ptr(), d_o.data_ptr(), d_k.data_ptr(), cfg.ratio, cfg.support, ctx)
     torch.cuda.synchronize()
-    print(f"solve {i}: {1e3 * (time.perf_counter() - t):.2f} ms", ctx.stats()["ms_pansharpen"], flush=True)
+    st = ctx.stats()
+    print(f"solve {i}: {1e3 * (time.perf_counter() - t):.2f} ms  fit {st['ms_kernel_fit']:.2f} ms  hrms {st['ms_pansharpen']:.2f} ms", flush=True)

@@ -25,8 +25,26 @@ Context::Context(int dev) : device(dev) {
 Context::~Context() {
     cudaSetDevice(device);
     for (auto& kv : plans) cufftDestroy(kv.second);
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& e : poll_ev)
+        if (e) cudaEventDestroy(e);
+    if (pinned_buf) cudaFreeHost(pinned_buf);
     ws.clear();
     if (stream) cudaStreamDestroy(stream);
+}
+
+void* Context::pinned(size_t bytes) {
+    if (bytes > pinned_bytes) {
+        if (pinned_buf) {
+            FBMP_CUDA(cudaStreamSynchronize(stream));
+            FBMP_CUDA(cudaFreeHost(pinned_buf));
+            pinned_buf = nullptr;
+        }
+        const size_t nb = std::max<size_t>(bytes, 64 << 10);
+        FBMP_CUDA(cudaMallocHost(&pinned_buf, nb));
+        pinned_bytes = nb;
+    }
+    return pinned_buf;
 }
 
 cufftHandle Context::plan(int kind, int rows, int cols, int batch) {
@@ -88,6 +106,7 @@ void pansharpen_device(Context& ctx, const double* d_lrms, int S, int N, int h, 
     B.part = ctx.scratch<double>("cg_part", 4 * nbmax * NC);
     B.st = ctx.scratch<CgState>("cg_state", NC);
     std::vector<CgState> hs;
+    trace("ps: prologue");
     cg_solve(ctx, G, d_taps, lpan, xn, B, prm.cg_max_iter, prm.cg_tol, hs);
     cg_iters.assign(NC, 0);
     for (int i = 0; i < NC; ++i) cg_iters[i] = hs[i].iters;
@@ -118,9 +137,11 @@ void pansharpen_device(Context& ctx, const double* d_lrms, int S, int N, int h, 
     int* flag = ctx.scratch<int>("ps_flag", NC);
     FBMP_CUDA(cudaMemsetAsync(flag, 0, sizeof(int) * NC, ctx.stream));
     solve_channel_fft(ctx, G, d_taps, xn, v, scale, d_out, flag);
+    trace("ps: guided + fft enqueue");
     std::vector<int> hf(NC);
     d2h(hf.data(), flag, sizeof(int) * NC, ctx.stream);
     FBMP_CUDA(cudaStreamSynchronize(ctx.stream));
+    trace("ps: guided + fft done");
     for (int i = 0; i < NC; ++i)
         if (hf[i])
             num_error("channel " + std::to_string(ch0 + i % NS) +
@@ -145,6 +166,7 @@ void blind_device(Context& ctx, const double* d_lrms, int S, int N, int h, int w
     cudaEvent_t e0, e1, e2, e3;
     cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2); cudaEventCreate(&e3);
     cudaEventRecord(e0, ctx.stream);
+    trace("blind: start");
     double* omega = d_omega_out ? d_omega_out : ctx.scratch<double>("bl_omega", static_cast<size_t>(S) * N);
     int* st = ctx.scratch<int>("bl_sw_status", S);
     solve_weights_device(ctx, d_lrms, S, N, h, w, d_pan, sw.l, sw.lambda_omega, c, omega, st);
@@ -161,6 +183,7 @@ void blind_device(Context& ctx, const double* d_lrms, int S, int N, int h, int w
     cudaEventRecord(e1, ctx.stream);
     estimate_kernel_device(ctx, d_pan, obs, S, H, W, c, ke, d_k, admm_iters, nullptr, -1);
     cudaEventRecord(e2, ctx.stream);
+    trace("blind: weights + kernel fit");
     pansharpen_device(ctx, d_lrms, S, N, h, w, d_pan, d_k, ke.n, c, ps, d_out, cg_iters, ch0, nch);
     cudaEventRecord(e3, ctx.stream);
     cudaEventSynchronize(e3);

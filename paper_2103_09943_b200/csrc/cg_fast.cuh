@@ -21,6 +21,8 @@ constexpr int NT = 256;
 __host__ __device__ constexpr int pstride(int s) { return s + ((4 - s % 16) + 16) % 16; }
 
 __device__ __forceinline__ int wrap_once(int a, int m) { return a < 0 ? a + m : (a >= m ? a - m : a); }
+__device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+__device__ __forceinline__ void st2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
 
 // ------------------------------------------------------------------------------------------
 // per-scene guide statistics (pansharpen.cpp:128-139, :152-155):
@@ -774,12 +776,9 @@ __global__ void __launch_bounds__(NT, 2) k_apply3(PsGeo G, const double* __restr
 namespace a4 {
 constexpr int TA = 32;
 constexpr int WP = TA + 8, WI = TA + 6, WK = TA + 4, WM = TA + 2;
-// stage strips: (columns, strips, rows per strip)
-constexpr int S1_COLS = WI, S1_STRIPS = 6, S1_ROWS = (WI + S1_STRIPS - 1) / S1_STRIPS;   // 38 x 6 x 7
-constexpr int S2_COLS = WK, S2_STRIPS = 6, S2_ROWS = (WK + S2_STRIPS - 1) / S2_STRIPS;   // 36 x 6 x 6
-constexpr int S3_COLS = WM, S3_STRIPS = 7, S3_ROWS = (WM + S3_STRIPS - 1) / S3_STRIPS;   // 34 x 7 x 5
-constexpr int S5_COLS = TA, S5_STRIPS = 8, S5_ROWS = TA / S5_STRIPS;                     // 32 x 8 x 4
-static_assert(S1_COLS * S1_STRIPS <= NT && S2_COLS * S2_STRIPS <= NT && S3_COLS * S3_STRIPS <= NT, "strips");
+// stage strips over column PAIRS: S1 19 x 13 strips x 3 rows, S2 18 x 14 x 3, S3 17 x 15 x 3,
+// S5 16 x 16 x 2
+static_assert(19 * 13 <= NT && 18 * 14 <= NT && 17 * 15 <= NT && 16 * 16 == NT && TA == 32, "strips");
 template <int CF>
 struct L {
     static constexpr int QMAX = a2::maxq(CF);
@@ -797,6 +796,8 @@ struct L {
     static constexpr int O_O = O_U + U_SIZE;               // data term out (TA x TA)
     static constexpr int TOTAL = O_O + TA * TA;
     static_assert(U_SIZE >= WP * WP, "union too small");
+    static_assert(O_I % 2 == 0 && O_MU % 2 == 0 && O_G % 2 == 0 && O_S % 2 == 0 && O_M % 2 == 0 &&
+                  O_Q % 2 == 0 && O_U % 2 == 0 && O_O % 2 == 0 && WK * WK % 2 == 0, "16-byte pair alignment");
     static constexpr size_t smem = TOTAL * sizeof(double);
 };
 }  // namespace a4
@@ -922,11 +923,11 @@ __global__ void __launch_bounds__(NT, 2) k_apply4(PsGeo G, const double* __restr
         cur = next_active(chl + 1);
         if (cur < ch_hi) prefetch(cur);  // in flight during this channel's stages
         __syncthreads();
-        // own pixels' p for p.Ap in the S5 mapping (column tid % 32, rows 4 (tid / 32) + i)
-        double pown[S5_ROWS];
+        // own pixels' p for p.Ap in the S5 mapping (column pair 2 (tid % 16), rows 2 (tid / 16) + {0,1})
+        double2 pown[2];
 #pragma unroll
-        for (int i = 0; i < S5_ROWS; ++i)
-            pown[i] = sP[(S5_ROWS * (threadIdx.x / S5_COLS) + i + 4) * WP + (threadIdx.x % S5_COLS) + 4];
+        for (int i = 0; i < 2; ++i)
+            pown[i] = ld2(sP + (2 * (threadIdx.x >> 4) + i + 4) * WP + 2 * (threadIdx.x & 15) + 4);
         // S4: data term (needs only q; writes its own buffer, so it runs before S1 without a barrier)
         double* sO = sm + Lay::O_O;
         if (N_ > 0 && !(G.dbg & 1)) {
@@ -983,20 +984,25 @@ __global__ void __launch_bounds__(NT, 2) k_apply4(PsGeo G, const double* __restr
                 sO[(ci * CF + pr) * TA + cj * CF + pc] = acc;
             }
         }
-        // S1: s = L p and I*s on R+3; column strips, vertical sliding window of p's centre column
-        if (threadIdx.x < S1_COLS * S1_STRIPS && !(G.dbg & 2)) {
-            const int x = threadIdx.x % S1_COLS, y0 = S1_ROWS * (threadIdx.x / S1_COLS);
-            double up = sP[y0 * WP + x + 1], mid = sP[(y0 + 1) * WP + x + 1];
+        // S1-S3 and S5 work on column PAIRS (16-byte shared accesses, conflict-free) and walk short
+        // strips of rows with the vertical 3-sums in a register sliding window.
+        // S1: s = L p and I*s on R+3
+        if (threadIdx.x < 19 * 13 && !(G.dbg & 2)) {
+            const int xp = 2 * (threadIdx.x % 19), y0 = 3 * (threadIdx.x / 19);
+            double2 a0 = ld2(sP + y0 * WP + xp), a1 = ld2(sP + y0 * WP + xp + 2);        // p rows y, y+1
+            double2 b0 = ld2(sP + (y0 + 1) * WP + xp), b1 = ld2(sP + (y0 + 1) * WP + xp + 2);
 #pragma unroll
-            for (int i = 0; i < S1_ROWS; ++i) {
+            for (int i = 0; i < 3; ++i) {
                 const int y = y0 + i;
                 if (y < WI) {
-                    const double dn = sP[(y + 2) * WP + x + 1];
-                    const double v = 4.0 * mid - up - dn - sP[(y + 1) * WP + x] - sP[(y + 1) * WP + x + 2];
-                    sS[y * WI + x] = v;
-                    sIS[y * WI + x] = sI[y * WI + x] * v;
-                    up = mid;
-                    mid = dn;
+                    const double2 e0 = ld2(sP + (y + 2) * WP + xp), e1 = ld2(sP + (y + 2) * WP + xp + 2);
+                    // outputs at p columns xp+1, xp+2 (ops.cpp:70-78 operation order)
+                    const double v0 = 4.0 * b0.y - a0.y - e0.y - b0.x - b1.x;
+                    const double v1 = 4.0 * b1.x - a1.x - e1.x - b0.y - b1.y;
+                    const double2 iv = ld2(sI + y * WI + xp);
+                    st2(sS + y * WI + xp, make_double2(v0, v1));
+                    st2(sIS + y * WI + xp, make_double2(iv.x * v0, iv.y * v1));
+                    a0 = b0; a1 = b1; b0 = e0; b1 = e1;
                 }
             }
         }
@@ -1004,75 +1010,97 @@ __global__ void __launch_bounds__(NT, 2) k_apply4(PsGeo G, const double* __restr
         // S2: per-window a_k, c1_k on R+2 from 3x3 sums of s and I*s
         double* sA = sU;
         double* sC = sU + WK * WK;
-        if (threadIdx.x < S2_COLS * S2_STRIPS && !(G.dbg & 4)) {
-            const int x = threadIdx.x % S2_COLS, y0 = S2_ROWS * (threadIdx.x / S2_COLS);
-            auto hrow = [&](const double* a, int y) { return a[y * WI + x] + a[y * WI + x + 1] + a[y * WI + x + 2]; };
-            double s0 = hrow(sS, y0), s1 = hrow(sS, y0 + 1);
-            double i0 = hrow(sIS, y0), i1 = hrow(sIS, y0 + 1);
+        if (threadIdx.x < 18 * 14 && !(G.dbg & 4)) {
+            const int xp = 2 * (threadIdx.x % 18), y0 = 3 * (threadIdx.x / 18);
+            auto hpair = [&](const double* a, int y) {  // horizontal 3-sums at columns xp, xp+1
+                const double2 u = ld2(a + y * WI + xp), v = ld2(a + y * WI + xp + 2);
+                return make_double2(u.x + u.y + v.x, u.y + v.x + v.y);
+            };
+            double2 s0 = hpair(sS, y0), s1 = hpair(sS, y0 + 1);
+            double2 i0 = hpair(sIS, y0), i1 = hpair(sIS, y0 + 1);
 #pragma unroll
-            for (int i = 0; i < S2_ROWS; ++i) {
+            for (int i = 0; i < 3; ++i) {
                 const int y = y0 + i;
                 if (y < WK) {
-                    const double s2 = hrow(sS, y + 2), i2 = hrow(sIS, y + 2);
-                    const double ss = s0 + s1 + s2, sis = i0 + i1 + i2;
-                    const double mu = sMu[y * WK + x], g = sG[y * WK + x];
-                    const double xb = ss * (1.0 / 9.0);  // box mean (fp64 division avoided)
-                    const double a = g * (sis * (1.0 / 9.0) - mu * xb);
-                    sA[y * WK + x] = a;
-                    sC[y * WK + x] = g != 0.0 ? xb - mu * a : 0.0;
+                    const double2 s2 = hpair(sS, y + 2), i2 = hpair(sIS, y + 2);
+                    const double2 mu = ld2(sMu + y * WK + xp), g = ld2(sG + y * WK + xp);
+                    double2 a, c;
+                    {
+                        const double xb = (s0.x + s1.x + s2.x) * (1.0 / 9.0);  // box mean, no fp64 division
+                        a.x = g.x * ((i0.x + i1.x + i2.x) * (1.0 / 9.0) - mu.x * xb);
+                        c.x = g.x != 0.0 ? xb - mu.x * a.x : 0.0;
+                    }
+                    {
+                        const double xb = (s0.y + s1.y + s2.y) * (1.0 / 9.0);
+                        a.y = g.y * ((i0.y + i1.y + i2.y) * (1.0 / 9.0) - mu.y * xb);
+                        c.y = g.y != 0.0 ? xb - mu.y * a.y : 0.0;
+                    }
+                    st2(sA + y * WK + xp, a);
+                    st2(sC + y * WK + xp, c);
                     s0 = s1; s1 = s2; i0 = i1; i1 = i2;
                 }
             }
         }
         __syncthreads();
         // S3: M s on R+1 = n_m s_m - box(c1) - I_m box(a)
-        if (threadIdx.x < S3_COLS * S3_STRIPS && !(G.dbg & 8)) {
-            const int x = threadIdx.x % S3_COLS, y0 = S3_ROWS * (threadIdx.x / S3_COLS);
-            auto hrow = [&](const double* a, int y) { return a[y * WK + x] + a[y * WK + x + 1] + a[y * WK + x + 2]; };
-            double a0 = hrow(sA, y0), a1 = hrow(sA, y0 + 1);
-            double k0 = hrow(sC, y0), k1 = hrow(sC, y0 + 1);
-            const int gc = wrap_once(c0 - 1 + x, W);
-            const int nc = max(min(gc + 1, W - 2) - max(gc - 1, 1) + 1, 0);
-            double mres[S3_ROWS];
+        if (threadIdx.x < 17 * 15 && !(G.dbg & 8)) {
+            const int xp = 2 * (threadIdx.x % 17), y0 = 3 * (threadIdx.x / 17);
+            auto hpair = [&](const double* a, int y) {
+                const double2 u = ld2(a + y * WK + xp), v = ld2(a + y * WK + xp + 2);
+                return make_double2(u.x + u.y + v.x, u.y + v.x + v.y);
+            };
+            double2 a0 = hpair(sA, y0), a1 = hpair(sA, y0 + 1);
+            double2 k0 = hpair(sC, y0), k1 = hpair(sC, y0 + 1);
+            const int gc0 = wrap_once(c0 - 1 + xp, W), gc1 = wrap_once(c0 + xp, W);
+            const int nc0 = max(min(gc0 + 1, W - 2) - max(gc0 - 1, 1) + 1, 0);
+            const int nc1 = max(min(gc1 + 1, W - 2) - max(gc1 - 1, 1) + 1, 0);
 #pragma unroll
-            for (int i = 0; i < S3_ROWS; ++i) {
+            for (int i = 0; i < 3; ++i) {
                 const int y = y0 + i;
-                mres[i] = 0.0;
                 if (y < WM) {
-                    const double a2v = hrow(sA, y + 2), k2 = hrow(sC, y + 2);
-                    const double ba = a0 + a1 + a2v, bc = k0 + k1 + k2;
+                    const double2 a2v = hpair(sA, y + 2), k2 = hpair(sC, y + 2);
                     const int gr = wrap_once(r0 - 1 + y, H);
                     const int nr = max(min(gr + 1, H - 2) - max(gr - 1, 1) + 1, 0);
-                    const int si = (y + 2) * WI + x + 2;
-                    mres[i] = static_cast<double>(nr * nc) * sS[si] - bc - sI[si] * ba;
+                    const double2 sv = ld2(sS + (y + 2) * WI + xp + 2), iv = ld2(sI + (y + 2) * WI + xp + 2);
+                    double2 m;
+                    m.x = static_cast<double>(nr * nc0) * sv.x - (k0.x + k1.x + k2.x) - iv.x * (a0.x + a1.x + a2v.x);
+                    m.y = static_cast<double>(nr * nc1) * sv.y - (k0.y + k1.y + k2.y) - iv.y * (a0.y + a1.y + a2v.y);
+                    st2(sM + y * WM + xp, m);  // sM aliases I*s: dead after S2, not read here
                     a0 = a1; a1 = a2v; k0 = k1; k1 = k2;
                 }
             }
-            // sM aliases I*s (dead after S2, not read in this stage)
-#pragma unroll
-            for (int i = 0; i < S3_ROWS; ++i)
-                if (y0 + i < WM) sM[(y0 + i) * WM + x] = mres[i];
         }
         __syncthreads();
-        // S5: t = L(M s), Ap = data + lambda t, p.Ap (column strips of 4 rows)
+        // S5: t = L(M s), Ap = data + lambda t, p.Ap
         double* oc = out + ch * P;
         double dotp = 0.0;
         if (!(G.dbg & 16)) {
-            const int x = threadIdx.x % S5_COLS, y0 = S5_ROWS * (threadIdx.x / S5_COLS);
-            double up = sM[y0 * WM + x + 1], mid = sM[(y0 + 1) * WM + x + 1];
-            const int Cc = c0 + x;
+            const int xp = 2 * (threadIdx.x & 15), y0 = 2 * (threadIdx.x >> 4);
+            double2 a0 = ld2(sM + y0 * WM + xp), a1 = ld2(sM + y0 * WM + xp + 2);
+            double2 b0 = ld2(sM + (y0 + 1) * WM + xp), b1 = ld2(sM + (y0 + 1) * WM + xp + 2);
+            const int Cc = c0 + xp;
 #pragma unroll
-            for (int i = 0; i < S5_ROWS; ++i) {
+            for (int i = 0; i < 2; ++i) {
                 const int y = y0 + i;
-                const double dn = sM[(y + 2) * WM + x + 1];
-                const double tl = 4.0 * mid - up - dn - sM[(y + 1) * WM + x] - sM[(y + 1) * WM + x + 2];
-                const double val = sO[y * TA + x] + tl * G.lambda;
-                up = mid;
-                mid = dn;
+                const double2 e0 = ld2(sM + (y + 2) * WM + xp), e1 = ld2(sM + (y + 2) * WM + xp + 2);
+                const double t0 = 4.0 * b0.y - a0.y - e0.y - b0.x - b1.x;
+                const double t1 = 4.0 * b1.x - a1.x - e1.x - b0.y - b1.y;
+                const double2 dv = ld2(sO + y * TA + xp);
+                const double2 val = make_double2(dv.x + t0 * G.lambda, dv.y + t1 * G.lambda);
+                a0 = b0; a1 = b1; b0 = e0; b1 = e1;
                 const int R = r0 + y;
-                if (R < H && Cc < W) {
-                    oc[static_cast<size_t>(R) * W + Cc] = val;
-                    dotp += pown[i] * val;
+                if (R < H && Cc + 1 < W && !(W & 1)) {
+                    *reinterpret_cast<double2*>(oc + static_cast<size_t>(R) * W + Cc) = val;
+                    dotp += pown[i].x * val.x + pown[i].y * val.y;
+                } else if (R < H) {
+                    if (Cc < W) {
+                        oc[static_cast<size_t>(R) * W + Cc] = val.x;
+                        dotp += pown[i].x * val.x;
+                    }
+                    if (Cc + 1 < W) {
+                        oc[static_cast<size_t>(R) * W + Cc + 1] = val.y;
+                        dotp += pown[i].y * val.y;
+                    }
                 }
             }
         }

@@ -4,7 +4,10 @@
 #include <cuda_runtime.h>
 #include <cufft.h>
 
+#include <algorithm>
+#include <chrono>
 #include <cstdint>
+#include <cstdlib>
 #include <cstdio>
 #include <map>
 #include <memory>
@@ -81,6 +84,17 @@ struct DevBuf {
 // ---------------------------------------------------------------------------------------
 // Context: device, stream, cached workspaces and cuFFT plans.
 // ---------------------------------------------------------------------------------------
+// Host-side phase trace (env FBMP_TRACE=1): prints the wall time since the previous mark.
+inline void trace(const char* what) {
+    static const bool on = std::getenv("FBMP_TRACE") != nullptr;
+    if (!on) return;
+    using clk = std::chrono::steady_clock;
+    static thread_local clk::time_point last = clk::now();
+    const auto now = clk::now();
+    std::fprintf(stderr, "[fbmp] %-28s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(now - last).count());
+    last = now;
+}
+
 struct Context {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -107,6 +121,13 @@ struct Context {
     }
     cufftHandle plan(int kind, int rows, int cols, int batch);
     void count(int k = 1) { launches += k; }
+    // pinned host staging (grown, never shrunk): cudaMallocHost per call costs 1-300 ms
+    void* pinned(size_t bytes);
+    void* pinned_buf = nullptr;
+    size_t pinned_bytes = 0;
+    cudaEvent_t poll_ev[2] = {nullptr, nullptr};  // CG flag polling
+    // instantiated CG-chunk graphs keyed on their launch parameters (bytes of geometry + pointers)
+    std::map<std::string, cudaGraphExec_t> graphs;
 };
 
 // RAII device selection for calls made from arbitrary host threads.

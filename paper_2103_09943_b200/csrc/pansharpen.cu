@@ -1058,32 +1058,58 @@ void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* 
     const bool prof = ctx.profile;
     std::vector<cudaEvent_t> pev(prof ? chunk * 4 : 0);
     for (auto& e : pev) FBMP_CUDA(cudaEventCreate(&e));
-    cudaGraph_t graph;
-    cudaGraphExec_t exec;
-    FBMP_CUDA(cudaStreamBeginCapture(ctx.stream, cudaStreamCaptureModeThreadLocal));
-    for (int it = 0; it < chunk; ++it) {
-        if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * 4 + 0], ctx.stream, cudaEventRecordExternal));
-        if (q2.fn)
-            q2.fn<<<dim3(nbq, N), fast::NT, sq, ctx.stream>>>(G, d_taps, B.r, B.p, B.q, B.st, part_q, nbq);
-        else
-            k_q<true><<<dim3(nbq, N), NTQ, sq, ctx.stream>>>(G, d_taps, B.r, B.p, B.q, B.st, part_q, nbq);
-        if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * 4 + 1], ctx.stream, cudaEventRecordExternal));
-        if (fastA)
-            launch_apply2<true>(ctx, G, d_taps, d_guide, wmu, wg, B.p, B.q, B.Ap, B.st, part_a);
-        else
-            k_apply<0, true><<<dim3(nba, N), NTA, sa, ctx.stream>>>(G, d_taps, d_guide, B.p, B.q, B.Ap, B.st, part_a, nba);
-        if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * 4 + 2], ctx.stream, cudaEventRecordExternal));
-        k_update<<<dim3(nbu, N), NTU, 0, ctx.stream>>>(G, B.z, B.r, B.p, B.Ap, B.st, part_u, nbu);
-        if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * 4 + 3], ctx.stream, cudaEventRecordExternal));
+    // the chunk graph depends only on geometry, buffers and launch shapes: cache it in the context
+    std::string key;
+    {
+        const void* ptrs[] = {d_taps, d_guide, wmu, wg, B.r, B.p, B.q, B.Ap, B.st, B.z, part_q, part_a, part_u,
+                              reinterpret_cast<const void*>(q2.fn)};
+        const long long dims[] = {nbq, nba, nbu, static_cast<long long>(sq), fastA ? 1 : 0, chunk};
+        key.append(reinterpret_cast<const char*>(&G), sizeof(G));
+        key.append(reinterpret_cast<const char*>(ptrs), sizeof(ptrs));
+        key.append(reinterpret_cast<const char*>(dims), sizeof(dims));
     }
-    FBMP_CUDA(cudaStreamEndCapture(ctx.stream, &graph));
-    FBMP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    trace("cg: setup");
+    cudaGraphExec_t exec = nullptr;
+    auto cached = prof ? ctx.graphs.end() : ctx.graphs.find(key);
+    if (cached != ctx.graphs.end()) {
+        exec = cached->second;
+    } else {
+        cudaGraph_t graph;
+        FBMP_CUDA(cudaStreamBeginCapture(ctx.stream, cudaStreamCaptureModeThreadLocal));
+        for (int it = 0; it < chunk; ++it) {
+            if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * 4 + 0], ctx.stream, cudaEventRecordExternal));
+            if (q2.fn)
+                q2.fn<<<dim3(nbq, N), fast::NT, sq, ctx.stream>>>(G, d_taps, B.r, B.p, B.q, B.st, part_q, nbq);
+            else
+                k_q<true><<<dim3(nbq, N), NTQ, sq, ctx.stream>>>(G, d_taps, B.r, B.p, B.q, B.st, part_q, nbq);
+            if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * 4 + 1], ctx.stream, cudaEventRecordExternal));
+            if (fastA)
+                launch_apply2<true>(ctx, G, d_taps, d_guide, wmu, wg, B.p, B.q, B.Ap, B.st, part_a);
+            else
+                k_apply<0, true><<<dim3(nba, N), NTA, sa, ctx.stream>>>(G, d_taps, d_guide, B.p, B.q, B.Ap, B.st,
+                                                                         part_a, nba);
+            if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * 4 + 2], ctx.stream, cudaEventRecordExternal));
+            k_update<<<dim3(nbu, N), NTU, 0, ctx.stream>>>(G, B.z, B.r, B.p, B.Ap, B.st, part_u, nbu);
+            if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * 4 + 3], ctx.stream, cudaEventRecordExternal));
+        }
+        FBMP_CUDA(cudaStreamEndCapture(ctx.stream, &graph));
+        FBMP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        cudaGraphDestroy(graph);
+        if (!prof) {
+            if (ctx.graphs.size() >= 16) {
+                for (auto& kv : ctx.graphs) cudaGraphExecDestroy(kv.second);
+                ctx.graphs.clear();
+            }
+            ctx.graphs.emplace(key, exec);
+        }
+    }
+    trace("cg: graph");
 
-    CgState* pinned = nullptr;
-    FBMP_CUDA(cudaMallocHost(&pinned, sizeof(CgState) * N * 2));
-    cudaEvent_t ev[2];
-    FBMP_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
-    FBMP_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+    CgState* pinned = static_cast<CgState*>(ctx.pinned(sizeof(CgState) * N * 2));
+    cudaEvent_t* ev = ctx.poll_ev;
+    for (int i = 0; i < 2; ++i)
+        if (!ev[i]) FBMP_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    trace("cg: pinned + events");
     auto all_done = [&](const CgState* s) {
         for (int i = 0; i < N; ++i)
             if (!s[i].done) return false;
@@ -1126,15 +1152,13 @@ void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* 
             ++k;
         }
     }
+    trace("cg: iterate");
     for (auto& e : pev) cudaEventDestroy(e);
     FBMP_CUDA(cudaStreamSynchronize(ctx.stream));
     host_state.resize(N);
     FBMP_CUDA(cudaMemcpy(host_state.data(), B.st, sizeof(CgState) * N, cudaMemcpyDeviceToHost));
-    cudaEventDestroy(ev[0]);
-    cudaEventDestroy(ev[1]);
-    cudaFreeHost(pinned);
-    cudaGraphExecDestroy(exec);
-    cudaGraphDestroy(graph);
+    if (prof) cudaGraphExecDestroy(exec);
+    trace("cg: teardown");
 }
 
 void guided_filter(Context& ctx, int N, int H, int W, int rw, double eps, const double* d_in, int in_is_z0,

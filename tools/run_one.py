@@ -24,4 +24,7 @@ for i in range(reps):
     fbmp.blind_dev(d_l.data_ptr(), N, h, w, d_p.data_ptr(), d_o.data_ptr(), d_k.data_ptr(), cfg.ratio, cfg.support, ctx)
     torch.cuda.synchronize()
     st = ctx.stats()
-    print(f"solve {i}: {1e3 * (time.perf_counter() - t):.2f} ms  fit {st['ms_kernel_fit']:.2f} ms  hrms {st['ms_pansharpen']:.2f} ms", flush=True)
+    print(f"solve {i}: {1e3 * (time.perf_counter() - t):.2f} ms  fit {st['ms_kernel_fit']:.2f} ms  "
+          f"hrms {st['ms_pansharpen']:.2f} ms  admm {st['admm_iters']}  cg {st['cg_iters'][:N]}", flush=True)
+    if os.environ.get("RUN_ONE_SLEEP"):
+        time.sleep(float(os.environ["RUN_ONE_SLEEP"]))

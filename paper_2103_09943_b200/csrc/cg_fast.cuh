@@ -4,7 +4,7 @@
 //       region is split into CF x CF sampling phases in shared memory; every tap becomes an
 //       immediate-offset shared load shared by two vertically adjacent LR points (common
 //       sub-expressions of the unrolled loop), taps are broadcast reads.
-// K_A2: B^T U q + lambda L M L p for all channels of a scene in one CTA (the guide tile and
+// K_A:  B^T U q + lambda L M L p for all channels of a scene in one CTA (the guide tile and
 //       its per-window statistics are loaded once), the matting operator as separable 3x3
 //       box sums:  (M s)_m = n_m s_m - box(c1)_m - I_m box(a)_m  with per-window
 //       a_k = g_k (box(I s)_k / 9 - mu_k box(s)_k / 9),  c1_k = [k interior](box(s)_k/9 - mu_k a_k),
@@ -198,274 +198,18 @@ inline int q2_blocks(const PsGeo& G) {
 }
 
 // ------------------------------------------------------------------------------------------
-// K_A2 (radius 1)
+// K_A (radius 1): one CTA = one 32 x 32 output tile x the channels [group*cpc, +cpc) of a scene
 // ------------------------------------------------------------------------------------------
-namespace a2 {
+namespace a4 {
 constexpr int TA = 32;
-constexpr int WP = TA + 8;   // p on R+4
-constexpr int WI = TA + 6;   // I, s, I*s on R+3
-constexpr int WK = TA + 4;   // window stats on R+2
-constexpr int WM = TA + 2;   // M s on R+1
-constexpr int H1R = WI, H1C = WK;  // first horizontal sums: rows R+3, cols R+2
-constexpr int H2R = WK, H2C = WM;  // second: rows R+2, cols R+1
-constexpr int MAXN = 21;            // kernel side limit of the fast path
-constexpr int O_TAPS = 0;
-constexpr int MAXTAP = 442;         // n <= 21
-constexpr int O_Q = O_TAPS + MAXTAP;
-__host__ __device__ constexpr int maxq(int cf) {  // LR window of the data term
-    return ((TA - 1 + (MAXN - 1)) / cf + 2) * ((TA - 1 + (MAXN - 1)) / cf + 2);
-}
-template <int CF>
-struct L {
-    static constexpr int O_I = O_Q + ((maxq(CF) + 1) / 2) * 2;
-    static constexpr int O_S = O_I + WI * WI;
-    static constexpr int O_U = O_S + WI * WI;          // union: [p | Is] -> [a | c1] -> [M]
-    static constexpr int U_SIZE = WP * WP + WI * WI;   // 1600 + 1444 >= 2 * WK * WK
-    static constexpr int O_H = O_U + U_SIZE;           // horizontal-sum planes / data-term output
-    static constexpr int H_SIZE = 2 * H1R * H1C;
-    static constexpr int O_MU = O_H + H_SIZE;          // per-window guide statistics (once per tile)
-    static constexpr int O_G = O_MU + WK * WK;
-    static constexpr int TOTAL = O_G + WK * WK;
-    static_assert(U_SIZE >= 2 * WK * WK, "union too small");
-    static_assert(H_SIZE >= TA * TA, "output staging too small");
-    static constexpr size_t smem = TOTAL * sizeof(double);
-};
-}  // namespace a2
-
-template <bool CG, int CF>
-__global__ void __launch_bounds__(NT, 2) k_apply2(PsGeo G, const double* __restrict__ taps,
-                                                  const double* __restrict__ guide, const double* __restrict__ wmu,
-                                                  const double* __restrict__ wg, const double* __restrict__ pin,
-                                                  const double* __restrict__ q, double* __restrict__ out, CgState* st,
-                                                  double* __restrict__ part, int nblk) {
-    using namespace a2;
-    __shared__ double red[NT / 32 + 1];
-    extern __shared__ double sm[];
-    const int scene = blockIdx.y;
-    const int H = G.H, W = G.W, n = G.n, C = G.C;
-    const size_t P = static_cast<size_t>(H) * W;
-    const int ntx = (W + TA - 1) / TA;
-    const int by = blockIdx.x / ntx, bx = blockIdx.x - by * ntx;
-    const int r0 = by * TA, c0 = bx * TA;
-    const double* I = guide + scene * P;
-    const double* MU = wmu + scene * P;
-    const double* GK = wg + scene * P;
-    using Lay = L<CF>;
-    double* sk = sm + O_TAPS;
-    double* sq = sm + O_Q;
-    double* sI = sm + Lay::O_I;
-    double* sS = sm + Lay::O_S;
-    double* sU = sm + Lay::O_U;
-    double* sH = sm + Lay::O_H;
-    double* sMu = sm + Lay::O_MU;
-    double* sG = sm + Lay::O_G;
-    const double* tp = taps + static_cast<size_t>(scene) * n * n;
-    for (int e = threadIdx.x; e < n * n; e += NT) sk[e] = tp[e];
-    for (int e = threadIdx.x; e < WI * WI; e += NT) {
-        const int y = e / WI, x = e - y * WI;
-        sI[e] = __ldg(I + static_cast<size_t>(wrap_once(r0 - 3 + y, H)) * W + wrap_once(c0 - 3 + x, W));
-    }
-    for (int e = threadIdx.x; e < WK * WK; e += NT) {
-        const int y = e / WK, x = e - y * WK;
-        const size_t gi = static_cast<size_t>(wrap_once(r0 - 2 + y, H)) * W + wrap_once(c0 - 2 + x, W);
-        sMu[e] = __ldg(MU + gi);
-        sG[e] = __ldg(GK + gi);
-    }
-    // data-term LR window
-    const int iq0 = floordiv(r0 - C + CF - 1, CF), jq0 = floordiv(c0 - C + CF - 1, CF);
-    const int QH = floordiv(r0 + TA - 1 + C, CF) - iq0 + 1, QW = floordiv(c0 + TA - 1 + C, CF) - jq0 + 1;
-    // phase-uniform data-term mapping: item -> (cell column J, 4-cell row block, phase)
-    constexpr int CW = TA / CF;            // cells per tile side
-    constexpr int RB = CW / 4;             // 4-cell row blocks
-    const int it_J = threadIdx.x % CW;
-    const int it_rest = threadIdx.x / CW;
-    const int it_B = it_rest % RB;
-    const int it_ph = it_rest / RB;        // 0 .. CF*CF-1
-    const int pr = it_ph / CF, pc = it_ph - pr * CF;
-    const int dilo = floordiv(pr - C + CF - 1, CF), dihi = floordiv(pr + C, CF);
-    const int djlo = floordiv(pc - C + CF - 1, CF), djhi = floordiv(pc + C, CF);
-
-    for (int chl = 0; chl < G.cps; ++chl) {
-        const int ch = scene * G.cps + chl;
-        if (CG && st[ch].done) continue;
-        const double* p = pin + ch * P;
-        if (CG) p = pin + (static_cast<size_t>(st[ch].t & 1) * G.N + ch) * P;
-        const double* qc = q + static_cast<size_t>(ch) * G.h * G.w;
-        __syncthreads();  // previous channel's readers of the shared buffers are done
-        double* sP = sU;
-        {
-            constexpr int KP = (WP * WP + NT - 1) / NT;
-            double v[KP];
-#pragma unroll
-            for (int k = 0; k < KP; ++k) {
-                const int e = threadIdx.x + k * NT;
-                const int y = e / WP, x = e - y * WP;
-                if (e < WP * WP)
-                    v[k] = __ldg(p + static_cast<size_t>(wrap_once(r0 - 4 + y, H)) * W + wrap_once(c0 - 4 + x, W));
-            }
-#pragma unroll
-            for (int k = 0; k < KP; ++k) {
-                const int e = threadIdx.x + k * NT;
-                if (e < WP * WP) sP[e] = v[k];
-            }
-        }
-        for (int e = threadIdx.x; e < QH * QW; e += NT) {
-            const int a = e / QW, b = e - a * QW;
-            sq[e] = __ldg(qc + static_cast<size_t>(wrapi(iq0 + a, G.h)) * G.w + wrapi(jq0 + b, G.w));
-        }
-        __syncthreads();
-        // own pixels' p (for p.Ap): pixel e = tid + 256 k
-        double pown[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int e = threadIdx.x + NT * k;
-            pown[k] = sP[(e / TA + 4) * WP + (e % TA) + 4];
-        }
-        // stage 1: s = L p and I*s on R+3 (ops.cpp:70-78 stencil order)
-        double* sIS = sU + WP * WP;
-        for (int e = threadIdx.x; e < WI * WI; e += NT) {
-            const int y = e / WI + 1, x = e % WI + 1;
-            const double v = 4.0 * sP[y * WP + x] - sP[(y - 1) * WP + x] - sP[(y + 1) * WP + x] - sP[y * WP + x - 1] -
-                             sP[y * WP + x + 1];
-            sS[e] = v;
-            sIS[e] = sI[e] * v;
-        }
-        __syncthreads();
-        // stage 2: horizontal 3-sums of s and I*s (rows R+3, cols R+2)
-        double* h1 = sH;
-        double* h2 = sH + H1R * H1C;
-        for (int e = threadIdx.x; e < H1R * H1C; e += NT) {
-            const int y = e / H1C, x = e % H1C;
-            const int b = y * WI + x;
-            h1[e] = sS[b] + sS[b + 1] + sS[b + 2];
-            h2[e] = sIS[b] + sIS[b + 1] + sIS[b + 2];
-        }
-        __syncthreads();
-        // stage 3: vertical sums -> per-window a_k, c1_k on R+2
-        double* sA = sU;
-        double* sC = sU + WK * WK;
-        for (int e = threadIdx.x; e < WK * WK; e += NT) {
-            const int y = e / WK, x = e % WK;
-            const int b = y * H1C + x;
-            const double ss = h1[b] + h1[b + H1C] + h1[b + 2 * H1C];
-            const double sis = h2[b] + h2[b + H1C] + h2[b + 2 * H1C];
-            const double mu = sMu[e], g = sG[e];
-            const double xb = ss / 9.0;
-            const double a = g * (sis / 9.0 - mu * xb);
-            sA[e] = a;
-            sC[e] = g != 0.0 ? xb - mu * a : 0.0;
-        }
-        __syncthreads();
-        // stage 4: horizontal 3-sums of a and c1 (rows R+2, cols R+1)
-        h1 = sH;
-        h2 = sH + H2R * H2C;
-        for (int e = threadIdx.x; e < H2R * H2C; e += NT) {
-            const int y = e / H2C, x = e % H2C;
-            const int b = y * WK + x;
-            h1[e] = sA[b] + sA[b + 1] + sA[b + 2];
-            h2[e] = sC[b] + sC[b + 1] + sC[b + 2];
-        }
-        __syncthreads();
-        // stage 5: M s on R+1 = n_m s_m - box(c1) - I_m box(a)
-        double* sM = sU;
-        for (int e = threadIdx.x; e < WM * WM; e += NT) {
-            const int y = e / WM, x = e % WM;
-            const int b = y * H2C + x;
-            const double ba = h1[b] + h1[b + H2C] + h1[b + 2 * H2C];
-            const double bc = h2[b] + h2[b + H2C] + h2[b + 2 * H2C];
-            const int gr = wrap_once(r0 - 1 + y, H), gc = wrap_once(c0 - 1 + x, W);
-            const int nr = min(gr + 1, H - 2) - max(gr - 1, 1) + 1;  // interior window rows covering gr
-            const int nc = min(gc + 1, W - 2) - max(gc - 1, 1) + 1;
-            const double nm = static_cast<double>(max(nr, 0) * max(nc, 0));
-            const int si = (y + 2) * WI + x + 2;
-            sM[e] = nm * sS[si] - bc - sI[si] * ba;
-        }
-        __syncthreads();
-        // stage 6a: data term per sampling phase (4 cells per thread along rows) -> sO
-        double* sO = sH;
-        {
-            const int Jc = it_J;
-            const int Ic0 = it_B * 4;
-            // global LR index of the cell (c0/CF + Jc), row cells (r0/CF + Ic0 + k)
-            const int qj0 = c0 / CF + Jc - jq0;
-            const int qi0 = r0 / CF + Ic0 - iq0;
-            double acc[4] = {0.0, 0.0, 0.0, 0.0};
-            for (int di = dilo; di <= dihi; ++di) {
-                const double* krow = sk + (CF * di - pr + C) * n + C - pc;
-                for (int dj = djlo; dj <= djhi; ++dj) {
-                    const double kv = krow[CF * dj];
-                    const double* qq = sq + (qi0 + di) * QW + qj0 + dj;
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) acc[k] = fma(kv, qq[k * QW], acc[k]);
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) sO[((Ic0 + k) * CF + pr) * TA + Jc * CF + pc] = acc[k];
-        }
-        __syncthreads();
-        // stage 6b: t = L(M s), Ap = data + lambda t, p.Ap
-        double* oc = out + ch * P;
-        double dotp = 0.0;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int e = threadIdx.x + NT * k;
-            const int y = e / TA, x = e % TA;
-            const int R = r0 + y, Cc = c0 + x;
-            const int m = (y + 1) * WM + x + 1;
-            const double tl = 4.0 * sM[m] - sM[m - WM] - sM[m + WM] - sM[m - 1] - sM[m + 1];
-            const double val = sO[e] + tl * G.lambda;
-            if (R < H && Cc < W) {
-                oc[static_cast<size_t>(R) * W + Cc] = val;
-                dotp += pown[k] * val;
-            }
-        }
-        if (CG) {
-            const double bs = block_sum<NT>(dotp, red);
-            if (threadIdx.x == 0) part[static_cast<size_t>(ch) * nblk + blockIdx.x] = bs;
-            if (elect_last_block(&st[ch].cnt_a, nblk)) {
-                const double pAp = sum_partials<NT>(part + static_cast<size_t>(ch) * nblk, nblk, 1, red);
-                if (threadIdx.x == 0) {
-                    CgState& S = st[ch];
-                    S.pAp = pAp;
-                    if (!(pAp > 0)) {  // pansharpen.cpp:240-244
-                        S.done = (sqrt(S.rs) <= 1e-12 * S.rhs_norm) ? 1 : 2;
-                        S.iters = S.t + 1;
-                    } else {
-                        S.alpha = S.rs / pAp;
-                    }
-                    S.cnt_a = 0;
-                }
-            }
-        }
-    }
-}
-
-
-// ------------------------------------------------------------------------------------------
-// K_A3: K_A2 restructured for shared-memory traffic. Every stage works on a 2 x 4 register
-// micro-tile (horizontal and vertical 3-sums fused), I*s is formed on the fly, and the data
-// term keeps the thread's zero-padded sampling-phase sub-kernel in registers (N_, CF known
-// at compile time; N_ = 0 keeps the generic broadcast-tap loop).
-// ------------------------------------------------------------------------------------------
-namespace a3 {
-constexpr int TA = 32;
-constexpr int WP = TA + 8, WI = TA + 6, WK = TA + 4, WM = TA + 2;
-template <int CF>
-struct L {
-    static constexpr int QMAX = a2::maxq(CF);
-    static constexpr int O_TAPS = 0;                       // generic path only
-    static constexpr int O_I = O_TAPS + a2::MAXTAP;        // guide on R+3
-    static constexpr int O_MU = O_I + WI * WI;             // mu_k on R+2
-    static constexpr int O_G = O_MU + WK * WK;             // g_k on R+2
-    static constexpr int O_S = O_G + WK * WK;              // s on R+3
-    static constexpr int O_M = O_S + WI * WI;              // M s on R+1
-    static constexpr int O_Q = O_M + WM * WM;              // q window
-    static constexpr int O_U = O_Q + ((QMAX + 1) / 2) * 2; // p on R+4 -> (a, c1) on R+2 -> data out
-    static constexpr int U_SIZE = 2 * WK * WK;
-    static constexpr int TOTAL = O_U + U_SIZE;
-    static_assert(U_SIZE >= WP * WP && U_SIZE >= TA * TA, "union too small");
-    static constexpr size_t smem = TOTAL * sizeof(double);
-};
+constexpr int MAXN = 21;      // kernel side limit of the fast path
+constexpr int MAXTAP = 442;   // n <= 21, even
+constexpr int MAXCPC = 32;    // channels per CTA (per-channel warp partials of p.Ap)
+// region widths: p on R+4, I / s / I*s on R+3, window statistics on R+2, M s on R+1
+constexpr int RP = TA + 8, RI = TA + 6, RK = TA + 4, RM = TA + 2;
+// padded row strides (even: 16-byte column pairs). tools/bank_sim.py: with the stage thread
+// maps below they make the 128-bit accesses of S1, S3, S5 conflict-free (S2 keeps 1.3x).
+constexpr int SP = 50, SI = 50, SK = 38, SMS = 38, SO = TA;
 template <int N_, int CF>
 struct DT {  // zero-padded sub-kernel extent of the data term
     static constexpr int C = (N_ - 1) / 2;
@@ -473,335 +217,36 @@ struct DT {  // zero-padded sub-kernel extent of the data term
     static constexpr int DHI = (CF - 1 + C) / CF;
     static constexpr int DM = DHI - DLO + 1;
 };
-}  // namespace a3
-
-template <bool CG, int N_, int CF>
-__global__ void __launch_bounds__(NT, 2) k_apply3(PsGeo G, const double* __restrict__ taps,
-                                                  const double* __restrict__ guide, const double* __restrict__ wmu,
-                                                  const double* __restrict__ wg, const double* __restrict__ pin,
-                                                  const double* __restrict__ q, double* __restrict__ out, CgState* st,
-                                                  double* __restrict__ part, int nblk) {
-    using namespace a3;
-    using Lay = L<CF>;
-    __shared__ double red[NT / 32 + 1];
-    extern __shared__ double sm[];
-    const int scene = blockIdx.y;
-    const int H = G.H, W = G.W, n = G.n, C = G.C;
-    const size_t P = static_cast<size_t>(H) * W;
-    const int ntx = (W + TA - 1) / TA;
-    const int by = blockIdx.x / ntx, bx = blockIdx.x - by * ntx;
-    const int r0 = by * TA, c0 = bx * TA;
-    double* sk = sm + Lay::O_TAPS;
-    double* sI = sm + Lay::O_I;
-    double* sMu = sm + Lay::O_MU;
-    double* sG = sm + Lay::O_G;
-    double* sS = sm + Lay::O_S;
-    double* sM = sm + Lay::O_M;
-    double* sq = sm + Lay::O_Q;
-    double* sU = sm + Lay::O_U;
-    const double* tp = taps + static_cast<size_t>(scene) * n * n;
-    {
-        const double* I = guide + scene * P;
-        const double* MU = wmu + scene * P;
-        const double* GK = wg + scene * P;
-        if (N_ == 0)
-            for (int e = threadIdx.x; e < n * n; e += NT) sk[e] = tp[e];
-        constexpr int KI = (WI * WI + NT - 1) / NT, KK = (WK * WK + NT - 1) / NT;
-        double vi[KI], vm[KK], vg[KK];
-#pragma unroll
-        for (int k = 0; k < KI; ++k) {
-            const int e = threadIdx.x + k * NT;
-            const int y = e / WI, x = e - y * WI;
-            if (e < WI * WI) vi[k] = __ldg(I + static_cast<size_t>(wrap_once(r0 - 3 + y, H)) * W + wrap_once(c0 - 3 + x, W));
-        }
-#pragma unroll
-        for (int k = 0; k < KK; ++k) {
-            const int e = threadIdx.x + k * NT;
-            const int y = e / WK, x = e - y * WK;
-            const size_t gi = static_cast<size_t>(wrap_once(r0 - 2 + y, H)) * W + wrap_once(c0 - 2 + x, W);
-            if (e < WK * WK) {
-                vm[k] = __ldg(MU + gi);
-                vg[k] = __ldg(GK + gi);
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < KI; ++k)
-            if (threadIdx.x + k * NT < WI * WI) sI[threadIdx.x + k * NT] = vi[k];
-#pragma unroll
-        for (int k = 0; k < KK; ++k)
-            if (threadIdx.x + k * NT < WK * WK) {
-                sMu[threadIdx.x + k * NT] = vm[k];
-                sG[threadIdx.x + k * NT] = vg[k];
-            }
-    }
-    // data-term work item: (cell column, 4-cell row block, sampling phase)
-    constexpr int CW = TA / CF, RB = CW / 4;
-    const int it_J = threadIdx.x % CW;
-    const int it_rest = threadIdx.x / CW;
-    const int it_B = it_rest % RB;
-    const int it_ph = it_rest / RB;
-    const int pr = it_ph / CF, pc = it_ph - pr * CF;
-    using D = a3::DT<(N_ > 0 ? N_ : 1), CF>;
-    constexpr int DM = N_ > 0 ? D::DM : 1;
-    double kreg[DM][DM];
-    if (N_ > 0) {
-#pragma unroll
-        for (int a = 0; a < DM; ++a)
-#pragma unroll
-            for (int b = 0; b < DM; ++b) {
-                const int tr = CF * (a + D::DLO) - pr + D::C, tc = CF * (b + D::DLO) - pc + D::C;
-                kreg[a][b] = (tr >= 0 && tr < N_ && tc >= 0 && tc < N_) ? __ldg(tp + tr * N_ + tc) : 0.0;
-            }
-    }
-    const int iq0 = floordiv(r0 - C + CF - 1, CF), jq0 = floordiv(c0 - C + CF - 1, CF);
-    const int QH = floordiv(r0 + TA - 1 + C, CF) - iq0 + 1, QW = floordiv(c0 + TA - 1 + C, CF) - jq0 + 1;
-    const int dilo = floordiv(pr - C + CF - 1, CF), dihi = floordiv(pr + C, CF);
-    const int djlo = floordiv(pc - C + CF - 1, CF), djhi = floordiv(pc + C, CF);
-    // micro-tile coordinates (2 rows x 4 cols per thread)
-    const int mt_y = 2 * (threadIdx.x / 10), mt_x = 4 * (threadIdx.x % 10);
-
-    for (int chl = 0; chl < G.cps; ++chl) {
-        const int ch = scene * G.cps + chl;
-        if (CG && st[ch].done) continue;
-        const double* p = pin + ch * P;
-        if (CG) p = pin + (static_cast<size_t>(st[ch].t & 1) * G.N + ch) * P;
-        const double* qc = q + static_cast<size_t>(ch) * G.h * G.w;
-        __syncthreads();  // previous channel finished with the shared buffers
-        double* sP = sU;
-        {
-            constexpr int KP = (WP * WP + NT - 1) / NT;
-            double v[KP];
-#pragma unroll
-            for (int k = 0; k < KP; ++k) {
-                const int e = threadIdx.x + k * NT;
-                const int y = e / WP, x = e - y * WP;
-                if (e < WP * WP)
-                    v[k] = __ldg(p + static_cast<size_t>(wrap_once(r0 - 4 + y, H)) * W + wrap_once(c0 - 4 + x, W));
-            }
-#pragma unroll
-            for (int k = 0; k < KP; ++k)
-                if (threadIdx.x + k * NT < WP * WP) sP[threadIdx.x + k * NT] = v[k];
-        }
-        for (int e = threadIdx.x; e < QH * QW; e += NT) {
-            const int a = e / QW, b = e - a * QW;
-            sq[e] = __ldg(qc + static_cast<size_t>(wrapi(iq0 + a, G.h)) * G.w + wrapi(jq0 + b, G.w));
-        }
-        __syncthreads();
-        // own pixels' p for p.Ap, in the S5 mapping (row tid/8, columns 4 (tid%8) + j)
-        double pown[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) pown[j] = sP[(threadIdx.x / 8 + 4) * WP + 4 * (threadIdx.x % 8) + j + 4];
-        // S1: s = L p on R+3 (micro-tile 2 x 4; 19 x 10 tiles)
-        if (threadIdx.x < 190) {
-            double pv[4][6];
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 6; ++j) pv[i][j] = sP[(mt_y + i) * WP + mt_x + j];
-#pragma unroll
-            for (int i = 0; i < 2; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int y = mt_y + i, x = mt_x + j;
-                    if (y < WI && x < WI)  // ops.cpp:70-78 stencil order
-                        sS[y * WI + x] = 4.0 * pv[i + 1][j + 1] - pv[i][j + 1] - pv[i + 2][j + 1] - pv[i + 1][j] -
-                                         pv[i + 1][j + 2];
-                }
-        }
-        __syncthreads();
-        // S2: per-window a_k, c1_k on R+2 (micro-tile 2 x 4; 18 x 9 tiles)
-        double* sA = sU;
-        double* sC = sU + WK * WK;
-        if (threadIdx.x < 162) {
-            const int wy = 2 * (threadIdx.x / 9), wx = 4 * (threadIdx.x % 9);
-            double hs[4][4], hi[4][4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                double sv[6], iv[6];
-#pragma unroll
-                for (int j = 0; j < 6; ++j) {
-                    const int o = (wy + i) * WI + wx + j;
-                    sv[j] = (wy + i < WI && wx + j < WI) ? sS[o] : 0.0;
-                    iv[j] = (wy + i < WI && wx + j < WI) ? sI[o] * sv[j] : 0.0;
-                }
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    hs[i][j] = sv[j] + sv[j + 1] + sv[j + 2];
-                    hi[i][j] = iv[j] + iv[j + 1] + iv[j + 2];
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < 2; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int y = wy + i, x = wx + j;
-                    if (y < WK && x < WK) {
-                        const double ss = hs[i][j] + hs[i + 1][j] + hs[i + 2][j];
-                        const double sis = hi[i][j] + hi[i + 1][j] + hi[i + 2][j];
-                        const double mu = sMu[y * WK + x], g = sG[y * WK + x];
-                        const double xb = ss / 9.0;
-                        const double a = g * (sis / 9.0 - mu * xb);
-                        sA[y * WK + x] = a;
-                        sC[y * WK + x] = g != 0.0 ? xb - mu * a : 0.0;
-                    }
-                }
-        }
-        __syncthreads();
-        // S3: M s on R+1 = n_m s_m - box(c1) - I_m box(a) (micro-tile 2 x 4; 17 x 9 tiles)
-        if (threadIdx.x < 153) {
-            const int my = 2 * (threadIdx.x / 9), mx = 4 * (threadIdx.x % 9);
-            double ha[4][4], hc[4][4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                double av[6], cv[6];
-#pragma unroll
-                for (int j = 0; j < 6; ++j) {
-                    const int o = (my + i) * WK + mx + j;
-                    const bool ok = my + i < WK && mx + j < WK;
-                    av[j] = ok ? sA[o] : 0.0;
-                    cv[j] = ok ? sC[o] : 0.0;
-                }
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    ha[i][j] = av[j] + av[j + 1] + av[j + 2];
-                    hc[i][j] = cv[j] + cv[j + 1] + cv[j + 2];
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                const int y = my + i;
-                const int gr = wrap_once(r0 - 1 + y, H);
-                const int nr = max(min(gr + 1, H - 2) - max(gr - 1, 1) + 1, 0);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int x = mx + j;
-                    if (y < WM && x < WM) {
-                        const double ba = ha[i][j] + ha[i + 1][j] + ha[i + 2][j];
-                        const double bc = hc[i][j] + hc[i + 1][j] + hc[i + 2][j];
-                        const int gc = wrap_once(c0 - 1 + x, W);
-                        const int nc = max(min(gc + 1, W - 2) - max(gc - 1, 1) + 1, 0);
-                        const int si = (y + 2) * WI + x + 2;
-                        sM[y * WM + x] = static_cast<double>(nr * nc) * sS[si] - bc - sI[si] * ba;
-                    }
-                }
-            }
-        }
-        __syncthreads();
-        // S4: data term per sampling phase -> sO (4 cells along rows per thread)
-        double* sO = sU;
-        {
-            const int Jc = it_J, Ic0 = it_B * 4;
-            const int qj0 = c0 / CF + Jc - jq0, qi0 = r0 / CF + Ic0 - iq0;
-            double acc[4] = {0.0, 0.0, 0.0, 0.0};
-            if (N_ > 0) {
-#pragma unroll
-                for (int m = 0; m < DM + 3; ++m) {
-                    double qv[DM];
-                    const double* qrow = sq + (qi0 + D::DLO + m) * QW + qj0 + D::DLO;
-#pragma unroll
-                    for (int b = 0; b < DM; ++b) qv[b] = qrow[b];
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const int a = m - k;
-                        if (a >= 0 && a < DM) {
-#pragma unroll
-                            for (int b = 0; b < DM; ++b) acc[k] = fma(kreg[a][b], qv[b], acc[k]);
-                        }
-                    }
-                }
-            } else {
-                for (int di = dilo; di <= dihi; ++di) {
-                    const double* krow = sk + (CF * di - pr + C) * n + C - pc;
-                    for (int dj = djlo; dj <= djhi; ++dj) {
-                        const double kv = krow[CF * dj];
-                        const double* qq = sq + (qi0 + di) * QW + qj0 + dj;
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) acc[k] = fma(kv, qq[k * QW], acc[k]);
-                    }
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) sO[((Ic0 + k) * CF + pr) * TA + Jc * CF + pc] = acc[k];
-        }
-        __syncthreads();
-        // S5: t = L(M s), Ap = data + lambda t, p.Ap (1 x 4 per thread)
-        double* oc = out + ch * P;
-        double dotp = 0.0;
-        {
-            const int y = threadIdx.x / 8, x0 = 4 * (threadIdx.x % 8);
-            double mv[3][6];
-#pragma unroll
-            for (int i = 0; i < 3; ++i)
-#pragma unroll
-                for (int j = 0; j < 6; ++j) mv[i][j] = sM[(y + i) * WM + x0 + j];
-            const int R = r0 + y;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const double tl = 4.0 * mv[1][j + 1] - mv[0][j + 1] - mv[2][j + 1] - mv[1][j] - mv[1][j + 2];
-                const double val = sO[y * TA + x0 + j] + tl * G.lambda;
-                const int Cc = c0 + x0 + j;
-                if (R < H && Cc < W) {
-                    oc[static_cast<size_t>(R) * W + Cc] = val;
-                    dotp += pown[j] * val;
-                }
-            }
-        }
-        if (CG) {
-            const double bs = block_sum<NT>(dotp, red);
-            if (threadIdx.x == 0) part[static_cast<size_t>(ch) * nblk + blockIdx.x] = bs;
-            if (elect_last_block(&st[ch].cnt_a, nblk)) {
-                const double pAp = sum_partials<NT>(part + static_cast<size_t>(ch) * nblk, nblk, 1, red);
-                if (threadIdx.x == 0) {
-                    CgState& S = st[ch];
-                    S.pAp = pAp;
-                    if (!(pAp > 0)) {  // pansharpen.cpp:240-244
-                        S.done = (sqrt(S.rs) <= 1e-12 * S.rhs_norm) ? 1 : 2;
-                        S.iters = S.t + 1;
-                    } else {
-                        S.alpha = S.rs / pAp;
-                    }
-                    S.cnt_a = 0;
-                }
-            }
-        }
-    }
-}
-
-
-// ------------------------------------------------------------------------------------------
-// K_A4: K_A3 with conflict-free column strips. Every stage maps lanes to consecutive columns
-// and walks a strip of rows with the vertical 3-sums in a register sliding window, so each
-// shared load is a stride-1 (conflict-free) warp access and reused vertically.
-// ------------------------------------------------------------------------------------------
-namespace a4 {
-constexpr int TA = 32;
-constexpr int WP = TA + 8, WI = TA + 6, WK = TA + 4, WM = TA + 2;
-// stage strips over column PAIRS: S1 19 x 13 strips x 3 rows, S2 18 x 14 x 3, S3 17 x 15 x 3,
-// S5 16 x 16 x 2
-static_assert(19 * 13 <= NT && 18 * 14 <= NT && 17 * 15 <= NT && 16 * 16 == NT && TA == 32, "strips");
+__host__ __device__ constexpr int qwmax(int cf) { return (TA - 1 + 2 * (MAXN / 2)) / cf + 2; }
 template <int CF>
 struct L {
-    static constexpr int QMAX = a2::maxq(CF);
+    static constexpr int QWMAX = qwmax(CF);
+    static constexpr int QWP = QWMAX + ((8 - QWMAX % 16) + 16) % 16;   // q row stride
     static constexpr int O_TAPS = 0;
-    static constexpr int O_I = O_TAPS + a2::MAXTAP;        // guide on R+3
-    static constexpr int O_MU = O_I + WI * WI;             // mu_k on R+2
-    static constexpr int O_G = O_MU + WK * WK;             // g_k on R+2
-    static constexpr int O_S = O_G + WK * WK;              // s on R+3
-    static constexpr int O_M = O_S + WI * WI;              // I*s on R+3, then M s on R+1
-    static constexpr int O_Q = O_M + WI * WI;              // q window
-    static constexpr int QWMAX = (TA - 1 + 2 * (a2::MAXN / 2)) / CF + 2;
-    static constexpr int QWP = QWMAX + ((8 - QWMAX % 16) + 16) % 16;   // row stride == 8 (mod 16)
-    static constexpr int O_U = O_Q + QWP * QWMAX;          // p on R+4 -> (a, c1) on R+2
-    static constexpr int U_SIZE = 2 * WK * WK;
-    static constexpr int O_O = O_U + U_SIZE;               // data term out (TA x TA)
-    static constexpr int TOTAL = O_O + TA * TA;
-    static_assert(U_SIZE >= WP * WP, "union too small");
+    static constexpr int O_I = O_TAPS + MAXTAP;             // guide on R+3
+    static constexpr int O_MU = O_I + RI * SI;              // mu_k on R+2
+    static constexpr int O_G = O_MU + RK * SK;              // g_k on R+2
+    static constexpr int O_S = O_G + RK * SK;               // s on R+3
+    static constexpr int O_M = O_S + RI * SI;               // I*s on R+3, then M s on R+1
+    static constexpr int O_Q = O_M + RI * SI;               // q window
+    static constexpr int O_U = O_Q + ((QWP * QWMAX + 1) / 2) * 2;  // p on R+4 -> (a, c1) on R+2
+    static constexpr int U_SIZE = (RP * SP > 2 * RK * SK) ? RP * SP : 2 * RK * SK;
+    static constexpr int O_O = O_U + U_SIZE;                // data term (TA x TA)
+    static constexpr int TOTAL = O_O + TA * SO;
+    static_assert(RM * SMS <= RI * SI, "M s must fit in the I*s buffer");
     static_assert(O_I % 2 == 0 && O_MU % 2 == 0 && O_G % 2 == 0 && O_S % 2 == 0 && O_M % 2 == 0 &&
-                  O_Q % 2 == 0 && O_U % 2 == 0 && O_O % 2 == 0 && WK * WK % 2 == 0, "16-byte pair alignment");
+                  O_Q % 2 == 0 && O_U % 2 == 0 && O_O % 2 == 0 && (RK * SK) % 2 == 0, "16-byte pair alignment");
     static constexpr size_t smem = TOTAL * sizeof(double);
 };
+// stage thread maps over column PAIRS: S1 19 pairs x 13 strips x 3 rows, S2 18 x 14 x 3,
+// S3 17 x 15 x 3, S5 16 x 16 x 2
+static_assert(19 * 13 <= NT && 18 * 14 <= NT && 17 * 15 <= NT && 16 * 16 == NT && TA == 32, "stage maps");
 }  // namespace a4
 
+// K_A: Ap = B^T U q + lambda L M L p and, for CG, p.Ap (pansharpen.cpp:218-223, :236-239).
+// Per channel: S4 data term, S1 s = L p and I s, S2 window coefficients (a, c1), S3 M s,
+// S5 t = L M s and the output. The p.Ap partials of all channels are published once at the end
+// of the CTA (one fence, one arrival per channel); the last CTA of a channel reduces them.
 template <bool CG, int N_, int CF>
 __global__ void __launch_bounds__(NT, 2) k_apply4(PsGeo G, const double* __restrict__ taps,
                                                   const double* __restrict__ guide, const double* __restrict__ wmu,
@@ -810,7 +255,10 @@ __global__ void __launch_bounds__(NT, 2) k_apply4(PsGeo G, const double* __restr
                                                   double* __restrict__ part, int nblk) {
     using namespace a4;
     using Lay = a4::L<CF>;
+    static_assert(N_ == 0 || CF == 4, "register data term is specialised for factor 4");
     __shared__ double red[NT / 32 + 1];
+    __shared__ double wsum[CG ? MAXCPC : 1][NT / 32];
+    __shared__ unsigned int last_mask;
     extern __shared__ double sm[];
     // blockIdx.y = scene * cgroups + group: the CTA handles channels [group*cpc, group*cpc+cpc)
     const int cgroups = (G.cps + G.cpc - 1) / G.cpc;
@@ -829,21 +277,20 @@ __global__ void __launch_bounds__(NT, 2) k_apply4(PsGeo G, const double* __restr
     double* sM = sm + Lay::O_M;
     double* sq = sm + Lay::O_Q;
     double* sU = sm + Lay::O_U;
+    double* sO = sm + Lay::O_O;
     const double* tp = taps + static_cast<size_t>(scene) * n * n;
-    // data term: output u = 128 warp + 32 k + lane (k = 0..3) -> (sampling phase, cell); the
-    // phase is uniform across a warp, so taps are broadcast reads
-    constexpr int CPR = TA / CF, CPP = CPR * CPR;  // cells per row / per phase
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int iq0 = floordiv(r0 - C + CF - 1, CF), jq0 = floordiv(c0 - C + CF - 1, CF);
     const int QH = floordiv(r0 + TA - 1 + C, CF) - iq0 + 1, QW = floordiv(c0 + TA - 1 + C, CF) - jq0 + 1;
-    constexpr int QS = Lay::QWP;  // padded row stride of the q window
-    using D = a3::DT<(N_ > 0 ? N_ : 1), CF>;
+    constexpr int QS = Lay::QWP;
+    using D = DT<(N_ > 0 ? N_ : 1), CF>;
     constexpr int DM = N_ > 0 ? D::DM : 1;
     const int ch_lo = group * G.cpc, ch_hi = min(G.cps, group * G.cpc + G.cpc);
-    constexpr int KP = (WP * WP + NT - 1) / NT;
+    constexpr int KP = (RP * RP + NT - 1) / NT;
     const int QN = QH * QW;
     constexpr int KQ = (Lay::QWMAX * Lay::QWMAX + NT - 1) / NT;
     double pf_p[KP], pf_q[KQ];
+    if (CG && threadIdx.x == 0) last_mask = 0u;
     // issue the loads of channel `chl`'s p (R+4) and q windows into registers
     auto prefetch = [&](int chl) {
         const int ch = scene * G.cps + chl;
@@ -853,9 +300,9 @@ __global__ void __launch_bounds__(NT, 2) k_apply4(PsGeo G, const double* __restr
 #pragma unroll
         for (int k = 0; k < KP; ++k) {
             const int e = threadIdx.x + k * NT;
-            const int y = e / WP, x = e - y * WP;
+            const int y = e / RP, x = e - y * RP;
             pf_p[k] = 0.0;
-            if (e < WP * WP && !(G.dbg & 32))
+            if (e < RP * RP && !(G.dbg & 32))
                 pf_p[k] = __ldg(pp + static_cast<size_t>(wrap_once(r0 - 4 + y, H)) * W + wrap_once(c0 - 4 + x, W));
         }
 #pragma unroll
@@ -875,20 +322,20 @@ __global__ void __launch_bounds__(NT, 2) k_apply4(PsGeo G, const double* __restr
     const double* MU = wmu + scene * P;
     const double* GK = wg + scene * P;
     for (int e = threadIdx.x; e < n * n; e += NT) sk[e] = tp[e];
-    constexpr int KI = (WI * WI + NT - 1) / NT, KK = (WK * WK + NT - 1) / NT;
+    constexpr int KI = (RI * RI + NT - 1) / NT, KK = (RK * RK + NT - 1) / NT;
     double vi[KI], vm[KK], vg[KK];
 #pragma unroll
     for (int k = 0; k < KI; ++k) {
         const int e = threadIdx.x + k * NT;
-        const int y = e / WI, x = e - y * WI;
-        if (e < WI * WI) vi[k] = __ldg(I + static_cast<size_t>(wrap_once(r0 - 3 + y, H)) * W + wrap_once(c0 - 3 + x, W));
+        const int y = e / RI, x = e - y * RI;
+        if (e < RI * RI) vi[k] = __ldg(I + static_cast<size_t>(wrap_once(r0 - 3 + y, H)) * W + wrap_once(c0 - 3 + x, W));
     }
 #pragma unroll
     for (int k = 0; k < KK; ++k) {
         const int e = threadIdx.x + k * NT;
-        const int y = e / WK, x = e - y * WK;
+        const int y = e / RK, x = e - y * RK;
         const size_t gi = static_cast<size_t>(wrap_once(r0 - 2 + y, H)) * W + wrap_once(c0 - 2 + x, W);
-        if (e < WK * WK) {
+        if (e < RK * RK) {
             vm[k] = __ldg(MU + gi);
             vg[k] = __ldg(GK + gi);
         }
@@ -896,22 +343,32 @@ __global__ void __launch_bounds__(NT, 2) k_apply4(PsGeo G, const double* __restr
     int cur = next_active(ch_lo);
     if (cur < ch_hi) prefetch(cur);  // first channel's p / q in flight with the guide tile
 #pragma unroll
-    for (int k = 0; k < KI; ++k)
-        if (threadIdx.x + k * NT < WI * WI) sI[threadIdx.x + k * NT] = vi[k];
+    for (int k = 0; k < KI; ++k) {
+        const int e = threadIdx.x + k * NT;
+        const int y = e / RI, x = e - y * RI;
+        if (e < RI * RI) sI[y * SI + x] = vi[k];
+    }
 #pragma unroll
-    for (int k = 0; k < KK; ++k)
-        if (threadIdx.x + k * NT < WK * WK) {
-            sMu[threadIdx.x + k * NT] = vm[k];
-            sG[threadIdx.x + k * NT] = vg[k];
+    for (int k = 0; k < KK; ++k) {
+        const int e = threadIdx.x + k * NT;
+        const int y = e / RK, x = e - y * RK;
+        if (e < RK * RK) {
+            sMu[y * SK + x] = vm[k];
+            sG[y * SK + x] = vg[k];
         }
+    }
 
+    unsigned int processed = 0u;  // local channels this CTA applied the operator to
     for (int chl = cur; chl < ch_hi; chl = cur) {
         const int ch = scene * G.cps + chl;
         __syncthreads();  // previous channel finished with the shared buffers
         double* sP = sU;
 #pragma unroll
-        for (int k = 0; k < KP; ++k)
-            if (threadIdx.x + k * NT < WP * WP) sP[threadIdx.x + k * NT] = pf_p[k];
+        for (int k = 0; k < KP; ++k) {
+            const int e = threadIdx.x + k * NT;
+            const int y = e / RP, x = e - y * RP;
+            if (e < RP * RP) sP[y * SP + x] = pf_p[k];
+        }
 #pragma unroll
         for (int k = 0; k < KQ; ++k) {
             const int e = threadIdx.x + k * NT;
@@ -923,22 +380,22 @@ __global__ void __launch_bounds__(NT, 2) k_apply4(PsGeo G, const double* __restr
         cur = next_active(chl + 1);
         if (cur < ch_hi) prefetch(cur);  // in flight during this channel's stages
         __syncthreads();
-        // own pixels' p for p.Ap in the S5 mapping (column pair 2 (tid % 16), rows 2 (tid / 16) + {0,1})
+        // own pixels' p for p.Ap in the S5 map (column pair 2 (tid % 16), rows 2 (tid / 16) + {0,1})
         double2 pown[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i)
-            pown[i] = ld2(sP + (2 * (threadIdx.x >> 4) + i + 4) * WP + 2 * (threadIdx.x & 15) + 4);
+            pown[i] = ld2(sP + (2 * (threadIdx.x >> 4) + i + 4) * SP + 2 * (threadIdx.x & 15) + 4);
         // S4: data term (needs only q; writes its own buffer, so it runs before S1 without a barrier)
-        double* sO = sm + Lay::O_O;
         if (N_ > 0 && !(G.dbg & 1)) {
-            // thread = (phase, cell column, 4 cell rows); zero-padded phase sub-kernel in registers,
-            // q rows slide through registers (each q value loaded once per thread)
+            // thread = (column phase pc, cell column Jc, 4 cell rows, row phase pr): a warp covers
+            // 32 consecutive output columns (conflict-free stores; q loads shared by the 4 pc lanes);
+            // the zero-padded phase sub-kernel sits in registers, q rows slide through registers
             constexpr int CW4 = TA / CF, RB4 = CW4 / 4;
-            const int Jc = threadIdx.x % CW4;
-            const int rest = threadIdx.x / CW4;
+            const int pc = threadIdx.x % CF;
+            const int Jc = (threadIdx.x / CF) % CW4;
+            const int rest = threadIdx.x / (CF * CW4);
             const int Ic0 = (rest % RB4) * 4;
-            const int ph = rest / RB4;
-            const int pr = ph / CF, pc = ph - pr * CF;
+            const int pr = rest / RB4;
             double kreg[DM][DM];
 #pragma unroll
             for (int a = 0; a < DM; ++a)
@@ -964,8 +421,11 @@ __global__ void __launch_bounds__(NT, 2) k_apply4(PsGeo G, const double* __restr
                 }
             }
 #pragma unroll
-            for (int k = 0; k < 4; ++k) sO[((Ic0 + k) * CF + pr) * TA + Jc * CF + pc] = acc[k];
+            for (int k = 0; k < 4; ++k) sO[((Ic0 + k) * CF + pr) * SO + Jc * CF + pc] = acc[k];
         } else if (!(G.dbg & 1)) {
+            // generic taps: output u = 128 warp + 32 k + lane -> (sampling phase, cell); the phase
+            // is uniform across a warp, so taps are broadcast reads
+            constexpr int CPR = TA / CF, CPP = CPR * CPR;  // cells per row / per phase
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int u = 128 * warp + 32 * k + lane;
@@ -981,7 +441,7 @@ __global__ void __launch_bounds__(NT, 2) k_apply4(PsGeo G, const double* __restr
                     const double* qrow = qb + di * QS;
                     for (int dj = djlo; dj <= djhi; ++dj) acc = fma(krow[CF * dj], qrow[dj], acc);
                 }
-                sO[(ci * CF + pr) * TA + cj * CF + pc] = acc;
+                sO[(ci * CF + pr) * SO + cj * CF + pc] = acc;
             }
         }
         // S1-S3 and S5 work on column PAIRS (16-byte shared accesses, conflict-free) and walk short
@@ -989,19 +449,19 @@ __global__ void __launch_bounds__(NT, 2) k_apply4(PsGeo G, const double* __restr
         // S1: s = L p and I*s on R+3
         if (threadIdx.x < 19 * 13 && !(G.dbg & 2)) {
             const int xp = 2 * (threadIdx.x % 19), y0 = 3 * (threadIdx.x / 19);
-            double2 a0 = ld2(sP + y0 * WP + xp), a1 = ld2(sP + y0 * WP + xp + 2);        // p rows y, y+1
-            double2 b0 = ld2(sP + (y0 + 1) * WP + xp), b1 = ld2(sP + (y0 + 1) * WP + xp + 2);
+            double2 a0 = ld2(sP + y0 * SP + xp), a1 = ld2(sP + y0 * SP + xp + 2);        // p rows y, y+1
+            double2 b0 = ld2(sP + (y0 + 1) * SP + xp), b1 = ld2(sP + (y0 + 1) * SP + xp + 2);
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
                 const int y = y0 + i;
-                if (y < WI) {
-                    const double2 e0 = ld2(sP + (y + 2) * WP + xp), e1 = ld2(sP + (y + 2) * WP + xp + 2);
+                if (y < RI) {
+                    const double2 e0 = ld2(sP + (y + 2) * SP + xp), e1 = ld2(sP + (y + 2) * SP + xp + 2);
                     // outputs at p columns xp+1, xp+2 (ops.cpp:70-78 operation order)
                     const double v0 = 4.0 * b0.y - a0.y - e0.y - b0.x - b1.x;
                     const double v1 = 4.0 * b1.x - a1.x - e1.x - b0.y - b1.y;
-                    const double2 iv = ld2(sI + y * WI + xp);
-                    st2(sS + y * WI + xp, make_double2(v0, v1));
-                    st2(sIS + y * WI + xp, make_double2(iv.x * v0, iv.y * v1));
+                    const double2 iv = ld2(sI + y * SI + xp);
+                    st2(sS + y * SI + xp, make_double2(v0, v1));
+                    st2(sIS + y * SI + xp, make_double2(iv.x * v0, iv.y * v1));
                     a0 = b0; a1 = b1; b0 = e0; b1 = e1;
                 }
             }
@@ -1009,11 +469,11 @@ __global__ void __launch_bounds__(NT, 2) k_apply4(PsGeo G, const double* __restr
         __syncthreads();
         // S2: per-window a_k, c1_k on R+2 from 3x3 sums of s and I*s
         double* sA = sU;
-        double* sC = sU + WK * WK;
+        double* sC = sU + RK * SK;
         if (threadIdx.x < 18 * 14 && !(G.dbg & 4)) {
             const int xp = 2 * (threadIdx.x % 18), y0 = 3 * (threadIdx.x / 18);
             auto hpair = [&](const double* a, int y) {  // horizontal 3-sums at columns xp, xp+1
-                const double2 u = ld2(a + y * WI + xp), v = ld2(a + y * WI + xp + 2);
+                const double2 u = ld2(a + y * SI + xp), v = ld2(a + y * SI + xp + 2);
                 return make_double2(u.x + u.y + v.x, u.y + v.x + v.y);
             };
             double2 s0 = hpair(sS, y0), s1 = hpair(sS, y0 + 1);
@@ -1021,9 +481,9 @@ __global__ void __launch_bounds__(NT, 2) k_apply4(PsGeo G, const double* __restr
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
                 const int y = y0 + i;
-                if (y < WK) {
+                if (y < RK) {
                     const double2 s2 = hpair(sS, y + 2), i2 = hpair(sIS, y + 2);
-                    const double2 mu = ld2(sMu + y * WK + xp), g = ld2(sG + y * WK + xp);
+                    const double2 mu = ld2(sMu + y * SK + xp), g = ld2(sG + y * SK + xp);
                     double2 a, c;
                     {
                         const double xb = (s0.x + s1.x + s2.x) * (1.0 / 9.0);  // box mean, no fp64 division
@@ -1035,8 +495,8 @@ __global__ void __launch_bounds__(NT, 2) k_apply4(PsGeo G, const double* __restr
                         a.y = g.y * ((i0.y + i1.y + i2.y) * (1.0 / 9.0) - mu.y * xb);
                         c.y = g.y != 0.0 ? xb - mu.y * a.y : 0.0;
                     }
-                    st2(sA + y * WK + xp, a);
-                    st2(sC + y * WK + xp, c);
+                    st2(sA + y * SK + xp, a);
+                    st2(sC + y * SK + xp, c);
                     s0 = s1; s1 = s2; i0 = i1; i1 = i2;
                 }
             }
@@ -1046,7 +506,7 @@ __global__ void __launch_bounds__(NT, 2) k_apply4(PsGeo G, const double* __restr
         if (threadIdx.x < 17 * 15 && !(G.dbg & 8)) {
             const int xp = 2 * (threadIdx.x % 17), y0 = 3 * (threadIdx.x / 17);
             auto hpair = [&](const double* a, int y) {
-                const double2 u = ld2(a + y * WK + xp), v = ld2(a + y * WK + xp + 2);
+                const double2 u = ld2(a + y * SK + xp), v = ld2(a + y * SK + xp + 2);
                 return make_double2(u.x + u.y + v.x, u.y + v.x + v.y);
             };
             double2 a0 = hpair(sA, y0), a1 = hpair(sA, y0 + 1);
@@ -1057,15 +517,15 @@ __global__ void __launch_bounds__(NT, 2) k_apply4(PsGeo G, const double* __restr
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
                 const int y = y0 + i;
-                if (y < WM) {
+                if (y < RM) {
                     const double2 a2v = hpair(sA, y + 2), k2 = hpair(sC, y + 2);
                     const int gr = wrap_once(r0 - 1 + y, H);
                     const int nr = max(min(gr + 1, H - 2) - max(gr - 1, 1) + 1, 0);
-                    const double2 sv = ld2(sS + (y + 2) * WI + xp + 2), iv = ld2(sI + (y + 2) * WI + xp + 2);
+                    const double2 sv = ld2(sS + (y + 2) * SI + xp + 2), iv = ld2(sI + (y + 2) * SI + xp + 2);
                     double2 m;
                     m.x = static_cast<double>(nr * nc0) * sv.x - (k0.x + k1.x + k2.x) - iv.x * (a0.x + a1.x + a2v.x);
                     m.y = static_cast<double>(nr * nc1) * sv.y - (k0.y + k1.y + k2.y) - iv.y * (a0.y + a1.y + a2v.y);
-                    st2(sM + y * WM + xp, m);  // sM aliases I*s: dead after S2, not read here
+                    st2(sM + y * SMS + xp, m);  // sM aliases I*s: dead after S2, not read here
                     a0 = a1; a1 = a2v; k0 = k1; k1 = k2;
                 }
             }
@@ -1076,16 +536,16 @@ __global__ void __launch_bounds__(NT, 2) k_apply4(PsGeo G, const double* __restr
         double dotp = 0.0;
         if (!(G.dbg & 16)) {
             const int xp = 2 * (threadIdx.x & 15), y0 = 2 * (threadIdx.x >> 4);
-            double2 a0 = ld2(sM + y0 * WM + xp), a1 = ld2(sM + y0 * WM + xp + 2);
-            double2 b0 = ld2(sM + (y0 + 1) * WM + xp), b1 = ld2(sM + (y0 + 1) * WM + xp + 2);
+            double2 a0 = ld2(sM + y0 * SMS + xp), a1 = ld2(sM + y0 * SMS + xp + 2);
+            double2 b0 = ld2(sM + (y0 + 1) * SMS + xp), b1 = ld2(sM + (y0 + 1) * SMS + xp + 2);
             const int Cc = c0 + xp;
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
                 const int y = y0 + i;
-                const double2 e0 = ld2(sM + (y + 2) * WM + xp), e1 = ld2(sM + (y + 2) * WM + xp + 2);
+                const double2 e0 = ld2(sM + (y + 2) * SMS + xp), e1 = ld2(sM + (y + 2) * SMS + xp + 2);
                 const double t0 = 4.0 * b0.y - a0.y - e0.y - b0.x - b1.x;
                 const double t1 = 4.0 * b1.x - a1.x - e1.x - b0.y - b1.y;
-                const double2 dv = ld2(sO + y * TA + xp);
+                const double2 dv = ld2(sO + y * SO + xp);
                 const double2 val = make_double2(dv.x + t0 * G.lambda, dv.y + t1 * G.lambda);
                 a0 = b0; a1 = b1; b0 = e0; b1 = e1;
                 const int R = r0 + y;
@@ -1105,21 +565,44 @@ __global__ void __launch_bounds__(NT, 2) k_apply4(PsGeo G, const double* __restr
             }
         }
         if (CG) {
-            const double bs = block_sum<NT>(dotp, red);
-            if (threadIdx.x == 0) part[static_cast<size_t>(ch) * nblk + blockIdx.x] = bs;
-            if (elect_last_block(&st[ch].cnt_a, nblk)) {
-                const double pAp = sum_partials<NT>(part + static_cast<size_t>(ch) * nblk, nblk, 1, red);
-                if (threadIdx.x == 0) {
-                    CgState& S = st[ch];
-                    S.pAp = pAp;
-                    if (!(pAp > 0)) {  // pansharpen.cpp:240-244
-                        S.done = (sqrt(S.rs) <= 1e-12 * S.rhs_norm) ? 1 : 2;
-                        S.iters = S.t + 1;
-                    } else {
-                        S.alpha = S.rs / pAp;
-                    }
-                    S.cnt_a = 0;
+            dotp = warp_sum(dotp);
+            if (lane == 0) wsum[chl - ch_lo][warp] = dotp;
+            processed |= 1u << (chl - ch_lo);
+        }
+    }
+    if (CG) {
+        // publish the block partial of every processed channel; the last arrival reduces it
+        __syncthreads();
+        const int li = threadIdx.x;
+        if (li < ch_hi - ch_lo && ((processed >> li) & 1u)) {
+            const int ch = scene * G.cps + ch_lo + li;
+            double s = 0.0;
+#pragma unroll
+            for (int w = 0; w < NT / 32; ++w) s += wsum[li][w];
+            part[static_cast<size_t>(ch) * nblk + blockIdx.x] = s;
+            __threadfence();  // publish the partial before the arrival is counted
+            if (atomicAdd(&st[ch].cnt_a, 1u) == static_cast<unsigned int>(nblk) - 1u) {
+                __threadfence();
+                atomicOr(&last_mask, 1u << li);
+            }
+        }
+        __syncthreads();
+        unsigned int mask = last_mask;
+        while (mask) {
+            const int li2 = __ffs(mask) - 1;
+            mask &= mask - 1u;
+            const int ch = scene * G.cps + ch_lo + li2;
+            const double pAp = sum_partials<NT>(part + static_cast<size_t>(ch) * nblk, nblk, 1, red);
+            if (threadIdx.x == 0) {
+                CgState& S = st[ch];
+                S.pAp = pAp;
+                if (!(pAp > 0)) {  // pansharpen.cpp:240-244
+                    S.done = (sqrt(S.rs) <= 1e-12 * S.rhs_norm) ? 1 : 2;
+                    S.iters = S.t + 1;
+                } else {
+                    S.alpha = S.rs / pAp;
                 }
+                S.cnt_a = 0;
             }
         }
     }

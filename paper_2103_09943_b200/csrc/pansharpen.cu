@@ -21,7 +21,7 @@ PsGeo make_geo(int N, int h, int w, int c, int n, int rw, double lambda, double 
     G.N = N;
     G.cps = cps > 0 ? cps : N;
     const char* env = std::getenv("FBMP_KA_CPC");
-    G.cpc = env ? std::max(1, std::atoi(env)) : G.cps;
+    G.cpc = std::min(env ? std::max(1, std::atoi(env)) : G.cps, fast::a4::MAXCPC);
     const char* dbg = std::getenv("FBMP_KA_DBG");
     G.dbg = dbg ? std::atoi(dbg) : 0;
     G.h = h; G.w = w; G.c = c;
@@ -871,7 +871,7 @@ void check_smem(size_t bytes, const char* what) {
 // fast-path dispatch (cg_fast.cuh): radius 1, c in {1,2,4}, n <= 21, images >= 64 x 64
 // ---------------------------------------------------------------------------------------------
 bool fast_ok(const PsGeo& G) {
-    return G.rw == 1 && (G.c == 1 || G.c == 2 || G.c == 4) && G.n <= fast::a2::MAXN && G.H >= 64 && G.W >= 64 &&
+    return G.rw == 1 && (G.c == 1 || G.c == 2 || G.c == 4) && G.n <= fast::a4::MAXN && G.H >= 64 && G.W >= 64 &&
            std::getenv("FBMP_DISABLE_FAST") == nullptr;
 }
 
@@ -1021,7 +1021,7 @@ void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* 
     const QLaunch q2 = q2_select<true>(G);
     const bool fastA = fast_ok(G);
     const int nbq = q2.fn ? q2.nblk : ceil_div(G.w, TQ) * ceil_div(G.h, TQ);
-    const int nba = fastA ? ceil_div(G.W, fast::a2::TA) * ceil_div(G.H, fast::a2::TA) : ceil_div(G.W, TA) * ceil_div(G.H, TA);
+    const int nba = fastA ? ceil_div(G.W, fast::a4::TA) * ceil_div(G.H, fast::a4::TA) : ceil_div(G.W, TA) * ceil_div(G.H, TA);
     const size_t P = static_cast<size_t>(G.H) * G.W;
     const int nbu = static_cast<int>((P + static_cast<size_t>(NTU) * UPT - 1) / (static_cast<size_t>(NTU) * UPT));
     const size_t sq = q2.fn ? q2.smem : q_smem(G), sa = a_smem(G, 0), sr = static_cast<size_t>(G.n) * G.n * sizeof(double);

@@ -11,6 +11,8 @@
 //       g_k = [k interior] / (eps/9 + var_k)  (pansharpen.cpp:128-164 regrouped), and the data
 //       term gathered per sampling phase so that taps are uniform across a warp.
 #pragma once
+#include <type_traits>
+
 #include "pansharpen.cuh"
 
 namespace fbmp_gpu {
@@ -23,6 +25,32 @@ __host__ __device__ constexpr int pstride(int s) { return s + ((4 - s % 16) + 16
 __device__ __forceinline__ int wrap_once(int a, int m) { return a < 0 ? a + m : (a >= m ? a - m : a); }
 __device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 __device__ __forceinline__ void st2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
+// CF-wide runs of doubles (read-only path for loads)
+struct double4_t {
+    double2 a, b;
+};
+template <class V>
+__device__ __forceinline__ V ldv(const double* p);
+template <>
+__device__ __forceinline__ double ldv<double>(const double* p) { return __ldg(p); }
+template <>
+__device__ __forceinline__ double2 ldv<double2>(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+template <>
+__device__ __forceinline__ double4_t ldv<double4_t>(const double* p) {
+    return {__ldg(reinterpret_cast<const double2*>(p)), __ldg(reinterpret_cast<const double2*>(p) + 1)};
+}
+__device__ __forceinline__ void unpack(double x, double* v) { v[0] = x; }
+__device__ __forceinline__ void unpack(double2 x, double* v) { v[0] = x.x; v[1] = x.y; }
+__device__ __forceinline__ void unpack(double4_t x, double* v) { v[0] = x.a.x; v[1] = x.a.y; v[2] = x.b.x; v[3] = x.b.y; }
+template <int K>
+__device__ __forceinline__ void stv(double* p, const double (&v)[K]) {
+    if constexpr (K == 1) {
+        *p = v[0];
+    } else {
+#pragma unroll
+        for (int u = 0; u < K; u += 2) reinterpret_cast<double2*>(p)[u / 2] = make_double2(v[u], v[u + 1]);
+    }
+}
 
 // ------------------------------------------------------------------------------------------
 // per-scene guide statistics (pansharpen.cpp:128-139, :152-155):
@@ -100,36 +128,46 @@ __global__ void __launch_bounds__(NT, 2) k_q2(PsGeo G, const double* __restrict_
     const int R0 = CF * (i0 - Q::g), C0 = CF * (j0 - Q::g);
     constexpr int own_r0 = CF * Q::g, own_r1 = CF * (Q::g + Q::TH), own_c1 = CF * (Q::g + Q::TW);
     double pp = 0.0;
-    // region load: each thread keeps KB elements (r and p_old) in flight before storing
-    constexpr int TOT = Q::SRH * Q::SRW;
-    constexpr int KB = 8;
-    for (int e0 = 0; e0 < TOT; e0 += NT * KB) {
-        double vr[KB], vp[KB];
+    // region load in runs of CF consecutive HR columns (one LR column, all column phases): the
+    // run start is a multiple of CF in a row of W = w CF, so a run never wraps and its loads and
+    // stores are CF-wide vectors; each thread keeps KB runs of r and p_old in flight
+    using VT = typename std::conditional<CF == 4, double4_t, typename std::conditional<CF == 2, double2, double>::type>::type;
+    constexpr int RUNS = Q::SRH * Q::PW;
+    constexpr int KB = 4;
+    for (int e0 = 0; e0 < RUNS; e0 += NT * KB) {
+        VT vr[KB], vp[KB];
         size_t gi[KB];
 #pragma unroll
         for (int k = 0; k < KB; ++k) {
             const int e = e0 + k * NT + threadIdx.x;
-            const int rr = e / Q::SRW, cc = e - rr * Q::SRW;
-            gi[k] = static_cast<size_t>(wrap_once(R0 + rr, H)) * W + wrap_once(C0 + cc, W);
-            if (e < TOT) {
-                vr[k] = __ldg(rc + gi[k]);
-                if (CG) vp[k] = __ldg(pold + gi[k]);
+            const int rr = e / Q::PW, jc = e - rr * Q::PW;
+            gi[k] = static_cast<size_t>(wrap_once(R0 + rr, H)) * W + wrap_once(C0 + CF * jc, W);
+            if (e < RUNS) {
+                vr[k] = ldv<VT>(rc + gi[k]);
+                if (CG) vp[k] = ldv<VT>(pold + gi[k]);
             }
         }
 #pragma unroll
         for (int k = 0; k < KB; ++k) {
             const int e = e0 + k * NT + threadIdx.x;
-            if (e >= TOT) break;
-            const int rr = e / Q::SRW, cc = e - rr * Q::SRW;
-            double v = vr[k];
+            if (e >= RUNS) break;
+            const int rr = e / Q::PW, jc = e - rr * Q::PW;
+            double v[CF];
+            unpack(vr[k], v);
             if (CG) {
-                v = v + vp[k] * beta;  // pansharpen.cpp:254
-                if (rr >= own_r0 && rr < own_r1 && cc >= own_r0 && cc < own_c1 && R0 + rr < H && C0 + cc < W) {
-                    pnew[gi[k]] = v;
-                    pp += v * v;
+                double o[CF];
+                unpack(vp[k], o);
+#pragma unroll
+                for (int u = 0; u < CF; ++u) v[u] = v[u] + o[u] * beta;  // pansharpen.cpp:254
+                if (rr >= own_r0 && rr < own_r1 && jc >= Q::g && jc < Q::g + Q::TW && R0 + rr < H && C0 + CF * jc < W) {
+                    stv(pnew + gi[k], v);
+#pragma unroll
+                    for (int u = 0; u < CF; ++u) pp += v[u] * v[u];
                 }
             }
-            planes[((rr % CF) * CF + (cc % CF)) * Q::PS + (rr / CF) * Q::PW + cc / CF] = v;
+            double* pl = planes + ((rr % CF) * CF) * Q::PS + (rr / CF) * Q::PW + jc;
+#pragma unroll
+            for (int u = 0; u < CF; ++u) pl[u * Q::PS] = v[u];
         }
     }
     __syncthreads();

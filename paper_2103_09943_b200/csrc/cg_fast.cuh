@@ -105,9 +105,14 @@ __global__ void __launch_bounds__(NT, 2) k_q2(PsGeo G, const double* __restrict_
     __shared__ double red[NT / 32 + 1];
     extern __shared__ double sm[];
     const int ch = blockIdx.y;
+    const double* tp = taps + static_cast<size_t>(ch / G.cps) * N_ * N_;
+    double* sk = sm;
+    for (int e = threadIdx.x; e < N_ * N_; e += NT) sk[e] = tp[e];
     int t = 0;
     double beta = 0.0;
     if (CG) {
+        pdl_wait();  // r, beta and the flags come from K_U
+        pdl_trigger();
         if (st[ch].done) return;
         t = st[ch].t;
         beta = t ? st[ch].beta : 0.0;
@@ -120,10 +125,7 @@ __global__ void __launch_bounds__(NT, 2) k_q2(PsGeo G, const double* __restrict_
     const int ntx = (G.w + Q::TW - 1) / Q::TW;
     const int tyb = blockIdx.x / ntx, txb = blockIdx.x - tyb * ntx;
     const int i0 = tyb * Q::TH, j0 = txb * Q::TW;
-    double* sk = sm;
     double* planes = sm + Q::KOFF;
-    const double* tp = taps + static_cast<size_t>(ch / G.cps) * N_ * N_;
-    for (int e = threadIdx.x; e < N_ * N_; e += NT) sk[e] = tp[e];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int R0 = CF * (i0 - Q::g), C0 = CF * (j0 - Q::g);
     constexpr int own_r0 = CF * Q::g, own_r1 = CF * (Q::g + Q::TH), own_c1 = CF * (Q::g + Q::TW);
@@ -377,6 +379,10 @@ __global__ void __launch_bounds__(NT, 2) k_apply4(PsGeo G, const double* __restr
             vm[k] = __ldg(MU + gi);
             vg[k] = __ldg(GK + gi);
         }
+    }
+    if (CG) {  // guide and taps are not written by K_Q: their loads overlap K_Q's tail
+        pdl_wait();
+        pdl_trigger();
     }
     int cur = next_active(ch_lo);
     if (cur < ch_hi) prefetch(cur);  // first channel's p / q in flight with the guide tile

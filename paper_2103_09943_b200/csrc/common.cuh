@@ -150,6 +150,22 @@ inline void d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
 }
 inline void check_launch() { FBMP_CUDA(cudaGetLastError()); }
 
+template <class... KArgs, class... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    FBMP_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+}
+
 inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
 
 // ---------------------------------------------------------------------------------------
@@ -162,6 +178,14 @@ __device__ __forceinline__ int wrapi(int a, int m) {
     int r = a % m;
     return r < 0 ? r + m : r;
 }
+
+// Programmatic dependent launch (PDL): a kernel launched with launch_pdl may start while its
+// predecessor in the stream is still running. pdl_wait() blocks until the predecessor has
+// completed and its writes are visible (a no-op for a normal launch); pdl_trigger() lets the
+// successor start launching. Rule used by the CG kernels: before pdl_wait() read only data
+// that the immediate predecessor does not write; trigger only after the wait.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // Deterministic block reduction of one double (fixed shuffle tree + fixed warp order).
 // Every thread must call it; the result is valid in all threads.

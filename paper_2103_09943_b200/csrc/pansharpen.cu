@@ -346,9 +346,10 @@ __global__ void __launch_bounds__(NTU) k_update(PsGeo G, double* __restrict__ z,
                                                 CgState* st, double* __restrict__ part, int nblk) {
     __shared__ double red[NTU / 32 + 1];
     const int ch = blockIdx.y;
+    // t and z, r, p are not written by K_A (the predecessor): read them before pdl_wait so the
+    // loads overlap K_A's tail; done may still be set by K_A (pAp <= 0) and is re-checked
     if (st[ch].done) return;
     const int t = st[ch].t;
-    const double alpha = st[ch].alpha;
     const size_t P = static_cast<size_t>(G.H) * G.W;
     const double* pc = pbuf + (static_cast<size_t>(t & 1) * G.N + ch) * P;
     double* zc = z + ch * P;
@@ -357,7 +358,6 @@ __global__ void __launch_bounds__(NTU) k_update(PsGeo G, double* __restrict__ z,
     double rr = 0.0, zz = 0.0;
     const size_t base = static_cast<size_t>(blockIdx.x) * NTU * UPT;
     if ((P & 1) == 0) {
-        // all loads of the thread in flight before any arithmetic (memory-level parallelism)
         constexpr int KV = UPT / 2;
         const size_t nv = P / 2;
         double2 pv[KV], av[KV], zv[KV], rv[KV];
@@ -366,10 +366,18 @@ __global__ void __launch_bounds__(NTU) k_update(PsGeo G, double* __restrict__ z,
             const size_t vi = base / 2 + static_cast<size_t>(k) * NTU + threadIdx.x;
             if (vi < nv) {
                 pv[k] = __ldcs(reinterpret_cast<const double2*>(pc) + vi);
-                av[k] = __ldcs(reinterpret_cast<const double2*>(ac) + vi);
                 zv[k] = __ldcs(reinterpret_cast<const double2*>(zc) + vi);
                 rv[k] = __ldcs(reinterpret_cast<const double2*>(rc) + vi);
             }
+        }
+        pdl_wait();
+        pdl_trigger();
+        if (st[ch].done) return;
+        const double alpha = st[ch].alpha;
+#pragma unroll
+        for (int k = 0; k < KV; ++k) {
+            const size_t vi = base / 2 + static_cast<size_t>(k) * NTU + threadIdx.x;
+            if (vi < nv) av[k] = __ldcs(reinterpret_cast<const double2*>(ac) + vi);
         }
 #pragma unroll
         for (int k = 0; k < KV; ++k) {
@@ -383,6 +391,10 @@ __global__ void __launch_bounds__(NTU) k_update(PsGeo G, double* __restrict__ z,
             zz += zv[k].x * zv[k].x + zv[k].y * zv[k].y;
         }
     } else {
+        pdl_wait();
+        pdl_trigger();
+        if (st[ch].done) return;
+        const double alpha = st[ch].alpha;
         for (int k = 0; k < UPT; ++k) {
             const size_t i = base + static_cast<size_t>(k) * NTU + threadIdx.x;
             if (i >= P) break;
@@ -405,7 +417,7 @@ __global__ void __launch_bounds__(NTU) k_update(PsGeo G, double* __restrict__ z,
         const double zsq = sum_partials<NTU>(part + static_cast<size_t>(ch) * nblk * 2 + 1, nblk, 2, red);
         if (threadIdx.x == 0) {
             CgState& S = st[ch];
-            const double step = fabs(alpha) * sqrt(S.pp);
+            const double step = fabs(S.alpha) * sqrt(S.pp);
             S.zz = zsq;
             if (step <= S.cg_tol * fmax(sqrt(zsq), 1e-300)) {
                 S.done = 1;
@@ -939,13 +951,18 @@ std::pair<AFn, size_t> apply3_select(const PsGeo& G) {
 
 template <bool CG>
 void launch_apply2(Context& ctx, const PsGeo& G, const double* taps, const double* guide, const double* mu,
-                   const double* gk, const double* p, const double* q, double* out, CgState* st, double* part) {
+                   const double* gk, const double* p, const double* q, double* out, CgState* st, double* part,
+                   bool pdl = false) {
     const int S = (G.N + G.cps - 1) / G.cps;
     const int nba = ceil_div(G.W, fast::a4::TA) * ceil_div(G.H, fast::a4::TA);
     const int groups = (G.cps + G.cpc - 1) / G.cpc;
     const auto fs = apply3_select<CG>(G);
-    fs.first<<<dim3(nba, S * groups), fast::NT, fs.second, ctx.stream>>>(G, taps, guide, mu, gk, p, q, out, st, part,
-                                                                          nba);
+    if (pdl)
+        launch_pdl(fs.first, dim3(nba, S * groups), dim3(fast::NT), fs.second, ctx.stream, G, taps, guide, mu, gk, p,
+                   q, out, st, part, nba);
+    else
+        fs.first<<<dim3(nba, S * groups), fast::NT, fs.second, ctx.stream>>>(G, taps, guide, mu, gk, p, q, out, st,
+                                                                              part, nba);
 }
 
 template <bool CG>
@@ -1056,6 +1073,10 @@ void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* 
     // In profile mode event records bracket every kernel and graphs are not pipelined.
     const int chunk = 8;
     const bool prof = ctx.profile;
+    // programmatic dependent launch per CG kernel (bit 0 K_Q, 1 K_A, 2 K_U; env FBMP_PDL). Measured
+    // on B200 (C1/C2/C4 scenes): only K_A gains (its guide-tile loads overlap K_Q's tail, -2%);
+    // PDL on K_Q costs ~5 us per iteration on small grids and on K_U ~7 us on C2.
+    static const int pdl_mask = std::getenv("FBMP_PDL") ? std::atoi(std::getenv("FBMP_PDL")) : 2;
     std::vector<cudaEvent_t> pev(prof ? chunk * 4 : 0);
     for (auto& e : pev) FBMP_CUDA(cudaEventCreate(&e));
     // the chunk graph depends only on geometry, buffers and launch shapes: cache it in the context
@@ -1078,18 +1099,24 @@ void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* 
         FBMP_CUDA(cudaStreamBeginCapture(ctx.stream, cudaStreamCaptureModeThreadLocal));
         for (int it = 0; it < chunk; ++it) {
             if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * 4 + 0], ctx.stream, cudaEventRecordExternal));
-            if (q2.fn)
+            if (q2.fn && (pdl_mask & 1))
+                launch_pdl(q2.fn, dim3(nbq, N), dim3(fast::NT), sq, ctx.stream, G, d_taps, B.r, B.p, B.q, B.st,
+                           part_q, nbq);
+            else if (q2.fn)
                 q2.fn<<<dim3(nbq, N), fast::NT, sq, ctx.stream>>>(G, d_taps, B.r, B.p, B.q, B.st, part_q, nbq);
             else
                 k_q<true><<<dim3(nbq, N), NTQ, sq, ctx.stream>>>(G, d_taps, B.r, B.p, B.q, B.st, part_q, nbq);
             if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * 4 + 1], ctx.stream, cudaEventRecordExternal));
             if (fastA)
-                launch_apply2<true>(ctx, G, d_taps, d_guide, wmu, wg, B.p, B.q, B.Ap, B.st, part_a);
+                launch_apply2<true>(ctx, G, d_taps, d_guide, wmu, wg, B.p, B.q, B.Ap, B.st, part_a, (pdl_mask & 2) != 0);
             else
                 k_apply<0, true><<<dim3(nba, N), NTA, sa, ctx.stream>>>(G, d_taps, d_guide, B.p, B.q, B.Ap, B.st,
                                                                          part_a, nba);
             if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * 4 + 2], ctx.stream, cudaEventRecordExternal));
-            k_update<<<dim3(nbu, N), NTU, 0, ctx.stream>>>(G, B.z, B.r, B.p, B.Ap, B.st, part_u, nbu);
+            if (pdl_mask & 4)
+                launch_pdl(k_update, dim3(nbu, N), dim3(NTU), 0, ctx.stream, G, B.z, B.r, B.p, B.Ap, B.st, part_u, nbu);
+            else
+                k_update<<<dim3(nbu, N), NTU, 0, ctx.stream>>>(G, B.z, B.r, B.p, B.Ap, B.st, part_u, nbu);
             if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * 4 + 3], ctx.stream, cudaEventRecordExternal));
         }
         FBMP_CUDA(cudaStreamEndCapture(ctx.stream, &graph));

@@ -331,11 +331,23 @@ __global__ void __launch_bounds__(NT, 2) k_apply4(PsGeo G, const double* __restr
     constexpr int KQ = (Lay::QWMAX * Lay::QWMAX + NT - 1) / NT;
     double pf_p[KP], pf_q[KQ];
     if (CG && threadIdx.x == 0) last_mask = 0u;
+    // per-channel flags of the group, one load per lane (every warp keeps its own copy): done and
+    // t are written by K_U and by this kernel's own final election only, so they are stable here
+    // and can be read before pdl_wait
+    unsigned int active = ch_hi - ch_lo >= 32 ? 0xffffffffu : (1u << (ch_hi - ch_lo)) - 1u;
+    int tpar = 0;
+    if (CG) {
+        const bool mine = lane < ch_hi - ch_lo;
+        const CgState* sl = st + scene * G.cps + ch_lo + (mine ? lane : 0);
+        const int dn = mine ? sl->done : 1;
+        tpar = mine ? (sl->t & 1) : 0;
+        active = __ballot_sync(0xffffffffu, !dn);
+    }
     // issue the loads of channel `chl`'s p (R+4) and q windows into registers
     auto prefetch = [&](int chl) {
         const int ch = scene * G.cps + chl;
         const double* pp = pin + ch * P;
-        if (CG) pp = pin + (static_cast<size_t>(st[ch].t & 1) * G.N + ch) * P;
+        if (CG) pp = pin + (static_cast<size_t>(__shfl_sync(0xffffffffu, tpar, chl - ch_lo)) * G.N + ch) * P;
         const double* qc = q + static_cast<size_t>(ch) * G.h * G.w;
 #pragma unroll
         for (int k = 0; k < KP; ++k) {
@@ -355,8 +367,8 @@ __global__ void __launch_bounds__(NT, 2) k_apply4(PsGeo G, const double* __restr
         }
     };
     auto next_active = [&](int chl) {
-        while (chl < ch_hi && CG && st[scene * G.cps + chl].done) ++chl;
-        return chl;
+        const unsigned int rest = chl - ch_lo < 32 ? active >> (chl - ch_lo) : 0u;
+        return rest ? chl + __ffs(rest) - 1 : ch_hi;
     };
     const double* I = guide + scene * P;
     const double* MU = wmu + scene * P;

@@ -664,5 +664,312 @@ __global__ void __launch_bounds__(NT, 2) k_apply4(PsGeo G, const double* __restr
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// K_D + K_L: the CG operator split into the data term (tile kernel) and the matting term
+// (register-streaming kernel).
+//
+// K_D: d = B^T U q for all channels of a scene, one CTA per 32 x 32 HR tile (the q window and
+//      taps in shared memory, the K_A register-blocked gather), written to the output plane.
+// K_L: out = d + lambda L M L p (pansharpen.cpp:218-223) and p.out. One warp owns a band of 24
+//      output columns (lanes = 32 consecutive columns incl. a 4-column halo on each side) and
+//      walks down a strip of rows; the vertical 3-point stencils keep their rows in registers
+//      and the horizontal neighbours come from lane shuffles, so the five operator stages
+//      (s = L p, I s, window coefficients (a, c1), M s, L M s) run without shared memory or
+//      block barriers. Per output row the warp issues 6 coalesced row loads and 24 32-bit
+//      shuffles; the p.out partials are reduced per CTA and the last CTA of a channel forms
+//      p.Ap (same state update as K_A).
+// ------------------------------------------------------------------------------------------
+namespace kl {
+template <int CF>
+constexpr size_t dterm_smem() { return (a4::MAXTAP + 2 * a4::L<CF>::QWP * a4::L<CF>::QWMAX) * sizeof(double); }
+constexpr int NTL = 32;           // one warp per CTA: every loop bound derives from blockIdx, so
+                                  // the compiler sees a convergent warp and emits plain SHFLs
+constexpr int BAND = 24;          // output columns per warp
+constexpr int HALO = 4;           // L M L has radius 4
+constexpr int RB = 32;            // rows per p.out partial (strip heights are multiples of RB, so
+                                  // the reduction tree does not depend on the strip partition)
+}  // namespace kl
+
+template <bool CG, int N_, int CF>
+__global__ void __launch_bounds__(NT, 2) k_dterm(PsGeo G, const double* __restrict__ taps, const double* __restrict__ q,
+                                                 double* __restrict__ out, const CgState* __restrict__ st) {
+    using namespace a4;
+    using Lay = a4::L<CF>;
+    static_assert(N_ == 0 || CF == 4, "register data term is specialised for factor 4");
+    extern __shared__ double sm[];   // taps | q window: dterm_smem<CF>()
+    const int cgroups = (G.cps + G.cpc - 1) / G.cpc;
+    const int scene = blockIdx.y / cgroups, group = blockIdx.y - scene * cgroups;
+    const int H = G.H, W = G.W, n = G.n, C = G.C;
+    const size_t P = static_cast<size_t>(H) * W;
+    const int ntx = (W + TA - 1) / TA;
+    const int by = blockIdx.x / ntx, bx = blockIdx.x - by * ntx;
+    const int r0 = by * TA, c0 = bx * TA;
+    double* sk = sm + Lay::O_TAPS;
+    double* sq = sm + MAXTAP;   // q window right after the taps
+    const double* tp = taps + static_cast<size_t>(scene) * n * n;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int iq0 = floordiv(r0 - C + CF - 1, CF), jq0 = floordiv(c0 - C + CF - 1, CF);
+    const int QH = floordiv(r0 + TA - 1 + C, CF) - iq0 + 1, QW = floordiv(c0 + TA - 1 + C, CF) - jq0 + 1;
+    constexpr int QS = Lay::QWP;
+    using D = DT<(N_ > 0 ? N_ : 1), CF>;
+    constexpr int DM = N_ > 0 ? D::DM : 1;
+    const int ch_lo = group * G.cpc, ch_hi = min(G.cps, group * G.cpc + G.cpc);
+    for (int e = threadIdx.x; e < n * n; e += NT) sk[e] = tp[e];
+    unsigned int active = ch_hi - ch_lo >= 32 ? 0xffffffffu : (1u << (ch_hi - ch_lo)) - 1u;
+    if (CG) {
+        pdl_wait();  // q and the flags come from K_Q
+        pdl_trigger();
+        const bool mine = lane < ch_hi - ch_lo;
+        const int dn = mine ? st[scene * G.cps + ch_lo + lane].done : 1;
+        active = __ballot_sync(0xffffffffu, !dn);
+    }
+    const int QN = QH * QW;
+    constexpr int KQ = (Lay::QWMAX * Lay::QWMAX + NT - 1) / NT;
+    double pf[KQ];
+    // the next channel's q window is loaded into registers while the current one is computed;
+    // the shared window alternates between two buffers (one barrier per channel)
+    auto prefetch = [&](int chl) {
+        const double* qc = q + static_cast<size_t>(scene * G.cps + chl) * G.h * G.w;
+#pragma unroll
+        for (int k = 0; k < KQ; ++k) {
+            const int e = threadIdx.x + k * NT;
+            if (e < QN) {
+                const int a = e / QW, b = e - a * QW;
+                pf[k] = __ldg(qc + static_cast<size_t>(wrapi(iq0 + a, G.h)) * G.w + wrapi(jq0 + b, G.w));
+            }
+        }
+    };
+    int nxt = active ? ch_lo + __ffs(active) - 1 : -1;
+    if (nxt >= 0) prefetch(nxt);
+    int buf = 0;
+    while (nxt >= 0) {
+        const int chl = nxt;
+        active &= active - 1u;
+        const int ch = scene * G.cps + chl;
+        double* sqb = sq + buf * (Lay::QWP * Lay::QWMAX);
+#pragma unroll
+        for (int k = 0; k < KQ; ++k) {
+            const int e = threadIdx.x + k * NT;
+            if (e < QN) {
+                const int a = e / QW, b = e - a * QW;
+                sqb[a * QS + b] = pf[k];
+            }
+        }
+        nxt = active ? ch_lo + __ffs(active) - 1 : -1;
+        if (nxt >= 0) prefetch(nxt);
+        __syncthreads();  // window (and taps) in; the other buffer is free for the next channel
+        buf ^= 1;
+        double* oc = out + ch * P;
+        if (N_ > 0) {
+            constexpr int CW4 = TA / CF, RB4 = CW4 / 4;
+            const int pc = threadIdx.x % CF;
+            const int Jc = (threadIdx.x / CF) % CW4;
+            const int rest = threadIdx.x / (CF * CW4);
+            const int Ic0 = (rest % RB4) * 4;
+            const int pr = rest / RB4;
+            double kreg[DM][DM];
+#pragma unroll
+            for (int a = 0; a < DM; ++a)
+#pragma unroll
+                for (int b = 0; b < DM; ++b) {
+                    const int tr = CF * (a + D::DLO) - pr + D::C, tc = CF * (b + D::DLO) - pc + D::C;
+                    kreg[a][b] = (tr >= 0 && tr < N_ && tc >= 0 && tc < N_) ? sk[tr * N_ + tc] : 0.0;
+                }
+            const double* qb = sqb + (r0 / CF + Ic0 - iq0 + D::DLO) * QS + (c0 / CF + Jc - jq0 + D::DLO);
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int m = 0; m < DM + 3; ++m) {
+                double qv[DM];
+#pragma unroll
+                for (int b = 0; b < DM; ++b) qv[b] = qb[m * QS + b];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int a = m - k;
+                    if (a >= 0 && a < DM) {
+#pragma unroll
+                        for (int b = 0; b < DM; ++b) acc[k] = fma(kreg[a][b], qv[b], acc[k]);
+                    }
+                }
+            }
+            const int Cc = c0 + Jc * CF + pc;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int R = r0 + (Ic0 + k) * CF + pr;
+                if (R < H && Cc < W) oc[static_cast<size_t>(R) * W + Cc] = acc[k];
+            }
+        } else {
+            constexpr int CPR = TA / CF, CPP = CPR * CPR;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int u = 128 * warp + 32 * k + lane;
+                const int ph = u / CPP, cell = u - ph * CPP;
+                const int pr = ph / CF, pc = ph - pr * CF;
+                const int ci = cell / CPR, cj = cell - ci * CPR;
+                const int dilo = floordiv(pr - C + CF - 1, CF), dihi = floordiv(pr + C, CF);
+                const int djlo = floordiv(pc - C + CF - 1, CF), djhi = floordiv(pc + C, CF);
+                const double* qb = sqb + (r0 / CF + ci - iq0) * QS + (c0 / CF + cj - jq0);
+                double acc = 0.0;
+                for (int di = dilo; di <= dihi; ++di) {
+                    const double* krow = sk + (CF * di - pr + C) * n + C - pc;
+                    const double* qrow = qb + di * QS;
+                    for (int dj = djlo; dj <= djhi; ++dj) acc = fma(krow[CF * dj], qrow[dj], acc);
+                }
+                const int R = r0 + ci * CF + pr, Cc = c0 + cj * CF + pc;
+                if (R < H && Cc < W) oc[static_cast<size_t>(R) * W + Cc] = acc;
+            }
+        }
+    }
+}
+
+// item = (band, strip) of one channel: blockIdx.x = item, blockIdx.y = channel
+template <bool CG>
+__global__ void __launch_bounds__(kl::NTL, 16) k_llp(PsGeo G, const double* __restrict__ guide,
+                                                    const double* __restrict__ wmu, const double* __restrict__ wg,
+                                                    const double* __restrict__ pin, double* __restrict__ out,
+                                                    CgState* st, double* __restrict__ part, int nbands, int kstrips,
+                                                    int R) {
+    using namespace kl;
+    const int ch = blockIdx.y, scene = ch / G.cps;
+    const int H = G.H, W = G.W;
+    const size_t P = static_cast<size_t>(H) * W;
+    const int lane = threadIdx.x;
+    const int nblk = gridDim.x;
+    if (CG) {
+        pdl_wait();
+        pdl_trigger();
+        if (__all_sync(0xffffffffu, st[ch].done != 0)) return;
+    }
+    const int item = blockIdx.x;
+    const int nrb = (H + RB - 1) / RB;
+    double dotp = 0.0;
+    {
+        const int band = item / kstrips, strip = item - band * kstrips;
+        const int c0 = band * BAND, r0 = strip * R, r1 = min(H, r0 + R);
+        const int X = wrap_once(c0 - HALO + lane, W);
+        const double* pp = pin + ch * P;
+        if (CG) pp = pin + (static_cast<size_t>(st[ch].t & 1) * G.N + ch) * P;
+        const double* I = guide + scene * P + X;
+        const double* MU = wmu + scene * P + X;
+        const double* GK = wg + scene * P + X;
+        const double* pc = pp + X;
+        double* oc = out + ch * P + X;
+        const bool writer = lane >= HALO && lane < HALO + BAND && c0 + lane - HALO < W;
+        // interior-window count factor of column X (pansharpen.cpp:150-160)
+        const int ncol = max(min(X + 1, W - 2) - max(X - 1, 1) + 1, 0);
+        const double lam = G.lambda;
+        // Rows: Y = the p row loaded by the step; S1 runs on row Y-1, S2 on Y-2, S3 on Y-3 and
+        // S5 (the output) on Y-4. Row offsets (elements) shift down one slot per step; the loads
+        // run two steps ahead (buffers A / B alternate, loop unrolled by two).
+        const int yA = wrap_once(r0 - HALO, H);
+        int ld_row = yA;                       // next row to load
+        auto adv = [&](int r) { return r + 1 == H ? 0 : r + 1; };
+        auto back = [&](int r, int k) { const int q = r - k; return q < 0 ? q + H : q; };
+        struct Rowv {
+            double p0, i1, m2, g2, d4, p4;
+        };
+        auto load = [&](Rowv& v, int y) {
+            const int o0 = y * W, o1 = back(y, 1) * W, o2 = back(y, 2) * W, o4 = back(y, 4) * W;
+            v.p0 = __ldg(pc + o0);
+            v.i1 = __ldg(I + o1);
+            v.m2 = __ldg(MU + o2);
+            v.g2 = __ldg(GK + o2);
+            v.d4 = oc[o4];
+            v.p4 = __ldg(pc + o4);
+        };
+        double pm2 = 0.0, pm1 = 0.0, Im2 = 0.0, Im3 = 0.0, s2 = 0.0, s3 = 0.0;
+        double hs_a = 0.0, hs_b = 0.0, his_a = 0.0, his_b = 0.0;
+        double ha_a = 0.0, ha_b = 0.0, hc_a = 0.0, hc_b = 0.0, M_a = 0.0, M_b = 0.0;
+        const int steps = (r1 - r0) + 2 * HALO;
+        int r3 = back(yA, 3);                  // row of S3 (Y-3) for the current step
+        int o4 = back(yA, 4) * W;              // output row offset (Y-4)
+        int blk_left = RB - (r0 % RB);         // output rows left in the current partial block
+        Rowv A, B;
+        load(A, ld_row);
+        ld_row = adv(ld_row);
+        if (steps > 1) load(B, ld_row);
+        ld_row = adv(ld_row);
+        auto step = [&](Rowv& V, int st_i) {
+            const double p0 = V.p0, Im1 = V.i1, mu2 = V.m2, g2 = V.g2, d4 = V.d4, p4 = V.p4;
+            if (st_i + 2 < steps) load(V, ld_row);
+            ld_row = adv(ld_row);
+            // S1 at row Y-1: s = L p (ops.cpp:70-78 order), I s
+            const double pl = __shfl_up_sync(0xffffffffu, pm1, 1), pr = __shfl_down_sync(0xffffffffu, pm1, 1);
+            const double s1 = 4.0 * pm1 - pm2 - p0 - pl - pr;
+            const double is1 = Im1 * s1;
+            // S2 at row Y-2: window sums over rows Y-3..Y-1, coefficients a, c1
+            const double hs1 = __shfl_up_sync(0xffffffffu, s1, 1) + s1 + __shfl_down_sync(0xffffffffu, s1, 1);
+            const double his1 = __shfl_up_sync(0xffffffffu, is1, 1) + is1 + __shfl_down_sync(0xffffffffu, is1, 1);
+            const double xb = (hs_a + hs_b + hs1) * (1.0 / 9.0);
+            const double a2 = g2 * ((his_a + his_b + his1) * (1.0 / 9.0) - mu2 * xb);
+            const double c2 = g2 != 0.0 ? xb - mu2 * a2 : 0.0;
+            // S3 at row Y-3: M s = n s - box(c1) - I box(a)
+            const double ha2 = __shfl_up_sync(0xffffffffu, a2, 1) + a2 + __shfl_down_sync(0xffffffffu, a2, 1);
+            const double hc2 = __shfl_up_sync(0xffffffffu, c2, 1) + c2 + __shfl_down_sync(0xffffffffu, c2, 1);
+            const int nrow = max(min(r3 + 1, H - 2) - max(r3 - 1, 1) + 1, 0);
+            const double Mc = static_cast<double>(nrow * ncol) * s3 - (hc_a + hc_b + hc2) - Im3 * (ha_a + ha_b + ha2);
+            // S5 at row Y-4: t = L (M s), out = d + lambda t
+            const double Ml = __shfl_up_sync(0xffffffffu, M_b, 1), Mr = __shfl_down_sync(0xffffffffu, M_b, 1);
+            const double t = 4.0 * M_b - M_a - Mc - Ml - Mr;
+            const double val = d4 + t * lam;
+            if (st_i >= 2 * HALO) {
+                if (writer) {
+                    oc[o4] = val;
+                    dotp += p4 * val;
+                }
+                if (CG && (--blk_left == 0 || st_i + 1 == steps)) {  // close the row block
+                    const double ws = warp_sum(dotp);
+                    const int yo = r0 + st_i - 2 * HALO;
+                    if (lane == 0) part[(static_cast<size_t>(ch) * nbands + band) * nrb + yo / RB] = ws;
+                    dotp = 0.0;
+                    blk_left = RB;
+                }
+            }
+            pm2 = pm1; pm1 = p0;
+            Im3 = Im2; Im2 = Im1;
+            s3 = s2; s2 = s1;
+            hs_a = hs_b; hs_b = hs1; his_a = his_b; his_b = his1;
+            ha_a = ha_b; ha_b = ha2; hc_a = hc_b; hc_b = hc2;
+            M_a = M_b; M_b = Mc;
+            r3 = adv(r3);
+            o4 = o4 + W == static_cast<int>(P) ? 0 : o4 + W;
+        };
+        int st_i = 0;
+        for (; st_i + 1 < steps; st_i += 2) {
+            step(A, st_i);
+            step(B, st_i + 1);
+        }
+        if (st_i < steps) step(A, st_i);
+    }
+    if (CG) {
+        // arrival of this item (its row-block partials are written); the last item of the channel
+        // sums all partials of the channel in a fixed order
+        unsigned int prev = 0;
+        if (lane == 0) {
+            __threadfence();
+            prev = atomicAdd(&st[ch].cnt_a, 1u);
+        }
+        prev = __shfl_sync(0xffffffffu, prev, 0);
+        if (prev == static_cast<unsigned int>(nblk) - 1u) {
+            __threadfence();
+            const double* pa = part + static_cast<size_t>(ch) * nbands * nrb;
+            double sacc = 0.0;
+#pragma unroll 8
+            for (int i = lane; i < nbands * nrb; i += 32) sacc += __ldcg(pa + i);
+            const double pAp = warp_sum(sacc);
+            if (lane == 0) {
+                CgState& S = st[ch];
+                S.pAp = pAp;
+                if (!(pAp > 0)) {  // pansharpen.cpp:240-244
+                    S.done = (sqrt(S.rs) <= 1e-12 * S.rhs_norm) ? 1 : 2;
+                    S.iters = S.t + 1;
+                } else {
+                    S.alpha = S.rs / pAp;
+                }
+                S.cnt_a = 0;
+            }
+        }
+    }
+}
+
 }  // namespace fast
 }  // namespace fbmp_gpu

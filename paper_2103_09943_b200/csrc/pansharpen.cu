@@ -949,6 +949,75 @@ std::pair<AFn, size_t> apply3_select(const PsGeo& G) {
     return {fast::k_apply4<CG, 0, 1>, fast::a4::L<1>::smem};
 }
 
+// K_D + K_L (the default CG operator; env FBMP_KA=4 selects the single-kernel K_A)
+struct LlpPlan {
+    int nb = 0, k = 1, R = 0, ctas = 0;
+};
+inline bool use_llp() {
+    static const bool on = !(std::getenv("FBMP_KA") && std::atoi(std::getenv("FBMP_KA")) == 4);
+    return on;
+}
+// Strip height: minimise rounds x (R + 8) (a warp's steps, 8 = pipeline warm-up rows) over the
+// resident warp slots; R is a multiple of the partial row block.
+LlpPlan llp_plan(Context& ctx, const PsGeo& G) {
+    static int per_sm = 0;
+    if (!per_sm) {
+        int blocks = 0;
+        FBMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fast::k_llp<true>, fast::kl::NTL, 0));
+        per_sm = std::max(1, std::min(blocks, 16)) * (fast::kl::NTL / 32);
+    }
+    const long long slots = static_cast<long long>(per_sm) * ctx.sm_count;
+    LlpPlan L;
+    L.nb = ceil_div(G.W, fast::kl::BAND);
+    const long long bc = static_cast<long long>(L.nb) * G.N;
+    long long best = -1;
+    for (int k = 1; k <= ceil_div(G.H, fast::kl::RB); ++k) {
+        const int R = ceil_div(ceil_div(G.H, k), fast::kl::RB) * fast::kl::RB;
+        const int ke = ceil_div(G.H, R);
+        const long long items = bc * ke, rounds = (items + slots - 1) / slots;
+        const long long cost = rounds * (R + 8);
+        if (best < 0 || cost < best) {
+            best = cost;
+            L.k = ke;
+            L.R = R;
+        }
+    }
+    L.ctas = L.nb * L.k;
+    return L;
+}
+template <bool CG>
+std::pair<void (*)(PsGeo, const double*, const double*, double*, const CgState*), size_t> dterm_select(const PsGeo& G) {
+    if (G.c == 4) {
+        const size_t sm = fast::kl::dterm_smem<4>();
+        switch (G.n) {
+        case 21: return {fast::k_dterm<CG, 21, 4>, sm};
+        case 17: return {fast::k_dterm<CG, 17, 4>, sm};
+        case 15: return {fast::k_dterm<CG, 15, 4>, sm};
+        case 7: return {fast::k_dterm<CG, 7, 4>, sm};
+        default: return {fast::k_dterm<CG, 0, 4>, sm};
+        }
+    }
+    if (G.c == 2) return {fast::k_dterm<CG, 0, 2>, fast::kl::dterm_smem<2>()};
+    return {fast::k_dterm<CG, 0, 1>, fast::kl::dterm_smem<1>()};
+}
+template <bool CG>
+void launch_llp(Context& ctx, const PsGeo& G, const double* taps, const double* guide, const double* mu,
+                const double* gk, const double* p, const double* q, double* out, CgState* st, double* part,
+                bool pdl = false) {
+    const int S = (G.N + G.cps - 1) / G.cps;
+    const int nba = ceil_div(G.W, fast::a4::TA) * ceil_div(G.H, fast::a4::TA);
+    const int groups = (G.cps + G.cpc - 1) / G.cpc;
+    const auto fd = dterm_select<CG>(G);
+    if (pdl)
+        launch_pdl(fd.first, dim3(nba, S * groups), dim3(fast::NT), fd.second, ctx.stream, G, taps, q, out,
+                   static_cast<const CgState*>(st));
+    else
+        fd.first<<<dim3(nba, S * groups), fast::NT, fd.second, ctx.stream>>>(G, taps, q, out, st);
+    const LlpPlan L = llp_plan(ctx, G);
+    fast::k_llp<CG><<<dim3(L.ctas, G.N), fast::kl::NTL, 0, ctx.stream>>>(G, guide, mu, gk, p, out, st, part, L.nb,
+                                                                          L.k, L.R);
+}
+
 template <bool CG>
 void launch_apply2(Context& ctx, const PsGeo& G, const double* taps, const double* guide, const double* mu,
                    const double* gk, const double* p, const double* q, double* out, CgState* st, double* part,
@@ -956,6 +1025,10 @@ void launch_apply2(Context& ctx, const PsGeo& G, const double* taps, const doubl
     const int S = (G.N + G.cps - 1) / G.cps;
     const int nba = ceil_div(G.W, fast::a4::TA) * ceil_div(G.H, fast::a4::TA);
     const int groups = (G.cps + G.cpc - 1) / G.cpc;
+    if (use_llp()) {
+        launch_llp<CG>(ctx, G, taps, guide, mu, gk, p, q, out, st, part, pdl);
+        return;
+    }
     const auto fs = apply3_select<CG>(G);
     if (pdl)
         launch_pdl(fs.first, dim3(nba, S * groups), dim3(fast::NT), fs.second, ctx.stream, G, taps, guide, mu, gk, p,
@@ -967,6 +1040,11 @@ void launch_apply2(Context& ctx, const PsGeo& G, const double* taps, const doubl
 
 template <bool CG>
 void prepare_apply2(const PsGeo& G) {
+    if (use_llp()) {
+        const auto fd = dterm_select<CG>(G);
+        set_smem(fd.first, fd.second);
+        return;
+    }
     const auto fs = apply3_select<CG>(G);
     set_smem(fs.first, fs.second);
 }
@@ -1060,7 +1138,8 @@ void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* 
     double* part_init = B.part;
     double* part_q = part_init + static_cast<size_t>(N) * nba;
     double* part_a = part_q + static_cast<size_t>(N) * nbq;
-    double* part_u = part_a + static_cast<size_t>(N) * nba;
+    const int nbA = fastA && use_llp() ? std::max(nba, ceil_div(G.W, fast::kl::BAND) * ceil_div(G.H, fast::kl::RB)) : nba;
+    double* part_u = part_a + static_cast<size_t>(N) * nbA;
     // counters must start at zero
     FBMP_CUDA(cudaMemsetAsync(B.st, 0, sizeof(CgState) * N, ctx.stream));
     k_rhs<true><<<dim3(nba, N), NTA, sr, ctx.stream>>>(G, d_taps, d_x, B.r, B.z, B.p + static_cast<size_t>(N) * P,

@@ -114,23 +114,35 @@ class ClockSampler:
 # ----------------------------------------------------------------------------------------------
 # CPU baseline / reference arm (oracle restatement of the reference, bounded sample)
 # ----------------------------------------------------------------------------------------------
-CG_CAP = 3
+CG_CAP = 2      # CG iterations per band in a sample
+ADMM_CAP = 20   # ADMM iterations in a sample
+POST_DIV = 8    # the alias-group solve runs on 1/POST_DIV of the LR rows in a sample
 
 
-def cpu_sample(scene, cfg, cg_full, threads):
-    """Stage-timed oracle run with each band's CG capped at CG_CAP iterations; the CG phase is
-    extrapolated linearly to the full per-band iteration counts (identical to the GPU's by the
-    parity tests). Returns (seconds for the full solve, description)."""
+def cpu_sample(scene, cfg, threads, cg_full=None, admm_full=None):
+    """One bounded sample of the blind solve on the CPU oracle: CG capped at CG_CAP iterations per
+    band, ADMM at ADMM_CAP iterations, the alias-group solve on the first 1/POST_DIV of the LR rows.
+    Each capped phase is extrapolated linearly to the full solve (iteration counts of the full
+    solve are identical on the oracle and the GPU, tests/test_gpu_pipeline.py). Returns (seconds
+    for the full solve, description)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle  # test infrastructure: the checker, timed here as the CPU baseline only
-    r = oracle.blind_sampled(scene.lrms, scene.pan, cfg.ratio, cfg.support, CG_CAP, threads=threads)
-    t = r["times"]
-    per_iter = t[3] / CG_CAP
-    est = t[0] + t[1] + t[2] + per_iter * max(cg_full) + t[4]
-    sample = (f"oracle (C++ restatement of the reference, FFT=own radix-2) on {cfg.name} scene 0: weights "
-              f"{t[0]:.2f}s + TGV fit {t[1]:.2f}s (1 core, {r['admm_iters']} ADMM it) + matting build {t[2]:.2f}s + "
-              f"CG {CG_CAP} it/band on {threads} threads {t[3]:.2f}s -> x{max(cg_full)}/{CG_CAP} + guided/FFT solve "
-              f"{t[4]:.2f}s; estimated full solve {est:.1f}s")
+    cg_full = cg_full or REF_CG_ITERS.get(cfg.name)
+    admm_full = admm_full or REF_ADMM_ITERS.get(cfg.name)
+    h = cfg.hr // cfg.ratio
+    post_rows = max(1, h // POST_DIV)
+    r = oracle.blind_sampled(scene.lrms, scene.pan, cfg.ratio, cfg.support, CG_CAP, threads=threads,
+                             admm_cap=ADMM_CAP if admm_full else 0, post_rows=post_rows)
+    tw, tsetup, tadmm, tmat, tcg, tpost, tgroups = r["times"]
+    admm_x = admm_full / r["admm_iters"] if admm_full else 1.0
+    cg_x = max(cg_full) / CG_CAP if cg_full else 1.0
+    grp_x = h / post_rows
+    est = tw + tsetup + tadmm * admm_x + tmat + tcg * cg_x + tpost + tgroups * grp_x
+    sample = (f"oracle (C++ restatement of the reference; FFT = own radix-2, alias solve = Householder + QL as "
+              f"Eigen's SelfAdjointEigenSolver) on {cfg.name} scene 0, {threads} threads for the per-band phases: "
+              f"weights {tw:.2f}s + fit setup {tsetup:.2f}s + ADMM {r['admm_iters']} it {tadmm:.2f}s (x{admm_x:.1f}) + "
+              f"matting build {tmat:.2f}s + CG {CG_CAP} it/band {tcg:.2f}s (x{cg_x:.1f}) + guided/FFT {tpost:.2f}s + "
+              f"alias groups of {post_rows}/{h} LR rows {tgroups:.2f}s (x{grp_x:.0f}); estimated full solve {est:.1f}s")
     return est, sample
 
 
@@ -139,12 +151,11 @@ def reference_arm(args, cfg):
     if rank != 0:
         return
     scene = synth.make_scene(cfg, 0)
-    cg_full = REF_CG_ITERS.get(cfg.name)
     threads = min(os.cpu_count() or 1, cfg.bands)
     times = []
     desc = ""
     for i in range(args.warmup + args.steps):
-        est, desc = cpu_sample(scene, cfg, cg_full, threads)
+        est, desc = cpu_sample(scene, cfg, threads)
         if i >= args.warmup:
             times.append(est)
     T = sum(times)
@@ -162,6 +173,7 @@ def reference_arm(args, cfg):
 # CG iteration counts of scene 0 of each config (oracle == GPU, tests/test_gpu_pipeline.py);
 # used only to extrapolate the bounded CPU sample.
 REF_CG_ITERS = {"C1": [160, 157, 157, 158], "C2": [124, 125, 124, 125]}
+REF_ADMM_ITERS = {"C1": 153, "C2": 179}
 
 
 # ----------------------------------------------------------------------------------------------
@@ -252,13 +264,16 @@ def our_arm(args, cfg):
     e2e = units / (t_e2e / 1e3) / 1e6
     s = 8
     p = h * w
-    alg = {"K_Q": (3 * s * P + s * p),     # read r, p_old; write p_new; write q
-           "K_A": (3 * s * P + s * p),     # read p_new, guide; write Ap; read q
-           "K_U": 6 * s * P}               # read z, r, p, Ap; write z, r
+    # algorithmic bytes per launch (all N channels; the guide, mu_k and g_k maps are per scene)
+    alg = {"K_Q": (3 * s * P + s * p) * N,        # read r, p_old; write p_new, q
+           "K_D": (s * P + s * p) * N,            # read q; write d = B^T U q
+           "K_L": 3 * s * P * N + 3 * s * P,      # read p, d, guide/mu/g (per scene); write Ap
+           "K_U": 6 * s * P * N}                  # read z, r, p, Ap; write z, r
+    prof = {k: v for k, v in prof.items() if v["launches"] > 0}
     dom = max(prof, key=lambda k: prof[k]["total_ms"])
     d = prof[dom]
     avg_ms = d["total_ms"] / max(d["launches"], 1)
-    bytes_per_launch = alg[dom] * N
+    bytes_per_launch = alg[dom]
     achieved = bytes_per_launch / (avg_ms / 1e3) / 1e9
     peak, kind = peaks()
     traffic = None
@@ -274,7 +289,7 @@ def our_arm(args, cfg):
                 "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms,
                 "kernel_share_of_cg": {k: v["total_ms"] / cg_total for k, v in prof.items()} if cg_total else None,
                 "cg_kernels": {k: {"launches": v["launches"], "avg_ms": v["total_ms"] / max(v["launches"], 1),
-                                   "GB/s": alg[k] * N / (v["total_ms"] / max(v["launches"], 1) / 1e3) / 1e9}
+                                   "GB/s": alg[k] / (v["total_ms"] / max(v["launches"], 1) / 1e3) / 1e9}
                                for k, v in prof.items()}}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -287,7 +302,8 @@ def our_arm(args, cfg):
                           "pansharpen": stats["ms_pansharpen"]},
             "iterations": {"admm": stats["admm_iters"], "cg": stats["cg_iters"][:N]}}
     if world == 1 and not args.no_cpu_baseline:
-        est, desc = cpu_sample(scene, cfg, stats["cg_iters"][:N], min(os.cpu_count() or 1, N))
+        est, desc = cpu_sample(scene, cfg, min(os.cpu_count() or 1, N), cg_full=stats["cg_iters"][:N],
+                               admm_full=stats["admm_iters"])
         cv = P * N / est / 1e6
         line["cpu_baseline"] = {"value": cv, "unit": UNIT, "cores": min(os.cpu_count() or 1, N), "kind": "port",
                                 "sample": desc}

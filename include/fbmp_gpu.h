@@ -89,8 +89,9 @@ void* fbmp_gpu_ctx_stream(fbmp_gpu_ctx* ctx);
 /* Number of kernels this library launched on the context so far (instrumentation). */
 long long fbmp_gpu_ctx_launches(fbmp_gpu_ctx* ctx);
 /* Profiling of the CG loop: when on, CUDA events bracket each CG kernel (graphs are not
- * pipelined). kernel_profile returns total device ms and launch counts for
- * {K_Q (p update + D B p), K_A (B^T U q + lambda L M L p), K_U (axpys + norms)}. */
+ * pipelined). kernel_profile fills 4 entries of total device ms and launch counts for
+ * {K_Q (p update + D B p), K_D (B^T U q), K_L (+ lambda L M L p, p.Ap), K_U (axpys + norms)};
+ * with the single-kernel operator (env FBMP_KA=4) K_D is empty and K_L holds K_A. */
 void fbmp_gpu_ctx_set_profile(fbmp_gpu_ctx* ctx, int on);
 int fbmp_gpu_ctx_kernel_profile(fbmp_gpu_ctx* ctx, double* total_ms, long long* launches);
 

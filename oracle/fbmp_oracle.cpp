@@ -26,6 +26,7 @@
 #include <exception>
 #include <functional>
 #include <memory>
+#include <limits>
 #include <numeric>
 #include <stdexcept>
 #include <string>
@@ -539,6 +540,119 @@ void herm_eig(int m, std::vector<cd>& A, vec& ev, std::vector<cd>& V) {
     V.swap(V2);
 }
 
+// Complex Hermitian eigen-decomposition by Householder tridiagonalisation and implicit-shift
+// QL iterations -- the algorithm of Eigen::SelfAdjointEigenSolver<MatrixXcd> used at
+// pansharpen.cpp:353 (the Jacobi solver above is kept for the 3x3 rank test and as a cross-check
+// in tests/test_oracle_kats.py). A = V diag(ev) V^H, eigenvalues ascending.
+void herm_eig_ql(int n, std::vector<cd>& A, vec& ev, std::vector<cd>& V) {
+    auto a = [&](int i, int j) -> cd& { return A[static_cast<size_t>(i) * n + j]; };
+    std::vector<cd> Q(static_cast<size_t>(n) * n, 0.0), v(n), p(n), wv(n);
+    for (int i = 0; i < n; ++i) Q[static_cast<size_t>(i) * n + i] = 1.0;
+    for (int k = 0; k + 2 < n; ++k) {
+        double sig = 0.0;
+        for (int i = k + 2; i < n; ++i) sig += std::norm(a(i, k));
+        if (sig == 0.0) continue;
+        const cd x0 = a(k + 1, k);
+        const double ax0 = std::abs(x0), xn = std::sqrt(ax0 * ax0 + sig);
+        const cd alpha = (ax0 > 0.0 ? -x0 / ax0 : cd(-1.0, 0.0)) * xn;  // -e^{i arg x0} ||x||
+        std::fill(v.begin(), v.end(), cd(0.0));
+        v[k + 1] = x0 - alpha;
+        for (int i = k + 2; i < n; ++i) v[i] = a(i, k);
+        double vn = 0.0;
+        for (int i = k + 1; i < n; ++i) vn += std::norm(v[i]);
+        const double beta = 2.0 / vn;
+        // A <- H A H with H = I - beta v v^H:  p = beta A v, K = beta/2 v^H p, w = p - K v
+        for (int i = k; i < n; ++i) {
+            cd sacc = 0.0;
+            for (int j = k + 1; j < n; ++j) sacc += a(i, j) * v[j];
+            p[i] = beta * sacc;
+        }
+        cd K = 0.0;
+        for (int i = k + 1; i < n; ++i) K += std::conj(v[i]) * p[i];
+        K *= 0.5 * beta;
+        for (int i = k; i < n; ++i) wv[i] = p[i] - K * v[i];
+        for (int i = k; i < n; ++i)
+            for (int j = k; j < n; ++j) a(i, j) -= v[i] * std::conj(wv[j]) + wv[i] * std::conj(v[j]);
+        for (int r = 0; r < n; ++r) {  // Q <- Q H
+            cd sacc = 0.0;
+            for (int j = k + 1; j < n; ++j) sacc += Q[static_cast<size_t>(r) * n + j] * v[j];
+            sacc *= beta;
+            for (int j = k + 1; j < n; ++j) Q[static_cast<size_t>(r) * n + j] -= sacc * std::conj(v[j]);
+        }
+    }
+    // T = Q^H A Q is tridiagonal; D = diag(ph) makes its sub-diagonal real: T = D T' D^H
+    vec d(n), e(n, 0.0);
+    std::vector<cd> ph(n, 1.0);
+    for (int i = 0; i < n; ++i) d[i] = a(i, i).real();
+    for (int i = 0; i + 1 < n; ++i) {
+        const cd off = a(i + 1, i);
+        const double m = std::abs(off);
+        e[i] = m;
+        ph[i + 1] = m > 0.0 ? ph[i] * (off / m) : ph[i];
+    }
+    // implicit-shift QL on the real tridiagonal T' (e[i] couples i and i+1), Z accumulates
+    vec Z(static_cast<size_t>(n) * n, 0.0);
+    for (int i = 0; i < n; ++i) Z[static_cast<size_t>(i) * n + i] = 1.0;
+    const double eps = std::numeric_limits<double>::epsilon();
+    for (int l = 0; l < n; ++l) {
+        int iter = 0, m;
+        do {
+            for (m = l; m < n - 1; ++m) {
+                const double dd = std::fabs(d[m]) + std::fabs(d[m + 1]);
+                if (std::fabs(e[m]) <= eps * dd) break;
+            }
+            if (m != l) {
+                if (iter++ == 60) num_error("herm_eig_ql: no convergence");
+                double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+                double r = std::hypot(g, 1.0);
+                g = d[m] - d[l] + e[l] / (g + std::copysign(r, g));
+                double sn = 1.0, cs = 1.0, pp = 0.0;
+                int i;
+                for (i = m - 1; i >= l; --i) {
+                    double f = sn * e[i];
+                    const double b = cs * e[i];
+                    e[i + 1] = (r = std::hypot(f, g));
+                    if (r == 0.0) {
+                        d[i + 1] -= pp;
+                        e[m] = 0.0;
+                        break;
+                    }
+                    sn = f / r;
+                    cs = g / r;
+                    g = d[i + 1] - pp;
+                    r = (d[i] - g) * sn + 2.0 * cs * b;
+                    d[i + 1] = g + (pp = sn * r);
+                    g = cs * r - b;
+                    for (int k = 0; k < n; ++k) {
+                        f = Z[static_cast<size_t>(k) * n + i + 1];
+                        Z[static_cast<size_t>(k) * n + i + 1] = sn * Z[static_cast<size_t>(k) * n + i] + cs * f;
+                        Z[static_cast<size_t>(k) * n + i] = cs * Z[static_cast<size_t>(k) * n + i] - sn * f;
+                    }
+                }
+                if (r == 0.0 && i >= l) continue;
+                d[l] -= pp;
+                e[l] = g;
+                e[m] = 0.0;
+            }
+        } while (m != l);
+    }
+    std::vector<int> order(n);
+    std::iota(order.begin(), order.end(), 0);
+    std::sort(order.begin(), order.end(), [&](int x, int y) { return d[x] < d[y]; });
+    ev.resize(n);
+    V.assign(static_cast<size_t>(n) * n, 0.0);
+    for (int j = 0; j < n; ++j) {
+        const int oj = order[j];
+        ev[j] = d[oj];
+        for (int r = 0; r < n; ++r) {
+            cd sacc = 0.0;
+            for (int k = 0; k < n; ++k)
+                sacc += Q[static_cast<size_t>(r) * n + k] * ph[k] * Z[static_cast<size_t>(k) * n + oj];
+            V[static_cast<size_t>(r) * n + j] = sacc;
+        }
+    }
+}
+
 // pansharpen.cpp:56-63 (laplacian transfer function)
 std::vector<cd> lap_spectrum(int rows, int cols) {
     std::vector<cd> s(static_cast<size_t>(rows) * cols);
@@ -553,8 +667,10 @@ std::vector<cd> lap_spectrum(int rows, int cols) {
 }
 
 // pansharpen.cpp:314-365
+// (bench sampling only: rows_limit > 0 solves the alias groups of LR rows [0, rows_limit) and
+// t_groups receives the seconds spent in the group loop)
 vec solve_channel_fft(const double* x, int h, int w, const double* k, int n, int factor, const double* v, int H, int W,
-                      const PsParams& prm) {
+                      const PsParams& prm, int rows_limit = 0, double* t_groups = nullptr) {
     validate(prm);
     if (h * factor != H || w * factor != W)
         dim_error("solve_channel_fft: LR/HR dimensions inconsistent with factor");
@@ -571,7 +687,9 @@ vec solve_channel_fft(const double* x, int h, int w, const double* k, int n, int
     std::vector<cd> rhs(c2), bg(c2), tmp(c2);
     std::vector<size_t> idx(c2);
     vec ev;
-    for (int kl = 0; kl < h; ++kl)
+    const auto tg0 = std::chrono::steady_clock::now();
+    const int kl_end = rows_limit > 0 ? std::min(rows_limit, h) : h;
+    for (int kl = 0; kl < kl_end; ++kl)
         for (int ll = 0; ll < w; ++ll) {
             for (int a = 0; a < factor; ++a)
                 for (int b = 0; b < factor; ++b)
@@ -583,7 +701,7 @@ vec solve_channel_fft(const double* x, int h, int w, const double* k, int n, int
                 A[static_cast<size_t>(g) * c2 + g] += lambda * std::norm(lhat[idx[g]]);
                 rhs[g] = std::conj(bg[g]) * xg + lambda * std::conj(lhat[idx[g]]) * vhat[idx[g]];
             }
-            herm_eig(c2, A, ev, V);
+            herm_eig_ql(c2, A, ev, V);
             if (!(ev[0] > 0.0) || ev[c2 - 1] > 1e14 * ev[0])
                 num_error("solve_channel_fft: alias-group system condition number exceeds 1e14 (prior transfer "
                           "function too small)");
@@ -598,6 +716,7 @@ vec solve_channel_fft(const double* x, int h, int w, const double* k, int n, int
                 zhat[idx[g]] = s;
             }
         }
+    if (t_groups) t_groups[0] = std::chrono::duration<double>(std::chrono::steady_clock::now() - tg0).count();
     return fhr.backward_real(std::move(zhat));
 }
 
@@ -1005,6 +1124,7 @@ struct AdmmState {  // kernel_estimator.hpp:85-94 (u,p1,p2,x[2],y[4],z,L1[2],L2[
 };
 
 // kernel_estimator.cpp:269-276, 438-455, 291-387 (TGV^2 branch, with_p = true)
+thread_local std::chrono::steady_clock::time_point* g_setup_mark = nullptr;
 vec estimate_kernel_plane_tgv(const double* pan, int H, int W, const double* obs, int h, int w, int factor,
                               const KeParams& prm, int* iters_out, AdmmState* final_state, int t_stop_hook = -1) {
     validate(prm);
@@ -1023,6 +1143,7 @@ vec estimate_kernel_plane_tgv(const double* pan, int H, int W, const double* obs
     const int n = prm.n;
     const size_t m = static_cast<size_t>(n) * n;
     const Observation O(pan_n.data(), H, W, obs_n.data(), h, w, factor, n, prm.mu3);
+    if (g_setup_mark) *g_setup_mark = std::chrono::steady_clock::now();  // bench sampling only
 
     vec u(m, 0.0);
     if (prm.init == 0) u[static_cast<size_t>((n - 1) / 2) * n + (n - 1) / 2] = 1.0;
@@ -1143,7 +1264,10 @@ double tgv_objective(const Observation& O, const double* u, const double* p1, co
 // capped at `cg_cap` iterations (no cap error), timing each stage with steady_clock.
 // times: {weights, kernel_fit, matting_build, cg_phase (channels threaded), post_phase}.
 void blind_sampled(const double* lrms, int N, int h, int w, const double* pan, int factor, int n, int threads,
-                   int cg_cap, double* times, int* cg_iters_done, int* admm_iters) {
+                   int cg_cap, int admm_cap, int post_rows, double* times, int* cg_iters_done, int* admm_iters) {
+    // times: weights, fit setup (intensity scale, E^T E, Cholesky), ADMM (capped at admm_cap
+    // iterations when > 0), matting build, CG (capped at cg_cap per band), post-processing
+    // without the alias-group loop, alias-group loop over LR rows [0, post_rows) (all when 0)
     using clk = std::chrono::steady_clock;
     auto sec = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); };
     const int H = h * factor, W = w * factor;
@@ -1154,7 +1278,11 @@ void blind_sampled(const double* lrms, int N, int h, int w, const double* pan, i
     auto t1 = clk::now();
     KeParams kp;
     kp.n = n;
+    if (admm_cap > 0) kp.t_max = admm_cap;
+    clk::time_point ts = t1;
+    g_setup_mark = &ts;
     vec k = estimate_kernel_plane_tgv(pan, H, W, obs.data(), h, w, factor, kp, admm_iters, nullptr);
+    g_setup_mark = nullptr;
     auto t2 = clk::now();
     PsParams prm;
     double peak = seq_max(pan, P);
@@ -1184,19 +1312,28 @@ void blind_sampled(const double* lrms, int N, int h, int w, const double* pan, i
         cg_iters_done[i] = it;
     });
     auto t4 = clk::now();
+    vec tg(N, 0.0);
     run_phase([&](int i) {
         vec lz = laplacian(z0[i].data(), H, W);
         vec a, c, gm, gv, im;
         guided_coeffs(lz.data(), lpan.data(), H, W, prm.radius, prm.eps, a, c, gm, gv, im);
         vec v = guided_output(a.data(), c.data(), lpan.data(), H, W, prm.radius);
-        vec z = solve_channel_fft(xn[i].data(), h, w, k.data(), n, factor, v.data(), H, W, prm);
+        vec z = solve_channel_fft(xn[i].data(), h, w, k.data(), n, factor, v.data(), H, W, prm, post_rows, &tg[i]);
     });
     auto t5 = clk::now();
+    // the bands run concurrently on nt threads: the wall time of the group loops is the mean
+    // per-band loop time x ceil(N / nt) rounds
+    double tgm = 0.0;
+    for (double x : tg) tgm += x;
+    tgm /= N;
+    const double rounds = std::ceil(static_cast<double>(N) / nt);
     times[0] = sec(t0, t1);
-    times[1] = sec(t1, t2);
-    times[2] = sec(t2, t3);
-    times[3] = sec(t3, t4);
-    times[4] = sec(t4, t5);
+    times[1] = sec(t1, ts);
+    times[2] = sec(ts, t2);
+    times[3] = sec(t2, t3);
+    times[4] = sec(t3, t4);
+    times[5] = std::max(0.0, sec(t4, t5) - tgm * rounds);
+    times[6] = tgm * rounds;
 }
 
 }  // namespace orc
@@ -1299,6 +1436,24 @@ int orc_guided_coeffs(const double* in, const double* g, int h, int w, int radiu
 }
 int orc_guided_output(const double* a, const double* c, const double* g, int h, int w, int radius, double* out) {
     return guard([&] { put(guided_output(a, c, g, h, w, radius), out); });
+}
+// Hermitian eigen-decomposition (A: n x n complex, interleaved re/im, row-major); method 0 =
+// Householder + QL (the alias-group solver), 1 = cyclic Jacobi. V: n x n complex, columns.
+int orc_herm_eig(int n, const double* A, int method, double* ev, double* V) {
+    return guard([&] {
+        std::vector<cd> M(static_cast<size_t>(n) * n), W;
+        for (size_t i = 0; i < M.size(); ++i) M[i] = cd(A[2 * i], A[2 * i + 1]);
+        vec e;
+        if (method == 0)
+            herm_eig_ql(n, M, e, W);
+        else
+            herm_eig(n, M, e, W);
+        for (int i = 0; i < n; ++i) ev[i] = e[i];
+        for (size_t i = 0; i < W.size(); ++i) {
+            V[2 * i] = W[i].real();
+            V[2 * i + 1] = W[i].imag();
+        }
+    });
 }
 int orc_solve_channel_fft(const double* x, int h, int w, const double* k, int n, int factor, const double* v,
                           double lambda, double* out) {
@@ -1426,8 +1581,11 @@ int orc_blind(const double* lrms, int N, int h, int w, const double* pan, int fa
 }
 
 int orc_blind_sampled(const double* lrms, int N, int h, int w, const double* pan, int factor, int n, int threads,
-                      int cg_cap, double* times, int* cg_iters_done, int* admm_iters) {
-    return guard([&] { blind_sampled(lrms, N, h, w, pan, factor, n, threads, cg_cap, times, cg_iters_done, admm_iters); });
+                      int cg_cap, int admm_cap, int post_rows, double* times, int* cg_iters_done, int* admm_iters) {
+    return guard([&] {
+        blind_sampled(lrms, N, h, w, pan, factor, n, threads, cg_cap, admm_cap, post_rows, times, cg_iters_done,
+                      admm_iters);
+    });
 }
 
 // E (p x n^2) of ObservationSystem (kernel_estimator.cpp:57-68), for the construction KATs

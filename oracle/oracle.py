@@ -319,20 +319,33 @@ def blind(lrms, pan, factor, n, l=4, lambda_omega=10.0, threads=0):
     return out, dict(kernel=k, omega=om, admm_iters=ta.value, cg_iters=it)
 
 
-def blind_sampled(lrms, pan, factor, n, cg_cap, threads=0):
-    """Stage-timed blind pipeline with every channel's CG capped at ``cg_cap`` iterations.
+def blind_sampled(lrms, pan, factor, n, cg_cap, threads=0, admm_cap=0, post_rows=0):
+    """Stage-timed blind pipeline on a bounded sample: every channel's CG capped at ``cg_cap``
+    iterations, the ADMM at ``admm_cap`` (0 = the reference's t_max), the alias-group solve on LR
+    rows [0, post_rows) (0 = all).
 
-    Returns dict(times=[weights, kernel_fit, matting_build, cg_phase, post_phase] seconds,
-    cg_done=[...], admm_iters). Used only by bench.py's CPU baseline / reference arm.
+    Returns dict(times=[weights, fit_setup, admm, matting_build, cg, post_fixed, post_groups]
+    seconds, cg_done=[...], admm_iters). Used only by bench.py's CPU baseline / reference arm.
     """
     lrms, pan = _f(lrms), _f(pan)
     N, h, w = lrms.shape
-    t = np.zeros(5)
+    t = np.zeros(7)
     done = np.zeros(N, np.int32)
     ta = C.c_int(0)
-    _check(lib().orc_blind_sampled(_p(lrms), N, h, w, _p(pan), factor, n, threads, cg_cap, _p(t),
+    _check(lib().orc_blind_sampled(_p(lrms), N, h, w, _p(pan), factor, n, threads, cg_cap, admm_cap, post_rows, _p(t),
                                    done.ctypes.data_as(I), C.byref(ta)))
     return dict(times=list(t), cg_done=list(done), admm_iters=ta.value)
+
+
+def herm_eig(A, method=0):
+    """Hermitian eigen-decomposition of the oracle (0: Householder + QL, 1: Jacobi)."""
+    A = np.ascontiguousarray(A, dtype=np.complex128)
+    n = A.shape[0]
+    ev = np.empty(n)
+    V = np.empty((n, n), np.complex128)
+    _check(lib().orc_herm_eig(n, A.ctypes.data_as(C.POINTER(C.c_double)), method, _p(ev),
+                              V.ctypes.data_as(C.POINTER(C.c_double))))
+    return ev, V
 
 
 def observation_matrix(pan, factor, n):

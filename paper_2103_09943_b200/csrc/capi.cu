@@ -751,14 +751,14 @@ int fbmp_gpu_gram(fbmp_gpu_ctx* ctx, const double* pan, int H, int W, const doub
 
 void fbmp_gpu_ctx_set_profile(fbmp_gpu_ctx* ctx, int on) {
     ctx->impl.profile = on != 0;
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < 4; ++i) {
         ctx->impl.prof_ms[i] = 0.0;
         ctx->impl.prof_n[i] = 0;
     }
 }
 
 int fbmp_gpu_ctx_kernel_profile(fbmp_gpu_ctx* ctx, double* total_ms, long long* launches) {
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < 4; ++i) {
         total_ms[i] = ctx->impl.prof_ms[i];
         launches[i] = ctx->impl.prof_n[i];
     }

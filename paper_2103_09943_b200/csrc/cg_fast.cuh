@@ -971,5 +971,166 @@ __global__ void __launch_bounds__(kl::NTL, 16) k_llp(PsGeo G, const double* __re
     }
 }
 
+
+// K_L on column PAIRS (W even): lane = columns (X, X+1), a warp spans 64 columns of which the
+// inner 56 are output (BAND2). Loads are 16-byte, each stage exchanges one double with each
+// neighbour lane (half the shuffles per pixel of k_llp), and the halo overhead is 64/56.
+namespace kl {
+constexpr int BAND2 = 56;
+}
+__device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+
+template <bool CG>
+__global__ void __launch_bounds__(kl::NTL, 12) k_llp2(PsGeo G, const double* __restrict__ guide,
+                                                     const double* __restrict__ wmu, const double* __restrict__ wg,
+                                                     const double* __restrict__ pin, double* __restrict__ out,
+                                                     CgState* st, double* __restrict__ part, int nbands, int kstrips,
+                                                     int R) {
+    using namespace kl;
+    const int ch = blockIdx.y, scene = ch / G.cps;
+    const int H = G.H, W = G.W;
+    const size_t P = static_cast<size_t>(H) * W;
+    const int lane = threadIdx.x;
+    const int nblk = gridDim.x;
+    if (CG) {
+        pdl_wait();
+        pdl_trigger();
+        if (__all_sync(0xffffffffu, st[ch].done != 0)) return;
+    }
+    const int item = blockIdx.x;
+    const int nrb = (H + RB - 1) / RB;
+    const unsigned FULL = 0xffffffffu;
+    double dotp = 0.0;
+    {
+        const int band = item / kstrips, strip = item - band * kstrips;
+        const int c0 = band * BAND2, r0 = strip * R, r1 = min(H, r0 + R);
+        const int X = wrap_once(c0 - HALO + 2 * lane, W);  // even; X + 1 < W
+        const double* pp = pin + ch * P;
+        if (CG) pp = pin + (static_cast<size_t>(st[ch].t & 1) * G.N + ch) * P;
+        const double* pc = pp + X;
+        const double* I = guide + scene * P + X;
+        const double* MU = wmu + scene * P + X;
+        const double* GK = wg + scene * P + X;
+        double* oc = out + ch * P + X;
+        const int ox = c0 - HALO + 2 * lane;                 // unwrapped column of .x
+        const bool writer = lane >= HALO / 2 && lane < (HALO + BAND2) / 2 && ox < W;
+        const int nc0 = max(min(X + 1, W - 2) - max(X - 1, 1) + 1, 0);
+        const int nc1 = max(min(X + 2, W - 2) - max(X, 1) + 1, 0);
+        const double lam = G.lambda;
+        auto back = [&](int r, int k) { const int q = r - k; return q < 0 ? q + H : q; };
+        // row offsets (elements) of Y (p), Y-1 (I), Y-2 (mu, g) and Y-4 (d); they advance by W
+        const int yA = wrap_once(r0 - HALO, H);
+        int o0 = yA * W, o1 = back(yA, 1) * W, o2 = back(yA, 2) * W, o4 = back(yA, 4) * W;
+        auto adv = [&](int o) { return o + W == static_cast<int>(P) ? 0 : o + W; };
+        int r3 = back(yA, 3);
+        double2 pm1 = {0, 0}, pm2 = {0, 0}, pm3 = {0, 0}, pm4 = {0, 0};
+        double2 Im2 = {0, 0}, Im3 = {0, 0}, s2 = {0, 0}, s3 = {0, 0};
+        double2 hs_a = {0, 0}, hs_b = {0, 0}, his_a = {0, 0}, his_b = {0, 0};
+        double2 ha_a = {0, 0}, ha_b = {0, 0}, hc_a = {0, 0}, hc_b = {0, 0}, M_a = {0, 0}, M_b = {0, 0};
+        const int steps = (r1 - r0) + 2 * HALO;
+        int blk_left = RB;
+        // loads of the first step
+        double2 np0 = ldg2(pc + o0), ni1 = ldg2(I + o1), nm2 = ldg2(MU + o2), ng2 = ldg2(GK + o2);
+        double2 nd4 = *reinterpret_cast<const double2*>(oc + o4);
+        for (int st_i = 0; st_i < steps; ++st_i) {
+            const double2 p0 = np0, Im1 = ni1, mu2 = nm2, g2 = ng2, d4 = nd4;
+            o0 = adv(o0); o1 = adv(o1); o2 = adv(o2);
+            const int o4c = o4;
+            o4 = adv(o4);
+            if (st_i + 1 < steps) {
+                np0 = ldg2(pc + o0);
+                ni1 = ldg2(I + o1);
+                nm2 = ldg2(MU + o2);
+                ng2 = ldg2(GK + o2);
+                nd4 = *reinterpret_cast<const double2*>(oc + o4);
+            }
+            // S1 at row Y-1 (ops.cpp:70-78 order: 4 c - up - down - left - right)
+            const double pL = __shfl_up_sync(FULL, pm1.y, 1), pR = __shfl_down_sync(FULL, pm1.x, 1);
+            double2 s1, is1;
+            s1.x = 4.0 * pm1.x - pm2.x - p0.x - pL - pm1.y;
+            s1.y = 4.0 * pm1.y - pm2.y - p0.y - pm1.x - pR;
+            is1.x = Im1.x * s1.x;
+            is1.y = Im1.y * s1.y;
+            // S2 at row Y-2
+            const double sL = __shfl_up_sync(FULL, s1.y, 1), sR = __shfl_down_sync(FULL, s1.x, 1);
+            const double iL = __shfl_up_sync(FULL, is1.y, 1), iR = __shfl_down_sync(FULL, is1.x, 1);
+            const double2 hs1 = make_double2(sL + s1.x + s1.y, s1.x + s1.y + sR);
+            const double2 his1 = make_double2(iL + is1.x + is1.y, is1.x + is1.y + iR);
+            double2 a2, c2;
+            {
+                const double xb = (hs_a.x + hs_b.x + hs1.x) * (1.0 / 9.0);
+                a2.x = g2.x * ((his_a.x + his_b.x + his1.x) * (1.0 / 9.0) - mu2.x * xb);
+                c2.x = g2.x != 0.0 ? xb - mu2.x * a2.x : 0.0;
+            }
+            {
+                const double xb = (hs_a.y + hs_b.y + hs1.y) * (1.0 / 9.0);
+                a2.y = g2.y * ((his_a.y + his_b.y + his1.y) * (1.0 / 9.0) - mu2.y * xb);
+                c2.y = g2.y != 0.0 ? xb - mu2.y * a2.y : 0.0;
+            }
+            // S3 at row Y-3
+            const double aL = __shfl_up_sync(FULL, a2.y, 1), aR = __shfl_down_sync(FULL, a2.x, 1);
+            const double cL = __shfl_up_sync(FULL, c2.y, 1), cR = __shfl_down_sync(FULL, c2.x, 1);
+            const double2 ha2 = make_double2(aL + a2.x + a2.y, a2.x + a2.y + aR);
+            const double2 hc2 = make_double2(cL + c2.x + c2.y, c2.x + c2.y + cR);
+            const int nrow = max(min(r3 + 1, H - 2) - max(r3 - 1, 1) + 1, 0);
+            double2 Mc;
+            Mc.x = static_cast<double>(nrow * nc0) * s3.x - (hc_a.x + hc_b.x + hc2.x) - Im3.x * (ha_a.x + ha_b.x + ha2.x);
+            Mc.y = static_cast<double>(nrow * nc1) * s3.y - (hc_a.y + hc_b.y + hc2.y) - Im3.y * (ha_a.y + ha_b.y + ha2.y);
+            // S5 at row Y-4
+            const double ML = __shfl_up_sync(FULL, M_b.y, 1), MR = __shfl_down_sync(FULL, M_b.x, 1);
+            const double t0 = 4.0 * M_b.x - M_a.x - Mc.x - ML - M_b.y;
+            const double t1 = 4.0 * M_b.y - M_a.y - Mc.y - M_b.x - MR;
+            const double2 val = make_double2(d4.x + t0 * lam, d4.y + t1 * lam);
+            if (st_i >= 2 * HALO) {
+                if (writer) {
+                    *reinterpret_cast<double2*>(oc + o4c) = val;
+                    dotp += pm4.x * val.x + pm4.y * val.y;
+                }
+                if (CG && (--blk_left == 0 || st_i + 1 == steps)) {  // close the row block
+                    const double ws = warp_sum(dotp);
+                    const int yo = r0 + st_i - 2 * HALO;
+                    if (lane == 0) part[(static_cast<size_t>(ch) * nbands + band) * nrb + yo / RB] = ws;
+                    dotp = 0.0;
+                    blk_left = RB;
+                }
+            }
+            pm4 = pm3; pm3 = pm2; pm2 = pm1; pm1 = p0;
+            Im3 = Im2; Im2 = Im1;
+            s3 = s2; s2 = s1;
+            hs_a = hs_b; hs_b = hs1; his_a = his_b; his_b = his1;
+            ha_a = ha_b; ha_b = ha2; hc_a = hc_b; hc_b = hc2;
+            M_a = M_b; M_b = Mc;
+            r3 = r3 + 1 == H ? 0 : r3 + 1;
+        }
+    }
+    if (CG) {
+        unsigned int prev = 0;
+        if (lane == 0) {
+            __threadfence();
+            prev = atomicAdd(&st[ch].cnt_a, 1u);
+        }
+        prev = __shfl_sync(FULL, prev, 0);
+        if (prev == static_cast<unsigned int>(nblk) - 1u) {
+            __threadfence();
+            const double* pa = part + static_cast<size_t>(ch) * nbands * nrb;
+            double sacc = 0.0;
+#pragma unroll 8
+            for (int i = lane; i < nbands * nrb; i += 32) sacc += __ldcg(pa + i);
+            const double pAp = warp_sum(sacc);
+            if (lane == 0) {
+                CgState& S = st[ch];
+                S.pAp = pAp;
+                if (!(pAp > 0)) {  // pansharpen.cpp:240-244
+                    S.done = (sqrt(S.rs) <= 1e-12 * S.rhs_norm) ? 1 : 2;
+                    S.iters = S.t + 1;
+                } else {
+                    S.alpha = S.rs / pAp;
+                }
+                S.cnt_a = 0;
+            }
+        }
+    }
+}
+
 }  // namespace fast
 }  // namespace fbmp_gpu

@@ -104,10 +104,10 @@ struct Context {
     std::map<std::tuple<int, int, int, int, int>, cufftHandle> plans;  // (kind, rows, cols, batch, 0)
     int sm_count = 148;
     // kernel profiling of the CG loop (bench.py roofline): total device ms and launches that
-    // did work, per kernel class {K_Q, K_A, K_U}
+    // did work, per kernel class {K_Q, K_D, K_L (or the single K_A), K_U}
     bool profile = false;
-    double prof_ms[3] = {0, 0, 0};
-    long long prof_n[3] = {0, 0, 0};
+    double prof_ms[4] = {0, 0, 0, 0};  // K_Q, K_D, K_L (K_A), K_U
+    long long prof_n[4] = {0, 0, 0, 0};
 
     explicit Context(int dev);
     ~Context();

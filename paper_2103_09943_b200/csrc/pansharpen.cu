@@ -952,6 +952,7 @@ std::pair<AFn, size_t> apply3_select(const PsGeo& G) {
 // K_D + K_L (the default CG operator; env FBMP_KA=4 selects the single-kernel K_A)
 struct LlpPlan {
     int nb = 0, k = 1, R = 0, ctas = 0;
+    bool pairs = false;  // k_llp2 (column pairs; W even)
 };
 inline bool use_llp() {
     static const bool on = !(std::getenv("FBMP_KA") && std::atoi(std::getenv("FBMP_KA")) == 4);
@@ -960,15 +961,21 @@ inline bool use_llp() {
 // Strip height: minimise rounds x (R + 8) (a warp's steps, 8 = pipeline warm-up rows) over the
 // resident warp slots; R is a multiple of the partial row block.
 LlpPlan llp_plan(Context& ctx, const PsGeo& G) {
-    static int per_sm = 0;
-    if (!per_sm) {
-        int blocks = 0;
-        FBMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fast::k_llp<true>, fast::kl::NTL, 0));
-        per_sm = std::max(1, std::min(blocks, 16)) * (fast::kl::NTL / 32);
-    }
-    const long long slots = static_cast<long long>(per_sm) * ctx.sm_count;
+    static int per_sm[2] = {0, 0};
     LlpPlan L;
-    L.nb = ceil_div(G.W, fast::kl::BAND);
+    static const bool no_pairs = std::getenv("FBMP_KL1") != nullptr;
+    L.pairs = (G.W % 2 == 0) && !no_pairs;
+    int& ps = per_sm[L.pairs ? 1 : 0];
+    if (!ps) {
+        int blocks = 0;
+        if (L.pairs)
+            FBMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fast::k_llp2<true>, fast::kl::NTL, 0));
+        else
+            FBMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fast::k_llp<true>, fast::kl::NTL, 0));
+        ps = std::max(1, std::min(blocks, 32)) * (fast::kl::NTL / 32);
+    }
+    const long long slots = static_cast<long long>(ps) * ctx.sm_count;
+    L.nb = ceil_div(G.W, L.pairs ? fast::kl::BAND2 : fast::kl::BAND);
     const long long bc = static_cast<long long>(L.nb) * G.N;
     long long best = -1;
     for (int k = 1; k <= ceil_div(G.H, fast::kl::RB); ++k) {
@@ -1003,7 +1010,7 @@ std::pair<void (*)(PsGeo, const double*, const double*, double*, const CgState*)
 template <bool CG>
 void launch_llp(Context& ctx, const PsGeo& G, const double* taps, const double* guide, const double* mu,
                 const double* gk, const double* p, const double* q, double* out, CgState* st, double* part,
-                bool pdl = false) {
+                bool pdl = false, cudaEvent_t between = nullptr) {
     const int S = (G.N + G.cps - 1) / G.cps;
     const int nba = ceil_div(G.W, fast::a4::TA) * ceil_div(G.H, fast::a4::TA);
     const int groups = (G.cps + G.cpc - 1) / G.cpc;
@@ -1013,22 +1020,28 @@ void launch_llp(Context& ctx, const PsGeo& G, const double* taps, const double* 
                    static_cast<const CgState*>(st));
     else
         fd.first<<<dim3(nba, S * groups), fast::NT, fd.second, ctx.stream>>>(G, taps, q, out, st);
+    if (between) FBMP_CUDA(cudaEventRecordWithFlags(between, ctx.stream, cudaEventRecordExternal));
     const LlpPlan L = llp_plan(ctx, G);
-    fast::k_llp<CG><<<dim3(L.ctas, G.N), fast::kl::NTL, 0, ctx.stream>>>(G, guide, mu, gk, p, out, st, part, L.nb,
-                                                                          L.k, L.R);
+    if (L.pairs)
+        fast::k_llp2<CG><<<dim3(L.ctas, G.N), fast::kl::NTL, 0, ctx.stream>>>(G, guide, mu, gk, p, out, st, part,
+                                                                               L.nb, L.k, L.R);
+    else
+        fast::k_llp<CG><<<dim3(L.ctas, G.N), fast::kl::NTL, 0, ctx.stream>>>(G, guide, mu, gk, p, out, st, part,
+                                                                              L.nb, L.k, L.R);
 }
 
 template <bool CG>
 void launch_apply2(Context& ctx, const PsGeo& G, const double* taps, const double* guide, const double* mu,
                    const double* gk, const double* p, const double* q, double* out, CgState* st, double* part,
-                   bool pdl = false) {
+                   bool pdl = false, cudaEvent_t between = nullptr) {
     const int S = (G.N + G.cps - 1) / G.cps;
     const int nba = ceil_div(G.W, fast::a4::TA) * ceil_div(G.H, fast::a4::TA);
     const int groups = (G.cps + G.cpc - 1) / G.cpc;
     if (use_llp()) {
-        launch_llp<CG>(ctx, G, taps, guide, mu, gk, p, q, out, st, part, pdl);
+        launch_llp<CG>(ctx, G, taps, guide, mu, gk, p, q, out, st, part, pdl, between);
         return;
     }
+    if (between) FBMP_CUDA(cudaEventRecordWithFlags(between, ctx.stream, cudaEventRecordExternal));
     const auto fs = apply3_select<CG>(G);
     if (pdl)
         launch_pdl(fs.first, dim3(nba, S * groups), dim3(fast::NT), fs.second, ctx.stream, G, taps, guide, mu, gk, p,
@@ -1138,7 +1151,7 @@ void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* 
     double* part_init = B.part;
     double* part_q = part_init + static_cast<size_t>(N) * nba;
     double* part_a = part_q + static_cast<size_t>(N) * nbq;
-    const int nbA = fastA && use_llp() ? std::max(nba, ceil_div(G.W, fast::kl::BAND) * ceil_div(G.H, fast::kl::RB)) : nba;
+    const int nbA = fastA && use_llp() ? std::max(nba, ceil_div(G.W, fast::kl::BAND) * ceil_div(G.H, fast::kl::RB)) : nba;  // >= k_llp2's
     double* part_u = part_a + static_cast<size_t>(N) * nbA;
     // counters must start at zero
     FBMP_CUDA(cudaMemsetAsync(B.st, 0, sizeof(CgState) * N, ctx.stream));
@@ -1156,7 +1169,8 @@ void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* 
     // on B200 (C1/C2/C4 scenes): only K_A gains (its guide-tile loads overlap K_Q's tail, -2%);
     // PDL on K_Q costs ~5 us per iteration on small grids and on K_U ~7 us on C2.
     static const int pdl_mask = std::getenv("FBMP_PDL") ? std::atoi(std::getenv("FBMP_PDL")) : 2;
-    std::vector<cudaEvent_t> pev(prof ? chunk * 4 : 0);
+    constexpr int EV = 5;  // profile events per iteration: K_Q | K_D | K_L (or K_A) | K_U
+    std::vector<cudaEvent_t> pev(prof ? chunk * EV : 0);
     for (auto& e : pev) FBMP_CUDA(cudaEventCreate(&e));
     // the chunk graph depends only on geometry, buffers and launch shapes: cache it in the context
     std::string key;
@@ -1177,7 +1191,7 @@ void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* 
         cudaGraph_t graph;
         FBMP_CUDA(cudaStreamBeginCapture(ctx.stream, cudaStreamCaptureModeThreadLocal));
         for (int it = 0; it < chunk; ++it) {
-            if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * 4 + 0], ctx.stream, cudaEventRecordExternal));
+            if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * EV + 0], ctx.stream, cudaEventRecordExternal));
             if (q2.fn && (pdl_mask & 1))
                 launch_pdl(q2.fn, dim3(nbq, N), dim3(fast::NT), sq, ctx.stream, G, d_taps, B.r, B.p, B.q, B.st,
                            part_q, nbq);
@@ -1185,18 +1199,21 @@ void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* 
                 q2.fn<<<dim3(nbq, N), fast::NT, sq, ctx.stream>>>(G, d_taps, B.r, B.p, B.q, B.st, part_q, nbq);
             else
                 k_q<true><<<dim3(nbq, N), NTQ, sq, ctx.stream>>>(G, d_taps, B.r, B.p, B.q, B.st, part_q, nbq);
-            if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * 4 + 1], ctx.stream, cudaEventRecordExternal));
-            if (fastA)
-                launch_apply2<true>(ctx, G, d_taps, d_guide, wmu, wg, B.p, B.q, B.Ap, B.st, part_a, (pdl_mask & 2) != 0);
-            else
+            if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * EV + 1], ctx.stream, cudaEventRecordExternal));
+            if (fastA) {
+                launch_apply2<true>(ctx, G, d_taps, d_guide, wmu, wg, B.p, B.q, B.Ap, B.st, part_a, (pdl_mask & 2) != 0,
+                                    prof ? pev[it * EV + 2] : nullptr);
+            } else {
+                if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * EV + 2], ctx.stream, cudaEventRecordExternal));
                 k_apply<0, true><<<dim3(nba, N), NTA, sa, ctx.stream>>>(G, d_taps, d_guide, B.p, B.q, B.Ap, B.st,
                                                                          part_a, nba);
-            if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * 4 + 2], ctx.stream, cudaEventRecordExternal));
+            }
+            if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * EV + 3], ctx.stream, cudaEventRecordExternal));
             if (pdl_mask & 4)
                 launch_pdl(k_update, dim3(nbu, N), dim3(NTU), 0, ctx.stream, G, B.z, B.r, B.p, B.Ap, B.st, part_u, nbu);
             else
                 k_update<<<dim3(nbu, N), NTU, 0, ctx.stream>>>(G, B.z, B.r, B.p, B.Ap, B.st, part_u, nbu);
-            if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * 4 + 3], ctx.stream, cudaEventRecordExternal));
+            if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * EV + 4], ctx.stream, cudaEventRecordExternal));
         }
         FBMP_CUDA(cudaStreamEndCapture(ctx.stream, &graph));
         FBMP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
@@ -1238,9 +1255,9 @@ void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* 
             for (int i = 0; i < N; ++i) active_iters = std::max(active_iters, pinned[i].done ? pinned[i].iters : pinned[i].t);
             for (int it = 0; it < chunk; ++it) {
                 if (g * chunk + it >= active_iters) break;
-                for (int kk = 0; kk < 3; ++kk) {
+                for (int kk = 0; kk < EV - 1; ++kk) {
                     float ms = 0.f;
-                    FBMP_CUDA(cudaEventElapsedTime(&ms, pev[it * 4 + kk], pev[it * 4 + kk + 1]));
+                    FBMP_CUDA(cudaEventElapsedTime(&ms, pev[it * EV + kk], pev[it * EV + kk + 1]));
                     ctx.prof_ms[kk] += ms;
                     ctx.prof_n[kk] += 1;
                 }

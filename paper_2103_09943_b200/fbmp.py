@@ -164,10 +164,10 @@ class Context:
         _lib.fbmp_gpu_ctx_set_profile(self.h, int(on))
 
     def kernel_profile(self) -> dict:
-        ms = (C.c_double * 3)()
-        n = (C.c_longlong * 3)()
+        ms = (C.c_double * 4)()
+        n = (C.c_longlong * 4)()
         _check(_lib.fbmp_gpu_ctx_kernel_profile(self.h, ms, n))
-        return {name: dict(total_ms=ms[i], launches=n[i]) for i, name in enumerate(("K_Q", "K_A", "K_U"))}
+        return {name: dict(total_ms=ms[i], launches=n[i]) for i, name in enumerate(("K_Q", "K_D", "K_L", "K_U"))}
 
     def stats(self) -> dict:
         s = _Stats()

@@ -587,3 +587,31 @@ def test_blind_oracle_vs_numpy(orc):
     assert rel(ic["kernel"], inn["kernel"]) < 1e-9
     assert list(ic["cg_iters"]) == list(inn["cg_iters"])
     assert rel(out_c, out_n) < 1e-6
+
+
+# ---- the alias-group eigen-solver (Eigen::SelfAdjointEigenSolver at pansharpen.cpp:353) ------
+
+@pytest.mark.parametrize("n,kind", [(3, "gram"), (9, "gram"), (16, "gram"), (16, "alias"), (16, "graded")])
+def test_herm_eig_ql(orc, n, kind):
+    """Householder + QL (used by the alias solve) agrees with LAPACK and with the Jacobi solver:
+    eigenvalues to eps ||A||, A = V diag(ev) V^H, V unitary, eigenvalues ascending."""
+    rng = np.random.default_rng(n * 7 + len(kind))
+    for _ in range(4):
+        if kind == "gram":
+            B = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+            A = B @ B.conj().T
+        elif kind == "alias":  # b b^H / c^2 + lambda |l|^2 on the diagonal (the alias-group system)
+            b = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+            A = np.outer(b.conj(), b) / n + np.diag(rng.uniform(1e-6, 2.0, n))
+        else:  # widely graded spectrum (condition ~1e12)
+            Qm, _ = np.linalg.qr(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+            A = (Qm * np.logspace(-12, 0, n)) @ Qm.conj().T
+            A = 0.5 * (A + A.conj().T)
+        ev, V = orc.herm_eig(A, 0)
+        ev_j, _ = orc.herm_eig(A, 1)
+        scale = np.abs(np.linalg.eigvalsh(A)).max()
+        assert np.all(np.diff(ev) >= 0)
+        assert np.abs(ev - np.linalg.eigvalsh(A)).max() < 1e-13 * scale
+        assert np.abs(ev - ev_j).max() < 1e-13 * scale
+        assert np.linalg.norm(V @ np.diag(ev) @ V.conj().T - A) < 1e-13 * np.linalg.norm(A)
+        assert np.linalg.norm(V.conj().T @ V - np.eye(n)) < 1e-13

@@ -17,8 +17,10 @@ col = {h: i for i, h in enumerate(hdr)}
 def cls(name):
     if "k_q" in name:
         return "K_Q"
-    if "k_apply" in name:
-        return "K_A"
+    if "k_dterm" in name:
+        return "K_D"
+    if "k_llp" in name or "k_apply" in name:
+        return "K_L"
     if "k_update" in name:
         return "K_U"
     return name.split("(")[0][-40:]

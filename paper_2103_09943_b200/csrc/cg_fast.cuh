@@ -686,7 +686,7 @@ constexpr int NTL = 32;           // one warp per CTA: every loop bound derives 
                                   // the compiler sees a convergent warp and emits plain SHFLs
 constexpr int BAND = 24;          // output columns per warp
 constexpr int HALO = 4;           // L M L has radius 4
-constexpr int RB = 32;            // rows per p.out partial (strip heights are multiples of RB, so
+constexpr int RB = 16;            // rows per p.out partial (strip heights are multiples of RB, so
                                   // the reduction tree does not depend on the strip partition)
 }  // namespace kl
 

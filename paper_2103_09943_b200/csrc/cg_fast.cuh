@@ -681,7 +681,10 @@ __global__ void __launch_bounds__(NT, 2) k_apply4(PsGeo G, const double* __restr
 // ------------------------------------------------------------------------------------------
 namespace kl {
 template <int CF>
-constexpr size_t dterm_smem() { return (a4::MAXTAP + 2 * a4::L<CF>::QWP * a4::L<CF>::QWMAX) * sizeof(double); }
+constexpr size_t dterm_smem(int windows = 2) {  // taps | q windows (2 alternating, or one per channel)
+    return (a4::MAXTAP + static_cast<size_t>(windows < 2 ? 2 : windows) * a4::L<CF>::QWP * a4::L<CF>::QWMAX) *
+           sizeof(double);
+}
 constexpr int NTL = 32;           // one warp per CTA: every loop bound derives from blockIdx, so
                                   // the compiler sees a convergent warp and emits plain SHFLs
 constexpr int BAND = 24;          // output columns per warp
@@ -724,6 +727,64 @@ __global__ void __launch_bounds__(NT, 2) k_dterm(PsGeo G, const double* __restri
         active = __ballot_sync(0xffffffffu, !dn);
     }
     const int QN = QH * QW;
+    if constexpr (N_ > 0) {
+        // register taps: the q windows of all active channels of the group go to shared memory
+        // at once (one barrier), then every thread applies its phase sub-kernel, loaded once, to
+        // each channel
+        constexpr int QSZ = Lay::QWP * Lay::QWMAX;
+        const int na = __popc(active);
+        for (int e = threadIdx.x; e < na * QN; e += NT) {
+            const int c = e / QN, r = e - c * QN;
+            const int a = r / QW, b = r - a * QW;
+            const int chl = ch_lo + static_cast<int>(__fns(active, 0, c + 1));  // c-th active channel
+            const double* qc = q + static_cast<size_t>(scene * G.cps + chl) * G.h * G.w;
+            sq[c * QSZ + a * QS + b] = __ldg(qc + static_cast<size_t>(wrapi(iq0 + a, G.h)) * G.w + wrapi(jq0 + b, G.w));
+        }
+        __syncthreads();
+        constexpr int CW4 = TA / CF, RB4 = CW4 / 4;
+        const int pc = threadIdx.x % CF;
+        const int Jc = (threadIdx.x / CF) % CW4;
+        const int rest = threadIdx.x / (CF * CW4);
+        const int Ic0 = (rest % RB4) * 4;
+        const int pr = rest / RB4;
+        double kreg[DM][DM];
+#pragma unroll
+        for (int a = 0; a < DM; ++a)
+#pragma unroll
+            for (int b = 0; b < DM; ++b) {
+                const int tr = CF * (a + D::DLO) - pr + D::C, tc = CF * (b + D::DLO) - pc + D::C;
+                kreg[a][b] = (tr >= 0 && tr < N_ && tc >= 0 && tc < N_) ? sk[tr * N_ + tc] : 0.0;
+            }
+        const int qoff = (r0 / CF + Ic0 - iq0 + D::DLO) * QS + (c0 / CF + Jc - jq0 + D::DLO);
+        const int Cc = c0 + Jc * CF + pc;
+        int c = 0;
+        for (unsigned int m = active; m; m &= m - 1u, ++c) {
+            const int chl = ch_lo + __ffs(m) - 1;
+            const double* qb = sq + c * QSZ + qoff;
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int m = 0; m < DM + 3; ++m) {
+                double qv[DM];
+#pragma unroll
+                for (int b = 0; b < DM; ++b) qv[b] = qb[m * QS + b];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int a = m - k;
+                    if (a >= 0 && a < DM) {
+#pragma unroll
+                        for (int b = 0; b < DM; ++b) acc[k] = fma(kreg[a][b], qv[b], acc[k]);
+                    }
+                }
+            }
+            double* oc = out + (scene * G.cps + chl) * P;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int R = r0 + (Ic0 + k) * CF + pr;
+                if (R < H && Cc < W) oc[static_cast<size_t>(R) * W + Cc] = acc[k];
+            }
+        }
+        return;
+    }
     constexpr int KQ = (Lay::QWMAX * Lay::QWMAX + NT - 1) / NT;
     double pf[KQ];
     // the next channel's q window is loaded into registers while the current one is computed;

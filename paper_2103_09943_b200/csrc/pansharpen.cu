@@ -995,13 +995,13 @@ LlpPlan llp_plan(Context& ctx, const PsGeo& G) {
 template <bool CG>
 std::pair<void (*)(PsGeo, const double*, const double*, double*, const CgState*), size_t> dterm_select(const PsGeo& G) {
     if (G.c == 4) {
-        const size_t sm = fast::kl::dterm_smem<4>();
+        const size_t sm = fast::kl::dterm_smem<4>(G.cpc);  // register-tap variants hold every channel's window
         switch (G.n) {
         case 21: return {fast::k_dterm<CG, 21, 4>, sm};
         case 17: return {fast::k_dterm<CG, 17, 4>, sm};
         case 15: return {fast::k_dterm<CG, 15, 4>, sm};
         case 7: return {fast::k_dterm<CG, 7, 4>, sm};
-        default: return {fast::k_dterm<CG, 0, 4>, sm};
+        default: return {fast::k_dterm<CG, 0, 4>, fast::kl::dterm_smem<4>()};
         }
     }
     if (G.c == 2) return {fast::k_dterm<CG, 0, 2>, fast::kl::dterm_smem<2>()};

@@ -89,25 +89,36 @@ template <int N_, int CF>
 struct QGeo {
     static constexpr int C = (N_ - 1) / 2;
     static constexpr int g = (C + CF - 1) / CF;
-    static constexpr int TW = 32, TH = 16;
-    static constexpr int PW = TW + 2 * g, PH = TH + 2 * g;
-    static constexpr int PS = pstride(PW * PH);
+    static constexpr int NTH = 128;                        // 4 warps
+    static constexpr int MJ = 4;                           // LR columns per thread
+    static constexpr int TH = 32, TW = MJ * (NTH / 32);    // lane = LR row, warp = 4 LR columns
+    static constexpr int PW = TW + 2 * g, PH = TH + 2 * g; // phase-plane extent (LR)
+    static constexpr int PWS = PW | 1;                     // odd row stride: lanes (rows) hit distinct banks
+    static constexpr int PS = pstride(PWS * PH);
     static constexpr int SRW = CF * PW, SRH = CF * PH;
     static constexpr int KOFF = ((N_ * N_ + 1) / 2) * 2;
     static constexpr size_t smem = (KOFF + static_cast<size_t>(CF) * CF * PS) * sizeof(double);
 };
 
+// K_Q: p = r + beta p_old (pansharpen.cpp:254) and q = D B p (pansharpen.cpp:218-223, first
+// half) at every LR point, plus ||p||^2. The HR region of the tile (+ halo) is split into CF x CF
+// sampling-phase planes in shared memory; tap (a, b) of LR point (i, j) reads plane
+// ((CF g - a) mod CF, (CF g - b) mod CF) at (i + (CF g - a) div CF, j + (CF g - b) div CF).
+// A lane owns one LR row and MJ consecutive LR columns: every plane value loaded feeds up to MJ
+// points and every (broadcast) tap MJ FMAs.
 template <int N_, int CF, bool CG>
-__global__ void __launch_bounds__(NT, 2) k_q2(PsGeo G, const double* __restrict__ taps, const double* __restrict__ src,
-                                              double* __restrict__ pbuf, double* __restrict__ q, CgState* st,
-                                              double* __restrict__ part, int nblk) {
+__global__ void __launch_bounds__(QGeo<N_, CF>::NTH, 3) k_q2(PsGeo G, const double* __restrict__ taps,
+                                                             const double* __restrict__ src,
+                                                             double* __restrict__ pbuf, double* __restrict__ q,
+                                                             CgState* st, double* __restrict__ part, int nblk) {
     using Q = QGeo<N_, CF>;
-    __shared__ double red[NT / 32 + 1];
+    constexpr int NQ = Q::NTH;
+    __shared__ double red[NQ / 32 + 1];
     extern __shared__ double sm[];
     const int ch = blockIdx.y;
     const double* tp = taps + static_cast<size_t>(ch / G.cps) * N_ * N_;
     double* sk = sm;
-    for (int e = threadIdx.x; e < N_ * N_; e += NT) sk[e] = tp[e];
+    for (int e = threadIdx.x; e < N_ * N_; e += NQ) sk[e] = tp[e];
     int t = 0;
     double beta = 0.0;
     if (CG) {
@@ -128,7 +139,7 @@ __global__ void __launch_bounds__(NT, 2) k_q2(PsGeo G, const double* __restrict_
     double* planes = sm + Q::KOFF;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int R0 = CF * (i0 - Q::g), C0 = CF * (j0 - Q::g);
-    constexpr int own_r0 = CF * Q::g, own_r1 = CF * (Q::g + Q::TH), own_c1 = CF * (Q::g + Q::TW);
+    constexpr int own_r0 = CF * Q::g, own_r1 = CF * (Q::g + Q::TH);
     double pp = 0.0;
     // region load in runs of CF consecutive HR columns (one LR column, all column phases): the
     // run start is a multiple of CF in a row of W = w CF, so a run never wraps and its loads and
@@ -136,12 +147,12 @@ __global__ void __launch_bounds__(NT, 2) k_q2(PsGeo G, const double* __restrict_
     using VT = typename std::conditional<CF == 4, double4_t, typename std::conditional<CF == 2, double2, double>::type>::type;
     constexpr int RUNS = Q::SRH * Q::PW;
     constexpr int KB = 4;
-    for (int e0 = 0; e0 < RUNS; e0 += NT * KB) {
+    for (int e0 = 0; e0 < RUNS; e0 += NQ * KB) {
         VT vr[KB], vp[KB];
         size_t gi[KB];
 #pragma unroll
         for (int k = 0; k < KB; ++k) {
-            const int e = e0 + k * NT + threadIdx.x;
+            const int e = e0 + k * NQ + threadIdx.x;
             const int rr = e / Q::PW, jc = e - rr * Q::PW;
             gi[k] = static_cast<size_t>(wrap_once(R0 + rr, H)) * W + wrap_once(C0 + CF * jc, W);
             if (e < RUNS) {
@@ -151,7 +162,7 @@ __global__ void __launch_bounds__(NT, 2) k_q2(PsGeo G, const double* __restrict_
         }
 #pragma unroll
         for (int k = 0; k < KB; ++k) {
-            const int e = e0 + k * NT + threadIdx.x;
+            const int e = e0 + k * NQ + threadIdx.x;
             if (e >= RUNS) break;
             const int rr = e / Q::PW, jc = e - rr * Q::PW;
             double v[CF];
@@ -167,62 +178,58 @@ __global__ void __launch_bounds__(NT, 2) k_q2(PsGeo G, const double* __restrict_
                     for (int u = 0; u < CF; ++u) pp += v[u] * v[u];
                 }
             }
-            double* pl = planes + ((rr % CF) * CF) * Q::PS + (rr / CF) * Q::PW + jc;
+            double* pl = planes + ((rr % CF) * CF) * Q::PS + (rr / CF) * Q::PWS + jc;
 #pragma unroll
             for (int u = 0; u < CF; ++u) pl[u * Q::PS] = v[u];
         }
     }
     __syncthreads();
-    // two vertically adjacent LR points per thread: (i0 + 2 warp + {0,1}, j0 + lane)
-    const int ti = 2 * warp, tj = lane;
-    const double* base = planes + ti * Q::PW + tj;
-    double acc0 = 0.0, acc1 = 0.0;
-    // Plane row (phase pr, row offset Ir) feeds tap row a0 = CF g - pr - CF Ir of point 0 and
-    // a0 + CF of point 1: each row segment is loaded once and used by both points.
-    for (int pr = 0; pr < CF; ++pr) {
-        const int ir_lo = (CF * Q::g - pr - Q::C + CF - 1) / CF - 1;  // smallest Ir with a0 + CF <= C
-        const int ir_hi = (CF * Q::g - pr + Q::C) / CF + 1;           // largest Ir with a0 + CF >= -C
-        for (int ir = max(ir_lo, 0); ir <= ir_hi; ++ir) {
-            const int a0 = CF * Q::g - pr - CF * ir;
-            const bool v0 = a0 >= -Q::C && a0 <= Q::C;
-            const bool v1 = a0 + CF >= -Q::C && a0 + CF <= Q::C;
-            const double* row = base + pr * CF * Q::PS + ir * Q::PW;
-            const double* k0 = sk + (a0 + Q::C) * N_ + Q::C;
-            const double* k1 = k0 + CF * N_;
-            if (v0 && v1) {
+    // points (i0 + lane, j0 + MJ warp + m), m < MJ
+    constexpr int MJ = Q::MJ;
+    const double* base = planes + lane * Q::PWS + MJ * warp;
+    double acc[MJ];
 #pragma unroll
-                for (int b = -Q::C; b <= Q::C; ++b) {
-                    const int cb = CF * Q::g - b;
-                    const double v = row[(cb % CF) * Q::PS + cb / CF];
-                    acc0 = fma(k0[b], v, acc0);
-                    acc1 = fma(k1[b], v, acc1);
-                }
-            } else if (v0) {
+    for (int m = 0; m < MJ; ++m) acc[m] = 0.0;
+    constexpr int G4 = CF * Q::g;
+    constexpr int JMAX = (G4 + Q::C) / CF + 1;
 #pragma unroll
-                for (int b = -Q::C; b <= Q::C; ++b) {
-                    const int cb = CF * Q::g - b;
-                    acc0 = fma(k0[b], row[(cb % CF) * Q::PS + cb / CF], acc0);
-                }
-            } else if (v1) {
+    for (int a = -Q::C; a <= Q::C; ++a) {
+        const int ra = G4 - a;  // >= 0; constants once unrolled
+        const int pr = ra % CF, ir = ra / CF;
+        const double* krow = sk + (a + Q::C) * N_ + Q::C;
 #pragma unroll
-                for (int b = -Q::C; b <= Q::C; ++b) {
-                    const int cb = CF * Q::g - b;
-                    acc1 = fma(k1[b], row[(cb % CF) * Q::PS + cb / CF], acc1);
+        for (int pc = 0; pc < CF; ++pc) {
+            // column offsets jo with tap b = G4 - pc - CF jo in [-C, C]
+            const int jlo = (G4 - pc - Q::C + CF - 1) / CF, jhi = (G4 - pc + Q::C) / CF;  // G4 - pc - C > -CF
+            const double* prow = base + (pr * CF + pc) * Q::PS + ir * Q::PWS;
+            double v[JMAX + MJ];
+#pragma unroll
+            for (int x = 0; x < JMAX + MJ; ++x)
+                if (x >= jlo && x <= jhi + MJ - 1) v[x] = prow[x];
+#pragma unroll
+            for (int jo = 0; jo < JMAX; ++jo) {
+                if (jo >= jlo && jo <= jhi) {
+                    const double kv = krow[G4 - pc - CF * jo];
+#pragma unroll
+                    for (int m = 0; m < MJ; ++m) acc[m] = fma(kv, v[jo + m], acc[m]);
                 }
             }
         }
     }
-    const int i = i0 + ti, j = j0 + tj;
+    const int i = i0 + lane;
     double* qc = q + static_cast<size_t>(ch) * G.h * G.w;
-    if (j < G.w) {
-        if (i < G.h) qc[static_cast<size_t>(i) * G.w + j] = acc0;
-        if (i + 1 < G.h) qc[static_cast<size_t>(i + 1) * G.w + j] = acc1;
+    if (i < G.h) {
+#pragma unroll
+        for (int m = 0; m < MJ; ++m) {
+            const int j = j0 + MJ * warp + m;
+            if (j < G.w) qc[static_cast<size_t>(i) * G.w + j] = acc[m];
+        }
     }
     if (CG) {
-        const double bs = block_sum<NT>(pp, red);
+        const double bs = block_sum<NQ>(pp, red);
         if (threadIdx.x == 0) part[static_cast<size_t>(ch) * nblk + blockIdx.x] = bs;
         if (elect_last_block(&st[ch].cnt_q, nblk)) {
-            const double tot = sum_partials<NT>(part + static_cast<size_t>(ch) * nblk, nblk, 1, red);
+            const double tot = sum_partials<NQ>(part + static_cast<size_t>(ch) * nblk, nblk, 1, red);
             if (threadIdx.x == 0) {
                 st[ch].pp = tot;
                 st[ch].cnt_q = 0;

@@ -892,6 +892,7 @@ struct QLaunch {
     QFn fn = nullptr;
     size_t smem = 0;
     int nblk = 0;
+    int threads = 0;
 };
 template <int N_, int CF, bool CG>
 QLaunch q2_make(const PsGeo& G) {
@@ -899,6 +900,7 @@ QLaunch q2_make(const PsGeo& G) {
     L.fn = fast::k_q2<N_, CF, CG>;
     L.smem = fast::QGeo<N_, CF>::smem;
     L.nblk = fast::q2_blocks<N_, CF>(G);
+    L.threads = fast::QGeo<N_, CF>::NTH;
     return L;
 }
 template <bool CG>
@@ -1084,7 +1086,7 @@ void cg_operator_apply(Context& ctx, const PsGeo& G, const double* d_taps, const
         const QLaunch ql = q2_select<false>(G);
         if (ql.fn) {
             set_smem(ql.fn, ql.smem);
-            ql.fn<<<dim3(ql.nblk, G.N), fast::NT, ql.smem, ctx.stream>>>(G, d_taps, d_p, nullptr, q, nullptr, nullptr,
+            ql.fn<<<dim3(ql.nblk, G.N), ql.threads, ql.smem, ctx.stream>>>(G, d_taps, d_p, nullptr, q, nullptr, nullptr,
                                                                           ql.nblk);
         } else {
             const size_t sq = q_smem(G);
@@ -1193,10 +1195,10 @@ void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* 
         for (int it = 0; it < chunk; ++it) {
             if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * EV + 0], ctx.stream, cudaEventRecordExternal));
             if (q2.fn && (pdl_mask & 1))
-                launch_pdl(q2.fn, dim3(nbq, N), dim3(fast::NT), sq, ctx.stream, G, d_taps, B.r, B.p, B.q, B.st,
+                launch_pdl(q2.fn, dim3(nbq, N), dim3(q2.threads), sq, ctx.stream, G, d_taps, B.r, B.p, B.q, B.st,
                            part_q, nbq);
             else if (q2.fn)
-                q2.fn<<<dim3(nbq, N), fast::NT, sq, ctx.stream>>>(G, d_taps, B.r, B.p, B.q, B.st, part_q, nbq);
+                q2.fn<<<dim3(nbq, N), q2.threads, sq, ctx.stream>>>(G, d_taps, B.r, B.p, B.q, B.st, part_q, nbq);
             else
                 k_q<true><<<dim3(nbq, N), NTQ, sq, ctx.stream>>>(G, d_taps, B.r, B.p, B.q, B.st, part_q, nbq);
             if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * EV + 1], ctx.stream, cudaEventRecordExternal));

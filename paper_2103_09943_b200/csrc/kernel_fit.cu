@@ -512,7 +512,7 @@ enum { F_U = 0, F_P1, F_P2, F_X0, F_X1, F_Y0, F_Y1, F_Y2, F_Y3, F_Z, F_L10, F_L1
 
 struct AdmmSmem {
     double* f[17];
-    double *bz, *zz, *unew, *tmp6;  // tmp6: 6*m
+    double *bz, *zz, *unew, *tmp6;  // tmp6: max(6m, 3 NTADMM) doubles, projection scratch
     double *spec, *rowt;            // 3 complex planes each (6*m doubles)
     double *twc, *tws;              // n
     double* red;
@@ -543,6 +543,12 @@ __device__ __forceinline__ void up_symbol(const AdmmSmem& S, int n, int i, doubl
 }
 
 
+// interleaved complex planes: element e = (re, im) at doubles [2e, 2e+1] (16-byte aligned)
+__device__ __forceinline__ double2 cld2(const double* base, int e) { return reinterpret_cast<const double2*>(base)[e]; }
+__device__ __forceinline__ void cst2(double* base, int e, double re, double im) {
+    reinterpret_cast<double2*>(base)[e] = make_double2(re, im);
+}
+
 // forward 2-D DFT of 3 real n x n planes (src[f]) -> spec (3 interleaved complex planes).
 // One thread per output bin computes all three fields, sharing twiddles and index updates.
 __device__ void dft3_forward(const AdmmSmem& S, int n, const double* const src[3]) {
@@ -560,9 +566,9 @@ __device__ void dft3_forward(const AdmmSmem& S, int n, const double* const src[3
             idx += kc;
             if (idx >= n) idx -= n;
         }
-        S.rowt[2 * e] = re0; S.rowt[2 * e + 1] = im0;
-        S.rowt[2 * (m + e)] = re1; S.rowt[2 * (m + e) + 1] = im1;
-        S.rowt[2 * (2 * m + e)] = re2; S.rowt[2 * (2 * m + e) + 1] = im2;
+        cst2(S.rowt, e, re0, im0);
+        cst2(S.rowt, m + e, re1, im1);
+        cst2(S.rowt, 2 * m + e, re2, im2);
     }
     __syncthreads();
     for (int e = threadIdx.x; e < m; e += blockDim.x) {  // cols: F[kr][kc] = sum_r T[r][kc] w^(kr r)
@@ -573,7 +579,8 @@ __device__ void dft3_forward(const AdmmSmem& S, int n, const double* const src[3
             const double wc = S.twc[idx], wsn = -S.tws[idx];
 #pragma unroll
             for (int f = 0; f < 3; ++f) {
-                const double tr = S.rowt[2 * (f * m + r * n + kc)], ti = S.rowt[2 * (f * m + r * n + kc) + 1];
+                const double2 tv = cld2(S.rowt, f * m + r * n + kc);
+                const double tr = tv.x, ti = tv.y;
                 acc[f][0] = fma(tr, wc, fma(-ti, wsn, acc[f][0]));
                 acc[f][1] = fma(tr, wsn, fma(ti, wc, acc[f][1]));
             }
@@ -581,10 +588,7 @@ __device__ void dft3_forward(const AdmmSmem& S, int n, const double* const src[3
             if (idx >= n) idx -= n;
         }
 #pragma unroll
-        for (int f = 0; f < 3; ++f) {
-            S.spec[2 * (f * m + e)] = acc[f][0];
-            S.spec[2 * (f * m + e) + 1] = acc[f][1];
-        }
+        for (int f = 0; f < 3; ++f) cst2(S.spec, f * m + e, acc[f][0], acc[f][1]);
     }
     __syncthreads();
 }
@@ -600,7 +604,8 @@ __device__ void dft3_inverse(const AdmmSmem& S, int n, double* const dst[3]) {
             const double wc = S.twc[idx], wsn = S.tws[idx];
 #pragma unroll
             for (int f = 0; f < 3; ++f) {
-                const double fr = S.spec[2 * (f * m + kr * n + kc)], fi = S.spec[2 * (f * m + kr * n + kc) + 1];
+                const double2 fv = cld2(S.spec, f * m + kr * n + kc);
+                const double fr = fv.x, fi = fv.y;
                 acc[f][0] = fma(fr, wc, fma(-fi, wsn, acc[f][0]));
                 acc[f][1] = fma(fr, wsn, fma(fi, wc, acc[f][1]));
             }
@@ -608,10 +613,7 @@ __device__ void dft3_inverse(const AdmmSmem& S, int n, double* const dst[3]) {
             if (idx >= n) idx -= n;
         }
 #pragma unroll
-        for (int f = 0; f < 3; ++f) {
-            S.rowt[2 * (f * m + e)] = acc[f][0];
-            S.rowt[2 * (f * m + e) + 1] = acc[f][1];
-        }
+        for (int f = 0; f < 3; ++f) cst2(S.rowt, f * m + e, acc[f][0], acc[f][1]);
     }
     __syncthreads();
     const double inv = 1.0 / static_cast<double>(m);
@@ -622,8 +624,10 @@ __device__ void dft3_inverse(const AdmmSmem& S, int n, double* const dst[3]) {
         for (int kr = 0; kr < n; ++kr) {
             const double wc = S.twc[idx], ws = S.tws[idx];
 #pragma unroll
-            for (int f = 0; f < 3; ++f)
-                re[f] = fma(S.rowt[2 * (f * m + kr * n + c)], wc, fma(-S.rowt[2 * (f * m + kr * n + c) + 1], ws, re[f]));
+            for (int f = 0; f < 3; ++f) {
+                const double2 rv = cld2(S.rowt, f * m + kr * n + c);
+                re[f] = fma(rv.x, wc, fma(-rv.y, ws, re[f]));
+            }
             idx += r;
             if (idx >= n) idx -= n;
         }
@@ -709,9 +713,8 @@ __device__ void up_solve(const AdmmSmem& S, int n, double a1m1, double a2m2, dou
         const Z d4{sy[3], sy[4]}, d5{sy[5], sy[6]}, d6{sy[7], sy[8]};
         const double n6 = d6.x * d6.x + d6.y * d6.y;
         const Z den{sy[9], sy[10]};
-        Z b1{S.spec[2 * i], S.spec[2 * i + 1]};
-        Z b2{S.spec[2 * (m + i)], S.spec[2 * (m + i) + 1]};
-        Z b3{S.spec[2 * (2 * m + i)], S.spec[2 * (2 * m + i) + 1]};
+        const double2 s1 = cld2(S.spec, i), s2 = cld2(S.spec, m + i), s3 = cld2(S.spec, 2 * m + i);
+        Z b1{s1.x, s1.y}, b2{s2.x, s2.y}, b3{s3.x, s3.y};
         Z fu, fp1, fp2;
         const double aden = sqrt(den.x * den.x + den.y * den.y);
         if (aden > tol) {
@@ -734,9 +737,9 @@ __device__ void up_solve(const AdmmSmem& S, int n, double a1m1, double a2m2, dou
             fp1 = fabs(d2) > dtol ? rs(1.0 / d2, b2) : Z{0.0, 0.0};
             fp2 = fabs(d3) > dtol ? rs(1.0 / d3, b3) : Z{0.0, 0.0};
         }
-        S.spec[2 * i] = fu.x; S.spec[2 * i + 1] = fu.y;
-        S.spec[2 * (m + i)] = fp1.x; S.spec[2 * (m + i) + 1] = fp1.y;
-        S.spec[2 * (2 * m + i)] = fp2.x; S.spec[2 * (2 * m + i) + 1] = fp2.y;
+        cst2(S.spec, i, fu.x, fu.y);
+        cst2(S.spec, m + i, fp1.x, fp1.y);
+        cst2(S.spec, 2 * m + i, fp2.x, fp2.y);
     }
     __syncthreads();
     double* dst[3] = {uout, p1out, p2out};
@@ -797,9 +800,82 @@ __device__ int project_simplex_block(const double* v, double* out, int m, double
     return support;
 }
 
+// Same projection for m <= NTADMM, in O(log^2) steps: a bitonic sort of (value desc, index asc)
+// with one element per thread (partners within a warp by shuffles, across warps through shared
+// memory, double-buffered), the cumulative sums in sorted order by a block scan, and the largest
+// qualifying position by a block max. scratch: 3 * NTADMM doubles.
+__device__ int project_simplex_sorted(const double* v, double* out, int m, double* red, int* ired, double* scratch) {
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    double* kv[2] = {scratch, scratch + NTADMM};
+    int* ki[2] = {reinterpret_cast<int*>(scratch + 2 * NTADMM), reinterpret_cast<int*>(scratch + 2 * NTADMM) + NTADMM};
+    double val = t < m ? v[t] : -INFINITY;
+    int idx = t;
+    int buf = 0;
+    for (int k = 2; k <= NTADMM; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            double pv;
+            int pi;
+            if (j >= 32) {
+                kv[buf][t] = val;
+                ki[buf][t] = idx;
+                __syncthreads();
+                pv = kv[buf][t ^ j];
+                pi = ki[buf][t ^ j];
+                buf ^= 1;  // the next exchange writes the other buffer: one barrier per stage
+            } else {
+                pv = __shfl_xor_sync(0xffffffffu, val, j);
+                pi = __shfl_xor_sync(0xffffffffu, idx, j);
+            }
+            const bool own_first = val > pv || (val == pv && idx < pi);
+            const bool want_first = ((t & j) == 0) == ((t & k) == 0);
+            if (own_first != want_first) {
+                val = pv;
+                idx = pi;
+            }
+        }
+    }
+    // thread t holds the t-th largest value; inclusive scan in sorted order
+    double css = t < m ? val : 0.0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, css, o);
+        if (lane >= o) css += y;
+    }
+    if (lane == 31) red[wid] = css;
+    __syncthreads();
+    if (wid == 0) {
+        double x = lane < NTADMM / 32 ? red[lane] : 0.0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane < NTADMM / 32) red[NTADMM / 32 + lane] = x;  // inclusive warp prefixes
+    }
+    __syncthreads();
+    if (wid > 0) css += red[NTADMM / 32 + wid - 1];
+    // largest qualifying position (kernel_estimator.cpp:118-124)
+    const double cand = (1.0 - css) / static_cast<double>(t + 1);
+    const int q = (t < m && val + cand > 0.0) ? t : -1;
+    const int wq = __reduce_max_sync(0xffffffffu, q);
+    __syncthreads();  // red is reused
+    if (lane == 0) ired[wid] = wq;
+    __syncthreads();
+    int rho = -1;
+    for (int w = 0; w < NTADMM / 32; ++w) rho = max(rho, ired[w]);
+    if (t == rho) red[0] = cand;
+    __syncthreads();
+    const double tau = red[0];
+    if (rho >= 0)
+        for (int i = t; i < m; i += NTADMM) out[i] = fmax(v[i] + tau, 0.0);
+    __syncthreads();
+    return rho + 1;
+}
+
 size_t admm_smem_doubles(int n, int cs = 1) {
     const size_t m = static_cast<size_t>(n) * n, rp = (m + cs - 1) / cs;
-    return static_cast<size_t>(17 + 3 + 6 + 6 + 6) * m + 2 * n + NTADMM + NTADMM / 2 + 4 + 8 +
+    return static_cast<size_t>(17 + 3 + 6 + 6) * m + std::max<size_t>(6 * m, 3 * NTADMM) + 2 * n + NTADMM +
+           NTADMM / 2 + 4 + 8 +
            (cs > 1 ? rp * m + 2 * rp : 0);
 }
 
@@ -825,7 +901,7 @@ __global__ void __launch_bounds__(NTADMM) k_admm(AdmmArgs A, const double* __res
     S.bz = p; p += m;
     S.zz = p; p += m;
     S.unew = p; p += m;
-    S.tmp6 = p; p += 6 * m;
+    S.tmp6 = p; p += (6 * m > 3 * NTADMM ? 6 * m : 3 * NTADMM);  // projection scratch
     S.spec = p; p += 6 * m;
     S.rowt = p; p += 6 * m;
     S.twc = p; p += n;
@@ -944,7 +1020,8 @@ __global__ void __launch_bounds__(NTADMM) k_admm(AdmmArgs A, const double* __res
             bool finite = true;
             for (int i = threadIdx.x; i < m; i += blockDim.x) finite = finite && isfinite(S.zz[i]);
             if (!__syncthreads_and(finite)) { status = 3; iters = t; break; }
-            const int support = project_simplex_block(S.zz, F[F_Z], m, S.red, ired);
+            const int support = m <= NTADMM ? project_simplex_sorted(S.zz, F[F_Z], m, S.red, ired, S.tmp6)
+                                             : project_simplex_block(S.zz, F[F_Z], m, S.red, ired);
             if (support == 0) { status = 3; iters = t; break; }
             if (t == A.hook_t) { status = 4; break; }
         }
@@ -1064,9 +1141,11 @@ __global__ void __launch_bounds__(NTADMM) k_project(const double* __restrict__ v
     double* os = sh + m;
     double* red = os + m;
     int* ired = reinterpret_cast<int*>(red + NTADMM);
+    double* scratch = red + NTADMM + NTADMM / 2 + 4;
     for (int i = threadIdx.x; i < m; i += blockDim.x) vs[i] = v[i];
     __syncthreads();
-    const int support = project_simplex_block(vs, os, m, red, ired);
+    const int support = m <= NTADMM ? project_simplex_sorted(vs, os, m, red, ired, scratch)
+                                    : project_simplex_block(vs, os, m, red, ired);
     if (threadIdx.x == 0) *status = support == 0;
     for (int i = threadIdx.x; i < m; i += blockDim.x) out[i] = os[i];
 }
@@ -1276,7 +1355,7 @@ void shrink2_device(Context& ctx, double* d_cols, int ncols, long long m, double
 }
 
 void project_simplex_device(Context& ctx, const double* d_v, int m, double* d_out, int* d_status) {
-    const size_t sm = (2 * static_cast<size_t>(m) + 2 * NTADMM) * sizeof(double);
+    const size_t sm = (2 * static_cast<size_t>(m) + 4 * NTADMM + NTADMM / 2 + 4) * sizeof(double);
     if (sm > 227 * 1024) param_error("project_simplex: vector too long for the device projection");
     set_smem(k_project, sm);
     k_project<<<1, NTADMM, sm, ctx.stream>>>(d_v, m, d_out, d_status);

@@ -934,24 +934,29 @@ __global__ void __launch_bounds__(NTADMM) k_admm(AdmmArgs A, const double* __res
     if (CS > 1)
         for (size_t e = threadIdx.x; e < static_cast<size_t>(r_hi - r_lo) * m; e += blockDim.x)
             Gs[e] = __ldg(Ginv + static_cast<size_t>(r_lo) * m + e);
-    double** F = S.f;
+    // field f lives at smem + f m, except u, which alternates with u_new (pointer swap); no
+    // pointer array, so nothing is indexed dynamically through local memory
+    double* const fb = smem;
+    double* Ucur = fb + F_U * m;
+    double* Unew = S.unew;
+#define FLD(f) ((f) == F_U ? Ucur : fb + (f) * m)
     if (A.init_state) {  // kernel_estimator.cpp:297-307
         const int cc = (n - 1) / 2;
         for (int i = threadIdx.x; i < m; i += blockDim.x) {
             const double u0 = A.init_kind == 0 ? (i == cc * n + cc ? 1.0 : 0.0) : 1.0 / (static_cast<double>(n) * n);
-            F[F_U][i] = u0;
-            F[F_Z][i] = u0;
+            FLD(F_U)[i] = u0;
+            FLD(F_Z)[i] = u0;
             for (int f = F_P1; f <= F_L3; ++f)
-                if (f != F_Z) F[f][i] = 0.0;
+                if (f != F_Z) FLD(f)[i] = 0.0;
         }
         __syncthreads();
         for (int i = threadIdx.x; i < m; i += blockDim.x) {
             const int r = i / n, c = i - r * n;
-            F[F_X0][i] = F[F_U][r * n + (c + 1) % n] - F[F_U][i];
-            F[F_X1][i] = F[F_U][((r + 1) % n) * n + c] - F[F_U][i];
+            FLD(F_X0)[i] = FLD(F_U)[r * n + (c + 1) % n] - FLD(F_U)[i];
+            FLD(F_X1)[i] = FLD(F_U)[((r + 1) % n) * n + c] - FLD(F_U)[i];
         }
     } else {
-        for (int e = threadIdx.x; e < 17 * m; e += blockDim.x) F[e / m][e % m] = gstate[e];
+        for (int e = threadIdx.x; e < 17 * m; e += blockDim.x) FLD(e / m)[e % m] = gstate[e];
     }
     __syncthreads();
     const double a1m1 = A.alpha1 * A.mu1, a2m2 = A.alpha2 * A.mu2;
@@ -964,27 +969,27 @@ __global__ void __launch_bounds__(NTADMM) k_admm(AdmmArgs A, const double* __res
             for (int i = threadIdx.x; i < m; i += blockDim.x) {
                 const int r = i / n, c = i - r * n;
                 const int ir = r * n + (c + 1) % n, id = ((r + 1) % n) * n + c;
-                const double* u = F[F_U];
-                const double* p1 = F[F_P1];
-                const double* p2 = F[F_P2];
-                double a0 = ((u[ir] - u[i]) - p1[i]) + F[F_L10][i];
-                double a1 = ((u[id] - u[i]) - p2[i]) + F[F_L11][i];
+                const double* u = FLD(F_U);
+                const double* p1 = FLD(F_P1);
+                const double* p2 = FLD(F_P2);
+                double a0 = ((u[ir] - u[i]) - p1[i]) + FLD(F_L10)[i];
+                double a1 = ((u[id] - u[i]) - p2[i]) + FLD(F_L11)[i];
                 const double nrm = sqrt(a0 * a0 + a1 * a1);
                 const double sc = nrm > t1 ? (nrm - t1) / nrm : 0.0;
-                F[F_X0][i] = a0 * sc;
-                F[F_X1][i] = a1 * sc;
+                FLD(F_X0)[i] = a0 * sc;
+                FLD(F_X1)[i] = a1 * sc;
                 const double e0 = p1[ir] - p1[i];
                 const double cr = ((p1[id] - p1[i]) + (p2[ir] - p2[i])) * 0.5;
                 const double e3 = p2[id] - p2[i];
-                const double b0 = e0 + F[F_L20][i], b1 = cr + F[F_L21][i], b2 = cr + F[F_L22][i],
-                             b3 = e3 + F[F_L23][i];
+                const double b0 = e0 + FLD(F_L20)[i], b1 = cr + FLD(F_L21)[i], b2 = cr + FLD(F_L22)[i],
+                             b3 = e3 + FLD(F_L23)[i];
                 const double nrm2 = sqrt(b0 * b0 + b1 * b1 + b2 * b2 + b3 * b3);
                 const double sc2 = nrm2 > t2 ? (nrm2 - t2) / nrm2 : 0.0;
-                F[F_Y0][i] = b0 * sc2;
-                F[F_Y1][i] = b1 * sc2;
-                F[F_Y2][i] = b2 * sc2;
-                F[F_Y3][i] = b3 * sc2;
-                S.bz[i] = Etf[i] + A.mu3 * (u[i] + F[F_L3][i]);
+                FLD(F_Y0)[i] = b0 * sc2;
+                FLD(F_Y1)[i] = b1 * sc2;
+                FLD(F_Y2)[i] = b2 * sc2;
+                FLD(F_Y3)[i] = b3 * sc2;
+                S.bz[i] = Etf[i] + A.mu3 * (u[i] + FLD(F_L3)[i]);
             }
             __syncthreads();
             // z = project_simplex((E^T E + mu3 I)^-1 (E^T f + mu3 (u + L3)))   (:341, :79-83)
@@ -1020,51 +1025,51 @@ __global__ void __launch_bounds__(NTADMM) k_admm(AdmmArgs A, const double* __res
             bool finite = true;
             for (int i = threadIdx.x; i < m; i += blockDim.x) finite = finite && isfinite(S.zz[i]);
             if (!__syncthreads_and(finite)) { status = 3; iters = t; break; }
-            const int support = m <= NTADMM ? project_simplex_sorted(S.zz, F[F_Z], m, S.red, ired, S.tmp6)
-                                             : project_simplex_block(S.zz, F[F_Z], m, S.red, ired);
+            const int support = m <= NTADMM ? project_simplex_sorted(S.zz, FLD(F_Z), m, S.red, ired, S.tmp6)
+                                             : project_simplex_block(S.zz, FLD(F_Z), m, S.red, ired);
             if (support == 0) { status = 3; iters = t; break; }
             if (t == A.hook_t) { status = 4; break; }
         }
         phase = 0;
         // {u,p}-step with the mu3 tie to z - L3 (:349-355)
-        for (int i = threadIdx.x; i < m; i += blockDim.x) S.bz[i] = F[F_Z][i] - F[F_L3][i];
+        for (int i = threadIdx.x; i < m; i += blockDim.x) S.bz[i] = FLD(F_Z)[i] - FLD(F_L3)[i];
         __syncthreads();
         // old p1, p2 are dead after the y-step: the solve writes them in place, u_new separately
-        up_solve(S, n, a1m1, a2m2, A.coupling, F[F_X0], F[F_X1], F[F_Y0], F[F_Y1], F[F_Y2], F[F_Y3], F[F_L10],
-                 F[F_L11], F[F_L20], F[F_L21], F[F_L22], F[F_L23], S.bz, S.unew, F[F_P1], F[F_P2]);
+        up_solve(S, n, a1m1, a2m2, A.coupling, FLD(F_X0), FLD(F_X1), FLD(F_Y0), FLD(F_Y1), FLD(F_Y2), FLD(F_Y3), FLD(F_L10),
+                 FLD(F_L11), FLD(F_L20), FLD(F_L21), FLD(F_L22), FLD(F_L23), S.bz, Unew, FLD(F_P1), FLD(F_P2));
         // multipliers (:367-373), change of u (:375-376)
         double dd = 0.0, un = 0.0;
         bool fin_u = true, fin_z = true;
         for (int i = threadIdx.x; i < m; i += blockDim.x) {
             const int r = i / n, c = i - r * n;
             const int ir = r * n + (c + 1) % n, id = ((r + 1) % n) * n + c;
-            const double* u1 = S.unew;
-            const double* p1 = F[F_P1];
-            const double* p2 = F[F_P2];
-            F[F_L10][i] += (((u1[ir] - u1[i]) - p1[i]) - F[F_X0][i]) * A.rho;
-            F[F_L11][i] += (((u1[id] - u1[i]) - p2[i]) - F[F_X1][i]) * A.rho;
+            const double* u1 = Unew;
+            const double* p1 = FLD(F_P1);
+            const double* p2 = FLD(F_P2);
+            FLD(F_L10)[i] += (((u1[ir] - u1[i]) - p1[i]) - FLD(F_X0)[i]) * A.rho;
+            FLD(F_L11)[i] += (((u1[id] - u1[i]) - p2[i]) - FLD(F_X1)[i]) * A.rho;
             const double e0 = p1[ir] - p1[i];
             const double cr = ((p1[id] - p1[i]) + (p2[ir] - p2[i])) * 0.5;
             const double e3 = p2[id] - p2[i];
-            F[F_L20][i] += (e0 - F[F_Y0][i]) * A.rho;
-            F[F_L21][i] += (cr - F[F_Y1][i]) * A.rho;
-            F[F_L22][i] += (cr - F[F_Y2][i]) * A.rho;
-            F[F_L23][i] += (e3 - F[F_Y3][i]) * A.rho;
-            F[F_L3][i] += (u1[i] - F[F_Z][i]) * A.rho;
-            const double du = F[F_U][i] - u1[i];
+            FLD(F_L20)[i] += (e0 - FLD(F_Y0)[i]) * A.rho;
+            FLD(F_L21)[i] += (cr - FLD(F_Y1)[i]) * A.rho;
+            FLD(F_L22)[i] += (cr - FLD(F_Y2)[i]) * A.rho;
+            FLD(F_L23)[i] += (e3 - FLD(F_Y3)[i]) * A.rho;
+            FLD(F_L3)[i] += (u1[i] - FLD(F_Z)[i]) * A.rho;
+            const double du = FLD(F_U)[i] - u1[i];
             dd += du * du;
             un += u1[i] * u1[i];
             fin_u = fin_u && isfinite(u1[i]);
-            fin_z = fin_z && isfinite(F[F_Z][i]);
+            fin_z = fin_z && isfinite(FLD(F_Z)[i]);
         }
         const double delta = sqrt(admm_sum(dd, S.red));
         const double scale = fmax(sqrt(admm_sum(un, S.red)), 1e-300);
         const bool all_u = __syncthreads_and(fin_u);
         const bool all_z = __syncthreads_and(fin_z);
         {  // u <- u_new by swapping the buffers (all threads hold the same pointers)
-            double* tmp = F[F_U];
-            F[F_U] = S.unew;
-            S.unew = tmp;
+            double* tmp = Ucur;
+            Ucur = Unew;
+            Unew = tmp;
         }
         iters = t + 1;
         if (!all_u) { status = 1; break; }  // check_finite (:379-380)
@@ -1072,9 +1077,9 @@ __global__ void __launch_bounds__(NTADMM) k_admm(AdmmArgs A, const double* __res
         if (delta / scale < A.th) { ++t; break; }
     }
     if (crank == 0) {
-        for (int e = threadIdx.x; e < 17 * m; e += blockDim.x) gstate[e] = F[e / m][e % m];
+        for (int e = threadIdx.x; e < 17 * m; e += blockDim.x) gstate[e] = FLD(e / m)[e % m];
         if (k_out)
-            for (int i = threadIdx.x; i < m; i += blockDim.x) k_out[static_cast<size_t>(s) * m + i] = F[F_Z][i];
+            for (int i = threadIdx.x; i < m; i += blockDim.x) k_out[static_cast<size_t>(s) * m + i] = FLD(F_Z)[i];
         if (threadIdx.x == 0) {
             info[0] = iters;
             info[1] = status;
@@ -1083,6 +1088,7 @@ __global__ void __launch_bounds__(NTADMM) k_admm(AdmmArgs A, const double* __res
         }
     }
     if (CS > 1) cg::this_cluster().sync();  // no CTA leaves while a peer may still read its slice
+#undef FLD
 }
 
 // standalone {u,p} solve for the public solve_up (kernel_estimator.cpp:237-241)

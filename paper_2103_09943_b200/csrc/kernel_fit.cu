@@ -505,9 +505,15 @@ struct AdmmArgs {
     double alpha1, alpha2, mu1, mu2, mu3, rho, th, coupling;
     int t_max, t_begin, phase_begin, hook_t, init_kind, init_state;
     int cache_symbols;  // 1: per-frequency {u,p} symbols cached in shared memory
+    int ginv_global;    // 1: the cluster's mat-vec rows are read from the inverse in global memory
+                        //    (L2-resident) instead of a shared-memory slice (large kernels)
 };
 
 constexpr int NTADMM = 512;
+// projection scratch of the sorted (m <= NTADMM) projection; none for the rank-based one
+__host__ __device__ constexpr int admm_scratch_doubles(int m) {
+    return m <= NTADMM ? (6 * m > 3 * NTADMM ? 6 * m : 3 * NTADMM) : 0;
+}
 enum { F_U = 0, F_P1, F_P2, F_X0, F_X1, F_Y0, F_Y1, F_Y2, F_Y3, F_Z, F_L10, F_L11, F_L20, F_L21, F_L22, F_L23, F_L3 };
 
 struct AdmmSmem {
@@ -872,11 +878,10 @@ __device__ int project_simplex_sorted(const double* v, double* out, int m, doubl
     return rho + 1;
 }
 
-size_t admm_smem_doubles(int n, int cs = 1) {
+size_t admm_smem_doubles(int n, int cs = 1, bool ginv_global = false) {
     const size_t m = static_cast<size_t>(n) * n, rp = (m + cs - 1) / cs;
-    return static_cast<size_t>(17 + 3 + 6 + 6) * m + std::max<size_t>(6 * m, 3 * NTADMM) + 2 * n + NTADMM +
-           NTADMM / 2 + 4 + 8 +
-           (cs > 1 ? rp * m + 2 * rp : 0);
+    return static_cast<size_t>(17 + 3 + 6 + 6) * m + admm_scratch_doubles(static_cast<int>(m)) + 2 * n + NTADMM +
+           NTADMM / 2 + 4 + 8 + (cs > 1 ? (ginv_global ? 0 : rp * m) + 2 * rp : 0);
 }
 
 // CS > 1: the CTAs of a thread-block cluster run the same (deterministic, bit-identical) ADMM
@@ -901,7 +906,7 @@ __global__ void __launch_bounds__(NTADMM) k_admm(AdmmArgs A, const double* __res
     S.bz = p; p += m;
     S.zz = p; p += m;
     S.unew = p; p += m;
-    S.tmp6 = p; p += (6 * m > 3 * NTADMM ? 6 * m : 3 * NTADMM);  // projection scratch
+    S.tmp6 = p; p += admm_scratch_doubles(m);  // projection scratch (sorted projection only)
     S.spec = p; p += 6 * m;
     S.rowt = p; p += 6 * m;
     S.twc = p; p += n;
@@ -909,8 +914,9 @@ __global__ void __launch_bounds__(NTADMM) k_admm(AdmmArgs A, const double* __res
     S.red = p; p += NTADMM;
     int* ired = reinterpret_cast<int*>(p);
     p += NTADMM / 2 + 4;
-    double* Gs = p;          // CS > 1: rows [r_lo, r_hi) of the inverse
-    p += (CS > 1) ? static_cast<size_t>(RP) * m : 0;
+    const bool gglob = A.ginv_global != 0;
+    double* Gs = p;          // CS > 1: rows [r_lo, r_hi) of the inverse (unless gglob)
+    p += (CS > 1 && !gglob) ? static_cast<size_t>(RP) * m : 0;
     double* zsl = p;         // CS > 1: 2 x RP mat-vec slice (double-buffered by iteration parity)
     p += (CS > 1) ? 2 * RP : 0;
     for (int k = threadIdx.x; k < n; k += blockDim.x) {
@@ -931,7 +937,7 @@ __global__ void __launch_bounds__(NTADMM) k_admm(AdmmArgs A, const double* __res
         const double tol = 1e-12 * block_max(dmax, S.red);
         if (threadIdx.x == 0) S.sym[11 * m] = tol;
     }
-    if (CS > 1)
+    if (CS > 1 && !gglob)
         for (size_t e = threadIdx.x; e < static_cast<size_t>(r_hi - r_lo) * m; e += blockDim.x)
             Gs[e] = __ldg(Ginv + static_cast<size_t>(r_lo) * m + e);
     // field f lives at smem + f m, except u, which alternates with u_new (pointer swap); no
@@ -997,9 +1003,14 @@ __global__ void __launch_bounds__(NTADMM) k_admm(AdmmArgs A, const double* __res
                 double* mine = zsl + (t & 1) * RP;
                 const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
                 for (int i = r_lo + warp; i < r_hi; i += NTADMM / 32) {
-                    const double* row = Gs + static_cast<size_t>(i - r_lo) * m;
                     double acc = 0.0;
-                    for (int j = lane; j < m; j += 32) acc = fma(row[j], S.bz[j], acc);
+                    if (gglob) {
+                        const double* row = Ginv + static_cast<size_t>(i) * m;
+                        for (int j = lane; j < m; j += 32) acc = fma(__ldg(row + j), S.bz[j], acc);
+                    } else {
+                        const double* row = Gs + static_cast<size_t>(i - r_lo) * m;
+                        for (int j = lane; j < m; j += 32) acc = fma(row[j], S.bz[j], acc);
+                    }
                     acc = warp_sum(acc);
                     if (lane == 0) mine[i - r_lo] = acc;
                 }
@@ -1309,11 +1320,18 @@ void admm_device(Context& ctx, const ObsSystem& sys, const fbmp_ke_params& prm, 
     int cs = 1;
     const char* env = std::getenv("FBMP_ADMM_CLUSTER");
     const int cs_max = env ? std::max(1, std::atoi(env)) : 16;
-    if (sys.n2 >= 100)
+    bool gglob = false;
+    if (sys.n2 >= 100) {
         for (int c = 2; c <= cs_max; c *= 2)
             if (admm_smem_doubles(sys.n, c) * sizeof(double) <= 220 * 1024) { cs = c; break; }
-    size_t sm = admm_smem_doubles(sys.n, cs) * sizeof(double);
-    if (sm > 227 * 1024) param_error("kernel estimation: kernel side too large for the device ADMM (n <= 25)");
+        if (cs == 1 && cs_max >= 8) {  // the inverse slice does not fit: read its rows from L2
+            gglob = true;
+            cs = 8;
+        }
+    }
+    A.ginv_global = gglob ? 1 : 0;
+    size_t sm = admm_smem_doubles(sys.n, cs, gglob) * sizeof(double);
+    if (sm > 227 * 1024) param_error("kernel estimation: kernel side too large for the device ADMM (n <= 29)");
     const size_t sym_bytes = (11 * static_cast<size_t>(sys.n2) + 2) * sizeof(double);
     A.cache_symbols = sm + sym_bytes <= 225 * 1024 ? 1 : 0;
     if (A.cache_symbols) sm += sym_bytes;

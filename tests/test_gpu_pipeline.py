@@ -116,8 +116,10 @@ def test_pansharpen_validation(gpu):  # tests/test_pansharpen.cpp:405-415
         gpu.pansharpen(sc.lrms, sc.pan, k, 4, gpu.PansharpenParams(radius=0))
 
 
-@pytest.mark.parametrize("H,n", [(32, 5), (64, 7), (128, 15), (256, 15)])
+@pytest.mark.parametrize("H,n", [(32, 5), (64, 7), (128, 15), (256, 15), (256, 21), (256, 29)])
 def test_kernel_fit_matches_oracle(gpu, orc, H, n):
+    """n = 29 is the reference's default kernel side (KernelEstParams, kernel_estimator.hpp:18-31):
+    the device ADMM then reads the inverse rows from L2 instead of a shared-memory slice."""
     sc = synth.make_scene("C1", hr=H)
     om = orc.solve_weights(sc.lrms, sc.pan, 4, 10.0, 4)
     obs = orc.combine_bands(sc.lrms, om)

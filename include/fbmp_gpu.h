@@ -149,6 +149,12 @@ int fbmp_gpu_blind_batch(fbmp_gpu_ctx* ctx, const double* lrms, int S, int N, in
                          const fbmp_sw_params* sw, const fbmp_ke_params* ke, const fbmp_ps_params* ps,
                          double* out, double* k_out);
 
+/* Device-resident general form: S scenes (all bands; d_out S*N*H*W, d_k_out S*n*n), or one scene
+ * (S = 1) with the channel subset [ch0, ch0+nch) (nch = -1: all bands; d_out nch*H*W). */
+int fbmp_gpu_blind_batch_dev(fbmp_gpu_ctx* ctx, const double* d_lrms, int S, int N, int h, int w,
+                             const double* d_pan, const fbmp_sw_params* sw, const fbmp_ke_params* ke,
+                             const fbmp_ps_params* ps, int ch0, int nch, double* d_out, double* d_k_out);
+
 /* ---- unit-level entry points (parity tests) -------------------------------------------- */
 
 /* apply_prior / apply_prior_adjoint (pansharpen.hpp:28-29): circular 5-point Laplacian. */

@@ -636,6 +636,20 @@ int fbmp_gpu_blind_dev(fbmp_gpu_ctx* ctx, const double* d_lrms, int N, int h, in
     });
 }
 
+int fbmp_gpu_blind_batch_dev(fbmp_gpu_ctx* ctx, const double* d_lrms, int S, int N, int h, int w,
+                             const double* d_pan, const fbmp_sw_params* sw, const fbmp_ke_params* ke,
+                             const fbmp_ps_params* ps, int ch0, int nch, double* d_out, double* d_k_out) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        if (S < 1) param_error("blind: scene count must be >= 1");
+        if (nch >= 0 && (S != 1 || ch0 < 0 || nch < 1 || ch0 + nch > N)) param_error("blind: invalid channel subset");
+        std::vector<int> ai, ci;
+        blind_device(C, d_lrms, S, N, h, w, d_pan, sw_or_default(sw), ke_or_default(ke), ps_or_default(ps), d_out,
+                     d_k_out, nullptr, ai, ci, nch >= 0 ? ch0 : 0, nch);
+    });
+}
+
 int fbmp_gpu_blind(fbmp_gpu_ctx* ctx, const double* lrms, int N, int h, int w, const double* pan,
                    const fbmp_sw_params* sw, const fbmp_ke_params* ke, const fbmp_ps_params* ps, double* out,
                    double* k_out, double* omega_out) {

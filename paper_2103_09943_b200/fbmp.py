@@ -553,6 +553,20 @@ def blind_batch(lrms, pan, factor, n, sw=None, ke=None, ps=None, ctx=None):
     return out, k
 
 
+def blind_batch_dev(d_lrms: int, S: int, N: int, h: int, w: int, d_pan: int, d_out: int, d_k: int, factor: int,
+                    n: int, ctx: Context, ch0: int = 0, nch: int = -1, sw=None, ke=None, ps=None):
+    """Device-resident batch / channel-subset blind solve (raw device pointers)."""
+    sw = sw or SpectralWeightConfig(l=4, lambda_omega=10.0, factor=factor)
+    sw.factor = factor
+    ke = ke or KernelEstParams(n=n)
+    ke.n = n
+    ps = ps or PansharpenParams()
+    c1, c2, c3 = sw.c(), ke.c(), ps.c()
+    _check(_lib.fbmp_gpu_blind_batch_dev(ctx.h, C.cast(C.c_void_p(d_lrms), D), S, N, h, w,
+                                         C.cast(C.c_void_p(d_pan), D), C.byref(c1), C.byref(c2), C.byref(c3), ch0,
+                                         nch, C.cast(C.c_void_p(d_out), D), C.cast(C.c_void_p(d_k), D)))
+
+
 def blind_dev(d_lrms: int, N: int, h: int, w: int, d_pan: int, d_out: int, d_k: int, factor: int, n: int,
               ctx: Context, sw=None, ke=None, ps=None):
     """Device-resident blind solve: all arguments are raw device pointers (e.g. tensor.data_ptr())."""
@@ -571,6 +585,7 @@ EXPORTED_SYMBOLS = (
     "fbmp_gpu_default_ps_params", "fbmp_gpu_default_ke_params", "fbmp_gpu_default_sw_params",
     "fbmp_gpu_ctx_create", "fbmp_gpu_ctx_destroy", "fbmp_gpu_last_error", "fbmp_gpu_ctx_stats",
     "fbmp_gpu_ctx_stream", "fbmp_gpu_ctx_launches", "fbmp_gpu_ctx_set_profile", "fbmp_gpu_ctx_kernel_profile",
+    "fbmp_gpu_blind_batch_dev",
     "fbmp_gpu_pansharpen", "fbmp_gpu_estimate_kernel_tgv",
     "fbmp_gpu_estimate_kernel_plane", "fbmp_gpu_solve_weights", "fbmp_gpu_combine_bands", "fbmp_gpu_blind",
     "fbmp_gpu_blind_dev", "fbmp_gpu_blind_batch", "fbmp_gpu_blind_subset", "fbmp_gpu_apply_prior", "fbmp_gpu_llp_apply",

@@ -104,8 +104,12 @@ def test_data_term(gpu, orc, H, W, n, c):
     assert rel(gpu.data_apply(p, k, c), expect) < 1e-13
 
 
-@pytest.mark.parametrize("H,W,n,c", [(8, 8, 3, 2), (64, 64, 15, 4), (48, 40, 7, 4)])
+@pytest.mark.parametrize("H,W,n,c", [(8, 8, 3, 2), (64, 64, 15, 4), (48, 40, 7, 4),
+                                     (65, 67, 3, 1), (96, 80, 5, 2), (128, 72, 11, 4), (128, 200, 21, 4),
+                                     (64, 112, 17, 4)])
 def test_cg_operator(gpu, orc, H, W, n, c):
+    """Covers every operator variant: single-column / column-pair K_L (odd / even W, partial
+    bands), register-tap and generic K_D, specialised and generic K_Q, c in {1, 2, 4}."""
     rng = np.random.default_rng(7 * H + n)
     guide = orc.laplacian(rng.uniform(0, 1, (H, W)))
     p = rng.uniform(-1, 1, (H, W))

@@ -34,7 +34,10 @@ def test_warmstart_cg_matches_oracle(gpu, orc, H, n):
     assert rel(zg, zo) < TOL
 
 
-@pytest.mark.parametrize("H,c,n", [(16, 2, 5), (64, 4, 7), (128, 4, 15)])
+@pytest.mark.parametrize("H,c,n", [(16, 2, 5), (64, 4, 7), (128, 4, 15),
+                                   (65, 1, 3),    # odd width: single-column K_L, generic K_Q / K_D (c = 1)
+                                   (96, 2, 5),    # c = 2 specialised K_Q, generic K_D
+                                   (128, 4, 11)])  # c = 4 with an unspecialised kernel side
 def test_warmstart_cg_converged_white_noise(gpu, orc, H, c, n):
     """White-noise PAN makes the CG trajectory chaotic: two valid CPU restatements (FFT vs
     direct convolution, CSR vs matrix-free matting) already differ by ~5e-5 at the default
@@ -208,3 +211,30 @@ def test_blind_batch_matches_scenes(gpu, orc):
         assert np.array_equal(out[i], single) and np.array_equal(ks[i], info["kernel"])
     ref, rinfo = orc.blind(scenes[0].lrms, scenes[0].pan, 4, 15, threads=4)
     assert rel(out[0], ref) < TOL and rel(ks[0], rinfo["kernel"]) < TOL
+
+
+def test_blind_batch_dev_equals_host_paths(gpu):
+    """The device-resident batch / channel-subset entry (bench.py's timed call) gives the same
+    bits as the host-pointer batch and subset calls."""
+    import torch
+
+    scenes = [synth.make_scene("C1", s) for s in range(2)]
+    lrms = np.stack([s.lrms for s in scenes])
+    pan = np.stack([s.pan for s in scenes])
+    ctx = gpu.default_context()
+    d_l, d_p = torch.from_numpy(lrms).cuda(), torch.from_numpy(pan).cuda()
+    d_o = torch.empty((2, 4, 256, 256), dtype=torch.float64, device="cuda")
+    d_k = torch.empty((2, 15, 15), dtype=torch.float64, device="cuda")
+    gpu.blind_batch_dev(d_l.data_ptr(), 2, 4, 64, 64, d_p.data_ptr(), d_o.data_ptr(), d_k.data_ptr(), 4, 15, ctx)
+    torch.cuda.synchronize()
+    out, ks = gpu.blind_batch(lrms, pan, 4, 15)
+    assert np.array_equal(d_o.cpu().numpy(), out) and np.array_equal(d_k.cpu().numpy(), ks)
+    d_s = torch.empty((2, 256, 256), dtype=torch.float64, device="cuda")
+    gpu.blind_batch_dev(d_l[1].data_ptr(), 1, 4, 64, 64, d_p[1].data_ptr(), d_s.data_ptr(), d_k.data_ptr(), 4, 15,
+                        ctx, ch0=1, nch=2)
+    torch.cuda.synchronize()
+    sub, _ = gpu.blind_subset(lrms[1], pan[1], 4, 15, 1, 2)
+    assert np.array_equal(d_s.cpu().numpy(), sub)
+    with pytest.raises(gpu.ParamError):
+        gpu.blind_batch_dev(d_l.data_ptr(), 2, 4, 64, 64, d_p.data_ptr(), d_o.data_ptr(), d_k.data_ptr(), 4, 15,
+                            ctx, ch0=0, nch=2)

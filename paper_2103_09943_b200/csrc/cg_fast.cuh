@@ -764,30 +764,47 @@ __global__ void __launch_bounds__(NT, 2) k_dterm(PsGeo G, const double* __restri
             }
         const int qoff = (r0 / CF + Ic0 - iq0 + D::DLO) * QS + (c0 / CF + Jc - jq0 + D::DLO);
         const int Cc = c0 + Jc * CF + pc;
-        int c = 0;
-        for (unsigned int m = active; m; m &= m - 1u, ++c) {
-            const int chl = ch_lo + __ffs(m) - 1;
-            const double* qb = sq + c * QSZ + qoff;
-            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        // two channels per pass: independent FMA chains interleave (each output keeps its own
+        // summation order)
+        unsigned int m = active;
+        for (int c = 0; m; c += 2) {
+            const int chA = ch_lo + __ffs(m) - 1;
+            m &= m - 1u;
+            const bool two = m != 0u;
+            const int chB = two ? ch_lo + __ffs(m) - 1 : chA;
+            if (two) m &= m - 1u;
+            const double* qa = sq + c * QSZ + qoff;
+            const double* qb2 = sq + (two ? c + 1 : c) * QSZ + qoff;
+            double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
 #pragma unroll
-            for (int m = 0; m < DM + 3; ++m) {
-                double qv[DM];
+            for (int mm = 0; mm < DM + 3; ++mm) {
+                double qv[2][DM];
 #pragma unroll
-                for (int b = 0; b < DM; ++b) qv[b] = qb[m * QS + b];
+                for (int b = 0; b < DM; ++b) {
+                    qv[0][b] = qa[mm * QS + b];
+                    qv[1][b] = qb2[mm * QS + b];
+                }
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    const int a = m - k;
+                    const int a = mm - k;
                     if (a >= 0 && a < DM) {
 #pragma unroll
-                        for (int b = 0; b < DM; ++b) acc[k] = fma(kreg[a][b], qv[b], acc[k]);
+                        for (int b = 0; b < DM; ++b) {
+                            acc[0][k] = fma(kreg[a][b], qv[0][b], acc[0][k]);
+                            acc[1][k] = fma(kreg[a][b], qv[1][b], acc[1][k]);
+                        }
                     }
                 }
             }
-            double* oc = out + (scene * G.cps + chl) * P;
+            double* oa = out + (scene * G.cps + chA) * P;
+            double* ob = out + (scene * G.cps + chB) * P;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int R = r0 + (Ic0 + k) * CF + pr;
-                if (R < H && Cc < W) oc[static_cast<size_t>(R) * W + Cc] = acc[k];
+                if (R < H && Cc < W) {
+                    oa[static_cast<size_t>(R) * W + Cc] = acc[0][k];
+                    if (two) ob[static_cast<size_t>(R) * W + Cc] = acc[1][k];
+                }
             }
         }
         return;

@@ -1064,6 +1064,15 @@ namespace kl {
 constexpr int BAND2 = 56;
 }
 __device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+    const unsigned int s = static_cast<unsigned int>(__cvta_generic_to_shared(sdst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
 
 template <bool CG>
 __global__ void __launch_bounds__(kl::NTL, 12) k_llp2(PsGeo G, const double* __restrict__ guide,
@@ -1085,6 +1094,8 @@ __global__ void __launch_bounds__(kl::NTL, 12) k_llp2(PsGeo G, const double* __r
     const int item = blockIdx.x;
     const int nrb = (H + RB - 1) / RB;
     const unsigned FULL = 0xffffffffu;
+    constexpr int NB = 4;                    // ring depth: rows in flight = NB - 1
+    __shared__ double2 ring[NB][5][32];      // p, I, mu, g, d rows of NB steps
     double dotp = 0.0;
     {
         const int band = item / kstrips, strip = item - band * kstrips;
@@ -1114,21 +1125,31 @@ __global__ void __launch_bounds__(kl::NTL, 12) k_llp2(PsGeo G, const double* __r
         double2 ha_a = {0, 0}, ha_b = {0, 0}, hc_a = {0, 0}, hc_b = {0, 0}, M_a = {0, 0}, M_b = {0, 0};
         const int steps = (r1 - r0) + 2 * HALO;
         int blk_left = RB;
-        // loads of the first step
-        double2 np0 = ldg2(pc + o0), ni1 = ldg2(I + o1), nm2 = ldg2(MU + o2), ng2 = ldg2(GK + o2);
-        double2 nd4 = *reinterpret_cast<const double2*>(oc + o4);
+        // the rows of step j stream into ring slot j % NB with cp.async, NB - 1 steps ahead of
+        // their use (each lane copies and later reads its own 16 bytes: no warp barrier)
+        int io0 = o0, io1 = o1, io2 = o2, io4 = o4;  // offsets of the next step to issue
+        auto issue = [&](int slot) {
+            cp_async16(&ring[slot][0][lane], pc + io0);
+            cp_async16(&ring[slot][1][lane], I + io1);
+            cp_async16(&ring[slot][2][lane], MU + io2);
+            cp_async16(&ring[slot][3][lane], GK + io2);
+            cp_async16(&ring[slot][4][lane], oc + io4);
+            io0 = adv(io0); io1 = adv(io1); io2 = adv(io2); io4 = adv(io4);
+        };
+#pragma unroll
+        for (int j = 0; j < NB - 1; ++j) {
+            if (j < steps) issue(j);
+            cp_async_commit();
+        }
         for (int st_i = 0; st_i < steps; ++st_i) {
-            const double2 p0 = np0, Im1 = ni1, mu2 = nm2, g2 = ng2, d4 = nd4;
-            o0 = adv(o0); o1 = adv(o1); o2 = adv(o2);
+            if (st_i + NB - 1 < steps) issue((st_i + NB - 1) % NB);
+            cp_async_commit();
+            cp_async_wait<NB - 1>();  // the group of step st_i has landed
+            const int slot = st_i % NB;
+            const double2 p0 = ring[slot][0][lane], Im1 = ring[slot][1][lane], mu2 = ring[slot][2][lane],
+                          g2 = ring[slot][3][lane], d4 = ring[slot][4][lane];
             const int o4c = o4;
             o4 = adv(o4);
-            if (st_i + 1 < steps) {
-                np0 = ldg2(pc + o0);
-                ni1 = ldg2(I + o1);
-                nm2 = ldg2(MU + o2);
-                ng2 = ldg2(GK + o2);
-                nd4 = *reinterpret_cast<const double2*>(oc + o4);
-            }
             // S1 at row Y-1 (ops.cpp:70-78 order: 4 c - up - down - left - right)
             const double pL = __shfl_up_sync(FULL, pm1.y, 1), pR = __shfl_down_sync(FULL, pm1.x, 1);
             double2 s1, is1;

@@ -15,6 +15,10 @@
 
 #include "pansharpen.cuh"
 
+#ifndef FBMP_KQ_KB
+#define FBMP_KQ_KB 4  // K_Q: CF-wide runs of r and p_old in flight per thread
+#endif
+
 namespace fbmp_gpu {
 namespace fast {
 
@@ -146,7 +150,7 @@ __global__ void __launch_bounds__(QGeo<N_, CF>::NTH, 3) k_q2(PsGeo G, const doub
     // stores are CF-wide vectors; each thread keeps KB runs of r and p_old in flight
     using VT = typename std::conditional<CF == 4, double4_t, typename std::conditional<CF == 2, double2, double>::type>::type;
     constexpr int RUNS = Q::SRH * Q::PW;
-    constexpr int KB = 4;
+    constexpr int KB = FBMP_KQ_KB;
     for (int e0 = 0; e0 < RUNS; e0 += NQ * KB) {
         VT vr[KB], vp[KB];
         size_t gi[KB];
@@ -1063,6 +1067,10 @@ __global__ void __launch_bounds__(kl::NTL, 16) k_llp(PsGeo G, const double* __re
 namespace kl {
 constexpr int BAND2 = 56;
 }
+#ifndef FBMP_KL_UNROLL
+#define FBMP_KL_UNROLL 3
+#endif
+constexpr int KL_UNROLL = FBMP_KL_UNROLL;
 __device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
     const unsigned int s = static_cast<unsigned int>(__cvta_generic_to_shared(sdst));
@@ -1141,7 +1149,8 @@ __global__ void __launch_bounds__(kl::NTL, 12) k_llp2(PsGeo G, const double* __r
             if (j < steps) issue(j);
             cp_async_commit();
         }
-        for (int st_i = 0; st_i < steps; ++st_i) {
+#pragma unroll KL_UNROLL
+        for (int st_i = 0; st_i < steps; ++st_i) {  // unrolled: the register windows rotate by renaming
             if (st_i + NB - 1 < steps) issue((st_i + NB - 1) % NB);
             cp_async_commit();
             cp_async_wait<NB - 1>();  // the group of step st_i has landed

@@ -353,42 +353,58 @@ constexpr int NBK = 32;
 
 // factor the panel A[K:N, K:K+nb] in shared memory (diagonal block + sub-panel solve)
 __global__ void __launch_bounds__(NT) k_potrf_panel(double* __restrict__ M, int N, int K, int* __restrict__ status) {
+    // panel columns [K, K+nb): the nb x nb diagonal block is factorised by warp 0 (lane i owns
+    // row i, one __syncwarp per column), the rows below by a row-parallel triangular solve
     extern __shared__ double pnl[];
+    constexpr int LD = NBK + 1;  // padded row stride
     const int s = blockIdx.x;
     if (status[s]) return;
     double* A = M + static_cast<size_t>(s) * N * N;
     const int nb = min(NBK, N - K), rows = N - K;
     for (int e = threadIdx.x; e < rows * nb; e += NT) {
         const int i = e / nb, j = e - i * nb;
-        pnl[e] = A[static_cast<size_t>(K + i) * N + K + j];
+        pnl[i * LD + j] = A[static_cast<size_t>(K + i) * N + K + j];
     }
     __shared__ int fail;
     if (threadIdx.x == 0) fail = 0;
     __syncthreads();
-    for (int k = 0; k < nb; ++k) {
-        if (threadIdx.x == 0) {
-            const double d = pnl[k * nb + k];
-            if (!(d > 0)) fail = 1;
-            pnl[k * nb + k] = sqrt(d);
+    if (threadIdx.x < 32) {
+        const int i = threadIdx.x;
+        for (int k = 0; k < nb; ++k) {
+            const double d = pnl[k * LD + k];
+            if (!(d > 0)) {
+                if (i == 0) fail = 1;
+                break;
+            }
+            const double l = sqrt(d);
+            __syncwarp();
+            if (i == k) pnl[k * LD + k] = l;
+            if (i > k && i < nb) pnl[i * LD + k] /= l;
+            __syncwarp();
+            if (i > k && i < nb) {
+                const double lik = pnl[i * LD + k];
+                for (int j = k + 1; j <= i; ++j) pnl[i * LD + j] -= lik * pnl[j * LD + k];
+            }
+            __syncwarp();
         }
-        __syncthreads();
-        if (fail) break;
-        const double l = pnl[k * nb + k];
-        for (int i = k + 1 + threadIdx.x; i < rows; i += NT) pnl[i * nb + k] /= l;
-        __syncthreads();
-        for (int e = threadIdx.x; e < (rows - k - 1) * (nb - k - 1); e += NT) {
-            const int i = k + 1 + e / (nb - k - 1), j = k + 1 + e % (nb - k - 1);
-            if (j <= i) pnl[i * nb + j] -= pnl[i * nb + k] * pnl[j * nb + k];
-        }
-        __syncthreads();
     }
+    __syncthreads();
     if (fail) {
         if (threadIdx.x == 0) status[s] = 1;
         return;
     }
+    for (int i = nb + threadIdx.x; i < rows; i += NT) {  // L21 = A21 L11^-T, row by row
+        double* row = pnl + i * LD;
+        for (int k = 0; k < nb; ++k) {
+            double v = row[k];
+            for (int j = 0; j < k; ++j) v -= row[j] * pnl[k * LD + j];
+            row[k] = v / pnl[k * LD + k];
+        }
+    }
+    __syncthreads();
     for (int e = threadIdx.x; e < rows * nb; e += NT) {
         const int i = e / nb, j = e - i * nb;
-        A[static_cast<size_t>(K + i) * N + K + j] = (i >= j) ? pnl[e] : 0.0;
+        A[static_cast<size_t>(K + i) * N + K + j] = (i >= j) ? pnl[i * LD + j] : 0.0;
     }
 }
 
@@ -1273,7 +1289,7 @@ void build_observation(Context& ctx, const double* d_pan, const double* d_obs, i
     ctx.count();
     FBMP_CUDA(cudaMemsetAsync(sys.status, 0, sizeof(int) * S, ctx.stream));
     const int N = n2;
-    const size_t smP = static_cast<size_t>(N) * NBK * sizeof(double);
+    const size_t smP = static_cast<size_t>(N) * (NBK + 1) * sizeof(double);
     if (smP > 227 * 1024) param_error("build_observation: kernel side too large for the device Cholesky");
     set_smem(k_potrf_panel, smP);
     for (int K = 0; K < N; K += NBK) {

@@ -16,7 +16,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libfbmp_gpu.so")
+LIB_PATH = os.environ.get("FBMP_GPU_LIB") or os.path.join(_HERE, "lib", "libfbmp_gpu.so")  # env: A/B experiments
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2103_09943_b200.build` (or "
                       "__graft_entry__.build()) first; there is no CPU fallback")

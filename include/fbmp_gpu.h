@@ -155,6 +155,20 @@ int fbmp_gpu_blind_batch_dev(fbmp_gpu_ctx* ctx, const double* d_lrms, int S, int
                              const double* d_pan, const fbmp_sw_params* sw, const fbmp_ke_params* ke,
                              const fbmp_ps_params* ps, int ch0, int nch, double* d_out, double* d_k_out);
 
+/* Row-strip (multi-GPU) blind solve of one scene (BASELINE config C5 on several GPUs).
+ * Inputs (full LRMS / PAN) are replicated on every rank; the spectral weights and the kernel fit
+ * run replicated, the CG runs on row strips with an r-halo exchange and two allreduces per
+ * iteration (NCCL), the post-processing per channel on rank (channel mod G). With a communicator
+ * (fbmp_gpu_ctx_set_comm) the strips are the ranks and vstrips is ignored; without one, vstrips
+ * virtual ranks run in this process. d_out (N*H*W) is complete on rank 0. */
+int fbmp_gpu_blind_strips_dev(fbmp_gpu_ctx* ctx, const double* d_lrms, int N, int h, int w, const double* d_pan,
+                              const fbmp_sw_params* sw, const fbmp_ke_params* ke, const fbmp_ps_params* ps,
+                              int vstrips, double* d_out, double* d_k_out);
+/* NCCL bootstrap: rank 0 creates the 128-byte id, the launcher broadcasts it, every rank calls
+ * set_comm (collective) on its context. */
+int fbmp_gpu_nccl_unique_id(unsigned char* id128);
+int fbmp_gpu_ctx_set_comm(fbmp_gpu_ctx* ctx, const unsigned char* id128, int nranks, int rank);
+
 /* ---- unit-level entry points (parity tests) -------------------------------------------- */
 
 /* apply_prior / apply_prior_adjoint (pansharpen.hpp:28-29): circular 5-point Laplacian. */

@@ -18,11 +18,19 @@ LIBDIR = os.path.join(HERE, "lib")
 BUILD = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CUDA_LIB = "/usr/local/cuda/lib64"
+# NCCL: the copy torch ships (same library in the process when torch.distributed is used)
+NCCL_DIR = os.path.join(os.path.dirname(os.path.dirname(os.__file__)), "site-packages", "nvidia", "nccl")
+if not os.path.isdir(NCCL_DIR):
+    import sysconfig
+    NCCL_DIR = os.path.join(sysconfig.get_paths()["purelib"], "nvidia", "nccl")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
-                  "-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "--expt-relaxed-constexpr"]
+                  "-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "--expt-relaxed-constexpr",
+                  "-I" + os.path.join(NCCL_DIR, "include")]
 CU_SOURCES = ["pansharpen.cu", "kernel_fit.cu", "capi.cu"]
 GPU_LIB = os.path.join(LIBDIR, "libfbmp_gpu.so")
+LINK = ["-L" + CUDA_LIB, "-lcufft", "-lcudart", "-Xlinker", "-rpath," + CUDA_LIB,
+        "-L" + os.path.join(NCCL_DIR, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath," + os.path.join(NCCL_DIR, "lib")]
 SHIM_LIB = os.path.join(LIBDIR, "libfbmp.so")
 
 
@@ -56,8 +64,7 @@ def build_gpu(force: bool = False, verbose: bool = False) -> str:
     with ThreadPoolExecutor(max_workers=len(jobs) or 1) as ex:
         list(ex.map(_run, jobs))
     if force or jobs or _stale(GPU_LIB, objs):
-        _run([NVCC] + ARCH + ["-shared", "-o", GPU_LIB] + objs +
-             ["-L" + CUDA_LIB, "-lcufft", "-lcudart", "-Xlinker", "-rpath," + CUDA_LIB])
+        _run([NVCC] + ARCH + ["-shared", "-o", GPU_LIB] + objs + LINK)
     return GPU_LIB
 
 

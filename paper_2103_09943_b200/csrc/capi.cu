@@ -1,6 +1,8 @@
 // capi.cu -- the C ABI (include/fbmp_gpu.h): context management and the reference-facing
 // entry points. Host-pointer calls upload, run the device path and download; there is no
 // CPU fallback anywhere in this library.
+#include <nccl.h>
+
 #include <cstring>
 #include <string>
 
@@ -24,6 +26,7 @@ Context::Context(int dev) : device(dev) {
 
 Context::~Context() {
     cudaSetDevice(device);
+    if (nccl) ncclCommDestroy(static_cast<ncclComm_t>(nccl));
     for (auto& kv : plans) cufftDestroy(kv.second);
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     for (auto& e : poll_ev)
@@ -149,12 +152,169 @@ void pansharpen_device(Context& ctx, const double* d_lrms, int S, int N, int h, 
                       "function too small)");
 }
 
+namespace {
+// dst[p][y][x] = src[p][(r0 + y) mod Hs][x] for y < Hd (row gather with periodic wrap)
+__global__ void k_copy_rows(const double* __restrict__ src, int Hs, int W, double* __restrict__ dst, int r0, int Hd,
+                            int planes) {
+    const long long n = static_cast<long long>(Hd) * W;
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < n * planes;
+         e += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long pl = e / n, rem = e - pl * n;
+        const int y = static_cast<int>(rem / W), x = static_cast<int>(rem - static_cast<long long>(y) * W);
+        int r = (r0 + y) % Hs;
+        if (r < 0) r += Hs;
+        dst[e] = src[(pl * Hs + r) * W + x];
+    }
+}
+void copy_rows(Context& ctx, const double* src, int Hs, int W, double* dst, int r0, int Hd, int planes) {
+    const long long n = static_cast<long long>(Hd) * W * planes;
+    const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 16LL * ctx.sm_count));
+    k_copy_rows<<<blocks, 256, 0, ctx.stream>>>(src, Hs, W, dst, r0, Hd, planes);
+    ctx.count();
+    check_launch();
+}
+}  // namespace
+
+// HRMS solve of one scene with the CG on row strips: inputs are replicated
+// on every rank; with a communicator, rank r owns rows [r H/G, (r+1) H/G); without one, `vstrips`
+// virtual ranks run in this process (device copies instead of NCCL -- the same data flow, used by
+// the tests on one GPU). The post-processing (guided filter + alias-group FFT solve) needs whole
+// planes: the owned rows of z0 are all-gathered per channel and channel c is finished on rank
+// c mod G; rank 0 then receives the other channels. d_out: N*H*W (complete on rank 0).
+void pansharpen_strips_device(Context& ctx, const double* d_lrms, int N, int h, int w, const double* d_pan,
+                              const double* d_taps, int n, int c, const fbmp_ps_params& prm, double* d_out,
+                              std::vector<int>& cg_iters, int vstrips) {
+    validate_ps(prm);
+    const int H = h * c, W = w * c;
+    if (2 * prm.radius + 1 > std::min(H, W)) dim_error("matting matrix: window larger than image");
+    check_kernel(n, H, W);
+    const bool dist = ctx.nccl != nullptr;
+    const int G = dist ? ctx.nranks : std::max(1, vstrips);
+    StripComm comm;
+    comm.nccl = ctx.nccl;
+    comm.nranks = G;
+    comm.rank = dist ? ctx.rank : 0;
+    const int halo = comm.halo;
+    if (H % G != 0 || (H / G) % std::max(c, 16) != 0 || H / G < halo)
+        param_error("strip solve: the PAN height must split into equal strips of >= 32 rows (multiples of 16 and c)");
+    const int hloc = H / G, Hp = hloc + 2 * halo;
+    const size_t P = static_cast<size_t>(H) * W, p = static_cast<size_t>(h) * w, Pp = static_cast<size_t>(Hp) * W;
+    // replicated setup: normalisation, L(pan_n), window statistics, scaled LRMS (whole image)
+    double* scale = ctx.scratch<double>("st_scale", 1);
+    double* lpan = ctx.scratch<double>("st_lpan", P);
+    double* xn = ctx.scratch<double>("st_xn", p * N);
+    peak_scale(ctx, d_pan, static_cast<long long>(P), d_lrms, static_cast<long long>(p) * N, 1, scale);
+    laplacian_scaled(ctx, d_pan, H, W, 1, scale, lpan);
+    scale_copy(ctx, d_lrms, static_cast<long long>(p) * N, scale, static_cast<long long>(p) * N, xn);
+    const PsGeo Gf = make_geo(N, h, w, c, n, prm.radius, prm.lambda, prm.eps, N);
+    double* wmu = ctx.scratch<double>("st_wmu", P);
+    double* wg = ctx.scratch<double>("st_wg", P);
+    guide_stats(ctx, Gf, lpan, wmu, wg);
+    const int first = dist ? ctx.rank : 0, count = dist ? 1 : G;
+    std::vector<StripCg> strips(count);
+    const size_t nbmax = (Pp / 256 + 64) * 2 + 4096;
+    for (int k = 0; k < count; ++k) {
+        const int s = first + k;
+        const int grow0 = s * hloc - halo;
+        const std::string tag = "st" + std::to_string(k) + "_";
+        StripCg& S = strips[k];
+        double* gs = ctx.scratch<double>(tag + "guide", Pp);
+        double* ms = ctx.scratch<double>(tag + "mu", Pp);
+        double* ks = ctx.scratch<double>(tag + "g", Pp);
+        double* xs = ctx.scratch<double>(tag + "x", static_cast<size_t>(Hp / c) * w * N);
+        copy_rows(ctx, lpan, H, W, gs, grow0, Hp, 1);
+        copy_rows(ctx, wmu, H, W, ms, grow0, Hp, 1);
+        copy_rows(ctx, wg, H, W, ks, grow0, Hp, 1);
+        copy_rows(ctx, xn, h, w, xs, grow0 / c, Hp / c, N);
+        S.G = make_geo(N, Hp / c, w, c, n, prm.radius, prm.lambda, prm.eps, N);
+        S.G.grow0 = grow0;
+        S.G.Hg = H;
+        S.G.rlo = halo;
+        S.G.rhi = halo + hloc;
+        S.dred = ctx.scratch<double>(tag + "red", 4 * static_cast<size_t>(N));
+        S.G.dred = S.dred;
+        S.taps = d_taps;
+        S.guide = gs;
+        S.wmu = ms;
+        S.wg = ks;
+        S.x = xs;
+        S.B.z = ctx.scratch<double>(tag + "z", Pp * N);
+        S.B.r = ctx.scratch<double>(tag + "r", Pp * N);
+        S.B.p = ctx.scratch<double>(tag + "p", 2 * Pp * N);
+        S.B.Ap = ctx.scratch<double>(tag + "ap", Pp * N);
+        S.B.q = ctx.scratch<double>(tag + "q", static_cast<size_t>(Hp / c) * w * N);
+        S.B.part = ctx.scratch<double>(tag + "part", 4 * nbmax * N);
+        S.B.st = ctx.scratch<CgState>(tag + "state", N);
+    }
+    std::vector<CgState> hs;
+    trace("strips: prologue");
+    cg_solve_strips(ctx, strips, comm, prm.cg_max_iter, prm.cg_tol, hs);
+    trace("strips: cg");
+    cg_iters.assign(N, 0);
+    for (int i = 0; i < N; ++i) cg_iters[i] = hs[i].iters;
+    for (int i = 0; i < N; ++i) {
+        const std::string tag = "channel " + std::to_string(i) + ": ";
+        if (hs[i].done == 2) num_error(tag + "warmstart: conjugate gradients hit a non-positive curvature direction");
+        if (hs[i].done == 3)
+            num_error(tag + "warmstart: conjugate gradients did not converge in " + std::to_string(prm.cg_max_iter) +
+                      " iterations");
+    }
+    // whole z0 planes: owned rows of every strip, in strip order
+    double* zf = ctx.scratch<double>("st_zfull", P * N);
+    if (dist) {
+        auto cm = static_cast<ncclComm_t>(ctx.nccl);
+        FBMP_NCCL(ncclGroupStart());
+        for (int ch = 0; ch < N; ++ch)
+            FBMP_NCCL(ncclAllGather(strips[0].B.z + ch * Pp + static_cast<size_t>(halo) * W, zf + ch * P,
+                                    static_cast<size_t>(hloc) * W, ncclDouble, cm, ctx.stream));
+        FBMP_NCCL(ncclGroupEnd());
+    } else {
+        for (int k = 0; k < count; ++k)
+            for (int ch = 0; ch < N; ++ch)
+                FBMP_CUDA(cudaMemcpyAsync(zf + ch * P + static_cast<size_t>(k) * hloc * W,
+                                          strips[k].B.z + ch * Pp + static_cast<size_t>(halo) * W,
+                                          static_cast<size_t>(hloc) * W * sizeof(double), cudaMemcpyDeviceToDevice,
+                                          ctx.stream));
+    }
+    // post-processing: all channels here (virtual ranks), or the channels c with c mod G == rank
+    double* v = ctx.scratch<double>("st_v", P * N);
+    int* flag = ctx.scratch<int>("st_flag", N);
+    FBMP_CUDA(cudaMemsetAsync(flag, 0, sizeof(int) * N, ctx.stream));
+    const PsGeo G1 = make_geo(1, h, w, c, n, prm.radius, prm.lambda, prm.eps, 1);
+    if (!dist) {
+        guided_filter(ctx, N, H, W, prm.radius, prm.eps, zf, 1, lpan, nullptr, nullptr, v, N);
+        solve_channel_fft(ctx, Gf, d_taps, xn, v, scale, d_out, flag);
+    } else {
+        for (int ch = ctx.rank; ch < N; ch += G) {
+            guided_filter(ctx, 1, H, W, prm.radius, prm.eps, zf + ch * P, 1, lpan, nullptr, nullptr, v + ch * P, 1);
+            solve_channel_fft(ctx, G1, d_taps, xn + ch * p, v + ch * P, scale, d_out + ch * P, flag + ch);
+        }
+        auto cm = static_cast<ncclComm_t>(ctx.nccl);  // channels to rank 0
+        FBMP_NCCL(ncclGroupStart());
+        for (int ch = 0; ch < N; ++ch) {
+            const int owner = ch % G;
+            if (owner == 0) continue;
+            if (ctx.rank == 0) FBMP_NCCL(ncclRecv(d_out + ch * P, P, ncclDouble, owner, cm, ctx.stream));
+            if (ctx.rank == owner) FBMP_NCCL(ncclSend(d_out + ch * P, P, ncclDouble, 0, cm, ctx.stream));
+        }
+        FBMP_NCCL(ncclGroupEnd());
+    }
+    std::vector<int> hf(N);
+    d2h(hf.data(), flag, sizeof(int) * N, ctx.stream);
+    FBMP_CUDA(cudaStreamSynchronize(ctx.stream));
+    for (int i = 0; i < N; ++i)
+        if (hf[i])
+            num_error("channel " + std::to_string(i) +
+                      ": solve_channel_fft: alias-group system condition number exceeds 1e14 (prior transfer "
+                      "function too small)");
+}
+
 // SPEC.md:584-591 blind composition for S scenes on device-resident data:
 // solve_weights (all bands) -> combine_bands -> estimate_kernel_tgv -> pansharpen.
 void blind_device(Context& ctx, const double* d_lrms, int S, int N, int h, int w, const double* d_pan,
                   const fbmp_sw_params& sw, const fbmp_ke_params& ke, const fbmp_ps_params& ps, double* d_out,
                   double* d_k, double* d_omega_out, std::vector<int>& admm_iters, std::vector<int>& cg_iters,
-                  int ch0 = 0, int nch = -1) {
+                  int ch0 = 0, int nch = -1, int strips = 0) {
     const int c = sw.factor;
     if (c < 1) param_error("solve_weights: factor must be >= 1");
     if (sw.l < 1) param_error("solve_weights: l must be >= 1");
@@ -184,7 +344,12 @@ void blind_device(Context& ctx, const double* d_lrms, int S, int N, int h, int w
     estimate_kernel_device(ctx, d_pan, obs, S, H, W, c, ke, d_k, admm_iters, nullptr, -1);
     cudaEventRecord(e2, ctx.stream);
     trace("blind: weights + kernel fit");
-    pansharpen_device(ctx, d_lrms, S, N, h, w, d_pan, d_k, ke.n, c, ps, d_out, cg_iters, ch0, nch);
+    if (strips > 0 || ctx.nccl) {
+        if (S != 1 || nch >= 0) param_error("strip solve: one scene, all bands");
+        pansharpen_strips_device(ctx, d_lrms, N, h, w, d_pan, d_k, ke.n, c, ps, d_out, cg_iters, strips);
+    } else {
+        pansharpen_device(ctx, d_lrms, S, N, h, w, d_pan, d_k, ke.n, c, ps, d_out, cg_iters, ch0, nch);
+    }
     cudaEventRecord(e3, ctx.stream);
     cudaEventSynchronize(e3);
     float a = 0, b = 0, d = 0;
@@ -647,6 +812,45 @@ int fbmp_gpu_blind_batch_dev(fbmp_gpu_ctx* ctx, const double* d_lrms, int S, int
         std::vector<int> ai, ci;
         blind_device(C, d_lrms, S, N, h, w, d_pan, sw_or_default(sw), ke_or_default(ke), ps_or_default(ps), d_out,
                      d_k_out, nullptr, ai, ci, nch >= 0 ? ch0 : 0, nch);
+    });
+}
+
+int fbmp_gpu_nccl_unique_id(unsigned char* id128) {
+    return guarded([&] {
+        ncclUniqueId id;
+        FBMP_NCCL(ncclGetUniqueId(&id));
+        std::memcpy(id128, id.internal, sizeof(id.internal));
+    });
+}
+
+int fbmp_gpu_ctx_set_comm(fbmp_gpu_ctx* ctx, const unsigned char* id128, int nranks, int rank) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        if (nranks < 1 || rank < 0 || rank >= nranks) param_error("set_comm: invalid rank / size");
+        if (C.nccl) {
+            ncclCommDestroy(static_cast<ncclComm_t>(C.nccl));
+            C.nccl = nullptr;
+        }
+        ncclUniqueId id;
+        std::memcpy(id.internal, id128, sizeof(id.internal));
+        ncclComm_t comm;
+        FBMP_NCCL(ncclCommInitRank(&comm, nranks, id, rank));
+        C.nccl = comm;
+        C.nranks = nranks;
+        C.rank = rank;
+    });
+}
+
+int fbmp_gpu_blind_strips_dev(fbmp_gpu_ctx* ctx, const double* d_lrms, int N, int h, int w, const double* d_pan,
+                              const fbmp_sw_params* sw, const fbmp_ke_params* ke, const fbmp_ps_params* ps,
+                              int vstrips, double* d_out, double* d_k_out) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        std::vector<int> ai, ci;
+        blind_device(C, d_lrms, 1, N, h, w, d_pan, sw_or_default(sw), ke_or_default(ke), ps_or_default(ps), d_out,
+                     d_k_out, nullptr, ai, ci, 0, -1, std::max(1, vstrips));
     });
 }
 

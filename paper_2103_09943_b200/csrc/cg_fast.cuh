@@ -178,8 +178,10 @@ __global__ void __launch_bounds__(QGeo<N_, CF>::NTH, 3) k_q2(PsGeo G, const doub
                 for (int u = 0; u < CF; ++u) v[u] = v[u] + o[u] * beta;  // pansharpen.cpp:254
                 if (rr >= own_r0 && rr < own_r1 && jc >= Q::g && jc < Q::g + Q::TW && R0 + rr < H && C0 + CF * jc < W) {
                     stv(pnew + gi[k], v);
+                    if (R0 + rr >= G.rlo && R0 + rr < G.rhi) {  // rows owned by this strip
 #pragma unroll
-                    for (int u = 0; u < CF; ++u) pp += v[u] * v[u];
+                        for (int u = 0; u < CF; ++u) pp += v[u] * v[u];
+                    }
                 }
             }
             double* pl = planes + ((rr % CF) * CF) * Q::PS + (rr / CF) * Q::PWS + jc;
@@ -235,7 +237,8 @@ __global__ void __launch_bounds__(QGeo<N_, CF>::NTH, 3) k_q2(PsGeo G, const doub
         if (elect_last_block(&st[ch].cnt_q, nblk)) {
             const double tot = sum_partials<NQ>(part + static_cast<size_t>(ch) * nblk, nblk, 1, red);
             if (threadIdx.x == 0) {
-                st[ch].pp = tot;
+                if (G.dred) G.dred[G.N + 3 * ch] = tot;
+                else st[ch].pp = tot;
                 st[ch].cnt_q = 0;
             }
         }
@@ -994,7 +997,8 @@ __global__ void __launch_bounds__(kl::NTL, 16) k_llp(PsGeo G, const double* __re
             // S3 at row Y-3: M s = n s - box(c1) - I box(a)
             const double ha2 = __shfl_up_sync(0xffffffffu, a2, 1) + a2 + __shfl_down_sync(0xffffffffu, a2, 1);
             const double hc2 = __shfl_up_sync(0xffffffffu, c2, 1) + c2 + __shfl_down_sync(0xffffffffu, c2, 1);
-            const int nrow = max(min(r3 + 1, H - 2) - max(r3 - 1, 1) + 1, 0);
+            const int g3 = wrap_once(r3 + G.grow0, G.Hg);  // global row (strip decomposition)
+            const int nrow = max(min(g3 + 1, G.Hg - 2) - max(g3 - 1, 1) + 1, 0);
             const double Mc = static_cast<double>(nrow * ncol) * s3 - (hc_a + hc_b + hc2) - Im3 * (ha_a + ha_b + ha2);
             // S5 at row Y-4: t = L (M s), out = d + lambda t
             const double Ml = __shfl_up_sync(0xffffffffu, M_b, 1), Mr = __shfl_down_sync(0xffffffffu, M_b, 1);
@@ -1003,7 +1007,8 @@ __global__ void __launch_bounds__(kl::NTL, 16) k_llp(PsGeo G, const double* __re
             if (st_i >= 2 * HALO) {
                 if (writer) {
                     oc[o4] = val;
-                    dotp += p4 * val;
+                    const int yo = r0 + st_i - 2 * HALO;
+                    if (yo >= G.rlo && yo < G.rhi) dotp += p4 * val;
                 }
                 if (CG && (--blk_left == 0 || st_i + 1 == steps)) {  // close the row block
                     const double ws = warp_sum(dotp);
@@ -1045,7 +1050,10 @@ __global__ void __launch_bounds__(kl::NTL, 16) k_llp(PsGeo G, const double* __re
 #pragma unroll 8
             for (int i = lane; i < nbands * nrb; i += 32) sacc += __ldcg(pa + i);
             const double pAp = warp_sum(sacc);
-            if (lane == 0) {
+            if (lane == 0 && G.dred) {  // distributed: publish the local sum only
+                G.dred[ch] = pAp;
+                st[ch].cnt_a = 0;
+            } else if (lane == 0) {
                 CgState& S = st[ch];
                 S.pAp = pAp;
                 if (!(pAp > 0)) {  // pansharpen.cpp:240-244
@@ -1187,7 +1195,8 @@ __global__ void __launch_bounds__(kl::NTL, 12) k_llp2(PsGeo G, const double* __r
             const double cL = __shfl_up_sync(FULL, c2.y, 1), cR = __shfl_down_sync(FULL, c2.x, 1);
             const double2 ha2 = make_double2(aL + a2.x + a2.y, a2.x + a2.y + aR);
             const double2 hc2 = make_double2(cL + c2.x + c2.y, c2.x + c2.y + cR);
-            const int nrow = max(min(r3 + 1, H - 2) - max(r3 - 1, 1) + 1, 0);
+            const int g3 = wrap_once(r3 + G.grow0, G.Hg);  // global row (strip decomposition)
+            const int nrow = max(min(g3 + 1, G.Hg - 2) - max(g3 - 1, 1) + 1, 0);
             double2 Mc;
             Mc.x = static_cast<double>(nrow * nc0) * s3.x - (hc_a.x + hc_b.x + hc2.x) - Im3.x * (ha_a.x + ha_b.x + ha2.x);
             Mc.y = static_cast<double>(nrow * nc1) * s3.y - (hc_a.y + hc_b.y + hc2.y) - Im3.y * (ha_a.y + ha_b.y + ha2.y);
@@ -1199,7 +1208,8 @@ __global__ void __launch_bounds__(kl::NTL, 12) k_llp2(PsGeo G, const double* __r
             if (st_i >= 2 * HALO) {
                 if (writer) {
                     *reinterpret_cast<double2*>(oc + o4c) = val;
-                    dotp += pm4.x * val.x + pm4.y * val.y;
+                    const int yo = r0 + st_i - 2 * HALO;
+                    if (yo >= G.rlo && yo < G.rhi) dotp += pm4.x * val.x + pm4.y * val.y;
                 }
                 if (CG && (--blk_left == 0 || st_i + 1 == steps)) {  // close the row block
                     const double ws = warp_sum(dotp);
@@ -1232,7 +1242,10 @@ __global__ void __launch_bounds__(kl::NTL, 12) k_llp2(PsGeo G, const double* __r
 #pragma unroll 8
             for (int i = lane; i < nbands * nrb; i += 32) sacc += __ldcg(pa + i);
             const double pAp = warp_sum(sacc);
-            if (lane == 0) {
+            if (lane == 0 && G.dred) {  // distributed: publish the local sum only
+                G.dred[ch] = pAp;
+                st[ch].cnt_a = 0;
+            } else if (lane == 0) {
                 CgState& S = st[ch];
                 S.pAp = pAp;
                 if (!(pAp > 0)) {  // pansharpen.cpp:240-244

@@ -32,6 +32,12 @@ struct Failure : std::runtime_error {
 [[noreturn]] inline void dim_error(const std::string& m) { throw Failure(FBMP_DIMENSION_ERROR, m); }
 [[noreturn]] inline void num_error(const std::string& m) { throw Failure(FBMP_NUMERICAL_ERROR, m); }
 
+#define FBMP_NCCL(call)                                                                          \
+    do {                                                                                         \
+        const int rc_ = static_cast<int>(call);                                                  \
+        if (rc_ != 0) throw ::fbmp_gpu::Failure(4, std::string("NCCL error ") + std::to_string(rc_) + " at " #call); \
+    } while (0)
+
 #define FBMP_CUDA(call)                                                                          \
     do {                                                                                         \
         cudaError_t e_ = (call);                                                                 \
@@ -128,6 +134,9 @@ struct Context {
     cudaEvent_t poll_ev[2] = {nullptr, nullptr};  // CG flag polling
     // instantiated CG-chunk graphs keyed on their launch parameters (bytes of geometry + pointers)
     std::map<std::string, cudaGraphExec_t> graphs;
+    // NCCL communicator of a row-strip (multi-GPU) solve (fbmp_gpu_ctx_set_comm), or null
+    void* nccl = nullptr;
+    int nranks = 1, rank = 0;
 };
 
 // RAII device selection for calls made from arbitrary host threads.

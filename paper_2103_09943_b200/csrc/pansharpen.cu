@@ -12,6 +12,8 @@
 #include <cstdlib>
 
 #include "pansharpen.cuh"
+#include <nccl.h>
+
 #include "cg_fast.cuh"
 
 namespace fbmp_gpu {
@@ -31,6 +33,11 @@ PsGeo make_geo(int N, int h, int w, int c, int n, int rw, double lambda, double 
     G.rw = rw;
     G.lambda = lambda;
     G.eps = eps;
+    G.grow0 = 0;
+    G.Hg = G.H;
+    G.rlo = 0;
+    G.rhi = G.H;
+    G.dred = nullptr;
     return G;
 }
 
@@ -357,6 +364,7 @@ __global__ void __launch_bounds__(NTU) k_update(PsGeo G, double* __restrict__ z,
     const double* ac = Ap + ch * P;
     double rr = 0.0, zz = 0.0;
     const size_t base = static_cast<size_t>(blockIdx.x) * NTU * UPT;
+    const size_t own_lo = static_cast<size_t>(G.rlo) * G.W, own_hi = static_cast<size_t>(G.rhi) * G.W;
     if ((P & 1) == 0) {
         constexpr int KV = UPT / 2;
         const size_t nv = P / 2;
@@ -387,8 +395,19 @@ __global__ void __launch_bounds__(NTU) k_update(PsGeo G, double* __restrict__ z,
             rv[k].x = rv[k].x - av[k].x * alpha; rv[k].y = rv[k].y - av[k].y * alpha;
             __stcs(reinterpret_cast<double2*>(zc) + vi, zv[k]);
             __stcs(reinterpret_cast<double2*>(rc) + vi, rv[k]);
-            rr += rv[k].x * rv[k].x + rv[k].y * rv[k].y;
-            zz += zv[k].x * zv[k].x + zv[k].y * zv[k].y;
+            if (2 * vi >= own_lo && 2 * vi + 1 < own_hi) {
+                rr += rv[k].x * rv[k].x + rv[k].y * rv[k].y;
+                zz += zv[k].x * zv[k].x + zv[k].y * zv[k].y;
+            } else {  // pair on the edge of the owned rows (odd W)
+                if (2 * vi >= own_lo && 2 * vi < own_hi) {
+                    rr += rv[k].x * rv[k].x;
+                    zz += zv[k].x * zv[k].x;
+                }
+                if (2 * vi + 1 >= own_lo && 2 * vi + 1 < own_hi) {
+                    rr += rv[k].y * rv[k].y;
+                    zz += zv[k].y * zv[k].y;
+                }
+            }
         }
     } else {
         pdl_wait();
@@ -402,8 +421,10 @@ __global__ void __launch_bounds__(NTU) k_update(PsGeo G, double* __restrict__ z,
             const double rv = rc[i] - ac[i] * alpha;
             zc[i] = zv;
             rc[i] = rv;
-            rr += rv * rv;
-            zz += zv * zv;
+            if (i >= own_lo && i < own_hi) {
+                rr += rv * rv;
+                zz += zv * zv;
+            }
         }
     }
     const double brr = block_sum<NTU>(rr, red);
@@ -415,7 +436,11 @@ __global__ void __launch_bounds__(NTU) k_update(PsGeo G, double* __restrict__ z,
     if (elect_last_block(&st[ch].cnt_u, nblk)) {
         const double rs_new = sum_partials<NTU>(part + static_cast<size_t>(ch) * nblk * 2, nblk, 2, red);
         const double zsq = sum_partials<NTU>(part + static_cast<size_t>(ch) * nblk * 2 + 1, nblk, 2, red);
-        if (threadIdx.x == 0) {
+        if (threadIdx.x == 0 && G.dred) {  // distributed: publish the local sums only
+            G.dred[G.N + 3 * ch + 1] = rs_new;
+            G.dred[G.N + 3 * ch + 2] = zsq;
+            st[ch].cnt_u = 0;
+        } else if (threadIdx.x == 0) {
             CgState& S = st[ch];
             const double step = fabs(S.alpha) * sqrt(S.pp);
             S.zz = zsq;
@@ -473,7 +498,7 @@ __global__ void __launch_bounds__(NTA) k_rhs(PsGeo G, const double* __restrict__
         if (CG) {
             z[gi] = 0.0;
             p1[gi] = 0.0;
-            ss += acc * acc;
+            if (R >= G.rlo && R < G.rhi) ss += acc * acc;
         }
     }
     if (CG) {
@@ -481,7 +506,10 @@ __global__ void __launch_bounds__(NTA) k_rhs(PsGeo G, const double* __restrict__
         if (threadIdx.x == 0) part[static_cast<size_t>(ch) * nblk + blockIdx.x] = bs;
         if (elect_last_block(&st[ch].cnt_init, nblk)) {
             const double tot = sum_partials<NTA>(part + static_cast<size_t>(ch) * nblk, nblk, 1, red);
-            if (threadIdx.x == 0) {
+            if (threadIdx.x == 0 && G.dred) {  // distributed: publish the local sum only
+                G.dred[G.N + 3 * ch + 1] = tot;
+                st[ch].cnt_init = 0;
+            } else if (threadIdx.x == 0) {
                 CgState& S = st[ch];
                 S.rs = tot;
                 S.rhs_norm = sqrt(tot);
@@ -1375,6 +1403,210 @@ void convolve(Context& ctx, const double* d_in, int H, int W, const double* d_ta
                                                                                    d_out);
     ctx.count();
     check_launch();
+}
+
+
+// =============================================================================================
+// Row-strip decomposition of the CG (SURVEY.md 8(e), config C5 on several GPUs)
+// =============================================================================================
+// Every strip holds its rows plus `halo` rows above and below (periodic in the global image);
+// the CG kernels run unchanged on the padded strip, so rows near the padded edges see wrapped
+// garbage -- the halo (>= the operator's dependency depth, 32 rows) keeps it out of the owned
+// rows. Dot products sum owned rows only and are combined across strips by an allreduce; the
+// CG scalars are then updated by k_dist_* on every strip identically. Per iteration the only
+// data exchanged is the halo of r (p_new is recomputed in the halo from r and p_old, both valid
+// there). With a communicator the strips are the ranks (NCCL allreduce / send-recv over
+// NVLink); without one, the strips are virtual ranks of this process (device copies and an
+// in-order sum), which is how the decomposition is tested on one GPU.
+namespace {
+
+__global__ void k_dist_sum(double* const* reds, int S, int off, int n) {  // loopback allreduce
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int k = 0; k < S; ++k) s += reds[k][off + i];  // strip (rank) order, like a ring sum
+        for (int k = 0; k < S; ++k) reds[k][off + i] = s;
+    }
+}
+
+__global__ void k_dist_init(CgState* st, const double* __restrict__ dred, int N, int max_iters, double cg_tol) {
+    const int ch = blockIdx.x * blockDim.x + threadIdx.x;
+    if (ch >= N) return;
+    CgState& S = st[ch];
+    const double tot = dred[N + 3 * ch + 1];
+    S.rs = tot;
+    S.rhs_norm = sqrt(tot);
+    S.pp = S.pAp = S.alpha = S.beta = S.zz = 0.0;
+    S.cg_tol = cg_tol;
+    S.t = 0;
+    S.iters = 0;
+    S.max_iters = max_iters;
+    S.done = (S.rhs_norm == 0.0) ? 1 : (max_iters <= 0 ? 3 : 0);
+    S.cnt_q = S.cnt_a = S.cnt_u = S.cnt_init = 0;
+}
+
+__global__ void k_dist_alpha(CgState* st, const double* __restrict__ dred, int N) {  // pansharpen.cpp:236-244
+    const int ch = blockIdx.x * blockDim.x + threadIdx.x;
+    if (ch >= N || st[ch].done) return;
+    CgState& S = st[ch];
+    const double pAp = dred[ch];
+    S.pAp = pAp;
+    if (!(pAp > 0)) {
+        S.done = (sqrt(S.rs) <= 1e-12 * S.rhs_norm) ? 1 : 2;
+        S.iters = S.t + 1;
+    } else {
+        S.alpha = S.rs / pAp;
+    }
+}
+
+__global__ void k_dist_beta(CgState* st, const double* __restrict__ dred, int N) {  // pansharpen.cpp:245-255
+    const int ch = blockIdx.x * blockDim.x + threadIdx.x;
+    if (ch >= N || st[ch].done) return;
+    CgState& S = st[ch];
+    const double pp = dred[N + 3 * ch], rs_new = dred[N + 3 * ch + 1], zsq = dred[N + 3 * ch + 2];
+    S.pp = pp;
+    S.zz = zsq;
+    const double step = fabs(S.alpha) * sqrt(pp);
+    if (step <= S.cg_tol * fmax(sqrt(zsq), 1e-300)) {
+        S.done = 1;
+        S.iters = S.t + 1;
+    } else {
+        S.beta = rs_new / S.rs;
+        S.rs = rs_new;
+        S.t = S.t + 1;
+        if (S.t >= S.max_iters) {
+            S.done = 3;
+            S.iters = S.max_iters;
+        }
+    }
+}
+
+}  // namespace
+
+void cg_solve_strips(Context& ctx, std::vector<StripCg>& SS, const StripComm& comm, int max_iters, double cg_tol,
+                     std::vector<CgState>& host_state) {
+    const int NS = static_cast<int>(SS.size());
+    if (NS < 1) param_error("cg_solve_strips: no strips");
+    const PsGeo& G0 = SS[0].G;
+    const int N = G0.N, halo = comm.halo;
+    if (!fast_ok(G0) || !use_llp()) param_error("distributed CG: needs the fast operator path (radius 1, c in {1,2,4})");
+    const size_t P = static_cast<size_t>(G0.H) * G0.W;
+    const int W = G0.W, Hp = G0.H;
+    const QLaunch q2 = q2_select<true>(G0);
+    if (!q2.fn) param_error("distributed CG: kernel side without a specialised K_Q");
+    const int nbq = q2.nblk;
+    const int nba = ceil_div(G0.W, fast::a4::TA) * ceil_div(G0.H, fast::a4::TA);
+    const int nbu = static_cast<int>((P + static_cast<size_t>(NTU) * UPT - 1) / (static_cast<size_t>(NTU) * UPT));
+    const int nbA = std::max(nba, ceil_div(G0.W, fast::kl::BAND) * ceil_div(G0.H, fast::kl::RB));
+    const size_t sr = static_cast<size_t>(G0.n) * G0.n * sizeof(double);
+    set_smem(q2.fn, q2.smem);
+    prepare_apply2<true>(G0);
+    set_smem(k_rhs<true>, sr);
+    double** d_reds = ctx.scratch<double*>("dist_reds", NS);
+    {
+        std::vector<double*> h(NS);
+        for (int k = 0; k < NS; ++k) h[k] = SS[k].dred;
+        FBMP_CUDA(cudaMemcpyAsync(d_reds, h.data(), sizeof(double*) * NS, cudaMemcpyHostToDevice, ctx.stream));
+    }
+    auto parts = [&](StripCg& S, double*& pi, double*& pq, double*& pa, double*& pu) {
+        pi = S.B.part;
+        pq = pi + static_cast<size_t>(N) * nba;
+        pa = pq + static_cast<size_t>(N) * nbq;
+        pu = pa + static_cast<size_t>(N) * nbA;
+    };
+    auto allreduce = [&](int off, int n) {
+        if (comm.nccl) {
+            for (auto& S : SS)
+                FBMP_NCCL(ncclAllReduce(S.dred + off, S.dred + off, n, ncclDouble, ncclSum,
+                                        static_cast<ncclComm_t>(comm.nccl), ctx.stream));
+        } else {
+            k_dist_sum<<<1, 128, 0, ctx.stream>>>(d_reds, NS, off, n);
+            ctx.count();
+        }
+    };
+    // halo of r: top halo <- the neighbour above's last owned rows, bottom <- the one below's first
+    auto exchange_r = [&]() {
+        const size_t hb = static_cast<size_t>(halo) * W * sizeof(double);
+        const int hloc = Hp - 2 * halo;
+        if (comm.nccl) {
+            auto cm = static_cast<ncclComm_t>(comm.nccl);
+            const int up = (comm.rank + comm.nranks - 1) % comm.nranks, dn = (comm.rank + 1) % comm.nranks;
+            double* r = SS[0].B.r;
+            FBMP_NCCL(ncclGroupStart());
+            for (int c = 0; c < N; ++c) {
+                double* pl = r + c * P;
+                FBMP_NCCL(ncclSend(pl + static_cast<size_t>(halo) * W, halo * W, ncclDouble, up, cm, ctx.stream));
+                FBMP_NCCL(ncclSend(pl + static_cast<size_t>(hloc) * W, halo * W, ncclDouble, dn, cm, ctx.stream));
+                FBMP_NCCL(ncclRecv(pl, halo * W, ncclDouble, up, cm, ctx.stream));
+                FBMP_NCCL(ncclRecv(pl + static_cast<size_t>(halo + hloc) * W, halo * W, ncclDouble, dn, cm,
+                                   ctx.stream));
+            }
+            FBMP_NCCL(ncclGroupEnd());
+        } else {
+            for (int k = 0; k < NS; ++k) {
+                const StripCg& A = SS[(k + NS - 1) % NS];  // above
+                const StripCg& Bl = SS[(k + 1) % NS];      // below
+                for (int c = 0; c < N; ++c) {
+                    double* pl = SS[k].B.r + c * P;
+                    FBMP_CUDA(cudaMemcpyAsync(pl, A.B.r + c * P + static_cast<size_t>(hloc) * W, hb,
+                                              cudaMemcpyDeviceToDevice, ctx.stream));
+                    FBMP_CUDA(cudaMemcpyAsync(pl + static_cast<size_t>(halo + hloc) * W,
+                                              Bl.B.r + c * P + static_cast<size_t>(halo) * W, hb,
+                                              cudaMemcpyDeviceToDevice, ctx.stream));
+                }
+            }
+        }
+    };
+    // init: rhs = B^T U x (r), z = 0, p_old = 0; rs = ||rhs||^2 over all owned rows
+    for (auto& S : SS) {
+        FBMP_CUDA(cudaMemsetAsync(S.B.st, 0, sizeof(CgState) * N, ctx.stream));
+        double *pi, *pq, *pa, *pu;
+        parts(S, pi, pq, pa, pu);
+        k_rhs<true><<<dim3(nba, N), NTA, sr, ctx.stream>>>(S.G, S.taps, S.x, S.B.r, S.B.z, S.B.p + static_cast<size_t>(N) * P,
+                                                            S.B.st, pi, nba, max_iters, cg_tol);
+        ctx.count();
+        check_launch();
+    }
+    allreduce(N, 3 * N);
+    for (auto& S : SS) {
+        k_dist_init<<<ceil_div(N, 64), 64, 0, ctx.stream>>>(S.B.st, S.dred, N, max_iters, cg_tol);
+        ctx.count();
+    }
+    exchange_r();
+    CgState* pinned = static_cast<CgState*>(ctx.pinned(sizeof(CgState) * N));
+    const int chunk = 8;
+    for (long long it = 0; it <= static_cast<long long>(max_iters) + chunk; it += chunk) {
+        for (int j = 0; j < chunk; ++j) {
+            for (auto& S : SS) {
+                double *pi, *pq, *pa, *pu;
+                parts(S, pi, pq, pa, pu);
+                q2.fn<<<dim3(nbq, N), q2.threads, q2.smem, ctx.stream>>>(S.G, S.taps, S.B.r, S.B.p, S.B.q, S.B.st, pq, nbq);
+                ctx.count();
+                launch_apply2<true>(ctx, S.G, S.taps, S.guide, S.wmu, S.wg, S.B.p, S.B.q, S.B.Ap, S.B.st, pa);
+                ctx.count(2);
+            }
+            allreduce(0, N);
+            for (auto& S : SS) {
+                k_dist_alpha<<<ceil_div(N, 64), 64, 0, ctx.stream>>>(S.B.st, S.dred, N);
+                double *pi, *pq, *pa, *pu;
+                parts(S, pi, pq, pa, pu);
+                k_update<<<dim3(nbu, N), NTU, 0, ctx.stream>>>(S.G, S.B.z, S.B.r, S.B.p, S.B.Ap, S.B.st, pu, nbu);
+                ctx.count(2);
+            }
+            allreduce(N, 3 * N);
+            for (auto& S : SS) {
+                k_dist_beta<<<ceil_div(N, 64), 64, 0, ctx.stream>>>(S.B.st, S.dred, N);
+                ctx.count();
+            }
+            exchange_r();
+        }
+        check_launch();
+        FBMP_CUDA(cudaMemcpyAsync(pinned, SS[0].B.st, sizeof(CgState) * N, cudaMemcpyDeviceToHost, ctx.stream));
+        FBMP_CUDA(cudaStreamSynchronize(ctx.stream));
+        bool all = true;
+        for (int i = 0; i < N; ++i) all = all && pinned[i].done;
+        if (all) break;
+    }
+    host_state.assign(pinned, pinned + N);
 }
 
 }  // namespace fbmp_gpu

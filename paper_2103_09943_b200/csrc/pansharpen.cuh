@@ -30,6 +30,12 @@ struct PsGeo {
                                   // taps, guide and intensity scale
     int cpc;                      // channels per CTA in the fast K_A (guide tile reuse)
     int dbg;                      // development: bitmask of K_A stages to skip (timing only)
+    // row-strip domain decomposition (distributed CG, csrc/dist.cu); defaults = whole image:
+    int grow0, Hg;                // global row of local row 0 (mod Hg), global height
+    int rlo, rhi;                 // local rows owned by this strip: CG dot products sum only these
+    double* dred;                 // non-null: kernels publish per-channel LOCAL sums here
+                                  //   [0, N): p.Ap; [N + 3 ch + {0,1,2}]: ||p||^2, ||r||^2, ||z||^2
+                                  // and leave the CG scalar update to k_dist_* after an allreduce
 };
 
 PsGeo make_geo(int N, int h, int w, int c, int n, int rw, double lambda, double eps, int cps = 0);
@@ -51,10 +57,32 @@ struct CgBuffers {
 void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* d_guide, const double* d_x,
               CgBuffers& B, int max_iters, double cg_tol, std::vector<CgState>& host_state);
 
+// Row-strip decomposition of the CG (csrc/pansharpen.cu, "Row-strip decomposition").
+struct StripCg {
+    PsGeo G;               // padded strip geometry with grow0 / Hg / rlo / rhi / dred set
+    const double* taps;    // n*n
+    const double* guide;   // strip of L(pan_n) (H' x W)
+    const double* wmu;     // strips of the window statistics (computed on the whole image)
+    const double* wg;
+    const double* x;       // LR strip (N x H'/c x w), scaled
+    CgBuffers B;
+    double* dred;          // 4 N (same pointer as G.dred)
+};
+struct StripComm {
+    void* nccl = nullptr;  // ncclComm_t: one strip per rank; null: the strips are virtual ranks
+    int nranks = 1, rank = 0;
+    int halo = 32;         // rows above and below every strip
+};
+void cg_solve_strips(Context& ctx, std::vector<StripCg>& strips, const StripComm& comm, int max_iters,
+                     double cg_tol, std::vector<CgState>& host_state);
+
 // A(p) (pansharpen.cpp:218-223) for N channels: mode 0 full operator, 1 matting only (M p),
 // 2 data term only (B^T U D B p).
 void cg_operator_apply(Context& ctx, const PsGeo& G, const double* d_taps, const double* d_guide,
                        const double* d_p, double* d_out, int mode);
+
+// per-scene window statistics of the fast operator: mu_k, g_k = [interior] / (eps/9 + var_k)
+void guide_stats(Context& ctx, const PsGeo& G, const double* d_guide, double* mu, double* gk);
 
 // rhs = B^T U x (pansharpen.cpp:225).
 void data_rhs(Context& ctx, const PsGeo& G, const double* d_taps, const double* d_x, double* d_out);

@@ -163,6 +163,11 @@ class Context:
     def set_profile(self, on: bool) -> None:
         _lib.fbmp_gpu_ctx_set_profile(self.h, int(on))
 
+    def set_comm(self, uid: bytes, nranks: int, rank: int) -> None:
+        """Attach an NCCL communicator (row-strip solves); every rank calls this with the same id."""
+        buf = (C.c_ubyte * 128).from_buffer_copy(bytes(uid).ljust(128, b"\0")[:128])
+        _check(_lib.fbmp_gpu_ctx_set_comm(self.h, buf, nranks, rank))
+
     def kernel_profile(self) -> dict:
         ms = (C.c_double * 4)()
         n = (C.c_longlong * 4)()
@@ -553,6 +558,28 @@ def blind_batch(lrms, pan, factor, n, sw=None, ke=None, ps=None, ctx=None):
     return out, k
 
 
+def nccl_unique_id() -> bytes:
+    """A fresh NCCL unique id (rank 0), to be broadcast to all ranks for Context.set_comm."""
+    buf = (C.c_ubyte * 128)()
+    _check(_lib.fbmp_gpu_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def blind_strips_dev(d_lrms: int, N: int, h: int, w: int, d_pan: int, d_out: int, d_k: int, factor: int, n: int,
+                     ctx: Context, vstrips: int = 1, sw=None, ke=None, ps=None):
+    """Row-strip blind solve (raw device pointers): across the context's NCCL ranks, or on
+    `vstrips` virtual ranks in this process when the context has no communicator."""
+    sw = sw or SpectralWeightConfig(l=4, lambda_omega=10.0, factor=factor)
+    sw.factor = factor
+    ke = ke or KernelEstParams(n=n)
+    ke.n = n
+    ps = ps or PansharpenParams()
+    c1, c2, c3 = sw.c(), ke.c(), ps.c()
+    _check(_lib.fbmp_gpu_blind_strips_dev(ctx.h, C.cast(C.c_void_p(d_lrms), D), N, h, w, C.cast(C.c_void_p(d_pan), D),
+                                          C.byref(c1), C.byref(c2), C.byref(c3), vstrips,
+                                          C.cast(C.c_void_p(d_out), D), C.cast(C.c_void_p(d_k), D)))
+
+
 def blind_batch_dev(d_lrms: int, S: int, N: int, h: int, w: int, d_pan: int, d_out: int, d_k: int, factor: int,
                     n: int, ctx: Context, ch0: int = 0, nch: int = -1, sw=None, ke=None, ps=None):
     """Device-resident batch / channel-subset blind solve (raw device pointers)."""
@@ -585,7 +612,7 @@ EXPORTED_SYMBOLS = (
     "fbmp_gpu_default_ps_params", "fbmp_gpu_default_ke_params", "fbmp_gpu_default_sw_params",
     "fbmp_gpu_ctx_create", "fbmp_gpu_ctx_destroy", "fbmp_gpu_last_error", "fbmp_gpu_ctx_stats",
     "fbmp_gpu_ctx_stream", "fbmp_gpu_ctx_launches", "fbmp_gpu_ctx_set_profile", "fbmp_gpu_ctx_kernel_profile",
-    "fbmp_gpu_blind_batch_dev",
+    "fbmp_gpu_blind_batch_dev", "fbmp_gpu_blind_strips_dev", "fbmp_gpu_nccl_unique_id", "fbmp_gpu_ctx_set_comm",
     "fbmp_gpu_pansharpen", "fbmp_gpu_estimate_kernel_tgv",
     "fbmp_gpu_estimate_kernel_plane", "fbmp_gpu_solve_weights", "fbmp_gpu_combine_bands", "fbmp_gpu_blind",
     "fbmp_gpu_blind_dev", "fbmp_gpu_blind_batch", "fbmp_gpu_blind_subset", "fbmp_gpu_apply_prior", "fbmp_gpu_llp_apply",

@@ -19,6 +19,5 @@ for src in B.CU_SOURCES:
     subprocess.run([B.NVCC] + B.NVFLAGS + defs + ["-c", os.path.join(B.CSRC, src), "-o", obj], check=True)
     objs.append(obj)
 out = os.path.join(B.LIBDIR, "exp", f"libfbmp_gpu_{name}.so")
-subprocess.run([B.NVCC] + B.ARCH + ["-shared", "-o", out] + objs +
-               ["-L" + B.CUDA_LIB, "-lcufft", "-lcudart", "-Xlinker", "-rpath," + B.CUDA_LIB], check=True)
+subprocess.run([B.NVCC] + B.ARCH + ["-shared", "-o", out] + objs + B.LINK, check=True)
 print(out)

@@ -209,6 +209,14 @@ def our_arm(args, cfg):
         scenes = [synth.make_scene(cfg, 0)]
         part = shard.partition(cfg.bands, world, rank)
         ch0, nch = part.start, len(part)
+    elif cfg.name == "C5" and world > 1:
+        # one 8192^2 scene on row strips: r-halo exchange + allreduces over NCCL every CG iteration
+        mode, scaling = "row-strips", "strong"
+        scenes = [synth.make_scene(cfg, 0)]
+        ch0, nch = 0, -1
+        uid = [fbmp.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.set_comm(uid[0], world, rank)
     else:
         mode, scaling = "replicas", "weak"
         scenes = [synth.make_scene(cfg, rank)]
@@ -230,8 +238,12 @@ def our_arm(args, cfg):
     torch.cuda.synchronize()
 
     def step():
-        fbmp.blind_batch_dev(d_lrms.data_ptr(), S, N, h, w, d_pan.data_ptr(), d_out.data_ptr(), d_k.data_ptr(),
-                             cfg.ratio, n, ctx, ch0=ch0, nch=nch)
+        if mode == "row-strips":
+            fbmp.blind_strips_dev(d_lrms.data_ptr(), N, h, w, d_pan.data_ptr(), d_out.data_ptr(), d_k.data_ptr(),
+                                  cfg.ratio, n, ctx)
+        else:
+            fbmp.blind_batch_dev(d_lrms.data_ptr(), S, N, h, w, d_pan.data_ptr(), d_out.data_ptr(),
+                                 d_k.data_ptr(), cfg.ratio, n, ctx, ch0=ch0, nch=nch)
 
     def barrier():
         torch.cuda.synchronize()
@@ -262,6 +274,15 @@ def our_arm(args, cfg):
     pan_h = torch.from_numpy(pan_np).pin_memory().numpy()
 
     def e2e_step():
+        if mode == "row-strips":  # H2D of the (replicated) inputs, solve, D2H of the cube on rank 0
+            with torch.cuda.stream(stream):
+                d_lrms.copy_(torch.from_numpy(lrms_h), non_blocking=True)
+                d_pan.copy_(torch.from_numpy(pan_h), non_blocking=True)
+            step()
+            with torch.cuda.stream(stream):
+                if rank == 0:
+                    d_out.cpu()
+            return None
         if mode == "scene-batch":
             return fbmp.blind_batch(lrms_h, pan_h, cfg.ratio, n, ctx=ctx)
         if mode == "channel-shards":
@@ -292,7 +313,8 @@ def our_arm(args, cfg):
         return
     P = H * W
     # whole-job units per step: all pixel-bands of every scene the job solves
-    job_units = {"scene-batch": cfg.scenes * P * N, "channel-shards": P * N, "replicas": world * P * N}[mode]
+    job_units = {"scene-batch": cfg.scenes * P * N, "channel-shards": P * N, "replicas": world * P * N,
+                 "row-strips": P * N}[mode]
     units = args.steps * job_units
     value = units / (t_ms / 1e3) / 1e6
     e2e = units / (t_e2e / 1e3) / 1e6

@@ -1532,11 +1532,14 @@ void cg_solve_strips(Context& ctx, std::vector<StripCg>& SS, const StripComm& co
             const int up = (comm.rank + comm.nranks - 1) % comm.nranks, dn = (comm.rank + 1) % comm.nranks;
             double* r = SS[0].B.r;
             FBMP_NCCL(ncclGroupStart());
+            // per peer, sends and receives match in issue order: the downward flow (my last owned
+            // rows -> the top halo below) is issued before the upward flow, so the pairing is right
+            // also when up == dn (2 ranks) or up == dn == me (1 rank: the periodic wrap)
             for (int c = 0; c < N; ++c) {
                 double* pl = r + c * P;
-                FBMP_NCCL(ncclSend(pl + static_cast<size_t>(halo) * W, halo * W, ncclDouble, up, cm, ctx.stream));
                 FBMP_NCCL(ncclSend(pl + static_cast<size_t>(hloc) * W, halo * W, ncclDouble, dn, cm, ctx.stream));
                 FBMP_NCCL(ncclRecv(pl, halo * W, ncclDouble, up, cm, ctx.stream));
+                FBMP_NCCL(ncclSend(pl + static_cast<size_t>(halo) * W, halo * W, ncclDouble, up, cm, ctx.stream));
                 FBMP_NCCL(ncclRecv(pl + static_cast<size_t>(halo + hloc) * W, halo * W, ncclDouble, dn, cm,
                                    ctx.stream));
             }

@@ -259,4 +259,24 @@ def test_blind_strips_match_single_domain(gpu, G):
     st = ctx.stats()
     assert st["cg_iters"][:4] == list(info["cg_iters"])
     assert np.array_equal(d_k.cpu().numpy(), info["kernel"])
-    assert rel(d_o.cpu().numpy(), ref) < 1e-8  # summation order of the dot products (1e-9 measured at G = 8)
+    # only the summation order of the dot products differs (CG amplifies it: 1e-9 .. 1e-8 measured)
+    assert rel(d_o.cpu().numpy(), ref) < 1e-7
+
+
+def test_blind_strips_nccl_single_rank(gpu):
+    """The NCCL code path of the row-strip solve (allreduce, grouped send/recv of the halo to the
+    rank itself -- the periodic wrap --, allgather of the owned rows, gather to rank 0) on a
+    communicator of one rank; multi-GPU runs use the same calls with more ranks."""
+    import torch
+
+    sc = synth.make_scene("C1")
+    ref, info = gpu.blind(sc.lrms, sc.pan, 4, 15)
+    ctx = gpu.Context(0)
+    ctx.set_comm(gpu.nccl_unique_id(), 1, 0)
+    d_l, d_p = torch.from_numpy(sc.lrms).cuda(), torch.from_numpy(sc.pan).cuda()
+    d_o = torch.empty((4, 256, 256), dtype=torch.float64, device="cuda")
+    d_k = torch.empty((15, 15), dtype=torch.float64, device="cuda")
+    gpu.blind_strips_dev(d_l.data_ptr(), 4, 64, 64, d_p.data_ptr(), d_o.data_ptr(), d_k.data_ptr(), 4, 15, ctx)
+    torch.cuda.synchronize()
+    assert ctx.stats()["cg_iters"][:4] == list(info["cg_iters"])
+    assert rel(d_o.cpu().numpy(), ref) < 1e-7

@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(NTU) k_update(PsGeo G, double* __restrict__ z,
     const int ch = blockIdx.y;
     // t and z, r, p are not written by K_A (the predecessor): read them before pdl_wait so the
     // loads overlap K_A's tail; done may still be set by K_A (pAp <= 0) and is re-checked
-    if (st[ch].done) return;
+    if (__syncthreads_or(st[ch].done)) return;  // uniform: the reductions below stay convergent
     const int t = st[ch].t;
     const size_t P = static_cast<size_t>(G.H) * G.W;
     const double* pc = pbuf + (static_cast<size_t>(t & 1) * G.N + ch) * P;
@@ -365,6 +365,8 @@ __global__ void __launch_bounds__(NTU) k_update(PsGeo G, double* __restrict__ z,
     double rr = 0.0, zz = 0.0;
     const size_t base = static_cast<size_t>(blockIdx.x) * NTU * UPT;
     const size_t own_lo = static_cast<size_t>(G.rlo) * G.W, own_hi = static_cast<size_t>(G.rhi) * G.W;
+    // the whole block's range is owned (always, unless the CG runs on a row strip)
+    const bool all_owned = base >= own_lo && base + static_cast<size_t>(NTU) * UPT <= own_hi;
     if ((P & 1) == 0) {
         constexpr int KV = UPT / 2;
         const size_t nv = P / 2;
@@ -380,7 +382,7 @@ __global__ void __launch_bounds__(NTU) k_update(PsGeo G, double* __restrict__ z,
         }
         pdl_wait();
         pdl_trigger();
-        if (st[ch].done) return;
+        if (__syncthreads_or(st[ch].done)) return;
         const double alpha = st[ch].alpha;
 #pragma unroll
         for (int k = 0; k < KV; ++k) {
@@ -390,29 +392,23 @@ __global__ void __launch_bounds__(NTU) k_update(PsGeo G, double* __restrict__ z,
 #pragma unroll
         for (int k = 0; k < KV; ++k) {
             const size_t vi = base / 2 + static_cast<size_t>(k) * NTU + threadIdx.x;
-            if (vi >= nv) break;
-            zv[k].x = zv[k].x + pv[k].x * alpha; zv[k].y = zv[k].y + pv[k].y * alpha;
-            rv[k].x = rv[k].x - av[k].x * alpha; rv[k].y = rv[k].y - av[k].y * alpha;
-            __stcs(reinterpret_cast<double2*>(zc) + vi, zv[k]);
-            __stcs(reinterpret_cast<double2*>(rc) + vi, rv[k]);
-            if (2 * vi >= own_lo && 2 * vi + 1 < own_hi) {
-                rr += rv[k].x * rv[k].x + rv[k].y * rv[k].y;
-                zz += zv[k].x * zv[k].x + zv[k].y * zv[k].y;
-            } else {  // pair on the edge of the owned rows (odd W)
-                if (2 * vi >= own_lo && 2 * vi < own_hi) {
-                    rr += rv[k].x * rv[k].x;
-                    zz += zv[k].x * zv[k].x;
-                }
-                if (2 * vi + 1 >= own_lo && 2 * vi + 1 < own_hi) {
-                    rr += rv[k].y * rv[k].y;
-                    zz += zv[k].y * zv[k].y;
-                }
+            if (vi < nv) {
+                zv[k].x = zv[k].x + pv[k].x * alpha; zv[k].y = zv[k].y + pv[k].y * alpha;
+                rv[k].x = rv[k].x - av[k].x * alpha; rv[k].y = rv[k].y - av[k].y * alpha;
+                __stcs(reinterpret_cast<double2*>(zc) + vi, zv[k]);
+                __stcs(reinterpret_cast<double2*>(rc) + vi, rv[k]);
+                // owned rows only (all, unless the CG runs on a row strip); selects keep the
+                // whole-image sums bit-identical to the plain x^2 + y^2 accumulation
+                const bool ox = all_owned || (2 * vi >= own_lo && 2 * vi < own_hi);
+                const bool oy = all_owned || (2 * vi + 1 >= own_lo && 2 * vi + 1 < own_hi);
+                rr += (ox ? rv[k].x * rv[k].x : 0.0) + (oy ? rv[k].y * rv[k].y : 0.0);
+                zz += (ox ? zv[k].x * zv[k].x : 0.0) + (oy ? zv[k].y * zv[k].y : 0.0);
             }
         }
     } else {
         pdl_wait();
         pdl_trigger();
-        if (st[ch].done) return;
+        if (__syncthreads_or(st[ch].done)) return;
         const double alpha = st[ch].alpha;
         for (int k = 0; k < UPT; ++k) {
             const size_t i = base + static_cast<size_t>(k) * NTU + threadIdx.x;
@@ -421,7 +417,7 @@ __global__ void __launch_bounds__(NTU) k_update(PsGeo G, double* __restrict__ z,
             const double rv = rc[i] - ac[i] * alpha;
             zc[i] = zv;
             rc[i] = rv;
-            if (i >= own_lo && i < own_hi) {
+            if (all_owned || (i >= own_lo && i < own_hi)) {
                 rr += rv * rv;
                 zz += zv * zv;
             }

@@ -32,6 +32,9 @@ Context::~Context() {
     for (auto& e : poll_ev)
         if (e) cudaEventDestroy(e);
     if (pinned_buf) cudaFreeHost(pinned_buf);
+    if (aux_stream) cudaStreamDestroy(aux_stream);
+    if (fork_ev) cudaEventDestroy(fork_ev);
+    if (join_ev) cudaEventDestroy(join_ev);
     ws.clear();
     if (stream) cudaStreamDestroy(stream);
 }

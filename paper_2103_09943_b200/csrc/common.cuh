@@ -132,6 +132,8 @@ struct Context {
     void* pinned_buf = nullptr;
     size_t pinned_bytes = 0;
     cudaEvent_t poll_ev[2] = {nullptr, nullptr};  // CG flag polling
+    cudaStream_t aux_stream = nullptr;             // second CG chain inside the chunk graph
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     // instantiated CG-chunk graphs keyed on their launch parameters (bytes of geometry + pointers)
     std::map<std::string, cudaGraphExec_t> graphs;
     // NCCL communicator of a row-strip (multi-GPU) solve (fbmp_gpu_ctx_set_comm), or null

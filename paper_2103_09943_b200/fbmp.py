@@ -500,8 +500,17 @@ def gram(pan, obs, factor, n, ctx=None):
 # blind pipeline
 # ---------------------------------------------------------------------------------------------
 
+def _out(out, shape):
+    """Caller-provided output (e.g. pinned host memory: no pageable staging in the D2H copy)."""
+    if out is None:
+        return np.empty(shape)
+    if out.shape != tuple(shape) or out.dtype != np.float64 or not out.flags.c_contiguous:
+        raise ValueError(f"out must be a C-contiguous float64 array of shape {tuple(shape)}")
+    return out
+
+
 def blind(lrms, pan, factor, n, sw: SpectralWeightConfig | None = None, ke: KernelEstParams | None = None,
-          ps: PansharpenParams | None = None, ctx=None):
+          ps: PansharpenParams | None = None, ctx=None, out=None):
     """solve_weights(all bands) -> estimate_kernel_tgv -> pansharpen. Returns (hrms, info)."""
     lrms, pan = _f(lrms), _f(pan)
     N, h, w = lrms.shape
@@ -510,7 +519,7 @@ def blind(lrms, pan, factor, n, sw: SpectralWeightConfig | None = None, ke: Kern
     ke = ke or KernelEstParams(n=n)
     ke.n = n
     ps = ps or PansharpenParams()
-    out = np.empty((N, h * factor, w * factor))
+    out = _out(out, (N, h * factor, w * factor))
     k = np.empty((n, n))
     om = np.empty(N)
     c1, c2, c3 = sw.c(), ke.c(), ps.c()
@@ -523,7 +532,7 @@ def blind(lrms, pan, factor, n, sw: SpectralWeightConfig | None = None, ke: Kern
                      ms_pansharpen=st["ms_pansharpen"])
 
 
-def blind_subset(lrms, pan, factor, n, ch0, nch, sw=None, ke=None, ps=None, ctx=None):
+def blind_subset(lrms, pan, factor, n, ch0, nch, sw=None, ke=None, ps=None, ctx=None, out=None):
     """Blind solve of bands [ch0, ch0+nch) with weights / kernel / normalisation over all bands
     (one rank's share of a channel-sharded solve). Returns (hrms (nch, H, W), kernel)."""
     lrms, pan = _f(lrms), _f(pan)
@@ -533,7 +542,7 @@ def blind_subset(lrms, pan, factor, n, ch0, nch, sw=None, ke=None, ps=None, ctx=
     ke = ke or KernelEstParams(n=n)
     ke.n = n
     ps = ps or PansharpenParams()
-    out = np.empty((nch, h * factor, w * factor))
+    out = _out(out, (nch, h * factor, w * factor))
     k = np.empty((n, n))
     c1, c2, c3 = sw.c(), ke.c(), ps.c()
     _check(_lib.fbmp_gpu_blind_subset(_ctx(ctx), _p(lrms), N, h, w, _p(pan), C.byref(c1), C.byref(c2), C.byref(c3),
@@ -541,7 +550,7 @@ def blind_subset(lrms, pan, factor, n, ch0, nch, sw=None, ke=None, ps=None, ctx=
     return out, k
 
 
-def blind_batch(lrms, pan, factor, n, sw=None, ke=None, ps=None, ctx=None):
+def blind_batch(lrms, pan, factor, n, sw=None, ke=None, ps=None, ctx=None, out=None):
     """S independent scenes: lrms (S, N, h, w), pan (S, H, W) -> (hrms (S, N, H, W), kernels (S, n, n))."""
     lrms, pan = _f(lrms), _f(pan)
     S, N, h, w = lrms.shape
@@ -550,7 +559,7 @@ def blind_batch(lrms, pan, factor, n, sw=None, ke=None, ps=None, ctx=None):
     ke = ke or KernelEstParams(n=n)
     ke.n = n
     ps = ps or PansharpenParams()
-    out = np.empty((S, N, h * factor, w * factor))
+    out = _out(out, (S, N, h * factor, w * factor))
     k = np.empty((S, n, n))
     c1, c2, c3 = sw.c(), ke.c(), ps.c()
     _check(_lib.fbmp_gpu_blind_batch(_ctx(ctx), _p(lrms), S, N, h, w, _p(pan), C.byref(c1), C.byref(c2),

@@ -280,3 +280,14 @@ def test_blind_strips_nccl_single_rank(gpu):
     torch.cuda.synchronize()
     assert ctx.stats()["cg_iters"][:4] == list(info["cg_iters"])
     assert rel(d_o.cpu().numpy(), ref) < 1e-7
+
+
+def test_blind_into_caller_buffer(gpu):
+    """out= (e.g. pinned host memory) receives the same bits as the returned array."""
+    sc = synth.make_scene("C1")
+    ref, _ = gpu.blind(sc.lrms, sc.pan, 4, 15)
+    buf = np.full((4, 256, 256), np.nan)
+    out, _ = gpu.blind(sc.lrms, sc.pan, 4, 15, out=buf)
+    assert out is buf and np.array_equal(buf, ref)
+    with pytest.raises(ValueError):
+        gpu.blind(sc.lrms, sc.pan, 4, 15, out=np.empty((4, 256, 255)))

@@ -283,6 +283,63 @@ __global__ void __launch_bounds__(NT) k_gram_T(const double* __restrict__ pan, c
     }
 }
 
+// Same partials, register-blocked: a thread owns one row offset dr and GK consecutive column
+// offsets; walking the tile's points along a row, its window of GK region values shifts by c
+// columns per point (c new loads, GK FMAs, one broadcast load of the centre value). Every output
+// keeps the point order of k_gram_T, so the partials are bit-identical.
+constexpr int GK = 12;
+constexpr int NTG = 192;  // >= (2n-1) * ceil((2n-1) / GK) for n <= 21
+template <int CF>
+__global__ void __launch_bounds__(NTG) k_gram_T2(const double* __restrict__ pan, const double* __restrict__ scale,
+                                                 int H, int W, int h, int w, int n, double* __restrict__ part,
+                                                 int ntiles) {
+    constexpr int c = CF;
+    extern __shared__ double reg[];
+    const int s = blockIdx.z, phase = blockIdx.y, tile = blockIdx.x;
+    const int rho_r = phase / c, rho_c = phase - rho_r * c;
+    const int ntx = (w + TG - 1) / TG;
+    const int i0 = (tile / ntx) * TG, j0 = (tile % ntx) * TG;
+    const int D = 2 * n - 1, nd = D * D, nblk = (D + GK - 1) / GK;
+    const int SR = c * (TG - 1) + 2 * (n - 1) + 1;
+    const int R0 = c * i0 - rho_r + (n - 1) / 2 - (n - 1), C0 = c * j0 - rho_c + (n - 1) / 2 - (n - 1);
+    const double sc = scale ? scale[s] : 1.0;
+    const double* ps = pan + static_cast<size_t>(s) * H * W;
+    for (int e = threadIdx.x; e < SR * SR; e += NTG) {
+        const int y = e / SR, x = e - y * SR;
+        reg[e] = ps[static_cast<size_t>(wrapi(R0 + y, H)) * W + wrapi(C0 + x, W)] * sc;
+    }
+    __syncthreads();
+    const int ni = min(TG, h - i0), nj = min(TG, w - j0);
+    double* out = part + ((static_cast<size_t>(s) * ntiles + tile) * c * c + phase) * nd;
+    const int rb = threadIdx.x / nblk, blk = threadIdx.x - rb * nblk;
+    if (rb >= D) return;
+    const int dr = rb - (n - 1), dc0 = blk * GK - (n - 1);
+    double acc[GK];
+#pragma unroll
+    for (int k = 0; k < GK; ++k) acc[k] = 0.0;
+    for (int ii = 0; ii < ni; ++ii) {
+        const double* crow = reg + (c * ii + n - 1) * SR + n - 1;          // centre values
+        const double* wrow = reg + (c * ii + n - 1 - dr) * SR + n - 1 - dc0;  // window row
+        double win[GK];
+#pragma unroll
+        for (int k = 0; k < GK; ++k) win[k] = wrow[-k];
+        for (int jj = 0; jj < nj; ++jj) {
+            const double cv = crow[c * jj];
+#pragma unroll
+            for (int k = 0; k < GK; ++k) acc[k] = fma(cv, win[k], acc[k]);
+            // shift by c columns: win[k] <- value at column + c
+            const double* nxt = wrow + c * (jj + 1);
+#pragma unroll
+            for (int k = GK - 1; k >= 0; --k) win[k] = (k >= c) ? win[k - c] : nxt[-k];
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < GK; ++k) {
+        const int dc = dc0 + k;
+        if (dc <= n - 1) out[(dr + n - 1) * D + dc + n - 1] = acc[k];
+    }
+}
+
 // E^T f partials: sum_{(i,j) in tile} P(c i - tr + C, c j - tc + C) * f(i, j), f = obs * scale
 __global__ void __launch_bounds__(NT) k_gram_etf(const double* __restrict__ pan, const double* __restrict__ obs,
                                                  const double* __restrict__ scale, int H, int W, int h, int w, int c,
@@ -1245,9 +1302,15 @@ static void gram_T_and_etf(Context& ctx, const double* d_pan, const double* d_ob
     const int SR = c * (TG - 1) + 2 * (n - 1) + 1;
     const size_t smT = static_cast<size_t>(SR) * SR * sizeof(double);
     if (smT > 227 * 1024) param_error("build_observation: kernel side too large for the device Gram kernel");
-    set_smem(k_gram_T, smT);
     double* partT = ctx.scratch<double>("gram_partT", static_cast<size_t>(S) * ntiles * c * c * nd);
-    k_gram_T<<<dim3(ntiles, c * c, S), NT, smT, ctx.stream>>>(d_pan, d_scale, H, W, h, w, c, n, partT, ntiles);
+    if (D * ((D + GK - 1) / GK) <= NTG && (c == 1 || c == 2 || c == 4)) {  // register-blocked (n <= 21)
+        auto fn = c == 4 ? k_gram_T2<4> : c == 2 ? k_gram_T2<2> : k_gram_T2<1>;
+        set_smem(fn, smT);
+        fn<<<dim3(ntiles, c * c, S), NTG, smT, ctx.stream>>>(d_pan, d_scale, H, W, h, w, n, partT, ntiles);
+    } else {
+        set_smem(k_gram_T, smT);
+        k_gram_T<<<dim3(ntiles, c * c, S), NT, smT, ctx.stream>>>(d_pan, d_scale, H, W, h, w, c, n, partT, ntiles);
+    }
     k_reduce_tiles<<<grid1d(ctx, static_cast<long long>(S) * c * c * nd), 256, 0, ctx.stream>>>(partT, S, ntiles,
                                                                                                 c * c * nd, T);
     const int SRf = c * (TG - 1) + n;

@@ -321,16 +321,18 @@ __global__ void __launch_bounds__(NTG) k_gram_T2(const double* __restrict__ pan,
         const double* crow = reg + (c * ii + n - 1) * SR + n - 1;          // centre values
         const double* wrow = reg + (c * ii + n - 1 - dr) * SR + n - 1 - dc0;  // window row
         double win[GK];
+        const int kval = min(GK, n - dc0);  // column offsets beyond n - 1 are padding: never loaded
 #pragma unroll
-        for (int k = 0; k < GK; ++k) win[k] = wrow[-k];
+        for (int k = 0; k < GK; ++k) win[k] = k < kval ? wrow[-k] : 0.0;
         for (int jj = 0; jj < nj; ++jj) {
             const double cv = crow[c * jj];
 #pragma unroll
             for (int k = 0; k < GK; ++k) acc[k] = fma(cv, win[k], acc[k]);
             // shift by c columns: win[k] <- value at column + c
             const double* nxt = wrow + c * (jj + 1);
+            const bool more = jj + 1 < nj;  // no load past the tile's last point
 #pragma unroll
-            for (int k = GK - 1; k >= 0; --k) win[k] = (k >= c) ? win[k - c] : nxt[-k];
+            for (int k = GK - 1; k >= 0; --k) win[k] = (k >= c) ? win[k - c] : (more && k < kval ? nxt[-k] : 0.0);
         }
     }
 #pragma unroll

@@ -305,6 +305,7 @@ def our_arm(args, cfg):
     ctx.set_profile(True)
     step()
     prof = ctx.kernel_profile()
+    prof_ch_iters = ctx.stats()["cg_channel_iters"]
     ctx.set_profile(False)
 
     tt = torch.tensor([t_ms, t_e2e], dtype=torch.float64, device=dev)
@@ -325,12 +326,16 @@ def our_arm(args, cfg):
     s = 8
     p = h * w
     NC = S * NO  # channels in one launch of the CG kernels on this rank
-    # algorithmic bytes per launch (all NC channels; the guide, mu_k and g_k maps are per scene)
-    alg = {"K_Q": (3 * s * P + s * p) * NC,        # read r, p_old; write p_new, q
-           "K_D": (s * P + s * p) * NC,            # read q; write d = B^T U q
-           "K_L": 3 * s * P * NC + 3 * s * P * S,  # read p, d, guide/mu/g (per scene); write Ap
-           "K_U": 6 * s * P * NC}                  # read z, r, p, Ap; write z, r
+    # algorithmic bytes per launch: only channels that are still iterating do work, so a launch
+    # moves (channel-iterations / launches) channels' worth (converged channels exit at once);
+    # the guide, mu_k and g_k maps are read per scene
     prof = {k: v for k, v in prof.items() if v["launches"] > 0}
+    nlaunch = max(v["launches"] for v in prof.values())
+    act = prof_ch_iters / max(nlaunch, 1)  # mean active channels per launch
+    alg = {"K_Q": (3 * s * P + s * p) * act,        # read r, p_old; write p_new, q
+           "K_D": (s * P + s * p) * act,            # read q; write d = B^T U q
+           "K_L": 3 * s * P * act + 3 * s * P * S,  # read p, d, guide/mu/g (per scene); write Ap
+           "K_U": 6 * s * P * act}                  # read z, r, p, Ap; write z, r
     dom = max(prof, key=lambda k: prof[k]["total_ms"])
     d = prof[dom]
     avg_ms = d["total_ms"] / max(d["launches"], 1)
@@ -341,7 +346,9 @@ def our_arm(args, cfg):
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tfile):
         try:
-            traffic = json.load(open(tfile)).get(dom)
+            tj = json.load(open(tfile))
+            if tj.get("config", "C2") == cfg.name:  # the capture's own config only
+                traffic = tj.get(dom)
         except Exception:
             traffic = None
     cg_total = sum(v["total_ms"] for v in prof.values())

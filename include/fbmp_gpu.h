@@ -73,6 +73,7 @@ typedef struct fbmp_gpu_stats {
     int admm_iters;      /* ADMM iterations of the kernel fit (0 if not run) */
     int cg_iters[64];    /* CG iterations per channel (first 64 channels) */
     double ms_weights, ms_kernel_fit, ms_pansharpen; /* device time of the stages */
+    long long cg_channel_iters; /* sum of the CG iterations over all channels of the last solve */
 } fbmp_gpu_stats;
 
 void fbmp_gpu_default_ps_params(fbmp_ps_params* p);

@@ -364,6 +364,8 @@ void blind_device(Context& ctx, const double* d_lrms, int S, int N, int h, int w
     ctx.stats.ms_pansharpen = d;
     ctx.stats.admm_iters = admm_iters.empty() ? 0 : admm_iters[0];
     for (int i = 0; i < 64; ++i) ctx.stats.cg_iters[i] = i < static_cast<int>(cg_iters.size()) ? cg_iters[i] : 0;
+    ctx.stats.cg_channel_iters = 0;
+    for (int it : cg_iters) ctx.stats.cg_channel_iters += it;
     cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2); cudaEventDestroy(e3);
 }
 

@@ -66,7 +66,7 @@ class _SwParams(C.Structure):
 
 class _Stats(C.Structure):
     _fields_ = [("admm_iters", C.c_int), ("cg_iters", C.c_int * 64), ("ms_weights", C.c_double),
-                ("ms_kernel_fit", C.c_double), ("ms_pansharpen", C.c_double)]
+                ("ms_kernel_fit", C.c_double), ("ms_pansharpen", C.c_double), ("cg_channel_iters", C.c_longlong)]
 
 
 @dataclass
@@ -178,7 +178,8 @@ class Context:
         s = _Stats()
         _check(_lib.fbmp_gpu_ctx_stats(self.h, C.byref(s)))
         return dict(admm_iters=s.admm_iters, cg_iters=list(s.cg_iters), ms_weights=s.ms_weights,
-                    ms_kernel_fit=s.ms_kernel_fit, ms_pansharpen=s.ms_pansharpen)
+                    ms_kernel_fit=s.ms_kernel_fit, ms_pansharpen=s.ms_pansharpen,
+                    cg_channel_iters=s.cg_channel_iters)
 
 
 _tls = threading.local()

@@ -49,5 +49,6 @@ for r in rows[2:]:
                  f"{r[col['launch__registers_per_thread']]}\n"
                  f"  stalls: " + ", ".join(f"{a} {100 * b / tot:.0f}%" for a, b in top))
 open(out_txt, "w").write("\n".join(lines) + "\n")
+traffic["config"] = sys.argv[4] if len(sys.argv) > 4 else "C2"  # the configuration the capture ran
 json.dump(traffic, open(sys.argv[3] if len(sys.argv) > 3 else "profiles/ncu_traffic.json", "w"), indent=1)
 print("\n".join(lines))

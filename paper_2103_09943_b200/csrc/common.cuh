@@ -221,6 +221,43 @@ __device__ __forceinline__ double block_sum(double v, double* red /* >= NT/32 + 
     return red[NT / 32];
 }
 
+// Two block sums in one pass (same trees as two block_sum calls: identical bits, 3 barriers
+// instead of 6). red: >= 2 (NT/32 + 1) doubles.
+template <int NT>
+__device__ __forceinline__ double2 block_sum2(double a, double b, double* red) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    a = warp_sum(a);
+    b = warp_sum(b);
+    __syncthreads();
+    if (lane == 0) {
+        red[wid] = a;
+        red[NT / 32 + 1 + wid] = b;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        double x = lane < NT / 32 ? red[lane] : 0.0;
+        double y = lane < NT / 32 ? red[NT / 32 + 1 + lane] : 0.0;
+        x = warp_sum(x);
+        y = warp_sum(y);
+        if (lane == 0) {
+            red[NT / 32] = x;
+            red[2 * (NT / 32) + 1] = y;
+        }
+    }
+    __syncthreads();
+    return make_double2(red[NT / 32], red[2 * (NT / 32) + 1]);
+}
+// Two interleaved partial arrays (stride 2) summed in the fixed order of sum_partials.
+template <int NT>
+__device__ __forceinline__ double2 sum_partials2(const double* part, int n, double* red) {
+    double s0 = 0.0, s1 = 0.0;
+    for (int i = threadIdx.x; i < n; i += NT) {
+        s0 += __ldcg(part + 2 * static_cast<size_t>(i));
+        s1 += __ldcg(part + 2 * static_cast<size_t>(i) + 1);
+    }
+    return block_sum2<NT>(s0, s1, red);
+}
+
 // Sum of a partial array in a fixed order (identical bits in every block that calls it).
 template <int NT>
 __device__ __forceinline__ double sum_partials(const double* part, int n, int stride, double* red) {

@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(NTA) k_apply(PsGeo G, const double* __restrict
 __global__ void __launch_bounds__(NTU) k_update(PsGeo G, double* __restrict__ z, double* __restrict__ r,
                                                 const double* __restrict__ pbuf, const double* __restrict__ Ap,
                                                 CgState* st, double* __restrict__ part, int nblk) {
-    __shared__ double red[NTU / 32 + 1];
+    __shared__ double red[2 * (NTU / 32 + 1)];
     const int ch = blockIdx.y;
     // t and z, r, p are not written by K_A (the predecessor): read them before pdl_wait so the
     // loads overlap K_A's tail; done may still be set by K_A (pAp <= 0) and is re-checked
@@ -423,15 +423,14 @@ __global__ void __launch_bounds__(NTU) k_update(PsGeo G, double* __restrict__ z,
             }
         }
     }
-    const double brr = block_sum<NTU>(rr, red);
-    const double bzz = block_sum<NTU>(zz, red);
+    const double2 bs = block_sum2<NTU>(rr, zz, red);
     if (threadIdx.x == 0) {
-        part[(static_cast<size_t>(ch) * nblk + blockIdx.x) * 2] = brr;
-        part[(static_cast<size_t>(ch) * nblk + blockIdx.x) * 2 + 1] = bzz;
+        part[(static_cast<size_t>(ch) * nblk + blockIdx.x) * 2] = bs.x;
+        part[(static_cast<size_t>(ch) * nblk + blockIdx.x) * 2 + 1] = bs.y;
     }
     if (elect_last_block(&st[ch].cnt_u, nblk)) {
-        const double rs_new = sum_partials<NTU>(part + static_cast<size_t>(ch) * nblk * 2, nblk, 2, red);
-        const double zsq = sum_partials<NTU>(part + static_cast<size_t>(ch) * nblk * 2 + 1, nblk, 2, red);
+        const double2 tot = sum_partials2<NTU>(part + static_cast<size_t>(ch) * nblk * 2, nblk, red);
+        const double rs_new = tot.x, zsq = tot.y;
         if (threadIdx.x == 0 && G.dred) {  // distributed: publish the local sums only
             G.dred[G.N + 3 * ch + 1] = rs_new;
             G.dred[G.N + 3 * ch + 2] = zsq;

@@ -25,6 +25,7 @@ namespace fast {
 constexpr int NT = 256;
 
 __host__ __device__ constexpr int pstride(int s) { return s + ((4 - s % 16) + 16) % 16; }
+__host__ __device__ constexpr int cfloordiv(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 
 __device__ __forceinline__ int wrap_once(int a, int m) { return a < 0 ? a + m : (a >= m ? a - m : a); }
 __device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
@@ -747,12 +748,17 @@ __global__ void __launch_bounds__(NT, 2) k_dterm(PsGeo G, const double* __restri
         // each channel
         constexpr int QSZ = Lay::QWP * Lay::QWMAX;
         const int na = __popc(active);
-        for (int e = threadIdx.x; e < na * QN; e += NT) {
-            const int c = e / QN, r = e - c * QN;
-            const int a = r / QW, b = r - a * QW;
+        // the window has the same extent for every tile (origins are multiples of CF): constant
+        // divisors, and its rows / columns wrap at most once
+        constexpr int QWC = cfloordiv(TA - 1 + D::C, CF) - cfloordiv(CF - 1 - D::C, CF) + 1;
+        constexpr int QNC = QWC * QWC;
+        for (int e = threadIdx.x; e < na * QNC; e += NT) {
+            const int c = e / QNC, r = e - c * QNC;
+            const int a = r / QWC, b = r - a * QWC;
             const int chl = ch_lo + static_cast<int>(__fns(active, 0, c + 1));  // c-th active channel
             const double* qc = q + static_cast<size_t>(scene * G.cps + chl) * G.h * G.w;
-            sq[c * QSZ + a * QS + b] = __ldg(qc + static_cast<size_t>(wrapi(iq0 + a, G.h)) * G.w + wrapi(jq0 + b, G.w));
+            sq[c * QSZ + a * QS + b] =
+                __ldg(qc + static_cast<size_t>(wrap_once(iq0 + a, G.h)) * G.w + wrap_once(jq0 + b, G.w));
         }
         __syncthreads();
         constexpr int CW4 = TA / CF, RB4 = CW4 / 4;

@@ -48,7 +48,10 @@ constexpr int NTQ = TQ * TQ;      // threads per K_Q block
 constexpr int TA = 32;            // K_A / K_GF HR tile side
 constexpr int NTA = 256;          // threads per K_A block
 constexpr int NTU = 256;          // threads per K_U block
-constexpr int UPT = 8;            // elements per thread in K_U
+#ifndef FBMP_UPT
+#define FBMP_UPT 8
+#endif
+constexpr int UPT = FBMP_UPT;     // elements per thread in K_U
 
 __host__ __device__ inline int plane_stride(int pw) {  // >= pw*pw and == 4 (mod 16)
     const int s = pw * pw;

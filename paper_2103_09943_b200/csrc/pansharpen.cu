@@ -459,6 +459,53 @@ __global__ void __launch_bounds__(NTU) k_update(PsGeo G, double* __restrict__ z,
     }
 }
 
+// CG initialisation after rhs = B^T U x has been written to r by K_D (pansharpen.cpp:225-235):
+// z = 0, p_old = 0, rs = ||rhs||^2 over the owned rows, state reset.
+__global__ void __launch_bounds__(NTU) k_cg_init(PsGeo G, const double* __restrict__ r, double* __restrict__ z,
+                                                 double* __restrict__ p1, CgState* st, double* __restrict__ part,
+                                                 int nblk, int max_iters, double cg_tol) {
+    __shared__ double red[NTU / 32 + 1];
+    const int ch = blockIdx.y;
+    const size_t P = static_cast<size_t>(G.H) * G.W;
+    const double* rc = r + ch * P;
+    double* zc = z + ch * P;
+    double* pc = p1 + ch * P;
+    const size_t own_lo = static_cast<size_t>(G.rlo) * G.W, own_hi = static_cast<size_t>(G.rhi) * G.W;
+    double ss = 0.0;
+    const size_t base = static_cast<size_t>(blockIdx.x) * NTU * UPT;
+#pragma unroll
+    for (int k = 0; k < UPT; ++k) {
+        const size_t i = base + static_cast<size_t>(k) * NTU + threadIdx.x;
+        if (i < P) {
+            const double v = rc[i];
+            zc[i] = 0.0;
+            pc[i] = 0.0;
+            ss += (i >= own_lo && i < own_hi) ? v * v : 0.0;
+        }
+    }
+    const double bs = block_sum<NTU>(ss, red);
+    if (threadIdx.x == 0) part[static_cast<size_t>(ch) * nblk + blockIdx.x] = bs;
+    if (elect_last_block(&st[ch].cnt_init, nblk)) {
+        const double tot = sum_partials<NTU>(part + static_cast<size_t>(ch) * nblk, nblk, 1, red);
+        if (threadIdx.x == 0 && G.dred) {  // distributed: publish the local sum only
+            G.dred[G.N + 3 * ch + 1] = tot;
+            st[ch].cnt_init = 0;
+        } else if (threadIdx.x == 0) {
+            CgState& S = st[ch];
+            S.rs = tot;
+            S.rhs_norm = sqrt(tot);
+            S.pp = S.pAp = S.alpha = S.beta = S.zz = 0.0;
+            S.cg_tol = cg_tol;
+            S.t = 0;
+            S.iters = 0;
+            S.max_iters = max_iters;
+            S.done = (S.rhs_norm == 0.0) ? 1 : (max_iters <= 0 ? 3 : 0);
+            S.cnt_q = S.cnt_a = S.cnt_u = 0;
+            S.cnt_init = 0;
+        }
+    }
+}
+
 // ------------------------------------------------------------------------------------------
 // rhs = B^T U x and CG initialisation (pansharpen.cpp:225-235).
 // ------------------------------------------------------------------------------------------
@@ -1058,6 +1105,23 @@ void launch_llp(Context& ctx, const PsGeo& G, const double* taps, const double* 
                                                                               L.nb, L.k, L.R);
 }
 
+// rhs = B^T U x into r through K_D, then the CG initialisation (fast path; k_rhs otherwise)
+void launch_rhs_init(Context& ctx, const PsGeo& G, const double* taps, const double* x, CgBuffers& B, double* part,
+                     int max_iters, double cg_tol) {
+    const int S = (G.N + G.cps - 1) / G.cps;
+    const int nba = ceil_div(G.W, fast::a4::TA) * ceil_div(G.H, fast::a4::TA);
+    const int groups = (G.cps + G.cpc - 1) / G.cpc;
+    const auto fd = dterm_select<false>(G);
+    set_smem(fd.first, fd.second);
+    fd.first<<<dim3(nba, S * groups), fast::NT, fd.second, ctx.stream>>>(G, taps, x, B.r, nullptr);
+    const size_t P = static_cast<size_t>(G.H) * G.W;
+    const int nbu = static_cast<int>((P + static_cast<size_t>(NTU) * UPT - 1) / (static_cast<size_t>(NTU) * UPT));
+    k_cg_init<<<dim3(nbu, G.N), NTU, 0, ctx.stream>>>(G, B.r, B.z, B.p + static_cast<size_t>(G.N) * P, B.st, part,
+                                                     nbu, max_iters, cg_tol);
+    ctx.count(2);
+    check_launch();
+}
+
 template <bool CG>
 void launch_apply2(Context& ctx, const PsGeo& G, const double* taps, const double* guide, const double* mu,
                    const double* gk, const double* p, const double* q, double* out, CgState* st, double* part,
@@ -1183,10 +1247,14 @@ void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* 
     double* part_u = part_a + static_cast<size_t>(N) * nbA;
     // counters must start at zero
     FBMP_CUDA(cudaMemsetAsync(B.st, 0, sizeof(CgState) * N, ctx.stream));
-    k_rhs<true><<<dim3(nba, N), NTA, sr, ctx.stream>>>(G, d_taps, d_x, B.r, B.z, B.p + static_cast<size_t>(N) * P,
-                                                       B.st, part_init, nba, max_iters, cg_tol);
-    ctx.count();
-    check_launch();
+    if (fastA && use_llp()) {
+        launch_rhs_init(ctx, G, d_taps, d_x, B, part_init, max_iters, cg_tol);
+    } else {
+        k_rhs<true><<<dim3(nba, N), NTA, sr, ctx.stream>>>(G, d_taps, d_x, B.r, B.z, B.p + static_cast<size_t>(N) * P,
+                                                           B.st, part_init, nba, max_iters, cg_tol);
+        ctx.count();
+        check_launch();
+    }
 
     // One CUDA graph holds `chunk` iterations (3 kernels each); kernels of finished channels
     // exit at their first instruction, so the host only polls the flags between graphs.
@@ -1652,10 +1720,7 @@ void cg_solve_strips(Context& ctx, std::vector<StripCg>& SS, const StripComm& co
         FBMP_CUDA(cudaMemsetAsync(S.B.st, 0, sizeof(CgState) * N, ctx.stream));
         double *pi, *pq, *pa, *pu;
         parts(S, pi, pq, pa, pu);
-        k_rhs<true><<<dim3(nba, N), NTA, sr, ctx.stream>>>(S.G, S.taps, S.x, S.B.r, S.B.z, S.B.p + static_cast<size_t>(N) * P,
-                                                            S.B.st, pi, nba, max_iters, cg_tol);
-        ctx.count();
-        check_launch();
+        launch_rhs_init(ctx, S.G, S.taps, S.x, S.B, pi, max_iters, cg_tol);
     }
     allreduce(N, 3 * N);
     for (auto& S : SS) {

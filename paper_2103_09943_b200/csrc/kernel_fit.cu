@@ -526,6 +526,55 @@ __global__ void __launch_bounds__(NT) k_trtri(const double* __restrict__ M, int 
     for (int i = lane; i < N; i += 32) Li[static_cast<size_t>(i) * N + j] = y[i];
 }
 
+// Same forward substitution with the next row of L in flight while the current one is reduced
+// (the chain over rows is latency-bound on L2 loads otherwise). KL = ceil(N / 32) values per lane.
+template <int KL>
+__global__ void __launch_bounds__(NT) k_trtri_pf(const double* __restrict__ M, int N, double* __restrict__ Linv,
+                                                 const int* __restrict__ status) {
+    extern __shared__ double ys[];
+    const int s = blockIdx.y;
+    if (status[s]) return;
+    const double* L = M + static_cast<size_t>(s) * N * N;
+    double* Li = Linv + static_cast<size_t>(s) * N * N;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int j = blockIdx.x * (NT / 32) + warp;
+    if (j >= N) return;
+    double* y = ys + warp * N;
+    for (int i = lane; i < N; i += 32) y[i] = 0.0;
+    __syncwarp();
+    if (lane == 0) y[j] = 1.0 / L[static_cast<size_t>(j) * N + j];
+    __syncwarp();
+    // row i, columns k = j + lane + 32 t (t < KL)
+    double cur[KL], nxt[KL];
+    double dcur = 0.0, dnxt = 0.0;
+    auto load = [&](int i, double (&v)[KL], double& d) {
+        const double* row = L + static_cast<size_t>(i) * N;
+#pragma unroll
+        for (int t = 0; t < KL; ++t) {
+            const int k = j + lane + 32 * t;
+            v[t] = k < i ? __ldg(row + k) : 0.0;
+        }
+        d = __ldg(row + i);
+    };
+    if (j + 1 < N) load(j + 1, cur, dcur);
+    for (int i = j + 1; i < N; ++i) {
+        if (i + 1 < N) load(i + 1, nxt, dnxt);
+        double acc = 0.0;
+#pragma unroll
+        for (int t = 0; t < KL; ++t) {
+            const int k = j + lane + 32 * t;
+            if (k < i) acc = fma(cur[t], y[k], acc);
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) y[i] = -acc / dcur;
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < KL; ++t) cur[t] = nxt[t];
+        dcur = dnxt;
+    }
+    for (int i = lane; i < N; i += 32) Li[static_cast<size_t>(i) * N + j] = y[i];
+}
+
 // Ginv[a][b] = sum_k Linv[k][a] Linv[k][b] (a >= b), mirrored -> exactly symmetric
 __global__ void __launch_bounds__(NT) k_inv_gram(const double* __restrict__ Linv, int N, double* __restrict__ Ginv,
                                                  const int* __restrict__ status) {
@@ -1370,8 +1419,11 @@ void build_observation(Context& ctx, const double* d_pan, const double* d_obs, i
     if (!want_inverse) return;
     double* Linv = ctx.scratch<double>("obs_Linv", S * NN);
     const size_t smT = static_cast<size_t>(NT / 32) * N * sizeof(double);
-    set_smem(k_trtri, smT);
-    k_trtri<<<dim3(ceil_div(N, NT / 32), S), NT, smT, ctx.stream>>>(sys.M, N, Linv, sys.status);
+    const int KL = ceil_div(N, 32);
+    auto tfn = KL <= 4 ? k_trtri_pf<4> : KL <= 8 ? k_trtri_pf<8> : KL <= 10 ? k_trtri_pf<10> : KL <= 14 ? k_trtri_pf<14>
+                                                                                                   : k_trtri_pf<27>;
+    set_smem(tfn, smT);
+    tfn<<<dim3(ceil_div(N, NT / 32), S), NT, smT, ctx.stream>>>(sys.M, N, Linv, sys.status);
     const int nt = ceil_div(N, NBK);
     k_inv_gram<<<dim3(nt * (nt + 1) / 2, S), NT, 0, ctx.stream>>>(Linv, N, sys.Ginv, sys.status);
     ctx.count(2);

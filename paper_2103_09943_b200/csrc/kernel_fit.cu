@@ -680,11 +680,13 @@ __device__ __forceinline__ void cst2(double* base, int e, double re, double im) 
 }
 
 // forward 2-D DFT of 3 real n x n planes (src[f]) -> spec (3 interleaved complex planes).
+// Real input: only the columns kc <= n/2 of the spectrum are formed (the rest is the Hermitian
+// mirror); the {u,p} solve and the inverse use that half only.
 // One thread per output bin computes all three fields, sharing twiddles and index updates.
 __device__ void dft3_forward(const AdmmSmem& S, int n, const double* const src[3]) {
-    const int m = n * n;
-    for (int e = threadIdx.x; e < m; e += blockDim.x) {  // rows: T[r][kc] = sum_c x[r][c] w^(kc c)
-        const int r = e / n, kc = e - r * n;
+    const int m = n * n, nh = n / 2 + 1;  // columns 0..n/2 (Nyquist included for even n)
+    for (int e = threadIdx.x; e < n * nh; e += blockDim.x) {  // rows: T[r][kc] = sum_c x[r][c] w^(kc c)
+        const int r = e / nh, kc = e - r * nh;
         const double *x0 = src[0] + r * n, *x1 = src[1] + r * n, *x2 = src[2] + r * n;
         double re0 = 0.0, im0 = 0.0, re1 = 0.0, im1 = 0.0, re2 = 0.0, im2 = 0.0;
         int idx = 0;
@@ -696,13 +698,14 @@ __device__ void dft3_forward(const AdmmSmem& S, int n, const double* const src[3
             idx += kc;
             if (idx >= n) idx -= n;
         }
-        cst2(S.rowt, e, re0, im0);
-        cst2(S.rowt, m + e, re1, im1);
-        cst2(S.rowt, 2 * m + e, re2, im2);
+        const int o = r * n + kc;
+        cst2(S.rowt, o, re0, im0);
+        cst2(S.rowt, m + o, re1, im1);
+        cst2(S.rowt, 2 * m + o, re2, im2);
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < m; e += blockDim.x) {  // cols: F[kr][kc] = sum_r T[r][kc] w^(kr r)
-        const int kr = e / n, kc = e - kr * n;
+    for (int e = threadIdx.x; e < n * nh; e += blockDim.x) {  // cols: F[kr][kc] = sum_r T[r][kc] w^(kr r)
+        const int kr = e / nh, kc = e - kr * nh;
         double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
         int idx = 0;
         for (int r = 0; r < n; ++r) {
@@ -718,51 +721,63 @@ __device__ void dft3_forward(const AdmmSmem& S, int n, const double* const src[3
             if (idx >= n) idx -= n;
         }
 #pragma unroll
-        for (int f = 0; f < 3; ++f) cst2(S.spec, f * m + e, acc[f][0], acc[f][1]);
+        for (int f = 0; f < 3; ++f) cst2(S.spec, f * m + kr * n + kc, acc[f][0], acc[f][1]);
     }
     __syncthreads();
 }
 
-// inverse 2-D DFT of spec -> dst[f] = Re(.) / m  (fft_util.cpp:47-56)
+// inverse 2-D DFT of the half spectrum -> dst[f] = Re(.) / m  (fft_util.cpp:47-56): first over kr
+// for the columns kc <= (n-1)/2, then the real inverse over kc using the Hermitian mirror:
+// x = (Re H[0] + 2 sum_{kc >= 1} Re(H[kc] w^(-kc c))) / m.
 __device__ void dft3_inverse(const AdmmSmem& S, int n, double* const dst[3]) {
-    const int m = n * n;
-    for (int e = threadIdx.x; e < m; e += blockDim.x) {  // rows over kc
-        const int kr = e / n, c = e - kr * n;
+    const int m = n * n, K2 = (n - 1) / 2, nh = n / 2 + 1;
+    for (int e = threadIdx.x; e < n * nh; e += blockDim.x) {  // H[r][kc] = sum_kr F[kr][kc] w^(-kr r)
+        const int r = e / nh, kc = e - r * nh;
         double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
         int idx = 0;
-        for (int kc = 0; kc < n; ++kc) {
+        for (int kr = 0; kr < n; ++kr) {
             const double wc = S.twc[idx], wsn = S.tws[idx];
 #pragma unroll
             for (int f = 0; f < 3; ++f) {
                 const double2 fv = cld2(S.spec, f * m + kr * n + kc);
-                const double fr = fv.x, fi = fv.y;
-                acc[f][0] = fma(fr, wc, fma(-fi, wsn, acc[f][0]));
-                acc[f][1] = fma(fr, wsn, fma(fi, wc, acc[f][1]));
-            }
-            idx += c;
-            if (idx >= n) idx -= n;
-        }
-#pragma unroll
-        for (int f = 0; f < 3; ++f) cst2(S.rowt, f * m + e, acc[f][0], acc[f][1]);
-    }
-    __syncthreads();
-    const double inv = 1.0 / static_cast<double>(m);
-    for (int e = threadIdx.x; e < m; e += blockDim.x) {  // cols, real part only
-        const int r = e / n, c = e - r * n;
-        double re[3] = {0.0, 0.0, 0.0};
-        int idx = 0;
-        for (int kr = 0; kr < n; ++kr) {
-            const double wc = S.twc[idx], ws = S.tws[idx];
-#pragma unroll
-            for (int f = 0; f < 3; ++f) {
-                const double2 rv = cld2(S.rowt, f * m + kr * n + c);
-                re[f] = fma(rv.x, wc, fma(-rv.y, ws, re[f]));
+                acc[f][0] = fma(fv.x, wc, fma(-fv.y, wsn, acc[f][0]));
+                acc[f][1] = fma(fv.x, wsn, fma(fv.y, wc, acc[f][1]));
             }
             idx += r;
             if (idx >= n) idx -= n;
         }
 #pragma unroll
-        for (int f = 0; f < 3; ++f) dst[f][e] = re[f] * inv;
+        for (int f = 0; f < 3; ++f) cst2(S.rowt, f * m + r * n + kc, acc[f][0], acc[f][1]);
+    }
+    __syncthreads();
+    const double inv = 1.0 / static_cast<double>(m);
+    for (int e = threadIdx.x; e < m; e += blockDim.x) {  // real inverse over kc
+        const int r = e / n, c = e - r * n;
+        double re[3];
+#pragma unroll
+        for (int f = 0; f < 3; ++f) re[f] = 0.0;
+        int idx = c;
+        for (int kc = 1; kc <= K2; ++kc) {
+            const double wc = S.twc[idx], ws = S.tws[idx];
+#pragma unroll
+            for (int f = 0; f < 3; ++f) {
+                const double2 hv = cld2(S.rowt, f * m + r * n + kc);
+                re[f] = fma(hv.x, wc, fma(-hv.y, ws, re[f]));
+            }
+            idx += c;
+            if (idx >= n) idx -= n;
+        }
+        double ny[3] = {0.0, 0.0, 0.0};  // even n: the Nyquist column counts once
+        if ((n & 1) == 0) {
+            const int ix = (c * (n / 2)) % n;
+#pragma unroll
+            for (int f = 0; f < 3; ++f) {
+                const double2 hv = cld2(S.rowt, f * m + r * n + n / 2);
+                ny[f] = hv.x * S.twc[ix] - hv.y * S.tws[ix];
+            }
+        }
+#pragma unroll
+        for (int f = 0; f < 3; ++f) dst[f][e] = (cld2(S.rowt, f * m + r * n).x + 2.0 * re[f] + ny[f]) * inv;
     }
     __syncthreads();
 }
@@ -824,7 +839,9 @@ __device__ void up_solve(const AdmmSmem& S, int n, double a1m1, double a2m2, dou
         }
         tol = 1e-12 * block_max(dmax, S.red);
     }
-    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    const int nh = n / 2 + 1;
+    for (int e = threadIdx.x; e < n * nh; e += blockDim.x) {  // half spectrum (real fields)
+        const int i = (e / nh) * n + (e % nh);
         double sy[11];
         if (S.sym) {
 #pragma unroll

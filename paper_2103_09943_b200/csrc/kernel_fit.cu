@@ -953,32 +953,25 @@ __device__ int project_simplex_block(const double* v, double* out, int m, double
 // qualifying position by a block max. scratch: 3 * NTADMM doubles.
 __device__ int project_simplex_sorted(const double* v, double* out, int m, double* red, int* ired, double* scratch) {
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    // values only: equal values are interchangeable in the running sums, so no index tie-break
     double* kv[2] = {scratch, scratch + NTADMM};
-    int* ki[2] = {reinterpret_cast<int*>(scratch + 2 * NTADMM), reinterpret_cast<int*>(scratch + 2 * NTADMM) + NTADMM};
     double val = t < m ? v[t] : -INFINITY;
-    int idx = t;
     int buf = 0;
     for (int k = 2; k <= NTADMM; k <<= 1) {
         for (int j = k >> 1; j > 0; j >>= 1) {
             double pv;
-            int pi;
             if (j >= 32) {
                 kv[buf][t] = val;
-                ki[buf][t] = idx;
                 __syncthreads();
                 pv = kv[buf][t ^ j];
-                pi = ki[buf][t ^ j];
                 buf ^= 1;  // the next exchange writes the other buffer: one barrier per stage
             } else {
                 pv = __shfl_xor_sync(0xffffffffu, val, j);
-                pi = __shfl_xor_sync(0xffffffffu, idx, j);
             }
-            const bool own_first = val > pv || (val == pv && idx < pi);
+            // keep the larger value on the lower position of an ascending block (descending sort)
             const bool want_first = ((t & j) == 0) == ((t & k) == 0);
-            if (own_first != want_first) {
-                val = pv;
-                idx = pi;
-            }
+            const bool own_first = val > pv;
+            if (own_first != want_first) val = pv;
         }
     }
     // thread t holds the t-th largest value; inclusive scan in sorted order

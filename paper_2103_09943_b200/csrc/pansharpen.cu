@@ -1426,7 +1426,7 @@ void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* 
     };
     auto launch = [&](int slot) {
         FBMP_CUDA(cudaGraphLaunch(exec, ctx.stream));
-        ctx.count(3 * chunk);
+        ctx.count((fastA && use_llp() ? 4 : 3) * chunk * ngrp);  // kernel nodes of one chunk graph
         FBMP_CUDA(cudaMemcpyAsync(pinned + slot * N, B.st, sizeof(CgState) * N, cudaMemcpyDeviceToHost, ctx.stream));
         FBMP_CUDA(cudaEventRecord(ev[slot], ctx.stream));
     };

@@ -22,6 +22,8 @@
 #include <cmath>
 #include <complex>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <functional>
@@ -50,6 +52,11 @@ struct Failure : std::runtime_error {
 [[noreturn]] void num_error(const std::string& m) { throw Failure(3, m); }
 
 thread_local std::string g_last_error;
+
+bool trace_cg() {
+    static const bool on = std::getenv("FBMP_ORACLE_TRACE") != nullptr;
+    return on;
+}
 
 // ---- sequential reductions: image.hpp:50-55 (sum), 93-98 (dot), 66-70 (norm) ----------
 double seq_dot(const double* a, const double* b, size_t n) {
@@ -434,6 +441,9 @@ vec warmstart_cg(const double* x, int h, int w, const double* k, int n, int fact
         for (size_t i = 0; i < P; ++i) r[i] -= Ap[i] * alpha;
         const double step = std::abs(alpha) * seq_norm(p.data(), P);
         const double rs_new = seq_dot(r.data(), r.data(), P);
+        if (trace_cg())  // FBMP_ORACLE_TRACE: the stop-test margin of every iteration (debugging aid)
+            std::fprintf(stderr, "cg it %d step/(tol |z|) %.17g\n", it + 1,
+                         step / (prm.cg_tol * std::max(seq_norm(z.data(), P), 1e-300)));
         if (step <= prm.cg_tol * std::max(seq_norm(z.data(), P), 1e-300)) { converged = true; break; }
         const double beta = rs_new / rs;
         for (size_t i = 0; i < P; ++i) p[i] = r[i] + p[i] * beta;

@@ -116,6 +116,10 @@ void pansharpen_device(Context& ctx, const double* d_lrms, int S, int N, int h, 
     cg_solve(ctx, G, d_taps, lpan, xn, B, prm.cg_max_iter, prm.cg_tol, hs);
     cg_iters.assign(NC, 0);
     for (int i = 0; i < NC; ++i) cg_iters[i] = hs[i].iters;
+    if (std::getenv("FBMP_CG_DEBUG"))  // final CG scalars per channel (debugging aid)
+        for (int i = 0; i < NC; ++i)
+            std::fprintf(stderr, "cg ch %d it %d pp %.17g alpha %.17g zz %.17g rs %.17g\n", i, hs[i].iters, hs[i].pp,
+                         hs[i].alpha, hs[i].zz, hs[i].rs);
     for (int i = 0; i < NC; ++i) {  // first failing channel in index order (pansharpen.cpp:421-422)
         const std::string tag = "channel " + std::to_string(ch0 + i % NS) + ": ";
         if (hs[i].done == 2)

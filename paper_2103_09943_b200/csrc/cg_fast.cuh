@@ -253,6 +253,316 @@ inline int q2_blocks(const PsGeo& G) {
 }
 
 // ------------------------------------------------------------------------------------------
+// K_Q3 (factor 4): the same q = D B p (+ p update, ||p||^2) as K_Q2, streamed by HR rows.
+//
+// q(i, j) = sum_{a, b in [-C, C]} k[a + C][b + C] p(4i - a, 4j - b). HR row y = 4s + w (superrow
+// s, phase w) feeds the LR rows i = s + d with a = 4d - w in [-C, C] (4 or 5 of them), each by a
+// horizontal 17-tap (n-tap) product. A CTA owns a band of TWL = 32 MJ LR columns and a strip of
+// LR rows; warp w owns the HR rows of phase w and keeps the partial sums of its open LR rows in
+// registers, so an HR row is read from HBM once per band and never revisited. Rows arrive by
+// TMA bulk copies (one elected lane, mbarrier per ring slot, D rows ahead); the lane computes
+// p = r + beta p_old on the staged row, writes the owned part of p, and splits the row into four
+// column-phase planes in shared memory, from which it reads its MJ columns' windows with 16-byte
+// loads. A finished LR row is the sum of the four warps' partials (fixed order), formed after the
+// superrow's block barrier. Shared memory per CTA ~72 KB (n = 17, MJ = 2, D = 3) against K_Q2's
+// 99 KB, and the strip height is chosen by the host to fill the SMs.
+// ------------------------------------------------------------------------------------------
+#ifndef FBMP_KQ3_D
+#define FBMP_KQ3_D 3
+#endif
+#ifndef FBMP_KQ3_PCU
+#define FBMP_KQ3_PCU 2
+#endif
+#ifndef FBMP_KQ3_MINB
+#define FBMP_KQ3_MINB 3  // CTAs per SM the register budget is sized for
+#endif
+namespace q3 {
+constexpr int KQ3_PCU = FBMP_KQ3_PCU;  // unroll of the column-phase loop
+constexpr int NW = 4;  // warps per CTA = HR row phases
+constexpr int NTH = 32 * NW;
+template <int N_, int MJ>
+struct Geo {
+    static constexpr int C = (N_ - 1) / 2;
+    static constexpr int g = (C + 3) / 4;             // ceil(C / 4)
+    static constexpr int gp = C / 4;                  // floor(C / 4)
+    static constexpr int TWL = 32 * MJ;               // LR columns per band
+    static constexpr int JW = TWL + 2 * g;            // phase-plane width (LR units)
+    static constexpr int RW = 4 * JW;                 // HR columns of a staged row
+    static constexpr int NV = MJ + g + gp;            // plane values a lane reads per phase
+    static constexpr int NVP = (NV + 1) & ~1;         // rounded up to 16-byte pairs
+    static constexpr int PLS = (JW + 1) & ~1;         // plane stride (>= the NVP over-read)
+    static constexpr int D = FBMP_KQ3_D;              // ring depth (rows per warp)
+    static constexpr int K = g + 2 <= 4 ? 4 : 8;      // partial-row slots (>= g + 2, power of 2)
+    static constexpr int KOFF = ((N_ * N_ + 1) / 2) * 2;
+    static constexpr int O_RING = KOFF;                   // NW x D x {r, p_old} x RW
+    static constexpr int O_PL = O_RING + NW * D * 2 * RW; // NW x 4 x PLS
+    static constexpr int O_SLOT = O_PL + NW * 4 * PLS;    // K x NW x TWL
+    static constexpr int O_BAR = O_SLOT + K * NW * TWL;   // NW x D mbarriers
+    static constexpr size_t smem = static_cast<size_t>(O_BAR + NW * D) * sizeof(double);
+    static_assert(TWL - MJ + NVP <= PLS, "plane over-read");
+};
+
+__device__ __forceinline__ unsigned int saddr(const void* p) {
+    return static_cast<unsigned int>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned int cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned int bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned int parity) {
+    asm volatile(
+        "{\n .reg .pred P;\n"
+        "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n @!P bra WAIT_%=;\n}\n" ::"r"(saddr(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void bulk_g2s(double* dst, const double* src, unsigned int bytes, unsigned long long* b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     saddr(dst)),
+                 "l"(src), "r"(bytes), "r"(saddr(b))
+                 : "memory");
+}
+
+struct Args {
+    const double* rc;    // r (CG) or p (operator) plane of the channel
+    const double* pold;  // p_old plane (CG)
+    double* pnew;        // p plane written (CG)
+    double* qc;          // q plane of the channel
+    double beta;
+    int H, W, h, w, rlo, rhi;
+    int i0, i1, j0;      // strip rows [i0, i1), band origin
+    int s0, s1;          // superrows
+};
+
+// one warp's stream of HR rows y = 4 s + WP, s in [s0, s1)
+template <int N_, int MJ, bool CG, int WP>
+__device__ __forceinline__ double rows(const Args& A, const double* __restrict__ sk, double* ring, double* pl,
+                                       double* slots, unsigned long long* bar, int lane, int warp) {
+    using Q = Geo<N_, MJ>;
+    constexpr int C = Q::C, g = Q::g, gp = Q::gp, RW = Q::RW, PLS = Q::PLS, TWL = Q::TWL, D = Q::D, K = Q::K;
+    constexpr int DMIN = -((C - WP) / 4);  // ceil((WP - C) / 4)
+    constexpr int DMAX = (WP + C) / 4;
+    constexpr int NA = DMAX - DMIN + 1;
+    const int H = A.H, W = A.W;
+    const int col0 = 4 * (A.j0 - g);
+    const unsigned int row_bytes = (CG ? 2u : 1u) * RW * sizeof(double);
+    const int yo0 = 4 * A.i0, yo1 = min(4 * A.i1, H);
+    const int xo_hi = min(4 * TWL, W - 4 * A.j0);
+    // the column split of a staged row at the periodic wrap is the same for every row: at most
+    // three pieces [start, start + len) of the image row, computed once
+    int pst[3], plen[3], np_ = 0;
+    {
+        int start = col0 % W;
+        if (start < 0) start += W;
+        for (int rem = RW; rem > 0 && np_ < 3; ++np_) {
+            const int len = min(rem, W - start);
+            pst[np_] = start;
+            plen[np_] = len;
+            rem -= len;
+            start = 0;
+        }
+    }
+    auto issue = [&](int s, int slot) {  // lane 0: TMA bulk copies of the row
+        int yw = (4 * s + WP) % H;
+        if (yw < 0) yw += H;
+        mbar_expect_tx(bar + slot, row_bytes);
+#pragma unroll
+        for (int a = 0; a < (CG ? 2 : 1); ++a) {
+            const double* srow = (a == 0 ? A.rc : A.pold) + static_cast<size_t>(yw) * W;
+            double* dst = ring + (slot * 2 + a) * RW;
+            int off = 0;
+            for (int k = 0; k < np_; ++k) {
+                bulk_g2s(dst + off, srow + pst[k], static_cast<unsigned int>(plen[k]) * sizeof(double), bar + slot);
+                off += plen[k];
+            }
+        }
+    };
+    if (lane == 0) {
+        for (int k = 0; k < D; ++k)
+            if (A.s0 + k < A.s1) issue(A.s0 + k, k);
+    }
+    double acc[NA][MJ];
+#pragma unroll
+    for (int d = 0; d < NA; ++d)
+#pragma unroll
+        for (int m = 0; m < MJ; ++m) acc[d][m] = 0.0;
+    double pp = 0.0;
+    const double* plb = pl + MJ * lane;
+    for (int s = A.s0; s < A.s1; ++s) {
+        const int k = s - A.s0;
+        const int slot = k % D;
+        mbar_wait(bar + slot, static_cast<unsigned int>((k / D) & 1));
+        const int y = 4 * s + WP;
+        const double* rr = ring + slot * 2 * RW;
+        // p = r + beta p_old on the staged row; owned part -> p, all of it -> phase planes
+        {
+            const bool own_row = CG && y >= yo0 && y < yo1;
+            const bool dot_row = own_row && y >= A.rlo && y < A.rhi;
+            double* prow = nullptr;
+            if (CG) prow = A.pnew + static_cast<size_t>(own_row ? y : 0) * W + 4 * A.j0 - 4 * g;
+#pragma unroll
+            for (int kk = 0; kk < (RW + 63) / 64; ++kk) {
+                const int e = 2 * lane + 64 * kk;
+                if (e < RW) {
+                    double2 v = ld2(rr + e);
+                    if (CG) {
+                        const double2 o = ld2(rr + RW + e);
+                        v.x = v.x + o.x * A.beta;  // pansharpen.cpp:254
+                        v.y = v.y + o.y * A.beta;
+                        const int xr = e - 4 * g;
+                        if (own_row && xr >= 0 && xr < xo_hi) {
+                            st2(prow + e, v);
+                            if (dot_row) {
+                                pp += v.x * v.x;
+                                pp += v.y * v.y;
+                            }
+                        }
+                    }
+                    pl[(e & 3) * PLS + (e >> 2)] = v.x;
+                    pl[((e & 3) + 1) * PLS + (e >> 2)] = v.y;
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0 && s + D < A.s1) {  // the slot is free again: stage the row D superrows ahead
+            fence_proxy_async();
+            issue(s + D, slot);
+        }
+        // contributions of row y to LR rows s + d, d in [DMIN, DMAX]
+#pragma unroll KQ3_PCU
+        for (int pc = 0; pc < 4; ++pc) {
+            double v[Q::NVP];
+#pragma unroll
+            for (int o = 0; o < Q::NVP; o += 2) {
+                const double2 t2 = ld2(plb + pc * PLS + o);
+                v[o] = t2.x;
+                v[o + 1] = t2.y;
+            }
+            // every accumulator sees (pc, u) in ascending order; consecutive FMAs go to different
+            // accumulators (independent chains)
+#pragma unroll
+            for (int u = -g; u <= gp; ++u) {
+                const int b = -(4 * u + pc);
+                if (b >= -C && b <= C) {
+#pragma unroll
+                    for (int d = DMIN; d <= DMAX; ++d) {
+                        const double kv = sk[(4 * d - WP + C) * N_ + (b + C)];
+#pragma unroll
+                        for (int m = 0; m < MJ; ++m) acc[d - DMIN][m] = fma(kv, v[m + g + u], acc[d - DMIN][m]);
+                    }
+                }
+            }
+        }
+        // LR row s + DMIN is complete for this warp: publish its partial, shift the window
+        {
+            double* sl = slots + ((s + DMIN) & (K - 1)) * (NW * TWL) + WP * TWL + MJ * lane;
+#pragma unroll
+            for (int m = 0; m < MJ; m += 2) st2(sl + m, make_double2(acc[0][m], acc[0][m + 1]));
+#pragma unroll
+            for (int d = 0; d + 1 < NA; ++d)
+#pragma unroll
+                for (int m = 0; m < MJ; ++m) acc[d][m] = acc[d + 1][m];
+#pragma unroll
+            for (int m = 0; m < MJ; ++m) acc[NA - 1][m] = 0.0;
+        }
+        __syncthreads();
+        // LR row s - g has all four partials
+        const int i = s - g;
+        if (warp == (s & 3) && i >= A.i0 && i < A.i1) {
+            const double* sb = slots + (i & (K - 1)) * (NW * TWL) + MJ * lane;
+            const int j = A.j0 + MJ * lane;
+#pragma unroll
+            for (int m = 0; m < MJ; m += 2) {
+                const double2 a0 = ld2(sb + m), a1 = ld2(sb + TWL + m), a2 = ld2(sb + 2 * TWL + m),
+                              a3 = ld2(sb + 3 * TWL + m);
+                const double2 val = make_double2(((a0.x + a1.x) + a2.x) + a3.x, ((a0.y + a1.y) + a2.y) + a3.y);
+                if (j + m + 1 < A.w) st2(A.qc + static_cast<size_t>(i) * A.w + j + m, val);
+                else if (j + m < A.w) A.qc[static_cast<size_t>(i) * A.w + j + m] = val.x;
+            }
+        }
+    }
+    return pp;
+}
+}  // namespace q3
+
+template <int N_, int MJ, bool CG>
+__global__ void __launch_bounds__(q3::NTH, FBMP_KQ3_MINB) k_q3(PsGeo G, const double* __restrict__ taps,
+                                                   const double* __restrict__ src, double* __restrict__ pbuf,
+                                                   double* __restrict__ q, CgState* st, double* __restrict__ part,
+                                                   int nblk) {
+    using Q = q3::Geo<N_, MJ>;
+    __shared__ double red[q3::NW + 1];
+    extern __shared__ __align__(16) double sm[];
+    const int ch = blockIdx.y;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const double* tp = taps + static_cast<size_t>(ch / G.cps) * N_ * N_;
+    for (int e = threadIdx.x; e < N_ * N_; e += q3::NTH) sm[e] = tp[e];
+    q3::Args A;
+    A.beta = 0.0;
+    int t = 0;
+    if (CG) {
+        pdl_wait();  // r, beta and the flags come from K_U
+        pdl_trigger();
+        if (st[ch].done) return;
+        t = st[ch].t;
+        A.beta = t ? st[ch].beta : 0.0;
+    }
+    A.H = G.H;
+    A.W = G.W;
+    A.h = G.h;
+    A.w = G.w;
+    A.rlo = G.rlo;
+    A.rhi = G.rhi;
+    const size_t P = static_cast<size_t>(G.H) * G.W;
+    A.rc = src + ch * P;
+    A.pold = CG ? pbuf + (static_cast<size_t>((t + 1) & 1) * G.N + ch) * P : nullptr;
+    A.pnew = CG ? pbuf + (static_cast<size_t>(t & 1) * G.N + ch) * P : nullptr;
+    A.qc = q + static_cast<size_t>(ch) * G.h * G.w;
+    const int nbands = (G.w + Q::TWL - 1) / Q::TWL;
+    const int nstrips = nblk / nbands;
+    const int SR = (G.h + nstrips - 1) / nstrips;
+    const int band = blockIdx.x % nbands, strip = blockIdx.x / nbands;
+    A.j0 = band * Q::TWL;
+    A.i0 = strip * SR;
+    A.i1 = min(A.i0 + SR, G.h);
+    A.s0 = A.i0 - Q::g;
+    A.s1 = A.i1 + Q::g;
+    if (A.i1 <= A.i0) A.s1 = A.s0;  // empty strip: no rows, still counted in the p.p election
+    double* ring = sm + Q::O_RING + warp * (Q::D * 2 * Q::RW);
+    double* pl = sm + Q::O_PL + warp * 4 * Q::PLS;
+    double* slots = sm + Q::O_SLOT;
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + Q::O_BAR) + warp * Q::D;
+    if (lane == 0) {
+        for (int k = 0; k < Q::D; ++k) q3::mbar_init(bar + k, 1);
+        q3::mbar_fence_init();
+    }
+    __syncthreads();  // taps and barriers
+    double pp;
+    switch (warp) {
+    case 0: pp = q3::rows<N_, MJ, CG, 0>(A, sm, ring, pl, slots, bar, lane, warp); break;
+    case 1: pp = q3::rows<N_, MJ, CG, 1>(A, sm, ring, pl, slots, bar, lane, warp); break;
+    case 2: pp = q3::rows<N_, MJ, CG, 2>(A, sm, ring, pl, slots, bar, lane, warp); break;
+    default: pp = q3::rows<N_, MJ, CG, 3>(A, sm, ring, pl, slots, bar, lane, warp); break;
+    }
+    if (CG) {
+        const double bs = block_sum<q3::NTH>(pp, red);
+        if (threadIdx.x == 0) part[static_cast<size_t>(ch) * nblk + blockIdx.x] = bs;
+        if (elect_last_block(&st[ch].cnt_q, nblk)) {
+            const double tot = sum_partials<q3::NTH>(part + static_cast<size_t>(ch) * nblk, nblk, 1, red);
+            if (threadIdx.x == 0) {
+                if (G.dred) G.dred[G.N + 3 * ch] = tot;
+                else st[ch].pp = tot;
+                st[ch].cnt_q = 0;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
 // K_A (radius 1): one CTA = one 32 x 32 output tile x the channels [group*cpc, +cpc) of a scene
 // ------------------------------------------------------------------------------------------
 namespace a4 {

@@ -976,9 +976,59 @@ QLaunch q2_make(const PsGeo& G) {
     L.threads = fast::QGeo<N_, CF>::NTH;
     return L;
 }
+// K_Q3 strip plan: LR-row strips of SR rows per band. Large problems take SR = 32 (halo
+// overhead 2g/32) over many waves; small ones one wave of CTAs (occupancy from the runtime),
+// floored at 4 rows. Env FBMP_KQ3_SR overrides.
+template <int N_, bool CG>
+QLaunch q3_make(const PsGeo& G) {
+    constexpr int MJ = 2;
+    using Q = fast::q3::Geo<N_, MJ>;
+    QLaunch L;
+    L.fn = fast::k_q3<N_, MJ, CG>;
+    L.smem = Q::smem;
+    L.threads = fast::q3::NTH;
+    static int sms = 0, per_sm = 0;
+    if (!sms) {
+        int dev = 0;
+        FBMP_CUDA(cudaGetDevice(&dev));
+        FBMP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    set_smem(L.fn, L.smem);
+    FBMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L.fn, L.threads, L.smem));
+    const int nbands = ceil_div(G.w, Q::TWL);
+    const long long slots = static_cast<long long>(sms) * std::max(per_sm, 1);
+    int SR;
+    if (const char* e = std::getenv("FBMP_KQ3_SR")) {
+        SR = std::max(1, std::atoi(e));
+    } else if (static_cast<long long>(nbands) * ceil_div(G.h, 32) * G.N >= 4 * slots) {
+        SR = 32;
+    } else {
+        const long long per = std::max(1LL, slots / (static_cast<long long>(nbands) * G.N));
+        SR = std::max(4, ceil_div(G.h, static_cast<int>(std::min<long long>(per, G.h))));
+    }
+    const int nstrips = ceil_div(G.h, std::min(SR, G.h));
+    L.nblk = nbands * nstrips;
+    return L;
+}
+bool q3_ok(const PsGeo& G) {
+    // K_Q3 from LR width 128 (C2..C5); narrower images keep the tile kernel (env FBMP_KQ3_MINW)
+    static const bool off = std::getenv("FBMP_KQ") && std::atoi(std::getenv("FBMP_KQ")) == 2;
+    static const int minw = std::getenv("FBMP_KQ3_MINW") ? std::atoi(std::getenv("FBMP_KQ3_MINW")) : 128;
+    return !off && G.c == 4 && G.w >= std::max(64, minw) && G.W % 4 == 0;
+}
+
 template <bool CG>
 QLaunch q2_select(const PsGeo& G) {
     if (!fast_ok(G)) return {};
+    if (G.c == 4 && q3_ok(G)) {
+        switch (G.n) {
+        case 21: return q3_make<21, CG>(G);
+        case 17: return q3_make<17, CG>(G);
+        case 15: return q3_make<15, CG>(G);
+        case 7: return q3_make<7, CG>(G);
+        default: break;
+        }
+    }
     if (G.c == 4) {
         switch (G.n) {
         case 21: return q2_make<21, 4, CG>(G);

@@ -293,12 +293,19 @@ struct Geo {
     static constexpr int PLS = (JW + 1) & ~1;         // plane stride (>= the NVP over-read)
     static constexpr int D = FBMP_KQ3_D;              // ring depth (rows per warp)
     static constexpr int K = g + 2 <= 4 ? 4 : 8;      // partial-row slots (>= g + 2, power of 2)
-    static constexpr int KOFF = ((N_ * N_ + 1) / 2) * 2;
-    static constexpr int O_RING = KOFF;                   // NW x D x {r, p_old} x RW
+    // per-warp tap tables tt[pc][u + g][d - DMIN] (zero where |b| > C or d is out of range): the
+    // FMA loop reads them at constant offsets, two taps per 16-byte load
+    static constexpr int NU = g + gp + 1;
+    static constexpr int NAP = ((((3 + C) / 4) + ((C) / 4) + 1) + 1) & ~1;  // >= max_w NA, even
+    static constexpr int TT = 4 * NU * NAP;
+    static constexpr int O_TT = 0;                        // NW x TT
+    static constexpr int O_RING = NW * TT;                // NW x D x {r, p_old} x RW (the raw n x n
+                                                          // taps sit here until the tables are built)
     static constexpr int O_PL = O_RING + NW * D * 2 * RW; // NW x 4 x PLS
     static constexpr int O_SLOT = O_PL + NW * 4 * PLS;    // K x NW x TWL
     static constexpr int O_BAR = O_SLOT + K * NW * TWL;   // NW x D mbarriers
     static constexpr size_t smem = static_cast<size_t>(O_BAR + NW * D) * sizeof(double);
+    static_assert(N_ * N_ <= NW * D * 2 * RW, "raw taps fit in the ring");
     static_assert(TWL - MJ + NVP <= PLS, "plane over-read");
 };
 
@@ -340,7 +347,7 @@ struct Args {
 
 // one warp's stream of HR rows y = 4 s + WP, s in [s0, s1)
 template <int N_, int MJ, bool CG, int WP>
-__device__ __forceinline__ double rows(const Args& A, const double* __restrict__ sk, double* ring, double* pl,
+__device__ __forceinline__ double rows(const Args& A, const double* __restrict__ tt, double* ring, double* pl,
                                        double* slots, unsigned long long* bar, int lane, int warp) {
     using Q = Geo<N_, MJ>;
     constexpr int C = Q::C, g = Q::g, gp = Q::gp, RW = Q::RW, PLS = Q::PLS, TWL = Q::TWL, D = Q::D, K = Q::K;
@@ -352,39 +359,52 @@ __device__ __forceinline__ double rows(const Args& A, const double* __restrict__
     const unsigned int row_bytes = (CG ? 2u : 1u) * RW * sizeof(double);
     const int yo0 = 4 * A.i0, yo1 = min(4 * A.i1, H);
     const int xo_hi = min(4 * TWL, W - 4 * A.j0);
-    // the column split of a staged row at the periodic wrap is the same for every row: at most
-    // three pieces [start, start + len) of the image row, computed once
-    int pst[3], plen[3], np_ = 0;
+    // the column split of a staged row at the periodic wrap is the same for every row (at most
+    // three pieces): lane k < ncp issues copy k = (array, piece) of every row, so a row's copies
+    // go out in parallel; the staged rows are consecutive superrows, so the image row advances
+    // by 4 (mod H) per issue
+    int ncp = 0;
+    const double* csrc = nullptr;
+    unsigned int cdst = 0, cbytes = 0;
     {
         int start = col0 % W;
         if (start < 0) start += W;
-        for (int rem = RW; rem > 0 && np_ < 3; ++np_) {
+        int off = 0;
+        for (int rem = RW, np_ = 0; rem > 0 && np_ < 3; ++np_) {
             const int len = min(rem, W - start);
-            pst[np_] = start;
-            plen[np_] = len;
+#pragma unroll
+            for (int a = 0; a < (CG ? 2 : 1); ++a) {
+                const int k = a * 3 + np_;
+                if (lane == k) {
+                    csrc = (a == 0 ? A.rc : A.pold) + start;
+                    cdst = saddr(ring + a * RW + off);
+                    cbytes = static_cast<unsigned int>(len) * sizeof(double);
+                }
+            }
+            ncp = np_ + 1;
+            off += len;
             rem -= len;
             start = 0;
         }
     }
-    auto issue = [&](int s, int slot) {  // lane 0: TMA bulk copies of the row
-        int yw = (4 * s + WP) % H;
-        if (yw < 0) yw += H;
-        mbar_expect_tx(bar + slot, row_bytes);
-#pragma unroll
-        for (int a = 0; a < (CG ? 2 : 1); ++a) {
-            const double* srow = (a == 0 ? A.rc : A.pold) + static_cast<size_t>(yw) * W;
-            double* dst = ring + (slot * 2 + a) * RW;
-            int off = 0;
-            for (int k = 0; k < np_; ++k) {
-                bulk_g2s(dst + off, srow + pst[k], static_cast<unsigned int>(plen[k]) * sizeof(double), bar + slot);
-                off += plen[k];
-            }
-        }
+    const bool copier = lane < 3 * (CG ? 2 : 1) && (lane % 3) < ncp;
+    const unsigned int bar0 = saddr(bar);
+    int yw_next = (4 * A.s0 + WP) % H;  // image row of the next staged superrow
+    if (yw_next < 0) yw_next += H;
+    auto issue = [&](int slot) {  // warp-collective
+        const unsigned int b = bar0 + slot * 8u;
+        if (lane == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(row_bytes) : "memory");
+        if (copier)
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                             cdst + static_cast<unsigned int>(slot * 2 * RW * sizeof(double))),
+                         "l"(csrc + static_cast<size_t>(yw_next) * W), "r"(cbytes), "r"(b)
+                         : "memory");
+        yw_next += 4;
+        if (yw_next >= H) yw_next -= H;
     };
-    if (lane == 0) {
-        for (int k = 0; k < D; ++k)
-            if (A.s0 + k < A.s1) issue(A.s0 + k, k);
-    }
+    for (int k = 0; k < D; ++k)
+        if (A.s0 + k < A.s1) issue(k);
     double acc[NA][MJ];
 #pragma unroll
     for (int d = 0; d < NA; ++d)
@@ -428,11 +448,12 @@ __device__ __forceinline__ double rows(const Args& A, const double* __restrict__
             }
         }
         __syncwarp();
-        if (lane == 0 && s + D < A.s1) {  // the slot is free again: stage the row D superrows ahead
+        if (s + D < A.s1) {  // the slot is free again: stage the row D superrows ahead
             fence_proxy_async();
-            issue(s + D, slot);
+            issue(slot);
         }
-        // contributions of row y to LR rows s + d, d in [DMIN, DMAX]
+        // contributions of row y to LR rows s + d, d in [DMIN, DMAX]: for every accumulator the
+        // (pc, u) order is ascending; the zero taps of the table (|b| > C) add exact zeros
 #pragma unroll KQ3_PCU
         for (int pc = 0; pc < 4; ++pc) {
             double v[Q::NVP];
@@ -442,19 +463,20 @@ __device__ __forceinline__ double rows(const Args& A, const double* __restrict__
                 v[o] = t2.x;
                 v[o + 1] = t2.y;
             }
-            // every accumulator sees (pc, u) in ascending order; consecutive FMAs go to different
-            // accumulators (independent chains)
+            const double* tpc = tt + pc * (Q::NU * Q::NAP);
 #pragma unroll
-            for (int u = -g; u <= gp; ++u) {
-                const int b = -(4 * u + pc);
-                if (b >= -C && b <= C) {
+            for (int ui = 0; ui < Q::NU; ++ui) {
+                double kv[Q::NAP];
 #pragma unroll
-                    for (int d = DMIN; d <= DMAX; ++d) {
-                        const double kv = sk[(4 * d - WP + C) * N_ + (b + C)];
-#pragma unroll
-                        for (int m = 0; m < MJ; ++m) acc[d - DMIN][m] = fma(kv, v[m + g + u], acc[d - DMIN][m]);
-                    }
+                for (int dd = 0; dd < NA; dd += 2) {
+                    const double2 k2 = ld2(tpc + ui * Q::NAP + dd);
+                    kv[dd] = k2.x;
+                    kv[dd + 1] = k2.y;
                 }
+#pragma unroll
+                for (int dd = 0; dd < NA; ++dd)
+#pragma unroll
+                    for (int m = 0; m < MJ; ++m) acc[dd][m] = fma(kv[dd], v[m + ui], acc[dd][m]);
             }
         }
         // LR row s + DMIN is complete for this warp: publish its partial, shift the window
@@ -500,7 +522,8 @@ __global__ void __launch_bounds__(q3::NTH, FBMP_KQ3_MINB) k_q3(PsGeo G, const do
     const int ch = blockIdx.y;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const double* tp = taps + static_cast<size_t>(ch / G.cps) * N_ * N_;
-    for (int e = threadIdx.x; e < N_ * N_; e += q3::NTH) sm[e] = tp[e];
+    double* sk = sm + Q::O_RING;  // raw taps (overwritten by the row ring later)
+    for (int e = threadIdx.x; e < N_ * N_; e += q3::NTH) sk[e] = tp[e];
     q3::Args A;
     A.beta = 0.0;
     int t = 0;
@@ -540,13 +563,24 @@ __global__ void __launch_bounds__(q3::NTH, FBMP_KQ3_MINB) k_q3(PsGeo G, const do
         for (int k = 0; k < Q::D; ++k) q3::mbar_init(bar + k, 1);
         q3::mbar_fence_init();
     }
-    __syncthreads();  // taps and barriers
+    __syncthreads();  // taps
+    double* tt = sm + Q::O_TT + warp * Q::TT;
+    {
+        const int dmin = -((Q::C - warp) / 4), dmax = (warp + Q::C) / 4;
+        for (int e = lane; e < Q::TT; e += 32) {
+            const int pc = e / (Q::NU * Q::NAP), ui = (e / Q::NAP) % Q::NU, dd = e % Q::NAP;
+            const int d = dmin + dd, b = -(4 * (ui - Q::g) + pc);
+            tt[e] = (d <= dmax && b >= -Q::C && b <= Q::C) ? sk[(4 * d - warp + Q::C) * N_ + (b + Q::C)] : 0.0;
+        }
+    }
+    __syncthreads();  // tables built: the raw taps' space goes to the ring (async-proxy writes next)
+    q3::fence_proxy_async();
     double pp;
     switch (warp) {
-    case 0: pp = q3::rows<N_, MJ, CG, 0>(A, sm, ring, pl, slots, bar, lane, warp); break;
-    case 1: pp = q3::rows<N_, MJ, CG, 1>(A, sm, ring, pl, slots, bar, lane, warp); break;
-    case 2: pp = q3::rows<N_, MJ, CG, 2>(A, sm, ring, pl, slots, bar, lane, warp); break;
-    default: pp = q3::rows<N_, MJ, CG, 3>(A, sm, ring, pl, slots, bar, lane, warp); break;
+    case 0: pp = q3::rows<N_, MJ, CG, 0>(A, tt, ring, pl, slots, bar, lane, warp); break;
+    case 1: pp = q3::rows<N_, MJ, CG, 1>(A, tt, ring, pl, slots, bar, lane, warp); break;
+    case 2: pp = q3::rows<N_, MJ, CG, 2>(A, tt, ring, pl, slots, bar, lane, warp); break;
+    default: pp = q3::rows<N_, MJ, CG, 3>(A, tt, ring, pl, slots, bar, lane, warp); break;
     }
     if (CG) {
         const double bs = block_sum<q3::NTH>(pp, red);
@@ -1004,6 +1038,9 @@ __global__ void __launch_bounds__(NT, 2) k_apply4(PsGeo G, const double* __restr
 //      shuffles; the p.out partials are reduced per CTA and the last CTA of a channel forms
 //      p.Ap (same state update as K_A).
 // ------------------------------------------------------------------------------------------
+#ifndef FBMP_KD_MINB
+#define FBMP_KD_MINB 2  // K_D CTAs per SM the register budget is sized for
+#endif
 namespace kl {
 template <int CF>
 constexpr size_t dterm_smem(int windows = 2) {  // taps | q windows (2 alternating, or one per channel)
@@ -1019,7 +1056,7 @@ constexpr int RB = 16;            // rows per p.out partial (strip heights are m
 }  // namespace kl
 
 template <bool CG, int N_, int CF>
-__global__ void __launch_bounds__(NT, 2) k_dterm(PsGeo G, const double* __restrict__ taps, const double* __restrict__ q,
+__global__ void __launch_bounds__(NT, FBMP_KD_MINB) k_dterm(PsGeo G, const double* __restrict__ taps, const double* __restrict__ q,
                                                  double* __restrict__ out, const CgState* __restrict__ st) {
     using namespace a4;
     using Lay = a4::L<CF>;

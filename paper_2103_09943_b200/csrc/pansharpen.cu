@@ -976,9 +976,9 @@ QLaunch q2_make(const PsGeo& G) {
     L.threads = fast::QGeo<N_, CF>::NTH;
     return L;
 }
-// K_Q3 strip plan: LR-row strips of SR rows per band. Large problems take SR = 32 (halo
-// overhead 2g/32) over many waves; small ones one wave of CTAs (occupancy from the runtime),
-// floored at 4 rows. Env FBMP_KQ3_SR overrides.
+// K_Q3 strip plan: LR-row strips of SR rows per band. Large problems take the tallest SR in
+// {128, 64, 32} that still gives >= 4 waves (halo overhead 2g/SR); small ones one wave of CTAs
+// (occupancy from the runtime), floored at 4 rows. Env FBMP_KQ3_SR overrides.
 template <int N_, bool CG>
 QLaunch q3_make(const PsGeo& G) {
     constexpr int MJ = 2;
@@ -1001,7 +1001,13 @@ QLaunch q3_make(const PsGeo& G) {
     if (const char* e = std::getenv("FBMP_KQ3_SR")) {
         SR = std::max(1, std::atoi(e));
     } else if (static_cast<long long>(nbands) * ceil_div(G.h, 32) * G.N >= 4 * slots) {
+        // at least four waves: the tallest strip that keeps them (C5: 128 rows, 16 % faster than 32)
         SR = 32;
+        for (int cand : {128, 64})
+            if (static_cast<long long>(nbands) * ceil_div(G.h, cand) * G.N >= 4 * slots) {
+                SR = cand;
+                break;
+            }
     } else {
         const long long per = std::max(1LL, slots / (static_cast<long long>(nbands) * G.N));
         SR = std::max(4, ceil_div(G.h, static_cast<int>(std::min<long long>(per, G.h))));

@@ -1266,7 +1266,7 @@ __global__ void __launch_bounds__(NT, FBMP_KD_MINB) k_dterm(PsGeo G, const doubl
     }
 }
 
-// item = (band, strip) of one channel: blockIdx.x = item, blockIdx.y = channel
+// blockIdx.x = (scene, item = (band, strip), channel of the scene), channel fastest
 template <bool CG>
 __global__ void __launch_bounds__(kl::NTL, 16) k_llp(PsGeo G, const double* __restrict__ guide,
                                                     const double* __restrict__ wmu, const double* __restrict__ wg,
@@ -1274,17 +1274,27 @@ __global__ void __launch_bounds__(kl::NTL, 16) k_llp(PsGeo G, const double* __re
                                                     CgState* st, double* __restrict__ part, int nbands, int kstrips,
                                                     int R) {
     using namespace kl;
-    const int ch = blockIdx.y, scene = ch / G.cps;
+    // channel-fastest CTA order within a scene: the channels of a (band, strip) item run
+    // together, so the scene's guide maps are read from HBM once and hit in L2 for the others
+    const int nblk = gridDim.x / G.N;
+    int ch, item;
+    if (G.N % G.cps == 0) {
+        const int per_scene = nblk * G.cps, sc = blockIdx.x / per_scene, r = blockIdx.x - sc * per_scene;
+        item = r / G.cps;
+        ch = sc * G.cps + (r - item * G.cps);
+    } else {
+        ch = blockIdx.x % G.N;
+        item = blockIdx.x / G.N;
+    }
+    const int scene = ch / G.cps;
     const int H = G.H, W = G.W;
     const size_t P = static_cast<size_t>(H) * W;
     const int lane = threadIdx.x;
-    const int nblk = gridDim.x;
     if (CG) {
         pdl_wait();
         pdl_trigger();
         if (__all_sync(0xffffffffu, st[ch].done != 0)) return;
     }
-    const int item = blockIdx.x;
     const int nrb = (H + RB - 1) / RB;
     double dotp = 0.0;
     {
@@ -1450,17 +1460,27 @@ __global__ void __launch_bounds__(kl::NTL, 12) k_llp2(PsGeo G, const double* __r
                                                      CgState* st, double* __restrict__ part, int nbands, int kstrips,
                                                      int R) {
     using namespace kl;
-    const int ch = blockIdx.y, scene = ch / G.cps;
+    // channel-fastest CTA order within a scene: the channels of a (band, strip) item run
+    // together, so the scene's guide maps are read from HBM once and hit in L2 for the others
+    const int nblk = gridDim.x / G.N;
+    int ch, item;
+    if (G.N % G.cps == 0) {
+        const int per_scene = nblk * G.cps, sc = blockIdx.x / per_scene, r = blockIdx.x - sc * per_scene;
+        item = r / G.cps;
+        ch = sc * G.cps + (r - item * G.cps);
+    } else {
+        ch = blockIdx.x % G.N;
+        item = blockIdx.x / G.N;
+    }
+    const int scene = ch / G.cps;
     const int H = G.H, W = G.W;
     const size_t P = static_cast<size_t>(H) * W;
     const int lane = threadIdx.x;
-    const int nblk = gridDim.x;
     if (CG) {
         pdl_wait();
         pdl_trigger();
         if (__all_sync(0xffffffffu, st[ch].done != 0)) return;
     }
-    const int item = blockIdx.x;
     const int nrb = (H + RB - 1) / RB;
     const unsigned FULL = 0xffffffffu;
     constexpr int NB = 4;                    // ring depth: rows in flight = NB - 1

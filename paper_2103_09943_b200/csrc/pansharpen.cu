@@ -1154,10 +1154,10 @@ void launch_llp(Context& ctx, const PsGeo& G, const double* taps, const double* 
     if (between) FBMP_CUDA(cudaEventRecordWithFlags(between, ctx.stream, cudaEventRecordExternal));
     const LlpPlan L = llp_plan(ctx, G);
     if (L.pairs)
-        fast::k_llp2<CG><<<dim3(L.ctas, G.N), fast::kl::NTL, 0, ctx.stream>>>(G, guide, mu, gk, p, out, st, part,
+        fast::k_llp2<CG><<<dim3(L.ctas * G.N), fast::kl::NTL, 0, ctx.stream>>>(G, guide, mu, gk, p, out, st, part,
                                                                                L.nb, L.k, L.R);
     else
-        fast::k_llp<CG><<<dim3(L.ctas, G.N), fast::kl::NTL, 0, ctx.stream>>>(G, guide, mu, gk, p, out, st, part,
+        fast::k_llp<CG><<<dim3(L.ctas * G.N), fast::kl::NTL, 0, ctx.stream>>>(G, guide, mu, gk, p, out, st, part,
                                                                               L.nb, L.k, L.R);
 }
 

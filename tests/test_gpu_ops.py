@@ -106,10 +106,13 @@ def test_data_term(gpu, orc, H, W, n, c):
 
 @pytest.mark.parametrize("H,W,n,c", [(8, 8, 3, 2), (64, 64, 15, 4), (48, 40, 7, 4),
                                      (65, 67, 3, 1), (96, 80, 5, 2), (128, 72, 11, 4), (128, 200, 21, 4),
-                                     (64, 112, 17, 4)])
+                                     (64, 112, 17, 4),
+                                     (512, 640, 17, 4),   # K_Q3: LR width 160 = two full bands + a partial one
+                                     (512, 512, 21, 4), (768, 512, 7, 4)])
 def test_cg_operator(gpu, orc, H, W, n, c):
     """Covers every operator variant: single-column / column-pair K_L (odd / even W, partial
-    bands), register-tap and generic K_D, specialised and generic K_Q, c in {1, 2, 4}."""
+    bands), register-tap and generic K_D, tile K_Q2, row-streaming K_Q3 (LR width >= 128)
+    and generic K_Q, c in {1, 2, 4}."""
     rng = np.random.default_rng(7 * H + n)
     guide = orc.laplacian(rng.uniform(0, 1, (H, W)))
     p = rng.uniform(-1, 1, (H, W))
@@ -117,7 +120,8 @@ def test_cg_operator(gpu, orc, H, W, n, c):
     M = orc.Matting(guide, 1, 1e-4)
     data = orc.conv(orc.upsample_adjoint(orc.downsample(orc.conv(p, k), c), c), k, adjoint=True)
     expect = data + orc.laplacian(M.apply(orc.laplacian(p))) * 2e-4
-    assert rel(gpu.cg_operator(guide, p, k, c), expect) < 1e-12
+    # the oracle's summed-area-table box means lose digits as the image grows
+    assert rel(gpu.cg_operator(guide, p, k, c), expect) < (1e-12 if H * W < 100_000 else 1e-11)
 
 
 @pytest.mark.parametrize("shape,r,eps", [((7, 7), 1, 1e-2), ((7, 7), 1, 1e-3), ((50, 45), 1, 1e-4), ((30, 30), 2, 1e-3)])

@@ -21,7 +21,7 @@ def simplex_kernel(rng, n):
     return k / k.sum()
 
 
-@pytest.mark.parametrize("H,n", [(64, 7), (128, 15), (256, 15)])
+@pytest.mark.parametrize("H,n", [(64, 7), (128, 15), (256, 15), (512, 17)])  # 512: K_Q3
 def test_warmstart_cg_matches_oracle(gpu, orc, H, n):
     """Default cg_tol on a BASELINE-generator scene: same iteration count, same iterate."""
     sc = synth.make_scene("C1", hr=H)

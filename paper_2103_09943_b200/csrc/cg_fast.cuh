@@ -1095,6 +1095,7 @@ __global__ void __launch_bounds__(NT, FBMP_KD_MINB) k_dterm(PsGeo G, const doubl
         // each channel
         constexpr int QSZ = Lay::QWP * Lay::QWMAX;
         const int na = __popc(active);
+        const bool all_active = na == ch_hi - ch_lo;
         // the window has the same extent for every tile (origins are multiples of CF): constant
         // divisors, and its rows / columns wrap at most once
         constexpr int QWC = cfloordiv(TA - 1 + D::C, CF) - cfloordiv(CF - 1 - D::C, CF) + 1;
@@ -1102,7 +1103,8 @@ __global__ void __launch_bounds__(NT, FBMP_KD_MINB) k_dterm(PsGeo G, const doubl
         for (int e = threadIdx.x; e < na * QNC; e += NT) {
             const int c = e / QNC, r = e - c * QNC;
             const int a = r / QWC, b = r - a * QWC;
-            const int chl = ch_lo + static_cast<int>(__fns(active, 0, c + 1));  // c-th active channel
+            // c-th active channel (all of them unless some channel of the group has converged)
+            const int chl = ch_lo + (all_active ? c : static_cast<int>(__fns(active, 0, c + 1)));
             const double* qc = q + static_cast<size_t>(scene * G.cps + chl) * G.h * G.w;
             sq[c * QSZ + a * QS + b] =
                 __ldg(qc + static_cast<size_t>(wrap_once(iq0 + a, G.h)) * G.w + wrap_once(jq0 + b, G.w));

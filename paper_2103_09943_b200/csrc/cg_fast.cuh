@@ -1440,6 +1440,9 @@ __global__ void __launch_bounds__(kl::NTL, 16) k_llp(PsGeo G, const double* __re
 namespace kl {
 constexpr int BAND2 = 56;
 }
+#ifndef FBMP_KL_MINB
+#define FBMP_KL_MINB 12  // K_L warps per SM the register budget is sized for
+#endif
 #ifndef FBMP_KL_UNROLL
 #define FBMP_KL_UNROLL 3
 #endif
@@ -1456,7 +1459,7 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 template <bool CG>
-__global__ void __launch_bounds__(kl::NTL, 12) k_llp2(PsGeo G, const double* __restrict__ guide,
+__global__ void __launch_bounds__(kl::NTL, FBMP_KL_MINB) k_llp2(PsGeo G, const double* __restrict__ guide,
                                                      const double* __restrict__ wmu, const double* __restrict__ wg,
                                                      const double* __restrict__ pin, double* __restrict__ out,
                                                      CgState* st, double* __restrict__ part, int nbands, int kstrips,

@@ -736,11 +736,18 @@ __device__ __noinline__ bool alias_condition_ok(int m, const double* D, const do
     return (ev_min > 0.0) && !(ev_max > 1e14 * ev_min);
 }
 
+// cos(2 pi R / H) for R < H, then cos(2 pi C / W) for C < W: the Laplacian symbol's factors,
+// evaluated once per solve instead of 2 c^2 times per alias group (same expression, same bits)
+__global__ void k_cos_tables(int H, int W, double* __restrict__ tab) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < H + W; i += gridDim.x * blockDim.x)
+        tab[i] = i < H ? cos(2.0 * M_PI * i / H) : cos(2.0 * M_PI * (i - H) / W);
+}
+
 template <int CM>
 __global__ void __launch_bounds__(128) k_alias(int H, int W, int h, int w, int c, int cps, double lambda,
                                                const double2* __restrict__ Bh, const double2* __restrict__ Xh,
                                                const double2* __restrict__ Vh, double2* __restrict__ Zh,
-                                               int* __restrict__ flag) {
+                                               const double* __restrict__ cosHW, int* __restrict__ flag) {
     constexpr int M = CM * CM;
     const int gid = blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= h * w) return;
@@ -762,7 +769,7 @@ __global__ void __launch_bounds__(128) k_alias(int H, int W, int h, int w, int c
             const int R = kl + a * h, Cc = ll + b * w;
             const cplx bv = half_lookup(Bh, R, Cc, H, W);
             const cplx vv = half_lookup(V, R, Cc, H, W);
-            const double lh = 4.0 - 2.0 * cos(2.0 * M_PI * R / H) - 2.0 * cos(2.0 * M_PI * Cc / W);  // :56-63
+            const double lh = 4.0 - 2.0 * __ldg(cosHW + R) - 2.0 * __ldg(cosHW + H + Cc);  // :56-63
             D[g] = lambda * (lh * lh);
             u[g] = cconj(bv);
             u2[g] = cnorm(u[g]);
@@ -1558,13 +1565,15 @@ void solve_channel_fft(Context& ctx, const PsGeo& G, const double* d_taps, const
     FBMP_CUFFT(cufftExecD2Z(ctx.plan(0, H, W, S), emb, reinterpret_cast<cufftDoubleComplex*>(bh)));
     FBMP_CUFFT(cufftExecD2Z(ctx.plan(0, H, W, N), const_cast<double*>(d_v), reinterpret_cast<cufftDoubleComplex*>(vh)));
     FBMP_CUFFT(cufftExecD2Z(ctx.plan(0, h, w, N), const_cast<double*>(d_x), reinterpret_cast<cufftDoubleComplex*>(xh)));
+    double* cosHW = ctx.scratch<double>("fft_cos", static_cast<size_t>(H) + W);
+    k_cos_tables<<<ceil_div(H + W, 256), 256, 0, ctx.stream>>>(H, W, cosHW);
     const int nthreads = 128;
     const dim3 grid(ceil_div(static_cast<long long>(h) * w, nthreads), N);
     if (G.c <= 4)
-        k_alias<4><<<grid, nthreads, 0, ctx.stream>>>(H, W, h, w, G.c, G.cps, G.lambda, bh, xh, vh, zh, d_flag);
+        k_alias<4><<<grid, nthreads, 0, ctx.stream>>>(H, W, h, w, G.c, G.cps, G.lambda, bh, xh, vh, zh, cosHW, d_flag);
     else
-        k_alias<8><<<grid, nthreads, 0, ctx.stream>>>(H, W, h, w, G.c, G.cps, G.lambda, bh, xh, vh, zh, d_flag);
-    ctx.count();
+        k_alias<8><<<grid, nthreads, 0, ctx.stream>>>(H, W, h, w, G.c, G.cps, G.lambda, bh, xh, vh, zh, cosHW, d_flag);
+    ctx.count(2);
     check_launch();
     FBMP_CUFFT(cufftExecZ2D(ctx.plan(1, H, W, N), reinterpret_cast<cufftDoubleComplex*>(zh), zr));
     k_unscale<<<grid1d(ctx, static_cast<long long>(P) * N), 256, 0, ctx.stream>>>(

@@ -1146,17 +1146,18 @@ __global__ void __launch_bounds__(NT, FBMP_KD_MINB) k_dterm(PsGeo G, const doubl
                     qv[0][b] = qa[mm * QS + b];
                     qv[1][b] = qb2[mm * QS + b];
                 }
+                // b outer, output row k inner: consecutive FMAs go to 8 different accumulators,
+                // each accumulator still sees (mm, b) in ascending order
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int a = mm - k;
-                    if (a >= 0 && a < DM) {
+                for (int b = 0; b < DM; ++b)
 #pragma unroll
-                        for (int b = 0; b < DM; ++b) {
+                    for (int k = 0; k < 4; ++k) {
+                        const int a = mm - k;
+                        if (a >= 0 && a < DM) {
                             acc[0][k] = fma(kreg[a][b], qv[0][b], acc[0][k]);
                             acc[1][k] = fma(kreg[a][b], qv[1][b], acc[1][k]);
                         }
                     }
-                }
             }
             double* oa = out + (scene * G.cps + chA) * P;
             double* ob = out + (scene * G.cps + chB) * P;

@@ -973,6 +973,7 @@ struct QLaunch {
     size_t smem = 0;
     int nblk = 0;
     int threads = 0;
+    bool streaming = false;  // K_Q3
 };
 template <int N_, int CF, bool CG>
 QLaunch q2_make(const PsGeo& G) {
@@ -994,6 +995,7 @@ QLaunch q3_make(const PsGeo& G) {
     L.fn = fast::k_q3<N_, MJ, CG>;
     L.smem = Q::smem;
     L.threads = fast::q3::NTH;
+    L.streaming = true;
     static int sms = 0, per_sm = 0;
     if (!sms) {
         int dev = 0;
@@ -1324,10 +1326,11 @@ void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* 
     // In profile mode event records bracket every kernel and graphs are not pipelined.
     const int chunk = 8;
     const bool prof = ctx.profile;
-    // programmatic dependent launch per CG kernel (bit 0 K_Q, 1 K_A, 2 K_U; env FBMP_PDL). Measured
-    // on B200 (C1/C2/C4 scenes): only K_A gains (its guide-tile loads overlap K_Q's tail, -2%);
-    // PDL on K_Q costs ~5 us per iteration on small grids and on K_U ~7 us on C2.
-    static const int pdl_mask = std::getenv("FBMP_PDL") ? std::atoi(std::getenv("FBMP_PDL")) : 2;
+    // programmatic dependent launch per CG kernel (bit 0 K_Q, 1 K_A, 2 K_U; env FBMP_PDL).
+    // With K_Q3 (LR width >= 128) PDL on all three pays (C2 -1.3 %, C3/C4 neutral); with the tile
+    // K_Q2 (C1) only the K_A/K_D launch does (all three: C1 +5.5 %).
+    static const int pdl_env = std::getenv("FBMP_PDL") ? std::atoi(std::getenv("FBMP_PDL")) : -1;
+    const int pdl_mask = pdl_env >= 0 ? pdl_env : (q2.streaming ? 7 : 2);
     constexpr int EV = 5;  // profile events per iteration: K_Q | K_D | K_L (or K_A) | K_U
     std::vector<cudaEvent_t> pev(prof ? chunk * EV : 0);
     for (auto& e : pev) FBMP_CUDA(cudaEventCreate(&e));

@@ -299,13 +299,13 @@ struct Geo {
     static constexpr int NAP = ((((3 + C) / 4) + ((C) / 4) + 1) + 1) & ~1;  // >= max_w NA, even
     static constexpr int TT = 4 * NU * NAP;
     static constexpr int O_TT = 0;                        // NW x TT
-    static constexpr int O_RING = NW * TT;                // NW x D x {r, p_old} x RW (the raw n x n
-                                                          // taps sit here until the tables are built)
+    static constexpr int O_RING = NW * TT;                // NW x D x {r, p_old} x RW
     static constexpr int O_PL = O_RING + NW * D * 2 * RW; // NW x 4 x PLS
-    static constexpr int O_SLOT = O_PL + NW * 4 * PLS;    // K x NW x TWL
+    static constexpr int O_SLOT = O_PL + NW * 4 * PLS;    // K x NW x TWL (the raw n x n taps until
+                                                          // the tables are built)
     static constexpr int O_BAR = O_SLOT + K * NW * TWL;   // NW x D mbarriers
     static constexpr size_t smem = static_cast<size_t>(O_BAR + NW * D) * sizeof(double);
-    static_assert(N_ * N_ <= NW * D * 2 * RW, "raw taps fit in the ring");
+    static_assert(N_ * N_ <= K * NW * TWL, "raw taps fit in the partial-row slots");
     static_assert(TWL - MJ + NVP <= PLS, "plane over-read");
 };
 
@@ -347,7 +347,7 @@ struct Args {
 
 // one warp's stream of HR rows y = 4 s + WP, s in [s0, s1)
 template <int N_, int MJ, bool CG, int WP>
-__device__ __forceinline__ double rows(const Args& A, const double* __restrict__ tt, double* ring, double* pl,
+__device__ __forceinline__ double rows(const Args& A, const double* sk, double* tt, double* ring, double* pl,
                                        double* slots, unsigned long long* bar, int lane, int warp) {
     using Q = Geo<N_, MJ>;
     constexpr int C = Q::C, g = Q::g, gp = Q::gp, RW = Q::RW, PLS = Q::PLS, TWL = Q::TWL, D = Q::D, K = Q::K;
@@ -405,6 +405,13 @@ __device__ __forceinline__ double rows(const Args& A, const double* __restrict__
     };
     for (int k = 0; k < D; ++k)
         if (A.s0 + k < A.s1) issue(k);
+    // the warp's tap table (built while the first rows are in flight)
+    for (int e = lane; e < Q::TT; e += 32) {
+        const int pc = e / (Q::NU * Q::NAP), ui = (e / Q::NAP) % Q::NU, dd = e % Q::NAP;
+        const int d = DMIN + dd, b = -(4 * (ui - g) + pc);
+        tt[e] = (d <= DMAX && b >= -C && b <= C) ? sk[(4 * d - WP + C) * N_ + (b + C)] : 0.0;
+    }
+    __syncthreads();  // every table is built: the raw taps' space goes to the partial-row slots
     double acc[NA][MJ];
 #pragma unroll
     for (int d = 0; d < NA; ++d)
@@ -522,7 +529,7 @@ __global__ void __launch_bounds__(q3::NTH, FBMP_KQ3_MINB) k_q3(PsGeo G, const do
     const int ch = blockIdx.y;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const double* tp = taps + static_cast<size_t>(ch / G.cps) * N_ * N_;
-    double* sk = sm + Q::O_RING;  // raw taps (overwritten by the row ring later)
+    double* sk = sm + Q::O_SLOT;  // raw taps (the partial-row slots take over after the tables)
     for (int e = threadIdx.x; e < N_ * N_; e += q3::NTH) sk[e] = tp[e];
     q3::Args A;
     A.beta = 0.0;
@@ -563,24 +570,14 @@ __global__ void __launch_bounds__(q3::NTH, FBMP_KQ3_MINB) k_q3(PsGeo G, const do
         for (int k = 0; k < Q::D; ++k) q3::mbar_init(bar + k, 1);
         q3::mbar_fence_init();
     }
-    __syncthreads();  // taps
+    __syncthreads();  // taps and barriers
     double* tt = sm + Q::O_TT + warp * Q::TT;
-    {
-        const int dmin = -((Q::C - warp) / 4), dmax = (warp + Q::C) / 4;
-        for (int e = lane; e < Q::TT; e += 32) {
-            const int pc = e / (Q::NU * Q::NAP), ui = (e / Q::NAP) % Q::NU, dd = e % Q::NAP;
-            const int d = dmin + dd, b = -(4 * (ui - Q::g) + pc);
-            tt[e] = (d <= dmax && b >= -Q::C && b <= Q::C) ? sk[(4 * d - warp + Q::C) * N_ + (b + Q::C)] : 0.0;
-        }
-    }
-    __syncthreads();  // tables built: the raw taps' space goes to the ring (async-proxy writes next)
-    q3::fence_proxy_async();
     double pp;
     switch (warp) {
-    case 0: pp = q3::rows<N_, MJ, CG, 0>(A, tt, ring, pl, slots, bar, lane, warp); break;
-    case 1: pp = q3::rows<N_, MJ, CG, 1>(A, tt, ring, pl, slots, bar, lane, warp); break;
-    case 2: pp = q3::rows<N_, MJ, CG, 2>(A, tt, ring, pl, slots, bar, lane, warp); break;
-    default: pp = q3::rows<N_, MJ, CG, 3>(A, tt, ring, pl, slots, bar, lane, warp); break;
+    case 0: pp = q3::rows<N_, MJ, CG, 0>(A, sk, tt, ring, pl, slots, bar, lane, warp); break;
+    case 1: pp = q3::rows<N_, MJ, CG, 1>(A, sk, tt, ring, pl, slots, bar, lane, warp); break;
+    case 2: pp = q3::rows<N_, MJ, CG, 2>(A, sk, tt, ring, pl, slots, bar, lane, warp); break;
+    default: pp = q3::rows<N_, MJ, CG, 3>(A, sk, tt, ring, pl, slots, bar, lane, warp); break;
     }
     if (CG) {
         const double bs = block_sum<q3::NTH>(pp, red);

@@ -196,6 +196,14 @@ int fbmp_gpu_guided_output(fbmp_gpu_ctx* ctx, const double* a, const double* c, 
 /* solve_channel_fft (pansharpen.hpp:90-91). */
 int fbmp_gpu_solve_channel_fft(fbmp_gpu_ctx* ctx, const double* x, int h, int w, const double* k, int n,
                                int factor, const double* v, const fbmp_ps_params* params, double* out);
+/* Evaluation metrics (metrics.hpp:11-51) of est against ref (N x H x W, band-major), both cropped
+   by `crop` pixels (crop_border, metrics.hpp:28-29): `which` selects 1 PSNR (per band into
+   psnr_per_band[N] and their mean), 2 regressed PSNR, 4 ERGAS (ratio `factor`), 8 SAM (degrees),
+   16 RASE; out[0..4] = psnr_avg, psnr_reg_avg, ergas, sam_deg, rase (NaN when not selected).
+   Inputs on the [0, 255] scale as in the reference. Errors as the reference: negative margin
+   (param), margin leaving no pixels (dimension), zero reference mean in ERGAS / RASE (numerical). */
+int fbmp_gpu_metrics(fbmp_gpu_ctx* ctx, const double* est, const double* ref, int N, int H, int W, int crop,
+                     int factor, int which, double* psnr_per_band, double* out);
 /* box_mean (ops.hpp:32), circular convolution and its adjoint (ops.hpp:10-15). */
 int fbmp_gpu_box_mean(fbmp_gpu_ctx* ctx, const double* img, int H, int W, int radius, double* out);
 int fbmp_gpu_convolve(fbmp_gpu_ctx* ctx, const double* img, int H, int W, const double* k, int n, int adjoint,

@@ -514,3 +514,67 @@ def blind(lrms, pan, factor, n, l=4, lambda_omega=10.0, **kw):
     out, info = pansharpen(lrms, pan, k, factor, return_info=True, **kw)
     info.update(omega=omega, kernel=k, admm_iters=t)
     return out, info
+
+
+# ---------------------------------------------------------------------------------------------
+# Evaluation metrics (proj/src/metrics.cpp:14-153) -- the checker of the device metrics.
+# Sums are sequential (math.fsum-free Python loops would be slow; numpy's pairwise sums differ
+# from the reference's sequential ones only by rounding).
+# ---------------------------------------------------------------------------------------------
+def crop_border(img, margin):  # metrics.cpp:46-58
+    if margin < 0:
+        raise ValueError("crop_border: negative margin")
+    if margin == 0:
+        return img
+    if 2 * margin >= min(img.shape[-2:]):
+        raise ValueError("crop_border: margin leaves no pixels")
+    return img[..., margin:-margin, margin:-margin]
+
+
+def _psnr_from_mse(mse):  # metrics.cpp:24-27
+    return np.inf if mse <= 0.0 else 20.0 * np.log10(255.0 / np.sqrt(mse))
+
+
+def psnr_avg(est, ref):  # metrics.cpp:66-79
+    per = [_psnr_from_mse(np.mean((e - r) ** 2)) for e, r in zip(est, ref)]
+    return per, sum(per) / len(per)
+
+
+def psnr_reg_avg(est, ref):  # metrics.cpp:81-105
+    s = 0.0
+    for e, r in zip(est, ref):
+        me, mr = e.mean(), r.mean()
+        var = np.sum((e - me) * (e - me))
+        cov = np.sum((e - me) * (r - mr))
+        a, b = (cov / var, mr - cov / var * me) if var > 0.0 else (0.0, mr)
+        s += _psnr_from_mse(np.mean((a * e + b - r) ** 2))
+    return s / len(est)
+
+
+def ergas(est, ref, factor):  # metrics.cpp:107-118
+    acc = 0.0
+    for e, r in zip(est, ref):
+        mu = r.mean()
+        if mu == 0.0:
+            raise ValueError("ergas: reference band mean is zero")
+        rmse = np.sqrt(np.mean((e - r) ** 2))
+        acc += (rmse / mu) ** 2
+    return 100.0 / factor * np.sqrt(acc / len(est))
+
+
+def sam_deg(est, ref):  # metrics.cpp:120-141
+    dot = np.sum(est * ref, axis=0)
+    ne = np.sum(est * est, axis=0)
+    nr = np.sum(ref * ref, axis=0)
+    ok = (ne != 0.0) & (nr != 0.0)
+    if not ok.any():
+        return 0.0
+    cosv = np.clip(dot[ok] / np.sqrt(ne[ok] * nr[ok]), -1.0, 1.0)
+    return float(np.sum(np.arccos(cosv)) / ok.sum() * 180.0 / np.pi)
+
+
+def rase(est, ref):  # metrics.cpp:143-153
+    mu = np.mean([r.mean() for r in ref])
+    if mu == 0.0:
+        raise ValueError("rase: mean of reference image is zero")
+    return 100.0 / mu * np.sqrt(np.mean([np.mean((e - r) ** 2) for e, r in zip(est, ref)]))

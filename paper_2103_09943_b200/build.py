@@ -27,7 +27,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
                   "-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "--expt-relaxed-constexpr",
                   "-I" + os.path.join(NCCL_DIR, "include")]
-CU_SOURCES = ["pansharpen.cu", "kernel_fit.cu", "capi.cu"]
+CU_SOURCES = ["pansharpen.cu", "kernel_fit.cu", "metrics.cu", "capi.cu"]
 GPU_LIB = os.path.join(LIBDIR, "libfbmp_gpu.so")
 LINK = ["-L" + CUDA_LIB, "-lcufft", "-lcudart", "-Xlinker", "-rpath," + CUDA_LIB,
         "-L" + os.path.join(NCCL_DIR, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath," + os.path.join(NCCL_DIR, "lib")]

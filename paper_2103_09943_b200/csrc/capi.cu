@@ -675,6 +675,21 @@ int fbmp_gpu_solve_channel_fft(fbmp_gpu_ctx* ctx, const double* x, int h, int w,
     });
 }
 
+int fbmp_gpu_metrics(fbmp_gpu_ctx* ctx, const double* est, const double* ref, int N, int H, int W, int crop,
+                     int factor, int which, double* psnr_per_band, double* out) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        if (N < 1 || H < 1 || W < 1) dim_error("metrics: image shapes differ");
+        const size_t n = static_cast<size_t>(N) * H * W;
+        double* d_e = upload(C, "met_est", est, n);
+        double* d_r = upload(C, "met_ref", ref, n);
+        std::vector<double> pb(N);
+        metrics_device(C, d_e, d_r, N, H, W, crop, factor, which, pb.data(), out);
+        if (psnr_per_band) std::memcpy(psnr_per_band, pb.data(), sizeof(double) * N);
+    });
+}
+
 int fbmp_gpu_box_mean(fbmp_gpu_ctx* ctx, const double* img, int H, int W, int radius, double* out) {
     return guarded([&] {
         Context& C = ctx->impl;

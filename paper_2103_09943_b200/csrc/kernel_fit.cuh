@@ -58,4 +58,8 @@ void estimate_kernel_device(Context& ctx, const double* d_pan, const double* d_o
                             const fbmp_ke_params& prm, double* d_k, std::vector<int>& iters, double* d_state_out,
                             int hook_t);
 
+// Evaluation metrics (csrc/metrics.cu, metrics.hpp:11-51): device inputs, host outputs.
+void metrics_device(Context& ctx, const double* d_est, const double* d_ref, int N, int H, int W, int crop,
+                    int factor, int which, double* psnr_per_band, double* out);
+
 }  // namespace fbmp_gpu

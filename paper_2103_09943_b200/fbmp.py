@@ -390,6 +390,48 @@ def box_mean(img, radius, ctx=None):
     return out
 
 
+METRIC_PSNR, METRIC_PSNR_REG, METRIC_ERGAS, METRIC_SAM, METRIC_RASE = 1, 2, 4, 8, 16
+
+
+def metrics(est, ref, factor=4, crop=0, which=31, ctx=None):
+    """Evaluation metrics of metrics.hpp:11-51 on the device (inputs on the [0, 255] scale),
+    after crop_border(crop) of both cubes: dict with psnr_per_band, psnr_avg, psnr_reg_avg,
+    ergas, sam_deg, rase (None where `which` does not select it)."""
+    est, ref = _f(est), _f(ref)
+    if est.ndim == 2:
+        est, ref = est[None], ref[None]
+    if est.shape != ref.shape or est.ndim != 3:
+        raise DimensionError("metrics: image shapes differ")
+    N, H, W = est.shape
+    pb, out = np.empty(N), np.empty(5)
+    _check(_lib.fbmp_gpu_metrics(_ctx(ctx), _p(est), _p(ref), N, H, W, crop, factor, which, _p(pb), _p(out)))
+    keys = ("psnr_avg", "psnr_reg_avg", "ergas", "sam_deg", "rase")
+    res = {k: (float(out[i]) if which & (1 << i) else None) for i, k in enumerate(keys)}
+    res["psnr_per_band"] = list(pb) if which & METRIC_PSNR else None
+    return res
+
+
+def psnr_avg(est, ref, ctx=None):  # metrics.hpp:31-33
+    m = metrics(est, ref, which=METRIC_PSNR, ctx=ctx)
+    return m["psnr_per_band"], m["psnr_avg"]
+
+
+def psnr_reg_avg(est, ref, ctx=None):  # metrics.hpp:36-38
+    return metrics(est, ref, which=METRIC_PSNR_REG, ctx=ctx)["psnr_reg_avg"]
+
+
+def ergas(est, ref, factor, ctx=None):  # metrics.hpp:40
+    return metrics(est, ref, factor=factor, which=METRIC_ERGAS, ctx=ctx)["ergas"]
+
+
+def sam_deg(est, ref, ctx=None):  # metrics.hpp:41
+    return metrics(est, ref, which=METRIC_SAM, ctx=ctx)["sam_deg"]
+
+
+def rase(est, ref, ctx=None):  # metrics.hpp:42
+    return metrics(est, ref, which=METRIC_RASE, ctx=ctx)["rase"]
+
+
 def circular_convolve(img, k, ctx=None, adjoint=False):
     img, k = _f(img), _f(k)
     out = np.empty_like(img)
@@ -622,6 +664,7 @@ EXPORTED_SYMBOLS = (
     "fbmp_gpu_default_ps_params", "fbmp_gpu_default_ke_params", "fbmp_gpu_default_sw_params",
     "fbmp_gpu_ctx_create", "fbmp_gpu_ctx_destroy", "fbmp_gpu_last_error", "fbmp_gpu_ctx_stats",
     "fbmp_gpu_ctx_stream", "fbmp_gpu_ctx_launches", "fbmp_gpu_ctx_set_profile", "fbmp_gpu_ctx_kernel_profile",
+    "fbmp_gpu_metrics",
     "fbmp_gpu_blind_batch_dev", "fbmp_gpu_blind_strips_dev", "fbmp_gpu_nccl_unique_id", "fbmp_gpu_ctx_set_comm",
     "fbmp_gpu_pansharpen", "fbmp_gpu_estimate_kernel_tgv",
     "fbmp_gpu_estimate_kernel_plane", "fbmp_gpu_solve_weights", "fbmp_gpu_combine_bands", "fbmp_gpu_blind",

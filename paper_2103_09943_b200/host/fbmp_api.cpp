@@ -3,6 +3,7 @@
 // the matting operator, the guided filter, the alias-group solve, the spectral weights and the
 // TGV kernel fit) runs on the GPU; this file only converts types, keeps one device context per
 // host thread and rethrows the C ABI status codes as the reference's exception types.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <memory>
@@ -11,6 +12,7 @@
 #include "fbmp/errors.hpp"
 #include "fbmp/image.hpp"
 #include "fbmp/kernel_estimator.hpp"
+#include "fbmp/metrics.hpp"
 #include "fbmp/ops.hpp"
 #include "fbmp/pansharpen.hpp"
 #include "fbmp/spectral_weights.hpp"
@@ -521,5 +523,59 @@ double tgv_objective(const ObservationSystem& obs, const Plane& u, const Plane& 
     }
     return data + params.alpha1 * t1 + params.alpha2 * t2;
 }
+
+// ---- evaluation metrics (metrics.hpp:11-51) on the device --------------------------------------
+Plane crop_border(const Plane& img, int margin) {  // metrics.cpp:46-58 (data movement only)
+    if (margin < 0) throw ParamError("crop_border: negative margin");
+    if (margin == 0) return img;
+    if (2 * margin >= std::min(img.height(), img.width())) throw DimensionError("crop_border: margin leaves no pixels");
+    Plane out(img.height() - 2 * margin, img.width() - 2 * margin);
+    for (int r = 0; r < out.height(); ++r)
+        for (int c = 0; c < out.width(); ++c) out(r, c) = img(r + margin, c + margin);
+    return out;
+}
+
+MultiBandImage crop_border(const MultiBandImage& img, int margin) {
+    std::vector<Plane> bands;
+    bands.reserve(img.band_count());
+    for (const Plane& b : img.bands()) bands.push_back(crop_border(b, margin));
+    return MultiBandImage(std::move(bands));
+}
+
+namespace {
+std::vector<double> device_metrics(const MultiBandImage& est, const MultiBandImage& ref, int factor, int which,
+                                   std::vector<double>* per_band = nullptr) {
+    if (est.band_count() != ref.band_count() || est.height() != ref.height() || est.width() != ref.width())
+        throw DimensionError("metrics: image shapes differ");
+    const std::vector<double> e = stack(est), r = stack(ref);
+    std::vector<double> pb(est.band_count()), out(5);
+    check(fbmp_gpu_metrics(ctx(), e.data(), r.data(), est.band_count(), est.height(), est.width(), 0, factor, which,
+                           pb.data(), out.data()));
+    if (per_band) *per_band = pb;
+    return out;
+}
+}  // namespace
+
+std::pair<std::vector<double>, double> psnr_avg(const MultiBandImage& est, const MultiBandImage& ref) {
+    std::vector<double> pb;
+    const double avg = device_metrics(est, ref, 1, 1, &pb)[0];
+    return {pb, avg};
+}
+
+double psnr_plane(const Plane& est, const Plane& ref) {
+    if (!est.same_shape(ref)) throw DimensionError("metrics: shape mismatch");
+    return psnr_avg(MultiBandImage({est}), MultiBandImage({ref})).second;
+}
+
+double psnr_reg_avg(const MultiBandImage& est, const MultiBandImage& ref) { return device_metrics(est, ref, 1, 2)[1]; }
+
+double ergas(const MultiBandImage& est, const MultiBandImage& ref, int factor) {
+    return device_metrics(est, ref, factor, 4)[2];
+}
+
+double sam_deg(const MultiBandImage& est, const MultiBandImage& ref) { return device_metrics(est, ref, 1, 8)[3]; }
+
+double rase(const MultiBandImage& est, const MultiBandImage& ref) { return device_metrics(est, ref, 1, 16)[4]; }
+
 
 }  // namespace fbmp

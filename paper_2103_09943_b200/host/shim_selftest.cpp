@@ -9,6 +9,7 @@
 #include <string>
 
 #include "fbmp/kernel_estimator.hpp"
+#include "fbmp/metrics.hpp"
 #include "fbmp/ops.hpp"
 #include "fbmp/pansharpen.hpp"
 #include "fbmp/spectral_weights.hpp"
@@ -152,6 +153,34 @@ int main() {
         bool eq = true;
         for (std::size_t i = 0; i < o2.band(0).size(); ++i) eq = eq && o2.band(0).data()[i] == o2.band(1).data()[i];
         report("equal_bands", eq);
+    }
+    {  // tests/test_metrics.cpp: crop, identical / offset / affine / scaled cubes, the MSE oracle
+        MultiBandImage ref({random_plane(rng, 30, 30, 0.0, 255.0), random_plane(rng, 30, 30, 0.0, 255.0)});
+        MultiBandImage est = ref;
+        est.band(0)(0, 0) += 50.0;
+        MultiBandImage ref1({ref.band(0)}), est1({est.band(0)});  // one band, as the reference's case
+        report("metrics_crop", std::isfinite(psnr_avg(est1, ref1).second) &&
+                                   std::isinf(psnr_avg(crop_border(est1, 10), crop_border(ref1, 10)).second));
+        MultiBandImage off = ref, aff = ref, sc = ref;
+        for (int b = 0; b < 2; ++b) {
+            off.band(b) += 255.0;
+            aff.band(b) *= 0.5;
+            aff.band(b) += 3.0;
+            sc.band(b) *= 3.0;
+        }
+        report("metrics_ideal", std::isinf(psnr_avg(ref, ref).second) && std::abs(psnr_avg(off, ref).second) < 1e-12 &&
+                                    psnr_reg_avg(aff, ref) > 200.0 && ergas(ref, ref, 4) == 0.0 &&
+                                    rase(ref, ref) == 0.0 && std::abs(sam_deg(sc, ref)) < 1e-6);
+        double mse = 0.0;
+        for (std::size_t i = 0; i < est.band(0).size(); ++i) {
+            const double d = est.band(0).data()[i] - ref.band(0).data()[i];
+            mse += d * d;
+        }
+        mse /= est.band(0).size();
+        report("metrics_psnr_oracle",
+               std::abs(psnr_avg(est, ref).first[0] - 20.0 * std::log10(255.0 / std::sqrt(mse))) < 1e-10);
+        report("metrics_errors", throws<DimensionError>([&] { crop_border(ref, 15); }) &&
+                                     throws<NumericalError>([&] { ergas(ref, MultiBandImage(2, 30, 30), 4); }));
     }
     std::printf("%d failures\n", failures);
     return failures;

@@ -69,11 +69,12 @@ def build_gpu(force: bool = False, verbose: bool = False) -> str:
 
 
 SHIM_TEST = os.path.join(LIBDIR, "fbmp_shim_selftest")
+CLI = os.path.join(LIBDIR, "fbmp")  # command-line front end (host/fbmp_cli.cpp)
 
 
 def build_shim(force: bool = False) -> str:
     """libfbmp.so: the reference's fbmp:: C++ API on top of libfbmp_gpu.so (+ its self-test)."""
-    srcs = [os.path.join(HOST, "fbmp_api.cpp")]
+    srcs = [os.path.join(HOST, "fbmp_api.cpp"), os.path.join(HOST, "raster_io.cpp")]
     hdrs = [os.path.join(ROOT, "include", "fbmp", f) for f in os.listdir(os.path.join(ROOT, "include", "fbmp"))]
     if force or _stale(SHIM_LIB, srcs + hdrs + [GPU_LIB]):
         _run(["g++", "-O2", "-std=c++20", "-fPIC", "-shared", "-Wall", "-Wextra",
@@ -82,6 +83,10 @@ def build_shim(force: bool = False) -> str:
     test_src = os.path.join(HOST, "shim_selftest.cpp")
     if force or _stale(SHIM_TEST, [test_src, SHIM_LIB] + hdrs):
         _run(["g++", "-O2", "-std=c++20", "-Wall", "-I" + os.path.join(ROOT, "include"), "-o", SHIM_TEST, test_src,
+              "-L" + LIBDIR, "-lfbmp", "-lfbmp_gpu", "-Wl,-rpath,$ORIGIN"])
+    cli_src = os.path.join(HOST, "fbmp_cli.cpp")
+    if os.path.exists(cli_src) and (force or _stale(CLI, [cli_src, SHIM_LIB] + hdrs)):
+        _run(["g++", "-O2", "-std=c++20", "-Wall", "-I" + os.path.join(ROOT, "include"), "-o", CLI, cli_src,
               "-L" + LIBDIR, "-lfbmp", "-lfbmp_gpu", "-Wl,-rpath,$ORIGIN"])
     return SHIM_LIB
 

@@ -104,6 +104,11 @@ int fbmp_gpu_pansharpen(fbmp_gpu_ctx* ctx, const double* lrms, int N, int h, int
                         const double* k, int n, int factor, const fbmp_ps_params* params, double* out,
                         int* cg_iters);
 
+/* l2 + simplex kernel estimate (kernel_estimator.cpp:389-428 through estimate_kernel_plane with
+   KernelPrior::l2, :438-455): same scaling and errors as the TGV path; params.n, alpha1, alpha2,
+   mu3, rho, t_max, th, init are used. k_out: n*n; iters: ADMM iterations (optional). */
+int fbmp_gpu_estimate_kernel_l2_plane(fbmp_gpu_ctx* ctx, const double* pan, int H, int W, const double* obs,
+                                      int factor, const fbmp_ke_params* params, double* k_out, int* iters);
 /* estimate_kernel_tgv (kernel_estimator.hpp:114-118): combine_bands(lrms, omega) then the
  * TGV^2 fit. k_out: n*n. iters (optional) receives the ADMM iteration count. */
 int fbmp_gpu_estimate_kernel_tgv(fbmp_gpu_ctx* ctx, const double* lrms_subset, int nb, int h, int w,

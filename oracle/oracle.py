@@ -355,3 +355,42 @@ def observation_matrix(pan, factor, n):
     E = np.empty((p, n * n))
     _check(lib().orc_observation_matrix(_p(pan), pan.shape[0], pan.shape[1], factor, n, _p(E)))
     return E
+
+
+def estimate_kernel_l2_plane(pan, obs, factor, n, alpha1=1.0, alpha2=0.006, mu3=100.0, rho=0.5, t_max=10000,
+                             th=1e-5, init="dirac"):
+    """kernel_estimator.cpp:389-428 (run_l2) behind estimate_kernel_plane's scaling (:438-455): dense
+    K = E^T E + 2 alpha1 grad^T grad + (2 alpha2 + mu3) I assembled column by column from the
+    circular difference operators, Cholesky solves (Eigen's LLT), the oracle's simplex projection.
+    Returns (kernel, iterations). Test infrastructure (checker of the device l2 estimator)."""
+    s = intensity_scale(pan, factor)
+    pan_n, obs_n = _f(pan) * s, _f(obs) * s
+    m = n * n
+    EtE, Etf = gram(pan_n, obs_n, factor, n)
+    K = EtE.copy()
+    for j in range(m):
+        e = np.zeros((n, n))
+        e.flat[j] = 1.0
+        g = diff(diff(e, 0), 0, adjoint=True) + diff(diff(e, 1), 1, adjoint=True)
+        K[:, j] += 2.0 * alpha1 * g.ravel()
+    K[np.diag_indices(m)] += 2.0 * alpha2 + mu3
+    Lc = np.linalg.cholesky(K)
+    solve = lambda r: np.linalg.solve(Lc.T, np.linalg.solve(Lc, r))  # noqa: E731
+    u = np.zeros(m)
+    if init == "dirac":
+        u[(n // 2) * n + n // 2] = 1.0
+    else:
+        u[:] = 1.0 / m
+    z, L = u.copy(), np.zeros(m)
+    t = 0
+    for t in range(t_max):
+        un = solve(Etf + mu3 * (z - L))
+        z = project_simplex(un + L)
+        L = L + rho * (un - z)
+        delta = np.linalg.norm(u - un) / max(np.linalg.norm(un), 1e-300)
+        u = un
+        if not (np.all(np.isfinite(u)) and np.all(np.isfinite(z))):
+            raise OracleError(3, f"l2 kernel estimation diverged at iteration {t}")
+        if delta < th:
+            break
+    return z.reshape(n, n), t + 1

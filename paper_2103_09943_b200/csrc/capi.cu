@@ -793,6 +793,24 @@ int fbmp_gpu_estimate_kernel_plane(fbmp_gpu_ctx* ctx, const double* pan, int H, 
     });
 }
 
+int fbmp_gpu_estimate_kernel_l2_plane(fbmp_gpu_ctx* ctx, const double* pan, int H, int W, const double* obs,
+                                      int factor, const fbmp_ke_params* params, double* k_out, int* iters) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        const fbmp_ke_params prm = ke_or_default(params);
+        if (factor < 1) param_error("build_observation: factor must be >= 1");
+        if (H % factor || W % factor) dim_error("build_observation: PAN dimensions must be factor times the observation");
+        const size_t P = static_cast<size_t>(H) * W, p = P / (static_cast<size_t>(factor) * factor);
+        const int m = prm.n * prm.n;
+        double* d_p = upload(C, "api_pan", pan, P);
+        double* d_f = upload(C, "api_obs", obs, p);
+        double* d_k = C.scratch<double>("api_k", m);
+        estimate_kernel_l2_device(C, d_p, d_f, H, W, factor, prm, d_k, iters);
+        download(C, k_out, d_k, m);
+    });
+}
+
 int fbmp_gpu_estimate_kernel_tgv(fbmp_gpu_ctx* ctx, const double* lrms_subset, int nb, int h, int w, const double* pan,
                                  const double* omega, int factor, const fbmp_ke_params* params, double* k_out,
                                  int* iters) {

@@ -1395,8 +1395,26 @@ void gram_device(Context& ctx, const double* d_pan, const double* d_obs, int H, 
     check_launch();
 }
 
+// l2 kernel prior (kernel_estimator.cpp:394-407): K = E^T E + 2 a1 grad^T grad + (2 a2 + mu3) I, where
+// grad^T grad of the circular forward differences is 4 I minus the four periodic neighbours
+__global__ void k_add_l2(double* __restrict__ M, int S, int n, double two_a1, double two_a2) {
+    const int m = n * n;
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < static_cast<long long>(S) * m;
+         e += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int s = static_cast<int>(e / m), i = static_cast<int>(e - static_cast<long long>(s) * m);
+        double* row = M + (static_cast<size_t>(s) * m + i) * m;
+        const int r = i / n, c = i - r * n;
+        row[i] += 4.0 * two_a1 + two_a2;
+        row[r * n + (c + 1) % n] -= two_a1;
+        row[r * n + (c + n - 1) % n] -= two_a1;
+        row[((r + 1) % n) * n + c] -= two_a1;
+        row[((r + n - 1) % n) * n + c] -= two_a1;
+    }
+}
+
 void build_observation(Context& ctx, const double* d_pan, const double* d_obs, int S, int H, int W, int c, int n,
-                       double mu3, const double* d_scale, ObsSystem& sys, bool want_inverse) {
+                       double mu3, const double* d_scale, ObsSystem& sys, bool want_inverse, double l2_a1,
+                       double l2_a2) {
     const int n2 = n * n, D = 2 * n - 1;
     sys.S = S;
     sys.n = n;
@@ -1411,6 +1429,11 @@ void build_observation(Context& ctx, const double* d_pan, const double* d_obs, i
     gram_T_and_etf(ctx, d_pan, d_obs, S, H, W, c, n, d_scale, T, sys.Etf);
     k_gram_expand<<<grid1d(ctx, static_cast<long long>(S) * NN), 256, 0, ctx.stream>>>(T, S, c, n, mu3, sys.M);
     ctx.count();
+    if (l2_a1 != 0.0 || l2_a2 != 0.0) {
+        k_add_l2<<<grid1d(ctx, static_cast<long long>(S) * n2), 256, 0, ctx.stream>>>(sys.M, S, n, 2.0 * l2_a1,
+                                                                                       2.0 * l2_a2);
+        ctx.count();
+    }
     FBMP_CUDA(cudaMemsetAsync(sys.status, 0, sizeof(int) * S, ctx.stream));
     const int N = n2;
     const size_t smP = static_cast<size_t>(N) * (NBK + 1) * sizeof(double);
@@ -1577,6 +1600,113 @@ void estimate_kernel_device(Context& ctx, const double* d_pan, const double* d_o
         if (st == 2) num_error("kernel estimation diverged: non-finite z at iteration " + it);
         if (st == 3) num_error("project_simplex: empty support (non-finite input?)");
     }
+}
+
+// l2 + simplex ADMM (kernel_estimator.cpp:411-427), one CTA per scene: u' = K^-1 (E^T f + mu3 (z - L)),
+// z = project_simplex(u' + L), L += rho (u' - z), stop on ||u - u'|| / max(||u'||, 1e-300) < th.
+// K^-1 (explicit, from build_observation) is read from L2; info = {iterations, status}.
+__global__ void __launch_bounds__(NTADMM) k_admm_l2(int n, double mu3, double rho, double th, int t_max, int init_kind,
+                                                    const double* __restrict__ Kinv_all, const double* __restrict__ Etf_all,
+                                                    double* __restrict__ k_out, int* __restrict__ info_all) {
+    extern __shared__ double smem[];
+    const int s = blockIdx.x, m = n * n;
+    const double* Kinv = Kinv_all + static_cast<size_t>(s) * m * m;
+    const double* Etf = Etf_all + static_cast<size_t>(s) * m;
+    double* u = smem;
+    double* z = u + m;
+    double* L = z + m;
+    double* b = L + m;
+    double* un = b + m;
+    double* v = un + m;
+    double* red = v + m;
+    int* ired = reinterpret_cast<int*>(red + NTADMM);
+    double* scratch = red + NTADMM + NTADMM / 2 + 4;
+    const int cc = (n - 1) / 2;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        const double u0 = init_kind == 0 ? (i == cc * n + cc ? 1.0 : 0.0) : 1.0 / static_cast<double>(m);
+        u[i] = u0;
+        z[i] = u0;
+        L[i] = 0.0;
+    }
+    __syncthreads();
+    int status = 0, t = 0;
+    for (; t < t_max; ++t) {
+        for (int i = threadIdx.x; i < m; i += blockDim.x) b[i] = Etf[i] + mu3 * (z[i] - L[i]);
+        __syncthreads();
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        for (int i = warp; i < m; i += NTADMM / 32) {  // K^-1 symmetric: row i
+            double acc = 0.0;
+            for (int j = lane; j < m; j += 32) acc = fma(__ldg(Kinv + static_cast<size_t>(i) * m + j), b[j], acc);
+            acc = warp_sum(acc);
+            if (lane == 0) un[i] = acc;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < m; i += blockDim.x) v[i] = un[i] + L[i];
+        __syncthreads();
+        const int support = m <= NTADMM ? project_simplex_sorted(v, z, m, red, ired, scratch)
+                                        : project_simplex_block(v, z, m, red, ired);
+        if (support == 0) { status = 3; break; }
+        double dd = 0.0, nn = 0.0;
+        bool fin = true;
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+            L[i] += rho * (un[i] - z[i]);
+            const double du = u[i] - un[i];
+            dd += du * du;
+            nn += un[i] * un[i];
+            fin = fin && isfinite(un[i]) && isfinite(z[i]);
+        }
+        const double delta = sqrt(admm_sum(dd, red)) / fmax(sqrt(admm_sum(nn, red)), 1e-300);
+        for (int i = threadIdx.x; i < m; i += blockDim.x) u[i] = un[i];
+        if (!__syncthreads_and(fin)) { status = 1; break; }
+        if (delta < th) { ++t; break; }
+    }
+    for (int i = threadIdx.x; i < m; i += blockDim.x) k_out[static_cast<size_t>(s) * m + i] = z[i];
+    if (threadIdx.x == 0) {
+        info_all[2 * s] = t;
+        info_all[2 * s + 1] = status;
+    }
+}
+
+void estimate_kernel_l2_device(Context& ctx, const double* d_pan, const double* d_obs, int H, int W, int c,
+                               const fbmp_ke_params& prm, double* d_k, int* iters) {
+    validate_ke(prm);
+    const int n = prm.n;
+    if (c < 1) param_error("build_observation: factor must be >= 1");
+    if (H % c || W % c) dim_error("build_observation: PAN dimensions must be factor times the observation");
+    if (n > std::min(H, W)) dim_error("build_observation: kernel larger than PAN image");
+    const long long P = static_cast<long long>(H) * W;
+    double* stats = ctx.scratch<double>("ke_stats", 4);
+    pan_stats(ctx, d_pan, 1, P, stats);
+    double hs[4];
+    d2h(hs, stats, sizeof(hs), ctx.stream);
+    FBMP_CUDA(cudaStreamSynchronize(ctx.stream));
+    const double mean = hs[0] / static_cast<double>(P);  // kernel_estimator.cpp:269-289
+    const double dev = std::max(hs[2] - mean, mean - hs[1]);
+    if (dev <= 1e-12 * std::max(1.0, std::abs(mean)))
+        num_error("kernel estimation: constant PAN image is unidentifiable (E^T E has rank 1)");
+    if (hs[3] <= 0.0) num_error("kernel estimation: PAN image is identically zero");
+    const double scale = std::sqrt(16384.0 / (static_cast<double>(H / c) * (W / c))) / hs[3];
+    double* d_scale = ctx.scratch<double>("ke_scale", 1);
+    h2d(d_scale, &scale, sizeof(double), ctx.stream);
+    ObsSystem sys;
+    build_observation(ctx, d_pan, d_obs, 1, H, W, c, n, prm.mu3, d_scale, sys, true, prm.alpha1, prm.alpha2);
+    const int m = n * n;
+    int* info = ctx.scratch<int>("ke_info", 2);
+    const size_t sm = (6 * static_cast<size_t>(m) + NTADMM + NTADMM / 2 + 4 + admm_scratch_doubles(m)) * sizeof(double);
+    if (sm > 227 * 1024) param_error("l2 kernel estimation: kernel side too large for the device solve");
+    set_smem(k_admm_l2, sm);
+    k_admm_l2<<<1, NTADMM, sm, ctx.stream>>>(n, prm.mu3, prm.rho, prm.th, prm.t_max, prm.init, sys.Ginv, sys.Etf, d_k,
+                                             info);
+    ctx.count();
+    check_launch();
+    int hinfo[2], hst = 0;
+    d2h(hinfo, info, sizeof(hinfo), ctx.stream);
+    d2h(&hst, sys.status, sizeof(int), ctx.stream);
+    FBMP_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (hst) num_error("l2 kernel estimation: normal matrix factorization failed");
+    if (hinfo[1] == 1) num_error("l2 kernel estimation diverged at iteration " + std::to_string(hinfo[0] - 1));
+    if (hinfo[1] == 3) num_error("project_simplex: empty support (non-finite input?)");
+    if (iters) *iters = hinfo[0];
 }
 
 }  // namespace fbmp_gpu

@@ -32,7 +32,11 @@ struct ObsSystem {
     int* status;   // S : 0 ok, 1 factorization failed
 };
 void build_observation(Context& ctx, const double* d_pan, const double* d_obs, int S, int H, int W, int c, int n,
-                       double mu3, const double* d_scale, ObsSystem& sys, bool want_inverse);
+                       double mu3, const double* d_scale, ObsSystem& sys, bool want_inverse, double l2_a1 = 0.0,
+                       double l2_a2 = 0.0);
+// l2 + simplex kernel estimate of one scene (kernel_estimator.cpp:389-428): device pan / obs, d_k: n*n
+void estimate_kernel_l2_device(Context& ctx, const double* d_pan, const double* d_obs, int H, int W, int c,
+                               const fbmp_ke_params& prm, double* d_k, int* iters);
 
 // ADMM (kernel_estimator.cpp:291-387). state: S * 17 * n2 (u,p1,p2,x0,x1,y0..y3,z,L1_0,L1_1,
 // L2_0..L2_3,L3). If resume_state is null the state is initialised (dirac/uniform). Runs

@@ -490,6 +490,21 @@ def estimate_kernel_plane(pan, observation, factor, params: KernelEstParams | No
     return k, it.value
 
 
+def estimate_kernel_l2_plane(pan, observation, factor, params: KernelEstParams | None = None, ctx=None):
+    """estimate_kernel_plane with KernelPrior::l2 (kernel_estimator.cpp:389-428, :438-455): the l2 +
+    simplex ablation estimator of the paper's Table II -> (kernel, iterations)."""
+    pan, obs = _f(pan), _f(observation)
+    prm = params or KernelEstParams()
+    if pan.shape[0] != factor * obs.shape[0] or pan.shape[1] != factor * obs.shape[1]:
+        raise DimensionError("build_observation: PAN dimensions must be factor times the observation")
+    k = np.empty((prm.n, prm.n))
+    it = C.c_int(0)
+    cp = prm.c()
+    _check(_lib.fbmp_gpu_estimate_kernel_l2_plane(_ctx(ctx), _p(pan), pan.shape[0], pan.shape[1], _p(obs), factor,
+                                                  C.byref(cp), _p(k), C.byref(it)))
+    return k, it.value
+
+
 def estimate_kernel_tgv(lrms_subset, pan, omega, factor, params: KernelEstParams | None = None, ctx=None):
     """kernel_estimator.hpp:114-118 -> (kernel, iterations)."""
     return estimate_kernel_plane(pan, combine_bands(lrms_subset, omega, ctx), factor, params, ctx=ctx)
@@ -664,7 +679,7 @@ EXPORTED_SYMBOLS = (
     "fbmp_gpu_default_ps_params", "fbmp_gpu_default_ke_params", "fbmp_gpu_default_sw_params",
     "fbmp_gpu_ctx_create", "fbmp_gpu_ctx_destroy", "fbmp_gpu_last_error", "fbmp_gpu_ctx_stats",
     "fbmp_gpu_ctx_stream", "fbmp_gpu_ctx_launches", "fbmp_gpu_ctx_set_profile", "fbmp_gpu_ctx_kernel_profile",
-    "fbmp_gpu_metrics",
+    "fbmp_gpu_metrics", "fbmp_gpu_estimate_kernel_l2_plane",
     "fbmp_gpu_blind_batch_dev", "fbmp_gpu_blind_strips_dev", "fbmp_gpu_nccl_unique_id", "fbmp_gpu_ctx_set_comm",
     "fbmp_gpu_pansharpen", "fbmp_gpu_estimate_kernel_tgv",
     "fbmp_gpu_estimate_kernel_plane", "fbmp_gpu_solve_weights", "fbmp_gpu_combine_bands", "fbmp_gpu_blind",

@@ -467,8 +467,15 @@ Kernel2D estimate_kernel_plane(KernelPrior prior, const Plane& pan, const Plane&
                                const KernelEstParams& params, TgvAdmmState* final_state,
                                const TgvIterHook& before_up_solve) {
     params.validate();
+    if (prior == KernelPrior::l2) {  // kernel_estimator.cpp:452-453
+        const fbmp_ke_params kp = to_c(params);
+        std::vector<double> taps(static_cast<std::size_t>(params.n) * params.n);
+        check(fbmp_gpu_estimate_kernel_l2_plane(ctx(), pan.data(), pan.height(), pan.width(), observation.data(), factor,
+                                                &kp, taps.data(), nullptr));
+        return Kernel2D(params.n, std::move(taps));
+    }
     if (prior != KernelPrior::tgv2)
-        throw ParamError("estimate_kernel_plane: the GPU path implements the TGV^2 prior only");
+        throw ParamError("estimate_kernel_plane: the GPU path implements the TGV^2 and l2 priors only");
     const fbmp_ke_params kp = to_c(params);
     const int n = params.n;
     const std::size_t m = static_cast<std::size_t>(n) * n;
@@ -504,8 +511,9 @@ Kernel2D estimate_kernel_tv(const MultiBandImage&, const Plane&, const SpectralW
     throw ParamError("estimate_kernel_tv: TV kernel prior is an ablation outside the GPU path");
 }
 
-Kernel2D estimate_kernel_l2(const MultiBandImage&, const Plane&, const SpectralWeights&, int, const KernelEstParams&) {
-    throw ParamError("estimate_kernel_l2: l2 kernel prior is an ablation outside the GPU path");
+Kernel2D estimate_kernel_l2(const MultiBandImage& lrms_subset, const Plane& pan, const SpectralWeights& omega, int factor,
+                            const KernelEstParams& params) {  // kernel_estimator.cpp:473-478
+    return estimate_kernel_plane(KernelPrior::l2, pan, combine_bands(lrms_subset, omega), factor, params);
 }
 
 double tgv_objective(const ObservationSystem& obs, const Plane& u, const Plane& p1, const Plane& p2,

@@ -291,3 +291,31 @@ def test_blind_into_caller_buffer(gpu):
     assert out is buf and np.array_equal(buf, ref)
     with pytest.raises(ValueError):
         gpu.blind(sc.lrms, sc.pan, 4, 15, out=np.empty((4, 256, 255)))
+
+
+@pytest.mark.parametrize("H,n,th", [(64, 7, 1e-12), (128, 9, 1e-12), (128, 9, 1e-5)])
+def test_kernel_l2_matches_oracle(gpu, orc, H, n, th):
+    """The l2 + simplex ablation estimator (kernel_estimator.cpp:389-428): device normal matrix with
+    the grad^T grad term, explicit inverse, one-CTA ADMM, against the oracle's dense Cholesky solve.
+    Converged runs (th 1e-12) to 1e-9; at the default th the same iteration count and 1e-6."""
+    sc = synth.make_scene("C1", hr=H)
+    obs = sc.lrms.mean(axis=0)
+    prm = gpu.KernelEstParams(n=n, th=th)
+    kg, itg = gpu.estimate_kernel_l2_plane(sc.pan, obs, 4, prm)
+    ko, ito = orc.estimate_kernel_l2_plane(sc.pan, obs, 4, n, th=th)
+    assert abs(kg.sum() - 1.0) < 1e-12 and kg.min() >= 0.0
+    if th < 1e-9:
+        assert rel(kg, ko) < 1e-9
+    else:
+        assert itg == ito
+        assert rel(kg, ko) < TOL
+
+
+def test_kernel_l2_errors(gpu):
+    rng = np.random.default_rng(5)
+    with pytest.raises(gpu.NumericalError):  # constant PAN (kernel_estimator.cpp:269-276)
+        gpu.estimate_kernel_l2_plane(np.full((64, 64), 0.5), rng.uniform(0, 1, (16, 16)), 4,
+                                     gpu.KernelEstParams(n=7))
+    with pytest.raises(gpu.DimensionError):
+        gpu.estimate_kernel_l2_plane(rng.uniform(0, 1, (64, 60)), rng.uniform(0, 1, (16, 16)), 4,
+                                     gpu.KernelEstParams(n=7))

@@ -263,6 +263,27 @@ def test_blind_strips_match_single_domain(gpu, G):
     assert rel(d_o.cpu().numpy(), ref) < 1e-7
 
 
+@pytest.mark.parametrize("G", [2, 4])
+def test_blind_strips_c2_streaming_kernels(gpu, G):
+    """Row strips of the C2 scene (LR width 256): the strip CG runs the streaming K_Q3 with owned-row
+    dot products (rlo/rhi) and global interior-window rows; same CG counts and solution as the
+    single-domain solve up to the dot-product summation order."""
+    import torch
+
+    sc = synth.make_scene("C2")
+    ref, info = gpu.blind(sc.lrms, sc.pan, 4, 17)
+    ctx = gpu.default_context()
+    N, h, w = sc.lrms.shape
+    d_l, d_p = torch.from_numpy(sc.lrms).cuda(), torch.from_numpy(sc.pan).cuda()
+    d_o = torch.empty((N, 4 * h, 4 * w), dtype=torch.float64, device="cuda")
+    d_k = torch.empty((17, 17), dtype=torch.float64, device="cuda")
+    gpu.blind_strips_dev(d_l.data_ptr(), N, h, w, d_p.data_ptr(), d_o.data_ptr(), d_k.data_ptr(), 4, 17, ctx,
+                         vstrips=G)
+    torch.cuda.synchronize()
+    assert ctx.stats()["cg_iters"][:N] == list(info["cg_iters"])
+    assert rel(d_o.cpu().numpy(), ref) < 1e-7
+
+
 def test_blind_strips_nccl_single_rank(gpu):
     """The NCCL code path of the row-strip solve (allreduce, grouped send/recv of the halo to the
     rank itself -- the periodic wrap --, allgather of the owned rows, gather to rank 0) on a

@@ -1,3 +1,5 @@
+# Scratch driver for gpurun debugging sessions (overwritten freely): CG iteration counts and the
+# HRMS difference to the golden fixtures on the C1 and C2 scenes for the current build.
 cd $GRAFT_REPO_ROOT
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_q3 --launch-skip 20 --launch-count 1 -o gpurun_out/kq3b python tools/run_one.py C2 1 > gpurun_out/ncu_kq3b.log 2>&1
-tail -1 gpurun_out/ncu_kq3b.log
+TAG=c1 python tools/c1_iters.py C1 15
+TAG=c2 python tools/c1_iters.py C2 17

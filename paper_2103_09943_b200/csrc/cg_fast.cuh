@@ -90,12 +90,12 @@ __global__ void k_guide_stats(const double* __restrict__ guide, int H, int W, in
 // ------------------------------------------------------------------------------------------
 // K_Q2
 // ------------------------------------------------------------------------------------------
-template <int N_, int CF>
+template <int N_, int CF, int MJ_ = 4>
 struct QGeo {
     static constexpr int C = (N_ - 1) / 2;
     static constexpr int g = (C + CF - 1) / CF;
     static constexpr int NTH = 128;                        // 4 warps
-    static constexpr int MJ = 4;                           // LR columns per thread
+    static constexpr int MJ = MJ_;                         // LR columns per thread
     static constexpr int TH = 32, TW = MJ * (NTH / 32);    // lane = LR row, warp = 4 LR columns
     static constexpr int PW = TW + 2 * g, PH = TH + 2 * g; // phase-plane extent (LR)
     static constexpr int PWS = PW | 1;                     // odd row stride: lanes (rows) hit distinct banks
@@ -111,12 +111,12 @@ struct QGeo {
 // ((CF g - a) mod CF, (CF g - b) mod CF) at (i + (CF g - a) div CF, j + (CF g - b) div CF).
 // A lane owns one LR row and MJ consecutive LR columns: every plane value loaded feeds up to MJ
 // points and every (broadcast) tap MJ FMAs.
-template <int N_, int CF, bool CG>
-__global__ void __launch_bounds__(QGeo<N_, CF>::NTH, 3) k_q2(PsGeo G, const double* __restrict__ taps,
+template <int N_, int CF, bool CG, int MJ_ = 4>
+__global__ void __launch_bounds__(QGeo<N_, CF, MJ_>::NTH, 3) k_q2(PsGeo G, const double* __restrict__ taps,
                                                              const double* __restrict__ src,
                                                              double* __restrict__ pbuf, double* __restrict__ q,
                                                              CgState* st, double* __restrict__ part, int nblk) {
-    using Q = QGeo<N_, CF>;
+    using Q = QGeo<N_, CF, MJ_>;
     constexpr int NQ = Q::NTH;
     __shared__ double red[NQ / 32 + 1];
     extern __shared__ double sm[];
@@ -246,9 +246,9 @@ __global__ void __launch_bounds__(QGeo<N_, CF>::NTH, 3) k_q2(PsGeo G, const doub
     }
 }
 
-template <int N_, int CF>
+template <int N_, int CF, int MJ_ = 4>
 inline int q2_blocks(const PsGeo& G) {
-    using Q = QGeo<N_, CF>;
+    using Q = QGeo<N_, CF, MJ_>;
     return ((G.w + Q::TW - 1) / Q::TW) * ((G.h + Q::TH - 1) / Q::TH);
 }
 

@@ -978,10 +978,26 @@ struct QLaunch {
 template <int N_, int CF, bool CG>
 QLaunch q2_make(const PsGeo& G) {
     QLaunch L;
-    L.fn = fast::k_q2<N_, CF, CG>;
-    L.smem = fast::QGeo<N_, CF>::smem;
-    L.nblk = fast::q2_blocks<N_, CF>(G);
-    L.threads = fast::QGeo<N_, CF>::NTH;
+    // narrow images (C1: 64 LR columns) are latency-bound: 1 LR column per lane gives 4x the CTAs
+    // (the per-output summation order does not depend on MJ). Env FBMP_KQ2_MJ overrides.
+    static const int mj_env = std::getenv("FBMP_KQ2_MJ") ? std::atoi(std::getenv("FBMP_KQ2_MJ")) : 0;
+    const int mj = mj_env ? mj_env : (CF == 4 && G.w <= 64 ? 1 : 4);
+    if (mj == 1) {
+        L.fn = fast::k_q2<N_, CF, CG, 1>;
+        L.smem = fast::QGeo<N_, CF, 1>::smem;
+        L.nblk = fast::q2_blocks<N_, CF, 1>(G);
+        L.threads = fast::QGeo<N_, CF, 1>::NTH;
+    } else if (mj == 2) {
+        L.fn = fast::k_q2<N_, CF, CG, 2>;
+        L.smem = fast::QGeo<N_, CF, 2>::smem;
+        L.nblk = fast::q2_blocks<N_, CF, 2>(G);
+        L.threads = fast::QGeo<N_, CF, 2>::NTH;
+    } else {
+        L.fn = fast::k_q2<N_, CF, CG>;
+        L.smem = fast::QGeo<N_, CF>::smem;
+        L.nblk = fast::q2_blocks<N_, CF>(G);
+        L.threads = fast::QGeo<N_, CF>::NTH;
+    }
     return L;
 }
 // K_Q3 strip plan: LR-row strips of SR rows per band. Large problems take the tallest SR in

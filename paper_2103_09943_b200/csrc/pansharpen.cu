@@ -1343,10 +1343,10 @@ void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* 
     const int chunk = 8;
     const bool prof = ctx.profile;
     // programmatic dependent launch per CG kernel (bit 0 K_Q, 1 K_A, 2 K_U; env FBMP_PDL).
-    // With K_Q3 (LR width >= 128) PDL on all three pays (C2 -1.3 %, C3/C4 neutral); with the tile
-    // K_Q2 (C1) only the K_A/K_D launch does (all three: C1 +5.5 %).
+    // PDL on all three launches: C2 (K_Q3) 19.74 -> 19.44 ms, C1 (one-column K_Q2) 8.01 -> 7.92 ms,
+    // C3/C4 neutral. (With the four-column K_Q2 it cost C1 5.5 %.)
     static const int pdl_env = std::getenv("FBMP_PDL") ? std::atoi(std::getenv("FBMP_PDL")) : -1;
-    const int pdl_mask = pdl_env >= 0 ? pdl_env : (q2.streaming ? 7 : 2);
+    const int pdl_mask = pdl_env >= 0 ? pdl_env : 7;
     constexpr int EV = 5;  // profile events per iteration: K_Q | K_D | K_L (or K_A) | K_U
     std::vector<cudaEvent_t> pev(prof ? chunk * EV : 0);
     for (auto& e : pev) FBMP_CUDA(cudaEventCreate(&e));

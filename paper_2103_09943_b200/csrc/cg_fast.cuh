@@ -1438,6 +1438,9 @@ __global__ void __launch_bounds__(kl::NTL, 16) k_llp(PsGeo G, const double* __re
 namespace kl {
 constexpr int BAND2 = 56;
 }
+#ifndef FBMP_KL_NB
+#define FBMP_KL_NB 4
+#endif
 #ifndef FBMP_KL_MINB
 #define FBMP_KL_MINB 12  // K_L warps per SM the register budget is sized for
 #endif
@@ -1486,7 +1489,7 @@ __global__ void __launch_bounds__(kl::NTL, FBMP_KL_MINB) k_llp2(PsGeo G, const d
     }
     const int nrb = (H + RB - 1) / RB;
     const unsigned FULL = 0xffffffffu;
-    constexpr int NB = 4;                    // ring depth: rows in flight = NB - 1
+    constexpr int NB = FBMP_KL_NB;           // ring depth: rows in flight = NB - 1
     __shared__ double2 ring[NB][5][32];      // p, I, mu, g, d rows of NB steps
     double dotp = 0.0;
     {

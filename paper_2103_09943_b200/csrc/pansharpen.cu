@@ -23,7 +23,11 @@ PsGeo make_geo(int N, int h, int w, int c, int n, int rw, double lambda, double 
     G.N = N;
     G.cps = cps > 0 ? cps : N;
     const char* env = std::getenv("FBMP_KA_CPC");
-    G.cpc = std::min(env ? std::max(1, std::atoi(env)) : G.cps, fast::a4::MAXCPC);
+    // channels per K_D CTA: all of the scene's, except on small images where fewer tiles than SMs
+    // would leave the GPU idle (C1: 64 tiles -> 2 channels per CTA, 7.90 -> 7.71 ms; same bits)
+    const long long tiles = static_cast<long long>((h * c + 31) / 32) * ((w * c + 31) / 32) * ((N + G.cps - 1) / G.cps);
+    const int cpc_def = tiles < 128 ? std::min(2, G.cps) : G.cps;
+    G.cpc = std::min(env ? std::max(1, std::atoi(env)) : cpc_def, fast::a4::MAXCPC);
     const char* dbg = std::getenv("FBMP_KA_DBG");
     G.dbg = dbg ? std::atoi(dbg) : 0;
     G.h = h; G.w = w; G.c = c;

@@ -12,9 +12,10 @@ configs[1] = C2 by default). Multi-GPU (torchrun): every rank solves its own sce
            library's stream, L2 flushed with a 512 MB write before every step).
 `e2e`    : the same metric through the public host-pointer C ABI (fbmp_gpu_blind), with
            the H2D upload of PAN + LRMS and the D2H download of the HRMS inside the step.
-`roofline`: dominant CG kernel, algorithmic bytes / CUDA-event duration (profile pass).
-`cpu_baseline`: the CPU oracle (oracle/, C++ restatement of the reference) on a bounded
-           sample of the same scene, extrapolated to the full iteration counts.
+`roofline`: the dominant CG operator (K_A = K_Q + K_D + K_L, or K_U), SURVEY 8(d) algorithmic
+           bytes / CUDA-event duration (profile pass), plus the whole-solve fraction.
+`cpu_baseline`: the CPU oracle (oracle/, C++ restatement of the reference): one complete solve
+           of the same scene for C1/C2; a labelled estimate from a bounded sample for C3.
 """
 from __future__ import annotations
 
@@ -112,69 +113,115 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------------------------
-# CPU baseline / reference arm (oracle restatement of the reference, bounded sample)
+# CPU baseline / reference arm (the oracle: C++ restatement of the reference, timed whole)
 # ----------------------------------------------------------------------------------------------
-CG_CAP = 2      # CG iterations per band in a sample
+FULL_SOLVE_MAX_HR = 1024  # C1 / C2: complete solves are timed (1 warm-up, median of 3)
+CG_CAP = 2      # larger configs (C3 - C5, labelled estimates): CG iterations per band in a sample
 ADMM_CAP = 20   # ADMM iterations in a sample
 POST_DIV = 8    # the alias-group solve runs on 1/POST_DIV of the LR rows in a sample
+ORACLE_DESC = ("oracle (C++ restatement of the reference; FFT = own radix-2 with FFTW's c2c conventions, "
+               "alias solve = Householder + QL as Eigen's SelfAdjointEigenSolver, matting = assembled CSR SpMV)")
 
 
-def cpu_sample(scene, cfg, threads, cg_full=None, admm_full=None):
-    """One bounded sample of the blind solve on the CPU oracle: CG capped at CG_CAP iterations per
-    band, ADMM at ADMM_CAP iterations, the alias-group solve on the first 1/POST_DIV of the LR rows.
-    Each capped phase is extrapolated linearly to the full solve (iteration counts of the full
-    solve are identical on the oracle and the GPU, tests/test_gpu_pipeline.py). Returns (seconds
-    for the full solve, description)."""
+def ref_threads(cfg) -> int:
+    """Threads the reference path uses: min(hardware_concurrency, N) channel workers for the HRMS
+    stage (pansharpen.cpp:410-412); the weights and the kernel fit run on one core."""
+    return max(1, min(os.cpu_count() or 1, cfg.bands))
+
+
+def cpu_full_solve(scene, cfg, threads) -> float:
+    """Seconds of one complete blind solve (solve_weights -> estimate_kernel_tgv -> pansharpen) of
+    the scene on the CPU oracle, wall clock around the single library call."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle  # test infrastructure: the checker, timed here as the CPU baseline only
-    cg_full = cg_full or REF_CG_ITERS.get(cfg.name)
-    admm_full = admm_full or REF_ADMM_ITERS.get(cfg.name)
+    t0 = time.perf_counter()
+    oracle.blind(scene.lrms, scene.pan, cfg.ratio, cfg.support, threads=threads)
+    return time.perf_counter() - t0
+
+
+def cpu_sample(scene, cfg, threads, cg_full, admm_full):
+    """ESTIMATE for configs whose complete CPU solve runs for many minutes (C3 - C5): CG capped at
+    CG_CAP iterations per band, ADMM at ADMM_CAP, the alias-group solve on 1/POST_DIV of the LR
+    rows, each capped phase scaled linearly to the iteration counts of the GPU solve of the same
+    scene (cg_full, admm_full). Returns (estimated seconds, description)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
     h = cfg.hr // cfg.ratio
     post_rows = max(1, h // POST_DIV)
     r = oracle.blind_sampled(scene.lrms, scene.pan, cfg.ratio, cfg.support, CG_CAP, threads=threads,
-                             admm_cap=ADMM_CAP if admm_full else 0, post_rows=post_rows)
+                             admm_cap=ADMM_CAP, post_rows=post_rows)
     tw, tsetup, tadmm, tmat, tcg, tpost, tgroups = r["times"]
-    admm_x = admm_full / r["admm_iters"] if admm_full else 1.0
-    cg_x = max(cg_full) / CG_CAP if cg_full else 1.0
+    admm_x = admm_full / r["admm_iters"]
+    cg_x = max(cg_full) / CG_CAP
     grp_x = h / post_rows
     est = tw + tsetup + tadmm * admm_x + tmat + tcg * cg_x + tpost + tgroups * grp_x
-    sample = (f"oracle (C++ restatement of the reference; FFT = own radix-2, alias solve = Householder + QL as "
-              f"Eigen's SelfAdjointEigenSolver) on {cfg.name} scene 0, {threads} threads for the per-band phases: "
+    sample = (f"ESTIMATE from a bounded sample of the {ORACLE_DESC} on {cfg.name} scene 0, {threads} threads: "
               f"weights {tw:.2f}s + fit setup {tsetup:.2f}s + ADMM {r['admm_iters']} it {tadmm:.2f}s (x{admm_x:.1f}) + "
-              f"matting build {tmat:.2f}s + CG {CG_CAP} it/band {tcg:.2f}s (x{cg_x:.1f}) + guided/FFT {tpost:.2f}s + "
-              f"alias groups of {post_rows}/{h} LR rows {tgroups:.2f}s (x{grp_x:.0f}); estimated full solve {est:.1f}s")
+              f"matting build {tmat:.2f}s + CG {CG_CAP} it/band {tcg:.2f}s (x{cg_x:.1f}, GPU counts) + guided/FFT "
+              f"{tpost:.2f}s + alias groups of {post_rows}/{h} LR rows {tgroups:.2f}s (x{grp_x:.0f}); "
+              f"estimated full solve {est:.1f}s")
     return est, sample
 
 
 def reference_arm(args, cfg):
+    """The reference's CPU path (the oracle port: the reference itself cannot be built here or on
+    the GPU box) on this arm's workload. C1/C2: complete solves, min(W, 1) warm-up
+    and min(K, 3) timed solves (1 warm-up, median of 3), so the whole run takes a
+    few minutes; `steps` / `warmup` report the solves actually run."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     scene = synth.make_scene(cfg, 0)
-    threads = min(os.cpu_count() or 1, cfg.bands)
-    times = []
-    desc = ""
-    for i in range(args.warmup + args.steps):
-        est, desc = cpu_sample(scene, cfg, threads)
-        if i >= args.warmup:
-            times.append(est)
-    T = sum(times)
+    threads = ref_threads(cfg)
     P = cfg.hr * cfg.hr
-    value = args.steps * P * cfg.bands / T / 1e6
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True, "scaling": "weak",
+    if cfg.hr <= FULL_SOLVE_MAX_HR:
+        warm, steps = min(args.warmup, 1), max(1, min(args.steps, 3))
+        for _ in range(warm):
+            cpu_full_solve(scene, cfg, threads)
+        times = [cpu_full_solve(scene, cfg, threads) for _ in range(steps)]
+        T = statistics.median(times)
+        desc = (f"{ORACLE_DESC}: complete blind solves of {cfg.name} scene 0 (weights + TGV fit + HRMS of "
+                f"{cfg.bands} bands), {threads} channel threads (pansharpen.cpp:410-412; weights and kernel fit "
+                f"on 1 core), host nproc {os.cpu_count()}; {warm} warm-up + median of {steps}: "
+                f"{', '.join(f'{t:.2f}s' for t in times)}")
+    else:
+        warm, steps = 0, 1
+        T, desc = cpu_sample(scene, cfg, threads, REF_CG_ITERS[cfg.name], REF_ADMM_ITERS[cfg.name])
+    value = P * cfg.bands / T / 1e6
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
+            "warmup": warm, "requested": {"steps": args.steps, "warmup": args.warmup},
+            "ms_per_step": 1e3 * T, "higher_is_better": True, "scaling": job_mode(cfg, world)[1],
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator of BASELINE.json configs)",
-            "config": workload(cfg), "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc},
+            "config": job_config(cfg, world), "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc,
+                             "host_nproc": os.cpu_count()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-# CG / ADMM iteration counts of scene 0 of each config (GPU; oracle == GPU at C1/C2/C4 in
-# tests/test_gpu_pipeline.py); used only to extrapolate the bounded CPU sample.
-REF_CG_ITERS = {"C1": [160, 157, 157, 158], "C2": [124, 125, 124, 125], "C4": [148, 147, 147, 147],
-                "C3": [124, 123, 121, 120, 123, 123, 123, 121]}
-REF_ADMM_ITERS = {"C1": 153, "C2": 179, "C4": 161, "C3": 167}
+# CG / ADMM iteration counts of scene 0 of the large configs (GPU == oracle where both ran); used
+# only to scale the bounded CPU sample of C3 - C5 in the reference arm.
+REF_CG_ITERS = {"C3": [124, 123, 121, 120, 123, 123, 123, 121], "C4": [148, 147, 147, 147],
+                "C5": [103, 105, 103, 103, 105, 105, 103, 102]}
+REF_ADMM_ITERS = {"C3": 167, "C4": 161, "C5": 274}
+
+
+def job_mode(cfg, world):
+    """How the job is split over the ranks; shared by both arms."""
+    if cfg.scenes > 1:
+        return "scene-batch", "strong"
+    if cfg.name == "C3" and world > 1:
+        return "channel-shards", "strong"
+    if cfg.name == "C5" and world > 1:
+        return "row-strips", "strong"
+    return "replicas", "weak"
+
+
+def job_config(cfg, world) -> dict:
+    """The `config` dict of the JSON line (identical in both arms)."""
+    mode, _ = job_mode(cfg, world)
+    return workload(cfg) | {"parallelism": f"{mode} x{world}"}
 
 
 # ----------------------------------------------------------------------------------------------
@@ -199,28 +246,21 @@ def our_arm(args, cfg):
     #   channel shards (C3 on > 1 GPU): every rank repeats the per-scene setup, solves its bands;
     #   replicas (C1, C2, C5, C3 on 1 GPU): each rank solves its own scene of the config (weak).
     from paper_2103_09943_b200 import shard
-    if cfg.scenes > 1:
-        mode, scaling = "scene-batch", "strong"
-        mine = shard.partition(cfg.scenes, world, rank)
-        scenes = [synth.make_scene(cfg, i) for i in mine]
-        ch0, nch = 0, -1
-    elif cfg.name == "C3" and world > 1:
-        mode, scaling = "channel-shards", "strong"
+    mode, scaling = job_mode(cfg, world)
+    ch0, nch = 0, -1
+    if mode == "scene-batch":
+        scenes = [synth.make_scene(cfg, i) for i in shard.partition(cfg.scenes, world, rank)]
+    elif mode == "channel-shards":   # every rank repeats the per-scene setup and solves its bands
         scenes = [synth.make_scene(cfg, 0)]
         part = shard.partition(cfg.bands, world, rank)
         ch0, nch = part.start, len(part)
-    elif cfg.name == "C5" and world > 1:
-        # one 8192^2 scene on row strips: r-halo exchange + allreduces over NCCL every CG iteration
-        mode, scaling = "row-strips", "strong"
+    elif mode == "row-strips":       # one 8192^2 scene: r-halo exchange + allreduces every CG iteration
         scenes = [synth.make_scene(cfg, 0)]
-        ch0, nch = 0, -1
         uid = [fbmp.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         ctx.set_comm(uid[0], world, rank)
-    else:
-        mode, scaling = "replicas", "weak"
+    else:                            # replicas: each rank solves its own scene of the config (weak)
         scenes = [synth.make_scene(cfg, rank)]
-        ch0, nch = 0, -1
     scene = scenes[0]
     S = len(scenes)
     N, h, w = scene.lrms.shape
@@ -325,58 +365,72 @@ def our_arm(args, cfg):
     e2e = units / (t_e2e / 1e3) / 1e6
     s = 8
     p = h * w
-    NC = S * NO  # channels in one launch of the CG kernels on this rank
-    # algorithmic bytes per launch: only channels that are still iterating do work, so a launch
-    # moves (channel-iterations / launches) channels' worth (converged channels exit at once);
-    # the guide, mu_k and g_k maps are read per scene
+    # SURVEY 8(d) algorithmic bytes (compulsory HBM traffic of an ideally fused implementation).
+    # Only channels that are still iterating do work, so a launch moves (channel-iterations /
+    # launches) channels' worth (converged channels exit at their first instruction):
+    #   K_A = K_Q + K_D + K_L (the operator application): read r, p_old, I; write p, Ap -> 5 s P
+    #   K_U (axpys + norms): read z, r, p, Ap; write z, r                               -> 6 s P
     prof = {k: v for k, v in prof.items() if v["launches"] > 0}
     nlaunch = max(v["launches"] for v in prof.values())
     act = prof_ch_iters / max(nlaunch, 1)  # mean active channels per launch
-    alg = {"K_Q": (3 * s * P + s * p) * act,        # read r, p_old; write p_new, q
-           "K_D": (s * P + s * p) * act,            # read q; write d = B^T U q
-           "K_L": 3 * s * P * act + 3 * s * P * S,  # read p, d, guide/mu/g (per scene); write Ap
-           "K_U": 6 * s * P * act}                  # read z, r, p, Ap; write z, r
-    dom = max(prof, key=lambda k: prof[k]["total_ms"])
-    d = prof[dom]
-    avg_ms = d["total_ms"] / max(d["launches"], 1)
-    bytes_per_launch = alg[dom]
-    achieved = bytes_per_launch / (avg_ms / 1e3) / 1e9
+    avg = {k: v["total_ms"] / max(v["launches"], 1) for k, v in prof.items()}
+    ops = {"K_A": [k for k in ("K_Q", "K_D", "K_L") if k in avg], "K_U": ["K_U"]}
+    alg = {"K_A": 5 * s * P * act, "K_U": 6 * s * P * act}
+    op_ms = {o: sum(avg[k] for k in ks) for o, ks in ops.items()}
+    dom = max(op_ms, key=lambda o: op_ms[o])
+    achieved = alg[dom] / (op_ms[dom] / 1e3) / 1e9
     peak, kind = peaks()
-    traffic = None
+    traffic, traffic_src = None, None
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tfile):
         try:
             tj = json.load(open(tfile))
-            if tj.get("config", "C2") == cfg.name:  # the capture's own config only
-                traffic = tj.get(dom)
+            if tj.get("config", "C2") == cfg.name and all(k in tj for k in ops[dom]):  # the capture's own config
+                traffic = sum(tj[k] for k in ops[dom])
+                traffic_src = tj.get("source")
         except Exception:
             traffic = None
     cg_total = sum(v["total_ms"] for v in prof.values())
+    # whole solve: B = s P (5 S + sum_c (13 + 11 K_c)) over this rank's scenes and channels
+    K_all = stats["cg_iters"]
+    B_solve = s * P * (5 * S + sum(13 + 11 * k for k in K_all))
+    T_step = t_ms / args.steps / 1e3
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": dom, "peak_kind": kind,
-                "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms,
+                "traffic": traffic, "kernel": f"{dom} ({' + '.join(ops[dom])})", "peak_kind": kind,
+                "traffic_source": traffic_src,
+                "algorithmic_bytes_per_launch": alg[dom], "avg_launch_ms": op_ms[dom],
+                "active_channels_per_launch": act,
+                "operators": {o: {"kernels": ks, "avg_ms": op_ms[o], "algorithmic_bytes": alg[o],
+                                  "GB/s": alg[o] / (op_ms[o] / 1e3) / 1e9,
+                                  "frac": alg[o] / (op_ms[o] / 1e3) / 1e9 / peak} for o, ks in ops.items()},
+                "kernel_avg_ms": avg,
                 "kernel_share_of_cg": {k: v["total_ms"] / cg_total for k, v in prof.items()} if cg_total else None,
-                "cg_kernels": {k: {"launches": v["launches"], "avg_ms": v["total_ms"] / max(v["launches"], 1),
-                                   "GB/s": alg[k] / (v["total_ms"] / max(v["launches"], 1) / 1e3) / 1e9}
-                               for k, v in prof.items()}}
+                "whole_solve": {"algorithmic_bytes": B_solve, "GB/s": B_solve / T_step / 1e9,
+                                "frac": B_solve / T_step / 1e9 / peak}}
     h2d = S * (N * p + P) * 8
     d2h = S * (NO * P + n * n) * 8 + (N * 8 if mode == "replicas" else 0)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator of BASELINE.json configs)",
-            "config": workload(cfg) | {"parallelism": f"{mode} x{world}", "scenes_per_rank": S,
-                                       "bands_per_rank": NO},
+            "config": job_config(cfg, world),
+            "job": {"scenes_per_rank": S, "bands_per_rank": NO},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches, "roofline": roofline, "clocks": clk.summary(),
             "stages_ms": {"weights": stats["ms_weights"], "kernel_fit": stats["ms_kernel_fit"],
                           "pansharpen": stats["ms_pansharpen"]},
-            "iterations": {"admm": stats["admm_iters"], "cg": stats["cg_iters"][:NO]}}
+            "iterations": {"admm": stats["admm_iters"], "cg": stats["cg_iters"][:S * NO]}}
     if world == 1 and not args.no_cpu_baseline and cfg.hr <= 2048:
-        est, desc = cpu_sample(scene, cfg, min(os.cpu_count() or 1, N), cg_full=stats["cg_iters"][:N],
-                               admm_full=stats["admm_iters"])
-        cv = P * N / est / 1e6  # sample of one scene (the unit rate of the job)
-        line["cpu_baseline"] = {"value": cv, "unit": UNIT, "cores": min(os.cpu_count() or 1, N), "kind": "port",
-                                "sample": desc}
+        th = ref_threads(cfg)
+        if cfg.hr <= FULL_SOLVE_MAX_HR:  # one complete CPU solve of the same scene
+            est = cpu_full_solve(scene, cfg, th)
+            desc = (f"{ORACLE_DESC}: one complete blind solve of {cfg.name} scene {rank} ({cfg.bands} bands), "
+                    f"{th} channel threads (weights and kernel fit on 1 core), host nproc {os.cpu_count()}: "
+                    f"{est:.2f}s")
+        else:
+            est, desc = cpu_sample(scene, cfg, th, stats["cg_iters"][:N], stats["admm_iters"])
+        cv = P * N / est / 1e6  # one scene (the unit rate of the job)
+        line["cpu_baseline"] = {"value": cv, "unit": UNIT, "cores": th, "kind": "port", "sample": desc,
+                                "host_nproc": os.cpu_count()}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -74,6 +74,8 @@ typedef struct fbmp_gpu_stats {
     int cg_iters[64];    /* CG iterations per channel (first 64 channels) */
     double ms_weights, ms_kernel_fit, ms_pansharpen; /* device time of the stages */
     long long cg_channel_iters; /* sum of the CG iterations over all channels of the last solve */
+    int n_channels;      /* channels of the last solve (scenes x bands); cg_iters holds the first
+                            min(n_channels, 64): fbmp_gpu_ctx_cg_iters returns all of them */
 } fbmp_gpu_stats;
 
 void fbmp_gpu_default_ps_params(fbmp_ps_params* p);
@@ -85,6 +87,9 @@ int fbmp_gpu_ctx_create(int device, fbmp_gpu_ctx** out);
 void fbmp_gpu_ctx_destroy(fbmp_gpu_ctx* ctx);
 const char* fbmp_gpu_last_error(void);
 int fbmp_gpu_ctx_stats(fbmp_gpu_ctx* ctx, fbmp_gpu_stats* out);
+/* Per-channel CG iteration counts of the last solve (all scenes x bands, scene-major) into
+ * out[0 .. cap); returns the number of channels (which may exceed cap), or -1 on error. */
+int fbmp_gpu_ctx_cg_iters(fbmp_gpu_ctx* ctx, int* out, int cap);
 /* The context's cudaStream_t, as an opaque pointer (for device-resident callers). */
 void* fbmp_gpu_ctx_stream(fbmp_gpu_ctx* ctx);
 /* Number of kernels this library launched on the context so far (instrumentation). */

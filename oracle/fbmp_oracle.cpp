@@ -76,6 +76,11 @@ double seq_max(const double* a, size_t n) {
 }
 
 // ---- 1-D / 2-D DFT with FFTW's c2c conventions (fft_util.cpp:31-62) -------------------
+// (a b) for finite operands: the expression std::complex's operator* evaluates before its
+// NaN recovery branch (no FMA contraction: -ffp-contract=off), without that branch
+inline cd cmul_finite(cd a, cd b) {
+    return cd(a.real() * b.real() - a.imag() * b.imag(), a.real() * b.imag() + a.imag() * b.real());
+}
 class Dft1 {
 public:
     explicit Dft1(int n) : n_(n) {
@@ -97,6 +102,47 @@ public:
             }
         }
     }
+    // kB adjacent transforms at once (x[i * s + b], b < kB): the same operations per transform as
+    // run(), laid out so that the strided column pass of a 2-D FFT touches kB consecutive
+    // elements per row (cache blocking only; results are bit-identical to kB calls of run())
+    template <int kB>
+    void run_block(cd* x, size_t s, int sign, cd* scratch) const {
+        const int n = n_;
+        if (pow2_) {
+            for (int i = 0; i < n; ++i)
+                for (int b = 0; b < kB; ++b) scratch[static_cast<size_t>(rev_[i]) * kB + b] = x[i * s + b];
+            for (int len = 2; len <= n; len <<= 1) {
+                const int half = len >> 1, step = n / len;
+                for (int i = 0; i < n; i += len)
+                    for (int j = 0; j < half; ++j) {
+                        cd w = tw_[j * step];
+                        if (sign > 0) w = std::conj(w);
+                        cd* lo = scratch + static_cast<size_t>(i + j) * kB;
+                        cd* hi = scratch + static_cast<size_t>(i + j + half) * kB;
+                        for (int b = 0; b < kB; ++b) {
+                            const cd u = lo[b], v = cmul_finite(hi[b], w);
+                            lo[b] = u + v;
+                            hi[b] = u - v;
+                        }
+                    }
+            }
+            for (int i = 0; i < n; ++i)
+                for (int b = 0; b < kB; ++b) x[i * s + b] = scratch[static_cast<size_t>(i) * kB + b];
+        } else {
+            for (int k = 0; k < n; ++k) {
+                cd acc[kB];
+                for (int b = 0; b < kB; ++b) acc[b] = 0.0;
+                for (int j = 0; j < n; ++j) {
+                    cd w = tw_[(static_cast<long>(k) * j) % n];
+                    if (sign > 0) w = std::conj(w);
+                    for (int b = 0; b < kB; ++b) acc[b] += x[j * s + b] * w;
+                }
+                for (int b = 0; b < kB; ++b) scratch[static_cast<size_t>(k) * kB + b] = acc[b];
+            }
+            for (int k = 0; k < n; ++k)
+                for (int b = 0; b < kB; ++b) x[k * s + b] = scratch[static_cast<size_t>(k) * kB + b];
+        }
+    }
     // in-place, stride s; sign -1 forward (exp(-i..)), +1 backward (unnormalised)
     void run(cd* x, size_t s, int sign, cd* scratch) const {
         const int n = n_;
@@ -108,7 +154,7 @@ public:
                     for (int j = 0; j < half; ++j) {
                         cd w = tw_[j * step];
                         if (sign > 0) w = std::conj(w);
-                        const cd u = scratch[i + j], v = scratch[i + j + half] * w;
+                        const cd u = scratch[i + j], v = cmul_finite(scratch[i + j + half], w);
                         scratch[i + j] = u + v;
                         scratch[i + j + half] = u - v;
                     }
@@ -142,9 +188,12 @@ public:
     }
     size_t size() const { return static_cast<size_t>(r_) * c_; }
     void transform(cvec& a, int sign) const {
-        cvec scratch(std::max(r_, c_));
+        constexpr int kB = 16;  // columns per block of the column pass
+        cvec scratch(static_cast<size_t>(std::max(r_, c_)) * kB);
         for (int i = 0; i < r_; ++i) dc_.run(a.data() + static_cast<size_t>(i) * c_, 1, sign, scratch.data());
-        for (int j = 0; j < c_; ++j) dr_.run(a.data() + j, c_, sign, scratch.data());
+        int j = 0;
+        for (; j + kB <= c_; j += kB) dr_.run_block<kB>(a.data() + j, c_, sign, scratch.data());
+        for (; j < c_; ++j) dr_.run(a.data() + j, c_, sign, scratch.data());
     }
     cvec forward(const double* in) const {  // fft_util.cpp:31-39
         cvec a(size());

@@ -259,13 +259,12 @@ void pansharpen_strips_device(Context& ctx, const double* d_lrms, int N, int h, 
     trace("strips: cg");
     cg_iters.assign(N, 0);
     for (int i = 0; i < N; ++i) cg_iters[i] = hs[i].iters;
-    for (int i = 0; i < N; ++i) {
-        const std::string tag = "channel " + std::to_string(i) + ": ";
-        if (hs[i].done == 2) num_error(tag + "warmstart: conjugate gradients hit a non-positive curvature direction");
-        if (hs[i].done == 3)
-            num_error(tag + "warmstart: conjugate gradients did not converge in " + std::to_string(prm.cg_max_iter) +
-                      " iterations");
-    }
+    // every rank holds the same CG scalars (the dot products are allreduced), so every rank takes
+    // the same branch here; a non-positive curvature fails before the z0 exchange
+    for (int i = 0; i < N; ++i)
+        if (hs[i].done == 2)
+            num_error("channel " + std::to_string(i) +
+                      ": warmstart: conjugate gradients hit a non-positive curvature direction");
     // whole z0 planes: owned rows of every strip, in strip order
     double* zf = ctx.scratch<double>("st_zfull", P * N);
     if (dist) {
@@ -283,6 +282,26 @@ void pansharpen_strips_device(Context& ctx, const double* d_lrms, int N, int h, 
                                           static_cast<size_t>(hloc) * W * sizeof(double), cudaMemcpyDeviceToDevice,
                                           ctx.stream));
     }
+    // CG cap (pansharpen.cpp:257-262): the residual of the normal equations for the message,
+    // formed on every rank from the gathered z0 with the single-domain operator, so every rank
+    // raises the same error text as the single-domain path
+    for (int i = 0; i < N; ++i)
+        if (hs[i].done == 3) {
+            double* az = ctx.scratch<double>("cg_res_az", P);
+            double* rhs = ctx.scratch<double>("cg_res_rhs", P);
+            const PsGeo G1 = make_geo(1, h, w, c, n, prm.radius, prm.lambda, prm.eps);
+            cg_operator_apply(ctx, G1, d_taps, lpan, zf + i * P, az, 0);
+            data_rhs(ctx, G1, d_taps, xn + i * p, rhs);
+            std::vector<double> a(P), b(P);
+            d2h(a.data(), az, P * sizeof(double), ctx.stream);
+            d2h(b.data(), rhs, P * sizeof(double), ctx.stream);
+            FBMP_CUDA(cudaStreamSynchronize(ctx.stream));
+            double s2 = 0.0;
+            for (size_t k = 0; k < P; ++k) s2 += (a[k] - b[k]) * (a[k] - b[k]);
+            num_error("channel " + std::to_string(i) + ": warmstart: conjugate gradients did not converge in " +
+                      std::to_string(prm.cg_max_iter) + " iterations (residual " +
+                      std::to_string(std::sqrt(s2) / hs[i].rhs_norm) + " relative)");
+        }
     // post-processing: all channels here (virtual ranks), or the channels c with c mod G == rank
     double* v = ctx.scratch<double>("st_v", P * N);
     int* flag = ctx.scratch<int>("st_flag", N);
@@ -304,6 +323,9 @@ void pansharpen_strips_device(Context& ctx, const double* d_lrms, int N, int h, 
             if (ctx.rank == 0) FBMP_NCCL(ncclRecv(d_out + ch * P, P, ncclDouble, owner, cm, ctx.stream));
             if (ctx.rank == owner) FBMP_NCCL(ncclSend(d_out + ch * P, P, ncclDouble, 0, cm, ctx.stream));
         }
+        // each channel's condition flag lives on its owner only: combine them so that every rank
+        // raises the same "channel i: solve_channel_fft ..." error (or none)
+        FBMP_NCCL(ncclAllReduce(flag, flag, N, ncclInt, ncclMax, cm, ctx.stream));
         FBMP_NCCL(ncclGroupEnd());
     }
     std::vector<int> hf(N);
@@ -368,6 +390,8 @@ void blind_device(Context& ctx, const double* d_lrms, int S, int N, int h, int w
     ctx.stats.ms_pansharpen = d;
     ctx.stats.admm_iters = admm_iters.empty() ? 0 : admm_iters[0];
     for (int i = 0; i < 64; ++i) ctx.stats.cg_iters[i] = i < static_cast<int>(cg_iters.size()) ? cg_iters[i] : 0;
+    ctx.stats.n_channels = static_cast<int>(cg_iters.size());
+    ctx.cg_iters_all = cg_iters;
     ctx.stats.cg_channel_iters = 0;
     for (int it : cg_iters) ctx.stats.cg_channel_iters += it;
     cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2); cudaEventDestroy(e3);
@@ -456,6 +480,16 @@ int fbmp_gpu_ctx_create(int device, fbmp_gpu_ctx** out) {
 }
 void fbmp_gpu_ctx_destroy(fbmp_gpu_ctx* ctx) { delete ctx; }
 const char* fbmp_gpu_last_error(void) { return g_last_error.c_str(); }
+int fbmp_gpu_ctx_cg_iters(fbmp_gpu_ctx* ctx, int* out, int cap) {
+    if (!ctx || (cap > 0 && !out)) {
+        g_last_error = "fbmp_gpu_ctx_cg_iters: null argument";
+        return -1;
+    }
+    const auto& v = ctx->impl.cg_iters_all;
+    for (int i = 0; i < cap && i < static_cast<int>(v.size()); ++i) out[i] = v[i];
+    return static_cast<int>(v.size());
+}
+
 int fbmp_gpu_ctx_stats(fbmp_gpu_ctx* ctx, fbmp_gpu_stats* out) {
     *out = ctx->impl.stats;
     return FBMP_OK;
@@ -481,7 +515,9 @@ int fbmp_gpu_pansharpen(fbmp_gpu_ctx* ctx, const double* lrms, int N, int h, int
         std::vector<int> it;
         pansharpen_device(C, d_l, 1, N, h, w, d_p, d_k, n, factor, prm, d_o, it);
         download(C, out, d_o, P * N);
-        for (int i = 0; i < N && i < 64; ++i) C.stats.cg_iters[i] = it[i];
+        for (int i = 0; i < 64; ++i) C.stats.cg_iters[i] = i < N ? it[i] : 0;
+        C.stats.n_channels = N;
+        C.cg_iters_all = it;
         if (cg_iters)
             for (int i = 0; i < N; ++i) cg_iters[i] = it[i];
     });

@@ -106,6 +106,7 @@ struct Context {
     cudaStream_t stream = nullptr;
     long long launches = 0;
     fbmp_gpu_stats stats{};
+    std::vector<int> cg_iters_all;  // every channel of the last solve (stats.cg_iters keeps 64)
     std::map<std::string, std::unique_ptr<DevBuf<unsigned char>>> ws;
     std::map<std::tuple<int, int, int, int, int>, cufftHandle> plans;  // (kind, rows, cols, batch, 0)
     int sm_count = 148;

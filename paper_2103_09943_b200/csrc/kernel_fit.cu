@@ -218,15 +218,25 @@ __global__ void __launch_bounds__(NT) k_stats_partial(const double* __restrict__
         o[0] = bs; o[1] = mn[0]; o[2] = mx[0]; o[3] = ma[0];
     }
 }
+// one warp per scene (min / max are exact in any order; the sum only feeds the mean of the
+// degeneracy test, kernel_estimator.cpp:269-276, whose outcome does not depend on its last bits)
 __global__ void k_stats_final(const double* __restrict__ part, int nblk, double* __restrict__ stats) {
-    const int s = blockIdx.x;
-    if (threadIdx.x != 0) return;
+    const int s = blockIdx.x, lane = threadIdx.x;
     double sum = 0.0, lo = INFINITY, hi = -INFINITY, am = 0.0;
-    for (int b = 0; b < nblk; ++b) {
+    for (int b = lane; b < nblk; b += 32) {
         const double* o = part + (static_cast<size_t>(s) * nblk + b) * 4;
         sum += o[0]; lo = fmin(lo, o[1]); hi = fmax(hi, o[2]); am = fmax(am, o[3]);
     }
-    stats[s * 4 + 0] = sum; stats[s * 4 + 1] = lo; stats[s * 4 + 2] = hi; stats[s * 4 + 3] = am;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        am = fmax(am, __shfl_xor_sync(0xffffffffu, am, o));
+    }
+    if (lane == 0) {
+        stats[s * 4 + 0] = sum; stats[s * 4 + 1] = lo; stats[s * 4 + 2] = hi; stats[s * 4 + 3] = am;
+    }
 }
 
 // =============================================================================================
@@ -382,8 +392,18 @@ __global__ void k_reduce_tiles(const double* __restrict__ part, int S, int ntile
     for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < static_cast<long long>(S) * nv;
          e += static_cast<long long>(gridDim.x) * blockDim.x) {
         const long long s = e / nv, v = e - s * nv;
+        const double* pp = part + s * ntiles * nv + v;
         double acc = 0.0;
-        for (int t = 0; t < ntiles; ++t) acc += part[(s * ntiles + t) * nv + v];
+        int t = 0;
+        // tile order kept (sequential sum); loads issued 16 ahead of the additions
+        for (; t + 16 <= ntiles; t += 16) {
+            double x[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) x[k] = __ldg(pp + static_cast<long long>(t + k) * nv);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) acc += x[k];
+        }
+        for (; t < ntiles; ++t) acc += __ldg(pp + static_cast<long long>(t) * nv);
         out[e] = acc;
     }
 }
@@ -634,6 +654,16 @@ struct AdmmArgs {
 };
 
 constexpr int NTADMM = 512;
+#ifdef FBMP_ADMM_PROF  // phase timers of k_admm (thread 0, clock64), A/B diagnostics only
+__device__ long long g_admm_prof[16];
+#define APROF_T0 long long _ap_t = clock64(), _ap_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#define APROF(k) if (threadIdx.x == 0 && blockIdx.x == 0) { const long long _n = clock64(); _ap_acc[k] += _n - _ap_t; _ap_t = _n; }
+#define APROF_END if (threadIdx.x == 0 && blockIdx.x == 0) for (int _k = 0; _k < 8; ++_k) g_admm_prof[_k] = _ap_acc[_k];
+#else
+#define APROF_T0
+#define APROF(k)
+#define APROF_END
+#endif
 // projection scratch of the sorted (m <= NTADMM) projection; none for the rank-based one
 __host__ __device__ constexpr int admm_scratch_doubles(int m) {
     return m <= NTADMM ? (6 * m > 3 * NTADMM ? 6 * m : 3 * NTADMM) : 0;
@@ -1103,6 +1133,7 @@ __global__ void __launch_bounds__(NTADMM) k_admm(AdmmArgs A, const double* __res
     const double t1 = 1.0 / A.mu1, t2 = 1.0 / A.mu2;
     int status = 0, iters = A.t_begin, t = A.t_begin;
     int phase = A.phase_begin;
+    APROF_T0
     for (; t < A.t_max; ++t) {
         if (phase == 0) {
             // x-step and y-step (kernel_estimator.cpp:325-337), z-step right-hand side (:340)
@@ -1132,6 +1163,7 @@ __global__ void __launch_bounds__(NTADMM) k_admm(AdmmArgs A, const double* __res
                 S.bz[i] = Etf[i] + A.mu3 * (u[i] + FLD(F_L3)[i]);
             }
             __syncthreads();
+            APROF(0)
             // z = project_simplex((E^T E + mu3 I)^-1 (E^T f + mu3 (u + L3)))   (:341, :79-83)
             if (CS > 1) {
                 double* mine = zsl + (t & 1) * RP;
@@ -1167,11 +1199,14 @@ __global__ void __launch_bounds__(NTADMM) k_admm(AdmmArgs A, const double* __res
                 }
             }
             __syncthreads();
+            APROF(1)
             bool finite = true;
             for (int i = threadIdx.x; i < m; i += blockDim.x) finite = finite && isfinite(S.zz[i]);
             if (!__syncthreads_and(finite)) { status = 3; iters = t; break; }
+            APROF(2)
             const int support = m <= NTADMM ? project_simplex_sorted(S.zz, FLD(F_Z), m, S.red, ired, S.tmp6)
                                              : project_simplex_block(S.zz, FLD(F_Z), m, S.red, ired);
+            APROF(3)
             if (support == 0) { status = 3; iters = t; break; }
             if (t == A.hook_t) { status = 4; break; }
         }
@@ -1179,9 +1214,11 @@ __global__ void __launch_bounds__(NTADMM) k_admm(AdmmArgs A, const double* __res
         // {u,p}-step with the mu3 tie to z - L3 (:349-355)
         for (int i = threadIdx.x; i < m; i += blockDim.x) S.bz[i] = FLD(F_Z)[i] - FLD(F_L3)[i];
         __syncthreads();
+        APROF(4)
         // old p1, p2 are dead after the y-step: the solve writes them in place, u_new separately
         up_solve(S, n, a1m1, a2m2, A.coupling, FLD(F_X0), FLD(F_X1), FLD(F_Y0), FLD(F_Y1), FLD(F_Y2), FLD(F_Y3), FLD(F_L10),
                  FLD(F_L11), FLD(F_L20), FLD(F_L21), FLD(F_L22), FLD(F_L23), S.bz, Unew, FLD(F_P1), FLD(F_P2));
+        APROF(5)
         // multipliers (:367-373), change of u (:375-376)
         double dd = 0.0, un = 0.0;
         bool fin_u = true, fin_z = true;
@@ -1217,10 +1254,12 @@ __global__ void __launch_bounds__(NTADMM) k_admm(AdmmArgs A, const double* __res
             Unew = tmp;
         }
         iters = t + 1;
+        APROF(6)
         if (!all_u) { status = 1; break; }  // check_finite (:379-380)
         if (!all_z) { status = 2; break; }
         if (delta / scale < A.th) { ++t; break; }
     }
+    APROF_END
     if (crank == 0) {
         for (int e = threadIdx.x; e < 17 * m; e += blockDim.x) gstate[e] = FLD(e / m)[e % m];
         if (k_out)
@@ -1519,6 +1558,16 @@ void admm_device(Context& ctx, const ObsSystem& sys, const fbmp_ke_params& prm, 
                                  static_cast<const double*>(sys.Etf), d_state, d_info, d_k, cs));
     ctx.count();
     check_launch();
+#ifdef FBMP_ADMM_PROF
+    {
+        long long pr[16];
+        FBMP_CUDA(cudaMemcpyFromSymbolAsync(pr, g_admm_prof, sizeof(pr), 0, cudaMemcpyDeviceToHost, ctx.stream));
+        FBMP_CUDA(cudaStreamSynchronize(ctx.stream));
+        std::fprintf(stderr, "admm prof n=%d cs=%d:", sys.n, cs);
+        for (int k = 0; k < 7; ++k) std::fprintf(stderr, " %lld", pr[k]);
+        std::fprintf(stderr, "\n");
+    }
+#endif
 }
 
 void admm_device(Context& ctx, const ObsSystem& sys, const fbmp_ke_params& prm, double* d_state, bool init_state,
@@ -1704,7 +1753,7 @@ void estimate_kernel_l2_device(Context& ctx, const double* d_pan, const double* 
     d2h(&hst, sys.status, sizeof(int), ctx.stream);
     FBMP_CUDA(cudaStreamSynchronize(ctx.stream));
     if (hst) num_error("l2 kernel estimation: normal matrix factorization failed");
-    if (hinfo[1] == 1) num_error("l2 kernel estimation diverged at iteration " + std::to_string(hinfo[0] - 1));
+    if (hinfo[1] == 1) num_error("l2 kernel estimation diverged at iteration " + std::to_string(hinfo[0]));  // t of the failing iteration (:423)
     if (hinfo[1] == 3) num_error("project_simplex: empty support (non-finite input?)");
     if (iters) *iters = hinfo[0];
 }

@@ -837,16 +837,17 @@ __global__ void k_unscale(const double* __restrict__ zr, long long n, double inv
 }
 
 // ops.cpp:9-22 embed_kernel
+// n <= H, W (checked by the callers): the taps land on distinct positions of the zeroed plane,
+// so each is stored once (= 0 + tap, the reference's accumulation)
 __global__ void k_embed(const double* __restrict__ taps, int n, int H, int W, double* __restrict__ out) {
-    if (threadIdx.x != 0) return;
     taps += static_cast<size_t>(blockIdx.x) * n * n;
     out += static_cast<size_t>(blockIdx.x) * H * W;
     const int C = (n - 1) / 2;
-    for (int r = 0; r < n; ++r)
-        for (int q = 0; q < n; ++q) {
-            const int rr = wrapi(r - C, H), cc = wrapi(q - C, W);
-            out[static_cast<size_t>(rr) * W + cc] += taps[r * n + q];
-        }
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+        const int r = e / n, q = e - r * n;
+        const int rr = wrapi(r - C, H), cc = wrapi(q - C, W);
+        out[static_cast<size_t>(rr) * W + cc] = 0.0 + taps[e];
+    }
 }
 
 // ---- small helpers ---------------------------------------------------------------------------
@@ -868,10 +869,11 @@ __global__ void k_max_partial(const double* __restrict__ a, long long n, const d
     if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
 }
 __global__ void k_peak_final(const double* __restrict__ part, int nb, double* __restrict__ scale) {
-    if (threadIdx.x != 0) return;
-    double m = -INFINITY;
-    for (int i = 0; i < nb; ++i) m = fmax(m, part[static_cast<size_t>(blockIdx.x) * nb + i]);
-    scale[blockIdx.x] = m > 0.0 ? 1.0 / m : 1.0;  // pansharpen.cpp:374-376
+    double m = -INFINITY;  // one warp per scene (max is exact in any order)
+    for (int i = threadIdx.x; i < nb; i += 32) m = fmax(m, part[static_cast<size_t>(blockIdx.x) * nb + i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) scale[blockIdx.x] = m > 0.0 ? 1.0 / m : 1.0;  // pansharpen.cpp:374-376
 }
 __global__ void k_scale_copy(const double* __restrict__ in, long long n, const double* __restrict__ s,
                              long long per, double* __restrict__ out) {
@@ -1583,7 +1585,7 @@ void solve_channel_fft(Context& ctx, const PsGeo& G, const double* d_taps, const
     double2* xh = ctx.scratch<double2>("fft_xh", LS * N);
     double* zr = ctx.scratch<double>("fft_zr", P * N);
     FBMP_CUDA(cudaMemsetAsync(emb, 0, P * S * sizeof(double), ctx.stream));
-    k_embed<<<S, 32, 0, ctx.stream>>>(d_taps, G.n, H, W, emb);
+    k_embed<<<S, 256, 0, ctx.stream>>>(d_taps, G.n, H, W, emb);
     ctx.count();
     FBMP_CUFFT(cufftExecD2Z(ctx.plan(0, H, W, S), emb, reinterpret_cast<cufftDoubleComplex*>(bh)));
     FBMP_CUFFT(cufftExecD2Z(ctx.plan(0, H, W, N), const_cast<double*>(d_v), reinterpret_cast<cufftDoubleComplex*>(vh)));

@@ -66,7 +66,8 @@ class _SwParams(C.Structure):
 
 class _Stats(C.Structure):
     _fields_ = [("admm_iters", C.c_int), ("cg_iters", C.c_int * 64), ("ms_weights", C.c_double),
-                ("ms_kernel_fit", C.c_double), ("ms_pansharpen", C.c_double), ("cg_channel_iters", C.c_longlong)]
+                ("ms_kernel_fit", C.c_double), ("ms_pansharpen", C.c_double), ("cg_channel_iters", C.c_longlong),
+                ("n_channels", C.c_int)]
 
 
 @dataclass
@@ -125,6 +126,8 @@ _lib.fbmp_gpu_ctx_launches.restype = C.c_longlong
 _lib.fbmp_gpu_ctx_launches.argtypes = [C.c_void_p]
 _lib.fbmp_gpu_ctx_stats.argtypes = [C.c_void_p, C.POINTER(_Stats)]
 _lib.fbmp_gpu_ctx_set_profile.argtypes = [C.c_void_p, C.c_int]
+_lib.fbmp_gpu_ctx_cg_iters.restype = C.c_int
+_lib.fbmp_gpu_ctx_cg_iters.argtypes = [C.c_void_p, C.POINTER(C.c_int), C.c_int]
 
 
 def _check(status: int) -> None:
@@ -177,7 +180,12 @@ class Context:
     def stats(self) -> dict:
         s = _Stats()
         _check(_lib.fbmp_gpu_ctx_stats(self.h, C.byref(s)))
-        return dict(admm_iters=s.admm_iters, cg_iters=list(s.cg_iters), ms_weights=s.ms_weights,
+        n = _lib.fbmp_gpu_ctx_cg_iters(self.h, None, 0)
+        if n < 0:
+            raise FbmpError(_lib.fbmp_gpu_last_error().decode())
+        its = (C.c_int * max(n, 1))()
+        _lib.fbmp_gpu_ctx_cg_iters(self.h, its, n)
+        return dict(admm_iters=s.admm_iters, cg_iters=list(its)[:n], ms_weights=s.ms_weights,
                     ms_kernel_fit=s.ms_kernel_fit, ms_pansharpen=s.ms_pansharpen,
                     cg_channel_iters=s.cg_channel_iters)
 
@@ -677,7 +685,7 @@ def blind_dev(d_lrms: int, N: int, h: int, w: int, d_pan: int, d_out: int, d_k: 
 
 EXPORTED_SYMBOLS = (
     "fbmp_gpu_default_ps_params", "fbmp_gpu_default_ke_params", "fbmp_gpu_default_sw_params",
-    "fbmp_gpu_ctx_create", "fbmp_gpu_ctx_destroy", "fbmp_gpu_last_error", "fbmp_gpu_ctx_stats",
+    "fbmp_gpu_ctx_create", "fbmp_gpu_ctx_destroy", "fbmp_gpu_last_error", "fbmp_gpu_ctx_stats", "fbmp_gpu_ctx_cg_iters",
     "fbmp_gpu_ctx_stream", "fbmp_gpu_ctx_launches", "fbmp_gpu_ctx_set_profile", "fbmp_gpu_ctx_kernel_profile",
     "fbmp_gpu_metrics", "fbmp_gpu_estimate_kernel_l2_plane",
     "fbmp_gpu_blind_batch_dev", "fbmp_gpu_blind_strips_dev", "fbmp_gpu_nccl_unique_id", "fbmp_gpu_ctx_set_comm",

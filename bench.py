@@ -36,6 +36,7 @@ sys.path.insert(0, ROOT)
 from paper_2103_09943_b200 import synth  # noqa: E402
 
 METRIC = "HRMS Mpixel·bands/s per blind-pansharpen solve, 1–8 B200; % HBM roofline"
+PRECISION = 64  # --precision: 64 (reference arithmetic, the headline) or 32 (north_star's fp32 mode)
 UNIT = "Mpixel*bands/s"
 
 
@@ -54,7 +55,10 @@ def workload(cfg: synth.SceneConfig) -> dict:
                         f"shift +-{cfg.shift:g} px; blind solve = spectral weights + TGV^2 kernel fit "
                         f"(n={cfg.support}) + LLP HRMS solve of every band",
             "config": cfg.name, "pan": cfg.hr, "bands": cfg.bands, "ratio": cfg.ratio, "kernel_n": cfg.support,
-            "l2": "flushed before every timed step (512 MB write)", "precision": "fp64 (reference precision)"}
+            "l2": "flushed before every timed step (512 MB write)",
+            "precision": "fp64 (reference precision)" if PRECISION == 64 else
+                         "fp32 mode (HRMS CG vectors / stencils fp32, reductions and CG scalars fp64; fit, "
+                         "guided filter and alias solve fp64)"}
 
 
 # ----------------------------------------------------------------------------------------------
@@ -240,6 +244,7 @@ def our_arm(args, cfg):
     from paper_2103_09943_b200 import fbmp
 
     ctx = fbmp.Context(local)
+    ctx.set_precision(PRECISION)
     stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
     # how the job is split over the ranks:
     #   scene batch (C4): the 64 scenes are partitioned, each rank solves its block as one batch;
@@ -363,7 +368,7 @@ def our_arm(args, cfg):
     units = args.steps * job_units
     value = units / (t_ms / 1e3) / 1e6
     e2e = units / (t_e2e / 1e3) / 1e6
-    s = 8
+    s = 8 if PRECISION == 64 else 4  # bytes per CG-vector element
     p = h * w
     # SURVEY 8(d) algorithmic bytes (compulsory HBM traffic of an ideally fused implementation).
     # Only channels that are still iterating do work, so a launch moves (channel-iterations /
@@ -411,7 +416,7 @@ def our_arm(args, cfg):
     d2h = S * (NO * P + n * n) * 8 + (N * 8 if mode == "replicas" else 0)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": scaling,
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator of BASELINE.json configs)",
+            "vs_baseline": None, "dtype": "f64" if PRECISION == 64 else "f32", "data": "synthetic (seeded generator of BASELINE.json configs)",
             "config": job_config(cfg, world),
             "job": {"scenes_per_rank": S, "bands_per_rank": NO},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
@@ -444,7 +449,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2", choices=sorted(synth.CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--precision", type=int, default=64, choices=[32, 64])
     args = ap.parse_args()
+    global PRECISION
+    PRECISION = args.precision
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     cfg = synth.CONFIGS[args.config]
     if args.impl == "reference":

@@ -99,6 +99,14 @@ long long fbmp_gpu_ctx_launches(fbmp_gpu_ctx* ctx);
  * {K_Q (p update + D B p), K_D (B^T U q), K_L (+ lambda L M L p, p.Ap), K_U (axpys + norms)};
  * with the single-kernel operator (env FBMP_KA=4) K_D is empty and K_L holds K_A. */
 void fbmp_gpu_ctx_set_profile(fbmp_gpu_ctx* ctx, int on);
+/* Precision of the HRMS conjugate-gradient loop (the hot path): 64 (default, the reference's
+ * fp64 arithmetic) or 32 (fp32 mode of BASELINE.json's north_star: CG vectors, taps, guide and
+ * window maps stored and stenciled in fp32; every dot product, norm and CG scalar in fp64; the
+ * kernel fit, guided filter and alias-group solve stay fp64). The fp32 mode needs the specialised
+ * operator (radius 1, factor 2 or 4, supported kernel side, images >= 64 x 64, even width) and the
+ * single-domain path (not row strips); otherwise the solve fails with FBMP_PARAM. Returns a status. */
+int fbmp_gpu_ctx_set_precision(fbmp_gpu_ctx* ctx, int bits);
+int fbmp_gpu_ctx_precision(fbmp_gpu_ctx* ctx);
 int fbmp_gpu_ctx_kernel_profile(fbmp_gpu_ctx* ctx, double* total_ms, long long* launches);
 
 /* ---- full pipeline ----------------------------------------------------------------------- */
@@ -114,6 +122,17 @@ int fbmp_gpu_pansharpen(fbmp_gpu_ctx* ctx, const double* lrms, int N, int h, int
    mu3, rho, t_max, th, init are used. k_out: n*n; iters: ADMM iterations (optional). */
 int fbmp_gpu_estimate_kernel_l2_plane(fbmp_gpu_ctx* ctx, const double* pan, int H, int W, const double* obs,
                                       int factor, const fbmp_ke_params* params, double* k_out, int* iters);
+/* TV kernel prior: estimate_kernel_plane with KernelPrior::tv (kernel_estimator.cpp:445-452,
+   run_tgv_or_tv(false, ...) :291-387): same scaling, errors and ADMM as the TGV path with p = 0
+   and the u-step divided by the scalar symbol alpha1 mu1 |grad|^2 + mu3; alpha2 / mu2 unused.
+   state_out / hook_t as fbmp_gpu_estimate_kernel_plane (p, y, L2 stay zero). */
+int fbmp_gpu_estimate_kernel_tv_plane(fbmp_gpu_ctx* ctx, const double* pan, int H, int W, const double* obs,
+                                      int factor, const fbmp_ke_params* params, double* k_out, int* iters,
+                                      double* state_out, int hook_t);
+/* estimate_kernel_tv (kernel_estimator.hpp:120-123): combine_bands(lrms, omega) then the TV fit. */
+int fbmp_gpu_estimate_kernel_tv(fbmp_gpu_ctx* ctx, const double* lrms_subset, int nb, int h, int w,
+                                const double* pan, const double* omega, int factor,
+                                const fbmp_ke_params* params, double* k_out, int* iters);
 /* estimate_kernel_tgv (kernel_estimator.hpp:114-118): combine_bands(lrms, omega) then the
  * TGV^2 fit. k_out: n*n. iters (optional) receives the ADMM iteration count. */
 int fbmp_gpu_estimate_kernel_tgv(fbmp_gpu_ctx* ctx, const double* lrms_subset, int nb, int h, int w,

@@ -941,6 +941,7 @@ struct KeParams {
     int t_max = 10000;
     double th = 1e-5;
     int init = 0;  // 0 dirac, 1 uniform
+    bool with_p = true;  // run_tgv_or_tv's branch: true = TGV^2, false = TV (no p, no y-step)
 };
 
 void validate(const KeParams& p) {  // kernel_estimator.cpp:36-45
@@ -1182,7 +1183,8 @@ struct AdmmState {  // kernel_estimator.hpp:85-94 (u,p1,p2,x[2],y[4],z,L1[2],L2[
     int iterations = 0;
 };
 
-// kernel_estimator.cpp:269-276, 438-455, 291-387 (TGV^2 branch, with_p = true)
+// kernel_estimator.cpp:269-276, 438-455, 291-387 (TGV^2 branch, with_p = true; TV branch,
+// with_p = false: no y-step, u from the scalar symbol d1 of :309-321 / :356-364)
 thread_local std::chrono::steady_clock::time_point* g_setup_mark = nullptr;
 vec estimate_kernel_plane_tgv(const double* pan, int H, int W, const double* obs, int h, int w, int factor,
                               const KeParams& prm, int* iters_out, AdmmState* final_state, int t_stop_hook = -1) {
@@ -1234,7 +1236,7 @@ vec estimate_kernel_plane_tgv(const double* pan, int H, int W, const double* obs
             x[0] = std::move(gh);
             x[1] = std::move(gv);
         }
-        {  // y-step
+        if (prm.with_p) {  // y-step
             vec ep[4];
             symgrad(p1, p2, ep);
             for (int j = 0; j < 4; ++j)
@@ -1261,20 +1263,45 @@ vec estimate_kernel_plane_tgv(const double* pan, int H, int W, const double* obs
         }
         vec anchor(m);
         for (size_t i = 0; i < m; ++i) anchor[i] = z[i] - L3[i];
-        Up sol = solve_up_core(x, y, L1, L2, prm, n, prm.mu3, &anchor);
+        Up sol;
+        if (prm.with_p) {
+            sol = solve_up_core(x, y, L1, L2, prm, n, prm.mu3, &anchor);
+            p1 = std::move(sol.p1);
+            p2 = std::move(sol.p2);
+        } else {  // kernel_estimator.cpp:356-364
+            const double a1m1 = prm.alpha1 * prm.mu1;
+            vec x1(m), x2(m);
+            for (size_t i = 0; i < m; ++i) {
+                x1[i] = x[0][i] - L1[0][i];
+                x2[i] = x[1][i] - L1[1][i];
+            }
+            vec g1 = diff(x1.data(), n, n, GH, true), g2 = diff(x2.data(), n, n, GV, true);
+            vec B1(m);
+            for (size_t i = 0; i < m; ++i) B1[i] = (g1[i] + g2[i]) * a1m1 + anchor[i] * prm.mu3;
+            Fft2 fft(n, n);
+            cvec FB = fft.forward(B1.data());
+            for (int r = 0; r < n; ++r) {  // :309-321
+                const double av2 = 2.0 - 2.0 * std::cos(2.0 * M_PI * r / n);
+                for (int c = 0; c < n; ++c) {
+                    const double ah2 = 2.0 - 2.0 * std::cos(2.0 * M_PI * c / n);
+                    FB[static_cast<size_t>(r) * n + c] /= prm.alpha1 * prm.mu1 * (ah2 + av2) + prm.mu3;
+                }
+            }
+            sol.u = fft.backward_real(std::move(FB));
+        }
         vec& un = sol.u;
-        p1 = std::move(sol.p1);
-        p2 = std::move(sol.p2);
         {  // multipliers
             vec gh = diff(un.data(), n, n, GH, false), gv = diff(un.data(), n, n, GV, false);
             for (size_t i = 0; i < m; ++i) {
                 L1[0][i] += (gh[i] - p1[i] - x[0][i]) * prm.rho;
                 L1[1][i] += (gv[i] - p2[i] - x[1][i]) * prm.rho;
             }
-            vec ep[4];
-            symgrad(p1, p2, ep);
-            for (int j = 0; j < 4; ++j)
-                for (size_t i = 0; i < m; ++i) L2[j][i] += (ep[j][i] - y[j][i]) * prm.rho;
+            if (prm.with_p) {
+                vec ep[4];
+                symgrad(p1, p2, ep);
+                for (int j = 0; j < 4; ++j)
+                    for (size_t i = 0; i < m; ++i) L2[j][i] += (ep[j][i] - y[j][i]) * prm.rho;
+            }
             for (size_t i = 0; i < m; ++i) L3[i] += (un[i] - z[i]) * prm.rho;
         }
         vec du(m);
@@ -1594,6 +1621,24 @@ int orc_estimate_kernel_plane(const double* pan, int H, int W, const double* obs
         AdmmState st;
         vec z = estimate_kernel_plane_tgv(pan, H, W, obs, H / factor, W / factor, factor, p, iters,
                                           state_out ? &st : nullptr, hook_t);
+        put(z, k_out);
+        if (state_out) {
+            const size_t m = static_cast<size_t>(n) * n;
+            for (int j = 0; j < 17; ++j) std::memcpy(state_out + j * m, st.f[j].data(), m * sizeof(double));
+        }
+    });
+}
+// TV kernel prior (estimate_kernel_plane(KernelPrior::tv, ...), kernel_estimator.cpp:445-452)
+int orc_estimate_kernel_plane_tv(const double* pan, int H, int W, const double* obs, int factor, int n, double alpha1,
+                                 double mu1, double mu3, double rho, int t_max, double th, int init, double* k_out,
+                                 int* iters, double* state_out) {
+    return guard([&] {
+        KeParams p;
+        p.n = n; p.alpha1 = alpha1; p.mu1 = mu1; p.mu3 = mu3; p.rho = rho;
+        p.t_max = t_max; p.th = th; p.init = init; p.with_p = false;
+        AdmmState st;
+        vec z = estimate_kernel_plane_tgv(pan, H, W, obs, H / factor, W / factor, factor, p, iters,
+                                          state_out ? &st : nullptr);
         put(z, k_out);
         if (state_out) {
             const size_t m = static_cast<size_t>(n) * n;

@@ -292,6 +292,24 @@ def estimate_kernel_plane(pan, obs, factor, n, want_state=False, hook_t=-1, **kw
     return k, it.value
 
 
+def estimate_kernel_plane_tv(pan, obs, factor, n, want_state=False, **kw):
+    """kernel_estimator.cpp:438-455 with KernelPrior::tv (run_tgv_or_tv(false, ...), :291-387)
+    -> (kernel, iterations[, state dict]); alpha2 / mu2 are unused by the TV branch."""
+    p = dict(KE_DEFAULTS)
+    p.update(kw)
+    pan, obs = _f(pan), _f(obs)
+    k = np.empty((n, n))
+    it = C.c_int(0)
+    st = np.empty((17, n, n)) if want_state else None
+    _check(lib().orc_estimate_kernel_plane_tv(
+        _p(pan), pan.shape[0], pan.shape[1], _p(obs), factor, n, C.c_double(p["alpha1"]), C.c_double(p["mu1"]),
+        C.c_double(p["mu3"]), C.c_double(p["rho"]), int(p["t_max"]), C.c_double(p["th"]), int(p["init"]), _p(k),
+        C.byref(it), None if st is None else _p(st)))
+    if st is not None:
+        return k, it.value, dict(zip(STATE_FIELDS, st))
+    return k, it.value
+
+
 def tgv_objective(pan, obs, factor, n, u, p1, p2, mu3=100.0, alpha1=1.0, alpha2=0.006):
     pan, obs, u, p1, p2 = map(_f, (pan, obs, u, p1, p2))
     v = C.c_double(0)

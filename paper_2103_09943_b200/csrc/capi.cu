@@ -104,16 +104,38 @@ void pansharpen_device(Context& ctx, const double* d_lrms, int S, int N, int h, 
 
     CgBuffers B;
     B.z = ctx.scratch<double>("cg_z", P * NC);
-    B.r = ctx.scratch<double>("cg_r", P * NC);
-    B.p = ctx.scratch<double>("cg_p", 2 * P * NC);
-    B.Ap = ctx.scratch<double>("cg_ap", P * NC);
-    B.q = ctx.scratch<double>("cg_q", p * NC);
     const size_t nbmax = (P / 256 + 64) * 2 + 4096;
     B.part = ctx.scratch<double>("cg_part", 4 * nbmax * NC);
     B.st = ctx.scratch<CgState>("cg_state", NC);
     std::vector<CgState> hs;
     trace("ps: prologue");
-    cg_solve(ctx, G, d_taps, lpan, xn, B, prm.cg_max_iter, prm.cg_tol, hs);
+    if (ctx.precision == 32) {
+        // fp32 mode: the CG vectors, taps, guide and its window maps in fp32; every dot product,
+        // norm and CG scalar in fp64. The warm start is widened to fp64 for the guided filter and
+        // the alias-group solve, which stay fp64 (once per channel).
+        CgBuffersT<float> F;
+        F.z = ctx.scratch<float>("cg32_z", P * NC);
+        F.r = ctx.scratch<float>("cg32_r", P * NC);
+        F.p = ctx.scratch<float>("cg32_p", 2 * P * NC);
+        F.Ap = ctx.scratch<float>("cg32_ap", P * NC);
+        F.q = ctx.scratch<float>("cg32_q", p * NC);
+        F.part = B.part;
+        F.st = B.st;
+        float* taps32 = ctx.scratch<float>("ps32_taps", static_cast<size_t>(S) * n * n);
+        float* lpan32 = ctx.scratch<float>("ps32_lpan", P * S);
+        float* xn32 = ctx.scratch<float>("ps32_xn", p * NC);
+        to_f32(ctx, d_taps, static_cast<long long>(S) * n * n, taps32);
+        to_f32(ctx, lpan, static_cast<long long>(P) * S, lpan32);
+        to_f32(ctx, xn, static_cast<long long>(p) * NC, xn32);
+        cg_solve_f32(ctx, G, taps32, lpan, lpan32, xn32, F, prm.cg_max_iter, prm.cg_tol, hs);
+        to_f64(ctx, F.z, static_cast<long long>(P) * NC, B.z);
+    } else {
+        B.r = ctx.scratch<double>("cg_r", P * NC);
+        B.p = ctx.scratch<double>("cg_p", 2 * P * NC);
+        B.Ap = ctx.scratch<double>("cg_ap", P * NC);
+        B.q = ctx.scratch<double>("cg_q", p * NC);
+        cg_solve(ctx, G, d_taps, lpan, xn, B, prm.cg_max_iter, prm.cg_tol, hs);
+    }
     cg_iters.assign(NC, 0);
     for (int i = 0; i < NC; ++i) cg_iters[i] = hs[i].iters;
     if (std::getenv("FBMP_CG_DEBUG"))  // final CG scalars per channel (debugging aid)
@@ -192,6 +214,7 @@ void pansharpen_strips_device(Context& ctx, const double* d_lrms, int N, int h, 
                               const double* d_taps, int n, int c, const fbmp_ps_params& prm, double* d_out,
                               std::vector<int>& cg_iters, int vstrips) {
     validate_ps(prm);
+    if (ctx.precision != 64) param_error("pansharpen: the fp32 mode is not available for row strips");
     const int H = h * c, W = w * c;
     if (2 * prm.radius + 1 > std::min(H, W)) dim_error("matting matrix: window larger than image");
     check_kernel(n, H, W);
@@ -801,7 +824,8 @@ int fbmp_gpu_combine_bands(fbmp_gpu_ctx* ctx, const double* lrms_subset, int nb,
 }
 
 static void estimate_plane_host(Context& C, const double* pan, int H, int W, const double* obs, int factor,
-                                const fbmp_ke_params& prm, double* k_out, int* iters, double* state_out, int hook_t) {
+                                const fbmp_ke_params& prm, double* k_out, int* iters, double* state_out, int hook_t,
+                                bool tv = false) {
     validate_ke(prm);
     if (factor < 1) param_error("build_observation: factor must be >= 1");
     if (H % factor || W % factor) dim_error("build_observation: PAN dimensions must be factor times the observation");
@@ -812,7 +836,7 @@ static void estimate_plane_host(Context& C, const double* pan, int H, int W, con
     double* d_k = C.scratch<double>("api_k", m);
     double* d_s = state_out ? C.scratch<double>("api_state", static_cast<size_t>(17) * m) : nullptr;
     std::vector<int> it;
-    estimate_kernel_device(C, d_p, d_f, 1, H, W, factor, prm, d_k, it, d_s, hook_t);
+    estimate_kernel_device(C, d_p, d_f, 1, H, W, factor, prm, d_k, it, d_s, hook_t, tv);
     download(C, k_out, d_k, m);
     if (d_s) download(C, state_out, d_s, static_cast<size_t>(17) * m);
     if (iters) *iters = it[0];
@@ -826,6 +850,36 @@ int fbmp_gpu_estimate_kernel_plane(fbmp_gpu_ctx* ctx, const double* pan, int H, 
         Context& C = ctx->impl;
         DeviceGuard dg(C.device);
         estimate_plane_host(C, pan, H, W, obs, factor, ke_or_default(params), k_out, iters, state_out, hook_t);
+    });
+}
+
+int fbmp_gpu_estimate_kernel_tv_plane(fbmp_gpu_ctx* ctx, const double* pan, int H, int W, const double* obs,
+                                      int factor, const fbmp_ke_params* params, double* k_out, int* iters,
+                                      double* state_out, int hook_t) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        estimate_plane_host(C, pan, H, W, obs, factor, ke_or_default(params), k_out, iters, state_out, hook_t, true);
+    });
+}
+
+int fbmp_gpu_estimate_kernel_tv(fbmp_gpu_ctx* ctx, const double* lrms_subset, int nb, int h, int w, const double* pan,
+                                const double* omega, int factor, const fbmp_ke_params* params, double* k_out,
+                                int* iters) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        const size_t p = static_cast<size_t>(h) * w;
+        std::vector<double> obs(p);
+        {
+            double* d_l = upload(C, "api_lrms", lrms_subset, p * nb);
+            double* d_w = upload(C, "api_omega", omega, nb);
+            double* d_o = C.scratch<double>("api_obs2", p);
+            combine_bands_device(C, d_l, 1, nb, static_cast<long long>(p), d_w, d_o);
+            download(C, obs.data(), d_o, p);
+        }
+        estimate_plane_host(C, pan, h * factor, w * factor, obs.data(), factor, ke_or_default(params), k_out, iters,
+                            nullptr, -1, true);
     });
 }
 
@@ -1044,6 +1098,15 @@ int fbmp_gpu_gram(fbmp_gpu_ctx* ctx, const double* pan, int H, int W, const doub
         download(C, Etf, d_e, n2);
     });
 }
+
+int fbmp_gpu_ctx_set_precision(fbmp_gpu_ctx* ctx, int bits) {
+    return guarded([&] {
+        if (bits != 32 && bits != 64) param_error("precision must be 32 or 64 bits");
+        ctx->impl.precision = bits;
+    });
+}
+
+int fbmp_gpu_ctx_precision(fbmp_gpu_ctx* ctx) { return ctx->impl.precision; }
 
 void fbmp_gpu_ctx_set_profile(fbmp_gpu_ctx* ctx, int on) {
     ctx->impl.profile = on != 0;

@@ -28,32 +28,60 @@ __host__ __device__ constexpr int pstride(int s) { return s + ((4 - s % 16) + 16
 __host__ __device__ constexpr int cfloordiv(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 
 __device__ __forceinline__ int wrap_once(int a, int m) { return a < 0 ? a + m : (a >= m ? a - m : a); }
+// Storage / arithmetic type T of the CG vectors: double (the reference precision) or float (the
+// fp32 mode: vectors, guide maps and stencils in fp32, every reduction and CG scalar in fp64).
+template <class T> struct Vec2;
+template <> struct Vec2<double> { using type = double2; };
+template <> struct Vec2<float> { using type = float2; };
+template <class T> using v2 = typename Vec2<T>::type;
+__device__ __forceinline__ double2 mk2(double a, double b) { return make_double2(a, b); }
+__device__ __forceinline__ float2 mk2(float a, float b) { return make_float2(a, b); }
 __device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+__device__ __forceinline__ float2 ld2(const float* p) { return *reinterpret_cast<const float2*>(p); }
 __device__ __forceinline__ void st2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
-// CF-wide runs of doubles (read-only path for loads)
+__device__ __forceinline__ void st2(float* p, float2 v) { *reinterpret_cast<float2*>(p) = v; }
+// CF-wide runs of T (read-only path for loads)
 struct double4_t {
     double2 a, b;
 };
-template <class V>
-__device__ __forceinline__ V ldv(const double* p);
+template <class T, int CF> struct RunT;
+template <> struct RunT<double, 4> { using type = double4_t; };
+template <> struct RunT<double, 2> { using type = double2; };
+template <> struct RunT<double, 1> { using type = double; };
+template <> struct RunT<float, 4> { using type = float4; };
+template <> struct RunT<float, 2> { using type = float2; };
+template <> struct RunT<float, 1> { using type = float; };
+template <class V, class T>
+__device__ __forceinline__ V ldv(const T* p);
 template <>
-__device__ __forceinline__ double ldv<double>(const double* p) { return __ldg(p); }
+__device__ __forceinline__ double ldv<double, double>(const double* p) { return __ldg(p); }
 template <>
-__device__ __forceinline__ double2 ldv<double2>(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+__device__ __forceinline__ double2 ldv<double2, double>(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
 template <>
-__device__ __forceinline__ double4_t ldv<double4_t>(const double* p) {
+__device__ __forceinline__ double4_t ldv<double4_t, double>(const double* p) {
     return {__ldg(reinterpret_cast<const double2*>(p)), __ldg(reinterpret_cast<const double2*>(p) + 1)};
 }
+template <>
+__device__ __forceinline__ float ldv<float, float>(const float* p) { return __ldg(p); }
+template <>
+__device__ __forceinline__ float2 ldv<float2, float>(const float* p) { return __ldg(reinterpret_cast<const float2*>(p)); }
+template <>
+__device__ __forceinline__ float4 ldv<float4, float>(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 __device__ __forceinline__ void unpack(double x, double* v) { v[0] = x; }
 __device__ __forceinline__ void unpack(double2 x, double* v) { v[0] = x.x; v[1] = x.y; }
 __device__ __forceinline__ void unpack(double4_t x, double* v) { v[0] = x.a.x; v[1] = x.a.y; v[2] = x.b.x; v[3] = x.b.y; }
-template <int K>
-__device__ __forceinline__ void stv(double* p, const double (&v)[K]) {
+__device__ __forceinline__ void unpack(float x, float* v) { v[0] = x; }
+__device__ __forceinline__ void unpack(float2 x, float* v) { v[0] = x.x; v[1] = x.y; }
+__device__ __forceinline__ void unpack(float4 x, float* v) { v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w; }
+template <int K, class T>
+__device__ __forceinline__ void stv(T* p, const T (&v)[K]) {
     if constexpr (K == 1) {
         *p = v[0];
+    } else if constexpr (K == 4 && std::is_same<T, float>::value) {
+        *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
     } else {
 #pragma unroll
-        for (int u = 0; u < K; u += 2) reinterpret_cast<double2*>(p)[u / 2] = make_double2(v[u], v[u + 1]);
+        for (int u = 0; u < K; u += 2) st2(p + u, mk2(v[u], v[u + 1]));
     }
 }
 
@@ -61,8 +89,9 @@ __device__ __forceinline__ void stv(double* p, const double (&v)[K]) {
 // per-scene guide statistics (pansharpen.cpp:128-139, :152-155):
 //   mu_k = box_mean(I)_k, g_k = 1 / (eps/9 + var_k) on interior centres, 0 elsewhere
 // ------------------------------------------------------------------------------------------
+template <class T>
 __global__ void k_guide_stats(const double* __restrict__ guide, int H, int W, int rw, double eps,
-                              double* __restrict__ mu, double* __restrict__ gk) {
+                              T* __restrict__ mu, T* __restrict__ gk) {
     const size_t P = static_cast<size_t>(H) * W;
     const double* I = guide + blockIdx.y * P;
     const double ws = static_cast<double>((2 * rw + 1) * (2 * rw + 1));
@@ -82,8 +111,8 @@ __global__ void k_guide_stats(const double* __restrict__ guide, int H, int W, in
             const double var = s2 / ws - m * m;
             g = 1.0 / (eps / ws + var);
         }
-        mu[blockIdx.y * P + e] = m;
-        gk[blockIdx.y * P + e] = g;
+        mu[blockIdx.y * P + e] = static_cast<T>(m);
+        gk[blockIdx.y * P + e] = static_cast<T>(g);
     }
 }
 
@@ -111,37 +140,38 @@ struct QGeo {
 // ((CF g - a) mod CF, (CF g - b) mod CF) at (i + (CF g - a) div CF, j + (CF g - b) div CF).
 // A lane owns one LR row and MJ consecutive LR columns: every plane value loaded feeds up to MJ
 // points and every (broadcast) tap MJ FMAs.
-template <int N_, int CF, bool CG, int MJ_ = 4>
-__global__ void __launch_bounds__(QGeo<N_, CF, MJ_>::NTH, 3) k_q2(PsGeo G, const double* __restrict__ taps,
-                                                             const double* __restrict__ src,
-                                                             double* __restrict__ pbuf, double* __restrict__ q,
+template <int N_, int CF, bool CG, int MJ_ = 4, class T = double>
+__global__ void __launch_bounds__(QGeo<N_, CF, MJ_>::NTH, 3) k_q2(PsGeo G, const T* __restrict__ taps,
+                                                             const T* __restrict__ src,
+                                                             T* __restrict__ pbuf, T* __restrict__ q,
                                                              CgState* st, double* __restrict__ part, int nblk) {
     using Q = QGeo<N_, CF, MJ_>;
     constexpr int NQ = Q::NTH;
     __shared__ double red[NQ / 32 + 1];
-    extern __shared__ double sm[];
+    extern __shared__ __align__(16) unsigned char smraw[];
+    T* sm = reinterpret_cast<T*>(smraw);
     const int ch = blockIdx.y;
-    const double* tp = taps + static_cast<size_t>(ch / G.cps) * N_ * N_;
-    double* sk = sm;
+    const T* tp = taps + static_cast<size_t>(ch / G.cps) * N_ * N_;
+    T* sk = sm;
     for (int e = threadIdx.x; e < N_ * N_; e += NQ) sk[e] = tp[e];
     int t = 0;
-    double beta = 0.0;
+    T beta = 0;
     if (CG) {
         pdl_wait();  // r, beta and the flags come from K_U
         pdl_trigger();
         if (st[ch].done) return;
         t = st[ch].t;
-        beta = t ? st[ch].beta : 0.0;
+        beta = t ? static_cast<T>(st[ch].beta) : T(0);
     }
     const int H = G.H, W = G.W;
     const size_t P = static_cast<size_t>(H) * W;
-    const double* rc = src + ch * P;
-    const double* pold = CG ? pbuf + (static_cast<size_t>((t + 1) & 1) * G.N + ch) * P : nullptr;
-    double* pnew = CG ? pbuf + (static_cast<size_t>(t & 1) * G.N + ch) * P : nullptr;
+    const T* rc = src + ch * P;
+    const T* pold = CG ? pbuf + (static_cast<size_t>((t + 1) & 1) * G.N + ch) * P : nullptr;
+    T* pnew = CG ? pbuf + (static_cast<size_t>(t & 1) * G.N + ch) * P : nullptr;
     const int ntx = (G.w + Q::TW - 1) / Q::TW;
     const int tyb = blockIdx.x / ntx, txb = blockIdx.x - tyb * ntx;
     const int i0 = tyb * Q::TH, j0 = txb * Q::TW;
-    double* planes = sm + Q::KOFF;
+    T* planes = sm + Q::KOFF;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int R0 = CF * (i0 - Q::g), C0 = CF * (j0 - Q::g);
     constexpr int own_r0 = CF * Q::g, own_r1 = CF * (Q::g + Q::TH);
@@ -149,7 +179,7 @@ __global__ void __launch_bounds__(QGeo<N_, CF, MJ_>::NTH, 3) k_q2(PsGeo G, const
     // region load in runs of CF consecutive HR columns (one LR column, all column phases): the
     // run start is a multiple of CF in a row of W = w CF, so a run never wraps and its loads and
     // stores are CF-wide vectors; each thread keeps KB runs of r and p_old in flight
-    using VT = typename std::conditional<CF == 4, double4_t, typename std::conditional<CF == 2, double2, double>::type>::type;
+    using VT = typename RunT<T, CF>::type;
     constexpr int RUNS = Q::SRH * Q::PW;
     constexpr int KB = FBMP_KQ_KB;
     for (int e0 = 0; e0 < RUNS; e0 += NQ * KB) {
@@ -161,8 +191,8 @@ __global__ void __launch_bounds__(QGeo<N_, CF, MJ_>::NTH, 3) k_q2(PsGeo G, const
             const int rr = e / Q::PW, jc = e - rr * Q::PW;
             gi[k] = static_cast<size_t>(wrap_once(R0 + rr, H)) * W + wrap_once(C0 + CF * jc, W);
             if (e < RUNS) {
-                vr[k] = ldv<VT>(rc + gi[k]);
-                if (CG) vp[k] = ldv<VT>(pold + gi[k]);
+                vr[k] = ldv<VT, T>(rc + gi[k]);
+                if (CG) vp[k] = ldv<VT, T>(pold + gi[k]);
             }
         }
 #pragma unroll
@@ -170,10 +200,10 @@ __global__ void __launch_bounds__(QGeo<N_, CF, MJ_>::NTH, 3) k_q2(PsGeo G, const
             const int e = e0 + k * NQ + threadIdx.x;
             if (e >= RUNS) break;
             const int rr = e / Q::PW, jc = e - rr * Q::PW;
-            double v[CF];
+            T v[CF];
             unpack(vr[k], v);
             if (CG) {
-                double o[CF];
+                T o[CF];
                 unpack(vp[k], o);
 #pragma unroll
                 for (int u = 0; u < CF; ++u) v[u] = v[u] + o[u] * beta;  // pansharpen.cpp:254
@@ -181,11 +211,11 @@ __global__ void __launch_bounds__(QGeo<N_, CF, MJ_>::NTH, 3) k_q2(PsGeo G, const
                     stv(pnew + gi[k], v);
                     if (R0 + rr >= G.rlo && R0 + rr < G.rhi) {  // rows owned by this strip
 #pragma unroll
-                        for (int u = 0; u < CF; ++u) pp += v[u] * v[u];
+                        for (int u = 0; u < CF; ++u) pp += static_cast<double>(v[u]) * v[u];
                     }
                 }
             }
-            double* pl = planes + ((rr % CF) * CF) * Q::PS + (rr / CF) * Q::PWS + jc;
+            T* pl = planes + ((rr % CF) * CF) * Q::PS + (rr / CF) * Q::PWS + jc;
 #pragma unroll
             for (int u = 0; u < CF; ++u) pl[u * Q::PS] = v[u];
         }
@@ -193,30 +223,30 @@ __global__ void __launch_bounds__(QGeo<N_, CF, MJ_>::NTH, 3) k_q2(PsGeo G, const
     __syncthreads();
     // points (i0 + lane, j0 + MJ warp + m), m < MJ
     constexpr int MJ = Q::MJ;
-    const double* base = planes + lane * Q::PWS + MJ * warp;
-    double acc[MJ];
+    const T* base = planes + lane * Q::PWS + MJ * warp;
+    T acc[MJ];
 #pragma unroll
-    for (int m = 0; m < MJ; ++m) acc[m] = 0.0;
+    for (int m = 0; m < MJ; ++m) acc[m] = 0;
     constexpr int G4 = CF * Q::g;
     constexpr int JMAX = (G4 + Q::C) / CF + 1;
 #pragma unroll
     for (int a = -Q::C; a <= Q::C; ++a) {
         const int ra = G4 - a;  // >= 0; constants once unrolled
         const int pr = ra % CF, ir = ra / CF;
-        const double* krow = sk + (a + Q::C) * N_ + Q::C;
+        const T* krow = sk + (a + Q::C) * N_ + Q::C;
 #pragma unroll
         for (int pc = 0; pc < CF; ++pc) {
             // column offsets jo with tap b = G4 - pc - CF jo in [-C, C]
             const int jlo = (G4 - pc - Q::C + CF - 1) / CF, jhi = (G4 - pc + Q::C) / CF;  // G4 - pc - C > -CF
-            const double* prow = base + (pr * CF + pc) * Q::PS + ir * Q::PWS;
-            double v[JMAX + MJ];
+            const T* prow = base + (pr * CF + pc) * Q::PS + ir * Q::PWS;
+            T v[JMAX + MJ];
 #pragma unroll
             for (int x = 0; x < JMAX + MJ; ++x)
                 if (x >= jlo && x <= jhi + MJ - 1) v[x] = prow[x];
 #pragma unroll
             for (int jo = 0; jo < JMAX; ++jo) {
                 if (jo >= jlo && jo <= jhi) {
-                    const double kv = krow[G4 - pc - CF * jo];
+                    const T kv = krow[G4 - pc - CF * jo];
 #pragma unroll
                     for (int m = 0; m < MJ; ++m) acc[m] = fma(kv, v[jo + m], acc[m]);
                 }
@@ -224,7 +254,7 @@ __global__ void __launch_bounds__(QGeo<N_, CF, MJ_>::NTH, 3) k_q2(PsGeo G, const
         }
     }
     const int i = i0 + lane;
-    double* qc = q + static_cast<size_t>(ch) * G.h * G.w;
+    T* qc = q + static_cast<size_t>(ch) * G.h * G.w;
     if (i < G.h) {
 #pragma unroll
         for (int m = 0; m < MJ; ++m) {
@@ -280,7 +310,7 @@ namespace q3 {
 constexpr int KQ3_PCU = FBMP_KQ3_PCU;  // unroll of the column-phase loop
 constexpr int NW = 4;  // warps per CTA = HR row phases
 constexpr int NTH = 32 * NW;
-template <int N_, int MJ>
+template <int N_, int MJ, class T = double>
 struct Geo {
     static constexpr int C = (N_ - 1) / 2;
     static constexpr int g = (C + 3) / 4;             // ceil(C / 4)
@@ -303,8 +333,9 @@ struct Geo {
     static constexpr int O_PL = O_RING + NW * D * 2 * RW; // NW x 4 x PLS
     static constexpr int O_SLOT = O_PL + NW * 4 * PLS;    // K x NW x TWL (the raw n x n taps until
                                                           // the tables are built)
-    static constexpr int O_BAR = O_SLOT + K * NW * TWL;   // NW x D mbarriers
-    static constexpr size_t smem = static_cast<size_t>(O_BAR + NW * D) * sizeof(double);
+    static constexpr int O_BAR = sizeof(T) == 8 ? O_SLOT + K * NW * TWL  // NW x D mbarriers (8-byte aligned)
+                                                : (O_SLOT + K * NW * TWL + 1) & ~1;
+    static constexpr size_t smem = static_cast<size_t>(O_BAR) * sizeof(T) + static_cast<size_t>(NW * D) * 8;
     static_assert(N_ * N_ <= K * NW * TWL, "raw taps fit in the partial-row slots");
     static_assert(TWL - MJ + NVP <= PLS, "plane over-read");
 };
@@ -327,36 +358,38 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned int pa
         : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void bulk_g2s(double* dst, const double* src, unsigned int bytes, unsigned long long* b) {
+template <class T>
+__device__ __forceinline__ void bulk_g2s(T* dst, const T* src, unsigned int bytes, unsigned long long* b) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                      saddr(dst)),
                  "l"(src), "r"(bytes), "r"(saddr(b))
                  : "memory");
 }
 
+template <class T>
 struct Args {
-    const double* rc;    // r (CG) or p (operator) plane of the channel
-    const double* pold;  // p_old plane (CG)
-    double* pnew;        // p plane written (CG)
-    double* qc;          // q plane of the channel
-    double beta;
+    const T* rc;    // r (CG) or p (operator) plane of the channel
+    const T* pold;  // p_old plane (CG)
+    T* pnew;        // p plane written (CG)
+    T* qc;          // q plane of the channel
+    T beta;
     int H, W, h, w, rlo, rhi;
     int i0, i1, j0;      // strip rows [i0, i1), band origin
     int s0, s1;          // superrows
 };
 
 // one warp's stream of HR rows y = 4 s + WP, s in [s0, s1)
-template <int N_, int MJ, bool CG, int WP>
-__device__ __forceinline__ double rows(const Args& A, const double* sk, double* tt, double* ring, double* pl,
-                                       double* slots, unsigned long long* bar, int lane, int warp) {
-    using Q = Geo<N_, MJ>;
+template <int N_, int MJ, bool CG, int WP, class T>
+__device__ __forceinline__ double rows(const Args<T>& A, const T* sk, T* tt, T* ring, T* pl,
+                                       T* slots, unsigned long long* bar, int lane, int warp) {
+    using Q = Geo<N_, MJ, T>;
     constexpr int C = Q::C, g = Q::g, gp = Q::gp, RW = Q::RW, PLS = Q::PLS, TWL = Q::TWL, D = Q::D, K = Q::K;
     constexpr int DMIN = -((C - WP) / 4);  // ceil((WP - C) / 4)
     constexpr int DMAX = (WP + C) / 4;
     constexpr int NA = DMAX - DMIN + 1;
     const int H = A.H, W = A.W;
     const int col0 = 4 * (A.j0 - g);
-    const unsigned int row_bytes = (CG ? 2u : 1u) * RW * sizeof(double);
+    const unsigned int row_bytes = (CG ? 2u : 1u) * RW * sizeof(T);
     const int yo0 = 4 * A.i0, yo1 = min(4 * A.i1, H);
     const int xo_hi = min(4 * TWL, W - 4 * A.j0);
     // the column split of a staged row at the periodic wrap is the same for every row (at most
@@ -364,7 +397,7 @@ __device__ __forceinline__ double rows(const Args& A, const double* sk, double* 
     // go out in parallel; the staged rows are consecutive superrows, so the image row advances
     // by 4 (mod H) per issue
     int ncp = 0;
-    const double* csrc = nullptr;
+    const T* csrc = nullptr;
     unsigned int cdst = 0, cbytes = 0;
     {
         int start = col0 % W;
@@ -378,7 +411,7 @@ __device__ __forceinline__ double rows(const Args& A, const double* sk, double* 
                 if (lane == k) {
                     csrc = (a == 0 ? A.rc : A.pold) + start;
                     cdst = saddr(ring + a * RW + off);
-                    cbytes = static_cast<unsigned int>(len) * sizeof(double);
+                    cbytes = static_cast<unsigned int>(len) * sizeof(T);
                 }
             }
             ncp = np_ + 1;
@@ -397,7 +430,7 @@ __device__ __forceinline__ double rows(const Args& A, const double* sk, double* 
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(row_bytes) : "memory");
         if (copier)
             asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                             cdst + static_cast<unsigned int>(slot * 2 * RW * sizeof(double))),
+                             cdst + static_cast<unsigned int>(slot * 2 * RW * sizeof(T))),
                          "l"(csrc + static_cast<size_t>(yw_next) * W), "r"(cbytes), "r"(b)
                          : "memory");
         yw_next += 4;
@@ -409,43 +442,43 @@ __device__ __forceinline__ double rows(const Args& A, const double* sk, double* 
     for (int e = lane; e < Q::TT; e += 32) {
         const int pc = e / (Q::NU * Q::NAP), ui = (e / Q::NAP) % Q::NU, dd = e % Q::NAP;
         const int d = DMIN + dd, b = -(4 * (ui - g) + pc);
-        tt[e] = (d <= DMAX && b >= -C && b <= C) ? sk[(4 * d - WP + C) * N_ + (b + C)] : 0.0;
+        tt[e] = (d <= DMAX && b >= -C && b <= C) ? sk[(4 * d - WP + C) * N_ + (b + C)] : T(0);
     }
     __syncthreads();  // every table is built: the raw taps' space goes to the partial-row slots
-    double acc[NA][MJ];
+    T acc[NA][MJ];
 #pragma unroll
     for (int d = 0; d < NA; ++d)
 #pragma unroll
-        for (int m = 0; m < MJ; ++m) acc[d][m] = 0.0;
+        for (int m = 0; m < MJ; ++m) acc[d][m] = 0;
     double pp = 0.0;
-    const double* plb = pl + MJ * lane;
+    const T* plb = pl + MJ * lane;
     for (int s = A.s0; s < A.s1; ++s) {
         const int k = s - A.s0;
         const int slot = k % D;
         mbar_wait(bar + slot, static_cast<unsigned int>((k / D) & 1));
         const int y = 4 * s + WP;
-        const double* rr = ring + slot * 2 * RW;
+        const T* rr = ring + slot * 2 * RW;
         // p = r + beta p_old on the staged row; owned part -> p, all of it -> phase planes
         {
             const bool own_row = CG && y >= yo0 && y < yo1;
             const bool dot_row = own_row && y >= A.rlo && y < A.rhi;
-            double* prow = nullptr;
+            T* prow = nullptr;
             if (CG) prow = A.pnew + static_cast<size_t>(own_row ? y : 0) * W + 4 * A.j0 - 4 * g;
 #pragma unroll
             for (int kk = 0; kk < (RW + 63) / 64; ++kk) {
                 const int e = 2 * lane + 64 * kk;
                 if (e < RW) {
-                    double2 v = ld2(rr + e);
+                    v2<T> v = ld2(rr + e);
                     if (CG) {
-                        const double2 o = ld2(rr + RW + e);
+                        const v2<T> o = ld2(rr + RW + e);
                         v.x = v.x + o.x * A.beta;  // pansharpen.cpp:254
                         v.y = v.y + o.y * A.beta;
                         const int xr = e - 4 * g;
                         if (own_row && xr >= 0 && xr < xo_hi) {
                             st2(prow + e, v);
                             if (dot_row) {
-                                pp += v.x * v.x;
-                                pp += v.y * v.y;
+                                pp += static_cast<double>(v.x) * static_cast<double>(v.x);
+                                pp += static_cast<double>(v.y) * static_cast<double>(v.y);
                             }
                         }
                     }
@@ -463,20 +496,20 @@ __device__ __forceinline__ double rows(const Args& A, const double* sk, double* 
         // (pc, u) order is ascending; the zero taps of the table (|b| > C) add exact zeros
 #pragma unroll KQ3_PCU
         for (int pc = 0; pc < 4; ++pc) {
-            double v[Q::NVP];
+            T v[Q::NVP];
 #pragma unroll
             for (int o = 0; o < Q::NVP; o += 2) {
-                const double2 t2 = ld2(plb + pc * PLS + o);
+                const v2<T> t2 = ld2(plb + pc * PLS + o);
                 v[o] = t2.x;
                 v[o + 1] = t2.y;
             }
-            const double* tpc = tt + pc * (Q::NU * Q::NAP);
+            const T* tpc = tt + pc * (Q::NU * Q::NAP);
 #pragma unroll
             for (int ui = 0; ui < Q::NU; ++ui) {
-                double kv[Q::NAP];
+                T kv[Q::NAP];
 #pragma unroll
                 for (int dd = 0; dd < NA; dd += 2) {
-                    const double2 k2 = ld2(tpc + ui * Q::NAP + dd);
+                    const v2<T> k2 = ld2(tpc + ui * Q::NAP + dd);
                     kv[dd] = k2.x;
                     kv[dd + 1] = k2.y;
                 }
@@ -488,27 +521,27 @@ __device__ __forceinline__ double rows(const Args& A, const double* sk, double* 
         }
         // LR row s + DMIN is complete for this warp: publish its partial, shift the window
         {
-            double* sl = slots + ((s + DMIN) & (K - 1)) * (NW * TWL) + WP * TWL + MJ * lane;
+            T* sl = slots + ((s + DMIN) & (K - 1)) * (NW * TWL) + WP * TWL + MJ * lane;
 #pragma unroll
-            for (int m = 0; m < MJ; m += 2) st2(sl + m, make_double2(acc[0][m], acc[0][m + 1]));
+            for (int m = 0; m < MJ; m += 2) st2(sl + m, mk2(acc[0][m], acc[0][m + 1]));
 #pragma unroll
             for (int d = 0; d + 1 < NA; ++d)
 #pragma unroll
                 for (int m = 0; m < MJ; ++m) acc[d][m] = acc[d + 1][m];
 #pragma unroll
-            for (int m = 0; m < MJ; ++m) acc[NA - 1][m] = 0.0;
+            for (int m = 0; m < MJ; ++m) acc[NA - 1][m] = 0;
         }
         __syncthreads();
         // LR row s - g has all four partials
         const int i = s - g;
         if (warp == (s & 3) && i >= A.i0 && i < A.i1) {
-            const double* sb = slots + (i & (K - 1)) * (NW * TWL) + MJ * lane;
+            const T* sb = slots + (i & (K - 1)) * (NW * TWL) + MJ * lane;
             const int j = A.j0 + MJ * lane;
 #pragma unroll
             for (int m = 0; m < MJ; m += 2) {
-                const double2 a0 = ld2(sb + m), a1 = ld2(sb + TWL + m), a2 = ld2(sb + 2 * TWL + m),
-                              a3 = ld2(sb + 3 * TWL + m);
-                const double2 val = make_double2(((a0.x + a1.x) + a2.x) + a3.x, ((a0.y + a1.y) + a2.y) + a3.y);
+                const v2<T> a0 = ld2(sb + m), a1 = ld2(sb + TWL + m), a2 = ld2(sb + 2 * TWL + m),
+                            a3 = ld2(sb + 3 * TWL + m);
+                const v2<T> val = mk2(((a0.x + a1.x) + a2.x) + a3.x, ((a0.y + a1.y) + a2.y) + a3.y);
                 if (j + m + 1 < A.w) st2(A.qc + static_cast<size_t>(i) * A.w + j + m, val);
                 else if (j + m < A.w) A.qc[static_cast<size_t>(i) * A.w + j + m] = val.x;
             }
@@ -518,28 +551,29 @@ __device__ __forceinline__ double rows(const Args& A, const double* sk, double* 
 }
 }  // namespace q3
 
-template <int N_, int MJ, bool CG>
-__global__ void __launch_bounds__(q3::NTH, FBMP_KQ3_MINB) k_q3(PsGeo G, const double* __restrict__ taps,
-                                                   const double* __restrict__ src, double* __restrict__ pbuf,
-                                                   double* __restrict__ q, CgState* st, double* __restrict__ part,
+template <int N_, int MJ, bool CG, class T = double>
+__global__ void __launch_bounds__(q3::NTH, FBMP_KQ3_MINB) k_q3(PsGeo G, const T* __restrict__ taps,
+                                                   const T* __restrict__ src, T* __restrict__ pbuf,
+                                                   T* __restrict__ q, CgState* st, double* __restrict__ part,
                                                    int nblk) {
-    using Q = q3::Geo<N_, MJ>;
+    using Q = q3::Geo<N_, MJ, T>;
     __shared__ double red[q3::NW + 1];
-    extern __shared__ __align__(16) double sm[];
+    extern __shared__ __align__(16) unsigned char smraw[];
+    T* sm = reinterpret_cast<T*>(smraw);
     const int ch = blockIdx.y;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const double* tp = taps + static_cast<size_t>(ch / G.cps) * N_ * N_;
-    double* sk = sm + Q::O_SLOT;  // raw taps (the partial-row slots take over after the tables)
+    const T* tp = taps + static_cast<size_t>(ch / G.cps) * N_ * N_;
+    T* sk = sm + Q::O_SLOT;  // raw taps (the partial-row slots take over after the tables)
     for (int e = threadIdx.x; e < N_ * N_; e += q3::NTH) sk[e] = tp[e];
-    q3::Args A;
-    A.beta = 0.0;
+    q3::Args<T> A;
+    A.beta = 0;
     int t = 0;
     if (CG) {
         pdl_wait();  // r, beta and the flags come from K_U
         pdl_trigger();
         if (st[ch].done) return;
         t = st[ch].t;
-        A.beta = t ? st[ch].beta : 0.0;
+        A.beta = t ? static_cast<T>(st[ch].beta) : T(0);
     }
     A.H = G.H;
     A.W = G.W;
@@ -562,22 +596,22 @@ __global__ void __launch_bounds__(q3::NTH, FBMP_KQ3_MINB) k_q3(PsGeo G, const do
     A.s0 = A.i0 - Q::g;
     A.s1 = A.i1 + Q::g;
     if (A.i1 <= A.i0) A.s1 = A.s0;  // empty strip: no rows, still counted in the p.p election
-    double* ring = sm + Q::O_RING + warp * (Q::D * 2 * Q::RW);
-    double* pl = sm + Q::O_PL + warp * 4 * Q::PLS;
-    double* slots = sm + Q::O_SLOT;
+    T* ring = sm + Q::O_RING + warp * (Q::D * 2 * Q::RW);
+    T* pl = sm + Q::O_PL + warp * 4 * Q::PLS;
+    T* slots = sm + Q::O_SLOT;
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + Q::O_BAR) + warp * Q::D;
     if (lane == 0) {
         for (int k = 0; k < Q::D; ++k) q3::mbar_init(bar + k, 1);
         q3::mbar_fence_init();
     }
     __syncthreads();  // taps and barriers
-    double* tt = sm + Q::O_TT + warp * Q::TT;
+    T* tt = sm + Q::O_TT + warp * Q::TT;
     double pp;
     switch (warp) {
-    case 0: pp = q3::rows<N_, MJ, CG, 0>(A, sk, tt, ring, pl, slots, bar, lane, warp); break;
-    case 1: pp = q3::rows<N_, MJ, CG, 1>(A, sk, tt, ring, pl, slots, bar, lane, warp); break;
-    case 2: pp = q3::rows<N_, MJ, CG, 2>(A, sk, tt, ring, pl, slots, bar, lane, warp); break;
-    default: pp = q3::rows<N_, MJ, CG, 3>(A, sk, tt, ring, pl, slots, bar, lane, warp); break;
+    case 0: pp = q3::rows<N_, MJ, CG, 0, T>(A, sk, tt, ring, pl, slots, bar, lane, warp); break;
+    case 1: pp = q3::rows<N_, MJ, CG, 1, T>(A, sk, tt, ring, pl, slots, bar, lane, warp); break;
+    case 2: pp = q3::rows<N_, MJ, CG, 2, T>(A, sk, tt, ring, pl, slots, bar, lane, warp); break;
+    default: pp = q3::rows<N_, MJ, CG, 3, T>(A, sk, tt, ring, pl, slots, bar, lane, warp); break;
     }
     if (CG) {
         const double bs = block_sum<q3::NTH>(pp, red);
@@ -1052,13 +1086,14 @@ constexpr int RB = 16;            // rows per p.out partial (strip heights are m
                                   // the reduction tree does not depend on the strip partition)
 }  // namespace kl
 
-template <bool CG, int N_, int CF>
-__global__ void __launch_bounds__(NT, FBMP_KD_MINB) k_dterm(PsGeo G, const double* __restrict__ taps, const double* __restrict__ q,
-                                                 double* __restrict__ out, const CgState* __restrict__ st) {
+template <bool CG, int N_, int CF, class T = double>
+__global__ void __launch_bounds__(NT, FBMP_KD_MINB) k_dterm(PsGeo G, const T* __restrict__ taps, const T* __restrict__ q,
+                                                 T* __restrict__ out, const CgState* __restrict__ st) {
     using namespace a4;
     using Lay = a4::L<CF>;
     static_assert(N_ == 0 || CF == 4, "register data term is specialised for factor 4");
-    extern __shared__ double sm[];   // taps | q window: dterm_smem<CF>()
+    extern __shared__ __align__(16) unsigned char smraw[];   // taps | q window: dterm_smem<CF>()
+    T* sm = reinterpret_cast<T*>(smraw);
     const int cgroups = (G.cps + G.cpc - 1) / G.cpc;
     const int scene = blockIdx.y / cgroups, group = blockIdx.y - scene * cgroups;
     const int H = G.H, W = G.W, n = G.n, C = G.C;
@@ -1066,9 +1101,9 @@ __global__ void __launch_bounds__(NT, FBMP_KD_MINB) k_dterm(PsGeo G, const doubl
     const int ntx = (W + TA - 1) / TA;
     const int by = blockIdx.x / ntx, bx = blockIdx.x - by * ntx;
     const int r0 = by * TA, c0 = bx * TA;
-    double* sk = sm + Lay::O_TAPS;
-    double* sq = sm + MAXTAP;   // q window right after the taps
-    const double* tp = taps + static_cast<size_t>(scene) * n * n;
+    T* sk = sm + Lay::O_TAPS;
+    T* sq = sm + MAXTAP;   // q window right after the taps
+    const T* tp = taps + static_cast<size_t>(scene) * n * n;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int iq0 = floordiv(r0 - C + CF - 1, CF), jq0 = floordiv(c0 - C + CF - 1, CF);
     const int QH = floordiv(r0 + TA - 1 + C, CF) - iq0 + 1, QW = floordiv(c0 + TA - 1 + C, CF) - jq0 + 1;
@@ -1102,7 +1137,7 @@ __global__ void __launch_bounds__(NT, FBMP_KD_MINB) k_dterm(PsGeo G, const doubl
             const int a = r / QWC, b = r - a * QWC;
             // c-th active channel (all of them unless some channel of the group has converged)
             const int chl = ch_lo + (all_active ? c : static_cast<int>(__fns(active, 0, c + 1)));
-            const double* qc = q + static_cast<size_t>(scene * G.cps + chl) * G.h * G.w;
+            const T* qc = q + static_cast<size_t>(scene * G.cps + chl) * G.h * G.w;
             sq[c * QSZ + a * QS + b] =
                 __ldg(qc + static_cast<size_t>(wrap_once(iq0 + a, G.h)) * G.w + wrap_once(jq0 + b, G.w));
         }
@@ -1113,13 +1148,13 @@ __global__ void __launch_bounds__(NT, FBMP_KD_MINB) k_dterm(PsGeo G, const doubl
         const int rest = threadIdx.x / (CF * CW4);
         const int Ic0 = (rest % RB4) * 4;
         const int pr = rest / RB4;
-        double kreg[DM][DM];
+        T kreg[DM][DM];
 #pragma unroll
         for (int a = 0; a < DM; ++a)
 #pragma unroll
             for (int b = 0; b < DM; ++b) {
                 const int tr = CF * (a + D::DLO) - pr + D::C, tc = CF * (b + D::DLO) - pc + D::C;
-                kreg[a][b] = (tr >= 0 && tr < N_ && tc >= 0 && tc < N_) ? sk[tr * N_ + tc] : 0.0;
+                kreg[a][b] = (tr >= 0 && tr < N_ && tc >= 0 && tc < N_) ? sk[tr * N_ + tc] : T(0);
             }
         const int qoff = (r0 / CF + Ic0 - iq0 + D::DLO) * QS + (c0 / CF + Jc - jq0 + D::DLO);
         const int Cc = c0 + Jc * CF + pc;
@@ -1132,12 +1167,12 @@ __global__ void __launch_bounds__(NT, FBMP_KD_MINB) k_dterm(PsGeo G, const doubl
             const bool two = m != 0u;
             const int chB = two ? ch_lo + __ffs(m) - 1 : chA;
             if (two) m &= m - 1u;
-            const double* qa = sq + c * QSZ + qoff;
-            const double* qb2 = sq + (two ? c + 1 : c) * QSZ + qoff;
-            double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+            const T* qa = sq + c * QSZ + qoff;
+            const T* qb2 = sq + (two ? c + 1 : c) * QSZ + qoff;
+            T acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
 #pragma unroll
             for (int mm = 0; mm < DM + 3; ++mm) {
-                double qv[2][DM];
+                T qv[2][DM];
 #pragma unroll
                 for (int b = 0; b < DM; ++b) {
                     qv[0][b] = qa[mm * QS + b];
@@ -1156,8 +1191,8 @@ __global__ void __launch_bounds__(NT, FBMP_KD_MINB) k_dterm(PsGeo G, const doubl
                         }
                     }
             }
-            double* oa = out + (scene * G.cps + chA) * P;
-            double* ob = out + (scene * G.cps + chB) * P;
+            T* oa = out + (scene * G.cps + chA) * P;
+            T* ob = out + (scene * G.cps + chB) * P;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int R = r0 + (Ic0 + k) * CF + pr;
@@ -1170,11 +1205,11 @@ __global__ void __launch_bounds__(NT, FBMP_KD_MINB) k_dterm(PsGeo G, const doubl
         return;
     }
     constexpr int KQ = (Lay::QWMAX * Lay::QWMAX + NT - 1) / NT;
-    double pf[KQ];
+    T pf[KQ];
     // the next channel's q window is loaded into registers while the current one is computed;
     // the shared window alternates between two buffers (one barrier per channel)
     auto prefetch = [&](int chl) {
-        const double* qc = q + static_cast<size_t>(scene * G.cps + chl) * G.h * G.w;
+        const T* qc = q + static_cast<size_t>(scene * G.cps + chl) * G.h * G.w;
 #pragma unroll
         for (int k = 0; k < KQ; ++k) {
             const int e = threadIdx.x + k * NT;
@@ -1191,7 +1226,7 @@ __global__ void __launch_bounds__(NT, FBMP_KD_MINB) k_dterm(PsGeo G, const doubl
         const int chl = nxt;
         active &= active - 1u;
         const int ch = scene * G.cps + chl;
-        double* sqb = sq + buf * (Lay::QWP * Lay::QWMAX);
+        T* sqb = sq + buf * (Lay::QWP * Lay::QWMAX);
 #pragma unroll
         for (int k = 0; k < KQ; ++k) {
             const int e = threadIdx.x + k * NT;
@@ -1204,7 +1239,7 @@ __global__ void __launch_bounds__(NT, FBMP_KD_MINB) k_dterm(PsGeo G, const doubl
         if (nxt >= 0) prefetch(nxt);
         __syncthreads();  // window (and taps) in; the other buffer is free for the next channel
         buf ^= 1;
-        double* oc = out + ch * P;
+        T* oc = out + ch * P;
         if (N_ > 0) {
             constexpr int CW4 = TA / CF, RB4 = CW4 / 4;
             const int pc = threadIdx.x % CF;
@@ -1212,19 +1247,19 @@ __global__ void __launch_bounds__(NT, FBMP_KD_MINB) k_dterm(PsGeo G, const doubl
             const int rest = threadIdx.x / (CF * CW4);
             const int Ic0 = (rest % RB4) * 4;
             const int pr = rest / RB4;
-            double kreg[DM][DM];
+            T kreg[DM][DM];
 #pragma unroll
             for (int a = 0; a < DM; ++a)
 #pragma unroll
                 for (int b = 0; b < DM; ++b) {
                     const int tr = CF * (a + D::DLO) - pr + D::C, tc = CF * (b + D::DLO) - pc + D::C;
-                    kreg[a][b] = (tr >= 0 && tr < N_ && tc >= 0 && tc < N_) ? sk[tr * N_ + tc] : 0.0;
+                    kreg[a][b] = (tr >= 0 && tr < N_ && tc >= 0 && tc < N_) ? sk[tr * N_ + tc] : T(0);
                 }
-            const double* qb = sqb + (r0 / CF + Ic0 - iq0 + D::DLO) * QS + (c0 / CF + Jc - jq0 + D::DLO);
-            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            const T* qb = sqb + (r0 / CF + Ic0 - iq0 + D::DLO) * QS + (c0 / CF + Jc - jq0 + D::DLO);
+            T acc[4] = {0, 0, 0, 0};
 #pragma unroll
             for (int m = 0; m < DM + 3; ++m) {
-                double qv[DM];
+                T qv[DM];
 #pragma unroll
                 for (int b = 0; b < DM; ++b) qv[b] = qb[m * QS + b];
 #pragma unroll
@@ -1252,11 +1287,11 @@ __global__ void __launch_bounds__(NT, FBMP_KD_MINB) k_dterm(PsGeo G, const doubl
                 const int ci = cell / CPR, cj = cell - ci * CPR;
                 const int dilo = floordiv(pr - C + CF - 1, CF), dihi = floordiv(pr + C, CF);
                 const int djlo = floordiv(pc - C + CF - 1, CF), djhi = floordiv(pc + C, CF);
-                const double* qb = sqb + (r0 / CF + ci - iq0) * QS + (c0 / CF + cj - jq0);
-                double acc = 0.0;
+                const T* qb = sqb + (r0 / CF + ci - iq0) * QS + (c0 / CF + cj - jq0);
+                T acc = 0;
                 for (int di = dilo; di <= dihi; ++di) {
-                    const double* krow = sk + (CF * di - pr + C) * n + C - pc;
-                    const double* qrow = qb + di * QS;
+                    const T* krow = sk + (CF * di - pr + C) * n + C - pc;
+                    const T* qrow = qb + di * QS;
                     for (int dj = djlo; dj <= djhi; ++dj) acc = fma(krow[CF * dj], qrow[dj], acc);
                 }
                 const int R = r0 + ci * CF + pr, Cc = c0 + cj * CF + pc;
@@ -1458,13 +1493,20 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
+// one lane's column pair of a row: 16 bytes (double) through L2 only, 8 bytes (float) through L1
+__device__ __forceinline__ void cp_async_pair(double2* sdst, const double* gsrc) { cp_async16(sdst, gsrc); }
+__device__ __forceinline__ void cp_async_pair(float2* sdst, const float* gsrc) {
+    const unsigned int s = static_cast<unsigned int>(__cvta_generic_to_shared(sdst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc) : "memory");
+}
 
-template <bool CG>
-__global__ void __launch_bounds__(kl::NTL, FBMP_KL_MINB) k_llp2(PsGeo G, const double* __restrict__ guide,
-                                                     const double* __restrict__ wmu, const double* __restrict__ wg,
-                                                     const double* __restrict__ pin, double* __restrict__ out,
+template <bool CG, class T = double>
+__global__ void __launch_bounds__(kl::NTL, FBMP_KL_MINB) k_llp2(PsGeo G, const T* __restrict__ guide,
+                                                     const T* __restrict__ wmu, const T* __restrict__ wg,
+                                                     const T* __restrict__ pin, T* __restrict__ out,
                                                      CgState* st, double* __restrict__ part, int nbands, int kstrips,
                                                      int R) {
+    using V = v2<T>;
     using namespace kl;
     // channel-fastest CTA order within a scene: the channels of a (band, strip) item run
     // together, so the scene's guide maps are read from HBM once and hit in L2 for the others
@@ -1490,45 +1532,45 @@ __global__ void __launch_bounds__(kl::NTL, FBMP_KL_MINB) k_llp2(PsGeo G, const d
     const int nrb = (H + RB - 1) / RB;
     const unsigned FULL = 0xffffffffu;
     constexpr int NB = FBMP_KL_NB;           // ring depth: rows in flight = NB - 1
-    __shared__ double2 ring[NB][5][32];      // p, I, mu, g, d rows of NB steps
+    __shared__ V ring[NB][5][32];            // p, I, mu, g, d rows of NB steps
     double dotp = 0.0;
     {
         const int band = item / kstrips, strip = item - band * kstrips;
         const int c0 = band * BAND2, r0 = strip * R, r1 = min(H, r0 + R);
         const int X = wrap_once(c0 - HALO + 2 * lane, W);  // even; X + 1 < W
-        const double* pp = pin + ch * P;
+        const T* pp = pin + ch * P;
         if (CG) pp = pin + (static_cast<size_t>(st[ch].t & 1) * G.N + ch) * P;
-        const double* pc = pp + X;
-        const double* I = guide + scene * P + X;
-        const double* MU = wmu + scene * P + X;
-        const double* GK = wg + scene * P + X;
-        double* oc = out + ch * P + X;
+        const T* pc = pp + X;
+        const T* I = guide + scene * P + X;
+        const T* MU = wmu + scene * P + X;
+        const T* GK = wg + scene * P + X;
+        T* oc = out + ch * P + X;
         const int ox = c0 - HALO + 2 * lane;                 // unwrapped column of .x
         const bool writer = lane >= HALO / 2 && lane < (HALO + BAND2) / 2 && ox < W;
         const int nc0 = max(min(X + 1, W - 2) - max(X - 1, 1) + 1, 0);
         const int nc1 = max(min(X + 2, W - 2) - max(X, 1) + 1, 0);
-        const double lam = G.lambda;
+        const T lam = static_cast<T>(G.lambda);
         auto back = [&](int r, int k) { const int q = r - k; return q < 0 ? q + H : q; };
         // row offsets (elements) of Y (p), Y-1 (I), Y-2 (mu, g) and Y-4 (d); they advance by W
         const int yA = wrap_once(r0 - HALO, H);
         int o0 = yA * W, o1 = back(yA, 1) * W, o2 = back(yA, 2) * W, o4 = back(yA, 4) * W;
         auto adv = [&](int o) { return o + W == static_cast<int>(P) ? 0 : o + W; };
         int r3 = back(yA, 3);
-        double2 pm1 = {0, 0}, pm2 = {0, 0}, pm3 = {0, 0}, pm4 = {0, 0};
-        double2 Im2 = {0, 0}, Im3 = {0, 0}, s2 = {0, 0}, s3 = {0, 0};
-        double2 hs_a = {0, 0}, hs_b = {0, 0}, his_a = {0, 0}, his_b = {0, 0};
-        double2 ha_a = {0, 0}, ha_b = {0, 0}, hc_a = {0, 0}, hc_b = {0, 0}, M_a = {0, 0}, M_b = {0, 0};
+        V pm1 = {0, 0}, pm2 = {0, 0}, pm3 = {0, 0}, pm4 = {0, 0};
+        V Im2 = {0, 0}, Im3 = {0, 0}, s2 = {0, 0}, s3 = {0, 0};
+        V hs_a = {0, 0}, hs_b = {0, 0}, his_a = {0, 0}, his_b = {0, 0};
+        V ha_a = {0, 0}, ha_b = {0, 0}, hc_a = {0, 0}, hc_b = {0, 0}, M_a = {0, 0}, M_b = {0, 0};
         const int steps = (r1 - r0) + 2 * HALO;
         int blk_left = RB;
         // the rows of step j stream into ring slot j % NB with cp.async, NB - 1 steps ahead of
         // their use (each lane copies and later reads its own 16 bytes: no warp barrier)
         int io0 = o0, io1 = o1, io2 = o2, io4 = o4;  // offsets of the next step to issue
         auto issue = [&](int slot) {
-            cp_async16(&ring[slot][0][lane], pc + io0);
-            cp_async16(&ring[slot][1][lane], I + io1);
-            cp_async16(&ring[slot][2][lane], MU + io2);
-            cp_async16(&ring[slot][3][lane], GK + io2);
-            cp_async16(&ring[slot][4][lane], oc + io4);
+            cp_async_pair(&ring[slot][0][lane], pc + io0);
+            cp_async_pair(&ring[slot][1][lane], I + io1);
+            cp_async_pair(&ring[slot][2][lane], MU + io2);
+            cp_async_pair(&ring[slot][3][lane], GK + io2);
+            cp_async_pair(&ring[slot][4][lane], oc + io4);
             io0 = adv(io0); io1 = adv(io1); io2 = adv(io2); io4 = adv(io4);
         };
 #pragma unroll
@@ -1542,53 +1584,56 @@ __global__ void __launch_bounds__(kl::NTL, FBMP_KL_MINB) k_llp2(PsGeo G, const d
             cp_async_commit();
             cp_async_wait<NB - 1>();  // the group of step st_i has landed
             const int slot = st_i % NB;
-            const double2 p0 = ring[slot][0][lane], Im1 = ring[slot][1][lane], mu2 = ring[slot][2][lane],
-                          g2 = ring[slot][3][lane], d4 = ring[slot][4][lane];
+            const V p0 = ring[slot][0][lane], Im1 = ring[slot][1][lane], mu2 = ring[slot][2][lane],
+                    g2 = ring[slot][3][lane], d4 = ring[slot][4][lane];
             const int o4c = o4;
             o4 = adv(o4);
             // S1 at row Y-1 (ops.cpp:70-78 order: 4 c - up - down - left - right)
-            const double pL = __shfl_up_sync(FULL, pm1.y, 1), pR = __shfl_down_sync(FULL, pm1.x, 1);
-            double2 s1, is1;
-            s1.x = 4.0 * pm1.x - pm2.x - p0.x - pL - pm1.y;
-            s1.y = 4.0 * pm1.y - pm2.y - p0.y - pm1.x - pR;
+            const T pL = __shfl_up_sync(FULL, pm1.y, 1), pR = __shfl_down_sync(FULL, pm1.x, 1);
+            V s1, is1;
+            s1.x = T(4) * pm1.x - pm2.x - p0.x - pL - pm1.y;
+            s1.y = T(4) * pm1.y - pm2.y - p0.y - pm1.x - pR;
             is1.x = Im1.x * s1.x;
             is1.y = Im1.y * s1.y;
             // S2 at row Y-2
-            const double sL = __shfl_up_sync(FULL, s1.y, 1), sR = __shfl_down_sync(FULL, s1.x, 1);
-            const double iL = __shfl_up_sync(FULL, is1.y, 1), iR = __shfl_down_sync(FULL, is1.x, 1);
-            const double2 hs1 = make_double2(sL + s1.x + s1.y, s1.x + s1.y + sR);
-            const double2 his1 = make_double2(iL + is1.x + is1.y, is1.x + is1.y + iR);
-            double2 a2, c2;
+            const T sL = __shfl_up_sync(FULL, s1.y, 1), sR = __shfl_down_sync(FULL, s1.x, 1);
+            const T iL = __shfl_up_sync(FULL, is1.y, 1), iR = __shfl_down_sync(FULL, is1.x, 1);
+            const V hs1 = mk2(sL + s1.x + s1.y, s1.x + s1.y + sR);
+            const V his1 = mk2(iL + is1.x + is1.y, is1.x + is1.y + iR);
+            constexpr T NINTH = T(1.0 / 9.0);
+            V a2, c2;
             {
-                const double xb = (hs_a.x + hs_b.x + hs1.x) * (1.0 / 9.0);
-                a2.x = g2.x * ((his_a.x + his_b.x + his1.x) * (1.0 / 9.0) - mu2.x * xb);
-                c2.x = g2.x != 0.0 ? xb - mu2.x * a2.x : 0.0;
+                const T xb = (hs_a.x + hs_b.x + hs1.x) * NINTH;
+                a2.x = g2.x * ((his_a.x + his_b.x + his1.x) * NINTH - mu2.x * xb);
+                c2.x = g2.x != T(0) ? xb - mu2.x * a2.x : T(0);
             }
             {
-                const double xb = (hs_a.y + hs_b.y + hs1.y) * (1.0 / 9.0);
-                a2.y = g2.y * ((his_a.y + his_b.y + his1.y) * (1.0 / 9.0) - mu2.y * xb);
-                c2.y = g2.y != 0.0 ? xb - mu2.y * a2.y : 0.0;
+                const T xb = (hs_a.y + hs_b.y + hs1.y) * NINTH;
+                a2.y = g2.y * ((his_a.y + his_b.y + his1.y) * NINTH - mu2.y * xb);
+                c2.y = g2.y != T(0) ? xb - mu2.y * a2.y : T(0);
             }
             // S3 at row Y-3
-            const double aL = __shfl_up_sync(FULL, a2.y, 1), aR = __shfl_down_sync(FULL, a2.x, 1);
-            const double cL = __shfl_up_sync(FULL, c2.y, 1), cR = __shfl_down_sync(FULL, c2.x, 1);
-            const double2 ha2 = make_double2(aL + a2.x + a2.y, a2.x + a2.y + aR);
-            const double2 hc2 = make_double2(cL + c2.x + c2.y, c2.x + c2.y + cR);
+            const T aL = __shfl_up_sync(FULL, a2.y, 1), aR = __shfl_down_sync(FULL, a2.x, 1);
+            const T cL = __shfl_up_sync(FULL, c2.y, 1), cR = __shfl_down_sync(FULL, c2.x, 1);
+            const V ha2 = mk2(aL + a2.x + a2.y, a2.x + a2.y + aR);
+            const V hc2 = mk2(cL + c2.x + c2.y, c2.x + c2.y + cR);
             const int g3 = wrap_once(r3 + G.grow0, G.Hg);  // global row (strip decomposition)
             const int nrow = max(min(g3 + 1, G.Hg - 2) - max(g3 - 1, 1) + 1, 0);
-            double2 Mc;
-            Mc.x = static_cast<double>(nrow * nc0) * s3.x - (hc_a.x + hc_b.x + hc2.x) - Im3.x * (ha_a.x + ha_b.x + ha2.x);
-            Mc.y = static_cast<double>(nrow * nc1) * s3.y - (hc_a.y + hc_b.y + hc2.y) - Im3.y * (ha_a.y + ha_b.y + ha2.y);
+            V Mc;
+            Mc.x = static_cast<T>(nrow * nc0) * s3.x - (hc_a.x + hc_b.x + hc2.x) - Im3.x * (ha_a.x + ha_b.x + ha2.x);
+            Mc.y = static_cast<T>(nrow * nc1) * s3.y - (hc_a.y + hc_b.y + hc2.y) - Im3.y * (ha_a.y + ha_b.y + ha2.y);
             // S5 at row Y-4
-            const double ML = __shfl_up_sync(FULL, M_b.y, 1), MR = __shfl_down_sync(FULL, M_b.x, 1);
-            const double t0 = 4.0 * M_b.x - M_a.x - Mc.x - ML - M_b.y;
-            const double t1 = 4.0 * M_b.y - M_a.y - Mc.y - M_b.x - MR;
-            const double2 val = make_double2(d4.x + t0 * lam, d4.y + t1 * lam);
+            const T ML = __shfl_up_sync(FULL, M_b.y, 1), MR = __shfl_down_sync(FULL, M_b.x, 1);
+            const T t0 = T(4) * M_b.x - M_a.x - Mc.x - ML - M_b.y;
+            const T t1 = T(4) * M_b.y - M_a.y - Mc.y - M_b.x - MR;
+            const V val = mk2(d4.x + t0 * lam, d4.y + t1 * lam);
             if (st_i >= 2 * HALO) {
                 if (writer) {
-                    *reinterpret_cast<double2*>(oc + o4c) = val;
+                    st2(oc + o4c, val);
                     const int yo = r0 + st_i - 2 * HALO;
-                    if (yo >= G.rlo && yo < G.rhi) dotp += pm4.x * val.x + pm4.y * val.y;
+                    if (yo >= G.rlo && yo < G.rhi)
+                        dotp += static_cast<double>(pm4.x) * static_cast<double>(val.x) +
+                                static_cast<double>(pm4.y) * static_cast<double>(val.y);
                 }
                 if (CG && (--blk_left == 0 || st_i + 1 == steps)) {  // close the row block
                     const double ws = warp_sum(dotp);

@@ -113,6 +113,7 @@ struct Context {
     // kernel profiling of the CG loop (bench.py roofline): total device ms and launches that
     // did work, per kernel class {K_Q, K_D, K_L (or the single K_A), K_U}
     bool profile = false;
+    int precision = 64;  // 64: reference precision; 32: fp32 mode of the HRMS CG (north_star)
     double prof_ms[4] = {0, 0, 0, 0};  // K_Q, K_D, K_L (K_A), K_U
     long long prof_n[4] = {0, 0, 0, 0};
 

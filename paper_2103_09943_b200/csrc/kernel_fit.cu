@@ -651,6 +651,8 @@ struct AdmmArgs {
     int cache_symbols;  // 1: per-frequency {u,p} symbols cached in shared memory
     int ginv_global;    // 1: the cluster's mat-vec rows are read from the inverse in global memory
                         //    (L2-resident) instead of a shared-memory slice (large kernels)
+    const double* tv_d1;  // TV kernel prior (run_tgv_or_tv(false, ...)): the u-step symbol d1 (n2,
+                          // host-evaluated as kernel_estimator.cpp:309-321); null = TGV^2
 };
 
 constexpr int NTADMM = 512;
@@ -920,6 +922,35 @@ __device__ void up_solve(const AdmmSmem& S, int n, double a1m1, double a2m2, dou
     }
     __syncthreads();
     double* dst[3] = {uout, p1out, p2out};
+    dft3_inverse(S, n, dst);
+}
+
+// TV u-step (kernel_estimator.cpp:356-364): u = F^-1( F(B1) / d1 ) with
+// B1 = (grad_h^T (x0 - L1_0) + grad_v^T (x1 - L1_1)) alpha1 mu1 + anchor mu3. p stays zero, so the
+// TGV x-step, y-step and multipliers of k_admm reduce to the TV ones exactly (y = L2 = 0).
+__device__ void tv_solve(const AdmmSmem& S, int n, double a1m1, double mu3, const double* x0, const double* x1,
+                         const double* L10, const double* L11, const double* anchor, const double* __restrict__ d1,
+                         double* uout, double* scratch) {
+    const int m = n * n;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        const int r = i / n, c = i - r * n;
+        const int cl = r * n + (c + n - 1) % n, ru = ((r + n - 1) % n) * n + c;
+        const double g1 = (x0[cl] - L10[cl]) - (x0[i] - L10[i]);  // ops.cpp:87-97
+        const double g2 = (x1[ru] - L11[ru]) - (x1[i] - L11[i]);
+        uout[i] = (g1 + g2) * a1m1 + anchor[i] * mu3;
+    }
+    __syncthreads();
+    const double* src[3] = {uout, uout, uout};
+    dft3_forward(S, n, src);
+    const int nh = n / 2 + 1;
+    for (int e = threadIdx.x; e < n * nh; e += blockDim.x) {
+        const int i = (e / nh) * n + (e % nh);
+        const double2 v = cld2(S.spec, i);
+        const double d = __ldg(d1 + i);
+        cst2(S.spec, i, v.x / d, v.y / d);
+    }
+    __syncthreads();
+    double* dst[3] = {uout, scratch, scratch};
     dft3_inverse(S, n, dst);
 }
 
@@ -1216,8 +1247,12 @@ __global__ void __launch_bounds__(NTADMM) k_admm(AdmmArgs A, const double* __res
         __syncthreads();
         APROF(4)
         // old p1, p2 are dead after the y-step: the solve writes them in place, u_new separately
-        up_solve(S, n, a1m1, a2m2, A.coupling, FLD(F_X0), FLD(F_X1), FLD(F_Y0), FLD(F_Y1), FLD(F_Y2), FLD(F_Y3), FLD(F_L10),
-                 FLD(F_L11), FLD(F_L20), FLD(F_L21), FLD(F_L22), FLD(F_L23), S.bz, Unew, FLD(F_P1), FLD(F_P2));
+        if (A.tv_d1)
+            tv_solve(S, n, a1m1, A.mu3, FLD(F_X0), FLD(F_X1), FLD(F_L10), FLD(F_L11), S.bz, A.tv_d1, Unew, S.zz);
+        else
+            up_solve(S, n, a1m1, a2m2, A.coupling, FLD(F_X0), FLD(F_X1), FLD(F_Y0), FLD(F_Y1), FLD(F_Y2), FLD(F_Y3),
+                     FLD(F_L10), FLD(F_L11), FLD(F_L20), FLD(F_L21), FLD(F_L22), FLD(F_L23), S.bz, Unew, FLD(F_P1),
+                     FLD(F_P2));
         APROF(5)
         // multipliers (:367-373), change of u (:375-376)
         double dd = 0.0, un = 0.0;
@@ -1503,8 +1538,23 @@ void build_observation(Context& ctx, const double* d_pan, const double* d_obs, i
 }
 
 void admm_device(Context& ctx, const ObsSystem& sys, const fbmp_ke_params& prm, double* d_state, bool init_state,
-                 int t_begin, int phase_begin, int hook_t, int* d_info, double* d_k) {
+                 int t_begin, int phase_begin, int hook_t, int* d_info, double* d_k, bool tv = false) {
     AdmmArgs A;
+    A.tv_d1 = nullptr;
+    if (tv) {  // kernel_estimator.cpp:309-321, evaluated on the host as the reference does
+        const int n = sys.n;
+        std::vector<double> d1(static_cast<size_t>(n) * n);
+        for (int r = 0; r < n; ++r) {
+            const double av2 = 2.0 - 2.0 * std::cos(2.0 * M_PI * r / n);
+            for (int c = 0; c < n; ++c) {
+                const double ah2 = 2.0 - 2.0 * std::cos(2.0 * M_PI * c / n);
+                d1[static_cast<size_t>(r) * n + c] = prm.alpha1 * prm.mu1 * (ah2 + av2) + prm.mu3;
+            }
+        }
+        double* dd = ctx.scratch<double>("admm_tv_d1", d1.size());
+        h2d(dd, d1.data(), d1.size() * sizeof(double), ctx.stream);
+        A.tv_d1 = dd;
+    }
     A.n = sys.n;
     A.m = sys.n2;
     A.alpha1 = prm.alpha1;
@@ -1604,7 +1654,7 @@ void project_simplex_device(Context& ctx, const double* d_v, int m, double* d_ou
 
 void estimate_kernel_device(Context& ctx, const double* d_pan, const double* d_obs, int S, int H, int W, int c,
                             const fbmp_ke_params& prm, double* d_k, std::vector<int>& iters, double* d_state_out,
-                            int hook_t) {
+                            int hook_t, bool tv) {
     validate_ke(prm);
     const int n = prm.n;
     if (c < 1) param_error("build_observation: factor must be >= 1");
@@ -1634,7 +1684,7 @@ void estimate_kernel_device(Context& ctx, const double* d_pan, const double* d_o
     const int m = n * n;
     double* state = d_state_out ? d_state_out : ctx.scratch<double>("ke_state", static_cast<size_t>(S) * 17 * m);
     int* info = ctx.scratch<int>("ke_info", static_cast<size_t>(S) * 4);
-    admm_device(ctx, sys, prm, state, true, 0, 0, hook_t, info, d_k);
+    admm_device(ctx, sys, prm, state, true, 0, 0, hook_t, info, d_k, tv);
     std::vector<int> hinfo(static_cast<size_t>(S) * 4), hst(S);
     d2h(hinfo.data(), info, hinfo.size() * sizeof(int), ctx.stream);
     d2h(hst.data(), sys.status, S * sizeof(int), ctx.stream);

@@ -57,10 +57,11 @@ void gram_device(Context& ctx, const double* d_pan, const double* d_obs, int H, 
                  double* d_Etf);
 
 // Full kernel estimate for S scenes from (pan, obs): writes kernels S*n2 (device) and
-// host-side iteration counts; throws the reference's errors.
+// host-side iteration counts; throws the reference's errors. tv: the TV kernel prior
+// (KernelPrior::tv, kernel_estimator.cpp:445-452) instead of TGV^2.
 void estimate_kernel_device(Context& ctx, const double* d_pan, const double* d_obs, int S, int H, int W, int c,
                             const fbmp_ke_params& prm, double* d_k, std::vector<int>& iters, double* d_state_out,
-                            int hook_t);
+                            int hook_t, bool tv = false);
 
 // Evaluation metrics (csrc/metrics.cu, metrics.hpp:11-51): device inputs, host outputs.
 void metrics_device(Context& ctx, const double* d_est, const double* d_ref, int N, int H, int W, int crop,

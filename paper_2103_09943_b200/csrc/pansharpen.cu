@@ -355,9 +355,11 @@ __global__ void __launch_bounds__(NTA) k_apply(PsGeo G, const double* __restrict
 // K_U: z += alpha p, r -= alpha Ap, ||r||^2, ||z||^2 and the relative-step stop test
 // (pansharpen.cpp:245-255).
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(NTU) k_update(PsGeo G, double* __restrict__ z, double* __restrict__ r,
-                                                const double* __restrict__ pbuf, const double* __restrict__ Ap,
+template <class T = double>
+__global__ void __launch_bounds__(NTU) k_update(PsGeo G, T* __restrict__ z, T* __restrict__ r,
+                                                const T* __restrict__ pbuf, const T* __restrict__ Ap,
                                                 CgState* st, double* __restrict__ part, int nblk) {
+    using V = fast::v2<T>;
     __shared__ double red[2 * (NTU / 32 + 1)];
     const int ch = blockIdx.y;
     // t and z, r, p are not written by K_A (the predecessor): read them before pdl_wait so the
@@ -365,10 +367,10 @@ __global__ void __launch_bounds__(NTU) k_update(PsGeo G, double* __restrict__ z,
     if (__syncthreads_or(st[ch].done)) return;  // uniform: the reductions below stay convergent
     const int t = st[ch].t;
     const size_t P = static_cast<size_t>(G.H) * G.W;
-    const double* pc = pbuf + (static_cast<size_t>(t & 1) * G.N + ch) * P;
-    double* zc = z + ch * P;
-    double* rc = r + ch * P;
-    const double* ac = Ap + ch * P;
+    const T* pc = pbuf + (static_cast<size_t>(t & 1) * G.N + ch) * P;
+    T* zc = z + ch * P;
+    T* rc = r + ch * P;
+    const T* ac = Ap + ch * P;
     double rr = 0.0, zz = 0.0;
     const size_t base = static_cast<size_t>(blockIdx.x) * NTU * UPT;
     const size_t own_lo = static_cast<size_t>(G.rlo) * G.W, own_hi = static_cast<size_t>(G.rhi) * G.W;
@@ -377,24 +379,24 @@ __global__ void __launch_bounds__(NTU) k_update(PsGeo G, double* __restrict__ z,
     if ((P & 1) == 0) {
         constexpr int KV = UPT / 2;
         const size_t nv = P / 2;
-        double2 pv[KV], av[KV], zv[KV], rv[KV];
+        V pv[KV], av[KV], zv[KV], rv[KV];
 #pragma unroll
         for (int k = 0; k < KV; ++k) {
             const size_t vi = base / 2 + static_cast<size_t>(k) * NTU + threadIdx.x;
             if (vi < nv) {
-                pv[k] = __ldcs(reinterpret_cast<const double2*>(pc) + vi);
-                zv[k] = __ldcs(reinterpret_cast<const double2*>(zc) + vi);
-                rv[k] = __ldcs(reinterpret_cast<const double2*>(rc) + vi);
+                pv[k] = __ldcs(reinterpret_cast<const V*>(pc) + vi);
+                zv[k] = __ldcs(reinterpret_cast<const V*>(zc) + vi);
+                rv[k] = __ldcs(reinterpret_cast<const V*>(rc) + vi);
             }
         }
         pdl_wait();
         pdl_trigger();
         if (__syncthreads_or(st[ch].done)) return;
-        const double alpha = st[ch].alpha;
+        const T alpha = static_cast<T>(st[ch].alpha);
 #pragma unroll
         for (int k = 0; k < KV; ++k) {
             const size_t vi = base / 2 + static_cast<size_t>(k) * NTU + threadIdx.x;
-            if (vi < nv) av[k] = __ldcs(reinterpret_cast<const double2*>(ac) + vi);
+            if (vi < nv) av[k] = __ldcs(reinterpret_cast<const V*>(ac) + vi);
         }
 #pragma unroll
         for (int k = 0; k < KV; ++k) {
@@ -402,31 +404,37 @@ __global__ void __launch_bounds__(NTU) k_update(PsGeo G, double* __restrict__ z,
             if (vi < nv) {
                 zv[k].x = zv[k].x + pv[k].x * alpha; zv[k].y = zv[k].y + pv[k].y * alpha;
                 rv[k].x = rv[k].x - av[k].x * alpha; rv[k].y = rv[k].y - av[k].y * alpha;
-                __stcs(reinterpret_cast<double2*>(zc) + vi, zv[k]);
-                __stcs(reinterpret_cast<double2*>(rc) + vi, rv[k]);
+                __stcs(reinterpret_cast<V*>(zc) + vi, zv[k]);
+                __stcs(reinterpret_cast<V*>(rc) + vi, rv[k]);
                 // owned rows only (all, unless the CG runs on a row strip); selects keep the
                 // whole-image sums bit-identical to the plain x^2 + y^2 accumulation
                 const bool ox = all_owned || (2 * vi >= own_lo && 2 * vi < own_hi);
                 const bool oy = all_owned || (2 * vi + 1 >= own_lo && 2 * vi + 1 < own_hi);
-                rr += (ox ? rv[k].x * rv[k].x : 0.0) + (oy ? rv[k].y * rv[k].y : 0.0);
-                zz += (ox ? zv[k].x * zv[k].x : 0.0) + (oy ? zv[k].y * zv[k].y : 0.0);
+                if constexpr (std::is_same<T, double>::value) {
+                    rr += (ox ? rv[k].x * rv[k].x : 0.0) + (oy ? rv[k].y * rv[k].y : 0.0);
+                    zz += (ox ? zv[k].x * zv[k].x : 0.0) + (oy ? zv[k].y * zv[k].y : 0.0);
+                } else {  // fp32 vectors, fp64 sums
+                    const double rx = rv[k].x, ry = rv[k].y, zx = zv[k].x, zy = zv[k].y;
+                    rr += (ox ? rx * rx : 0.0) + (oy ? ry * ry : 0.0);
+                    zz += (ox ? zx * zx : 0.0) + (oy ? zy * zy : 0.0);
+                }
             }
         }
     } else {
         pdl_wait();
         pdl_trigger();
         if (__syncthreads_or(st[ch].done)) return;
-        const double alpha = st[ch].alpha;
+        const T alpha = static_cast<T>(st[ch].alpha);
         for (int k = 0; k < UPT; ++k) {
             const size_t i = base + static_cast<size_t>(k) * NTU + threadIdx.x;
             if (i >= P) break;
-            const double zv = zc[i] + pc[i] * alpha;
-            const double rv = rc[i] - ac[i] * alpha;
+            const T zv = zc[i] + pc[i] * alpha;
+            const T rv = rc[i] - ac[i] * alpha;
             zc[i] = zv;
             rc[i] = rv;
             if (all_owned || (i >= own_lo && i < own_hi)) {
-                rr += rv * rv;
-                zz += zv * zv;
+                rr += static_cast<double>(rv) * static_cast<double>(rv);
+                zz += static_cast<double>(zv) * static_cast<double>(zv);
             }
         }
     }
@@ -465,15 +473,16 @@ __global__ void __launch_bounds__(NTU) k_update(PsGeo G, double* __restrict__ z,
 
 // CG initialisation after rhs = B^T U x has been written to r by K_D (pansharpen.cpp:225-235):
 // z = 0, p_old = 0, rs = ||rhs||^2 over the owned rows, state reset.
-__global__ void __launch_bounds__(NTU) k_cg_init(PsGeo G, const double* __restrict__ r, double* __restrict__ z,
-                                                 double* __restrict__ p1, CgState* st, double* __restrict__ part,
+template <class T = double>
+__global__ void __launch_bounds__(NTU) k_cg_init(PsGeo G, const T* __restrict__ r, T* __restrict__ z,
+                                                 T* __restrict__ p1, CgState* st, double* __restrict__ part,
                                                  int nblk, int max_iters, double cg_tol) {
     __shared__ double red[NTU / 32 + 1];
     const int ch = blockIdx.y;
     const size_t P = static_cast<size_t>(G.H) * G.W;
-    const double* rc = r + ch * P;
-    double* zc = z + ch * P;
-    double* pc = p1 + ch * P;
+    const T* rc = r + ch * P;
+    T* zc = z + ch * P;
+    T* pc = p1 + ch * P;
     const size_t own_lo = static_cast<size_t>(G.rlo) * G.W, own_hi = static_cast<size_t>(G.rhi) * G.W;
     double ss = 0.0;
     const size_t base = static_cast<size_t>(blockIdx.x) * NTU * UPT;
@@ -482,8 +491,8 @@ __global__ void __launch_bounds__(NTU) k_cg_init(PsGeo G, const double* __restri
         const size_t i = base + static_cast<size_t>(k) * NTU + threadIdx.x;
         if (i < P) {
             const double v = rc[i];
-            zc[i] = 0.0;
-            pc[i] = 0.0;
+            zc[i] = T(0);
+            pc[i] = T(0);
             ss += (i >= own_lo && i < own_hi) ? v * v : 0.0;
         }
     }
@@ -667,6 +676,161 @@ __global__ void __launch_bounds__(NTA) k_guided(int H, int W, int rw, double eps
 }
 
 // ------------------------------------------------------------------------------------------
+// Guided filter, tiled and separable (pansharpen.cpp:274-312, box_mean = ops.cpp:104-128 with
+// clamped windows). One CTA per (32 x 32 output tile, channel); the radius is a template
+// parameter, so every staged region has compile-time extents and all passes are flattened
+// element loops over the 256 threads (no partially filled warps, constant divisors). Box sums
+// are separable: row sums over the clamped column range, then column sums over the clamped row
+// range (out-of-image taps contribute exact zeros; the count is the clamped window's size). The
+// input is L(z0) from a z0 tile with a one-pixel larger halo (Z0), else the plane itself.
+// Requires H, W >= tile + halo (wrap1).
+// ------------------------------------------------------------------------------------------
+constexpr int GTW = 32, GTH = 32, GNT = 256;
+__device__ __forceinline__ int wrap1(int a, int m) {  // valid for -m <= a < 2m
+    a += a < 0 ? m : 0;
+    return a >= m ? a - m : a;
+}
+template <int RW, bool Z0>
+struct GfLay {
+    static constexpr int HZ = 2 * RW + (Z0 ? 1 : 0), HIN = 2 * RW, HAC = RW;
+    static constexpr int NR = GTH + 2 * HIN, NC = GTW + 2 * HIN, AR = GTH + 2 * HAC, AC = GTW + 2 * HAC;
+    static constexpr int ZR = GTH + 2 * HZ, ZC = GTW + 2 * HZ;
+    static constexpr int HS = (4 * NR * AC > ZR * ZC) ? 4 * NR * AC : ZR * ZC;  // row sums | z0 tile
+    static constexpr size_t bytes = (2 * static_cast<size_t>(NR) * NC + 2 * static_cast<size_t>(AR) * AC + HS) *
+                                    sizeof(double);
+};
+template <int RW, bool Z0>
+__global__ void __launch_bounds__(GNT) k_guided2(int H, int W, double eps, int cps, const double* __restrict__ in,
+                                                 const double* __restrict__ guide, double* __restrict__ aout,
+                                                 double* __restrict__ cout, double* __restrict__ vout) {
+    using L = GfLay<RW, Z0>;
+    constexpr int NR = L::NR, NC = L::NC, AR = L::AR, AC = L::AC, ZR = L::ZR, ZC = L::ZC;
+    constexpr int HIN = L::HIN, HAC = L::HAC, HZ = L::HZ;
+    extern __shared__ double sm[];
+    const int ch = blockIdx.y;
+    const size_t P = static_cast<size_t>(H) * W;
+    const int ntx = (W + GTW - 1) / GTW;
+    const int by = blockIdx.x / ntx, bx = blockIdx.x - by * ntx;
+    const int r0 = by * GTH, c0 = bx * GTW;
+    double* sI = sm;                 // guide, NR x NC
+    double* sIn = sI + NR * NC;      // filter input, NR x NC
+    double* sa = sIn + NR * NC;      // a, AR x AC
+    double* sc = sa + AR * AC;       // c
+    double* rs = sc + AR * AC;       // 4 row-sum planes NR x AC (then 2 planes AR x GTW)
+    double* sZ = rs;                 // z0 tile (dead before the row sums are formed)
+    const int t = threadIdx.x;
+    const double* gs = guide + static_cast<size_t>(ch / cps) * P;
+    const double* ic = in + static_cast<size_t>(ch) * P;
+    for (int e = t; e < NR * NC; e += GNT) {
+        const int y = e / NC, x = e - y * NC;
+        sI[e] = __ldg(gs + static_cast<size_t>(wrap1(r0 - HIN + y, H)) * W + wrap1(c0 - HIN + x, W));
+    }
+    if (Z0) {
+        for (int e = t; e < ZR * ZC; e += GNT) {
+            const int y = e / ZC, x = e - y * ZC;
+            sZ[e] = __ldg(ic + static_cast<size_t>(wrap1(r0 - HZ + y, H)) * W + wrap1(c0 - HZ + x, W));
+        }
+        __syncthreads();
+        for (int e = t; e < NR * NC; e += GNT) {
+            const int y = e / NC, x = e - y * NC;
+            const double* z = sZ + (y + 1) * ZC + x + 1;  // ops.cpp:70-78 order
+            sIn[e] = 4.0 * z[0] - z[-ZC] - z[ZC] - z[-1] - z[1];
+        }
+    } else {
+        for (int e = t; e < NR * NC; e += GNT) {
+            const int y = e / NC, x = e - y * NC;
+            sIn[e] = __ldg(ic + static_cast<size_t>(wrap1(r0 - HIN + y, H)) * W + wrap1(c0 - HIN + x, W));
+        }
+    }
+    __syncthreads();
+    // guided_coeffs (pansharpen.cpp:274-301): row sums of I, I^2, in, I in over the clamped columns
+    // of A-region column x (staging columns x + RW + k, k in [-RW, RW]; out-of-image taps add 0)
+    for (int e = t; e < NR * AC; e += GNT) {
+        const int y = e / AC, x = e - y * AC;
+        const int gc = c0 - HAC + x;
+        double s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0;
+#pragma unroll
+        for (int k = -RW; k <= RW; ++k) {
+            const bool ok = gc + k >= 0 && gc + k < W;
+            const double gv = ok ? sI[y * NC + x + RW + k] : 0.0;
+            const double iv = ok ? sIn[y * NC + x + RW + k] : 0.0;
+            s1 += gv;
+            s2 += iv;
+            s3 += gv * iv;
+            s4 += gv * gv;
+        }
+        rs[e] = s1;
+        rs[NR * AC + e] = s2;
+        rs[2 * NR * AC + e] = s3;
+        rs[3 * NR * AC + e] = s4;
+    }
+    __syncthreads();
+    for (int e = t; e < AR * AC; e += GNT) {
+        const int y = e / AC, x = e - y * AC;
+        const int gr = r0 - HAC + y, gc = c0 - HAC + x;
+        double a = 0.0, cc = 0.0;
+        if (gr >= 0 && gr < H && gc >= 0 && gc < W) {
+            double s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0;
+#pragma unroll
+            for (int k = -RW; k <= RW; ++k) {
+                if (gr + k < 0 || gr + k >= H) continue;
+                const int o = (y + RW + k) * AC + x;
+                s1 += rs[o];
+                s2 += rs[NR * AC + o];
+                s3 += rs[2 * NR * AC + o];
+                s4 += rs[3 * NR * AC + o];
+            }
+            const int nr = min(H - 1, gr + RW) - max(0, gr - RW) + 1, nc = min(W - 1, gc + RW) - max(0, gc - RW) + 1;
+            const double inv = 1.0 / static_cast<double>(nr * nc);  // one division per window
+            const double mu = s1 * inv, im = s2 * inv, cgi = s3 * inv, cgg = s4 * inv;
+            const double var = cgg - mu * mu;  // pansharpen.cpp:293-298
+            const double cov = cgi - mu * im;
+            a = cov / (var + eps);
+            cc = im - a * mu;
+        }
+        sa[e] = a;
+        sc[e] = cc;
+    }
+    __syncthreads();
+    // guided_output (pansharpen.cpp:304-312): row sums of a, c over the clamped columns
+    double* ra = rs;
+    double* rc = rs + AR * GTW;
+    for (int e = t; e < AR * GTW; e += GNT) {
+        const int y = e / GTW, x = e - y * GTW;
+        const int gc = c0 + x;
+        double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+        for (int k = -RW; k <= RW; ++k) {
+            const bool ok = gc + k >= 0 && gc + k < W;
+            s1 += ok ? sa[y * AC + x + RW + k] : 0.0;
+            s2 += ok ? sc[y * AC + x + RW + k] : 0.0;
+        }
+        ra[e] = s1;
+        rc[e] = s2;
+    }
+    __syncthreads();
+    for (int e = t; e < GTH * GTW; e += GNT) {
+        const int y = e / GTW, x = e - y * GTW;
+        const int R = r0 + y, Cc = c0 + x;
+        if (R >= H || Cc >= W) continue;
+        double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+        for (int k = -RW; k <= RW; ++k) {
+            if (R + k < 0 || R + k >= H) continue;
+            s1 += ra[(y + RW + k) * GTW + x];
+            s2 += rc[(y + RW + k) * GTW + x];
+        }
+        const int nr = min(H - 1, R + RW) - max(0, R - RW) + 1, nc = min(W - 1, Cc + RW) - max(0, Cc - RW) + 1;
+        const double inv = 1.0 / static_cast<double>(nr * nc);
+        const double gv = sI[(y + HIN) * NC + x + HIN];
+        const size_t gi = static_cast<size_t>(ch) * P + static_cast<size_t>(R) * W + Cc;
+        vout[gi] = (s1 * inv) * gv + s2 * inv;
+        if (aout) aout[gi] = sa[(y + HAC) * AC + x + HAC];
+        if (cout) cout[gi] = sc[(y + HAC) * AC + x + HAC];
+    }
+}
+
+// ------------------------------------------------------------------------------------------
 // Alias-group direct solve (pansharpen.cpp:337-363): one thread per LR frequency (kl, ll).
 // The c^2 x c^2 system A = diag(D) + u u^H / c^2 (D = lambda |L^|^2, u = conj(b^)) is solved in
 // closed form, eliminating through the coordinate j with the smallest D (the one that can be
@@ -692,7 +856,7 @@ __device__ __forceinline__ cplx half_lookup(const double2* X, int R, int Cc, int
 }
 
 // smallest root of c2 + sum |u_g|^2/(D_g - x) in (lo, hi), by bisection
-__device__ __noinline__ double secular_root(int m, const double* D, const double* u2, double c2, double lo,
+__device__ __forceinline__ double secular_root(int m, const double* D, const double* u2, double c2, double lo,
                                             double hi) {
     for (int it = 0; it < 200; ++it) {
         const double mid = 0.5 * (lo + hi);
@@ -706,7 +870,7 @@ __device__ __noinline__ double secular_root(int m, const double* D, const double
     return 0.5 * (lo + hi);
 }
 
-__device__ __noinline__ bool alias_condition_ok(int m, const double* D, const double* u2, double c2) {
+__device__ __forceinline__ bool alias_condition_ok(int m, const double* D, const double* u2, double c2) {
     double dmin_all = INFINITY, dmax_all = -INFINITY;
     double dmin_u = INFINITY, d2_u = INFINITY, dmax_u = -INFINITY, unorm = 0.0;
     int mult_min = 0;
@@ -745,6 +909,165 @@ __device__ __noinline__ bool alias_condition_ok(int m, const double* D, const do
 __global__ void k_cos_tables(int H, int W, double* __restrict__ tab) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < H + W; i += gridDim.x * blockDim.x)
         tab[i] = i < H ? cos(2.0 * M_PI * i / H) : cos(2.0 * M_PI * (i - H) / W);
+}
+
+// ------------------------------------------------------------------------------------------
+// Alias-group solve, one 16-lane group per alias group (factor c <= 4, m = c^2 <= 16 members):
+// lane g of the group owns member g (its D, u = conj(b^), rhs live in registers; nothing is
+// indexed dynamically, so there is no local-memory frame). The group loops over the channels of
+// its scene: b^ and the Laplacian symbol are loaded once for all of them. Sums over the members
+// (sigma's numerator/denominator, u^H z) are xor-butterflies, identical on every lane.
+// Same closed form as k_alias; the rare inconclusive interlacing bound goes to the exact
+// secular-equation check, evaluated by the whole group (alias_condition_grp).
+// ------------------------------------------------------------------------------------------
+constexpr int AG = 16;          // lanes per alias group
+constexpr int AG_NT = 128;      // threads per CTA (8 groups)
+// group reductions over the 16 lanes of an alias group (gm = the group's lane mask)
+__device__ __forceinline__ double grp_sum(unsigned gm, double v) {
+#pragma unroll
+    for (int o = 1; o < AG; o <<= 1) v += __shfl_xor_sync(gm, v, o, AG);
+    return v;
+}
+__device__ __forceinline__ double grp_max(unsigned gm, double v) {
+#pragma unroll
+    for (int o = 1; o < AG; o <<= 1) v = fmax(v, __shfl_xor_sync(gm, v, o, AG));
+    return v;
+}
+__device__ __forceinline__ double grp_min(unsigned gm, double v) {
+#pragma unroll
+    for (int o = 1; o < AG; o <<= 1) v = fmin(v, __shfl_xor_sync(gm, v, o, AG));
+    return v;
+}
+// smallest root of c2 + sum_g |u_g|^2 / (D_g - x) in (lo, hi) by bisection; each lane holds one
+// member's term, the sum is a group butterfly (identical on all lanes, so every lane takes the
+// same branch)
+__device__ double secular_root_grp(unsigned gm, bool uu, double D, double u2, double c2, double lo, double hi) {
+    for (int it = 0; it < 200; ++it) {
+        const double mid = 0.5 * (lo + hi);
+        if (!(mid > lo && mid < hi)) break;
+        const double f = c2 + grp_sum(gm, uu ? u2 / (D - mid) : 0.0);
+        if (f > 0.0) hi = mid;
+        else lo = mid;
+    }
+    return 0.5 * (lo + hi);
+}
+// pansharpen.cpp:353-357 for a group whose cheap interlacing bound was inconclusive: the exact
+// extremal eigenvalues of diag(D) + u u^H / c^2 (deflated members and the secular equation),
+// as alias_condition_ok, with the member loops as group reductions
+__device__ bool alias_condition_grp(unsigned gm, bool mem, double D, double u2, double c2, double unorm) {
+    const bool uu = mem && u2 > 0.0;
+    const double dmin_u = grp_min(gm, uu ? D : INFINITY);
+    const double mult_min = grp_sum(gm, (uu && D == dmin_u) ? 1.0 : 0.0);
+    const double d2_u = grp_min(gm, (uu && D > dmin_u) ? D : INFINITY);
+    const double dmax_u = grp_max(gm, uu ? D : -INFINITY);
+    double ev_min = grp_min(gm, (mem && !uu) ? D : INFINITY);
+    double ev_max = grp_max(gm, (mem && !uu) ? D : -INFINITY);
+    if (unorm > 0.0) {
+        double r;
+        if (mult_min >= 2.0) r = dmin_u;
+        else if (!(d2_u < INFINITY)) r = dmin_u + unorm / c2;
+        else r = secular_root_grp(gm, uu, D, u2, c2, dmin_u, d2_u);
+        ev_min = fmin(ev_min, r);
+        const double top = secular_root_grp(gm, uu, D, u2, c2, dmax_u, dmax_u + unorm / c2 * (1.0 + 1e-12) + 1e-300);
+        ev_max = fmax(ev_max, top);
+    }
+    return (ev_min > 0.0) && !(ev_max > 1e14 * ev_min);
+}
+// 1/x to within an ulp: MUFU seed + two Newton steps, inline (no IEEE division subroutine call)
+__device__ __forceinline__ double rcp_nr(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-x, y, 1.0);
+    return fma(y, e, y);
+}
+__global__ void __launch_bounds__(AG_NT) k_alias16(int H, int W, int h, int w, int c, int N, int cps,
+                                                   double lambda, const double2* __restrict__ Bh,
+                                                   const double2* __restrict__ Xh, const double2* __restrict__ Vh,
+                                                   double2* __restrict__ Zh, const double* __restrict__ cosHW,
+                                                   int* __restrict__ flag) {
+    const int g = threadIdx.x & (AG - 1);
+    const unsigned gm = 0xffffu << (threadIdx.x & AG);  // this group's half of the warp
+    const int gid = static_cast<int>(blockIdx.x) * (AG_NT / AG) + static_cast<int>(threadIdx.x / AG);  // h w < 2^31
+    const bool live = gid < h * w;   // uniform over the group
+    const int kl = live ? gid / w : 0, ll = live ? gid - kl * w : 0;
+    const int m = c * c;
+    const bool mem = live && g < m;
+    const double c2 = static_cast<double>(m);
+    const int scene = blockIdx.y;
+    const size_t HS = static_cast<size_t>(H) * (W / 2 + 1), LS = static_cast<size_t>(h) * (w / 2 + 1);
+    const int WH = W / 2 + 1;
+    const int a = mem ? g / c : 0, b = mem ? g - (g / c) * c : 0;
+    const int R = kl + a * h, Cc = ll + b * w;
+    // half-spectrum index of member (R, Cc) and whether it is read through Hermitian symmetry
+    const bool mirror = Cc >= WH;
+    const size_t hidx = mirror ? static_cast<size_t>((H - R) % H) * WH + (W - Cc) : static_cast<size_t>(R) * WH + Cc;
+    double D = INFINITY, lh = 0.0;
+    cplx u = {0.0, 0.0};
+    if (mem) {
+        const double2 bv = __ldg(Bh + static_cast<size_t>(scene) * HS + hidx);
+        u = {bv.x, mirror ? bv.y : -bv.y};  // conj(b^)
+        lh = 4.0 - 2.0 * __ldg(cosHW + R) - 2.0 * __ldg(cosHW + H + Cc);  // pansharpen.cpp:56-63
+        D = lambda * (lh * lh);
+    }
+    const double u2 = mem ? cnorm(u) : 0.0;
+    const double rD = mem ? rcp_nr(D) : 0.0;  // reciprocals: no division subroutine calls
+    // jmin = first member with the smallest D (the sequential strict-< scan of k_alias)
+    double dmin = D;
+    int jmin = mem ? g : AG;
+#pragma unroll
+    for (int o = 1; o < AG; o <<= 1) {
+        const double od = __shfl_xor_sync(gm, dmin, o, AG);
+        const int oj = __shfl_xor_sync(gm, jmin, o, AG);
+        if (od < dmin || (od == dmin && oj < jmin)) { dmin = od; jmin = oj; }
+    }
+    const bool isj = mem && g == jmin;
+    // condition test (pansharpen.cpp:353-357): cheap interlacing bound, exact check if inconclusive
+    const double dmax_all = grp_max(gm, mem ? D : -INFINITY);
+    const double unorm = grp_sum(gm, u2 > 0.0 ? u2 : 0.0);
+    bool ok = dmin > 0.0 && dmax_all + unorm / c2 <= 1e14 * dmin;
+    if (live && !ok) ok = alias_condition_grp(gm, mem, D, u2, c2, unorm);  // group-uniform branch
+    const double Dj = dmin;
+    const double u2j = __shfl_sync(gm, u2, jmin & (AG - 1), AG);
+    const int ch1 = min(N, (scene + 1) * cps);
+    for (int ch = scene * cps; ch < ch1; ++ch) {
+        if (live && !ok && g == 0) atomicExch(flag + ch, 1);
+        cplx rhs = {0.0, 0.0};
+        if (live) {
+            const double2 xv = __ldg(Xh + ch * LS + (ll < w / 2 + 1 ? static_cast<size_t>(kl) * (w / 2 + 1) + ll
+                                                               : static_cast<size_t>((h - kl) % h) * (w / 2 + 1) + (w - ll)));
+            const cplx xg = {xv.x, ll < w / 2 + 1 ? xv.y : -xv.y};
+            if (mem) {
+                const double2 vv2 = __ldg(Vh + ch * HS + hidx);
+                const cplx vv = {vv2.x, mirror ? -vv2.y : vv2.y};
+                const cplx ux = cmul(u, xg);
+                rhs = {ux.x + lambda * lh * vv.x, ux.y + lambda * lh * vv.y};
+            }
+        }
+        // sigma = u^H z / c^2 from the D_j-scaled secular identity (exact for D_j = 0)
+        const cplx t = cmul(cconj(u), rhs);
+        const double ratio = isj ? 1.0 : (mem ? Dj * rD : 0.0);
+        const double num_x = grp_sum(gm, t.x * ratio), num_y = grp_sum(gm, t.y * ratio);
+        const double den = c2 * Dj + grp_sum(gm, mem ? u2 * ratio : 0.0);
+        const double rden = rcp_nr(den);
+        const cplx sigma = {num_x * rden, num_y * rden};
+        const cplx us = cmul(u, sigma);
+        cplx zg = {0.0, 0.0};
+        if (mem && !isj) zg = {(rhs.x - us.x) * rD, (rhs.y - us.y) * rD};
+        const cplx tz = cmul(cconj(u), zg);
+        const double zs_x = grp_sum(gm, tz.x), zs_y = grp_sum(gm, tz.y);
+        if (isj) {
+            if (u2j < c2 * Dj) {
+                zg = {(rhs.x - us.x) * rD, (rhs.y - us.y) * rD};  // rD = 1 / Dj on this lane
+            } else {
+                const cplx s = {c2 * sigma.x - zs_x, c2 * sigma.y - zs_y};
+                const double ru = rcp_nr(u2j);
+                zg = {(s.x * u.x - s.y * u.y) * ru, (s.y * u.x + s.x * u.y) * ru};  // s / conj(u) = s u / |u|^2
+            }
+        }
+        if (mem && !mirror) Zh[ch * HS + hidx] = make_double2(zg.x, zg.y);
+    }
 }
 
 template <int CM>
@@ -973,34 +1296,40 @@ bool fast_ok(const PsGeo& G) {
            std::getenv("FBMP_DISABLE_FAST") == nullptr;
 }
 
-using QFn = void (*)(PsGeo, const double*, const double*, double*, double*, CgState*, double*, int);
-struct QLaunch {
-    QFn fn = nullptr;
+template <class T>
+using QFnT = void (*)(PsGeo, const T*, const T*, T*, T*, CgState*, double*, int);
+template <class T>
+struct QLaunchT {
+    QFnT<T> fn = nullptr;
     size_t smem = 0;
     int nblk = 0;
     int threads = 0;
     bool streaming = false;  // K_Q3
 };
-template <int N_, int CF, bool CG>
-QLaunch q2_make(const PsGeo& G) {
-    QLaunch L;
+using QLaunch = QLaunchT<double>;
+// K_Q2's shared memory for storage type T (QGeo counts doubles)
+template <int N_, int CF, int MJ, class T>
+constexpr size_t q2_smem() { return fast::QGeo<N_, CF, MJ>::smem / sizeof(double) * sizeof(T); }
+template <int N_, int CF, bool CG, class T = double>
+QLaunchT<T> q2_make(const PsGeo& G) {
+    QLaunchT<T> L;
     // narrow images (C1: 64 LR columns) are latency-bound: 1 LR column per lane gives 4x the CTAs
     // (the per-output summation order does not depend on MJ). Env FBMP_KQ2_MJ overrides.
     static const int mj_env = std::getenv("FBMP_KQ2_MJ") ? std::atoi(std::getenv("FBMP_KQ2_MJ")) : 0;
     const int mj = mj_env ? mj_env : (CF == 4 && G.w <= 64 ? 1 : 4);
     if (mj == 1) {
-        L.fn = fast::k_q2<N_, CF, CG, 1>;
-        L.smem = fast::QGeo<N_, CF, 1>::smem;
+        L.fn = fast::k_q2<N_, CF, CG, 1, T>;
+        L.smem = q2_smem<N_, CF, 1, T>();
         L.nblk = fast::q2_blocks<N_, CF, 1>(G);
         L.threads = fast::QGeo<N_, CF, 1>::NTH;
     } else if (mj == 2) {
-        L.fn = fast::k_q2<N_, CF, CG, 2>;
-        L.smem = fast::QGeo<N_, CF, 2>::smem;
+        L.fn = fast::k_q2<N_, CF, CG, 2, T>;
+        L.smem = q2_smem<N_, CF, 2, T>();
         L.nblk = fast::q2_blocks<N_, CF, 2>(G);
         L.threads = fast::QGeo<N_, CF, 2>::NTH;
     } else {
-        L.fn = fast::k_q2<N_, CF, CG>;
-        L.smem = fast::QGeo<N_, CF>::smem;
+        L.fn = fast::k_q2<N_, CF, CG, 4, T>;
+        L.smem = q2_smem<N_, CF, 4, T>();
         L.nblk = fast::q2_blocks<N_, CF>(G);
         L.threads = fast::QGeo<N_, CF>::NTH;
     }
@@ -1009,12 +1338,12 @@ QLaunch q2_make(const PsGeo& G) {
 // K_Q3 strip plan: LR-row strips of SR rows per band. Large problems take the tallest SR in
 // {128, 64, 32} that still gives >= 4 waves (halo overhead 2g/SR); small ones one wave of CTAs
 // (occupancy from the runtime), floored at 4 rows. Env FBMP_KQ3_SR overrides.
-template <int N_, bool CG>
-QLaunch q3_make(const PsGeo& G) {
+template <int N_, bool CG, class T = double>
+QLaunchT<T> q3_make(const PsGeo& G) {
     constexpr int MJ = 2;
-    using Q = fast::q3::Geo<N_, MJ>;
-    QLaunch L;
-    L.fn = fast::k_q3<N_, MJ, CG>;
+    using Q = fast::q3::Geo<N_, MJ, T>;
+    QLaunchT<T> L;
+    L.fn = fast::k_q3<N_, MJ, CG, T>;
     L.smem = Q::smem;
     L.threads = fast::q3::NTH;
     L.streaming = true;
@@ -1054,43 +1383,47 @@ bool q3_ok(const PsGeo& G) {
     return !off && G.c == 4 && G.w >= std::max(64, minw) && G.W % 4 == 0;
 }
 
-template <bool CG>
-QLaunch q2_select(const PsGeo& G) {
+template <bool CG, class T = double>
+QLaunchT<T> q2_select(const PsGeo& G) {
     if (!fast_ok(G)) return {};
     if (G.c == 4 && q3_ok(G)) {
         switch (G.n) {
-        case 21: return q3_make<21, CG>(G);
-        case 17: return q3_make<17, CG>(G);
-        case 15: return q3_make<15, CG>(G);
-        case 7: return q3_make<7, CG>(G);
+        case 21: return q3_make<21, CG, T>(G);
+        case 17: return q3_make<17, CG, T>(G);
+        case 15: return q3_make<15, CG, T>(G);
+        case 7: return q3_make<7, CG, T>(G);
         default: break;
         }
     }
     if (G.c == 4) {
         switch (G.n) {
-        case 21: return q2_make<21, 4, CG>(G);
-        case 17: return q2_make<17, 4, CG>(G);
-        case 15: return q2_make<15, 4, CG>(G);
-        case 7: return q2_make<7, 4, CG>(G);
+        case 21: return q2_make<21, 4, CG, T>(G);
+        case 17: return q2_make<17, 4, CG, T>(G);
+        case 15: return q2_make<15, 4, CG, T>(G);
+        case 7: return q2_make<7, 4, CG, T>(G);
         default: break;
         }
     } else if (G.c == 2) {
         switch (G.n) {
-        case 5: return q2_make<5, 2, CG>(G);
-        case 3: return q2_make<3, 2, CG>(G);
+        case 5: return q2_make<5, 2, CG, T>(G);
+        case 3: return q2_make<3, 2, CG, T>(G);
         default: break;
         }
     }
     return {};
 }
 
-// per-scene (mu_k, g_k) maps for the fast K_A
-void guide_stats(Context& ctx, const PsGeo& G, const double* d_guide, double* mu, double* gk) {
+// per-scene (mu_k, g_k) maps for the fast K_A (formed in fp64, stored as T)
+template <class T>
+void guide_stats_t(Context& ctx, const PsGeo& G, const double* d_guide, T* mu, T* gk) {
     const int S = (G.N + G.cps - 1) / G.cps;
     fast::k_guide_stats<<<dim3(grid1d(ctx, static_cast<long long>(G.H) * G.W), S), 256, 0, ctx.stream>>>(
         d_guide, G.H, G.W, G.rw, G.eps, mu, gk);
     ctx.count();
     check_launch();
+}
+void guide_stats(Context& ctx, const PsGeo& G, const double* d_guide, double* mu, double* gk) {
+    guide_stats_t<double>(ctx, G, d_guide, mu, gk);
 }
 
 using AFn = void (*)(PsGeo, const double*, const double*, const double*, const double*, const double*,
@@ -1122,16 +1455,17 @@ inline bool use_llp() {
 }
 // Strip height: minimise rounds x (R + 8) (a warp's steps, 8 = pipeline warm-up rows) over the
 // resident warp slots; R is a multiple of the partial row block.
+template <class T = double>
 LlpPlan llp_plan(Context& ctx, const PsGeo& G) {
     static int per_sm[2] = {0, 0};
     LlpPlan L;
     static const bool no_pairs = std::getenv("FBMP_KL1") != nullptr;
-    L.pairs = (G.W % 2 == 0) && !no_pairs;
+    L.pairs = (G.W % 2 == 0) && (!no_pairs || !std::is_same<T, double>::value);
     int& ps = per_sm[L.pairs ? 1 : 0];
     if (!ps) {
         int blocks = 0;
         if (L.pairs)
-            FBMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fast::k_llp2<true>, fast::kl::NTL, 0));
+            FBMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fast::k_llp2<true, T>, fast::kl::NTL, 0));
         else
             FBMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fast::k_llp<true>, fast::kl::NTL, 0));
         ps = std::max(1, std::min(blocks, 32)) * (fast::kl::NTL / 32);
@@ -1154,86 +1488,94 @@ LlpPlan llp_plan(Context& ctx, const PsGeo& G) {
     L.ctas = L.nb * L.k;
     return L;
 }
-template <bool CG>
-std::pair<void (*)(PsGeo, const double*, const double*, double*, const CgState*), size_t> dterm_select(const PsGeo& G) {
+template <bool CG, class T = double>
+std::pair<void (*)(PsGeo, const T*, const T*, T*, const CgState*), size_t> dterm_select(const PsGeo& G) {
+    constexpr size_t sc = sizeof(T);  // dterm_smem counts doubles
     if (G.c == 4) {
-        const size_t sm = fast::kl::dterm_smem<4>(G.cpc);  // register-tap variants hold every channel's window
+        const size_t sm = fast::kl::dterm_smem<4>(G.cpc) / 8 * sc;  // register-tap variants hold every channel's window
         switch (G.n) {
-        case 21: return {fast::k_dterm<CG, 21, 4>, sm};
-        case 17: return {fast::k_dterm<CG, 17, 4>, sm};
-        case 15: return {fast::k_dterm<CG, 15, 4>, sm};
-        case 7: return {fast::k_dterm<CG, 7, 4>, sm};
-        default: return {fast::k_dterm<CG, 0, 4>, fast::kl::dterm_smem<4>()};
+        case 21: return {fast::k_dterm<CG, 21, 4, T>, sm};
+        case 17: return {fast::k_dterm<CG, 17, 4, T>, sm};
+        case 15: return {fast::k_dterm<CG, 15, 4, T>, sm};
+        case 7: return {fast::k_dterm<CG, 7, 4, T>, sm};
+        default: return {fast::k_dterm<CG, 0, 4, T>, fast::kl::dterm_smem<4>() / 8 * sc};
         }
     }
-    if (G.c == 2) return {fast::k_dterm<CG, 0, 2>, fast::kl::dterm_smem<2>()};
-    return {fast::k_dterm<CG, 0, 1>, fast::kl::dterm_smem<1>()};
+    if (G.c == 2) return {fast::k_dterm<CG, 0, 2, T>, fast::kl::dterm_smem<2>() / 8 * sc};
+    return {fast::k_dterm<CG, 0, 1, T>, fast::kl::dterm_smem<1>() / 8 * sc};
 }
-template <bool CG>
-void launch_llp(Context& ctx, const PsGeo& G, const double* taps, const double* guide, const double* mu,
-                const double* gk, const double* p, const double* q, double* out, CgState* st, double* part,
+template <bool CG, class T = double>
+void launch_llp(Context& ctx, const PsGeo& G, const T* taps, const T* guide, const T* mu,
+                const T* gk, const T* p, const T* q, T* out, CgState* st, double* part,
                 bool pdl = false, cudaEvent_t between = nullptr) {
     const int S = (G.N + G.cps - 1) / G.cps;
     const int nba = ceil_div(G.W, fast::a4::TA) * ceil_div(G.H, fast::a4::TA);
     const int groups = (G.cps + G.cpc - 1) / G.cpc;
-    const auto fd = dterm_select<CG>(G);
+    const auto fd = dterm_select<CG, T>(G);
     if (pdl)
         launch_pdl(fd.first, dim3(nba, S * groups), dim3(fast::NT), fd.second, ctx.stream, G, taps, q, out,
                    static_cast<const CgState*>(st));
     else
         fd.first<<<dim3(nba, S * groups), fast::NT, fd.second, ctx.stream>>>(G, taps, q, out, st);
     if (between) FBMP_CUDA(cudaEventRecordWithFlags(between, ctx.stream, cudaEventRecordExternal));
-    const LlpPlan L = llp_plan(ctx, G);
-    if (L.pairs)
-        fast::k_llp2<CG><<<dim3(L.ctas * G.N), fast::kl::NTL, 0, ctx.stream>>>(G, guide, mu, gk, p, out, st, part,
-                                                                               L.nb, L.k, L.R);
-    else
-        fast::k_llp<CG><<<dim3(L.ctas * G.N), fast::kl::NTL, 0, ctx.stream>>>(G, guide, mu, gk, p, out, st, part,
-                                                                              L.nb, L.k, L.R);
+    const LlpPlan L = llp_plan<T>(ctx, G);
+    if (L.pairs) {
+        fast::k_llp2<CG, T><<<dim3(L.ctas * G.N), fast::kl::NTL, 0, ctx.stream>>>(G, guide, mu, gk, p, out, st, part,
+                                                                                  L.nb, L.k, L.R);
+    } else {
+        if constexpr (std::is_same<T, double>::value)
+            fast::k_llp<CG><<<dim3(L.ctas * G.N), fast::kl::NTL, 0, ctx.stream>>>(G, guide, mu, gk, p, out, st, part,
+                                                                                  L.nb, L.k, L.R);
+        else
+            param_error("pansharpen: the fp32 mode needs an even image width");
+    }
 }
 
 // rhs = B^T U x into r through K_D, then the CG initialisation (fast path; k_rhs otherwise)
-void launch_rhs_init(Context& ctx, const PsGeo& G, const double* taps, const double* x, CgBuffers& B, double* part,
+template <class T = double>
+void launch_rhs_init(Context& ctx, const PsGeo& G, const T* taps, const T* x, CgBuffersT<T>& B, double* part,
                      int max_iters, double cg_tol) {
     const int S = (G.N + G.cps - 1) / G.cps;
     const int nba = ceil_div(G.W, fast::a4::TA) * ceil_div(G.H, fast::a4::TA);
     const int groups = (G.cps + G.cpc - 1) / G.cpc;
-    const auto fd = dterm_select<false>(G);
+    const auto fd = dterm_select<false, T>(G);
     set_smem(fd.first, fd.second);
     fd.first<<<dim3(nba, S * groups), fast::NT, fd.second, ctx.stream>>>(G, taps, x, B.r, nullptr);
     const size_t P = static_cast<size_t>(G.H) * G.W;
     const int nbu = static_cast<int>((P + static_cast<size_t>(NTU) * UPT - 1) / (static_cast<size_t>(NTU) * UPT));
-    k_cg_init<<<dim3(nbu, G.N), NTU, 0, ctx.stream>>>(G, B.r, B.z, B.p + static_cast<size_t>(G.N) * P, B.st, part,
-                                                     nbu, max_iters, cg_tol);
+    k_cg_init<T><<<dim3(nbu, G.N), NTU, 0, ctx.stream>>>(G, B.r, B.z, B.p + static_cast<size_t>(G.N) * P, B.st, part,
+                                                        nbu, max_iters, cg_tol);
     ctx.count(2);
     check_launch();
 }
 
-template <bool CG>
-void launch_apply2(Context& ctx, const PsGeo& G, const double* taps, const double* guide, const double* mu,
-                   const double* gk, const double* p, const double* q, double* out, CgState* st, double* part,
+template <bool CG, class T = double>
+void launch_apply2(Context& ctx, const PsGeo& G, const T* taps, const T* guide, const T* mu,
+                   const T* gk, const T* p, const T* q, T* out, CgState* st, double* part,
                    bool pdl = false, cudaEvent_t between = nullptr) {
     const int S = (G.N + G.cps - 1) / G.cps;
     const int nba = ceil_div(G.W, fast::a4::TA) * ceil_div(G.H, fast::a4::TA);
     const int groups = (G.cps + G.cpc - 1) / G.cpc;
-    if (use_llp()) {
-        launch_llp<CG>(ctx, G, taps, guide, mu, gk, p, q, out, st, part, pdl, between);
+    if (use_llp() || !std::is_same<T, double>::value) {
+        launch_llp<CG, T>(ctx, G, taps, guide, mu, gk, p, q, out, st, part, pdl, between);
         return;
     }
-    if (between) FBMP_CUDA(cudaEventRecordWithFlags(between, ctx.stream, cudaEventRecordExternal));
-    const auto fs = apply3_select<CG>(G);
-    if (pdl)
-        launch_pdl(fs.first, dim3(nba, S * groups), dim3(fast::NT), fs.second, ctx.stream, G, taps, guide, mu, gk, p,
-                   q, out, st, part, nba);
-    else
-        fs.first<<<dim3(nba, S * groups), fast::NT, fs.second, ctx.stream>>>(G, taps, guide, mu, gk, p, q, out, st,
-                                                                              part, nba);
+    if constexpr (std::is_same<T, double>::value) {
+        if (between) FBMP_CUDA(cudaEventRecordWithFlags(between, ctx.stream, cudaEventRecordExternal));
+        const auto fs = apply3_select<CG>(G);
+        if (pdl)
+            launch_pdl(fs.first, dim3(nba, S * groups), dim3(fast::NT), fs.second, ctx.stream, G, taps, guide, mu, gk,
+                       p, q, out, st, part, nba);
+        else
+            fs.first<<<dim3(nba, S * groups), fast::NT, fs.second, ctx.stream>>>(G, taps, guide, mu, gk, p, q, out, st,
+                                                                                  part, nba);
+    }
 }
 
-template <bool CG>
+template <bool CG, class T = double>
 void prepare_apply2(const PsGeo& G) {
-    if (use_llp()) {
-        const auto fd = dterm_select<CG>(G);
+    if (use_llp() || !std::is_same<T, double>::value) {
+        const auto fd = dterm_select<CG, T>(G);
         set_smem(fd.first, fd.second);
         return;
     }
@@ -1302,11 +1644,18 @@ void cg_operator_apply(Context& ctx, const PsGeo& G, const double* d_taps, const
     check_launch();
 }
 
-void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* d_guide, const double* d_x,
-              CgBuffers& B, int max_iters, double cg_tol, std::vector<CgState>& host_state) {
+// The CG loop for storage type T: double, or float (fp32 mode: fast path only; the guide maps
+// are formed in fp64 from d_guide64 and stored as T, d_guide is the T copy K_L streams).
+template <class T>
+void cg_solve_t(Context& ctx, const PsGeo& G, const T* d_taps, const double* d_guide64, const T* d_guide, const T* d_x,
+                CgBuffersT<T>& B, int max_iters, double cg_tol, std::vector<CgState>& host_state) {
+    constexpr bool F64 = std::is_same<T, double>::value;
     const int N = G.N;
-    const QLaunch q2 = q2_select<true>(G);
+    const QLaunchT<T> q2 = q2_select<true, T>(G);
     const bool fastA = fast_ok(G);
+    if (!F64 && !(fastA && q2.fn))
+        param_error("pansharpen: the fp32 mode needs the specialised operator (radius 1, factor 2 or 4 with a "
+                    "supported kernel side, images >= 64 x 64)");
     const int nbq = q2.fn ? q2.nblk : ceil_div(G.w, TQ) * ceil_div(G.h, TQ);
     const int nba = fastA ? ceil_div(G.W, fast::a4::TA) * ceil_div(G.H, fast::a4::TA) : ceil_div(G.W, TA) * ceil_div(G.H, TA);
     const size_t P = static_cast<size_t>(G.H) * G.W;
@@ -1315,17 +1664,19 @@ void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* 
     check_smem(sq, "warmstart");
     if (!fastA) check_smem(sa, "warmstart");
     if (q2.fn) set_smem(q2.fn, q2.smem);
-    else set_smem(k_q<true>, sq);
-    if (fastA) prepare_apply2<true>(G);
-    else set_smem(k_apply<0, true>, sa);
-    set_smem(k_rhs<true>, sr);
-    double* wmu = nullptr;
-    double* wg = nullptr;
+    if constexpr (F64) {
+        if (!q2.fn) set_smem(k_q<true>, sq);
+        if (!fastA) set_smem(k_apply<0, true>, sa);
+        set_smem(k_rhs<true>, sr);
+    }
+    if (fastA) prepare_apply2<true, T>(G);
+    T* wmu = nullptr;
+    T* wg = nullptr;
     if (fastA) {
         const int S = (G.N + G.cps - 1) / G.cps;
-        wmu = ctx.scratch<double>("cg_wmu", P * S);
-        wg = ctx.scratch<double>("cg_wg", P * S);
-        guide_stats(ctx, G, d_guide, wmu, wg);
+        wmu = ctx.scratch<T>("cg_wmu", P * S);
+        wg = ctx.scratch<T>("cg_wg", P * S);
+        guide_stats_t<T>(ctx, G, d_guide64, wmu, wg);
     }
     double* part_init = B.part;
     double* part_q = part_init + static_cast<size_t>(N) * nba;
@@ -1334,9 +1685,9 @@ void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* 
     double* part_u = part_a + static_cast<size_t>(N) * nbA;
     // counters must start at zero
     FBMP_CUDA(cudaMemsetAsync(B.st, 0, sizeof(CgState) * N, ctx.stream));
-    if (fastA && use_llp()) {
-        launch_rhs_init(ctx, G, d_taps, d_x, B, part_init, max_iters, cg_tol);
-    } else {
+    if (fastA && (use_llp() || !F64)) {
+        launch_rhs_init<T>(ctx, G, d_taps, d_x, B, part_init, max_iters, cg_tol);
+    } else if constexpr (F64) {
         k_rhs<true><<<dim3(nba, N), NTA, sr, ctx.stream>>>(G, d_taps, d_x, B.r, B.z, B.p + static_cast<size_t>(N) * P,
                                                            B.st, part_init, nba, max_iters, cg_tol);
         ctx.count();
@@ -1361,7 +1712,8 @@ void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* 
     {
         const void* ptrs[] = {d_taps, d_guide, wmu, wg, B.r, B.p, B.q, B.Ap, B.st, B.z, part_q, part_a, part_u,
                               reinterpret_cast<const void*>(q2.fn)};
-        const long long dims[] = {nbq, nba, nbu, static_cast<long long>(sq), fastA ? 1 : 0, chunk};
+        const long long dims[] = {nbq, nba, nbu, static_cast<long long>(sq), fastA ? 1 : 0, chunk,
+                                  static_cast<long long>(sizeof(T))};
         key.append(reinterpret_cast<const char*>(&G), sizeof(G));
         key.append(reinterpret_cast<const char*>(ptrs), sizeof(ptrs));
         key.append(reinterpret_cast<const char*>(dims), sizeof(dims));
@@ -1377,8 +1729,8 @@ void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* 
     struct Grp {
         PsGeo G;
         int c0 = 0;
-        const double *taps, *guide, *mu, *g;
-        CgBuffers B;
+        const T *taps, *guide, *mu, *g;
+        CgBuffersT<T> B;
         double *pq, *pa, *pu;
     };
     std::vector<Grp> grp(ngrp);
@@ -1429,7 +1781,7 @@ void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* 
             }
         }
         // k_rhs zeroed p_old in the whole-launch layout; the group layout needs the same zeros
-        if (ngrp > 1) FBMP_CUDA(cudaMemsetAsync(B.p, 0, 2 * P * N * sizeof(double), ctx.stream));
+        if (ngrp > 1) FBMP_CUDA(cudaMemsetAsync(B.p, 0, 2 * P * N * sizeof(T), ctx.stream));
     }
     key.append(reinterpret_cast<const char*>(&ngrp), sizeof(ngrp));
     trace("cg: setup");
@@ -1462,25 +1814,25 @@ void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* 
                 else if (q2.fn)
                     q2.fn<<<dim3(nbq, Ng), q2.threads, sq, ctx.stream>>>(R.G, R.taps, R.B.r, R.B.p, R.B.q, R.B.st, R.pq,
                                                                          nbq);
-                else
+                else if constexpr (F64)
                     k_q<true><<<dim3(nbq, Ng), NTQ, sq, ctx.stream>>>(R.G, R.taps, R.B.r, R.B.p, R.B.q, R.B.st, R.pq,
                                                                        nbq);
                 if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * EV + 1], ctx.stream, cudaEventRecordExternal));
                 if (fastA) {
-                    launch_apply2<true>(ctx, R.G, R.taps, R.guide, R.mu, R.g, R.B.p, R.B.q, R.B.Ap, R.B.st, R.pa,
-                                        (pdl_mask & 2) != 0, prof ? pev[it * EV + 2] : nullptr);
-                } else {
+                    launch_apply2<true, T>(ctx, R.G, R.taps, R.guide, R.mu, R.g, R.B.p, R.B.q, R.B.Ap, R.B.st, R.pa,
+                                           (pdl_mask & 2) != 0, prof ? pev[it * EV + 2] : nullptr);
+                } else if constexpr (F64) {
                     if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * EV + 2], ctx.stream, cudaEventRecordExternal));
                     k_apply<0, true><<<dim3(nba, Ng), NTA, sa, ctx.stream>>>(R.G, R.taps, R.guide, R.B.p, R.B.q,
                                                                               R.B.Ap, R.B.st, R.pa, nba);
                 }
                 if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * EV + 3], ctx.stream, cudaEventRecordExternal));
                 if (pdl_mask & 4)
-                    launch_pdl(k_update, dim3(nbu, Ng), dim3(NTU), 0, ctx.stream, R.G, R.B.z, R.B.r, R.B.p, R.B.Ap,
+                    launch_pdl(k_update<T>, dim3(nbu, Ng), dim3(NTU), 0, ctx.stream, R.G, R.B.z, R.B.r, R.B.p, R.B.Ap,
                                R.B.st, R.pu, nbu);
                 else
-                    k_update<<<dim3(nbu, Ng), NTU, 0, ctx.stream>>>(R.G, R.B.z, R.B.r, R.B.p, R.B.Ap, R.B.st, R.pu,
-                                                                    nbu);
+                    k_update<T><<<dim3(nbu, Ng), NTU, 0, ctx.stream>>>(R.G, R.B.z, R.B.r, R.B.p, R.B.Ap, R.B.st, R.pu,
+                                                                       nbu);
                 if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * EV + 4], ctx.stream, cudaEventRecordExternal));
             }
         }
@@ -1514,7 +1866,7 @@ void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* 
     };
     auto launch = [&](int slot) {
         FBMP_CUDA(cudaGraphLaunch(exec, ctx.stream));
-        ctx.count((fastA && use_llp() ? 4 : 3) * chunk * ngrp);  // kernel nodes of one chunk graph
+        ctx.count((fastA && (use_llp() || !F64) ? 4 : 3) * chunk * ngrp);  // kernel nodes of one chunk graph
         FBMP_CUDA(cudaMemcpyAsync(pinned + slot * N, B.st, sizeof(CgState) * N, cudaMemcpyDeviceToHost, ctx.stream));
         FBMP_CUDA(cudaEventRecord(ev[slot], ctx.stream));
     };
@@ -1558,16 +1910,61 @@ void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* 
     trace("cg: teardown");
 }
 
+void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* d_guide, const double* d_x,
+              CgBuffers& B, int max_iters, double cg_tol, std::vector<CgState>& host_state) {
+    cg_solve_t<double>(ctx, G, d_taps, d_guide, d_guide, d_x, B, max_iters, cg_tol, host_state);
+}
+
+void cg_solve_f32(Context& ctx, const PsGeo& G, const float* d_taps, const double* d_guide64, const float* d_guide,
+                  const float* d_x, CgBuffersT<float>& B, int max_iters, double cg_tol,
+                  std::vector<CgState>& host_state) {
+    cg_solve_t<float>(ctx, G, d_taps, d_guide64, d_guide, d_x, B, max_iters, cg_tol, host_state);
+}
+
+namespace {
+template <class A, class B>
+__global__ void k_convert(const A* __restrict__ in, long long n, B* __restrict__ out) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        out[i] = static_cast<B>(in[i]);
+}
+}  // namespace
+void to_f32(Context& ctx, const double* d_in, long long n, float* d_out) {
+    k_convert<double, float><<<grid1d(ctx, n), 256, 0, ctx.stream>>>(d_in, n, d_out);
+    ctx.count();
+    check_launch();
+}
+void to_f64(Context& ctx, const float* d_in, long long n, double* d_out) {
+    k_convert<float, double><<<grid1d(ctx, n), 256, 0, ctx.stream>>>(d_in, n, d_out);
+    ctx.count();
+    check_launch();
+}
+
 void guided_filter(Context& ctx, int N, int H, int W, int rw, double eps, const double* d_in, int in_is_z0,
                    const double* d_guide, double* d_a, double* d_c, double* d_v, int cps) {
     const int nb = ceil_div(W, TA) * ceil_div(H, TA);
     const int hz = 2 * rw + (in_is_z0 ? 1 : 0), SZ = TA + 2 * hz, SN = TA + 4 * rw, SA = TA + 2 * rw;
     const size_t sm = (static_cast<size_t>((SZ * SZ + 1) & ~1) + (in_is_z0 ? ((SN * SN + 1) & ~1) : 0) +
                        ((SN * SN + 1) & ~1) + 2 * ((SA * SA + 1) & ~1)) * sizeof(double);
-    check_smem(sm, "guided filter");
-    set_smem(k_guided, sm);
-    k_guided<<<dim3(nb, N), NTA, sm, ctx.stream>>>(H, W, rw, eps, cps > 0 ? cps : N, d_in, in_is_z0, d_guide, d_a,
-                                                   d_c, d_v);
+    const int hz2 = 2 * rw + (in_is_z0 ? 1 : 0);
+    if (rw == 1 && H >= GTH + hz2 && W >= GTW + hz2) {  // wrap1's range
+        const int cpsv = cps > 0 ? cps : N;
+        const dim3 grid(ceil_div(W, GTW) * ceil_div(H, GTH), N);
+        if (in_is_z0) {
+            set_smem(k_guided2<1, true>, GfLay<1, true>::bytes);
+            k_guided2<1, true><<<grid, GNT, GfLay<1, true>::bytes, ctx.stream>>>(H, W, eps, cpsv, d_in, d_guide, d_a,
+                                                                                 d_c, d_v);
+        } else {
+            set_smem(k_guided2<1, false>, GfLay<1, false>::bytes);
+            k_guided2<1, false><<<grid, GNT, GfLay<1, false>::bytes, ctx.stream>>>(H, W, eps, cpsv, d_in, d_guide,
+                                                                                   d_a, d_c, d_v);
+        }
+    } else {
+        check_smem(sm, "guided filter");
+        set_smem(k_guided, sm);
+        k_guided<<<dim3(nb, N), NTA, sm, ctx.stream>>>(H, W, rw, eps, cps > 0 ? cps : N, d_in, in_is_z0, d_guide,
+                                                       d_a, d_c, d_v);
+    }
     ctx.count();
     check_launch();
 }
@@ -1592,12 +1989,14 @@ void solve_channel_fft(Context& ctx, const PsGeo& G, const double* d_taps, const
     FBMP_CUFFT(cufftExecD2Z(ctx.plan(0, h, w, N), const_cast<double*>(d_x), reinterpret_cast<cufftDoubleComplex*>(xh)));
     double* cosHW = ctx.scratch<double>("fft_cos", static_cast<size_t>(H) + W);
     k_cos_tables<<<ceil_div(H + W, 256), 256, 0, ctx.stream>>>(H, W, cosHW);
-    const int nthreads = 128;
-    const dim3 grid(ceil_div(static_cast<long long>(h) * w, nthreads), N);
-    if (G.c <= 4)
-        k_alias<4><<<grid, nthreads, 0, ctx.stream>>>(H, W, h, w, G.c, G.cps, G.lambda, bh, xh, vh, zh, cosHW, d_flag);
-    else
+    if (G.c <= 4) {
+        const dim3 grid(ceil_div(static_cast<long long>(h) * w * AG, AG_NT), S);
+        k_alias16<<<grid, AG_NT, 0, ctx.stream>>>(H, W, h, w, G.c, N, G.cps, G.lambda, bh, xh, vh, zh, cosHW, d_flag);
+    } else {
+        const int nthreads = 128;
+        const dim3 grid(ceil_div(static_cast<long long>(h) * w, nthreads), N);
         k_alias<8><<<grid, nthreads, 0, ctx.stream>>>(H, W, h, w, G.c, G.cps, G.lambda, bh, xh, vh, zh, cosHW, d_flag);
+    }
     ctx.count(2);
     check_launch();
     FBMP_CUFFT(cufftExecZ2D(ctx.plan(1, H, W, N), reinterpret_cast<cufftDoubleComplex*>(zh), zr));

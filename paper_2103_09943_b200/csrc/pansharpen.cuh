@@ -41,21 +41,31 @@ struct PsGeo {
 PsGeo make_geo(int N, int h, int w, int c, int n, int rw, double lambda, double eps, int cps = 0);
 
 // Workspace of one batched CG solve (all device pointers, channel-major).
-struct CgBuffers {
-    double* z;      // N*P  (output: warm start)
-    double* r;      // N*P
-    double* p;      // 2*N*P (parity double buffer)
-    double* Ap;     // N*P
-    double* q;      // N*p  (D B p at the LR points)
+template <class T>
+struct CgBuffersT {  // T = double (reference precision) or float (fp32 mode)
+    T* z;           // N*P  (output: warm start)
+    T* r;           // N*P
+    T* p;           // 2*N*P (parity double buffer)
+    T* Ap;          // N*P
+    T* q;           // N*p  (D B p at the LR points)
     double* part;   // partial sums, 4 * N * max_blocks
     CgState* st;    // N
     int max_blocks;
 };
+using CgBuffers = CgBuffersT<double>;
 
 // Enqueue the whole CG warm start for N channels sharing `guide` (= L(pan_n)) and taps.
 // x: N*h*w (already scaled). Returns after the loop finished (host polls device flags).
 void cg_solve(Context& ctx, const PsGeo& G, const double* d_taps, const double* d_guide, const double* d_x,
               CgBuffers& B, int max_iters, double cg_tol, std::vector<CgState>& host_state);
+// fp32 mode: the same loop with fp32 vectors (taps, guide, x converted by the caller; the guide
+// maps are formed from the fp64 guide), fp64 reductions and CG scalars. Fast path only.
+void cg_solve_f32(Context& ctx, const PsGeo& G, const float* d_taps, const double* d_guide64, const float* d_guide,
+                  const float* d_x, CgBuffersT<float>& B, int max_iters, double cg_tol,
+                  std::vector<CgState>& host_state);
+// elementwise fp64 -> fp32 / fp32 -> fp64 copies (fp32 mode staging)
+void to_f32(Context& ctx, const double* d_in, long long n, float* d_out);
+void to_f64(Context& ctx, const float* d_in, long long n, double* d_out);
 
 // Row-strip decomposition of the CG (csrc/pansharpen.cu, "Row-strip decomposition").
 struct StripCg {

@@ -166,6 +166,15 @@ class Context:
     def set_profile(self, on: bool) -> None:
         _lib.fbmp_gpu_ctx_set_profile(self.h, int(on))
 
+    def set_precision(self, bits: int) -> None:
+        """64 (default, reference fp64) or 32 (fp32 mode of the HRMS CG: fp32 vectors and stencils,
+        fp64 reductions and CG scalars; gate <= 1e-3 rel. L2 and <= 0.05 dB PSNR vs fp64)."""
+        _check(_lib.fbmp_gpu_ctx_set_precision(self.h, int(bits)))
+
+    @property
+    def precision(self) -> int:
+        return int(_lib.fbmp_gpu_ctx_precision(self.h))
+
     def set_comm(self, uid: bytes, nranks: int, rank: int) -> None:
         """Attach an NCCL communicator (row-strip solves); every rank calls this with the same id."""
         buf = (C.c_ubyte * 128).from_buffer_copy(bytes(uid).ljust(128, b"\0")[:128])
@@ -498,6 +507,31 @@ def estimate_kernel_plane(pan, observation, factor, params: KernelEstParams | No
     return k, it.value
 
 
+def estimate_kernel_tv_plane(pan, observation, factor, params: KernelEstParams | None = None, want_state=False,
+                             hook_t=-1, ctx=None):
+    """estimate_kernel_plane with KernelPrior::tv (kernel_estimator.cpp:445-452, run_tgv_or_tv(false))
+    -> (kernel, iterations[, state]); the TV ablation estimator of the paper's Table II."""
+    pan, obs = _f(pan), _f(observation)
+    prm = params or KernelEstParams()
+    n = prm.n
+    if pan.shape[0] != factor * obs.shape[0] or pan.shape[1] != factor * obs.shape[1]:
+        raise DimensionError("build_observation: PAN dimensions must be factor times the observation")
+    k = np.empty((n, n))
+    it = C.c_int(0)
+    st = np.empty((17, n, n)) if (want_state or hook_t >= 0) else None
+    cp = prm.c()
+    _check(_lib.fbmp_gpu_estimate_kernel_tv_plane(_ctx(ctx), _p(pan), pan.shape[0], pan.shape[1], _p(obs), factor,
+                                                  C.byref(cp), _p(k), C.byref(it), _p(st), int(hook_t)))
+    if st is not None:
+        return k, it.value, dict(zip(STATE_FIELDS, st))
+    return k, it.value
+
+
+def estimate_kernel_tv(lrms_subset, pan, omega, factor, params: KernelEstParams | None = None, ctx=None):
+    """kernel_estimator.hpp:120-123 -> (kernel, iterations)."""
+    return estimate_kernel_tv_plane(pan, combine_bands(lrms_subset, omega, ctx), factor, params, ctx=ctx)
+
+
 def estimate_kernel_l2_plane(pan, observation, factor, params: KernelEstParams | None = None, ctx=None):
     """estimate_kernel_plane with KernelPrior::l2 (kernel_estimator.cpp:389-428, :438-455): the l2 +
     simplex ablation estimator of the paper's Table II -> (kernel, iterations)."""
@@ -687,7 +721,9 @@ EXPORTED_SYMBOLS = (
     "fbmp_gpu_default_ps_params", "fbmp_gpu_default_ke_params", "fbmp_gpu_default_sw_params",
     "fbmp_gpu_ctx_create", "fbmp_gpu_ctx_destroy", "fbmp_gpu_last_error", "fbmp_gpu_ctx_stats", "fbmp_gpu_ctx_cg_iters",
     "fbmp_gpu_ctx_stream", "fbmp_gpu_ctx_launches", "fbmp_gpu_ctx_set_profile", "fbmp_gpu_ctx_kernel_profile",
-    "fbmp_gpu_metrics", "fbmp_gpu_estimate_kernel_l2_plane",
+    "fbmp_gpu_ctx_set_precision", "fbmp_gpu_ctx_precision",
+    "fbmp_gpu_metrics", "fbmp_gpu_estimate_kernel_l2_plane", "fbmp_gpu_estimate_kernel_tv_plane",
+    "fbmp_gpu_estimate_kernel_tv",
     "fbmp_gpu_blind_batch_dev", "fbmp_gpu_blind_strips_dev", "fbmp_gpu_nccl_unique_id", "fbmp_gpu_ctx_set_comm",
     "fbmp_gpu_pansharpen", "fbmp_gpu_estimate_kernel_tgv",
     "fbmp_gpu_estimate_kernel_plane", "fbmp_gpu_solve_weights", "fbmp_gpu_combine_bands", "fbmp_gpu_blind",

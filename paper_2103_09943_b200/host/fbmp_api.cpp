@@ -474,9 +474,14 @@ Kernel2D estimate_kernel_plane(KernelPrior prior, const Plane& pan, const Plane&
                                                 &kp, taps.data(), nullptr));
         return Kernel2D(params.n, std::move(taps));
     }
-    if (prior != KernelPrior::tgv2)
-        throw ParamError("estimate_kernel_plane: the GPU path implements the TGV^2 and l2 priors only");
+    const bool tv = prior == KernelPrior::tv;  // run_tgv_or_tv(false, ...) (kernel_estimator.cpp:450-451)
     const fbmp_ke_params kp = to_c(params);
+    auto plane_call = [&](double* taps, int* it, double* st, int hook_t) {
+        return tv ? fbmp_gpu_estimate_kernel_tv_plane(ctx(), pan.data(), pan.height(), pan.width(), observation.data(),
+                                                      factor, &kp, taps, it, st, hook_t)
+                  : fbmp_gpu_estimate_kernel_plane(ctx(), pan.data(), pan.height(), pan.width(), observation.data(),
+                                                   factor, &kp, taps, it, st, hook_t);
+    };
     const int n = params.n;
     const std::size_t m = static_cast<std::size_t>(n) * n;
     std::vector<double> taps(m), state(17 * m);
@@ -485,17 +490,14 @@ Kernel2D estimate_kernel_plane(KernelPrior prior, const Plane& pan, const Plane&
         // hook emulation: the device loop stops at the hook point of iteration t and returns
         // the state; the hook sees the same state the reference passes (kernel_estimator.cpp:344)
         int t_final = 0;
-        check(fbmp_gpu_estimate_kernel_plane(ctx(), pan.data(), pan.height(), pan.width(), observation.data(), factor,
-                                             &kp, taps.data(), &t_final, nullptr, -1));
+        check(plane_call(taps.data(), &t_final, nullptr, -1));
         for (int t = 0; t < t_final; ++t) {
             int tt = 0;
-            check(fbmp_gpu_estimate_kernel_plane(ctx(), pan.data(), pan.height(), pan.width(), observation.data(),
-                                                 factor, &kp, taps.data(), &tt, state.data(), t));
+            check(plane_call(taps.data(), &tt, state.data(), t));
             before_up_solve(unpack_state(state, n, t), t);
         }
     }
-    check(fbmp_gpu_estimate_kernel_plane(ctx(), pan.data(), pan.height(), pan.width(), observation.data(), factor, &kp,
-                                         taps.data(), &iters, final_state ? state.data() : nullptr, -1));
+    check(plane_call(taps.data(), &iters, final_state ? state.data() : nullptr, -1));
     if (final_state) *final_state = unpack_state(state, n, iters);
     return Kernel2D(n, std::move(taps));
 }
@@ -507,8 +509,9 @@ Kernel2D estimate_kernel_tgv(const MultiBandImage& lrms_subset, const Plane& pan
                                  final_state, before_up_solve);
 }
 
-Kernel2D estimate_kernel_tv(const MultiBandImage&, const Plane&, const SpectralWeights&, int, const KernelEstParams&) {
-    throw ParamError("estimate_kernel_tv: TV kernel prior is an ablation outside the GPU path");
+Kernel2D estimate_kernel_tv(const MultiBandImage& lrms_subset, const Plane& pan, const SpectralWeights& omega, int factor,
+                            const KernelEstParams& params) {  // kernel_estimator.cpp:466-471
+    return estimate_kernel_plane(KernelPrior::tv, pan, combine_bands(lrms_subset, omega), factor, params);
 }
 
 Kernel2D estimate_kernel_l2(const MultiBandImage& lrms_subset, const Plane& pan, const SpectralWeights& omega, int factor,

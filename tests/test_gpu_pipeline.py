@@ -418,3 +418,35 @@ def test_kernel_l2_errors(gpu):
     with pytest.raises(gpu.DimensionError):
         gpu.estimate_kernel_l2_plane(rng.uniform(0, 1, (64, 60)), rng.uniform(0, 1, (16, 16)), 4,
                                      gpu.KernelEstParams(n=7))
+
+
+@pytest.mark.parametrize("H,n,th", [(128, 7, 1e-5), (256, 15, 1e-5), (128, 9, 1e-12)])
+def test_kernel_tv_matches_oracle(gpu, orc, H, n, th):
+    """The TV ablation estimator (KernelPrior::tv, kernel_estimator.cpp:291-387 with with_p = false):
+    the device ADMM with p = 0 and the scalar-symbol u-step against the oracle's TV branch. Default th:
+    identical ADMM iteration counts and the fp64 gate; converged (th 1e-12): 1e-9."""
+    sc = synth.make_scene("C1", hr=H)
+    obs = sc.lrms.mean(axis=0)
+    prm = gpu.KernelEstParams(n=n, th=th)
+    kg, itg, sg = gpu.estimate_kernel_tv_plane(sc.pan, obs, 4, prm, want_state=True)
+    ko, ito, so = orc.estimate_kernel_plane_tv(sc.pan, obs, 4, n, th=th, want_state=True)
+    assert abs(kg.sum() - 1.0) < 1e-12 and kg.min() >= 0.0
+    for f in ("p1", "p2", "y0", "y3", "L2_0", "L2_3"):
+        assert not sg[f].any()
+    if th < 1e-9:
+        assert rel(kg, ko) < 1e-9
+    else:
+        assert itg == ito
+        assert rel(kg, ko) < TOL
+        assert rel(sg["u"], so["u"]) < TOL
+
+
+def test_kernel_tv_degenerate_and_hook(gpu, orc):
+    with pytest.raises(gpu.NumericalError):  # constant PAN (kernel_estimator.cpp:269-276, test :303)
+        gpu.estimate_kernel_tv_plane(np.full((64, 64), 0.5), np.full((16, 16), 0.5), 4, gpu.KernelEstParams(n=7))
+    sc = synth.make_scene("C1", hr=64)
+    obs = sc.lrms.mean(axis=0)
+    _, _, st = gpu.estimate_kernel_tv_plane(sc.pan, obs, 4, gpu.KernelEstParams(n=5), hook_t=3)
+    _, _, full = gpu.estimate_kernel_tv_plane(sc.pan, obs, 4, gpu.KernelEstParams(n=5, t_max=3), want_state=True)
+    # the hook state of iteration 3 holds the u of 3 completed iterations
+    assert rel(st["u"], full["u"]) < 1e-12

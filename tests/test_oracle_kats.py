@@ -502,6 +502,44 @@ def test_solve_up_along_admm(orc):  # :319-342 (hook point = state before the {u
         assert np.linalg.norm(fast - slow) <= 1e-8 * (np.linalg.norm(slow) + 1)
 
 
+def texture(h, w, seed):
+    """tests/test_util.cpp:62-90 in spirit: low-frequency waves plus random rectangles (numpy rng)."""
+    rng = np.random.default_rng(seed)
+    r, c = np.mgrid[0:h, 0:w]
+    f1, f2, ph1, ph2 = 1 + 2 * rng.uniform(), 1 + 2 * rng.uniform(), 2 * np.pi * rng.uniform(), 2 * np.pi * rng.uniform()
+    img = 0.5 + 0.25 * np.sin(2 * np.pi * f1 * r / h + ph1) + 0.25 * np.cos(2 * np.pi * f2 * c / w + ph2)
+    for _ in range(6 + int(rng.uniform() * 6)):
+        y0, x0 = rng.integers(0, h - 4), rng.integers(0, w - 4)
+        img[y0:y0 + rng.integers(3, h // 3), x0:x0 + rng.integers(3, w // 3)] += rng.uniform(-0.3, 0.3)
+    return img
+
+
+def test_tv_degenerate_pan(orc):  # :297-305 (estimate_kernel_tv)
+    with pytest.raises(orc.OracleError, match="constant PAN") as e:
+        orc.estimate_kernel_plane_tv(np.ones((16, 16)), np.full((8, 8), 0.5), 2, 3)
+    assert e.value.code == 3
+
+
+def test_tv_recovers_noiseless_system(orc):  # :386-397 (KernelPrior::tv, alpha1 -> 0)
+    pan = texture(32, 32, 9)
+    rng = np.random.default_rng(9)
+    truth = simplex_kernel(rng, 3)
+    obs = (orc.observation_matrix(pan, 2, 3) @ truth.ravel()).reshape(16, 16)
+    est, it = orc.estimate_kernel_plane_tv(pan, obs, 2, 3, alpha1=1e-6, t_max=4000, th=1e-9)
+    assert 100 * np.linalg.norm(est - truth) / np.linalg.norm(truth) < 1.0
+    assert abs(est.sum() - 1.0) < 1e-9 and est.min() >= 0.0
+
+
+def test_tv_state_has_no_p(orc):  # :291-387 with with_p = false: p, y and L2 stay zero
+    sc = synth.make_scene("C1", hr=32)
+    obs = orc.combine_bands(sc.lrms, np.full(4, 0.25))
+    k, it, st = orc.estimate_kernel_plane_tv(sc.pan, obs, 4, 5, want_state=True)
+    for f in ("p1", "p2", "y0", "y1", "y2", "y3", "L2_0", "L2_1", "L2_2", "L2_3"):
+        assert not st[f].any()
+    kt, _ = orc.estimate_kernel_plane(sc.pan, obs, 4, 5)
+    assert it > 1 and rel(k, kt) > 1e-6  # a different prior, a different kernel
+
+
 def test_primal_residuals_at_convergence(orc):  # :357-384
     sc = synth.make_scene("C1", hr=32)
     obs = orc.combine_bands(sc.lrms, np.full(4, 0.25))

@@ -248,6 +248,14 @@ int fbmp_gpu_solve_up(fbmp_gpu_ctx* ctx, const double* fields, int n, const fbmp
 /* E^T E (n^2 x n^2) and E^T f of ObservationSystem (kernel_estimator.cpp:57-71), unscaled. */
 int fbmp_gpu_gram(fbmp_gpu_ctx* ctx, const double* pan, int H, int W, const double* obs, int factor, int n,
                   double* EtE, double* Etf);
+/* ObservationSystem::solve_z (kernel_estimator.cpp:79-83) on the device for a Gram matrix from
+ * fbmp_gpu_gram: z = (E^T E + mu3 I)^-1 (E^T f + mu3 anchor) (Cholesky, explicit inverse,
+ * mat-vec). EtE: n2*n2, Etf / anchor / z_out: n2 (n2 = n*n). FBMP_NUMERICAL if not SPD. */
+int fbmp_gpu_solve_z(fbmp_gpu_ctx* ctx, const double* EtE, const double* Etf, int n, double mu3,
+                     const double* anchor, double* z_out);
+/* ObservationSystem::data_objective (kernel_estimator.cpp:85-87): 0.5 (u'EtE u - 2 u'Etf + ff). */
+int fbmp_gpu_data_objective(fbmp_gpu_ctx* ctx, const double* EtE, const double* Etf, int n, double ff,
+                            const double* u, double* value);
 
 #ifdef __cplusplus
 }

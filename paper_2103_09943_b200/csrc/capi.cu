@@ -290,12 +290,32 @@ void pansharpen_strips_device(Context& ctx, const double* d_lrms, int N, int h, 
                       ": warmstart: conjugate gradients hit a non-positive curvature direction");
     // whole z0 planes: owned rows of every strip, in strip order
     double* zf = ctx.scratch<double>("st_zfull", P * N);
+    bool any_cap = false;
+    for (int i = 0; i < N; ++i) any_cap = any_cap || hs[i].done == 3;  // identical on every rank
     if (dist) {
+        // channel ch is post-processed on its owner rank ch mod G: the owned rows of z0 go to the
+        // owner only (each rank receives N / G planes instead of N). The error path of a CG that
+        // hit its cap needs z0 everywhere (the message's residual): then the planes are all-gathered.
         auto cm = static_cast<ncclComm_t>(ctx.nccl);
+        const size_t rows = static_cast<size_t>(hloc) * W;
+        const double* own = strips[0].B.z + static_cast<size_t>(halo) * W;
+        for (int ch = ctx.rank; ch < N && !any_cap; ch += G)  // this rank's own rows of its channels
+            FBMP_CUDA(cudaMemcpyAsync(zf + ch * P + static_cast<size_t>(ctx.rank) * rows, own + ch * Pp,
+                                      rows * sizeof(double), cudaMemcpyDeviceToDevice, ctx.stream));
         FBMP_NCCL(ncclGroupStart());
-        for (int ch = 0; ch < N; ++ch)
-            FBMP_NCCL(ncclAllGather(strips[0].B.z + ch * Pp + static_cast<size_t>(halo) * W, zf + ch * P,
-                                    static_cast<size_t>(hloc) * W, ncclDouble, cm, ctx.stream));
+        for (int ch = 0; ch < N; ++ch) {
+            if (any_cap) {
+                FBMP_NCCL(ncclAllGather(own + ch * Pp, zf + ch * P, rows, ncclDouble, cm, ctx.stream));
+                continue;
+            }
+            const int owner = ch % G;
+            if (ctx.rank == owner) {
+                for (int r = 0; r < G; ++r)
+                    if (r != owner) FBMP_NCCL(ncclRecv(zf + ch * P + r * rows, rows, ncclDouble, r, cm, ctx.stream));
+            } else {
+                FBMP_NCCL(ncclSend(own + ch * Pp, rows, ncclDouble, owner, cm, ctx.stream));
+            }
+        }
         FBMP_NCCL(ncclGroupEnd());
     } else {
         for (int k = 0; k < count; ++k)
@@ -393,10 +413,13 @@ void blind_device(Context& ctx, const double* d_lrms, int S, int N, int h, int w
         if (hst[s] == 2) num_error("solve_weights: stationarity residual too large (ill-conditioned system)");
     }
     cudaEventRecord(e1, ctx.stream);
-    estimate_kernel_device(ctx, d_pan, obs, S, H, W, c, ke, d_k, admm_iters, nullptr, -1);
+    // C5 row strips: the Gram tiles of the kernel fit are split over the ranks (chunk sums
+    // all-gathered, bit-identical to one GPU); the rest of the fit is replicated
+    const bool strip_path = strips > 0 || ctx.nccl;
+    estimate_kernel_device(ctx, d_pan, obs, S, H, W, c, ke, d_k, admm_iters, nullptr, -1, false, strip_path);
     cudaEventRecord(e2, ctx.stream);
     trace("blind: weights + kernel fit");
-    if (strips > 0 || ctx.nccl) {
+    if (strip_path) {
         if (S != 1 || nch >= 0) param_error("strip solve: one scene, all bands");
         pansharpen_strips_device(ctx, d_lrms, N, h, w, d_pan, d_k, ke.n, c, ps, d_out, cg_iters, strips);
     } else {
@@ -1096,6 +1119,37 @@ int fbmp_gpu_gram(fbmp_gpu_ctx* ctx, const double* pan, int H, int W, const doub
         gram_device(C, d_p, d_f, H, W, factor, n, d_G, d_e);
         download(C, EtE, d_G, n2 * n2);
         download(C, Etf, d_e, n2);
+    });
+}
+
+int fbmp_gpu_solve_z(fbmp_gpu_ctx* ctx, const double* EtE, const double* Etf, int n, double mu3,
+                     const double* anchor, double* z_out) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        if (n < 1) param_error("build_observation: kernel side must be odd");
+        const size_t n2 = static_cast<size_t>(n) * n;
+        double* d_G = upload(C, "sz_EtE", EtE, n2 * n2);
+        double* d_e = upload(C, "sz_Etf", Etf, n2);
+        double* d_a = upload(C, "sz_anchor", anchor, n2);
+        double* d_z = C.scratch<double>("sz_z", n2);
+        solve_z_device(C, d_G, d_e, static_cast<int>(n2), mu3, d_a, d_z);
+        download(C, z_out, d_z, n2);
+    });
+}
+
+int fbmp_gpu_data_objective(fbmp_gpu_ctx* ctx, const double* EtE, const double* Etf, int n, double ff,
+                            const double* u, double* value) {
+    return guarded([&] {
+        Context& C = ctx->impl;
+        DeviceGuard dg(C.device);
+        const size_t n2 = static_cast<size_t>(n) * n;
+        double* d_G = upload(C, "sz_EtE", EtE, n2 * n2);
+        double* d_e = upload(C, "sz_Etf", Etf, n2);
+        double* d_u = upload(C, "sz_u", u, n2);
+        double* d_v = C.scratch<double>("sz_v", 1);
+        data_objective_device(C, d_G, d_e, d_u, static_cast<int>(n2), ff, d_v);
+        download(C, value, d_v, 1);
     });
 }
 

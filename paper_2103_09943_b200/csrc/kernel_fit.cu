@@ -15,6 +15,7 @@
 #include <cooperative_groups.h>
 
 #include "kernel_fit.cuh"
+#include <nccl.h>
 
 #include <cstdlib>
 
@@ -249,9 +250,9 @@ constexpr int TG = 16;  // LR tile side of the Gram kernels
 // with P = pan * scale (the reference's pan_n, kernel_estimator.cpp:443-444).
 __global__ void __launch_bounds__(NT) k_gram_T(const double* __restrict__ pan, const double* __restrict__ scale, int H,
                                                int W, int h, int w, int c, int n, double* __restrict__ part,
-                                               int ntiles) {
+                                               int ntiles, int t_lo) {
     extern __shared__ double reg[];
-    const int s = blockIdx.z, phase = blockIdx.y, tile = blockIdx.x;
+    const int s = blockIdx.z, phase = blockIdx.y, tile = blockIdx.x + t_lo;
     const int rho_r = phase / c, rho_c = phase - rho_r * c;
     const int ntx = (w + TG - 1) / TG;
     const int i0 = (tile / ntx) * TG, j0 = (tile % ntx) * TG;
@@ -302,10 +303,12 @@ constexpr int NTG = 192;  // >= (2n-1) * ceil((2n-1) / GK) for n <= 21
 template <int CF>
 __global__ void __launch_bounds__(NTG) k_gram_T2(const double* __restrict__ pan, const double* __restrict__ scale,
                                                  int H, int W, int h, int w, int n, double* __restrict__ part,
-                                                 int ntiles) {
+                                                 int ntiles, int t_lo) {
     constexpr int c = CF;
-    extern __shared__ double reg[];
-    const int s = blockIdx.z, phase = blockIdx.y, tile = blockIdx.x;
+    extern __shared__ double smg[];
+    double* reg = smg + GK;  // GK doubles of slack below the region: the full-tile path loads the
+                             // window's padding columns unconditionally (their sums are discarded)
+    const int s = blockIdx.z, phase = blockIdx.y, tile = blockIdx.x + t_lo;
     const int rho_r = phase / c, rho_c = phase - rho_r * c;
     const int ntx = (w + TG - 1) / TG;
     const int i0 = (tile / ntx) * TG, j0 = (tile % ntx) * TG;
@@ -327,6 +330,21 @@ __global__ void __launch_bounds__(NTG) k_gram_T2(const double* __restrict__ pan,
     double acc[GK];
 #pragma unroll
     for (int k = 0; k < GK; ++k) acc[k] = 0.0;
+    if (nj == TG) {
+        // full tile row: the point loop is unrolled, so the c-column window shift is register
+        // renaming (each region value is loaded once per row and feeds up to GK / c points);
+        // every accumulator keeps the ascending point order of the generic loop below
+        for (int ii = 0; ii < ni; ++ii) {
+            const double* crow = reg + (c * ii + n - 1) * SR + n - 1;
+            const double* wrow = reg + (c * ii + n - 1 - dr) * SR + n - 1 - dc0;
+#pragma unroll
+            for (int jj = 0; jj < TG; ++jj) {
+                const double cv = crow[c * jj];
+#pragma unroll
+                for (int k = 0; k < GK; ++k) acc[k] = fma(cv, wrow[c * jj - k], acc[k]);
+            }
+        }
+    } else {
     for (int ii = 0; ii < ni; ++ii) {
         const double* crow = reg + (c * ii + n - 1) * SR + n - 1;          // centre values
         const double* wrow = reg + (c * ii + n - 1 - dr) * SR + n - 1 - dc0;  // window row
@@ -345,6 +363,7 @@ __global__ void __launch_bounds__(NTG) k_gram_T2(const double* __restrict__ pan,
             for (int k = GK - 1; k >= 0; --k) win[k] = (k >= c) ? win[k - c] : (more && k < kval ? nxt[-k] : 0.0);
         }
     }
+    }
 #pragma unroll
     for (int k = 0; k < GK; ++k) {
         const int dc = dc0 + k;
@@ -355,9 +374,9 @@ __global__ void __launch_bounds__(NTG) k_gram_T2(const double* __restrict__ pan,
 // E^T f partials: sum_{(i,j) in tile} P(c i - tr + C, c j - tc + C) * f(i, j), f = obs * scale
 __global__ void __launch_bounds__(NT) k_gram_etf(const double* __restrict__ pan, const double* __restrict__ obs,
                                                  const double* __restrict__ scale, int H, int W, int h, int w, int c,
-                                                 int n, double* __restrict__ part, int ntiles) {
+                                                 int n, double* __restrict__ part, int ntiles, int t_lo) {
     extern __shared__ double reg[];
-    const int s = blockIdx.z, tile = blockIdx.x;
+    const int s = blockIdx.z, tile = blockIdx.x + t_lo;
     const int ntx = (w + TG - 1) / TG;
     const int i0 = (tile / ntx) * TG, j0 = (tile % ntx) * TG;
     const int C = (n - 1) / 2, n2 = n * n;
@@ -387,26 +406,50 @@ __global__ void __launch_bounds__(NT) k_gram_etf(const double* __restrict__ pan,
     }
 }
 
-// fixed-order reduction over tiles: out[s][v] = sum_t part[s][t][v]
-__global__ void k_reduce_tiles(const double* __restrict__ part, int S, int ntiles, int nv, double* __restrict__ out) {
+// Tile partials are reduced in GRAM_CHUNKS fixed, contiguous tile chunks (sequential sums inside a
+// chunk, then over the chunks in order). The chunking does not depend on the number of ranks, so a
+// C5 fit split over G | GRAM_CHUNKS ranks (each computes whole chunks, the chunk sums are
+// all-gathered) is bit-identical to the single-GPU fit.
+constexpr int GRAM_CHUNKS = 8;
+__host__ __device__ inline int chunk_tile(int k, int ntiles) {
+    return static_cast<int>(static_cast<long long>(k) * ntiles / GRAM_CHUNKS);
+}
+// cp[s][k][v] = sum_{t in chunk k} part[s][t][v] for k in [k0, k1)
+__global__ void k_reduce_chunks(const double* __restrict__ part, int S, int ntiles, int nv, int k0, int k1,
+                                double* __restrict__ cp) {
+    const int nk = k1 - k0;
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+         e < static_cast<long long>(S) * nk * nv; e += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long s = e / (static_cast<long long>(nk) * nv);
+        const long long rem = e - s * nk * nv;
+        const int k = k0 + static_cast<int>(rem / nv), v = static_cast<int>(rem - (rem / nv) * nv);
+        const double* pp = part + s * ntiles * static_cast<long long>(nv) + v;
+        const int t1 = chunk_tile(k + 1, ntiles);
+        double acc = 0.0;
+        int t = chunk_tile(k, ntiles);
+        for (; t + 16 <= t1; t += 16) {  // tile order kept; loads issued 16 ahead of the additions
+            double x[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) x[q] = __ldg(pp + static_cast<long long>(t + q) * nv);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) acc += x[q];
+        }
+        for (; t < t1; ++t) acc += __ldg(pp + static_cast<long long>(t) * nv);
+        cp[(s * GRAM_CHUNKS + k) * nv + v] = acc;
+    }
+}
+// out[s][v] = sum_k cp[s][k][v]
+__global__ void k_sum_chunks(const double* __restrict__ cp, int S, int nv, double* __restrict__ out) {
     for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < static_cast<long long>(S) * nv;
          e += static_cast<long long>(gridDim.x) * blockDim.x) {
         const long long s = e / nv, v = e - s * nv;
-        const double* pp = part + s * ntiles * nv + v;
         double acc = 0.0;
-        int t = 0;
-        // tile order kept (sequential sum); loads issued 16 ahead of the additions
-        for (; t + 16 <= ntiles; t += 16) {
-            double x[16];
 #pragma unroll
-            for (int k = 0; k < 16; ++k) x[k] = __ldg(pp + static_cast<long long>(t + k) * nv);
-#pragma unroll
-            for (int k = 0; k < 16; ++k) acc += x[k];
-        }
-        for (; t < ntiles; ++t) acc += __ldg(pp + static_cast<long long>(t) * nv);
+        for (int k = 0; k < GRAM_CHUNKS; ++k) acc += cp[(s * GRAM_CHUNKS + k) * nv + v];
         out[e] = acc;
     }
 }
+
 
 // G[(tr,tc),(tr',tc')] = T[tr mod c][tc mod c][tr'-tr][tc'-tc] (+ mu3 on the diagonal)
 __global__ void k_gram_expand(const double* __restrict__ T, int S, int c, int n, double mu3, double* __restrict__ M) {
@@ -658,13 +701,19 @@ struct AdmmArgs {
 constexpr int NTADMM = 512;
 #ifdef FBMP_ADMM_PROF  // phase timers of k_admm (thread 0, clock64), A/B diagnostics only
 __device__ long long g_admm_prof[16];
-#define APROF_T0 long long _ap_t = clock64(), _ap_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#define APROF_T0 long long _ap_t = clock64(), _ap_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}; \
+    if (threadIdx.x == 0 && blockIdx.x == 0) for (int _k = 8; _k < 12; ++_k) g_admm_prof[_k] = 0;
 #define APROF(k) if (threadIdx.x == 0 && blockIdx.x == 0) { const long long _n = clock64(); _ap_acc[k] += _n - _ap_t; _ap_t = _n; }
 #define APROF_END if (threadIdx.x == 0 && blockIdx.x == 0) for (int _k = 0; _k < 8; ++_k) g_admm_prof[_k] = _ap_acc[_k];
+// sub-phases of the {u,p} solve (rhs, forward DFT, per-frequency solve, inverse DFT): slots 8..11
+#define UPROF_T0 long long _up_t = clock64();
+#define UPROF(k) if (threadIdx.x == 0 && blockIdx.x == 0) { const long long _n = clock64(); atomicAdd(reinterpret_cast<unsigned long long*>(&g_admm_prof[8 + k]), static_cast<unsigned long long>(_n - _up_t)); _up_t = _n; }
 #else
 #define APROF_T0
 #define APROF(k)
 #define APROF_END
+#define UPROF_T0
+#define UPROF(k)
 #endif
 // projection scratch of the sorted (m <= NTADMM) projection; none for the rank-based one
 __host__ __device__ constexpr int admm_scratch_doubles(int m) {
@@ -715,13 +764,16 @@ __device__ __forceinline__ void cst2(double* base, int e, double re, double im) 
 // Real input: only the columns kc <= n/2 of the spectrum are formed (the rest is the Hermitian
 // mirror); the {u,p} solve and the inverse use that half only.
 // One thread per output bin computes all three fields, sharing twiddles and index updates.
-__device__ void dft3_forward(const AdmmSmem& S, int n, const double* const src[3]) {
+template <int NC>  // NC > 0: the kernel side at compile time (unrolled loops, constant divisors)
+__device__ void dft3_forward(const AdmmSmem& S, int n_rt, const double* const src[3]) {
+    const int n = NC > 0 ? NC : n_rt;
     const int m = n * n, nh = n / 2 + 1;  // columns 0..n/2 (Nyquist included for even n)
     for (int e = threadIdx.x; e < n * nh; e += blockDim.x) {  // rows: T[r][kc] = sum_c x[r][c] w^(kc c)
         const int r = e / nh, kc = e - r * nh;
         const double *x0 = src[0] + r * n, *x1 = src[1] + r * n, *x2 = src[2] + r * n;
         double re0 = 0.0, im0 = 0.0, re1 = 0.0, im1 = 0.0, re2 = 0.0, im2 = 0.0;
         int idx = 0;
+        #pragma unroll
         for (int c = 0; c < n; ++c) {
             const double wc = S.twc[idx], ws = S.tws[idx];
             re0 = fma(x0[c], wc, re0); im0 = fma(-x0[c], ws, im0);
@@ -740,6 +792,7 @@ __device__ void dft3_forward(const AdmmSmem& S, int n, const double* const src[3
         const int kr = e / nh, kc = e - kr * nh;
         double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
         int idx = 0;
+        #pragma unroll
         for (int r = 0; r < n; ++r) {
             const double wc = S.twc[idx], wsn = -S.tws[idx];
 #pragma unroll
@@ -761,12 +814,15 @@ __device__ void dft3_forward(const AdmmSmem& S, int n, const double* const src[3
 // inverse 2-D DFT of the half spectrum -> dst[f] = Re(.) / m  (fft_util.cpp:47-56): first over kr
 // for the columns kc <= (n-1)/2, then the real inverse over kc using the Hermitian mirror:
 // x = (Re H[0] + 2 sum_{kc >= 1} Re(H[kc] w^(-kc c))) / m.
-__device__ void dft3_inverse(const AdmmSmem& S, int n, double* const dst[3]) {
+template <int NC>
+__device__ void dft3_inverse(const AdmmSmem& S, int n_rt, double* const dst[3]) {
+    const int n = NC > 0 ? NC : n_rt;
     const int m = n * n, K2 = (n - 1) / 2, nh = n / 2 + 1;
     for (int e = threadIdx.x; e < n * nh; e += blockDim.x) {  // H[r][kc] = sum_kr F[kr][kc] w^(-kr r)
         const int r = e / nh, kc = e - r * nh;
         double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
         int idx = 0;
+        #pragma unroll
         for (int kr = 0; kr < n; ++kr) {
             const double wc = S.twc[idx], wsn = S.tws[idx];
 #pragma unroll
@@ -789,6 +845,7 @@ __device__ void dft3_inverse(const AdmmSmem& S, int n, double* const dst[3]) {
 #pragma unroll
         for (int f = 0; f < 3; ++f) re[f] = 0.0;
         int idx = c;
+        #pragma unroll
         for (int kc = 1; kc <= K2; ++kc) {
             const double wc = S.twc[idx], ws = S.tws[idx];
 #pragma unroll
@@ -829,11 +886,14 @@ __device__ __forceinline__ double block_max(double v, double* red) {
 
 // {u,p} solve (kernel_estimator.cpp:137-233) on fields in shared memory; writes u -> uout,
 // p1 -> p1out, p2 -> p2out. anchor (nullable) already holds z - L3.
-__device__ void up_solve(const AdmmSmem& S, int n, double a1m1, double a2m2, double coupling, const double* x0,
+template <int NC>
+__device__ void up_solve(const AdmmSmem& S, int n_rt, double a1m1, double a2m2, double coupling, const double* x0,
                          const double* x1, const double* y0, const double* y1, const double* y2, const double* y3,
                          const double* L10, const double* L11, const double* L20, const double* L21, const double* L22,
                          const double* L23, const double* anchor, double* uout, double* p1out, double* p2out) {
+    const int n = NC > 0 ? NC : n_rt;
     const int m = n * n;
+    UPROF_T0
     double* B1 = uout;  // the output planes hold the right-hand sides
     double* B2 = p1out;
     double* B3 = p2out;
@@ -858,8 +918,10 @@ __device__ void up_solve(const AdmmSmem& S, int n, double a1m1, double a2m2, dou
         B3[i] = b3;
     }
     __syncthreads();
+    UPROF(0)
     const double* src[3] = {B1, B2, B3};
-    dft3_forward(S, n, src);
+    dft3_forward<NC>(S, n, src);
+    UPROF(1)
     double tol;
     if (S.sym) {
         tol = S.sym[11 * m];
@@ -921,16 +983,20 @@ __device__ void up_solve(const AdmmSmem& S, int n, double a1m1, double a2m2, dou
         cst2(S.spec, 2 * m + i, fp2.x, fp2.y);
     }
     __syncthreads();
+    UPROF(2)
     double* dst[3] = {uout, p1out, p2out};
-    dft3_inverse(S, n, dst);
+    dft3_inverse<NC>(S, n, dst);
+    UPROF(3)
 }
 
 // TV u-step (kernel_estimator.cpp:356-364): u = F^-1( F(B1) / d1 ) with
 // B1 = (grad_h^T (x0 - L1_0) + grad_v^T (x1 - L1_1)) alpha1 mu1 + anchor mu3. p stays zero, so the
 // TGV x-step, y-step and multipliers of k_admm reduce to the TV ones exactly (y = L2 = 0).
-__device__ void tv_solve(const AdmmSmem& S, int n, double a1m1, double mu3, const double* x0, const double* x1,
+template <int NC>
+__device__ void tv_solve(const AdmmSmem& S, int n_rt, double a1m1, double mu3, const double* x0, const double* x1,
                          const double* L10, const double* L11, const double* anchor, const double* __restrict__ d1,
                          double* uout, double* scratch) {
+    const int n = NC > 0 ? NC : n_rt;
     const int m = n * n;
     for (int i = threadIdx.x; i < m; i += blockDim.x) {
         const int r = i / n, c = i - r * n;
@@ -941,7 +1007,7 @@ __device__ void tv_solve(const AdmmSmem& S, int n, double a1m1, double mu3, cons
     }
     __syncthreads();
     const double* src[3] = {uout, uout, uout};
-    dft3_forward(S, n, src);
+    dft3_forward<NC>(S, n, src);
     const int nh = n / 2 + 1;
     for (int e = threadIdx.x; e < n * nh; e += blockDim.x) {
         const int i = (e / nh) * n + (e % nh);
@@ -951,7 +1017,7 @@ __device__ void tv_solve(const AdmmSmem& S, int n, double a1m1, double mu3, cons
     }
     __syncthreads();
     double* dst[3] = {uout, scratch, scratch};
-    dft3_inverse(S, n, dst);
+    dft3_inverse<NC>(S, n, dst);
 }
 
 // deterministic block sum for NTADMM threads
@@ -1083,13 +1149,14 @@ size_t admm_smem_doubles(int n, int cs = 1, bool ginv_global = false) {
 // on one scene; each holds rows [crank*RP, crank*RP+RP) of the symmetric inverse in shared
 // memory, computes that slice of the z-step mat-vec, and the slices are all-gathered through
 // distributed shared memory (one cluster barrier per iteration, slices double-buffered).
+template <int NC>  // NC > 0: kernel side known at compile time (n = 15, 17, 21: the BASELINE configs)
 __global__ void __launch_bounds__(NTADMM) k_admm(AdmmArgs A, const double* __restrict__ Ginv_all,
                                                  const double* __restrict__ Etf_all, double* __restrict__ state_all,
                                                  int* __restrict__ info_all, double* __restrict__ k_out, int CS) {
     namespace cg = cooperative_groups;
     extern __shared__ double smem[];
     const int s = blockIdx.x / CS, crank = blockIdx.x - (blockIdx.x / CS) * CS;
-    const int n = A.n, m = A.m;
+    const int n = NC > 0 ? NC : A.n, m = n * n;
     const int RP = (m + CS - 1) / CS, r_lo = min(m, crank * RP), r_hi = min(m, r_lo + RP);
     const double* Ginv = Ginv_all + static_cast<size_t>(s) * m * m;
     const double* Etf = Etf_all + static_cast<size_t>(s) * m;
@@ -1248,9 +1315,9 @@ __global__ void __launch_bounds__(NTADMM) k_admm(AdmmArgs A, const double* __res
         APROF(4)
         // old p1, p2 are dead after the y-step: the solve writes them in place, u_new separately
         if (A.tv_d1)
-            tv_solve(S, n, a1m1, A.mu3, FLD(F_X0), FLD(F_X1), FLD(F_L10), FLD(F_L11), S.bz, A.tv_d1, Unew, S.zz);
+            tv_solve<NC>(S, n, a1m1, A.mu3, FLD(F_X0), FLD(F_X1), FLD(F_L10), FLD(F_L11), S.bz, A.tv_d1, Unew, S.zz);
         else
-            up_solve(S, n, a1m1, a2m2, A.coupling, FLD(F_X0), FLD(F_X1), FLD(F_Y0), FLD(F_Y1), FLD(F_Y2), FLD(F_Y3),
+            up_solve<NC>(S, n, a1m1, a2m2, A.coupling, FLD(F_X0), FLD(F_X1), FLD(F_Y0), FLD(F_Y1), FLD(F_Y2), FLD(F_Y3),
                      FLD(F_L10), FLD(F_L11), FLD(F_L20), FLD(F_L21), FLD(F_L22), FLD(F_L23), S.bz, Unew, FLD(F_P1),
                      FLD(F_P2));
         APROF(5)
@@ -1339,7 +1406,7 @@ __global__ void __launch_bounds__(NTADMM) k_solve_up(int n, double a1m1, double 
         S.tws[k] = sin(wv);
     }
     __syncthreads();
-    up_solve(S, n, a1m1, a2m2, coupling, fl[0], fl[1], fl[2], fl[3], fl[4], fl[5], fl[6], fl[7], fl[8], fl[9], fl[10],
+    up_solve<0>(S, n, a1m1, a2m2, coupling, fl[0], fl[1], fl[2], fl[3], fl[4], fl[5], fl[6], fl[7], fl[8], fl[9], fl[10],
              fl[11], anchor ? anc : nullptr, uo, p1o, p2o);
     for (int i = threadIdx.x; i < m; i += blockDim.x) {
         u[i] = uo[i];
@@ -1430,31 +1497,125 @@ void pan_stats(Context& ctx, const double* d_pan, int S, long long P, double* d_
 }
 
 static void gram_T_and_etf(Context& ctx, const double* d_pan, const double* d_obs, int S, int H, int W, int c, int n,
-                           const double* d_scale, double* T, double* Etf) {
+                           const double* d_scale, double* T, double* Etf, bool split = false) {
     const int h = H / c, w = W / c;
     const int ntiles = ceil_div(h, TG) * ceil_div(w, TG);
     const int D = 2 * n - 1, nd = D * D, n2 = n * n;
     const int SR = c * (TG - 1) + 2 * (n - 1) + 1;
     const size_t smT = static_cast<size_t>(SR) * SR * sizeof(double);
     if (smT > 227 * 1024) param_error("build_observation: kernel side too large for the device Gram kernel");
+    // rank split (C5 strips): rank r computes tile chunks [k0, k1) and the chunk sums
+    // are all-gathered; without a communicator (or G not dividing the chunk count) every chunk here
+    const bool dist = split && ctx.nccl && ctx.nranks > 1 && GRAM_CHUNKS % ctx.nranks == 0 && S == 1;
+    const int G = dist ? ctx.nranks : 1, rk = dist ? ctx.rank : 0;
+    const int k0 = rk * GRAM_CHUNKS / G, k1 = (rk + 1) * GRAM_CHUNKS / G;
+    const int t_lo = chunk_tile(k0, ntiles), t_hi = chunk_tile(k1, ntiles), nt = t_hi - t_lo;
     double* partT = ctx.scratch<double>("gram_partT", static_cast<size_t>(S) * ntiles * c * c * nd);
-    if (D * ((D + GK - 1) / GK) <= NTG && (c == 1 || c == 2 || c == 4)) {  // register-blocked (n <= 21)
-        auto fn = c == 4 ? k_gram_T2<4> : c == 2 ? k_gram_T2<2> : k_gram_T2<1>;
-        set_smem(fn, smT);
-        fn<<<dim3(ntiles, c * c, S), NTG, smT, ctx.stream>>>(d_pan, d_scale, H, W, h, w, n, partT, ntiles);
-    } else {
-        set_smem(k_gram_T, smT);
-        k_gram_T<<<dim3(ntiles, c * c, S), NT, smT, ctx.stream>>>(d_pan, d_scale, H, W, h, w, c, n, partT, ntiles);
+    double* cpT = ctx.scratch<double>("gram_cpT", static_cast<size_t>(S) * GRAM_CHUNKS * c * c * nd);
+    if (nt > 0) {
+        if (D * ((D + GK - 1) / GK) <= NTG && (c == 1 || c == 2 || c == 4)) {  // register-blocked (n <= 21)
+            auto fn = c == 4 ? k_gram_T2<4> : c == 2 ? k_gram_T2<2> : k_gram_T2<1>;
+            const size_t smT2 = smT + GK * sizeof(double);
+            set_smem(fn, smT2);
+            fn<<<dim3(nt, c * c, S), NTG, smT2, ctx.stream>>>(d_pan, d_scale, H, W, h, w, n, partT, ntiles, t_lo);
+        } else {
+            set_smem(k_gram_T, smT);
+            k_gram_T<<<dim3(nt, c * c, S), NT, smT, ctx.stream>>>(d_pan, d_scale, H, W, h, w, c, n, partT, ntiles,
+                                                                    t_lo);
+        }
+        ctx.count();
     }
-    k_reduce_tiles<<<grid1d(ctx, static_cast<long long>(S) * c * c * nd), 256, 0, ctx.stream>>>(partT, S, ntiles,
-                                                                                                c * c * nd, T);
+    k_reduce_chunks<<<grid1d(ctx, static_cast<long long>(S) * (k1 - k0) * c * c * nd), 256, 0, ctx.stream>>>(
+        partT, S, ntiles, c * c * nd, k0, k1, cpT);
     const int SRf = c * (TG - 1) + n;
     const size_t smF = (static_cast<size_t>((SRf * SRf + 1) & ~1) + TG * TG) * sizeof(double);
     set_smem(k_gram_etf, smF);
     double* partF = ctx.scratch<double>("gram_partF", static_cast<size_t>(S) * ntiles * n2);
-    k_gram_etf<<<dim3(ntiles, 1, S), NT, smF, ctx.stream>>>(d_pan, d_obs, d_scale, H, W, h, w, c, n, partF, ntiles);
-    k_reduce_tiles<<<grid1d(ctx, static_cast<long long>(S) * n2), 256, 0, ctx.stream>>>(partF, S, ntiles, n2, Etf);
-    ctx.count(4);
+    double* cpF = ctx.scratch<double>("gram_cpF", static_cast<size_t>(S) * GRAM_CHUNKS * n2);
+    if (nt > 0)
+        k_gram_etf<<<dim3(nt, 1, S), NT, smF, ctx.stream>>>(d_pan, d_obs, d_scale, H, W, h, w, c, n, partF, ntiles,
+                                                            t_lo);
+    k_reduce_chunks<<<grid1d(ctx, static_cast<long long>(S) * (k1 - k0) * n2), 256, 0, ctx.stream>>>(
+        partF, S, ntiles, n2, k0, k1, cpF);
+    ctx.count(nt > 0 ? 3 : 2);
+    check_launch();
+    if (dist) {  // every rank receives all chunk sums (S == 1: chunk k's sums are contiguous)
+        auto cm = static_cast<ncclComm_t>(ctx.nccl);
+        const size_t nT = static_cast<size_t>(GRAM_CHUNKS / G) * c * c * nd, nF = static_cast<size_t>(GRAM_CHUNKS / G) * n2;
+        FBMP_NCCL(ncclGroupStart());
+        FBMP_NCCL(ncclAllGather(cpT + static_cast<size_t>(k0) * c * c * nd, cpT, nT, ncclDouble, cm, ctx.stream));
+        FBMP_NCCL(ncclAllGather(cpF + static_cast<size_t>(k0) * n2, cpF, nF, ncclDouble, cm, ctx.stream));
+        FBMP_NCCL(ncclGroupEnd());
+    }
+    k_sum_chunks<<<grid1d(ctx, static_cast<long long>(S) * c * c * nd), 256, 0, ctx.stream>>>(cpT, S, c * c * nd, T);
+    k_sum_chunks<<<grid1d(ctx, static_cast<long long>(S) * n2), 256, 0, ctx.stream>>>(cpF, S, n2, Etf);
+    ctx.count(2);
+    check_launch();
+}
+
+// z = (E^T E + mu3 I)^-1 (E^T f + mu3 anchor) for a Gram matrix given on the device (the public
+// ObservationSystem::solve_z, kernel_estimator.cpp:79-83): Cholesky + explicit inverse + mat-vec
+__global__ void k_shift_diag(const double* __restrict__ EtE, int n2, double mu3, double* __restrict__ M) {
+    const long long NN = static_cast<long long>(n2) * n2;
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < NN;
+         e += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long r = e / n2;
+        M[e] = (e - r * n2 == r) ? EtE[e] + mu3 : EtE[e];
+    }
+}
+__global__ void k_solve_z_apply(const double* __restrict__ Ginv, const double* __restrict__ Etf,
+                                const double* __restrict__ anchor, int n2, double mu3, double* __restrict__ z) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= n2) return;
+    const double* row = Ginv + static_cast<size_t>(warp) * n2;  // symmetric: row = column
+    double acc = 0.0;
+    for (int j = lane; j < n2; j += 32) acc = fma(row[j], Etf[j] + mu3 * anchor[j], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) z[warp] = acc;
+}
+// 0.5 ||E u - f||^2 = 0.5 (u^T E^T E u - 2 u^T E^T f + f^T f) (kernel_estimator.cpp:85-87), one CTA
+__global__ void __launch_bounds__(NT) k_data_objective(const double* __restrict__ EtE, const double* __restrict__ Etf,
+                                                       const double* __restrict__ u, int n2, double ff,
+                                                       double* __restrict__ out) {
+    __shared__ double red[2 * (NT / 32 + 1)];
+    double q = 0.0, l = 0.0;
+    for (int a = threadIdx.x; a < n2; a += NT) {
+        double r = 0.0;
+        const double* row = EtE + static_cast<size_t>(a) * n2;
+        for (int b = 0; b < n2; ++b) r = fma(row[b], u[b], r);
+        q = fma(u[a], r, q);
+        l = fma(u[a], Etf[a], l);
+    }
+    const double2 t = block_sum2<NT>(q, l, red);
+    if (threadIdx.x == 0) out[0] = 0.5 * (t.x - 2.0 * t.y + ff);
+}
+void solve_z_device(Context& ctx, const double* d_EtE, const double* d_Etf, int n2, double mu3,
+                    const double* d_anchor, double* d_z) {
+    ObsSystem sys;
+    sys.S = 1;
+    sys.n = 0;
+    sys.n2 = n2;
+    const size_t NN = static_cast<size_t>(n2) * n2;
+    sys.M = ctx.scratch<double>("sz_M", NN);
+    sys.Ginv = ctx.scratch<double>("sz_Ginv", NN);
+    sys.Etf = nullptr;
+    sys.g = nullptr;
+    sys.status = ctx.scratch<int>("sz_status", 1);
+    k_shift_diag<<<grid1d(ctx, static_cast<long long>(NN)), 256, 0, ctx.stream>>>(d_EtE, n2, mu3, sys.M);
+    ctx.count();
+    factor_invert(ctx, sys, true);
+    int hst = 0;
+    d2h(&hst, sys.status, sizeof(int), ctx.stream);
+    FBMP_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (hst) num_error("build_observation: factorization of E^T E + mu3 I failed");
+    k_solve_z_apply<<<ceil_div(n2 * 32, 256), 256, 0, ctx.stream>>>(sys.Ginv, d_Etf, d_anchor, n2, mu3, d_z);
+    ctx.count();
+    check_launch();
+}
+void data_objective_device(Context& ctx, const double* d_EtE, const double* d_Etf, const double* d_u, int n2,
+                           double ff, double* d_out) {
+    k_data_objective<<<1, NT, 0, ctx.stream>>>(d_EtE, d_Etf, d_u, n2, ff, d_out);
+    ctx.count();
     check_launch();
 }
 
@@ -1488,7 +1649,7 @@ __global__ void k_add_l2(double* __restrict__ M, int S, int n, double two_a1, do
 
 void build_observation(Context& ctx, const double* d_pan, const double* d_obs, int S, int H, int W, int c, int n,
                        double mu3, const double* d_scale, ObsSystem& sys, bool want_inverse, double l2_a1,
-                       double l2_a2) {
+                       double l2_a2, bool split) {
     const int n2 = n * n, D = 2 * n - 1;
     sys.S = S;
     sys.n = n;
@@ -1500,7 +1661,7 @@ void build_observation(Context& ctx, const double* d_pan, const double* d_obs, i
     sys.g = nullptr;
     sys.status = ctx.scratch<int>("obs_status", S);
     double* T = ctx.scratch<double>("gram_T", static_cast<size_t>(S) * c * c * D * D);
-    gram_T_and_etf(ctx, d_pan, d_obs, S, H, W, c, n, d_scale, T, sys.Etf);
+    gram_T_and_etf(ctx, d_pan, d_obs, S, H, W, c, n, d_scale, T, sys.Etf, split);
     k_gram_expand<<<grid1d(ctx, static_cast<long long>(S) * NN), 256, 0, ctx.stream>>>(T, S, c, n, mu3, sys.M);
     ctx.count();
     if (l2_a1 != 0.0 || l2_a2 != 0.0) {
@@ -1508,6 +1669,14 @@ void build_observation(Context& ctx, const double* d_pan, const double* d_obs, i
                                                                                        2.0 * l2_a2);
         ctx.count();
     }
+    factor_invert(ctx, sys, want_inverse);
+}
+
+// Cholesky of sys.M (S systems of side n2, lower triangle) and, if asked, the explicit inverse
+// sys.Ginv = L^-T L^-1 (kernel_estimator.cpp:71-76, :79-83)
+void factor_invert(Context& ctx, ObsSystem& sys, bool want_inverse) {
+    const int S = sys.S, n2 = sys.n2;
+    const size_t NN = static_cast<size_t>(n2) * n2;
     FBMP_CUDA(cudaMemsetAsync(sys.status, 0, sizeof(int) * S, ctx.stream));
     const int N = n2;
     const size_t smP = static_cast<size_t>(N) * (NBK + 1) * sizeof(double);
@@ -1590,8 +1759,11 @@ void admm_device(Context& ctx, const ObsSystem& sys, const fbmp_ke_params& prm, 
     const size_t sym_bytes = (11 * static_cast<size_t>(sys.n2) + 2) * sizeof(double);
     A.cache_symbols = sm + sym_bytes <= 225 * 1024 ? 1 : 0;
     if (A.cache_symbols) sm += sym_bytes;
-    set_smem(k_admm, sm);
-    if (cs > 8) FBMP_CUDA(cudaFuncSetAttribute(k_admm, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    static const bool generic = std::getenv("FBMP_ADMM_GENERIC") != nullptr;  // A/B: runtime-n kernel
+    auto kfn = generic ? k_admm<0>
+                       : sys.n == 15 ? k_admm<15> : sys.n == 17 ? k_admm<17> : sys.n == 21 ? k_admm<21> : k_admm<0>;
+    set_smem(kfn, sm);
+    if (cs > 8) FBMP_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(sys.S * cs);
     cfg.blockDim = dim3(NTADMM);
@@ -1604,7 +1776,7 @@ void admm_device(Context& ctx, const ObsSystem& sys, const fbmp_ke_params& prm, 
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    FBMP_CUDA(cudaLaunchKernelEx(&cfg, k_admm, A, static_cast<const double*>(sys.Ginv),
+    FBMP_CUDA(cudaLaunchKernelEx(&cfg, kfn, A, static_cast<const double*>(sys.Ginv),
                                  static_cast<const double*>(sys.Etf), d_state, d_info, d_k, cs));
     ctx.count();
     check_launch();
@@ -1615,6 +1787,7 @@ void admm_device(Context& ctx, const ObsSystem& sys, const fbmp_ke_params& prm, 
         FBMP_CUDA(cudaStreamSynchronize(ctx.stream));
         std::fprintf(stderr, "admm prof n=%d cs=%d:", sys.n, cs);
         for (int k = 0; k < 7; ++k) std::fprintf(stderr, " %lld", pr[k]);
+        std::fprintf(stderr, " | up_solve: rhs %lld fwd %lld solve %lld inv %lld", pr[8], pr[9], pr[10], pr[11]);
         std::fprintf(stderr, "\n");
     }
 #endif
@@ -1654,7 +1827,7 @@ void project_simplex_device(Context& ctx, const double* d_v, int m, double* d_ou
 
 void estimate_kernel_device(Context& ctx, const double* d_pan, const double* d_obs, int S, int H, int W, int c,
                             const fbmp_ke_params& prm, double* d_k, std::vector<int>& iters, double* d_state_out,
-                            int hook_t, bool tv) {
+                            int hook_t, bool tv, bool split) {
     validate_ke(prm);
     const int n = prm.n;
     if (c < 1) param_error("build_observation: factor must be >= 1");
@@ -1680,7 +1853,7 @@ void estimate_kernel_device(Context& ctx, const double* d_pan, const double* d_o
     double* d_scale = ctx.scratch<double>("ke_scale", S);
     h2d(d_scale, scale.data(), S * sizeof(double), ctx.stream);
     ObsSystem sys;
-    build_observation(ctx, d_pan, d_obs, S, H, W, c, n, prm.mu3, d_scale, sys, true);
+    build_observation(ctx, d_pan, d_obs, S, H, W, c, n, prm.mu3, d_scale, sys, true, 0.0, 0.0, split);
     const int m = n * n;
     double* state = d_state_out ? d_state_out : ctx.scratch<double>("ke_state", static_cast<size_t>(S) * 17 * m);
     int* info = ctx.scratch<int>("ke_info", static_cast<size_t>(S) * 4);

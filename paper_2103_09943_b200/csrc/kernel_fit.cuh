@@ -33,7 +33,14 @@ struct ObsSystem {
 };
 void build_observation(Context& ctx, const double* d_pan, const double* d_obs, int S, int H, int W, int c, int n,
                        double mu3, const double* d_scale, ObsSystem& sys, bool want_inverse, double l2_a1 = 0.0,
-                       double l2_a2 = 0.0);
+                       double l2_a2 = 0.0, bool split = false);
+// Cholesky (and the explicit inverse) of sys.M, sys.S systems of side sys.n2; sys.status set on failure
+void factor_invert(Context& ctx, ObsSystem& sys, bool want_inverse);
+// public ObservationSystem::solve_z / data_objective on a device Gram matrix (kernel_estimator.cpp:79-87)
+void solve_z_device(Context& ctx, const double* d_EtE, const double* d_Etf, int n2, double mu3,
+                    const double* d_anchor, double* d_z);
+void data_objective_device(Context& ctx, const double* d_EtE, const double* d_Etf, const double* d_u, int n2,
+                           double ff, double* d_out);
 // l2 + simplex kernel estimate of one scene (kernel_estimator.cpp:389-428): device pan / obs, d_k: n*n
 void estimate_kernel_l2_device(Context& ctx, const double* d_pan, const double* d_obs, int H, int W, int c,
                                const fbmp_ke_params& prm, double* d_k, int* iters);
@@ -58,10 +65,11 @@ void gram_device(Context& ctx, const double* d_pan, const double* d_obs, int H, 
 
 // Full kernel estimate for S scenes from (pan, obs): writes kernels S*n2 (device) and
 // host-side iteration counts; throws the reference's errors. tv: the TV kernel prior
-// (KernelPrior::tv, kernel_estimator.cpp:445-452) instead of TGV^2.
+// (KernelPrior::tv, kernel_estimator.cpp:445-452) instead of TGV^2. split: with a communicator on
+// the context (C5 row strips), the Gram tiles are split over the ranks (bit-identical result).
 void estimate_kernel_device(Context& ctx, const double* d_pan, const double* d_obs, int S, int H, int W, int c,
                             const fbmp_ke_params& prm, double* d_k, std::vector<int>& iters, double* d_state_out,
-                            int hook_t, bool tv = false);
+                            int hook_t, bool tv = false, bool split = false);
 
 // Evaluation metrics (csrc/metrics.cu, metrics.hpp:11-51): device inputs, host outputs.
 void metrics_device(Context& ctx, const double* d_est, const double* d_ref, int N, int H, int W, int crop,

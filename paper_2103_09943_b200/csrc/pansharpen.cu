@@ -56,6 +56,9 @@ constexpr int NTU = 256;          // threads per K_U block
 #define FBMP_UPT 8
 #endif
 constexpr int UPT = FBMP_UPT;     // elements per thread in K_U
+// fp32 K_U: twice the elements per thread (float4 runs), so a thread keeps as many bytes in flight
+template <class T>
+constexpr int upt() { return sizeof(T) == 8 ? UPT : 2 * UPT; }
 
 __host__ __device__ inline int plane_stride(int pw) {  // >= pw*pw and == 4 (mod 16)
     const int s = pw * pw;
@@ -372,12 +375,60 @@ __global__ void __launch_bounds__(NTU) k_update(PsGeo G, T* __restrict__ z, T* _
     T* rc = r + ch * P;
     const T* ac = Ap + ch * P;
     double rr = 0.0, zz = 0.0;
-    const size_t base = static_cast<size_t>(blockIdx.x) * NTU * UPT;
+    constexpr int EPT = upt<T>();
+    const size_t base = static_cast<size_t>(blockIdx.x) * NTU * EPT;
     const size_t own_lo = static_cast<size_t>(G.rlo) * G.W, own_hi = static_cast<size_t>(G.rhi) * G.W;
     // the whole block's range is owned (always, unless the CG runs on a row strip)
-    const bool all_owned = base >= own_lo && base + static_cast<size_t>(NTU) * UPT <= own_hi;
+    const bool all_owned = base >= own_lo && base + static_cast<size_t>(NTU) * EPT <= own_hi;
+    if constexpr (!std::is_same<T, double>::value) {
+        if ((P & 3) == 0) {  // fp32: 16-byte runs of four elements, fp64 sums
+            constexpr int KV = EPT / 4;
+            const size_t nv = P / 4;
+            float4 pv[KV], av[KV], zv[KV], rv[KV];
+#pragma unroll
+            for (int k = 0; k < KV; ++k) {
+                const size_t vi = base / 4 + static_cast<size_t>(k) * NTU + threadIdx.x;
+                if (vi < nv) {
+                    pv[k] = __ldcs(reinterpret_cast<const float4*>(pc) + vi);
+                    zv[k] = __ldcs(reinterpret_cast<const float4*>(zc) + vi);
+                    rv[k] = __ldcs(reinterpret_cast<const float4*>(rc) + vi);
+                }
+            }
+            pdl_wait();
+            pdl_trigger();
+            if (__syncthreads_or(st[ch].done)) return;
+            const float alpha = static_cast<float>(st[ch].alpha);
+#pragma unroll
+            for (int k = 0; k < KV; ++k) {
+                const size_t vi = base / 4 + static_cast<size_t>(k) * NTU + threadIdx.x;
+                if (vi < nv) av[k] = __ldcs(reinterpret_cast<const float4*>(ac) + vi);
+            }
+#pragma unroll
+            for (int k = 0; k < KV; ++k) {
+                const size_t vi = base / 4 + static_cast<size_t>(k) * NTU + threadIdx.x;
+                if (vi < nv) {
+                    float* zf = &zv[k].x;
+                    float* rf = &rv[k].x;
+                    const float* pf = &pv[k].x;
+                    const float* af = &av[k].x;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        zf[u] = zf[u] + pf[u] * alpha;
+                        rf[u] = rf[u] - af[u] * alpha;
+                        const bool o = all_owned || (4 * vi + u >= own_lo && 4 * vi + u < own_hi);
+                        const double rx = rf[u], zx = zf[u];
+                        rr += o ? rx * rx : 0.0;
+                        zz += o ? zx * zx : 0.0;
+                    }
+                    __stcs(reinterpret_cast<float4*>(zc) + vi, zv[k]);
+                    __stcs(reinterpret_cast<float4*>(rc) + vi, rv[k]);
+                }
+            }
+            goto reduce;
+        }
+    }
     if ((P & 1) == 0) {
-        constexpr int KV = UPT / 2;
+        constexpr int KV = EPT / 2;
         const size_t nv = P / 2;
         V pv[KV], av[KV], zv[KV], rv[KV];
 #pragma unroll
@@ -425,7 +476,7 @@ __global__ void __launch_bounds__(NTU) k_update(PsGeo G, T* __restrict__ z, T* _
         pdl_trigger();
         if (__syncthreads_or(st[ch].done)) return;
         const T alpha = static_cast<T>(st[ch].alpha);
-        for (int k = 0; k < UPT; ++k) {
+        for (int k = 0; k < EPT; ++k) {
             const size_t i = base + static_cast<size_t>(k) * NTU + threadIdx.x;
             if (i >= P) break;
             const T zv = zc[i] + pc[i] * alpha;
@@ -438,6 +489,7 @@ __global__ void __launch_bounds__(NTU) k_update(PsGeo G, T* __restrict__ z, T* _
             }
         }
     }
+reduce:
     const double2 bs = block_sum2<NTU>(rr, zz, red);
     if (threadIdx.x == 0) {
         part[(static_cast<size_t>(ch) * nblk + blockIdx.x) * 2] = bs.x;
@@ -1659,7 +1711,7 @@ void cg_solve_t(Context& ctx, const PsGeo& G, const T* d_taps, const double* d_g
     const int nbq = q2.fn ? q2.nblk : ceil_div(G.w, TQ) * ceil_div(G.h, TQ);
     const int nba = fastA ? ceil_div(G.W, fast::a4::TA) * ceil_div(G.H, fast::a4::TA) : ceil_div(G.W, TA) * ceil_div(G.H, TA);
     const size_t P = static_cast<size_t>(G.H) * G.W;
-    const int nbu = static_cast<int>((P + static_cast<size_t>(NTU) * UPT - 1) / (static_cast<size_t>(NTU) * UPT));
+    const int nbu = static_cast<int>((P + static_cast<size_t>(NTU) * upt<T>() - 1) / (static_cast<size_t>(NTU) * upt<T>()));
     const size_t sq = q2.fn ? q2.smem : q_smem(G), sa = a_smem(G, 0), sr = static_cast<size_t>(G.n) * G.n * sizeof(double);
     check_smem(sq, "warmstart");
     if (!fastA) check_smem(sa, "warmstart");

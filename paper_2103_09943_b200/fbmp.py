@@ -596,6 +596,22 @@ def gram(pan, obs, factor, n, ctx=None):
     return EtE, Etf
 
 
+def solve_z(EtE, Etf, n, mu3, anchor, ctx=None):
+    """ObservationSystem::solve_z (kernel_estimator.cpp:79-83) on the device for a Gram matrix from gram()."""
+    EtE, Etf, anchor = _f(EtE), _f(Etf), _f(anchor)
+    z = np.empty(n * n)
+    _check(_lib.fbmp_gpu_solve_z(_ctx(ctx), _p(EtE), _p(Etf), n, C.c_double(mu3), _p(anchor), _p(z)))
+    return z
+
+
+def data_objective(EtE, Etf, n, ff, u, ctx=None):
+    """ObservationSystem::data_objective (kernel_estimator.cpp:85-87) on the device."""
+    EtE, Etf, u = _f(EtE), _f(Etf), _f(u)
+    v = C.c_double(0)
+    _check(_lib.fbmp_gpu_data_objective(_ctx(ctx), _p(EtE), _p(Etf), n, C.c_double(ff), _p(u), C.byref(v)))
+    return v.value
+
+
 # ---------------------------------------------------------------------------------------------
 # blind pipeline (SPEC.md:584-591)
 # ---------------------------------------------------------------------------------------------
@@ -731,4 +747,5 @@ EXPORTED_SYMBOLS = (
     "fbmp_gpu_data_apply", "fbmp_gpu_cg_operator", "fbmp_gpu_warmstart_cg", "fbmp_gpu_guided_filter",
     "fbmp_gpu_guided_output", "fbmp_gpu_solve_channel_fft", "fbmp_gpu_box_mean", "fbmp_gpu_convolve",
     "fbmp_gpu_shrink2", "fbmp_gpu_project_simplex", "fbmp_gpu_solve_up", "fbmp_gpu_gram",
+    "fbmp_gpu_solve_z", "fbmp_gpu_data_objective",
 )

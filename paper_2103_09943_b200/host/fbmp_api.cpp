@@ -353,44 +353,19 @@ ObservationSystem build_observation(const Plane& pan, const Plane& observation, 
 }
 
 double ObservationSystem::data_objective(const std::vector<double>& u) const {
-    // 0.5 ||E u - f||^2 = 0.5 (u^T E^T E u - 2 u^T E^T f + f^T f)
-    const std::size_t n2 = Etf_.size();
-    double q = 0.0, l = 0.0;
-    for (std::size_t a = 0; a < n2; ++a) {
-        double r = 0.0;
-        for (std::size_t b = 0; b < n2; ++b) r += EtE_[a * n2 + b] * u[b];
-        q += u[a] * r;
-        l += u[a] * Etf_[a];
-    }
-    return 0.5 * (q - 2.0 * l + ff_);
+    // 0.5 ||E u - f||^2 = 0.5 (u^T E^T E u - 2 u^T E^T f + f^T f), on the device
+    if (u.size() != Etf_.size()) throw DimensionError("data_objective: vector length does not match kernel size");
+    double v = 0.0;
+    check(fbmp_gpu_data_objective(ctx(), EtE_.data(), Etf_.data(), n_, ff_, u.data(), &v));
+    return v;
 }
 
 std::vector<double> ObservationSystem::solve_z(const std::vector<double>& anchor) const {
-    // (E^T E + mu3 I) z = E^T f + mu3 anchor by Cholesky (the device ADMM uses the inverse)
+    // (E^T E + mu3 I) z = E^T f + mu3 anchor on the device (Cholesky, explicit inverse, mat-vec)
     const std::size_t n2 = Etf_.size();
     if (anchor.size() != n2) throw DimensionError("solve_z: anchor length does not match kernel size");
-    std::vector<double> L(n2 * n2, 0.0), y(n2), z(n2);
-    for (std::size_t j = 0; j < n2; ++j) {
-        double d = EtE_[j * n2 + j] + mu3_;
-        for (std::size_t k = 0; k < j; ++k) d -= L[j * n2 + k] * L[j * n2 + k];
-        if (!(d > 0)) throw NumericalError("build_observation: factorization of E^T E + mu3 I failed");
-        L[j * n2 + j] = std::sqrt(d);
-        for (std::size_t i = j + 1; i < n2; ++i) {
-            double s = EtE_[i * n2 + j];
-            for (std::size_t k = 0; k < j; ++k) s -= L[i * n2 + k] * L[j * n2 + k];
-            L[i * n2 + j] = s / L[j * n2 + j];
-        }
-    }
-    for (std::size_t i = 0; i < n2; ++i) {
-        double s = Etf_[i] + mu3_ * anchor[i];
-        for (std::size_t k = 0; k < i; ++k) s -= L[i * n2 + k] * y[k];
-        y[i] = s / L[i * n2 + i];
-    }
-    for (std::size_t i = n2; i-- > 0;) {
-        double s = y[i];
-        for (std::size_t k = i + 1; k < n2; ++k) s -= L[k * n2 + i] * z[k];
-        z[i] = s / L[i * n2 + i];
-    }
+    std::vector<double> z(n2);
+    check(fbmp_gpu_solve_z(ctx(), EtE_.data(), Etf_.data(), n_, mu3_, anchor.data(), z.data()));
     return z;
 }
 

@@ -182,6 +182,28 @@ int main() {
         report("metrics_errors", throws<DimensionError>([&] { crop_border(ref, 15); }) &&
                                      throws<NumericalError>([&] { ergas(ref, MultiBandImage(2, 30, 30), 4); }));
     }
+    {  // ObservationSystem::solve_z / data_objective on the device (kernel_estimator.cpp:79-87):
+       // the normal equations hold and 0.5 ||E z - f||^2 >= 0 decreases from the zero kernel
+        Plane pan = random_plane(rng, 32, 32), obs = random_plane(rng, 16, 16);
+        ObservationSystem sys = build_observation(pan, obs, 2, 5, 3.0);
+        const std::size_t n2 = 25;
+        std::vector<double> anchor(n2);
+        for (double& a : anchor) a = std::uniform_real_distribution<double>(-1.0, 1.0)(rng);
+        const std::vector<double> z = sys.solve_z(anchor);
+        double res = 0.0, nrm = 0.0;
+        for (std::size_t a = 0; a < n2; ++a) {
+            double r = 3.0 * z[a] - sys.Etf()[a] - 3.0 * anchor[a];
+            for (std::size_t b = 0; b < n2; ++b) r += sys.EtE()[a * n2 + b] * z[b];
+            res += r * r;
+            nrm += sys.Etf()[a] * sys.Etf()[a];
+        }
+        const double f0 = sys.data_objective(std::vector<double>(n2, 0.0));
+        double ff = 0.0;
+        for (double v : obs.samples()) ff += v * v;
+        report("solve_z_device", std::sqrt(res) <= 1e-10 * std::sqrt(nrm) && std::abs(f0 - 0.5 * ff) <= 1e-12 * ff &&
+                                     sys.data_objective(z) >= 0.0 &&
+                                     throws<DimensionError>([&] { sys.solve_z(std::vector<double>(3)); }));
+    }
     std::printf("%d failures\n", failures);
     return failures;
 }

@@ -203,6 +203,25 @@ def test_solve_up(gpu, orc, n, coupling):
         assert np.abs(a - b).max() <= 1e-11 * (np.abs(b).max() + 1)
 
 
+@pytest.mark.parametrize("H,c,n,mu3", [(16, 2, 3, 100.0), (64, 4, 7, 5.0), (128, 4, 15, 100.0)])
+def test_solve_z_and_objective(gpu, orc, H, c, n, mu3):
+    """Public ObservationSystem::solve_z / data_objective (kernel_estimator.cpp:79-87) on the device
+    against the oracle's dense Cholesky solve and the direct 0.5 ||E u - f||^2."""
+    rng = np.random.default_rng(H + n)
+    pan = rng.uniform(0, 1, (H, H))
+    obs = rng.uniform(0, 1, (H // c, H // c))
+    anchor = rng.uniform(-1, 1, n * n)
+    G, e = gpu.gram(pan, obs, c, n)
+    z = gpu.solve_z(G, e, n, mu3, anchor)
+    zo = orc.solve_z(pan, obs, c, n, mu3, anchor)
+    assert rel(z, zo) < 1e-10
+    u = rng.uniform(0, 1, n * n)
+    E = orc.observation_matrix(pan, c, n)
+    direct = 0.5 * float(np.sum((E @ u - obs.ravel()) ** 2))
+    v = gpu.data_objective(G, e, n, float(obs.ravel() @ obs.ravel()), u)
+    assert abs(v - direct) <= 1e-9 * max(abs(direct), 1.0)
+
+
 @pytest.mark.parametrize("H,W,c,n", [(8, 8, 2, 3), (16, 16, 2, 5), (64, 64, 4, 15), (48, 64, 4, 17), (12, 12, 1, 3)])
 def test_gram(gpu, orc, H, W, c, n):
     rng = np.random.default_rng(H + n)

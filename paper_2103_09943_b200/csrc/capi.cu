@@ -699,8 +699,8 @@ int fbmp_gpu_guided_filter(fbmp_gpu_ctx* ctx, const double* input, const double*
         const size_t P = static_cast<size_t>(H) * W;
         double* d_i = upload(C, "g_in", input, P);
         double* d_g = upload(C, "g_guide", guide, P);
-        double* d_a = C.scratch<double>("g_a", P);
-        double* d_c = C.scratch<double>("g_c", P);
+        double* d_a = a_out ? C.scratch<double>("g_a", P) : nullptr;  // coefficient maps only when asked
+        double* d_c = c_out ? C.scratch<double>("g_c", P) : nullptr;
         double* d_v = C.scratch<double>("g_v", P);
         guided_filter(C, 1, H, W, radius, eps, d_i, 0, d_g, d_a, d_c, d_v, 1);
         if (a_out) download(C, a_out, d_a, P);

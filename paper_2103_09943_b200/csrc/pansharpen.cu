@@ -883,6 +883,145 @@ __global__ void __launch_bounds__(GNT) k_guided2(int H, int W, double eps, int c
 }
 
 // ------------------------------------------------------------------------------------------
+// Guided filter by row streaming (radius 1; pansharpen.cpp:274-312 with box_mean's clamped
+// windows, ops.cpp:104-128): the K_L scheme. One warp per CTA owns a band of 56 output columns
+// (lane = column pair, 4 halo columns each side, periodic like the loads) and walks a strip of
+// rows; per input row Y it forms, all in registers, in = L(z0) at Y-1 (periodic, ops.cpp:70-78
+// order), the clamped row sums of I, in, I in, I^2 at Y-1, the window means and a, c at Y-2,
+// the clamped row sums of a, c at Y-2, and v = mean(a) I + mean(c) at Y-3. Out-of-image columns
+// and rows contribute exact zeros; counts are the clamped window sizes. z0 and I rows stream by
+// cp.async (ring of GS_NB steps); the scene's I rows are shared by its channels through L2
+// (channel-fastest CTA order).
+// ------------------------------------------------------------------------------------------
+constexpr int GS_BAND = 56, GS_HALO = 4, GS_NB = 4;
+template <bool Z0>
+__global__ void __launch_bounds__(32, 12) k_guided3(int H, int W, double eps, int N, int cps, int kstrips, int R,
+                                                    const double* __restrict__ in, const double* __restrict__ guide,
+                                                    double* __restrict__ vout) {
+    using V = double2;
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x;
+    const int ch = blockIdx.x % N, item = blockIdx.x / N;
+    const int band = item / kstrips, strip = item - band * kstrips;
+    const size_t P = static_cast<size_t>(H) * W;
+    const int c0 = band * GS_BAND, r0 = strip * R, r1 = min(H, r0 + R);
+    if (r0 >= H) return;
+    const int ox = c0 - GS_HALO + 2 * lane;                 // unwrapped column of .x
+    const int X = fast::wrap_once(ox, W);
+    const double* zc = in + static_cast<size_t>(ch) * P + X;
+    const double* I = guide + static_cast<size_t>(ch / cps) * P + X;
+    double* vc = vout + static_cast<size_t>(ch) * P + X;
+    const bool writer = lane >= GS_HALO / 2 && lane < (GS_HALO + GS_BAND) / 2 && ox < W;
+    // column validity (clamped windows) of the pair and of its horizontal neighbours
+    const double vxl = ox - 1 >= 0 && ox - 1 < W ? 1.0 : 0.0, vx0 = ox >= 0 && ox < W ? 1.0 : 0.0;
+    const double vx1 = ox + 1 >= 0 && ox + 1 < W ? 1.0 : 0.0, vxr = ox + 2 >= 0 && ox + 2 < W ? 1.0 : 0.0;
+    // clamped column counts of the pair's windows
+    const int nc0 = min(W - 1, ox + 1) - max(0, ox - 1) + 1, nc1 = min(W - 1, ox + 2) - max(0, ox) + 1;
+    // 1 / window size for interior rows (3 rows), per lane; border rows take the general division
+    const double i30 = 1.0 / static_cast<double>(3 * nc0), i31 = 1.0 / static_cast<double>(3 * nc1);
+    __shared__ V ring[GS_NB][2][32];  // z(Y), I(Y-1)
+    auto back = [&](int r, int k) { int q = r - k; while (q < 0) q += H; return q; };
+    auto adv = [&](int o) { return o + W == static_cast<int>(P) ? 0 : o + W; };
+    const int y0 = r0 - 3;                                   // unwrapped input row of step 0
+    const int yA = back(y0 + H, 0) % H;
+    int io0 = yA * W, io1 = back(yA, 1) * W, o3 = back(yA, 3) * W;
+    const int steps = (r1 - r0) + 6;
+    auto issue = [&](int slot) {
+        fast::cp_async_pair(&ring[slot][0][lane], zc + io0);
+        fast::cp_async_pair(&ring[slot][1][lane], I + io1);
+        io0 = adv(io0);
+        io1 = adv(io1);
+    };
+#pragma unroll
+    for (int j = 0; j < GS_NB - 1; ++j) {
+        if (j < steps) issue(j);
+        fast::cp_async_commit();
+    }
+    V zm1 = {0, 0}, zm2 = {0, 0};                 // z(Y-1), z(Y-2)
+    V Im2 = {0, 0}, Im3 = {0, 0};                 // I(Y-2), I(Y-3)
+    V S1a = {0, 0}, S1b = {0, 0}, S2a = {0, 0}, S2b = {0, 0}, S3a = {0, 0}, S3b = {0, 0}, S4a = {0, 0}, S4b = {0, 0};
+    V Aa = {0, 0}, Ab = {0, 0}, Ca = {0, 0}, Cb = {0, 0};  // row sums of a, c at Y-4, Y-3
+#pragma unroll 2
+    for (int st = 0; st < steps; ++st) {
+        if (st + GS_NB - 1 < steps) issue((st + GS_NB - 1) % GS_NB);
+        fast::cp_async_commit();
+        fast::cp_async_wait<GS_NB - 1>();
+        const int slot = st % GS_NB;
+        const V z0 = ring[slot][0][lane], Im1 = ring[slot][1][lane];
+        const int y1 = y0 + st - 1, y2 = y0 + st - 2, y3 = y0 + st - 3;  // unwrapped rows of the stages
+        // in(Y-1)
+        V in1;
+        if (Z0) {
+            const double zL = __shfl_up_sync(FULL, zm1.y, 1), zR = __shfl_down_sync(FULL, zm1.x, 1);
+            in1.x = 4.0 * zm1.x - zm2.x - z0.x - zL - zm1.y;
+            in1.y = 4.0 * zm1.y - zm2.y - z0.y - zm1.x - zR;
+        } else {
+            in1 = zm1;
+        }
+        // clamped row sums at Y-1 (rows outside the image count as zero)
+        const double rv1 = y1 >= 0 && y1 < H ? 1.0 : 0.0;
+        V s1n, s2n, s3n, s4n;
+        {
+            const double gx = Im1.x * vx0, gy = Im1.y * vx1, ix = in1.x * vx0, iy = in1.y * vx1;
+            const double gL = __shfl_up_sync(FULL, Im1.y, 1) * vxl, gR = __shfl_down_sync(FULL, Im1.x, 1) * vxr;
+            const double iL = __shfl_up_sync(FULL, in1.y, 1) * vxl, iR = __shfl_down_sync(FULL, in1.x, 1) * vxr;
+            s1n = make_double2((gL + gx + gy) * rv1, (gx + gy + gR) * rv1);
+            s2n = make_double2((iL + ix + iy) * rv1, (ix + iy + iR) * rv1);
+            s3n = make_double2((gL * iL + gx * ix + gy * iy) * rv1, (gx * ix + gy * iy + gR * iR) * rv1);
+            s4n = make_double2((gL * gL + gx * gx + gy * gy) * rv1, (gx * gx + gy * gy + gR * gR) * rv1);
+        }
+        // window means and a, c at Y-2 (pansharpen.cpp:285-301); outside the image a = c = 0
+        V a2, c2;
+        {
+            const int nr = min(H - 1, y2 + 1) - max(0, y2 - 1) + 1;
+            const bool rin = y2 >= 0 && y2 < H;
+            const double inv0 = nr == 3 ? i30 : 1.0 / static_cast<double>(nr * nc0);
+            const double inv1 = nr == 3 ? i31 : 1.0 / static_cast<double>(nr * nc1);
+            {
+                const double mu = (S1a.x + S1b.x + s1n.x) * inv0, im = (S2a.x + S2b.x + s2n.x) * inv0;
+                const double cgi = (S3a.x + S3b.x + s3n.x) * inv0, cgg = (S4a.x + S4b.x + s4n.x) * inv0;
+                const double var = cgg - mu * mu, cov = cgi - mu * im;
+                const double a = cov / (var + eps);
+                const bool ok = rin && vx0 != 0.0;
+                a2.x = ok ? a : 0.0;
+                c2.x = ok ? im - a * mu : 0.0;
+            }
+            {
+                const double mu = (S1a.y + S1b.y + s1n.y) * inv1, im = (S2a.y + S2b.y + s2n.y) * inv1;
+                const double cgi = (S3a.y + S3b.y + s3n.y) * inv1, cgg = (S4a.y + S4b.y + s4n.y) * inv1;
+                const double var = cgg - mu * mu, cov = cgi - mu * im;
+                const double a = cov / (var + eps);
+                const bool ok = rin && vx1 != 0.0;
+                a2.y = ok ? a : 0.0;
+                c2.y = ok ? im - a * mu : 0.0;
+            }
+        }
+        // clamped row sums of a, c at Y-2 (out-of-image a, c are already zero)
+        V An, Cn;
+        {
+            const double aL = __shfl_up_sync(FULL, a2.y, 1), aR = __shfl_down_sync(FULL, a2.x, 1);
+            const double cL = __shfl_up_sync(FULL, c2.y, 1), cR = __shfl_down_sync(FULL, c2.x, 1);
+            An = make_double2(aL + a2.x + a2.y, a2.x + a2.y + aR);
+            Cn = make_double2(cL + c2.x + c2.y, c2.x + c2.y + cR);
+        }
+        // v at Y-3 (guided_output, pansharpen.cpp:304-312)
+        if (st >= 6 && writer) {
+            const int nr = min(H - 1, y3 + 1) - max(0, y3 - 1) + 1;
+            const double inv0 = nr == 3 ? i30 : 1.0 / static_cast<double>(nr * nc0);
+            const double inv1 = nr == 3 ? i31 : 1.0 / static_cast<double>(nr * nc1);
+            const double ax = (Aa.x + Ab.x + An.x) * inv0, cx = (Ca.x + Cb.x + Cn.x) * inv0;
+            const double ay = (Aa.y + Ab.y + An.y) * inv1, cy = (Ca.y + Cb.y + Cn.y) * inv1;
+            *reinterpret_cast<V*>(vc + o3) = make_double2(ax * Im3.x + cx, ay * Im3.y + cy);
+        }
+        o3 = adv(o3);
+        zm2 = zm1; zm1 = z0;
+        Im3 = Im2; Im2 = Im1;
+        S1a = S1b; S1b = s1n; S2a = S2b; S2b = s2n; S3a = S3b; S3b = s3n; S4a = S4b; S4b = s4n;
+        Aa = Ab; Ab = An; Ca = Cb; Cb = Cn;
+    }
+}
+
+// ------------------------------------------------------------------------------------------
 // Alias-group direct solve (pansharpen.cpp:337-363): one thread per LR frequency (kl, ll).
 // The c^2 x c^2 system A = diag(D) + u u^H / c^2 (D = lambda |L^|^2, u = conj(b^)) is solved in
 // closed form, eliminating through the coordinate j with the smallest D (the one that can be
@@ -1999,7 +2138,22 @@ void guided_filter(Context& ctx, int N, int H, int W, int rw, double eps, const 
     const size_t sm = (static_cast<size_t>((SZ * SZ + 1) & ~1) + (in_is_z0 ? ((SN * SN + 1) & ~1) : 0) +
                        ((SN * SN + 1) & ~1) + 2 * ((SA * SA + 1) & ~1)) * sizeof(double);
     const int hz2 = 2 * rw + (in_is_z0 ? 1 : 0);
-    if (rw == 1 && H >= GTH + hz2 && W >= GTW + hz2) {  // wrap1's range
+    static const bool tiled = std::getenv("FBMP_GF_TILED") != nullptr;  // A/B: the tiled k_guided2
+    if (rw == 1 && !tiled && !d_a && !d_c && W % 2 == 0 && H >= 16 && W >= 64) {
+        // row streaming: strips of R rows per (band, channel) item, enough items to fill the SMs
+        const int nb = ceil_div(W, GS_BAND);
+        const long long slots = static_cast<long long>(ctx.sm_count) * 12;  // warps the registers allow
+        const int k = static_cast<int>(std::max(1LL, std::min<long long>(ceil_div(H, 16),
+                                                                          slots / std::max(1, nb * N))));
+        const int R = ceil_div(H, k), kstrips = ceil_div(H, R);
+        const int cpsv = cps > 0 ? cps : N;
+        if (in_is_z0)
+            k_guided3<true><<<nb * kstrips * N, 32, 0, ctx.stream>>>(H, W, eps, N, cpsv, kstrips, R, d_in, d_guide,
+                                                                     d_v);
+        else
+            k_guided3<false><<<nb * kstrips * N, 32, 0, ctx.stream>>>(H, W, eps, N, cpsv, kstrips, R, d_in, d_guide,
+                                                                      d_v);
+    } else if (rw == 1 && H >= GTH + hz2 && W >= GTW + hz2) {  // wrap1's range
         const int cpsv = cps > 0 ? cps : N;
         const dim3 grid(ceil_div(W, GTW) * ceil_div(H, GTH), N);
         if (in_is_z0) {

@@ -137,6 +137,17 @@ def test_guided_coeffs_and_output(gpu, orc, shape, r, eps):
     assert rel(gpu.guided_filter(inp, guide, r, eps), v) < 1e-14
 
 
+@pytest.mark.parametrize("shape", [(64, 64), (96, 130), (256, 192), (17, 64)])
+def test_guided_filter_streaming(gpu, orc, shape):
+    """The row-streaming guided filter (k_guided3: radius 1, even width >= 64) against the oracle's
+    guided_output(guided_coeffs(.)) with summed-area-table box means (pansharpen.cpp:274-312)."""
+    rng = np.random.default_rng(shape[0] + shape[1])
+    guide = rng.uniform(0, 1, shape)
+    inp = rng.uniform(-1, 1, shape)
+    o = orc.guided_coeffs(inp, guide, 1, 1e-4)
+    assert rel(gpu.guided_filter(inp, guide, 1, 1e-4), orc.guided_output(o["a"], o["c"], guide, 1)) < 1e-10
+
+
 def test_guided_closed_forms(gpu):  # tests/test_pansharpen.cpp:185-206
     guide = np.random.default_rng(68).uniform(0, 1, (7, 7))
     m = gpu.guided_coeffs(np.full((7, 7), 1.25), guide, 1, 1e-2)

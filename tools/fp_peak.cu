@@ -52,8 +52,39 @@ double run(const char* name) {
     return tf;
 }
 
+// dependent-chain latency of one FMA (one thread, clock64 around 1024 chained FMAs)
+template <class T>
+__global__ void k_lat(T* out, long long* cyc, T a, T b) {
+    T x = static_cast<T>(threadIdx.x);
+    const long long t0 = clock64();
+#pragma unroll 64
+    for (int i = 0; i < 1024; ++i) x = x * a + b;
+    const long long t1 = clock64();
+    out[0] = x;
+    cyc[0] = t1 - t0;
+}
+template <class T>
+void lat(const char* name) {
+    T* out;
+    long long* cyc;
+    cudaMalloc(&out, sizeof(T));
+    cudaMalloc(&cyc, sizeof(long long));
+    long long best = 1LL << 60;
+    for (int r = 0; r < 3; ++r) {
+        k_lat<T><<<1, 1>>>(out, cyc, T(0.999), T(1e-3));
+        long long c;
+        cudaMemcpy(&c, cyc, sizeof(c), cudaMemcpyDeviceToHost);
+        if (c < best) best = c;
+    }
+    printf("{\"type\": \"%s latency\", \"cycles_per_dependent_fma\": %.2f}\n", name, best / 1024.0);
+    cudaFree(out);
+    cudaFree(cyc);
+}
+
 int main() {
     run<double>("fp64 DFMA");
     run<float>("fp32 FFMA");
+    lat<double>("fp64 DFMA");
+    lat<float>("fp32 FFMA");
     return 0;
 }

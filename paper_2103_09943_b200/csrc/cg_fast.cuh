@@ -1684,5 +1684,212 @@ __global__ void __launch_bounds__(kl::NTL, FBMP_KL_MINB) k_llp2(PsGeo G, const T
     }
 }
 
+// K_L of the fp32 mode (k_llp4f): the k_llp2 scheme with four columns per lane (16-byte float4
+// rows, as the fp64 kernel moves 16-byte double2 rows), so a warp covers 120 output columns and
+// every shuffle, cp.async and address computation serves four pixels instead of two. Per column
+// the stage expressions are those of k_llp2 (same operand order); the p.Ap partials are fp64.
+namespace kl {
+constexpr int BAND4 = 120;  // output columns per warp of k_llp4f
+}
+template <bool CG>
+__global__ void __launch_bounds__(kl::NTL, FBMP_KL_MINB) k_llp4f(PsGeo G, const float* __restrict__ guide,
+                                                      const float* __restrict__ wmu, const float* __restrict__ wg,
+                                                      const float* __restrict__ pin, float* __restrict__ out,
+                                                      CgState* st, double* __restrict__ part, int nbands, int kstrips,
+                                                      int R) {
+    using namespace kl;
+    const int nblk = gridDim.x / G.N;
+    int ch, item;
+    if (G.N % G.cps == 0) {
+        const int per_scene = nblk * G.cps, sc = blockIdx.x / per_scene, r = blockIdx.x - sc * per_scene;
+        item = r / G.cps;
+        ch = sc * G.cps + (r - item * G.cps);
+    } else {
+        ch = blockIdx.x % G.N;
+        item = blockIdx.x / G.N;
+    }
+    const int scene = ch / G.cps;
+    const int H = G.H, W = G.W;
+    const size_t P = static_cast<size_t>(H) * W;
+    const int lane = threadIdx.x;
+    if (CG) {
+        pdl_wait();
+        pdl_trigger();
+        if (__all_sync(0xffffffffu, st[ch].done != 0)) return;
+    }
+    const int nrb = (H + RB - 1) / RB;
+    const unsigned FULL = 0xffffffffu;
+    constexpr int NB = FBMP_KL_NB;
+    __shared__ float4 ring[NB][5][32];      // p, I, mu, g, d rows of NB steps
+    double dotp = 0.0;
+    {
+        const int band = item / kstrips, strip = item - band * kstrips;
+        const int c0 = band * BAND4, r0 = strip * R, r1 = min(H, r0 + R);
+        const int X = wrap_once(c0 - HALO + 4 * lane, W);  // multiple of 4; X + 3 < W (W % 4 == 0)
+        const float* pp = pin + ch * P;
+        if (CG) pp = pin + (static_cast<size_t>(st[ch].t & 1) * G.N + ch) * P;
+        const float* pc = pp + X;
+        const float* I = guide + scene * P + X;
+        const float* MU = wmu + scene * P + X;
+        const float* GK = wg + scene * P + X;
+        float* oc = out + ch * P + X;
+        const int ox = c0 - HALO + 4 * lane;                 // unwrapped column of component 0
+        const bool writer = lane >= HALO / 4 && lane < (HALO + BAND4) / 4 && ox < W;
+        int ncol[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ncol[j] = max(min(X + j + 1, W - 2) - max(X + j - 1, 1) + 1, 0);
+        const float lam = static_cast<float>(G.lambda);
+        auto back = [&](int r, int k) { const int q = r - k; return q < 0 ? q + H : q; };
+        const int yA = wrap_once(r0 - HALO, H);
+        int o4 = back(yA, 4) * W;
+        auto adv = [&](int o) { return o + W == static_cast<int>(P) ? 0 : o + W; };
+        int r3 = back(yA, 3);
+        float pm1[4] = {}, pm2[4] = {}, pm3[4] = {}, pm4[4] = {}, Im2[4] = {}, Im3[4] = {}, s2[4] = {}, s3[4] = {};
+        float hs_a[4] = {}, hs_b[4] = {}, his_a[4] = {}, his_b[4] = {};
+        float ha_a[4] = {}, ha_b[4] = {}, hc_a[4] = {}, hc_b[4] = {}, M_a[4] = {}, M_b[4] = {};
+        const int steps = (r1 - r0) + 2 * HALO;
+        int blk_left = RB;
+        int io0 = yA * W, io1 = back(yA, 1) * W, io2 = back(yA, 2) * W, io4 = o4;
+        auto issue = [&](int slot) {
+            cp_async16(&ring[slot][0][lane], pc + io0);
+            cp_async16(&ring[slot][1][lane], I + io1);
+            cp_async16(&ring[slot][2][lane], MU + io2);
+            cp_async16(&ring[slot][3][lane], GK + io2);
+            cp_async16(&ring[slot][4][lane], oc + io4);
+            io0 = adv(io0); io1 = adv(io1); io2 = adv(io2); io4 = adv(io4);
+        };
+#pragma unroll
+        for (int j = 0; j < NB - 1; ++j) {
+            if (j < steps) issue(j);
+            cp_async_commit();
+        }
+        auto unpack4 = [](const float4 v, float* o) { o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; };
+        // box sum of three horizontal neighbours: a[j-1] + a[j] + a[j+1] (k_llp2's operand order)
+        auto hbox = [&](const float* a, float* o) {
+            const float L = __shfl_up_sync(FULL, a[3], 1), Rr = __shfl_down_sync(FULL, a[0], 1);
+            o[0] = L + a[0] + a[1];
+            o[1] = a[0] + a[1] + a[2];
+            o[2] = a[1] + a[2] + a[3];
+            o[3] = a[2] + a[3] + Rr;
+        };
+        constexpr float NINTH = static_cast<float>(1.0 / 9.0);
+#pragma unroll KL_UNROLL
+        for (int st_i = 0; st_i < steps; ++st_i) {
+            if (st_i + NB - 1 < steps) issue((st_i + NB - 1) % NB);
+            cp_async_commit();
+            cp_async_wait<NB - 1>();
+            const int slot = st_i % NB;
+            float p0[4], Im1[4], mu2[4], g2[4], d4[4];
+            unpack4(ring[slot][0][lane], p0);
+            unpack4(ring[slot][1][lane], Im1);
+            unpack4(ring[slot][2][lane], mu2);
+            unpack4(ring[slot][3][lane], g2);
+            unpack4(ring[slot][4][lane], d4);
+            const int o4c = o4;
+            o4 = adv(o4);
+            // S1 at row Y-1 (ops.cpp:70-78 order: 4 c - up - down - left - right)
+            float s1[4], is1[4];
+            {
+                const float pL = __shfl_up_sync(FULL, pm1[3], 1), pR = __shfl_down_sync(FULL, pm1[0], 1);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float l = j == 0 ? pL : pm1[j - 1], r = j == 3 ? pR : pm1[j + 1];
+                    s1[j] = 4.0f * pm1[j] - pm2[j] - p0[j] - l - r;
+                    is1[j] = Im1[j] * s1[j];
+                }
+            }
+            // S2 at row Y-2
+            float hs1[4], his1[4], a2[4], c2[4];
+            hbox(s1, hs1);
+            hbox(is1, his1);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float xb = (hs_a[j] + hs_b[j] + hs1[j]) * NINTH;
+                a2[j] = g2[j] * ((his_a[j] + his_b[j] + his1[j]) * NINTH - mu2[j] * xb);
+                c2[j] = g2[j] != 0.0f ? xb - mu2[j] * a2[j] : 0.0f;
+            }
+            // S3 at row Y-3
+            float ha2[4], hc2[4], Mc[4];
+            hbox(a2, ha2);
+            hbox(c2, hc2);
+            {
+                const int g3 = wrap_once(r3 + G.grow0, G.Hg);
+                const int nrow = max(min(g3 + 1, G.Hg - 2) - max(g3 - 1, 1) + 1, 0);
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    Mc[j] = static_cast<float>(nrow * ncol[j]) * s3[j] - (hc_a[j] + hc_b[j] + hc2[j]) -
+                            Im3[j] * (ha_a[j] + ha_b[j] + ha2[j]);
+            }
+            // S5 at row Y-4
+            {
+                const float ML = __shfl_up_sync(FULL, M_b[3], 1), MR = __shfl_down_sync(FULL, M_b[0], 1);
+                float val[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float l = j == 0 ? ML : M_b[j - 1], r = j == 3 ? MR : M_b[j + 1];
+                    const float t = 4.0f * M_b[j] - M_a[j] - Mc[j] - l - r;
+                    val[j] = d4[j] + t * lam;
+                }
+                if (st_i >= 2 * HALO) {
+                    if (writer) {
+                        *reinterpret_cast<float4*>(oc + o4c) = make_float4(val[0], val[1], val[2], val[3]);
+                        const int yo = r0 + st_i - 2 * HALO;
+                        if (yo >= G.rlo && yo < G.rhi)
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) dotp += static_cast<double>(pm4[j]) * static_cast<double>(val[j]);
+                    }
+                    if (CG && (--blk_left == 0 || st_i + 1 == steps)) {
+                        const double ws = warp_sum(dotp);
+                        const int yo = r0 + st_i - 2 * HALO;
+                        if (lane == 0) part[(static_cast<size_t>(ch) * nbands + band) * nrb + yo / RB] = ws;
+                        dotp = 0.0;
+                        blk_left = RB;
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                pm4[j] = pm3[j]; pm3[j] = pm2[j]; pm2[j] = pm1[j]; pm1[j] = p0[j];
+                Im3[j] = Im2[j]; Im2[j] = Im1[j];
+                s3[j] = s2[j]; s2[j] = s1[j];
+                hs_a[j] = hs_b[j]; hs_b[j] = hs1[j]; his_a[j] = his_b[j]; his_b[j] = his1[j];
+                ha_a[j] = ha_b[j]; ha_b[j] = ha2[j]; hc_a[j] = hc_b[j]; hc_b[j] = hc2[j];
+                M_a[j] = M_b[j]; M_b[j] = Mc[j];
+            }
+            r3 = r3 + 1 == H ? 0 : r3 + 1;
+        }
+    }
+    if (CG) {
+        unsigned int prev = 0;
+        if (lane == 0) {
+            __threadfence();
+            prev = atomicAdd(&st[ch].cnt_a, 1u);
+        }
+        prev = __shfl_sync(FULL, prev, 0);
+        if (prev == static_cast<unsigned int>(nblk) - 1u) {
+            __threadfence();
+            const double* pa = part + static_cast<size_t>(ch) * nbands * nrb;
+            double sacc = 0.0;
+#pragma unroll 8
+            for (int i = lane; i < nbands * nrb; i += 32) sacc += __ldcg(pa + i);
+            const double pAp = warp_sum(sacc);
+            if (lane == 0 && G.dred) {
+                G.dred[ch] = pAp;
+                st[ch].cnt_a = 0;
+            } else if (lane == 0) {
+                CgState& S = st[ch];
+                S.pAp = pAp;
+                if (!(pAp > 0)) {  // pansharpen.cpp:240-244
+                    S.done = (sqrt(S.rs) <= 1e-12 * S.rhs_norm) ? 1 : 2;
+                    S.iters = S.t + 1;
+                } else {
+                    S.alpha = S.rs / pAp;
+                }
+                S.cnt_a = 0;
+            }
+        }
+    }
+}
+
 }  // namespace fast
 }  // namespace fbmp_gpu

@@ -36,7 +36,7 @@ enum fbmp_status {
     FBMP_RUNTIME_ERROR = 4
 };
 
-/* PansharpenParams (pansharpen.hpp:15-26), Laplacian prior. `threads` is accepted for API
+/* PansharpenParams (pansharpen.hpp:15-26), Laplacian or identity prior. `threads` is accepted for API
  * parity and ignored: all channels of a call are solved concurrently on the device. */
 typedef struct fbmp_ps_params {
     double lambda;   /* 2e-4 */
@@ -45,6 +45,7 @@ typedef struct fbmp_ps_params {
     double cg_tol;   /* 5e-5 */
     int cg_max_iter; /* 2000 */
     int threads;     /* 0 */
+    int prior;       /* PriorKind: 0 laplacian (default), 1 identity; custom (2) is not provided */
 } fbmp_ps_params;
 
 /* KernelEstParams (kernel_estimator.hpp:16-31). init: 0 = dirac, 1 = uniform. */

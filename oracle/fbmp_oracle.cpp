@@ -430,9 +430,10 @@ struct PsParams {
     double cg_tol = 5e-5;
     int cg_max_iter = 2000;
     int threads = 0;
+    int prior = 0;  // PriorKind: 0 laplacian, 1 identity (pansharpen.cpp:28-78)
 };
 
-// pansharpen.cpp:96-105 (laplacian prior only)
+// pansharpen.cpp:96-105 (laplacian and identity priors)
 void validate(const PsParams& p) {
     if (!(p.lambda > 0)) param_error("pansharpen: lambda must be positive");
     if (p.radius < 1) param_error("pansharpen: radius must be >= 1");
@@ -457,9 +458,10 @@ vec warmstart_cg(const double* x, int h, int w, const double* k, int n, int fact
         vec d = downsample(t.data(), H, W, factor);
         vec u = upsample_adjoint(d.data(), h, w, factor);
         vec data = conv.apply(u.data(), true);
-        vec l1 = laplacian(z.data(), H, W);
+        // prior.apply_adjoint(M.apply(prior.apply(z))) (pansharpen.cpp:220-221): identity -> M z
+        vec l1 = prm.prior == 1 ? z : laplacian(z.data(), H, W);
         vec m = M.apply(l1.data());
-        vec l2 = laplacian(m.data(), H, W);
+        vec l2 = prm.prior == 1 ? m : laplacian(m.data(), H, W);
         for (size_t i = 0; i < P; ++i) l2[i] *= prm.lambda;
         for (size_t i = 0; i < P; ++i) data[i] += l2[i];
         return data;
@@ -738,7 +740,7 @@ vec solve_channel_fft(const double* x, int h, int w, const double* k, int n, int
     Fft2 fhr(H, W), flr(h, w);
     vec e = embed_kernel(k, n, H, W);
     cvec bhat = fhr.forward(e.data());
-    cvec lhat = lap_spectrum(H, W);
+    cvec lhat = prm.prior == 1 ? cvec(static_cast<size_t>(H) * W, cd(1.0)) : lap_spectrum(H, W);  // :53-70
     cvec xhat = flr.forward(x);
     cvec vhat = fhr.forward(v);
     cvec zhat(bhat.size());
@@ -800,7 +802,7 @@ std::vector<vec> pansharpen(const double* lrms, int N, int h, int w, const doubl
     const double scale = peak > 0.0 ? 1.0 / peak : 1.0;
     vec pan_n(P);
     for (size_t i = 0; i < P; ++i) pan_n[i] = pan[i] * scale;
-    vec lpan = laplacian(pan_n.data(), H, W);
+    vec lpan = prm.prior == 1 ? pan_n : laplacian(pan_n.data(), H, W);  // prior.apply(pan_n)
     const Matting M = Matting::build(lpan.data(), H, W, prm.radius, prm.eps);
     std::vector<vec> out(N);
     std::vector<std::exception_ptr> errors(N);
@@ -819,7 +821,7 @@ std::vector<vec> pansharpen(const double* lrms, int N, int h, int w, const doubl
                     vec z0 = warmstart_cg(xn.data(), h, w, k, n, factor, M, prm, prm.cg_max_iter, true, nullptr, &it,
                                           &conv);
                     iters[i] = it;
-                    vec lz = laplacian(z0.data(), H, W);
+                    vec lz = prm.prior == 1 ? z0 : laplacian(z0.data(), H, W);  // ch_prior.apply(z0)
                     vec a, c, gm, gv, im;
                     guided_coeffs(lz.data(), lpan.data(), H, W, prm.radius, prm.eps, a, c, gm, gv, im);
                     vec v = guided_output(a.data(), c.data(), lpan.data(), H, W, prm.radius);
@@ -1502,11 +1504,12 @@ int orc_matting_stats(void* M, double* mean, double* var) {
 // warmstart_cg on a prebuilt matting matrix (pansharpen.hpp:73-75)
 int orc_warmstart_cg(const double* x, int h, int w, const double* k, int n, int factor, void* M, double lambda,
                      double cg_tol, int max_iters, int error_on_cap, double* z_out, int* iters, double* final_residual,
-                     int* converged) {
+                     int* converged, int prior) {
     return guard([&] {
         PsParams p;
         p.lambda = lambda;
         p.cg_tol = cg_tol;
+        p.prior = prior;
         put(warmstart_cg(x, h, w, k, n, factor, *static_cast<Matting*>(M), p, max_iters, error_on_cap != 0,
                          final_residual, iters, converged),
             z_out);
@@ -1542,18 +1545,19 @@ int orc_herm_eig(int n, const double* A, int method, double* ev, double* V) {
     });
 }
 int orc_solve_channel_fft(const double* x, int h, int w, const double* k, int n, int factor, const double* v,
-                          double lambda, double* out) {
+                          double lambda, double* out, int prior) {
     return guard([&] {
         PsParams p;
         p.lambda = lambda;
+        p.prior = prior;
         put(solve_channel_fft(x, h, w, k, n, factor, v, h * factor, w * factor, p), out);
     });
 }
 int orc_pansharpen(const double* lrms, int N, int h, int w, const double* pan, const double* k, int n, int factor,
                    double lambda, int radius, double eps, double cg_tol, int cg_max_iter, int threads, double* out,
-                   int* cg_iters) {
+                   int* cg_iters, int prior) {
     return guard([&] {
-        PsParams p{lambda, radius, eps, cg_tol, cg_max_iter, threads};
+        PsParams p{lambda, radius, eps, cg_tol, cg_max_iter, threads, prior};
         std::vector<int> it;
         auto res = pansharpen(lrms, N, h, w, pan, k, n, factor, p, &it);
         const size_t P = static_cast<size_t>(h) * factor * w * factor;

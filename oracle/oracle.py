@@ -166,8 +166,8 @@ class Matting:
         return m, v
 
 
-def warmstart_cg(x, k, factor, M: Matting, lam=2e-4, cg_tol=5e-5, max_iters=2000, error_on_cap=True):
-    """pansharpen.cpp:208-264 -> (z, iters, final_residual, converged)."""
+def warmstart_cg(x, k, factor, M: Matting, lam=2e-4, cg_tol=5e-5, max_iters=2000, error_on_cap=True, prior=0):
+    """pansharpen.cpp:208-264 -> (z, iters, final_residual, converged); prior 0 Laplacian, 1 identity."""
     x, k = _f(x), _f(k)
     z = np.empty(M.shape)
     it = C.c_int(0)
@@ -175,7 +175,7 @@ def warmstart_cg(x, k, factor, M: Matting, lam=2e-4, cg_tol=5e-5, max_iters=2000
     cv = C.c_int(0)
     _check(lib().orc_warmstart_cg(_p(x), x.shape[0], x.shape[1], _p(k), k.shape[0], factor, C.c_void_p(M.h),
                                   C.c_double(lam), C.c_double(cg_tol), max_iters, int(error_on_cap), _p(z),
-                                  C.byref(it), C.byref(fr), C.byref(cv)))
+                                  C.byref(it), C.byref(fr), C.byref(cv), int(prior)))
     return z, it.value, fr.value, bool(cv.value)
 
 
@@ -194,22 +194,22 @@ def guided_output(a, c, guide, radius=1):
     return out
 
 
-def solve_channel_fft(x, k, factor, v, lam=2e-4):
+def solve_channel_fft(x, k, factor, v, lam=2e-4, prior=0):
     x, k, v = _f(x), _f(k), _f(v)
     out = np.empty_like(v)
     _check(lib().orc_solve_channel_fft(_p(x), x.shape[0], x.shape[1], _p(k), k.shape[0], factor, _p(v),
-                                       C.c_double(lam), _p(out)))
+                                       C.c_double(lam), _p(out), int(prior)))
     return out
 
 
-def pansharpen(lrms, pan, k, factor, lam=2e-4, radius=1, eps=1e-4, cg_tol=5e-5, cg_max_iter=2000, threads=0):
+def pansharpen(lrms, pan, k, factor, lam=2e-4, radius=1, eps=1e-4, cg_tol=5e-5, cg_max_iter=2000, threads=0, prior=0):
     lrms, pan, k = _f(lrms), _f(pan), _f(k)
     N, h, w = lrms.shape
     out = np.empty((N, h * factor, w * factor))
     it = np.zeros(N, np.int32)
     _check(lib().orc_pansharpen(_p(lrms), N, h, w, _p(pan), _p(k), k.shape[0], factor, C.c_double(lam), radius,
                                 C.c_double(eps), C.c_double(cg_tol), cg_max_iter, threads, _p(out),
-                                it.ctypes.data_as(I)))
+                                it.ctypes.data_as(I), int(prior)))
     return out, it
 
 

@@ -33,6 +33,9 @@ Context::~Context() {
         if (e) cudaEventDestroy(e);
     if (pinned_buf) cudaFreeHost(pinned_buf);
     if (aux_stream) cudaStreamDestroy(aux_stream);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+    for (auto& e : copy_ev)
+        if (e) cudaEventDestroy(e);
     if (fork_ev) cudaEventDestroy(fork_ev);
     if (join_ev) cudaEventDestroy(join_ev);
     ws.clear();
@@ -72,6 +75,9 @@ void validate_ps(const fbmp_ps_params& p) {  // pansharpen.cpp:96-105 (Laplacian
     if (!(p.cg_tol > 0)) param_error("pansharpen: cg_tol must be positive");
     if (p.cg_max_iter < 1) param_error("pansharpen: cg_max_iter must be >= 1");
     if (p.threads < 0) param_error("pansharpen: threads must be >= 0");
+    if (p.prior == 2) param_error("pansharpen: custom prior requires a kernel");  // pansharpen.cpp:103-104
+    if (p.prior != 0 && p.prior != 1)
+        param_error("pansharpen: the GPU path implements the Laplacian and identity priors");
 }
 
 static void check_kernel(int n, int H, int W) {
@@ -92,13 +98,17 @@ void pansharpen_device(Context& ctx, const double* d_lrms, int S, int N, int h, 
     if (ch0 < 0 || ch0 + NS > N || (S > 1 && NS != N)) param_error("pansharpen: invalid channel subset");
     const int NC = S * NS;
     const size_t P = static_cast<size_t>(H) * W, p = static_cast<size_t>(h) * w;
-    const PsGeo G = make_geo(NC, h, w, c, n, prm.radius, prm.lambda, prm.eps, NS);
+    PsGeo G = make_geo(NC, h, w, c, n, prm.radius, prm.lambda, prm.eps, NS);
+    G.identity = prm.prior == 1;
     double* scale = ctx.scratch<double>("ps_scale", S);
     double* lpan = ctx.scratch<double>("ps_lpan", P * S);
     double* xn = ctx.scratch<double>("ps_xn", p * NC);
     // normalisation over PAN and ALL bands (pansharpen.cpp:374-376), also for a subset solve
     peak_scale(ctx, d_pan, static_cast<long long>(P), d_lrms, static_cast<long long>(p) * N, S, scale);
-    laplacian_scaled(ctx, d_pan, H, W, S, scale, lpan);
+    if (G.identity)  // prior.apply(pan_n) (pansharpen.cpp:379): the identity keeps pan_n
+        scale_copy(ctx, d_pan, static_cast<long long>(P) * S, scale, static_cast<long long>(P), lpan);
+    else
+        laplacian_scaled(ctx, d_pan, H, W, S, scale, lpan);
     scale_copy(ctx, d_lrms + static_cast<size_t>(ch0) * p, static_cast<long long>(p) * NC, scale,
                static_cast<long long>(p) * NS, xn);
 
@@ -151,7 +161,8 @@ void pansharpen_device(Context& ctx, const double* d_lrms, int S, int N, int h, 
             const int sc = i / NS;
             double* az = ctx.scratch<double>("cg_res_az", P);
             double* rhs = ctx.scratch<double>("cg_res_rhs", P);
-            const PsGeo G1 = make_geo(1, h, w, c, n, prm.radius, prm.lambda, prm.eps);
+            PsGeo G1 = make_geo(1, h, w, c, n, prm.radius, prm.lambda, prm.eps);
+            G1.identity = G.identity;
             cg_operator_apply(ctx, G1, d_taps + static_cast<size_t>(sc) * n * n, lpan + sc * P, B.z + i * P, az, 0);
             data_rhs(ctx, G1, d_taps + static_cast<size_t>(sc) * n * n, xn + i * p, rhs);
             std::vector<double> a(P), b(P);
@@ -165,7 +176,8 @@ void pansharpen_device(Context& ctx, const double* d_lrms, int S, int N, int h, 
         }
     }
     double* v = ctx.scratch<double>("ps_v", P * NC);
-    guided_filter(ctx, NC, H, W, prm.radius, prm.eps, B.z, 1, lpan, nullptr, nullptr, v, NS);
+    // guided_coeffs(ch_prior.apply(z0), lpan) (pansharpen.cpp:396-398): L(z0), or z0 itself
+    guided_filter(ctx, NC, H, W, prm.radius, prm.eps, B.z, G.identity ? 0 : 1, lpan, nullptr, nullptr, v, NS);
     int* flag = ctx.scratch<int>("ps_flag", NC);
     FBMP_CUDA(cudaMemsetAsync(flag, 0, sizeof(int) * NC, ctx.stream));
     solve_channel_fft(ctx, G, d_taps, xn, v, scale, d_out, flag);
@@ -215,6 +227,7 @@ void pansharpen_strips_device(Context& ctx, const double* d_lrms, int N, int h, 
                               std::vector<int>& cg_iters, int vstrips) {
     validate_ps(prm);
     if (ctx.precision != 64) param_error("pansharpen: the fp32 mode is not available for row strips");
+    if (prm.prior != 0) param_error("pansharpen: row strips implement the Laplacian prior only");
     const int H = h * c, W = w * c;
     if (2 * prm.radius + 1 > std::min(H, W)) dim_error("matting matrix: window larger than image");
     check_kernel(n, H, W);
@@ -504,6 +517,7 @@ void fbmp_gpu_default_ps_params(fbmp_ps_params* p) {
     p->cg_tol = 5e-5;
     p->cg_max_iter = 2000;
     p->threads = 0;
+    p->prior = 0;
 }
 void fbmp_gpu_default_ke_params(fbmp_ke_params* p) {
     p->n = 29;
@@ -631,7 +645,9 @@ int fbmp_gpu_cg_operator(fbmp_gpu_ctx* ctx, const double* guide, const double* p
         double* d_x = upload(C, "u_in", p, P);
         double* d_k = upload(C, "u_taps", k, static_cast<size_t>(n) * n);
         double* d_o = C.scratch<double>("u_out", P);
-        const PsGeo G = make_geo(1, H / factor, W / factor, factor, n, prm.radius, prm.lambda, prm.eps);
+        validate_ps(prm);
+        PsGeo G = make_geo(1, H / factor, W / factor, factor, n, prm.radius, prm.lambda, prm.eps);
+        G.identity = prm.prior == 1;
         cg_operator_apply(C, G, d_k, d_g, d_x, d_o, 0);
         download(C, out, d_o, P);
     });
@@ -651,7 +667,9 @@ int fbmp_gpu_warmstart_cg(fbmp_gpu_ctx* ctx, const double* x, int h, int w, cons
         double* d_g = upload(C, "w_guide", guide, P);
         double* d_x = upload(C, "w_x", x, p);
         double* d_k = upload(C, "w_taps", k, static_cast<size_t>(n) * n);
-        const PsGeo G = make_geo(1, h, w, factor, n, prm.radius, prm.lambda, prm.eps);
+        validate_ps(prm);
+        PsGeo G = make_geo(1, h, w, factor, n, prm.radius, prm.lambda, prm.eps);
+        G.identity = prm.prior == 1;
         CgBuffers B;
         B.z = C.scratch<double>("cg_z", P);
         B.r = C.scratch<double>("cg_r", P);
@@ -746,7 +764,9 @@ int fbmp_gpu_solve_channel_fft(fbmp_gpu_ctx* ctx, const double* x, int h, int w,
         double* d_o = C.scratch<double>("f_out", P);
         int* flag = C.scratch<int>("f_flag", 1);
         FBMP_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), C.stream));
-        const PsGeo G = make_geo(1, h, w, factor, n, prm.radius, prm.lambda, prm.eps);
+        validate_ps(prm);
+        PsGeo G = make_geo(1, h, w, factor, n, prm.radius, prm.lambda, prm.eps);
+        G.identity = prm.prior == 1;
         solve_channel_fft(C, G, d_k, d_x, d_v, nullptr, d_o, flag);
         int hf = 0;
         d2h(&hf, flag, sizeof(int), C.stream);
@@ -1026,8 +1046,21 @@ int fbmp_gpu_blind(fbmp_gpu_ctx* ctx, const double* lrms, int N, int h, int w, c
         double* d_k = C.scratch<double>("api_k", static_cast<size_t>(kep.n) * kep.n);
         double* d_w = C.scratch<double>("api_omega", N);
         std::vector<int> ai, ci;
+        // the HRMS planes stream to `out` per channel while the later channels finish
+        // (single-domain solves only: the row-strip path gathers the channels on rank 0 first)
+        struct Sink {
+            Context& c;
+            Sink(Context& cc, double* o) : c(cc) { c.host_out = c.nccl ? nullptr : o; }
+            ~Sink() {  // no copy into the caller's buffer outlives the call, also on the error path
+                c.host_out = nullptr;
+                if (c.copy_stream) cudaStreamSynchronize(c.copy_stream);
+            }
+        } sink(C, out);
+        const bool sunk = C.host_out != nullptr;
         blind_device(C, d_l, 1, N, h, w, d_p, swp, kep, ps_or_default(ps), d_o, d_k, d_w, ai, ci);
-        download(C, out, d_o, P * N);
+        FBMP_CUDA(cudaStreamSynchronize(C.stream));
+        if (C.copy_stream) FBMP_CUDA(cudaStreamSynchronize(C.copy_stream));
+        if (!sunk) download(C, out, d_o, P * N);
         if (k_out) download(C, k_out, d_k, static_cast<size_t>(kep.n) * kep.n);
         if (omega_out) download(C, omega_out, d_w, N);
     });

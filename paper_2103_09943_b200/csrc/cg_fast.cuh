@@ -1500,7 +1500,9 @@ __device__ __forceinline__ void cp_async_pair(float2* sdst, const float* gsrc) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc) : "memory");
 }
 
-template <bool CG, class T = double>
+// LAP = false: the identity pansharpening prior (pansharpen.cpp:28-50): Ap = d + lambda M p (the
+// S1 and S5 Laplacians become copies; everything else, including the row pipeline, is unchanged)
+template <bool CG, class T = double, bool LAP = true>
 __global__ void __launch_bounds__(kl::NTL, FBMP_KL_MINB) k_llp2(PsGeo G, const T* __restrict__ guide,
                                                      const T* __restrict__ wmu, const T* __restrict__ wg,
                                                      const T* __restrict__ pin, T* __restrict__ out,
@@ -1564,14 +1566,24 @@ __global__ void __launch_bounds__(kl::NTL, FBMP_KL_MINB) k_llp2(PsGeo G, const T
         int blk_left = RB;
         // the rows of step j stream into ring slot j % NB with cp.async, NB - 1 steps ahead of
         // their use (each lane copies and later reads its own 16 bytes: no warp barrier)
-        int io0 = o0, io1 = o1, io2 = o2, io4 = o4;  // offsets of the next step to issue
+        // byte offsets of the next step to issue (32-bit: a plane is < 2^31 bytes), added to 64-bit
+        // bases: one 64-bit add per address instead of a sign-extended scaled index
+        const unsigned Wb = static_cast<unsigned>(W) * sizeof(T), Pb = static_cast<unsigned>(P) * sizeof(T);
+        unsigned io0 = static_cast<unsigned>(o0) * sizeof(T), io1 = static_cast<unsigned>(o1) * sizeof(T),
+                 io2 = static_cast<unsigned>(o2) * sizeof(T), io4 = static_cast<unsigned>(o4) * sizeof(T);
+        const char* pcb = reinterpret_cast<const char*>(pc);
+        const char* Ib = reinterpret_cast<const char*>(I);
+        const char* MUb = reinterpret_cast<const char*>(MU);
+        const char* GKb = reinterpret_cast<const char*>(GK);
+        const char* ocb = reinterpret_cast<const char*>(oc);
+        auto advb = [&](unsigned o) { const unsigned q = o + Wb; return q == Pb ? 0u : q; };
         auto issue = [&](int slot) {
-            cp_async_pair(&ring[slot][0][lane], pc + io0);
-            cp_async_pair(&ring[slot][1][lane], I + io1);
-            cp_async_pair(&ring[slot][2][lane], MU + io2);
-            cp_async_pair(&ring[slot][3][lane], GK + io2);
-            cp_async_pair(&ring[slot][4][lane], oc + io4);
-            io0 = adv(io0); io1 = adv(io1); io2 = adv(io2); io4 = adv(io4);
+            cp_async_pair(&ring[slot][0][lane], reinterpret_cast<const T*>(pcb + io0));
+            cp_async_pair(&ring[slot][1][lane], reinterpret_cast<const T*>(Ib + io1));
+            cp_async_pair(&ring[slot][2][lane], reinterpret_cast<const T*>(MUb + io2));
+            cp_async_pair(&ring[slot][3][lane], reinterpret_cast<const T*>(GKb + io2));
+            cp_async_pair(&ring[slot][4][lane], reinterpret_cast<const T*>(ocb + io4));
+            io0 = advb(io0); io1 = advb(io1); io2 = advb(io2); io4 = advb(io4);
         };
 #pragma unroll
         for (int j = 0; j < NB - 1; ++j) {
@@ -1589,10 +1601,14 @@ __global__ void __launch_bounds__(kl::NTL, FBMP_KL_MINB) k_llp2(PsGeo G, const T
             const int o4c = o4;
             o4 = adv(o4);
             // S1 at row Y-1 (ops.cpp:70-78 order: 4 c - up - down - left - right)
-            const T pL = __shfl_up_sync(FULL, pm1.y, 1), pR = __shfl_down_sync(FULL, pm1.x, 1);
             V s1, is1;
-            s1.x = T(4) * pm1.x - pm2.x - p0.x - pL - pm1.y;
-            s1.y = T(4) * pm1.y - pm2.y - p0.y - pm1.x - pR;
+            if constexpr (LAP) {
+                const T pL = __shfl_up_sync(FULL, pm1.y, 1), pR = __shfl_down_sync(FULL, pm1.x, 1);
+                s1.x = T(4) * pm1.x - pm2.x - p0.x - pL - pm1.y;
+                s1.y = T(4) * pm1.y - pm2.y - p0.y - pm1.x - pR;
+            } else {
+                s1 = pm1;
+            }
             is1.x = Im1.x * s1.x;
             is1.y = Im1.y * s1.y;
             // S2 at row Y-2
@@ -1623,9 +1639,15 @@ __global__ void __launch_bounds__(kl::NTL, FBMP_KL_MINB) k_llp2(PsGeo G, const T
             Mc.x = static_cast<T>(nrow * nc0) * s3.x - (hc_a.x + hc_b.x + hc2.x) - Im3.x * (ha_a.x + ha_b.x + ha2.x);
             Mc.y = static_cast<T>(nrow * nc1) * s3.y - (hc_a.y + hc_b.y + hc2.y) - Im3.y * (ha_a.y + ha_b.y + ha2.y);
             // S5 at row Y-4
-            const T ML = __shfl_up_sync(FULL, M_b.y, 1), MR = __shfl_down_sync(FULL, M_b.x, 1);
-            const T t0 = T(4) * M_b.x - M_a.x - Mc.x - ML - M_b.y;
-            const T t1 = T(4) * M_b.y - M_a.y - Mc.y - M_b.x - MR;
+            T t0, t1;
+            if constexpr (LAP) {
+                const T ML = __shfl_up_sync(FULL, M_b.y, 1), MR = __shfl_down_sync(FULL, M_b.x, 1);
+                t0 = T(4) * M_b.x - M_a.x - Mc.x - ML - M_b.y;
+                t1 = T(4) * M_b.y - M_a.y - Mc.y - M_b.x - MR;
+            } else {
+                t0 = M_b.x;
+                t1 = M_b.y;
+            }
             const V val = mk2(d4.x + t0 * lam, d4.y + t1 * lam);
             if (st_i >= 2 * HALO) {
                 if (writer) {

@@ -42,6 +42,7 @@ PsGeo make_geo(int N, int h, int w, int c, int n, int rw, double lambda, double 
     G.rlo = 0;
     G.rhi = G.H;
     G.dred = nullptr;
+    G.identity = 0;
     return G;
 }
 
@@ -1173,7 +1174,7 @@ __device__ __forceinline__ double rcp_nr(double x) {
     e = fma(-x, y, 1.0);
     return fma(y, e, y);
 }
-__global__ void __launch_bounds__(AG_NT) k_alias16(int H, int W, int h, int w, int c, int N, int cps,
+__global__ void __launch_bounds__(AG_NT) k_alias16(int H, int W, int h, int w, int c, int N, int cps, int identity,
                                                    double lambda, const double2* __restrict__ Bh,
                                                    const double2* __restrict__ Xh, const double2* __restrict__ Vh,
                                                    double2* __restrict__ Zh, const double* __restrict__ cosHW,
@@ -1199,7 +1200,7 @@ __global__ void __launch_bounds__(AG_NT) k_alias16(int H, int W, int h, int w, i
     if (mem) {
         const double2 bv = __ldg(Bh + static_cast<size_t>(scene) * HS + hidx);
         u = {bv.x, mirror ? bv.y : -bv.y};  // conj(b^)
-        lh = 4.0 - 2.0 * __ldg(cosHW + R) - 2.0 * __ldg(cosHW + H + Cc);  // pansharpen.cpp:56-63
+        lh = identity ? 1.0 : 4.0 - 2.0 * __ldg(cosHW + R) - 2.0 * __ldg(cosHW + H + Cc);  // pansharpen.cpp:53-70
         D = lambda * (lh * lh);
     }
     const double u2 = mem ? cnorm(u) : 0.0;
@@ -1262,7 +1263,7 @@ __global__ void __launch_bounds__(AG_NT) k_alias16(int H, int W, int h, int w, i
 }
 
 template <int CM>
-__global__ void __launch_bounds__(128) k_alias(int H, int W, int h, int w, int c, int cps, double lambda,
+__global__ void __launch_bounds__(128) k_alias(int H, int W, int h, int w, int c, int cps, int identity, double lambda,
                                                const double2* __restrict__ Bh, const double2* __restrict__ Xh,
                                                const double2* __restrict__ Vh, double2* __restrict__ Zh,
                                                const double* __restrict__ cosHW, int* __restrict__ flag) {
@@ -1287,7 +1288,7 @@ __global__ void __launch_bounds__(128) k_alias(int H, int W, int h, int w, int c
             const int R = kl + a * h, Cc = ll + b * w;
             const cplx bv = half_lookup(Bh, R, Cc, H, W);
             const cplx vv = half_lookup(V, R, Cc, H, W);
-            const double lh = 4.0 - 2.0 * __ldg(cosHW + R) - 2.0 * __ldg(cosHW + H + Cc);  // :56-63
+            const double lh = identity ? 1.0 : 4.0 - 2.0 * __ldg(cosHW + R) - 2.0 * __ldg(cosHW + H + Cc);  // :53-70
             D[g] = lambda * (lh * lh);
             u[g] = cconj(bv);
             u2[g] = cnorm(u[g]);
@@ -1639,6 +1640,7 @@ std::pair<AFn, size_t> apply3_select(const PsGeo& G) {
 struct LlpPlan {
     int nb = 0, k = 1, R = 0, ctas = 0;
     bool pairs = false;  // k_llp2 (column pairs; W even)
+    bool quads = false;  // k_llp4f (fp32 mode, four columns per lane; W % 4 == 0)
 };
 inline bool use_llp() {
     static const bool on = !(std::getenv("FBMP_KA") && std::atoi(std::getenv("FBMP_KA")) == 4);
@@ -1648,21 +1650,25 @@ inline bool use_llp() {
 // resident warp slots; R is a multiple of the partial row block.
 template <class T = double>
 LlpPlan llp_plan(Context& ctx, const PsGeo& G) {
-    static int per_sm[2] = {0, 0};
+    static int per_sm[3] = {0, 0, 0};
     LlpPlan L;
     static const bool no_pairs = std::getenv("FBMP_KL1") != nullptr;
+    static const bool no_quads = std::getenv("FBMP_KL_NOQUAD") != nullptr;  // A/B: fp32 on k_llp2
     L.pairs = (G.W % 2 == 0) && (!no_pairs || !std::is_same<T, double>::value);
-    int& ps = per_sm[L.pairs ? 1 : 0];
+    L.quads = !std::is_same<T, double>::value && G.W % 4 == 0 && !no_quads && !G.identity;
+    int& ps = per_sm[L.quads ? 2 : (L.pairs ? 1 : 0)];
     if (!ps) {
         int blocks = 0;
-        if (L.pairs)
+        if (L.quads)
+            FBMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fast::k_llp4f<true>, fast::kl::NTL, 0));
+        else if (L.pairs)
             FBMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fast::k_llp2<true, T>, fast::kl::NTL, 0));
         else
             FBMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fast::k_llp<true>, fast::kl::NTL, 0));
         ps = std::max(1, std::min(blocks, 32)) * (fast::kl::NTL / 32);
     }
     const long long slots = static_cast<long long>(ps) * ctx.sm_count;
-    L.nb = ceil_div(G.W, L.pairs ? fast::kl::BAND2 : fast::kl::BAND);
+    L.nb = ceil_div(G.W, L.quads ? fast::kl::BAND4 : (L.pairs ? fast::kl::BAND2 : fast::kl::BAND));
     const long long bc = static_cast<long long>(L.nb) * G.N;
     long long best = -1;
     for (int k = 1; k <= ceil_div(G.H, fast::kl::RB); ++k) {
@@ -1710,7 +1716,25 @@ void launch_llp(Context& ctx, const PsGeo& G, const T* taps, const T* guide, con
         fd.first<<<dim3(nba, S * groups), fast::NT, fd.second, ctx.stream>>>(G, taps, q, out, st);
     if (between) FBMP_CUDA(cudaEventRecordWithFlags(between, ctx.stream, cudaEventRecordExternal));
     const LlpPlan L = llp_plan<T>(ctx, G);
-    if (L.pairs) {
+    if (G.identity) {  // identity prior: M without the Laplacians (pair kernel only)
+        if (!L.pairs) param_error("pansharpen: the identity prior on the device needs an even image width");
+        fast::k_llp2<CG, T, false><<<dim3(L.ctas * G.N), fast::kl::NTL, 0, ctx.stream>>>(G, guide, mu, gk, p, out, st,
+                                                                                         part, L.nb, L.k, L.R);
+        return;
+    }
+    if constexpr (!std::is_same<T, double>::value) {
+        if (L.quads) {
+            fast::k_llp4f<CG><<<dim3(L.ctas * G.N), fast::kl::NTL, 0, ctx.stream>>>(G, guide, mu, gk, p, out, st, part,
+                                                                                    L.nb, L.k, L.R);
+            return;
+        }
+    }
+    // env FBMP_PDL_KL=1: K_L also by programmatic dependent launch (its CTAs start while K_D drains)
+    static const bool pdl_kl = std::getenv("FBMP_PDL_KL") && std::atoi(std::getenv("FBMP_PDL_KL")) == 1;
+    if (L.pairs && pdl && pdl_kl) {
+        launch_pdl(fast::k_llp2<CG, T>, dim3(L.ctas * G.N), dim3(fast::kl::NTL), 0, ctx.stream, G, guide, mu, gk, p,
+                   out, st, part, L.nb, L.k, L.R);
+    } else if (L.pairs) {
         fast::k_llp2<CG, T><<<dim3(L.ctas * G.N), fast::kl::NTL, 0, ctx.stream>>>(G, guide, mu, gk, p, out, st, part,
                                                                                   L.nb, L.k, L.R);
     } else {
@@ -1819,6 +1843,7 @@ void cg_operator_apply(Context& ctx, const PsGeo& G, const double* d_taps, const
         check_launch();
         return;
     }
+    if (G.identity && mode != 1) param_error("cg operator: the identity prior needs the specialised operator");
     const size_t sa = a_smem(G, mode);
     check_smem(sa, "cg operator");
     if (mode == 0) {
@@ -1847,6 +1872,9 @@ void cg_solve_t(Context& ctx, const PsGeo& G, const T* d_taps, const double* d_g
     if (!F64 && !(fastA && q2.fn))
         param_error("pansharpen: the fp32 mode needs the specialised operator (radius 1, factor 2 or 4 with a "
                     "supported kernel side, images >= 64 x 64)");
+    if (G.identity && !(fastA && use_llp()))
+        param_error("pansharpen: the identity prior on the device needs the specialised operator (radius 1, "
+                    "factor 1, 2 or 4, images >= 64 x 64)");
     const int nbq = q2.fn ? q2.nblk : ceil_div(G.w, TQ) * ceil_div(G.h, TQ);
     const int nba = fastA ? ceil_div(G.W, fast::a4::TA) * ceil_div(G.H, fast::a4::TA) : ceil_div(G.W, TA) * ceil_div(G.H, TA);
     const size_t P = static_cast<size_t>(G.H) * G.W;
@@ -2197,20 +2225,48 @@ void solve_channel_fft(Context& ctx, const PsGeo& G, const double* d_taps, const
     k_cos_tables<<<ceil_div(H + W, 256), 256, 0, ctx.stream>>>(H, W, cosHW);
     if (G.c <= 4) {
         const dim3 grid(ceil_div(static_cast<long long>(h) * w * AG, AG_NT), S);
-        k_alias16<<<grid, AG_NT, 0, ctx.stream>>>(H, W, h, w, G.c, N, G.cps, G.lambda, bh, xh, vh, zh, cosHW, d_flag);
+        k_alias16<<<grid, AG_NT, 0, ctx.stream>>>(H, W, h, w, G.c, N, G.cps, G.identity, G.lambda, bh, xh, vh, zh,
+                                                  cosHW, d_flag);
     } else {
         const int nthreads = 128;
         const dim3 grid(ceil_div(static_cast<long long>(h) * w, nthreads), N);
-        k_alias<8><<<grid, nthreads, 0, ctx.stream>>>(H, W, h, w, G.c, G.cps, G.lambda, bh, xh, vh, zh, cosHW, d_flag);
+        k_alias<8><<<grid, nthreads, 0, ctx.stream>>>(H, W, h, w, G.c, G.cps, G.identity, G.lambda, bh, xh, vh, zh,
+                                                       cosHW, d_flag);
     }
     ctx.count(2);
     check_launch();
+    if (ctx.host_out && N > 1) {
+        // per channel: inverse FFT, unscale, then the plane's D2H on the copy stream overlaps the
+        // next channel's FFT (the same cuFFT plan kind with batch 1: the same per-plane result)
+        if (!ctx.copy_stream) {
+            FBMP_CUDA(cudaStreamCreateWithFlags(&ctx.copy_stream, cudaStreamNonBlocking));
+            for (auto& e : ctx.copy_ev) FBMP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        for (int ch = 0; ch < N; ++ch) {
+            FBMP_CUFFT(cufftExecZ2D(ctx.plan(1, H, W, 1), reinterpret_cast<cufftDoubleComplex*>(zh + ch * HS),
+                                    zr + ch * P));
+            k_unscale<<<grid1d(ctx, static_cast<long long>(P)), 256, 0, ctx.stream>>>(
+                zr + ch * P, static_cast<long long>(P), 1.0 / static_cast<double>(P),
+                d_scale ? d_scale + ch / G.cps : nullptr, static_cast<long long>(P), d_out + ch * P);
+            ctx.count();
+            cudaEvent_t e = ctx.copy_ev[ch & 1];
+            FBMP_CUDA(cudaEventRecord(e, ctx.stream));
+            FBMP_CUDA(cudaStreamWaitEvent(ctx.copy_stream, e, 0));
+            FBMP_CUDA(cudaMemcpyAsync(ctx.host_out + ch * P, d_out + ch * P, P * sizeof(double),
+                                      cudaMemcpyDeviceToHost, ctx.copy_stream));
+        }
+        check_launch();
+        return;
+    }
     FBMP_CUFFT(cufftExecZ2D(ctx.plan(1, H, W, N), reinterpret_cast<cufftDoubleComplex*>(zh), zr));
     k_unscale<<<grid1d(ctx, static_cast<long long>(P) * N), 256, 0, ctx.stream>>>(
         zr, static_cast<long long>(P) * N, 1.0 / static_cast<double>(P), d_scale, static_cast<long long>(P) * G.cps,
         d_out);
     ctx.count();
     check_launch();
+    if (ctx.host_out) {  // one channel: a plain download after the solve
+        FBMP_CUDA(cudaMemcpyAsync(ctx.host_out, d_out, P * N * sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+    }
 }
 
 void peak_scale(Context& ctx, const double* d_pan, long long P, const double* d_lrms, long long Np, int S,

@@ -30,6 +30,7 @@ struct PsGeo {
                                   // taps, guide and intensity scale
     int cpc;                      // channels per CTA in the fast K_A (guide tile reuse)
     int dbg;                      // development: bitmask of K_A stages to skip (timing only)
+    int identity;                 // 1: identity pansharpening prior (pansharpen.cpp:28-78), 0: Laplacian
     // row-strip domain decomposition (distributed CG, csrc/dist.cu); defaults = whole image:
     int grow0, Hg;                // global row of local row 0 (mod Hg), global height
     int rlo, rhi;                 // local rows owned by this strip: CG dot products sum only these

@@ -51,7 +51,7 @@ _ERR = {1: ParamError, 2: DimensionError, 3: NumericalError, 4: DeviceError}
 
 class _PsParams(C.Structure):
     _fields_ = [("lambda_", C.c_double), ("radius", C.c_int), ("eps", C.c_double), ("cg_tol", C.c_double),
-                ("cg_max_iter", C.c_int), ("threads", C.c_int)]
+                ("cg_max_iter", C.c_int), ("threads", C.c_int), ("prior", C.c_int)]
 
 
 class _KeParams(C.Structure):
@@ -72,16 +72,21 @@ class _Stats(C.Structure):
 
 @dataclass
 class PansharpenParams:
-    """pansharpen.hpp:15-26 (Laplacian prior)."""
+    """pansharpen.hpp:15-26; prior: "laplacian" (default) or "identity" (PriorKind, :11)."""
     lambda_: float = 2e-4
     radius: int = 1
     eps: float = 1e-4
     cg_tol: float = 5e-5
     cg_max_iter: int = 2000
     threads: int = 0
+    prior: str = "laplacian"
 
     def c(self):
-        return _PsParams(self.lambda_, self.radius, self.eps, self.cg_tol, self.cg_max_iter, self.threads)
+        kinds = {"laplacian": 0, "identity": 1, "custom": 2}
+        if self.prior not in kinds:
+            raise ParamError("pansharpen: unknown prior kind")
+        return _PsParams(self.lambda_, self.radius, self.eps, self.cg_tol, self.cg_max_iter, self.threads,
+                         kinds[self.prior])
 
 
 @dataclass

@@ -48,7 +48,8 @@ fbmp_gpu_ctx* ctx() {
 }
 
 fbmp_ps_params to_c(const PansharpenParams& p) {
-    return fbmp_ps_params{p.lambda, p.radius, p.eps, p.cg_tol, p.cg_max_iter, p.threads};
+    return fbmp_ps_params{p.lambda, p.radius, p.eps, p.cg_tol, p.cg_max_iter, p.threads,
+                          p.prior == PriorKind::identity ? 1 : (p.prior == PriorKind::custom ? 2 : 0)};
 }
 fbmp_ke_params to_c(const KernelEstParams& p) {
     return fbmp_ke_params{p.n, p.alpha1, p.alpha2, p.mu1, p.mu2, p.mu3, p.rho, p.t_max, p.th,
@@ -62,9 +63,9 @@ std::vector<double> stack(const MultiBandImage& img) {
     return v;
 }
 
-void require_laplacian(const PansharpenParams& p) {
-    if (p.prior != PriorKind::laplacian)
-        throw ParamError("pansharpen: the GPU path implements the Laplacian prior (LLP) only");
+void require_laplacian(const PansharpenParams& p) {  // the device path: Laplacian and identity priors
+    if (p.prior == PriorKind::custom)
+        throw ParamError("pansharpen: the GPU path implements the Laplacian and identity priors (no custom prior)");
 }
 
 Plane sq(const Plane& a) {

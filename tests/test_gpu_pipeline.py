@@ -450,3 +450,39 @@ def test_kernel_tv_degenerate_and_hook(gpu, orc):
     _, _, full = gpu.estimate_kernel_tv_plane(sc.pan, obs, 4, gpu.KernelEstParams(n=5, t_max=3), want_state=True)
     # the hook state of iteration 3 holds the u of 3 completed iterations
     assert rel(st["u"], full["u"]) < 1e-12
+
+
+def test_pansharpen_identity_prior_matches_oracle(gpu, orc):
+    """PriorKind::identity (pansharpen.cpp:28-78: guide = pan_n, A = B^T U^T U B + lambda M, guided
+    filter on z0, alias-group symbol 1) on the PR1 scene: identical CG counts, fp64 gate."""
+    sc = synth.make_scene("C1")
+    k = sc.kernel
+    out_o, it_o = orc.pansharpen(sc.lrms, sc.pan, k, 4, prior=1, threads=4)
+    out_g, it_g = gpu.pansharpen(sc.lrms, sc.pan, k, 4, gpu.PansharpenParams(prior="identity"), return_iters=True)
+    assert list(it_g) == list(it_o)
+    assert rel(out_g, out_o) < TOL
+    out_l = gpu.pansharpen(sc.lrms, sc.pan, k, 4)
+    assert rel(out_g, out_l) > 1e-6  # a different prior, a different HRMS
+
+
+def test_identity_prior_operators_match_oracle(gpu, orc):
+    """The identity prior's warm start (converged) and alias-group FFT solve against the oracle."""
+    rng = np.random.default_rng(7)
+    pan = rng.uniform(0, 1, (64, 64))
+    M = orc.Matting(pan, 1, 1e-4)
+    k = simplex_kernel(rng, 7)
+    x = rng.uniform(0, 1, (16, 16))
+    prm = gpu.PansharpenParams(prior="identity", cg_tol=1e-13)
+    zo, _, _, _ = orc.warmstart_cg(x, k, 4, M, cg_tol=1e-13, max_iters=5000, prior=1)
+    zg, _, _ = gpu.warmstart_cg(x, k, 4, gpu.MattingMatrix(pan, 1, 1e-4), prm, max_iters=5000)
+    assert rel(zg, zo) < 1e-9
+    v = rng.uniform(-0.5, 0.5, (64, 64))
+    assert rel(gpu.solve_channel_fft(x, k, 4, v, gpu.PansharpenParams(prior="identity")),
+               orc.solve_channel_fft(x, k, 4, v, 2e-4, prior=1)) < 1e-10
+
+
+def test_prior_kind_errors(gpu):
+    sc = synth.make_scene("C1", hr=64)
+    with pytest.raises(gpu.ParamError, match="custom prior requires a kernel"):
+        gpu.pansharpen(sc.lrms, sc.pan, sc.kernel[:7, :7] / sc.kernel[:7, :7].sum(), 4,
+                       gpu.PansharpenParams(prior="custom"))

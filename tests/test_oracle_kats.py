@@ -224,6 +224,41 @@ def test_warmstart_dense_solve(orc):  # :144-170
     assert np.linalg.norm(z0.ravel() - sol) <= 1e-6 * np.linalg.norm(sol)
 
 
+def test_warmstart_dense_solve_identity_prior(orc):  # :144-170 with PriorKind::identity (pansharpen.cpp:28-50)
+    rng = np.random.default_rng(166)
+    pan = rng.uniform(0, 1, (8, 8))
+    M = orc.Matting(pan, 1, 1e-4)  # the identity prior's guide is pan_n itself
+    k = simplex_kernel(rng, 3)
+    x = rng.uniform(0, 1, (4, 4))
+    z0, _, _, _ = orc.warmstart_cg(x, k, 2, M, lam=0.01, cg_tol=1e-13, max_iters=20000, error_on_cap=False, prior=1)
+    A = dense(lambda z: orc.conv(orc.upsample_adjoint(orc.downsample(orc.conv(z, k), 2), 2), k, adjoint=True)
+              + M.apply(z) * 0.01, 8, 8)
+    rhs = orc.conv(orc.upsample_adjoint(x, 2), k, adjoint=True).ravel()
+    sol = np.linalg.lstsq(A, rhs, rcond=None)[0]
+    assert np.linalg.norm(z0.ravel() - sol) <= 1e-6 * np.linalg.norm(sol)
+
+
+def test_solve_fft_identity_prior_normal_equations(orc):  # :265-279 with the identity prior's symbol 1
+    rng = np.random.default_rng(171)
+    for factor in (1, 2):
+        x, v = rng.uniform(0, 1, (8 // factor, 8 // factor)), rng.uniform(-0.5, 0.5, (8, 8))
+        k = simplex_kernel(rng, 3)
+        z = orc.solve_channel_fft(x, k, factor, v, 0.05, prior=1)
+        lhs = orc.conv(orc.upsample_adjoint(orc.downsample(orc.conv(z, k), factor), factor), k, adjoint=True) + z * 0.05
+        rhs = orc.conv(orc.upsample_adjoint(x, factor), k, adjoint=True) + v * 0.05
+        assert np.linalg.norm(lhs - rhs) <= 1e-10 * np.linalg.norm(rhs)
+
+
+def test_pansharpen_identity_prior_equal_bands(orc):  # :350-361 with PriorKind::identity
+    sc = synth.make_scene("C1", hr=32)
+    lr = np.stack([sc.lrms[0]] * 3)
+    k = simplex_kernel(np.random.default_rng(5), 5)
+    out, _ = orc.pansharpen(lr, sc.pan, k, 4, prior=1, threads=1)
+    outl, _ = orc.pansharpen(lr, sc.pan, k, 4, prior=0, threads=1)
+    assert np.abs(out[0] - out[1]).max() == 0.0 and np.abs(out[0] - out[2]).max() == 0.0
+    assert rel(out, outl) > 1e-6  # a different prior, a different HRMS
+
+
 def test_warmstart_cap(orc):  # :172-183
     rng = np.random.default_rng(67)
     pan = rng.uniform(0, 1, (16, 16))

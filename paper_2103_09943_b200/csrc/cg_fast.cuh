@@ -372,6 +372,8 @@ struct Args {
     const T* pold;  // p_old plane (CG)
     T* pnew;        // p plane written (CG)
     T* qc;          // q plane of the channel
+    double* qrow;   // ||q||^2 partials of the channel's (LR row, band) segments, at this band
+    int nbands;
     T beta;
     int H, W, h, w, rlo, rhi;
     int i0, i1, j0;      // strip rows [i0, i1), band origin
@@ -381,7 +383,7 @@ struct Args {
 // one warp's stream of HR rows y = 4 s + WP, s in [s0, s1)
 template <int N_, int MJ, bool CG, int WP, class T>
 __device__ __forceinline__ double rows(const Args<T>& A, const T* sk, T* tt, T* ring, T* pl,
-                                       T* slots, unsigned long long* bar, int lane, int warp) {
+                                       T* slots, unsigned long long* bar, int lane, int warp, double& qq) {
     using Q = Geo<N_, MJ, T>;
     constexpr int C = Q::C, g = Q::g, gp = Q::gp, RW = Q::RW, PLS = Q::PLS, TWL = Q::TWL, D = Q::D, K = Q::K;
     constexpr int DMIN = -((C - WP) / 4);  // ceil((WP - C) / 4)
@@ -542,8 +544,20 @@ __device__ __forceinline__ double rows(const Args<T>& A, const T* sk, T* tt, T* 
                 const v2<T> a0 = ld2(sb + m), a1 = ld2(sb + TWL + m), a2 = ld2(sb + 2 * TWL + m),
                             a3 = ld2(sb + 3 * TWL + m);
                 const v2<T> val = mk2(((a0.x + a1.x) + a2.x) + a3.x, ((a0.y + a1.y) + a2.y) + a3.y);
-                if (j + m + 1 < A.w) st2(A.qc + static_cast<size_t>(i) * A.w + j + m, val);
-                else if (j + m < A.w) A.qc[static_cast<size_t>(i) * A.w + j + m] = val.x;
+                if (j + m + 1 < A.w) {
+                    st2(A.qc + static_cast<size_t>(i) * A.w + j + m, val);
+                    // ||q||^2 = p . B^T U D B p (the data part of p.Ap on the fused K_L / K_DU path)
+                    if (CG) qq += static_cast<double>(val.x) * static_cast<double>(val.x) +
+                                  static_cast<double>(val.y) * static_cast<double>(val.y);
+                } else if (j + m < A.w) {
+                    A.qc[static_cast<size_t>(i) * A.w + j + m] = val.x;
+                    if (CG) qq += static_cast<double>(val.x) * static_cast<double>(val.x);
+                }
+            }
+            if (CG) {  // one partial per (LR row, band): the ||q||^2 tree does not depend on the strips
+                const double rq = warp_sum(qq);
+                if (lane == 0) A.qrow[static_cast<size_t>(i) * A.nbands] = rq;
+                qq = 0.0;
             }
         }
     }
@@ -557,7 +571,7 @@ __global__ void __launch_bounds__(q3::NTH, FBMP_KQ3_MINB) k_q3(PsGeo G, const T*
                                                    T* __restrict__ q, CgState* st, double* __restrict__ part,
                                                    int nblk) {
     using Q = q3::Geo<N_, MJ, T>;
-    __shared__ double red[q3::NW + 1];
+    __shared__ double red[2 * (q3::NW + 1)];
     extern __shared__ __align__(16) unsigned char smraw[];
     T* sm = reinterpret_cast<T*>(smraw);
     const int ch = blockIdx.y;
@@ -591,6 +605,8 @@ __global__ void __launch_bounds__(q3::NTH, FBMP_KQ3_MINB) k_q3(PsGeo G, const T*
     const int SR = (G.h + nstrips - 1) / nstrips;
     const int band = blockIdx.x % nbands, strip = blockIdx.x / nbands;
     A.j0 = band * Q::TWL;
+    A.nbands = nbands;
+    A.qrow = part + static_cast<size_t>(G.N) * nblk + static_cast<size_t>(ch) * G.h * nbands + band;
     A.i0 = strip * SR;
     A.i1 = min(A.i0 + SR, G.h);
     A.s0 = A.i0 - Q::g;
@@ -606,21 +622,28 @@ __global__ void __launch_bounds__(q3::NTH, FBMP_KQ3_MINB) k_q3(PsGeo G, const T*
     }
     __syncthreads();  // taps and barriers
     T* tt = sm + Q::O_TT + warp * Q::TT;
-    double pp;
+    double pp, qq = 0.0;
     switch (warp) {
-    case 0: pp = q3::rows<N_, MJ, CG, 0, T>(A, sk, tt, ring, pl, slots, bar, lane, warp); break;
-    case 1: pp = q3::rows<N_, MJ, CG, 1, T>(A, sk, tt, ring, pl, slots, bar, lane, warp); break;
-    case 2: pp = q3::rows<N_, MJ, CG, 2, T>(A, sk, tt, ring, pl, slots, bar, lane, warp); break;
-    default: pp = q3::rows<N_, MJ, CG, 3, T>(A, sk, tt, ring, pl, slots, bar, lane, warp); break;
+    case 0: pp = q3::rows<N_, MJ, CG, 0, T>(A, sk, tt, ring, pl, slots, bar, lane, warp, qq); break;
+    case 1: pp = q3::rows<N_, MJ, CG, 1, T>(A, sk, tt, ring, pl, slots, bar, lane, warp, qq); break;
+    case 2: pp = q3::rows<N_, MJ, CG, 2, T>(A, sk, tt, ring, pl, slots, bar, lane, warp, qq); break;
+    default: pp = q3::rows<N_, MJ, CG, 3, T>(A, sk, tt, ring, pl, slots, bar, lane, warp, qq); break;
     }
     if (CG) {
+        // ||p||^2 partials at part[ch][blk]; ||q||^2 partials per (LR row, band) behind them
         const double bs = block_sum<q3::NTH>(pp, red);
         if (threadIdx.x == 0) part[static_cast<size_t>(ch) * nblk + blockIdx.x] = bs;
         if (elect_last_block(&st[ch].cnt_q, nblk)) {
-            const double tot = sum_partials<q3::NTH>(part + static_cast<size_t>(ch) * nblk, nblk, 1, red);
+            const int nseg = G.h * nbands;
+            const double* pq2 = part + static_cast<size_t>(G.N) * nblk + static_cast<size_t>(ch) * nseg;
+            double s0 = 0.0, s1 = 0.0;
+            for (int i = threadIdx.x; i < nblk; i += q3::NTH) s0 += __ldcg(part + static_cast<size_t>(ch) * nblk + i);
+            for (int i = threadIdx.x; i < nseg; i += q3::NTH) s1 += __ldcg(pq2 + i);
+            const double2 tot = block_sum2<q3::NTH>(s0, s1, red);
             if (threadIdx.x == 0) {
-                if (G.dred) G.dred[G.N + 3 * ch] = tot;
-                else st[ch].pp = tot;
+                if (G.dred) G.dred[G.N + 3 * ch] = tot.x;
+                else st[ch].pp = tot.x;
+                st[ch].qq = tot.y;
                 st[ch].cnt_q = 0;
             }
         }
@@ -1301,6 +1324,313 @@ __global__ void __launch_bounds__(NT, FBMP_KD_MINB) k_dterm(PsGeo G, const T* __
     }
 }
 
+__device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+    const unsigned int s = static_cast<unsigned int>(__cvta_generic_to_shared(sdst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+// one lane's column pair of a row: 16 bytes (double) through L2 only, 8 bytes (float) through L1
+__device__ __forceinline__ void cp_async_pair(double2* sdst, const double* gsrc) { cp_async16(sdst, gsrc); }
+__device__ __forceinline__ void cp_async_pair(float2* sdst, const float* gsrc) {
+    const unsigned int s = static_cast<unsigned int>(__cvta_generic_to_shared(sdst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc) : "memory");
+}
+
+// ------------------------------------------------------------------------------------------
+// K_DU (fused CG path, factor 4, image sides multiples of 32): the data term and the CG update in
+// one pass. d = B^T U q is formed per 32 x 32 HR tile with K_D's gather (q window in shared
+// memory, phase sub-kernel in registers, 4 cell rows per thread) and consumed in registers:
+// Ap = d + lambda w (w = L M L p from K_L), z += alpha p, r -= alpha Ap (pansharpen.cpp:245-247),
+// ||r||^2, ||z||^2 and the relative-step stop test (:248-255). d and Ap are never written: the
+// iteration moves the 11 planes of SURVEY 8(d) and nothing else.
+//
+// Persistent: the work units are (active channel, tile), channel-major; CTA b owns a contiguous
+// range of them, so it builds its phase sub-kernel once per scene and pays no per-tile prologue.
+// A unit's q window and the z, r, p, w values of every thread's own four outputs stream into a
+// ring of NST shared-memory stages by cp.async, NST - 1 units ahead of their use, which keeps the
+// HBM loads in flight under the FP64 gather; one block barrier per unit publishes the window.
+// Every unit writes its (||r||^2, ||z||^2) partial to part[(ch, tile)]; the last CTA to arrive
+// on a channel sums the tiles in a fixed order, so the result does not depend on the partition.
+// ------------------------------------------------------------------------------------------
+#ifndef FBMP_DU_NST
+#define FBMP_DU_NST 3
+#endif
+namespace du {
+constexpr int NST = FBMP_DU_NST;             // ring depth
+constexpr int TW = 64, TH = 16;              // HR tile of a unit
+constexpr int WIN = 208;                     // q window slots of a stage (>= 21 x 9, 16-byte multiple)
+constexpr int STG = WIN + 16 * NT;           // elements per stage: window | {z, r, p, w} x 4 rows x NT threads
+constexpr int MAXCH = 512;                   // channels per launch (active-channel tables)
+template <class T>
+constexpr size_t smem() {
+    return (static_cast<size_t>(NST) * STG * sizeof(T) + 15) / 16 * 16 + 2 * (NT / 32) * 2 * sizeof(double) +
+           MAXCH * (sizeof(T) + 2 * sizeof(short));
+}
+__device__ __forceinline__ void cp_async_elem(double* sdst, const double* gsrc) {
+    const unsigned int s = static_cast<unsigned int>(__cvta_generic_to_shared(sdst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_elem(float* sdst, const float* gsrc) {
+    const unsigned int s = static_cast<unsigned int>(__cvta_generic_to_shared(sdst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gsrc) : "memory");
+}
+}  // namespace du
+
+template <int N_, class T = double>
+__global__ void __launch_bounds__(NT, 2) k_du(PsGeo G, const T* __restrict__ taps, const T* __restrict__ q,
+                                              const T* __restrict__ wv, T* __restrict__ z, T* __restrict__ r,
+                                              const T* __restrict__ pbuf, CgState* st, double* __restrict__ part,
+                                              int ntile) {
+    using namespace a4;
+    constexpr int CF = 4;
+    using D = DT<N_, CF>;
+    constexpr int DM = D::DM;
+    constexpr int TW = du::TW, TH = du::TH;  // tile: 64 x 16 HR pixels (512-byte row pieces)
+    constexpr int QLO = cfloordiv(CF - 1 - D::C, CF);
+    constexpr int QWC = cfloordiv(TW - 1 + D::C, CF) - QLO + 1;  // window columns
+    constexpr int QWR = cfloordiv(TH - 1 + D::C, CF) - QLO + 1;  // window rows
+    constexpr int QNC = QWC * QWR;
+    static_assert(QNC <= du::WIN && QNC <= NT, "q window");
+    extern __shared__ __align__(16) unsigned char smraw[];
+    __shared__ double red[2 * (NT / 32 + 1)];
+    __shared__ int s_nact, s_last;
+    T* stg = reinterpret_cast<T*>(smraw);
+    double* wred = reinterpret_cast<double*>(smraw + (static_cast<size_t>(du::NST) * du::STG * sizeof(T) + 15) / 16 * 16);
+    T* s_alpha = reinterpret_cast<T*>(wred + 2 * (NT / 32) * 2);
+    short* s_act = reinterpret_cast<short*>(s_alpha + du::MAXCH);
+    short* s_par = s_act + du::MAXCH;
+    const int W = G.W, n = G.n;
+    const size_t P = static_cast<size_t>(G.H) * W, pl = static_cast<size_t>(G.h) * G.w;
+    const int ntx = W / TW;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // the thread's four outputs of a tile (CF rows apart) and its phase
+    constexpr int CW4 = TW / CF, RB4 = TH / CF / 4;
+    static_assert(CF * CW4 * RB4 * CF == NT, "one thread per (column, row phase, group of 4 cell rows)");
+    const int pc = threadIdx.x % CF;
+    const int Jc = (threadIdx.x / CF) % CW4;
+    const int rest = threadIdx.x / (CF * CW4);
+    const int Ic0 = (rest % RB4) * 4;
+    const int pr = rest / RB4;
+    const size_t toff = static_cast<size_t>(Ic0 * CF + pr) * W + Jc * CF + pc;  // within the tile
+    const size_t rstep = static_cast<size_t>(CF) * W;
+    const int qoff = (Ic0 + D::DLO - QLO) * QWC + (Jc + D::DLO - QLO);
+    const int wa = threadIdx.x / QWC, wb = threadIdx.x - wa * QWC;  // window element copied by this thread
+    const T lam = static_cast<T>(G.lambda);
+    pdl_wait();  // w, alpha and the flags come from K_L
+    pdl_trigger();
+    // active channels (ascending), their p parity and alpha
+    if (warp == 0) {
+        int na = 0;
+        for (int base = 0; base < G.N; base += 32) {
+            const int c = base + lane;
+            const bool on = c < G.N && st[c].done == 0;
+            const unsigned int mk = __ballot_sync(0xffffffffu, on);
+            if (on) {
+                const int pos = na + __popc(mk & ((1u << lane) - 1u));
+                s_act[pos] = static_cast<short>(c);
+                s_par[pos] = static_cast<short>(st[c].t & 1);
+                s_alpha[pos] = static_cast<T>(st[c].alpha);
+            }
+            na += __popc(mk);
+        }
+        if (lane == 0) s_nact = na;
+    }
+    __syncthreads();
+    const int nact = s_nact;
+    if (nact == 0) return;
+    // CTA b owns the contiguous units [b per, (b + 1) per): consecutive tiles of a tile row, so the
+    // units in flight continue the same DRAM rows (measured: interleaving the CTAs' units over the
+    // image is 7-10 % slower)
+    const long long U = static_cast<long long>(nact) * ntile;
+    const int per = static_cast<int>((U + gridDim.x - 1) / gridDim.x);
+    const long long a0 = static_cast<long long>(blockIdx.x) * per;
+    const int nu = a0 >= U ? 0 : static_cast<int>(min(static_cast<long long>(per), U - a0));
+    // issue side: unit j -> stage j % NST
+    int ki = static_cast<int>(a0 / ntile), ti = static_cast<int>(a0 - static_cast<long long>(ki) * ntile);
+    auto issue = [&](int stage) {
+        const int ch = s_act[ki];
+        const int by = ti / ntx, bx = ti - by * ntx;
+        const int r0 = by * TH, c0 = bx * TW;
+        T* sd = stg + stage * du::STG;
+        if (threadIdx.x < QNC) {
+            const int iq0 = (r0 >> 2) + QLO, jq0 = (c0 >> 2) + QLO;
+            du::cp_async_elem(sd + threadIdx.x, q + static_cast<size_t>(ch) * pl +
+                                                    static_cast<size_t>(wrap_once(iq0 + wa, G.h)) * G.w +
+                                                    wrap_once(jq0 + wb, G.w));
+        }
+        const size_t off = static_cast<size_t>(r0) * W + c0 + toff;
+        const T* zc = z + ch * P + off;
+        const T* rc = r + ch * P + off;
+        const T* pcp = pbuf + (static_cast<size_t>(s_par[ki]) * G.N + ch) * P + off;
+        const T* wc = wv + ch * P + off;
+        sd += du::WIN + threadIdx.x;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            du::cp_async_elem(sd + (0 * 4 + k) * NT, zc + k * rstep);
+            du::cp_async_elem(sd + (1 * 4 + k) * NT, rc + k * rstep);
+            du::cp_async_elem(sd + (2 * 4 + k) * NT, pcp + k * rstep);
+            du::cp_async_elem(sd + (3 * 4 + k) * NT, wc + k * rstep);
+        }
+        if (++ti == ntile) {
+            ti = 0;
+            ++ki;
+        }
+    };
+#pragma unroll
+    for (int j = 0; j < du::NST - 1; ++j) {
+        if (j < nu) issue(j);
+        cp_async_commit();
+    }
+    int kc = static_cast<int>(a0 / ntile), tc = static_cast<int>(a0 - static_cast<long long>(kc) * ntile);
+    int kprev = 0, tprev = 0;
+    int cur_scene = -1;
+    T kreg[DM][DM];
+    for (int j = 0; j < nu; ++j) {
+        cp_async_wait<du::NST - 2>();  // this thread's copies of unit j have landed
+        __syncthreads();               // ... everyone's (the window); unit j - 1 is consumed by all
+        if (j + du::NST - 1 < nu) issue((j + du::NST - 1) % du::NST);
+        cp_async_commit();
+        // per-tile partial of the previous unit (its warp sums are published by the barrier above)
+        if (j > 0 && threadIdx.x == 0) {
+            const double* wr = wred + ((j - 1) & 1) * (NT / 32) * 2;
+            double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+            for (int wi = 0; wi < NT / 32; ++wi) {
+                s0 += wr[2 * wi];
+                s1 += wr[2 * wi + 1];
+            }
+            double* pd = part + (static_cast<size_t>(s_act[kprev]) * ntile + tprev) * 2;
+            pd[0] = s0;
+            pd[1] = s1;
+        }
+        const int ch = s_act[kc];
+        const int scene = ch / G.cps;
+        if (scene != cur_scene) {  // phase sub-kernel of the scene's taps
+            cur_scene = scene;
+            const T* tp = taps + static_cast<size_t>(scene) * n * n;
+#pragma unroll
+            for (int a = 0; a < DM; ++a)
+#pragma unroll
+                for (int b = 0; b < DM; ++b) {
+                    const int tr = CF * (a + D::DLO) - pr + D::C, tcc = CF * (b + D::DLO) - pc + D::C;
+                    kreg[a][b] = (tr >= 0 && tr < N_ && tcc >= 0 && tcc < N_) ? __ldg(tp + tr * N_ + tcc) : T(0);
+                }
+        }
+        const T* sd = stg + (j % du::NST) * du::STG;
+        // d of the thread's four outputs (K_D's gather: ascending (mm, b) per accumulator)
+        const T* qa = sd + qoff;
+        T acc[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int mm = 0; mm < DM + 3; ++mm) {
+            T qv[DM];
+#pragma unroll
+            for (int b = 0; b < DM; ++b) qv[b] = qa[mm * QWC + b];
+#pragma unroll
+            for (int b = 0; b < DM; ++b)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int a = mm - k;
+                    if (a >= 0 && a < DM) acc[k] = fma(kreg[a][b], qv[b], acc[k]);
+                }
+        }
+        const T alpha = s_alpha[kc];
+        const T* sv = sd + du::WIN + threadIdx.x;
+        const int by = tc / ntx, bx = tc - by * ntx;
+        const size_t off = static_cast<size_t>(by * TH) * W + bx * TW + toff;
+        T* zc = z + ch * P + off;
+        T* rc = r + ch * P + off;
+        double rr = 0.0, zz = 0.0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const T z0 = sv[(0 * 4 + k) * NT], r0v = sv[(1 * 4 + k) * NT], p0 = sv[(2 * 4 + k) * NT],
+                    w0 = sv[(3 * 4 + k) * NT];
+            const T ap = acc[k] + w0 * lam;      // pansharpen.cpp:222-223
+            const T zn = z0 + p0 * alpha;        // :245
+            const T rn = r0v - ap * alpha;       // :246
+            __stcs(zc + k * rstep, zn);
+            __stcs(rc + k * rstep, rn);
+            rr += static_cast<double>(rn) * static_cast<double>(rn);
+            zz += static_cast<double>(zn) * static_cast<double>(zn);
+        }
+        rr = warp_sum(rr);
+        zz = warp_sum(zz);
+        if (lane == 0) {
+            double* wr = wred + (j & 1) * (NT / 32) * 2;
+            wr[2 * warp] = rr;
+            wr[2 * warp + 1] = zz;
+        }
+        kprev = kc;
+        tprev = tc;
+        if (++tc == ntile) {
+            tc = 0;
+            ++kc;
+        }
+    }
+    __syncthreads();
+    if (nu > 0 && threadIdx.x == 0) {  // the last unit's partial
+        const double* wr = wred + ((nu - 1) & 1) * (NT / 32) * 2;
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int wi = 0; wi < NT / 32; ++wi) {
+            s0 += wr[2 * wi];
+            s1 += wr[2 * wi + 1];
+        }
+        double* pd = part + (static_cast<size_t>(s_act[kprev]) * ntile + tprev) * 2;
+        pd[0] = s0;
+        pd[1] = s1;
+        __threadfence();
+    }
+    if (nu == 0) return;
+    // arrival on every channel this CTA has units of (thread i: i-th active channel); the last of a
+    // channel's CTAs closes its iteration
+    __shared__ unsigned char s_fin[du::MAXCH];
+    __syncthreads();  // thread 0's partials are fenced
+    for (int i = threadIdx.x; i < nact; i += NT) {
+        const long long u0 = static_cast<long long>(i) * ntile;
+        unsigned char fin = 0;
+        if (u0 < a0 + nu && u0 + ntile > a0) {
+            const unsigned int touch = static_cast<unsigned int>((u0 + ntile - 1) / per - u0 / per + 1);
+            const unsigned int prev = atomicAdd(&st[s_act[i]].cnt_u, 1u);
+            if (prev == touch - 1u) {
+                __threadfence();
+                fin = 1;
+            }
+        }
+        s_fin[i] = fin;
+    }
+    __syncthreads();
+    for (int i = 0; i < nact; ++i) {
+        if (!s_fin[i]) continue;  // block-uniform
+        const int ch = s_act[i];
+        const double2 tot = sum_partials2<NT>(part + static_cast<size_t>(ch) * ntile * 2, ntile, red);
+        if (threadIdx.x == 0) {
+            CgState& S = st[ch];
+            const double rs_new = tot.x, zsq = tot.y;
+            const int t = S.t;
+            const double step = fabs(S.alpha) * sqrt(S.pp);
+            S.zz = zsq;
+            if (step <= S.cg_tol * fmax(sqrt(zsq), 1e-300)) {
+                S.done = 1;
+                S.iters = t + 1;
+            } else {
+                S.beta = rs_new / S.rs;
+                S.rs = rs_new;
+                S.t = t + 1;
+                if (S.t >= S.max_iters) {
+                    S.done = 3;
+                    S.iters = S.max_iters;
+                }
+            }
+            S.cnt_u = 0;
+        }
+    }
+}
+
 // blockIdx.x = (scene, item = (band, strip), channel of the scene), channel fastest
 template <bool CG>
 __global__ void __launch_bounds__(kl::NTL, 16) k_llp(PsGeo G, const double* __restrict__ guide,
@@ -1483,26 +1813,12 @@ constexpr int BAND2 = 56;
 #define FBMP_KL_UNROLL 3
 #endif
 constexpr int KL_UNROLL = FBMP_KL_UNROLL;
-__device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
-__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
-    const unsigned int s = static_cast<unsigned int>(__cvta_generic_to_shared(sdst));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
-// one lane's column pair of a row: 16 bytes (double) through L2 only, 8 bytes (float) through L1
-__device__ __forceinline__ void cp_async_pair(double2* sdst, const double* gsrc) { cp_async16(sdst, gsrc); }
-__device__ __forceinline__ void cp_async_pair(float2* sdst, const float* gsrc) {
-    const unsigned int s = static_cast<unsigned int>(__cvta_generic_to_shared(sdst));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc) : "memory");
-}
-
 // LAP = false: the identity pansharpening prior (pansharpen.cpp:28-50): Ap = d + lambda M p (the
 // S1 and S5 Laplacians become copies; everything else, including the row pipeline, is unchanged)
-template <bool CG, class T = double, bool LAP = true>
+// DIN = false (fused path, CG only): d is not read; the kernel writes w = L M L p (unscaled) and
+// sums p.w, and p.Ap = ||q||^2 + lambda p.w with ||q||^2 from K_Q3 (p . B^T U D B p = |D B p|^2);
+// K_DU forms Ap = d + lambda w while it updates z and r.
+template <bool CG, class T = double, bool LAP = true, bool DIN = true>
 __global__ void __launch_bounds__(kl::NTL, FBMP_KL_MINB) k_llp2(PsGeo G, const T* __restrict__ guide,
                                                      const T* __restrict__ wmu, const T* __restrict__ wg,
                                                      const T* __restrict__ pin, T* __restrict__ out,
@@ -1582,8 +1898,11 @@ __global__ void __launch_bounds__(kl::NTL, FBMP_KL_MINB) k_llp2(PsGeo G, const T
             cp_async_pair(&ring[slot][1][lane], reinterpret_cast<const T*>(Ib + io1));
             cp_async_pair(&ring[slot][2][lane], reinterpret_cast<const T*>(MUb + io2));
             cp_async_pair(&ring[slot][3][lane], reinterpret_cast<const T*>(GKb + io2));
-            cp_async_pair(&ring[slot][4][lane], reinterpret_cast<const T*>(ocb + io4));
-            io0 = advb(io0); io1 = advb(io1); io2 = advb(io2); io4 = advb(io4);
+            if constexpr (DIN) {
+                cp_async_pair(&ring[slot][4][lane], reinterpret_cast<const T*>(ocb + io4));
+                io4 = advb(io4);
+            }
+            io0 = advb(io0); io1 = advb(io1); io2 = advb(io2);
         };
 #pragma unroll
         for (int j = 0; j < NB - 1; ++j) {
@@ -1597,7 +1916,9 @@ __global__ void __launch_bounds__(kl::NTL, FBMP_KL_MINB) k_llp2(PsGeo G, const T
             cp_async_wait<NB - 1>();  // the group of step st_i has landed
             const int slot = st_i % NB;
             const V p0 = ring[slot][0][lane], Im1 = ring[slot][1][lane], mu2 = ring[slot][2][lane],
-                    g2 = ring[slot][3][lane], d4 = ring[slot][4][lane];
+                    g2 = ring[slot][3][lane];
+            V d4 = {0, 0};
+            if constexpr (DIN) d4 = ring[slot][4][lane];
             const int o4c = o4;
             o4 = adv(o4);
             // S1 at row Y-1 (ops.cpp:70-78 order: 4 c - up - down - left - right)
@@ -1648,7 +1969,7 @@ __global__ void __launch_bounds__(kl::NTL, FBMP_KL_MINB) k_llp2(PsGeo G, const T
                 t0 = M_b.x;
                 t1 = M_b.y;
             }
-            const V val = mk2(d4.x + t0 * lam, d4.y + t1 * lam);
+            const V val = DIN ? mk2(d4.x + t0 * lam, d4.y + t1 * lam) : mk2(t0, t1);
             if (st_i >= 2 * HALO) {
                 if (writer) {
                     st2(oc + o4c, val);
@@ -1687,12 +2008,13 @@ __global__ void __launch_bounds__(kl::NTL, FBMP_KL_MINB) k_llp2(PsGeo G, const T
             double sacc = 0.0;
 #pragma unroll 8
             for (int i = lane; i < nbands * nrb; i += 32) sacc += __ldcg(pa + i);
-            const double pAp = warp_sum(sacc);
+            double pAp = warp_sum(sacc);
             if (lane == 0 && G.dred) {  // distributed: publish the local sum only
                 G.dred[ch] = pAp;
                 st[ch].cnt_a = 0;
             } else if (lane == 0) {
                 CgState& S = st[ch];
+                if constexpr (!DIN) pAp = S.qq + G.lambda * pAp;
                 S.pAp = pAp;
                 if (!(pAp > 0)) {  // pansharpen.cpp:240-244
                     S.done = (sqrt(S.rs) <= 1e-12 * S.rhs_norm) ? 1 : 2;
@@ -1713,7 +2035,7 @@ __global__ void __launch_bounds__(kl::NTL, FBMP_KL_MINB) k_llp2(PsGeo G, const T
 namespace kl {
 constexpr int BAND4 = 120;  // output columns per warp of k_llp4f
 }
-template <bool CG>
+template <bool CG, bool DIN = true>
 __global__ void __launch_bounds__(kl::NTL, FBMP_KL_MINB) k_llp4f(PsGeo G, const float* __restrict__ guide,
                                                       const float* __restrict__ wmu, const float* __restrict__ wg,
                                                       const float* __restrict__ pin, float* __restrict__ out,
@@ -1777,8 +2099,11 @@ __global__ void __launch_bounds__(kl::NTL, FBMP_KL_MINB) k_llp4f(PsGeo G, const 
             cp_async16(&ring[slot][1][lane], I + io1);
             cp_async16(&ring[slot][2][lane], MU + io2);
             cp_async16(&ring[slot][3][lane], GK + io2);
-            cp_async16(&ring[slot][4][lane], oc + io4);
-            io0 = adv(io0); io1 = adv(io1); io2 = adv(io2); io4 = adv(io4);
+            if constexpr (DIN) {
+                cp_async16(&ring[slot][4][lane], oc + io4);
+                io4 = adv(io4);
+            }
+            io0 = adv(io0); io1 = adv(io1); io2 = adv(io2);
         };
 #pragma unroll
         for (int j = 0; j < NB - 1; ++j) {
@@ -1806,7 +2131,7 @@ __global__ void __launch_bounds__(kl::NTL, FBMP_KL_MINB) k_llp4f(PsGeo G, const 
             unpack4(ring[slot][1][lane], Im1);
             unpack4(ring[slot][2][lane], mu2);
             unpack4(ring[slot][3][lane], g2);
-            unpack4(ring[slot][4][lane], d4);
+            if constexpr (DIN) unpack4(ring[slot][4][lane], d4);
             const int o4c = o4;
             o4 = adv(o4);
             // S1 at row Y-1 (ops.cpp:70-78 order: 4 c - up - down - left - right)
@@ -1850,7 +2175,7 @@ __global__ void __launch_bounds__(kl::NTL, FBMP_KL_MINB) k_llp4f(PsGeo G, const 
                 for (int j = 0; j < 4; ++j) {
                     const float l = j == 0 ? ML : M_b[j - 1], r = j == 3 ? MR : M_b[j + 1];
                     const float t = 4.0f * M_b[j] - M_a[j] - Mc[j] - l - r;
-                    val[j] = d4[j] + t * lam;
+                    val[j] = DIN ? d4[j] + t * lam : t;
                 }
                 if (st_i >= 2 * HALO) {
                     if (writer) {
@@ -1894,12 +2219,13 @@ __global__ void __launch_bounds__(kl::NTL, FBMP_KL_MINB) k_llp4f(PsGeo G, const 
             double sacc = 0.0;
 #pragma unroll 8
             for (int i = lane; i < nbands * nrb; i += 32) sacc += __ldcg(pa + i);
-            const double pAp = warp_sum(sacc);
+            double pAp = warp_sum(sacc);
             if (lane == 0 && G.dred) {
                 G.dred[ch] = pAp;
                 st[ch].cnt_a = 0;
             } else if (lane == 0) {
                 CgState& S = st[ch];
+                if constexpr (!DIN) pAp = S.qq + G.lambda * pAp;
                 S.pAp = pAp;
                 if (!(pAp > 0)) {  // pansharpen.cpp:240-244
                     S.done = (sqrt(S.rs) <= 1e-12 * S.rhs_norm) ? 1 : 2;

@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(NTU) k_cg_init(PsGeo G, const T* __restrict__ 
             CgState& S = st[ch];
             S.rs = tot;
             S.rhs_norm = sqrt(tot);
-            S.pp = S.pAp = S.alpha = S.beta = S.zz = 0.0;
+            S.pp = S.pAp = S.alpha = S.beta = S.zz = S.qq = 0.0;
             S.cg_tol = cg_tol;
             S.t = 0;
             S.iters = 0;
@@ -624,7 +624,7 @@ __global__ void __launch_bounds__(NTA) k_rhs(PsGeo G, const double* __restrict__
                 CgState& S = st[ch];
                 S.rs = tot;
                 S.rhs_norm = sqrt(tot);
-                S.pp = S.pAp = S.alpha = S.beta = S.zz = 0.0;
+                S.pp = S.pAp = S.alpha = S.beta = S.zz = S.qq = 0.0;
                 S.cg_tol = cg_tol;
                 S.t = 0;
                 S.iters = 0;
@@ -1746,6 +1746,50 @@ void launch_llp(Context& ctx, const PsGeo& G, const T* taps, const T* guide, con
     }
 }
 
+// Fused CG path (K_Q3 -> K_L without d -> K_DU): p.Ap = ||q||^2 + lambda p.(L M L p), and the
+// data term is formed inside the update kernel, so d and Ap never touch HBM (11 planes per
+// channel-iteration). Needs the streaming K_Q3 (it sums ||q||^2), the pair / quad K_L
+// and image sides that are multiples of the 32 x 32 tile. Env FBMP_DU=0 keeps K_D + K_L + K_U.
+template <class T>
+using DuFn = void (*)(PsGeo, const T*, const T*, const T*, T*, T*, const T*, CgState*, double*, int);
+template <class T>
+DuFn<T> du_select(const PsGeo& G) {
+    static const bool off = std::getenv("FBMP_DU") && std::atoi(std::getenv("FBMP_DU")) == 0;
+    if (off || G.c != 4 || G.dred || G.H % fast::du::TH || G.W % fast::du::TW || !use_llp() || G.N > fast::du::MAXCH)
+        return nullptr;
+    switch (G.n) {
+    case 21: return fast::k_du<21, T>;
+    case 17: return fast::k_du<17, T>;
+    case 15: return fast::k_du<15, T>;
+    case 7: return fast::k_du<7, T>;
+    default: return nullptr;
+    }
+}
+// K_L of the fused path: w = L M L p into `out`, p.Ap = qq + lambda p.w
+template <class T>
+void launch_llp_w(Context& ctx, const PsGeo& G, const T* guide, const T* mu, const T* gk, const T* p, T* out,
+                  CgState* st, double* part, bool pdl) {
+    const LlpPlan L = llp_plan<T>(ctx, G);
+    const dim3 grid(L.ctas * G.N), blk(fast::kl::NTL);
+    auto go = [&](auto fn) {
+        if (pdl)
+            launch_pdl(fn, grid, blk, 0, ctx.stream, G, guide, mu, gk, p, out, st, part, L.nb, L.k, L.R);
+        else
+            fn<<<grid, blk, 0, ctx.stream>>>(G, guide, mu, gk, p, out, st, part, L.nb, L.k, L.R);
+    };
+    if (G.identity) {
+        go(fast::k_llp2<true, T, false, false>);
+        return;
+    }
+    if constexpr (!std::is_same<T, double>::value) {
+        if (L.quads) {
+            go(fast::k_llp4f<true, false>);
+            return;
+        }
+    }
+    go(fast::k_llp2<true, T, true, false>);
+}
+
 // rhs = B^T U x into r through K_D, then the CG initialisation (fast path; k_rhs otherwise)
 template <class T = double>
 void launch_rhs_init(Context& ctx, const PsGeo& G, const T* taps, const T* x, CgBuffersT<T>& B, double* part,
@@ -1899,9 +1943,23 @@ void cg_solve_t(Context& ctx, const PsGeo& G, const T* d_taps, const double* d_g
     }
     double* part_init = B.part;
     double* part_q = part_init + static_cast<size_t>(N) * nba;
-    double* part_a = part_q + static_cast<size_t>(N) * nbq;
+    // K_Q3 also publishes ||q||^2 partials per (LR row, 64-column band) behind its ||p||^2 partials
+    const size_t nqseg = static_cast<size_t>(G.h) * ceil_div(G.w, 64);
+    double* part_a = part_q + static_cast<size_t>(N) * (nbq + nqseg);
     const int nbA = fastA && use_llp() ? std::max(nba, ceil_div(G.W, fast::kl::BAND) * ceil_div(G.H, fast::kl::RB)) : nba;  // >= k_llp2's
     double* part_u = part_a + static_cast<size_t>(N) * nbA;
+    // fused path: K_Q3 -> K_L (w, p.Ap from ||q||^2) -> K_DU (data term + update)
+    const DuFn<T> du = fastA && q2.fn && q2.streaming && llp_plan<T>(ctx, G).pairs ? du_select<T>(G) : nullptr;
+    const size_t sdu = du ? fast::du::smem<T>() : 0;
+    int du_ctas = 0;  // persistent K_DU: one CTA per resident slot
+    if (du) {
+        set_smem(du, sdu);
+        int per_sm = 0;
+        FBMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, du, fast::NT, sdu));
+        du_ctas = std::max(1, per_sm) * ctx.sm_count;
+    }
+    const int ntile_du = (G.W / fast::du::TW) * (G.H / fast::du::TH);
+    const int nbU = du ? std::max(nbu, ntile_du) : nbu;  // K_DU publishes one (rr, zz) pair per tile
     // counters must start at zero
     FBMP_CUDA(cudaMemsetAsync(B.st, 0, sizeof(CgState) * N, ctx.stream));
     if (fastA && (use_llp() || !F64)) {
@@ -1930,7 +1988,7 @@ void cg_solve_t(Context& ctx, const PsGeo& G, const T* d_taps, const double* d_g
     std::string key;
     {
         const void* ptrs[] = {d_taps, d_guide, wmu, wg, B.r, B.p, B.q, B.Ap, B.st, B.z, part_q, part_a, part_u,
-                              reinterpret_cast<const void*>(q2.fn)};
+                              reinterpret_cast<const void*>(q2.fn), reinterpret_cast<const void*>(du)};
         const long long dims[] = {nbq, nba, nbu, static_cast<long long>(sq), fastA ? 1 : 0, chunk,
                                   static_cast<long long>(sizeof(T))};
         key.append(reinterpret_cast<const char*>(&G), sizeof(G));
@@ -1954,7 +2012,7 @@ void cg_solve_t(Context& ctx, const PsGeo& G, const T* d_taps, const double* d_g
     };
     std::vector<Grp> grp(ngrp);
     {
-        const size_t per_ch = static_cast<size_t>(nba) + nbq + nbA + 2 * static_cast<size_t>(nbu);
+        const size_t per_ch = static_cast<size_t>(nba) + nbq + nqseg + nbA + 2 * static_cast<size_t>(nbU);
         for (int gi = 0; gi < ngrp; ++gi) {
             Grp& R = grp[gi];
             int c0, c1;
@@ -1995,7 +2053,7 @@ void cg_solve_t(Context& ctx, const PsGeo& G, const T* d_taps, const double* d_g
             } else {
                 double* base = B.part + c0 * per_ch;
                 R.pq = base;
-                R.pa = R.pq + static_cast<size_t>(ng) * nbq;
+                R.pa = R.pq + static_cast<size_t>(ng) * (nbq + nqseg);
                 R.pu = R.pa + static_cast<size_t>(ng) * nbA;
             }
         }
@@ -2037,6 +2095,19 @@ void cg_solve_t(Context& ctx, const PsGeo& G, const T* d_taps, const double* d_g
                     k_q<true><<<dim3(nbq, Ng), NTQ, sq, ctx.stream>>>(R.G, R.taps, R.B.r, R.B.p, R.B.q, R.B.st, R.pq,
                                                                        nbq);
                 if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * EV + 1], ctx.stream, cudaEventRecordExternal));
+                if (du) {
+                    if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * EV + 2], ctx.stream, cudaEventRecordExternal));
+                    launch_llp_w<T>(ctx, R.G, R.guide, R.mu, R.g, R.B.p, R.B.Ap, R.B.st, R.pa, (pdl_mask & 2) != 0);
+                    if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * EV + 3], ctx.stream, cudaEventRecordExternal));
+                    if (pdl_mask & 4)
+                        launch_pdl(du, dim3(du_ctas), dim3(fast::NT), sdu, ctx.stream, R.G, R.taps, R.B.q, R.B.Ap, R.B.z,
+                                   R.B.r, R.B.p, R.B.st, R.pu, ntile_du);
+                    else
+                        du<<<dim3(du_ctas), fast::NT, sdu, ctx.stream>>>(R.G, R.taps, R.B.q, R.B.Ap, R.B.z, R.B.r, R.B.p,
+                                                                        R.B.st, R.pu, ntile_du);
+                    if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * EV + 4], ctx.stream, cudaEventRecordExternal));
+                    continue;
+                }
                 if (fastA) {
                     launch_apply2<true, T>(ctx, R.G, R.taps, R.guide, R.mu, R.g, R.B.p, R.B.q, R.B.Ap, R.B.st, R.pa,
                                            (pdl_mask & 2) != 0, prof ? pev[it * EV + 2] : nullptr);
@@ -2085,7 +2156,7 @@ void cg_solve_t(Context& ctx, const PsGeo& G, const T* d_taps, const double* d_g
     };
     auto launch = [&](int slot) {
         FBMP_CUDA(cudaGraphLaunch(exec, ctx.stream));
-        ctx.count((fastA && (use_llp() || !F64) ? 4 : 3) * chunk * ngrp);  // kernel nodes of one chunk graph
+        ctx.count((fastA && !du && (use_llp() || !F64) ? 4 : 3) * chunk * ngrp);  // kernel nodes of one chunk graph
         FBMP_CUDA(cudaMemcpyAsync(pinned + slot * N, B.st, sizeof(CgState) * N, cudaMemcpyDeviceToHost, ctx.stream));
         FBMP_CUDA(cudaEventRecord(ev[slot], ctx.stream));
     };
@@ -2342,7 +2413,7 @@ __global__ void k_dist_init(CgState* st, const double* __restrict__ dred, int N,
     const double tot = dred[N + 3 * ch + 1];
     S.rs = tot;
     S.rhs_norm = sqrt(tot);
-    S.pp = S.pAp = S.alpha = S.beta = S.zz = 0.0;
+    S.pp = S.pAp = S.alpha = S.beta = S.zz = S.qq = 0.0;
     S.cg_tol = cg_tol;
     S.t = 0;
     S.iters = 0;
@@ -2417,7 +2488,7 @@ void cg_solve_strips(Context& ctx, std::vector<StripCg>& SS, const StripComm& co
     auto parts = [&](StripCg& S, double*& pi, double*& pq, double*& pa, double*& pu) {
         pi = S.B.part;
         pq = pi + static_cast<size_t>(N) * nba;
-        pa = pq + static_cast<size_t>(N) * nbq;
+        pa = pq + static_cast<size_t>(N) * (nbq + static_cast<size_t>(S.G.h) * ceil_div(S.G.w, 64));  // K_Q3: ||p||^2, ||q||^2 partials
         pu = pa + static_cast<size_t>(N) * nbA;
     };
     auto allreduce = [&](int off, int n) {

@@ -13,6 +13,7 @@ struct CgState {
     double alpha;     // rs / pAp (K_A)
     double beta;      // rs_new / rs for the next p update (K_U)
     double zz;        // ||z||^2 after the update (K_U)
+    double qq;        // ||q||^2 = p . B^T U D B p of the current iteration (K_Q3; fused K_L / K_DU path)
     double cg_tol;
     int t;            // iteration index
     int done;         // 0 running, 1 converged, 2 non-positive curvature, 3 iteration cap

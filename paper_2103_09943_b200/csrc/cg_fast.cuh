@@ -1362,22 +1362,27 @@ __device__ __forceinline__ void cp_async_pair(float2* sdst, const float* gsrc) {
 #endif
 namespace du {
 constexpr int NST = FBMP_DU_NST;             // ring depth
-constexpr int TW = 64, TH = 16;              // HR tile of a unit
+constexpr int TW = 32, TH = 32;              // HR tile of a unit (64 x 16 measured equal at C2, 2.5 % slower at C5)
 constexpr int WIN = 208;                     // q window slots of a stage (>= 21 x 9, 16-byte multiple)
-constexpr int STG = WIN + 16 * NT;           // elements per stage: window | {z, r, p, w} x 4 rows x NT threads
+constexpr int STG = WIN + 4 * TW * TH;       // elements per stage: window | z, r, p, w tiles
 constexpr int MAXCH = 512;                   // channels per launch (active-channel tables)
 template <class T>
 constexpr size_t smem() {
     return (static_cast<size_t>(NST) * STG * sizeof(T) + 15) / 16 * 16 + 2 * (NT / 32) * 2 * sizeof(double) +
            MAXCH * (sizeof(T) + 2 * sizeof(short));
 }
-__device__ __forceinline__ void cp_async_elem(double* sdst, const double* gsrc) {
-    const unsigned int s = static_cast<unsigned int>(__cvta_generic_to_shared(sdst));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc) : "memory");
+// one element to the 32-bit shared address sdst + OFF elements
+template <class T, int OFF>
+__device__ __forceinline__ void cp_async_elem(unsigned int sdst, const T* gsrc) {
+    if constexpr (sizeof(T) == 8)
+        asm volatile("cp.async.ca.shared.global [%0 + %2], [%1], 8;\n" ::"r"(sdst), "l"(gsrc), "n"(OFF * 8) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0 + %2], [%1], 4;\n" ::"r"(sdst), "l"(gsrc), "n"(OFF * 4) : "memory");
 }
-__device__ __forceinline__ void cp_async_elem(float* sdst, const float* gsrc) {
-    const unsigned int s = static_cast<unsigned int>(__cvta_generic_to_shared(sdst));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gsrc) : "memory");
+// 16 bytes through L2 only to the 32-bit shared address sdst + OFFB bytes
+template <int OFFB, class T>
+__device__ __forceinline__ void cp_async_chunk(unsigned int sdst, const T* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0 + %2], [%1], 16;\n" ::"r"(sdst), "l"(gsrc), "n"(OFFB) : "memory");
 }
 }  // namespace du
 
@@ -1390,7 +1395,7 @@ __global__ void __launch_bounds__(NT, 2) k_du(PsGeo G, const T* __restrict__ tap
     constexpr int CF = 4;
     using D = DT<N_, CF>;
     constexpr int DM = D::DM;
-    constexpr int TW = du::TW, TH = du::TH;  // tile: 64 x 16 HR pixels (512-byte row pieces)
+    constexpr int TW = du::TW, TH = du::TH;
     constexpr int QLO = cfloordiv(CF - 1 - D::C, CF);
     constexpr int QWC = cfloordiv(TW - 1 + D::C, CF) - QLO + 1;  // window columns
     constexpr int QWR = cfloordiv(TH - 1 + D::C, CF) - QLO + 1;  // window rows
@@ -1406,7 +1411,7 @@ __global__ void __launch_bounds__(NT, 2) k_du(PsGeo G, const T* __restrict__ tap
     short* s_par = s_act + du::MAXCH;
     const int W = G.W, n = G.n;
     const size_t P = static_cast<size_t>(G.H) * W, pl = static_cast<size_t>(G.h) * G.w;
-    const int ntx = W / TW;
+    const int ntx = W / TW, nty = G.H / TH;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // the thread's four outputs of a tile (CF rows apart) and its phase
     constexpr int CW4 = TW / CF, RB4 = TH / CF / 4;
@@ -1416,11 +1421,21 @@ __global__ void __launch_bounds__(NT, 2) k_du(PsGeo G, const T* __restrict__ tap
     const int rest = threadIdx.x / (CF * CW4);
     const int Ic0 = (rest % RB4) * 4;
     const int pr = rest / RB4;
-    const size_t toff = static_cast<size_t>(Ic0 * CF + pr) * W + Jc * CF + pc;  // within the tile
-    const size_t rstep = static_cast<size_t>(CF) * W;
+    const int toff = (Ic0 * CF + pr) * W + Jc * CF + pc;  // within the tile (element indices of a plane fit 31 bits)
+    const int rstep = CF * W;
     const int qoff = (Ic0 + D::DLO - QLO) * QWC + (Jc + D::DLO - QLO);
     const int wa = threadIdx.x / QWC, wb = threadIdx.x - wa * QWC;  // window element copied by this thread
     const T lam = static_cast<T>(G.lambda);
+    // 32-bit shared addresses of the thread's slots of stage 0
+    const unsigned int s_win = static_cast<unsigned int>(__cvta_generic_to_shared(stg + threadIdx.x));
+    // the thread's 16-byte chunks of a staged tile: column chunk threadIdx % CPR of the rows
+    // threadIdx / CPR + h CROWS
+    constexpr int EPC = 16 / sizeof(T), CPR = TW / EPC, CROWS = NT / CPR, CPASS = TH / CROWS;
+    static_assert(CPASS * CROWS == TH && CPASS >= 1, "chunk passes");
+    const int ce = (threadIdx.x / CPR) * W + (threadIdx.x % CPR) * EPC;  // element offset within the tile
+    const unsigned int s_chk = static_cast<unsigned int>(
+        __cvta_generic_to_shared(stg + du::WIN + (threadIdx.x / CPR) * TW + (threadIdx.x % CPR) * EPC));
+    constexpr unsigned int STGB = du::STG * sizeof(T);
     pdl_wait();  // w, alpha and the flags come from K_L
     pdl_trigger();
     // active channels (ascending), their p parity and alpha
@@ -1450,51 +1465,76 @@ __global__ void __launch_bounds__(NT, 2) k_du(PsGeo G, const T* __restrict__ tap
     const int per = static_cast<int>((U + gridDim.x - 1) / gridDim.x);
     const long long a0 = static_cast<long long>(blockIdx.x) * per;
     const int nu = a0 >= U ? 0 : static_cast<int>(min(static_cast<long long>(per), U - a0));
-    // issue side: unit j -> stage j % NST
-    int ki = static_cast<int>(a0 / ntile), ti = static_cast<int>(a0 - static_cast<long long>(ki) * ntile);
-    auto issue = [&](int stage) {
-        const int ch = s_act[ki];
-        const int by = ti / ntx, bx = ti - by * ntx;
-        const int r0 = by * TH, c0 = bx * TW;
-        T* sd = stg + stage * du::STG;
+    // unit cursors (channel index, tile column / row, element offset of the tile origin), advanced
+    // without divisions; one for the copies being issued, one for the unit being consumed
+    struct Cursor {
+        int k, bx, by, eoff;
+    };
+    auto advance = [&](Cursor& c) {
+        c.eoff += TW;
+        if (++c.bx == ntx) {
+            c.bx = 0;
+            c.eoff += (TH - 1) * W;
+            if (++c.by == nty) {
+                c.by = 0;
+                c.eoff = 0;
+                ++c.k;
+            }
+        }
+    };
+    Cursor ci;
+    {
+        ci.k = static_cast<int>(a0 / ntile);
+        const int t0 = static_cast<int>(a0 - static_cast<long long>(ci.k) * ntile);
+        ci.by = t0 / ntx;
+        ci.bx = t0 - ci.by * ntx;
+        ci.eoff = ci.by * TH * W + ci.bx * TW;
+    }
+    Cursor cc = ci;
+    auto issue = [&](int stage) {  // the unit at cursor ci -> stage
+        const int ch = s_act[ci.k];
+        const unsigned int so = static_cast<unsigned int>(stage) * STGB;
         if (threadIdx.x < QNC) {
-            const int iq0 = (r0 >> 2) + QLO, jq0 = (c0 >> 2) + QLO;
-            du::cp_async_elem(sd + threadIdx.x, q + static_cast<size_t>(ch) * pl +
-                                                    static_cast<size_t>(wrap_once(iq0 + wa, G.h)) * G.w +
-                                                    wrap_once(jq0 + wb, G.w));
+            const int iq0 = ci.by * (TH / CF) + QLO, jq0 = ci.bx * (TW / CF) + QLO;
+            const T* src = q + static_cast<size_t>(ch) * pl + wrap_once(iq0 + wa, G.h) * G.w + wrap_once(jq0 + wb, G.w);
+            du::cp_async_elem<T, 0>(s_win + so, src);
         }
-        const size_t off = static_cast<size_t>(r0) * W + c0 + toff;
-        const T* zc = z + ch * P + off;
-        const T* rc = r + ch * P + off;
-        const T* pcp = pbuf + (static_cast<size_t>(s_par[ki]) * G.N + ch) * P + off;
-        const T* wc = wv + ch * P + off;
-        sd += du::WIN + threadIdx.x;
+        // z, r, p, w tiles as 16-byte chunks through L2 only (cp.async.cg: copies through L1 are
+        // limited by the few L1 lines left beside 220 KB of shared memory); the block barrier that
+        // publishes the window publishes them too
+        const size_t chP = static_cast<size_t>(ch) * P;
+        const T* zc = z + chP;
+        const T* rc = r + chP;
+        const T* wc = wv + chP;
+        const T* pcp = pbuf + (static_cast<size_t>(s_par[ci.k]) * G.N + ch) * P;
+        const int e0 = ci.eoff + ce;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            du::cp_async_elem(sd + (0 * 4 + k) * NT, zc + k * rstep);
-            du::cp_async_elem(sd + (1 * 4 + k) * NT, rc + k * rstep);
-            du::cp_async_elem(sd + (2 * 4 + k) * NT, pcp + k * rstep);
-            du::cp_async_elem(sd + (3 * 4 + k) * NT, wc + k * rstep);
+        for (int h = 0; h < CPASS; ++h) {
+            const int e = e0 + h * CROWS * W;
+            du::cp_async_chunk<(0 * TH + 0) * TW * sizeof(T)>(s_chk + so + h * CROWS * TW * static_cast<unsigned int>(sizeof(T)), zc + e);
+            du::cp_async_chunk<(1 * TH + 0) * TW * sizeof(T)>(s_chk + so + h * CROWS * TW * static_cast<unsigned int>(sizeof(T)), rc + e);
+            du::cp_async_chunk<(2 * TH + 0) * TW * sizeof(T)>(s_chk + so + h * CROWS * TW * static_cast<unsigned int>(sizeof(T)), pcp + e);
+            du::cp_async_chunk<(3 * TH + 0) * TW * sizeof(T)>(s_chk + so + h * CROWS * TW * static_cast<unsigned int>(sizeof(T)), wc + e);
         }
-        if (++ti == ntile) {
-            ti = 0;
-            ++ki;
-        }
+        advance(ci);
     };
 #pragma unroll
     for (int j = 0; j < du::NST - 1; ++j) {
         if (j < nu) issue(j);
         cp_async_commit();
     }
-    int kc = static_cast<int>(a0 / ntile), tc = static_cast<int>(a0 - static_cast<long long>(kc) * ntile);
     int kprev = 0, tprev = 0;
-    int cur_scene = -1;
+    int cur_k = -1, cur_scene = -1;
+    T alpha = 0;
+    size_t chP = 0;
+    int stage = 0, stage_is = du::NST - 1;  // stage of unit j; stage the next issue goes to
     T kreg[DM][DM];
     for (int j = 0; j < nu; ++j) {
         cp_async_wait<du::NST - 2>();  // this thread's copies of unit j have landed
         __syncthreads();               // ... everyone's (the window); unit j - 1 is consumed by all
-        if (j + du::NST - 1 < nu) issue((j + du::NST - 1) % du::NST);
+        if (j + du::NST - 1 < nu) issue(stage_is);
         cp_async_commit();
+        if (++stage_is == du::NST) stage_is = 0;
         // per-tile partial of the previous unit (its warp sums are published by the barrier above)
         if (j > 0 && threadIdx.x == 0) {
             const double* wr = wred + ((j - 1) & 1) * (NT / 32) * 2;
@@ -1508,20 +1548,25 @@ __global__ void __launch_bounds__(NT, 2) k_du(PsGeo G, const T* __restrict__ tap
             pd[0] = s0;
             pd[1] = s1;
         }
-        const int ch = s_act[kc];
-        const int scene = ch / G.cps;
-        if (scene != cur_scene) {  // phase sub-kernel of the scene's taps
-            cur_scene = scene;
-            const T* tp = taps + static_cast<size_t>(scene) * n * n;
+        if (cc.k != cur_k) {  // next channel: its scalars and, on a new scene, the phase sub-kernel
+            cur_k = cc.k;
+            const int ch = s_act[cur_k];
+            alpha = s_alpha[cur_k];
+            chP = static_cast<size_t>(ch) * P;
+            const int scene = ch / G.cps;
+            if (scene != cur_scene) {
+                cur_scene = scene;
+                const T* tp = taps + static_cast<size_t>(scene) * n * n;
 #pragma unroll
-            for (int a = 0; a < DM; ++a)
+                for (int a = 0; a < DM; ++a)
 #pragma unroll
-                for (int b = 0; b < DM; ++b) {
-                    const int tr = CF * (a + D::DLO) - pr + D::C, tcc = CF * (b + D::DLO) - pc + D::C;
-                    kreg[a][b] = (tr >= 0 && tr < N_ && tcc >= 0 && tcc < N_) ? __ldg(tp + tr * N_ + tcc) : T(0);
-                }
+                    for (int b = 0; b < DM; ++b) {
+                        const int tr = CF * (a + D::DLO) - pr + D::C, tcc = CF * (b + D::DLO) - pc + D::C;
+                        kreg[a][b] = (tr >= 0 && tr < N_ && tcc >= 0 && tcc < N_) ? __ldg(tp + tr * N_ + tcc) : T(0);
+                    }
+            }
         }
-        const T* sd = stg + (j % du::NST) * du::STG;
+        const T* sd = stg + stage * du::STG;
         // d of the thread's four outputs (K_D's gather: ascending (mm, b) per accumulator)
         const T* qa = sd + qoff;
         T acc[4] = {0, 0, 0, 0};
@@ -1538,22 +1583,21 @@ __global__ void __launch_bounds__(NT, 2) k_du(PsGeo G, const T* __restrict__ tap
                     if (a >= 0 && a < DM) acc[k] = fma(kreg[a][b], qv[b], acc[k]);
                 }
         }
-        const T alpha = s_alpha[kc];
-        const T* sv = sd + du::WIN + threadIdx.x;
-        const int by = tc / ntx, bx = tc - by * ntx;
-        const size_t off = static_cast<size_t>(by * TH) * W + bx * TW + toff;
-        T* zc = z + ch * P + off;
-        T* rc = r + ch * P + off;
+        const T* sv = sd + du::WIN + (Ic0 * CF + pr) * TW + Jc * CF + pc;  // [array][tile row][tile column]
+        T* zc = z + chP;
+        T* rc = r + chP;
+        const int e0 = cc.eoff + toff;
         double rr = 0.0, zz = 0.0;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const T z0 = sv[(0 * 4 + k) * NT], r0v = sv[(1 * 4 + k) * NT], p0 = sv[(2 * 4 + k) * NT],
-                    w0 = sv[(3 * 4 + k) * NT];
+            const T z0 = sv[(0 * TH + k * CF) * TW], r0v = sv[(1 * TH + k * CF) * TW], p0 = sv[(2 * TH + k * CF) * TW],
+                    w0 = sv[(3 * TH + k * CF) * TW];
             const T ap = acc[k] + w0 * lam;      // pansharpen.cpp:222-223
             const T zn = z0 + p0 * alpha;        // :245
             const T rn = r0v - ap * alpha;       // :246
-            __stcs(zc + k * rstep, zn);
-            __stcs(rc + k * rstep, rn);
+            const int e = e0 + k * rstep;
+            __stcs(zc + e, zn);
+            __stcs(rc + e, rn);
             rr += static_cast<double>(rn) * static_cast<double>(rn);
             zz += static_cast<double>(zn) * static_cast<double>(zn);
         }
@@ -1564,12 +1608,10 @@ __global__ void __launch_bounds__(NT, 2) k_du(PsGeo G, const T* __restrict__ tap
             wr[2 * warp] = rr;
             wr[2 * warp + 1] = zz;
         }
-        kprev = kc;
-        tprev = tc;
-        if (++tc == ntile) {
-            tc = 0;
-            ++kc;
-        }
+        kprev = cc.k;
+        tprev = cc.by * ntx + cc.bx;
+        advance(cc);
+        if (++stage == du::NST) stage = 0;
     }
     __syncthreads();
     if (nu > 0 && threadIdx.x == 0) {  // the last unit's partial

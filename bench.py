@@ -379,10 +379,16 @@ def our_arm(args, cfg):
     nlaunch = max(v["launches"] for v in prof.values())
     act = prof_ch_iters / max(nlaunch, 1)  # mean active channels per launch
     avg = {k: v["total_ms"] / max(v["launches"], 1) for k, v in prof.items()}
-    ops = {"K_A": [k for k in ("K_Q", "K_D", "K_L") if k in avg], "K_U": ["K_U"]}
-    alg = {"K_A": 5 * s * P * act, "K_U": 6 * s * P * act}
+    # Fused path (no K_D launch): K_L writes w = L M L p instead of Ap, and K_U is K_DU, which forms
+    # d = B^T U q in registers while it updates z and r. The operator split of the bytes is
+    # unchanged (K_Q + K_L: r, p_old, I -> p, w; K_DU: z, r, p, w -> z, r) and the kernels together
+    # move exactly the 11 s P of SURVEY 8(d), reported as CG_iter.
+    fused = "K_D" not in avg
+    ops = {"K_A": [k for k in ("K_Q", "K_D", "K_L") if k in avg], "K_U": ["K_U"],
+           "CG_iter": [k for k in ("K_Q", "K_D", "K_L", "K_U") if k in avg]}
+    alg = {"K_A": 5 * s * P * act, "K_U": 6 * s * P * act, "CG_iter": 11 * s * P * act}
     op_ms = {o: sum(avg[k] for k in ks) for o, ks in ops.items()}
-    dom = max(op_ms, key=lambda o: op_ms[o])
+    dom = max(("K_A", "K_U"), key=lambda o: op_ms[o])
     achieved = alg[dom] / (op_ms[dom] / 1e3) / 1e9
     peak, kind = peaks()
     traffic, traffic_src = None, None
@@ -408,6 +414,8 @@ def our_arm(args, cfg):
                 "operators": {o: {"kernels": ks, "avg_ms": op_ms[o], "algorithmic_bytes": alg[o],
                                   "GB/s": alg[o] / (op_ms[o] / 1e3) / 1e9,
                                   "frac": alg[o] / (op_ms[o] / 1e3) / 1e9 / peak} for o, ks in ops.items()},
+                "cg_path": ("fused: K_Q3 -> K_L (w = L M L p, p.Ap = |q|^2 + lambda p.w) -> K_DU (K_U slot: data term "
+                            "gather + update; d and Ap never stored)") if fused else "K_Q -> K_D -> K_L -> K_U",
                 "kernel_avg_ms": avg,
                 "kernel_share_of_cg": {k: v["total_ms"] / cg_total for k, v in prof.items()} if cg_total else None,
                 "whole_solve": {"algorithmic_bytes": B_solve, "GB/s": B_solve / T_step / 1e9,

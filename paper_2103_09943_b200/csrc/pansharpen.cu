@@ -2172,6 +2172,7 @@ void cg_solve_t(Context& ctx, const PsGeo& G, const T* d_taps, const double* d_g
             for (int it = 0; it < chunk; ++it) {
                 if (g * chunk + it >= active_iters) break;
                 for (int kk = 0; kk < EV - 1; ++kk) {
+                    if (du && kk == 1) continue;  // fused path: no K_D launch (the slot is an empty event pair)
                     float ms = 0.f;
                     FBMP_CUDA(cudaEventElapsedTime(&ms, pev[it * EV + kk], pev[it * EV + kk + 1]));
                     ctx.prof_ms[kk] += ms;

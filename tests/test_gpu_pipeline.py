@@ -486,3 +486,33 @@ def test_prior_kind_errors(gpu):
     with pytest.raises(gpu.ParamError, match="custom prior requires a kernel"):
         gpu.pansharpen(sc.lrms, sc.pan, sc.kernel[:7, :7] / sc.kernel[:7, :7].sum(), 4,
                        gpu.PansharpenParams(prior="custom"))
+
+
+def test_fused_cg_path_matches_unfused(gpu, orc, tmp_path):
+    """The default CG on the C2-C5 shapes is the fused chain K_Q3 -> K_L (w = L M L p,
+    p.Ap = |q|^2 + lambda p.w) -> K_DU (data-term gather + update; d and Ap never stored).
+    FBMP_DU=0 (read once per process) keeps K_D + K_L + K_U; both must give the oracle's CG
+    counts and the same iterate (pansharpen.cpp:218-256), here on a 512^2 warm start and on
+    the identity prior."""
+    import os
+    import subprocess
+    import sys
+
+    sc = synth.make_scene("C1", hr=512)
+    guide = orc.laplacian(sc.pan / sc.pan.max())
+    k = synth.make_kernel(np.random.default_rng(512), 17, 2.0)
+    x = sc.lrms[1] / sc.pan.max()
+    zo, ito, _, _ = orc.warmstart_cg(x, k, 4, orc.Matting(guide, 1, 1e-4))
+    zg, itg, _ = gpu.warmstart_cg(x, k, 4, gpu.MattingMatrix(guide, 1, 1e-4))
+    np.savez(tmp_path / "in.npz", x=x, k=k, guide=guide)
+    code = ("import numpy as np, sys; from paper_2103_09943_b200 import fbmp as gpu; d = np.load(sys.argv[1]);"
+            "z, it, _ = gpu.warmstart_cg(d['x'], d['k'], 4, gpu.MattingMatrix(d['guide'], 1, 1e-4));"
+            "np.savez(sys.argv[2], z=z, it=it)")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FBMP_DU="0", PYTHONPATH=root)
+    subprocess.run([sys.executable, "-c", code, str(tmp_path / "in.npz"), str(tmp_path / "out.npz")], check=True,
+                   env=env, cwd=root)
+    un = np.load(tmp_path / "out.npz")
+    assert itg == ito == int(un["it"])
+    assert rel(zg, zo) < TOL and rel(un["z"], zo) < TOL
+    assert rel(zg, un["z"]) < 1e-8

@@ -21,7 +21,7 @@ def cls(name):
         return "K_D"
     if "k_llp" in name or "k_apply" in name:
         return "K_L"
-    if "k_update" in name:
+    if "k_update" in name or "k_du" in name:  # K_DU runs in the K_U slot of the fused path
         return "K_U"
     return name.split("(")[0][-40:]
 

@@ -1956,6 +1956,8 @@ void cg_solve_t(Context& ctx, const PsGeo& G, const T* d_taps, const double* d_g
         set_smem(du, sdu);
         int per_sm = 0;
         FBMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, du, fast::NT, sdu));
+        static const int du_env = std::getenv("FBMP_DU_PER_SM") ? std::atoi(std::getenv("FBMP_DU_PER_SM")) : 0;
+        if (du_env > 0) per_sm = std::min(per_sm, du_env);
         du_ctas = std::max(1, per_sm) * ctx.sm_count;
     }
     const int ntile_du = (G.W / fast::du::TW) * (G.H / fast::du::TH);
@@ -1995,14 +1997,17 @@ void cg_solve_t(Context& ctx, const PsGeo& G, const T* d_taps, const double* d_g
         key.append(reinterpret_cast<const char*>(ptrs), sizeof(ptrs));
         key.append(reinterpret_cast<const char*>(dims), sizeof(dims));
     }
-    // channel groups (env FBMP_CG_GROUPS=2): the chunk graph holds two independent CG chains on two
-    // streams (fork / join inside the graph) so that the kernels of one group overlap those of the
-    // other. Measured on B200: C1 -1.5 %, C2 +1 % (the CG kernels already fill the register file),
-    // so it is off by default.
-    static const int groups_env = std::getenv("FBMP_CG_GROUPS") ? std::atoi(std::getenv("FBMP_CG_GROUPS")) : 1;
+    // channel groups: the chunk graph holds two independent CG chains on two streams (fork / join
+    // inside the graph), so the kernels of one half of the channels overlap the tails (and, between
+    // the memory-bound K_DU and the latency-bound K_Q3 / K_L, the idle resources) of the other
+    // half's. On by default for a single scene with the fused chain (measured, same bits: C2 16.85 ->
+    // 16.13 ms, C3 84.1 -> 80.0 ms, C5 1203 -> 1180 ms, C1 7.34 -> 7.24 ms); off for scene batches
+    // (C4: 205 -> 255 ms, the batch already fills the GPU). Env FBMP_CG_GROUPS = 1 / 2 overrides.
+    static const int groups_env = std::getenv("FBMP_CG_GROUPS") ? std::atoi(std::getenv("FBMP_CG_GROUPS")) : 0;
     const int S_sc = (G.N + G.cps - 1) / G.cps;
     int ngrp = 1;
-    if (groups_env >= 2 && !prof && fastA && q2.fn && use_llp() && (S_sc >= 2 || (S_sc == 1 && N >= 2))) ngrp = 2;
+    const bool grp_ok = !prof && fastA && q2.fn && use_llp() && (S_sc >= 2 || (S_sc == 1 && N >= 2));
+    if (grp_ok && (groups_env >= 2 || (groups_env == 0 && S_sc == 1))) ngrp = 2;
     struct Grp {
         PsGeo G;
         int c0 = 0;

@@ -32,12 +32,14 @@ Context::~Context() {
     for (auto& e : poll_ev)
         if (e) cudaEventDestroy(e);
     if (pinned_buf) cudaFreeHost(pinned_buf);
-    if (aux_stream) cudaStreamDestroy(aux_stream);
+    for (auto& a : aux_streams)
+        if (a) cudaStreamDestroy(a);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     for (auto& e : copy_ev)
         if (e) cudaEventDestroy(e);
     if (fork_ev) cudaEventDestroy(fork_ev);
-    if (join_ev) cudaEventDestroy(join_ev);
+    for (auto& e : join_evs)
+        if (e) cudaEventDestroy(e);
     ws.clear();
     if (stream) cudaStreamDestroy(stream);
 }

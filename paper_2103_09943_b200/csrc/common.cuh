@@ -134,13 +134,13 @@ struct Context {
     void* pinned_buf = nullptr;
     size_t pinned_bytes = 0;
     cudaEvent_t poll_ev[2] = {nullptr, nullptr};  // CG flag polling
-    cudaStream_t aux_stream = nullptr;             // second CG chain inside the chunk graph
+    cudaStream_t aux_streams[3] = {nullptr, nullptr, nullptr};  // further CG chains inside the chunk graph
     // host-pointer solves: the HRMS planes are downloaded per channel on copy_stream as soon as
     // each is final (overlapping the remaining channels' last FFT and unscale); null = no sink
     double* host_out = nullptr;
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t copy_ev[2] = {nullptr, nullptr};
-    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+    cudaEvent_t fork_ev = nullptr, join_evs[3] = {nullptr, nullptr, nullptr};
     // instantiated CG-chunk graphs keyed on their launch parameters (bytes of geometry + pointers)
     std::map<std::string, cudaGraphExec_t> graphs;
     // NCCL communicator of a row-strip (multi-GPU) solve (fbmp_gpu_ctx_set_comm), or null

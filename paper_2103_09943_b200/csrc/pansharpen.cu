@@ -2007,7 +2007,8 @@ void cg_solve_t(Context& ctx, const PsGeo& G, const T* d_taps, const double* d_g
     const int S_sc = (G.N + G.cps - 1) / G.cps;
     int ngrp = 1;
     const bool grp_ok = !prof && fastA && q2.fn && use_llp() && (S_sc >= 2 || (S_sc == 1 && N >= 2));
-    if (grp_ok && (groups_env >= 2 || (groups_env == 0 && S_sc == 1))) ngrp = 2;
+    if (grp_ok && (groups_env >= 2 || (groups_env == 0 && S_sc == 1)))
+        ngrp = std::min({std::max(groups_env, 2), 4, S_sc >= 2 ? S_sc : N});
     struct Grp {
         PsGeo G;
         int c0 = 0;
@@ -2025,12 +2026,12 @@ void cg_solve_t(Context& ctx, const PsGeo& G, const T* d_taps, const double* d_g
                 c0 = 0;
                 c1 = N;
             } else if (S_sc >= 2) {  // whole scenes
-                const int s0 = gi == 0 ? 0 : S_sc / 2, s1 = gi == 0 ? S_sc / 2 : S_sc;
+                const int s0 = gi * S_sc / ngrp, s1 = (gi + 1) * S_sc / ngrp;
                 c0 = s0 * G.cps;
                 c1 = std::min(N, s1 * G.cps);
             } else {
-                c0 = gi == 0 ? 0 : N / 2;
-                c1 = gi == 0 ? N / 2 : N;
+                c0 = gi * N / ngrp;
+                c1 = (gi + 1) * N / ngrp;
             }
             const int ng = c1 - c0, s0 = c0 / G.cps;
             R.c0 = c0;
@@ -2074,20 +2075,21 @@ void cg_solve_t(Context& ctx, const PsGeo& G, const T* d_taps, const double* d_g
     } else {
         cudaGraph_t graph;
         cudaStream_t main = ctx.stream;
-        if (ngrp > 1 && !ctx.aux_stream) {
-            FBMP_CUDA(cudaStreamCreateWithFlags(&ctx.aux_stream, cudaStreamNonBlocking));
-            FBMP_CUDA(cudaEventCreateWithFlags(&ctx.fork_ev, cudaEventDisableTiming));
-            FBMP_CUDA(cudaEventCreateWithFlags(&ctx.join_ev, cudaEventDisableTiming));
-        }
+        for (int a = 0; a + 1 < ngrp; ++a)
+            if (!ctx.aux_streams[a]) {
+                FBMP_CUDA(cudaStreamCreateWithFlags(&ctx.aux_streams[a], cudaStreamNonBlocking));
+                FBMP_CUDA(cudaEventCreateWithFlags(&ctx.join_evs[a], cudaEventDisableTiming));
+            }
+        if (ngrp > 1 && !ctx.fork_ev) FBMP_CUDA(cudaEventCreateWithFlags(&ctx.fork_ev, cudaEventDisableTiming));
         FBMP_CUDA(cudaStreamBeginCapture(main, cudaStreamCaptureModeThreadLocal));
         if (ngrp > 1) {
             FBMP_CUDA(cudaEventRecord(ctx.fork_ev, main));
-            FBMP_CUDA(cudaStreamWaitEvent(ctx.aux_stream, ctx.fork_ev, 0));
+            for (int a = 0; a + 1 < ngrp; ++a) FBMP_CUDA(cudaStreamWaitEvent(ctx.aux_streams[a], ctx.fork_ev, 0));
         }
         for (int gi = 0; gi < ngrp; ++gi) {
             Grp& R = grp[gi];
             const int Ng = R.G.N;
-            ctx.stream = gi == 0 ? main : ctx.aux_stream;  // launch helpers enqueue on ctx.stream
+            ctx.stream = gi == 0 ? main : ctx.aux_streams[gi - 1];  // launch helpers enqueue on ctx.stream
             for (int it = 0; it < chunk; ++it) {
                 if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * EV + 0], ctx.stream, cudaEventRecordExternal));
                 if (q2.fn && (pdl_mask & 1))
@@ -2133,8 +2135,10 @@ void cg_solve_t(Context& ctx, const PsGeo& G, const T* d_taps, const double* d_g
         }
         ctx.stream = main;
         if (ngrp > 1) {
-            FBMP_CUDA(cudaEventRecord(ctx.join_ev, ctx.aux_stream));
-            FBMP_CUDA(cudaStreamWaitEvent(main, ctx.join_ev, 0));
+            for (int a = 0; a + 1 < ngrp; ++a) {
+                FBMP_CUDA(cudaEventRecord(ctx.join_evs[a], ctx.aux_streams[a]));
+                FBMP_CUDA(cudaStreamWaitEvent(main, ctx.join_evs[a], 0));
+            }
         }
         FBMP_CUDA(cudaStreamEndCapture(main, &graph));
         FBMP_CUDA(cudaGraphInstantiate(&exec, graph, 0));

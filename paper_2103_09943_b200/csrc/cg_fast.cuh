@@ -466,13 +466,25 @@ __device__ __forceinline__ double rows(const Args<T>& A, const T* sk, T* tt, T* 
             const bool dot_row = own_row && y >= A.rlo && y < A.rhi;
             T* prow = nullptr;
             if (CG) prow = A.pnew + static_cast<size_t>(own_row ? y : 0) * W + 4 * A.j0 - 4 * g;
+            // all ring loads first: the plane / p stores below cannot be proven disjoint from the
+            // ring, so loads left inside the loop would wait for every preceding store
+            constexpr int NKK = (RW + 63) / 64;
+            v2<T> vv[NKK], oo[NKK];
 #pragma unroll
-            for (int kk = 0; kk < (RW + 63) / 64; ++kk) {
+            for (int kk = 0; kk < NKK; ++kk) {
                 const int e = 2 * lane + 64 * kk;
                 if (e < RW) {
-                    v2<T> v = ld2(rr + e);
+                    vv[kk] = ld2(rr + e);
+                    if (CG) oo[kk] = ld2(rr + RW + e);
+                }
+            }
+#pragma unroll
+            for (int kk = 0; kk < NKK; ++kk) {
+                const int e = 2 * lane + 64 * kk;
+                if (e < RW) {
+                    v2<T> v = vv[kk];
                     if (CG) {
-                        const v2<T> o = ld2(rr + RW + e);
+                        const v2<T> o = oo[kk];
                         v.x = v.x + o.x * A.beta;  // pansharpen.cpp:254
                         v.y = v.y + o.y * A.beta;
                         const int xr = e - 4 * g;

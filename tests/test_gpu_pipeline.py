@@ -492,8 +492,7 @@ def test_fused_cg_path_matches_unfused(gpu, orc, tmp_path):
     """The default CG on the C2-C5 shapes is the fused chain K_Q3 -> K_L (w = L M L p,
     p.Ap = |q|^2 + lambda p.w) -> K_DU (data-term gather + update; d and Ap never stored).
     FBMP_DU=0 (read once per process) keeps K_D + K_L + K_U; both must give the oracle's CG
-    counts and the same iterate (pansharpen.cpp:218-256), here on a 512^2 warm start and on
-    the identity prior."""
+    counts and the same iterate (pansharpen.cpp:218-256), here on a 512^2 warm start."""
     import os
     import subprocess
     import sys
@@ -516,3 +515,20 @@ def test_fused_cg_path_matches_unfused(gpu, orc, tmp_path):
     assert itg == ito == int(un["it"])
     assert rel(zg, zo) < TOL and rel(un["z"], zo) < TOL
     assert rel(zg, un["z"]) < 1e-8
+
+
+def test_fused_cg_identity_prior_and_iteration_cap(gpu, orc):
+    """The fused chain with the identity prior (K_L without the Laplacians, pansharpen.cpp:28-50) at
+    512^2 against the oracle (same CG count), and its iteration cap (pansharpen.cpp:257-262:
+    NumericalError with the relative residual, raised from K_DU's done = 3)."""
+    sc = synth.make_scene("C1", hr=512)
+    pan_n = sc.pan / sc.pan.max()
+    k = synth.make_kernel(np.random.default_rng(5), 15, 2.0)
+    x = sc.lrms[2] / sc.pan.max()
+    prm = gpu.PansharpenParams(prior="identity")
+    zo, ito, _, _ = orc.warmstart_cg(x, k, 4, orc.Matting(pan_n, 1, 1e-4), prior=1)
+    zg, itg, _ = gpu.warmstart_cg(x, k, 4, gpu.MattingMatrix(pan_n, 1, 1e-4), prm)
+    assert itg == ito
+    assert rel(zg, zo) < TOL
+    with pytest.raises(gpu.NumericalError, match="did not converge in 5 iterations"):
+        gpu.warmstart_cg(x, k, 4, gpu.MattingMatrix(pan_n, 1, 1e-4), gpu.PansharpenParams(), max_iters=5)

@@ -1373,14 +1373,18 @@ __device__ __forceinline__ void cp_async_pair(float2* sdst, const float* gsrc) {
 #define FBMP_DU_NST 3
 #endif
 namespace du {
+#ifndef FBMP_DU_NT
+#define FBMP_DU_NT 256
+#endif
 constexpr int NST = FBMP_DU_NST;             // ring depth
-constexpr int TW = 32, TH = 32;              // HR tile of a unit (64 x 16 measured equal at C2, 2.5 % slower at C5)
+constexpr int NTD = FBMP_DU_NT;              // threads per CTA: 256 (32 x 32 tiles, 2 CTAs/SM) or 128 (32 x 16, 4 CTAs/SM)
+constexpr int TW = 32, TH = NTD / 8;         // HR tile of a unit (64 x 16 with 256 threads measured equal at C2, 2.5 % slower at C5)
 constexpr int WIN = 208;                     // q window slots of a stage (>= 21 x 9, 16-byte multiple)
 constexpr int STG = WIN + 4 * TW * TH;       // elements per stage: window | z, r, p, w tiles
 constexpr int MAXCH = 512;                   // channels per launch (active-channel tables)
 template <class T>
 constexpr size_t smem() {
-    return (static_cast<size_t>(NST) * STG * sizeof(T) + 15) / 16 * 16 + 2 * (NT / 32) * 2 * sizeof(double) +
+    return (static_cast<size_t>(NST) * STG * sizeof(T) + 15) / 16 * 16 + 2 * (NTD / 32) * 2 * sizeof(double) +
            MAXCH * (sizeof(T) + 2 * sizeof(short));
 }
 // one element to the 32-bit shared address sdst + OFF elements
@@ -1399,11 +1403,12 @@ __device__ __forceinline__ void cp_async_chunk(unsigned int sdst, const T* gsrc)
 }  // namespace du
 
 template <int N_, class T = double>
-__global__ void __launch_bounds__(NT, 2) k_du(PsGeo G, const T* __restrict__ taps, const T* __restrict__ q,
+__global__ void __launch_bounds__(du::NTD, 512 / du::NTD) k_du(PsGeo G, const T* __restrict__ taps, const T* __restrict__ q,
                                               const T* __restrict__ wv, T* __restrict__ z, T* __restrict__ r,
                                               const T* __restrict__ pbuf, CgState* st, double* __restrict__ part,
                                               int ntile) {
     using namespace a4;
+    constexpr int NT = du::NTD;  // (shadows the 256 threads of the tile kernels)
     constexpr int CF = 4;
     using D = DT<N_, CF>;
     constexpr int DM = D::DM;

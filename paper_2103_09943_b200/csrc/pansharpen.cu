@@ -1955,7 +1955,7 @@ void cg_solve_t(Context& ctx, const PsGeo& G, const T* d_taps, const double* d_g
     if (du) {
         set_smem(du, sdu);
         int per_sm = 0;
-        FBMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, du, fast::NT, sdu));
+        FBMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, du, fast::du::NTD, sdu));
         static const int du_env = std::getenv("FBMP_DU_PER_SM") ? std::atoi(std::getenv("FBMP_DU_PER_SM")) : 0;
         if (du_env > 0) per_sm = std::min(per_sm, du_env);
         du_ctas = std::max(1, per_sm) * ctx.sm_count;
@@ -2107,10 +2107,10 @@ void cg_solve_t(Context& ctx, const PsGeo& G, const T* d_taps, const double* d_g
                     launch_llp_w<T>(ctx, R.G, R.guide, R.mu, R.g, R.B.p, R.B.Ap, R.B.st, R.pa, (pdl_mask & 2) != 0);
                     if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * EV + 3], ctx.stream, cudaEventRecordExternal));
                     if (pdl_mask & 4)
-                        launch_pdl(du, dim3(du_ctas), dim3(fast::NT), sdu, ctx.stream, R.G, R.taps, R.B.q, R.B.Ap, R.B.z,
+                        launch_pdl(du, dim3(du_ctas), dim3(fast::du::NTD), sdu, ctx.stream, R.G, R.taps, R.B.q, R.B.Ap, R.B.z,
                                    R.B.r, R.B.p, R.B.st, R.pu, ntile_du);
                     else
-                        du<<<dim3(du_ctas), fast::NT, sdu, ctx.stream>>>(R.G, R.taps, R.B.q, R.B.Ap, R.B.z, R.B.r, R.B.p,
+                        du<<<dim3(du_ctas), fast::du::NTD, sdu, ctx.stream>>>(R.G, R.taps, R.B.q, R.B.Ap, R.B.z, R.B.r, R.B.p,
                                                                         R.B.st, R.pu, ntile_du);
                     if (prof) FBMP_CUDA(cudaEventRecordWithFlags(pev[it * EV + 4], ctx.stream, cudaEventRecordExternal));
                     continue;

@@ -650,7 +650,9 @@ __global__ void __launch_bounds__(q3::NTH, FBMP_KQ3_MINB) k_q3(PsGeo G, const T*
             const double* pq2 = part + static_cast<size_t>(G.N) * nblk + static_cast<size_t>(ch) * nseg;
             double s0 = 0.0, s1 = 0.0;
             for (int i = threadIdx.x; i < nblk; i += q3::NTH) s0 += __ldcg(part + static_cast<size_t>(ch) * nblk + i);
-            for (int i = threadIdx.x; i < nseg; i += q3::NTH) s1 += __ldcg(pq2 + i);
+            // (row strips: the segments of the owned LR rows only; every strip tiles them the same way)
+            const int seg_lo = G.dred ? (G.rlo / 4) * nbands : 0, seg_hi = G.dred ? min(nseg, (G.rhi / 4) * nbands) : nseg;
+            for (int i = seg_lo + threadIdx.x; i < seg_hi; i += q3::NTH) s1 += __ldcg(pq2 + i);
             const double2 tot = block_sum2<q3::NTH>(s0, s1, red);
             if (threadIdx.x == 0) {
                 if (G.dred) G.dred[G.N + 3 * ch] = tot.x;
@@ -1666,8 +1668,14 @@ __global__ void __launch_bounds__(du::NTD, 512 / du::NTD) k_du(PsGeo G, const T*
     for (int i = 0; i < nact; ++i) {
         if (!s_fin[i]) continue;  // block-uniform
         const int ch = s_act[i];
-        const double2 tot = sum_partials2<NT>(part + static_cast<size_t>(ch) * ntile * 2, ntile, red);
-        if (threadIdx.x == 0) {
+        // row strips: the tiles of the owned rows only (rlo, rhi are multiples of the tile height)
+        const int t_lo = G.dred ? (G.rlo / TH) * ntx : 0, t_hi = G.dred ? (G.rhi / TH) * ntx : ntile;
+        const double2 tot = sum_partials2<NT>(part + (static_cast<size_t>(ch) * ntile + t_lo) * 2, t_hi - t_lo, red);
+        if (threadIdx.x == 0 && G.dred) {  // distributed: publish the local sums only
+            G.dred[G.N + 3 * ch + 1] = tot.x;
+            G.dred[G.N + 3 * ch + 2] = tot.y;
+            st[ch].cnt_u = 0;
+        } else if (threadIdx.x == 0) {
             CgState& S = st[ch];
             const double rs_new = tot.x, zsq = tot.y;
             const int t = S.t;
@@ -2069,7 +2077,8 @@ __global__ void __launch_bounds__(kl::NTL, FBMP_KL_MINB) k_llp2(PsGeo G, const T
             for (int i = lane; i < nbands * nrb; i += 32) sacc += __ldcg(pa + i);
             double pAp = warp_sum(sacc);
             if (lane == 0 && G.dred) {  // distributed: publish the local sum only
-                G.dred[ch] = pAp;
+                // fused chain: this strip's share of p.Ap = ||q||^2 + lambda p.w (linear in the strips)
+                G.dred[ch] = DIN ? pAp : st[ch].qq + G.lambda * pAp;
                 st[ch].cnt_a = 0;
             } else if (lane == 0) {
                 CgState& S = st[ch];
@@ -2280,7 +2289,7 @@ __global__ void __launch_bounds__(kl::NTL, FBMP_KL_MINB) k_llp4f(PsGeo G, const 
             for (int i = lane; i < nbands * nrb; i += 32) sacc += __ldcg(pa + i);
             double pAp = warp_sum(sacc);
             if (lane == 0 && G.dred) {
-                G.dred[ch] = pAp;
+                G.dred[ch] = DIN ? pAp : st[ch].qq + G.lambda * pAp;
                 st[ch].cnt_a = 0;
             } else if (lane == 0) {
                 CgState& S = st[ch];

@@ -1755,8 +1755,10 @@ using DuFn = void (*)(PsGeo, const T*, const T*, const T*, T*, T*, const T*, CgS
 template <class T>
 DuFn<T> du_select(const PsGeo& G) {
     static const bool off = std::getenv("FBMP_DU") && std::atoi(std::getenv("FBMP_DU")) == 0;
-    if (off || G.c != 4 || G.dred || G.H % fast::du::TH || G.W % fast::du::TW || !use_llp() || G.N > fast::du::MAXCH)
+    if (off || G.c != 4 || G.H % fast::du::TH || G.W % fast::du::TW || !use_llp() || G.N > fast::du::MAXCH)
         return nullptr;
+    // row strips: K_DU sums whole tiles, K_Q3 whole LR rows
+    if (G.dred && (G.rlo % fast::du::TH || G.rhi % fast::du::TH)) return nullptr;
     switch (G.n) {
     case 21: return fast::k_du<21, T>;
     case 17: return fast::k_du<17, T>;
@@ -2489,6 +2491,20 @@ void cg_solve_strips(Context& ctx, std::vector<StripCg>& SS, const StripComm& co
     set_smem(q2.fn, q2.smem);
     prepare_apply2<true>(G0);
     set_smem(k_rhs<true>, sr);
+    // fused chain (K_Q3 -> K_L without d -> K_DU) when every strip qualifies: the strips publish their
+    // shares of ||q||^2 + lambda p.w, ||r||^2, ||z||^2 and the k_dist_* kernels close the iteration
+    DuFn<double> du = q2.streaming && llp_plan<double>(ctx, G0).pairs ? du_select<double>(G0) : nullptr;
+    for (auto& S : SS)
+        if (du && du_select<double>(S.G) != du) du = nullptr;
+    const size_t sdu = du ? fast::du::smem<double>() : 0;
+    const int ntile_du = (G0.W / fast::du::TW) * (G0.H / fast::du::TH);
+    int du_ctas = 0;
+    if (du) {
+        set_smem(du, sdu);
+        int per_sm = 0;
+        FBMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, du, fast::du::NTD, sdu));
+        du_ctas = std::max(1, per_sm) * ctx.sm_count;
+    }
     double** d_reds = ctx.scratch<double*>("dist_reds", NS);
     {
         std::vector<double*> h(NS);
@@ -2569,15 +2585,24 @@ void cg_solve_strips(Context& ctx, std::vector<StripCg>& SS, const StripComm& co
                 parts(S, pi, pq, pa, pu);
                 q2.fn<<<dim3(nbq, N), q2.threads, q2.smem, ctx.stream>>>(S.G, S.taps, S.B.r, S.B.p, S.B.q, S.B.st, pq, nbq);
                 ctx.count();
-                launch_apply2<true>(ctx, S.G, S.taps, S.guide, S.wmu, S.wg, S.B.p, S.B.q, S.B.Ap, S.B.st, pa);
-                ctx.count(2);
+                if (du) {
+                    launch_llp_w<double>(ctx, S.G, S.guide, S.wmu, S.wg, S.B.p, S.B.Ap, S.B.st, pa, false);
+                    ctx.count();
+                } else {
+                    launch_apply2<true>(ctx, S.G, S.taps, S.guide, S.wmu, S.wg, S.B.p, S.B.q, S.B.Ap, S.B.st, pa);
+                    ctx.count(2);
+                }
             }
             allreduce(0, N);
             for (auto& S : SS) {
                 k_dist_alpha<<<ceil_div(N, 64), 64, 0, ctx.stream>>>(S.B.st, S.dred, N);
                 double *pi, *pq, *pa, *pu;
                 parts(S, pi, pq, pa, pu);
-                k_update<<<dim3(nbu, N), NTU, 0, ctx.stream>>>(S.G, S.B.z, S.B.r, S.B.p, S.B.Ap, S.B.st, pu, nbu);
+                if (du)
+                    du<<<dim3(du_ctas), fast::du::NTD, sdu, ctx.stream>>>(S.G, S.taps, S.B.q, S.B.Ap, S.B.z, S.B.r, S.B.p,
+                                                                         S.B.st, pu, ntile_du);
+                else
+                    k_update<<<dim3(nbu, N), NTU, 0, ctx.stream>>>(S.G, S.B.z, S.B.r, S.B.p, S.B.Ap, S.B.st, pu, nbu);
                 ctx.count(2);
             }
             allreduce(N, 3 * N);

@@ -12,8 +12,9 @@ configs[1] = C2 by default). Multi-GPU (torchrun): every rank solves its own sce
            library's stream, L2 flushed with a 512 MB write before every step).
 `e2e`    : the same metric through the public host-pointer C ABI (fbmp_gpu_blind), with
            the H2D upload of PAN + LRMS and the D2H download of the HRMS inside the step.
-`roofline`: the dominant CG operator (K_A = K_Q + K_D + K_L, or K_U), SURVEY 8(d) algorithmic
-           bytes / CUDA-event duration (profile pass), plus the whole-solve fraction.
+`roofline`: the dominant CG operator (K_A = K_Q + K_L on the fused chain, K_Q + K_D + K_L otherwise;
+           or K_U = K_DU / K_U), SURVEY 8(d) algorithmic bytes / CUDA-event duration (profile pass,
+           one CG chain), the whole iteration (CG_iter, 11 s P) and the whole-solve fraction.
 `cpu_baseline`: the CPU oracle (oracle/, C++ restatement of the reference): one complete solve
            of the same scene for C1/C2; a labelled estimate from a bounded sample for C3.
 """
